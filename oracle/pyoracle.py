@@ -1,0 +1,365 @@
+"""ctypes bindings for the CPU checker (TEST / BASELINE INFRASTRUCTURE ONLY).
+
+* ``Oracle`` wraps ``oracle/liboracle.so`` — the C restatement in ``oracle.c``.
+* ``Reference`` wraps ``oracle/_ref/libssbh_ref.so`` — the unmodified reference
+  sources (``/root/reference/proj/src``) compiled by ``oracle/Makefile`` behind an
+  ``extern "C"`` shim (``oracle/ref_shim.cpp``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg import this module. The product package never does.
+Words are numpy ``uint64`` arrays, bit k = bit k%64 of word k/64 (LSB first).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+U64P = C.POINTER(C.c_uint64)
+U32P = C.POINTER(C.c_uint32)
+U8P = C.POINTER(C.c_uint8)
+
+
+def _p64(a):
+    return a.ctypes.data_as(U64P)
+
+
+def _p32(a):
+    return a.ctypes.data_as(U32P)
+
+
+def _p8(a):
+    return a.ctypes.data_as(U8P)
+
+
+def key_of(seed) -> np.ndarray:
+    """BASELINE integer seed N -> MasterSeed::from_hex('%064x' % N) = {0,0,0,N}."""
+    if isinstance(seed, np.ndarray):
+        return seed.astype(np.uint64)
+    if isinstance(seed, (list, tuple)):
+        return np.array(seed, dtype=np.uint64)
+    return np.array([0, 0, 0, int(seed)], dtype=np.uint64)
+
+
+def nwords(nbits: int) -> int:
+    return (int(nbits) + 63) // 64
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+class Oracle:
+    def __init__(self, path: str | None = None):
+        path = path or os.path.join(HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = C.CDLL(path)
+        self.L = L
+        L.or_tag.restype = C.c_uint64
+        L.or_tag.argtypes = [C.c_char_p]
+        L.or_threefry.argtypes = [U64P, U64P, U64P]
+        L.or_stream_word.restype = C.c_uint64
+        L.or_stream_word.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.or_uniform_below.restype = C.c_uint64
+        L.or_uniform_below.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.or_bernoulli.restype = C.c_int
+        L.or_bernoulli.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64]
+        L.or_stream_bits.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64, U64P]
+        L.or_make_input.argtypes = [U64P, C.c_double, C.c_uint64, U64P, C.c_int]
+        L.or_assign_subblocks.restype = C.c_int
+        L.or_assign_subblocks.argtypes = [C.c_uint64, C.c_uint32, U64P, U32P, U64P, C.c_int]
+        L.or_sift_partition.argtypes = [U8P, C.c_uint64, U32P, C.c_uint32, U64P, U64P]
+        L.or_xor_bit_range.argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64,
+                                       C.c_uint64, C.c_uint64]
+        for f in ("or_toeplitz_hash", "or_dense_toeplitz"):
+            getattr(L, f).argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, U64P]
+        L.or_blocked_toeplitz_hash.argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64,
+                                               C.c_uint64, U64P]
+        L.or_reverse_bits.argtypes = [U64P, C.c_uint64, U64P]
+        L.or_toeplitz_rows.argtypes = [U64P, C.c_uint64, U64P, U64P, C.c_uint64, U8P]
+        L.or_relative_entropy.restype = C.c_double
+        L.or_relative_entropy.argtypes = [C.c_double, C.c_double]
+        L.or_binomial_tail_bound.restype = C.c_double
+        L.or_binomial_tail_bound.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
+        L.or_block_limit.restype = C.c_uint64
+        L.or_block_limit.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64,
+                                     C.POINTER(C.c_int)]
+        L.or_cycle_estimate.restype = C.c_uint64
+        L.or_cycle_estimate.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_int)]
+        L.or_extract.restype = C.c_int
+        L.or_extract.argtypes = [U64P, C.c_uint64, C.c_uint32, U64P, U64P, C.c_int, C.c_uint64,
+                                 U64P, U64P, C.c_int]
+        L.or_extract_selected.restype = C.c_int
+        L.or_extract_selected.argtypes = [U64P, C.c_uint64, C.c_uint32, U64P, U64P, C.c_int,
+                                          C.c_uint64, U32P, C.c_uint32, U64P, U64P, C.c_int]
+        L.or_fnv_words.restype = C.c_uint64
+        L.or_fnv_words.argtypes = [U64P, C.c_uint64]
+
+    # -- PRF --------------------------------------------------------------------
+    def tag(self, name: str) -> int:
+        return int(self.L.or_tag(name.encode()))
+
+    def threefry(self, key, ctr) -> np.ndarray:
+        k, c = key_of(key), np.array(ctr, dtype=np.uint64)
+        out = np.zeros(4, dtype=np.uint64)
+        self.L.or_threefry(_p64(k), _p64(c), _p64(out))
+        return out
+
+    def word(self, key, purpose, sub, index) -> int:
+        return int(self.L.or_stream_word(_p64(key_of(key)), self.tag(purpose), sub, index))
+
+    def uniform_below(self, key, purpose, sub, bound, index) -> int:
+        return int(self.L.or_uniform_below(_p64(key_of(key)), self.tag(purpose), sub, bound,
+                                           index))
+
+    def bernoulli(self, key, purpose, sub, p, index) -> int:
+        return int(self.L.or_bernoulli(_p64(key_of(key)), self.tag(purpose), sub, p, index))
+
+    def bits(self, key, purpose, sub, nbits) -> np.ndarray:
+        out = np.zeros(max(nwords(nbits), 1), dtype=np.uint64)
+        self.L.or_stream_bits(_p64(key_of(key)), self.tag(purpose), sub, nbits, _p64(out))
+        return out[: nwords(nbits)]
+
+    def make_input(self, key, p, nbits, nthreads=0) -> np.ndarray:
+        out = np.zeros(max(nwords(nbits), 1), dtype=np.uint64)
+        self.L.or_make_input(_p64(key_of(key)), float(p), nbits, _p64(out), nthreads)
+        return out[: nwords(nbits)]
+
+    # -- sampler ----------------------------------------------------------------
+    def assign_subblocks(self, n, s, key, nthreads=0):
+        a = np.zeros(max(n, 1), dtype=np.uint32)
+        c = np.zeros(max(s, 1), dtype=np.uint64)
+        rc = self.L.or_assign_subblocks(n, s, _p64(key_of(key)), _p32(a), _p64(c), nthreads)
+        if rc:
+            raise ValueError("assign_subblocks: n_subblocks must be positive")
+        return a[:n], c[:s]
+
+    def sift_partition(self, keep, assignment, s):
+        keep = np.ascontiguousarray(keep, dtype=np.uint8)
+        assignment = np.ascontiguousarray(assignment, dtype=np.uint32)
+        n = len(keep)
+        off = np.zeros(s + 1, dtype=np.uint64)
+        idx = np.zeros(max(int(keep.sum()), 1), dtype=np.uint64)
+        self.L.or_sift_partition(_p8(keep), n, _p32(assignment), s, _p64(off), _p64(idx))
+        return off, idx[: int(off[-1])]
+
+    # -- toeplitz ---------------------------------------------------------------
+    def toeplitz_hash(self, seed, m, n, x) -> np.ndarray:
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+        self.L.or_toeplitz_hash(_p64(seed), m, n, _p64(x), _p64(out))
+        return out[: nwords(m)]
+
+    def dense_toeplitz(self, seed, m, n, x) -> np.ndarray:
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+        self.L.or_dense_toeplitz(_p64(seed), m, n, _p64(x), _p64(out))
+        return out[: nwords(m)]
+
+    def blocked_toeplitz_hash(self, seed, m, n, x, mp, np_) -> np.ndarray:
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+        self.L.or_blocked_toeplitz_hash(_p64(seed), m, n, _p64(x), mp, np_, _p64(out))
+        return out[: nwords(m)]
+
+    def reverse_bits(self, x, n) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        y = np.zeros(max(nwords(n), 1), dtype=np.uint64)
+        self.L.or_reverse_bits(_p64(x), n, _p64(y))
+        return y
+
+    def toeplitz_rows(self, seed, n, y_rev, rows) -> np.ndarray:
+        """K[i] for each i in rows; seed must be padded to cover max(rows)+64*ceil(n/64)+64."""
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        y_rev = np.ascontiguousarray(y_rev, dtype=np.uint64)
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        out = np.zeros(max(len(rows), 1), dtype=np.uint8)
+        self.L.or_toeplitz_rows(_p64(seed), n, _p64(y_rev), _p64(rows), len(rows), _p8(out))
+        return out[: len(rows)]
+
+    # -- abort threshold --------------------------------------------------------
+    def block_limit(self, n, p, eps, m):
+        err = C.c_int(0)
+        v = self.L.or_block_limit(n, p, eps, m, C.byref(err))
+        return int(v), err.value
+
+    def binomial_tail_bound(self, n, L, p):
+        return float(self.L.or_binomial_tail_bound(n, L, p))
+
+    def relative_entropy(self, x, p):
+        return float(self.L.or_relative_entropy(x, p))
+
+    def cycle_estimate(self, i, o, mp):
+        err = C.c_int(0)
+        v = self.L.or_cycle_estimate(i, o, mp, C.byref(err))
+        return int(v), err.value
+
+    # -- whole path -------------------------------------------------------------
+    def extract(self, x, n, s, samp, hsh, per_block, k, nthreads=0):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        key = np.zeros(max(nwords(s * k), 1), dtype=np.uint64)
+        nj = np.zeros(s, dtype=np.uint64)
+        rc = self.L.or_extract(_p64(x), n, s, _p64(key_of(samp)), _p64(key_of(hsh)),
+                               int(per_block), k, _p64(key), _p64(nj), nthreads)
+        if rc:
+            raise ValueError("toeplitz: m and n must be positive (empty sub-block)")
+        return key[: nwords(s * k)], nj
+
+    def extract_selected(self, x, n, s, samp, hsh, per_block, k, which, nthreads=0):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        which = np.ascontiguousarray(which, dtype=np.uint32)
+        kw = nwords(k)
+        keys = np.zeros(max(len(which) * kw, 1), dtype=np.uint64)
+        nj = np.zeros(s, dtype=np.uint64)
+        rc = self.L.or_extract_selected(_p64(x), n, s, _p64(key_of(samp)), _p64(key_of(hsh)),
+                                        int(per_block), k, _p32(which), len(which),
+                                        _p64(keys), _p64(nj), nthreads)
+        if rc:
+            raise ValueError("toeplitz: m and n must be positive (empty sub-block)")
+        return keys[: len(which) * kw].reshape(len(which), kw), nj
+
+    def fnv(self, words) -> int:
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        return int(self.L.or_fnv_words(_p64(w), len(w)))
+
+
+class Reference:
+    """The reference's own implementation (compiled from /root/reference by oracle/Makefile)."""
+
+    def __init__(self, path: str | None = None):
+        path = path or os.path.join(HERE, "_ref", "libssbh_ref.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = C.CDLL(path)
+        self.L = L
+        L.ref_prf_block.argtypes = [U64P, U64P, U64P]
+        L.ref_tag.restype = C.c_uint64
+        L.ref_tag.argtypes = [C.c_char_p]
+        L.ref_stream_word.restype = C.c_uint64
+        L.ref_stream_word.argtypes = [U64P, C.c_char_p, C.c_uint64, C.c_uint64]
+        L.ref_uniform_below.restype = C.c_int
+        L.ref_uniform_below.argtypes = [U64P, C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        U64P]
+        L.ref_bernoulli.restype = C.c_int
+        L.ref_bernoulli.argtypes = [U64P, C.c_char_p, C.c_uint64, C.c_double, C.c_uint64]
+        L.ref_stream_bits.argtypes = [U64P, C.c_char_p, C.c_uint64, C.c_uint64, U64P]
+        L.ref_assign_subblocks.restype = C.c_int
+        L.ref_assign_subblocks.argtypes = [C.c_uint64, C.c_uint32, U64P, U32P, U64P]
+        L.ref_sift_partition.restype = C.c_int
+        L.ref_sift_partition.argtypes = [U8P, C.c_uint64, U32P, C.c_uint32, U64P, U64P, U64P]
+        L.ref_toeplitz_hash.restype = C.c_int
+        L.ref_toeplitz_hash.argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64, U64P]
+        L.ref_blocked_toeplitz_hash.restype = C.c_int
+        L.ref_blocked_toeplitz_hash.argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64,
+                                                C.c_uint64, C.c_uint64, U64P]
+        L.ref_block_limit.restype = C.c_uint64
+        L.ref_block_limit.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64,
+                                      C.POINTER(C.c_int)]
+        L.ref_binomial_tail_bound.restype = C.c_double
+        L.ref_binomial_tail_bound.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
+        L.ref_cycle_estimate.restype = C.c_uint64
+        L.ref_cycle_estimate.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_int)]
+        L.ref_extract.restype = C.c_int
+        L.ref_extract.argtypes = [U64P, C.c_uint64, C.c_uint32, U64P, U64P, C.c_int,
+                                  C.c_uint64, U64P, U64P]
+        L.ref_time_sample.restype = C.c_double
+        L.ref_time_sample.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_double, U64P, U64P,
+                                      U64P, C.c_uint32, U64P, U64P]
+
+    def prf_block(self, key, ctr):
+        out = np.zeros(4, dtype=np.uint64)
+        self.L.ref_prf_block(_p64(key_of(key)), _p64(np.array(ctr, dtype=np.uint64)), _p64(out))
+        return out
+
+    def word(self, key, purpose, sub, i):
+        return int(self.L.ref_stream_word(_p64(key_of(key)), purpose.encode(), sub, i))
+
+    def uniform_below(self, key, purpose, sub, bound, i):
+        out = np.zeros(1, dtype=np.uint64)
+        rc = self.L.ref_uniform_below(_p64(key_of(key)), purpose.encode(), sub, bound, i,
+                                      _p64(out))
+        if rc:
+            raise ValueError("uniform_below: bound must be positive")
+        return int(out[0])
+
+    def bernoulli(self, key, purpose, sub, p, i):
+        return int(self.L.ref_bernoulli(_p64(key_of(key)), purpose.encode(), sub, p, i))
+
+    def bits(self, key, purpose, sub, nbits):
+        out = np.zeros(max(nwords(nbits), 1), dtype=np.uint64)
+        self.L.ref_stream_bits(_p64(key_of(key)), purpose.encode(), sub, nbits, _p64(out))
+        return out[: nwords(nbits)]
+
+    def assign_subblocks(self, n, s, key):
+        a = np.zeros(max(n, 1), dtype=np.uint32)
+        c = np.zeros(max(s, 1), dtype=np.uint64)
+        rc = self.L.ref_assign_subblocks(n, s, _p64(key_of(key)), _p32(a), _p64(c))
+        if rc:
+            raise ValueError("assign_subblocks: n_subblocks must be positive")
+        return a[:n], c[:s]
+
+    def sift_partition(self, keep, assignment, s):
+        keep = np.ascontiguousarray(keep, dtype=np.uint8)
+        assignment = np.ascontiguousarray(assignment, dtype=np.uint32)
+        off = np.zeros(s + 1, dtype=np.uint64)
+        idx = np.zeros(max(int(keep.sum()), 1), dtype=np.uint64)
+        ml = np.zeros(1, dtype=np.uint64)
+        rc = self.L.ref_sift_partition(_p8(keep), len(keep), _p32(assignment), s, _p64(off),
+                                       _p64(idx), _p64(ml))
+        if rc:
+            raise ValueError("sift_partition: flag count does not match partition")
+        return off, idx[: int(off[-1])], int(ml[0])
+
+    def toeplitz_hash(self, seed, m, n, x, nin=None):
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+        rc = self.L.ref_toeplitz_hash(_p64(seed), m, n, _p64(x), n if nin is None else nin,
+                                      _p64(out))
+        if rc:
+            raise ValueError(f"toeplitz: invalid argument (code {rc})")
+        return out[: nwords(m)]
+
+    def blocked_toeplitz_hash(self, seed, m, n, x, mp, np_):
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+        rc = self.L.ref_blocked_toeplitz_hash(_p64(seed), m, n, _p64(x), n, mp, np_, _p64(out))
+        if rc:
+            raise ValueError(f"toeplitz: invalid argument (code {rc})")
+        return out[: nwords(m)]
+
+    def block_limit(self, n, p, eps, m):
+        err = C.c_int(0)
+        v = self.L.ref_block_limit(n, p, eps, m, C.byref(err))
+        return int(v), err.value
+
+    def cycle_estimate(self, i, o, mp):
+        err = C.c_int(0)
+        v = self.L.ref_cycle_estimate(i, o, mp, C.byref(err))
+        return int(v), err.value
+
+    def extract(self, x, n, s, samp, hsh, per_block, k):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        key = np.zeros(max(nwords(s * k), 1), dtype=np.uint64)
+        nj = np.zeros(s, dtype=np.uint64)
+        rc = self.L.ref_extract(_p64(x), n, s, _p64(key_of(samp)), _p64(key_of(hsh)),
+                                int(per_block), k, _p64(key), _p64(nj))
+        if rc:
+            raise ValueError(f"extract failed (code {rc})")
+        return key[: nwords(s * k)], nj
+
+    def time_sample(self, n_sample, s_sample, k, p, in_seed, samp, hsh, nblocks):
+        bits = np.zeros(1, dtype=np.uint64)
+        dig = np.zeros(1, dtype=np.uint64)
+        secs = self.L.ref_time_sample(n_sample, s_sample, k, p, _p64(key_of(in_seed)),
+                                      _p64(key_of(samp)), _p64(key_of(hsh)), nblocks,
+                                      _p64(bits), _p64(dig))
+        return float(secs), int(bits[0]), int(dig[0])
