@@ -1,0 +1,208 @@
+/*
+ * ssbh_cuda.h — C-ABI of the B200-native sampled sub-block Toeplitz extractor.
+ *
+ * Plain pointers and sizes only (no C++ / torch types). Every entry point returns an
+ * ssbh_status; on failure ssbh_last_error() holds a thread-local message. The C++
+ * drop-in layer (include/ssbh/*.hpp) maps the codes back to the reference's exception
+ * types (std::invalid_argument, ssbh::infeasible_error, std::overflow_error,
+ * ssbh::io_error — proj/include/ssbh/errors.hpp:10-18).
+ *
+ * Bit layout (proj/include/ssbh/bitstring.hpp:11-15): bit k of a stream is bit k%64 of
+ * uint64 word k/64, storage past the length is zero. Host buffers are uint64 words;
+ * device buffers may be viewed as uint32 words (little-endian, same bit order).
+ *
+ * "Reference:" lines cite the reference interface each entry point replaces
+ * (paths under the reference tree proj/).
+ *
+ * Every compute entry point runs on the GPU (sm_100a); there is no CPU fallback.
+ * Without a usable CUDA device they return SSBH_NO_DEVICE.
+ */
+#ifndef SSBH_CUDA_H
+#define SSBH_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSBH_ABI_VERSION 1
+
+typedef enum {
+    SSBH_OK = 0,
+    SSBH_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    SSBH_INFEASIBLE = 2,       /* ssbh::infeasible_error (errors.hpp:10-13) */
+    SSBH_OVERFLOW = 3,         /* std::overflow_error (toeplitz.cpp:86-87) */
+    SSBH_IO = 4,               /* ssbh::io_error (errors.hpp:15-18) */
+    SSBH_CUDA = 5,             /* CUDA runtime / launch failure */
+    SSBH_NO_DEVICE = 6,        /* no usable sm_100 device */
+    SSBH_ABORT_OVERSIZE = 7    /* abort_check failed (ssbh_main.cpp:324-326) */
+} ssbh_status;
+
+/* ------------------------------------------------------------------ runtime */
+int ssbh_abi_version(void);
+const char* ssbh_last_error(void);
+/* Number of CUDA devices usable by the library (0 when none). */
+int ssbh_device_count(void);
+/* Selects the device used by subsequent calls from this host thread. */
+ssbh_status ssbh_set_device(int device);
+
+/* ---------------------------------------------------------------------- PRF */
+/* Reference: prf::block — proj/include/ssbh/prf.hpp:26-27, proj/src/prf.cpp:47-76.
+ * Scalar Threefry4x64-20 (same __host__ __device__ function as the kernels). */
+ssbh_status ssbh_prf_block(const uint64_t key[4], const uint64_t ctr[4], uint64_t out[4]);
+
+/* Reference: prf::tag — proj/include/ssbh/prf.hpp:29-37 (FNV-1a-64). */
+uint64_t ssbh_prf_tag(const char* purpose, size_t len);
+
+/* Reference: KeyedStream::bits — proj/include/ssbh/prf.hpp:65, proj/src/prf.cpp:104-115.
+ * Host output, ceil(nbits/64) words, zero tail. GPU-generated. */
+ssbh_status ssbh_stream_bits(const uint64_t key[4], uint64_t tag, uint64_t sub, uint64_t nbits,
+                             uint64_t* out_words);
+
+/* Reference: KeyedStream::word — prf.hpp:56, prf.cpp:80-82; out[q] = word(first + q). */
+ssbh_status ssbh_stream_words(const uint64_t key[4], uint64_t tag, uint64_t sub, uint64_t first,
+                              uint64_t count, uint64_t* out);
+
+/* Reference: KeyedStream::uniform_below — prf.hpp:59, prf.cpp:84-94 (rejection sampled,
+ * retry counter in ctr[3]); out[q] = uniform_below(bound, first + q). bound == 0 ->
+ * SSBH_INVALID_ARGUMENT. */
+ssbh_status ssbh_stream_uniform_below(const uint64_t key[4], uint64_t tag, uint64_t sub,
+                                      uint64_t bound, uint64_t first, uint64_t count,
+                                      uint64_t* out);
+
+/* Reference: KeyedStream::bernoulli — prf.hpp:62, prf.cpp:96-102. Packed output: bit q of
+ * out_words = bernoulli(p, first + q). p outside [0,1] -> SSBH_INVALID_ARGUMENT. */
+ssbh_status ssbh_stream_bernoulli(const uint64_t key[4], uint64_t tag, uint64_t sub, double p,
+                                  uint64_t first, uint64_t count, uint64_t* out_words);
+
+/* ------------------------------------------------------------------ sampler */
+/* Reference: assign_subblocks — proj/include/ssbh/sampling.hpp:37-38,
+ * proj/src/sampling.cpp:10-25. assignment[i] = V_i in [1, s] (uint32), raw_counts[s]. */
+ssbh_status ssbh_assign_subblocks(uint64_t n_rounds, uint32_t n_subblocks, const uint64_t key[4],
+                                  uint32_t* assignment, uint64_t* raw_counts);
+
+/* Reference: sift_partition — sampling.hpp:41, sampling.cpp:27-39. CSR result: block j's
+ * kept round indices (round order) are indices[offsets[j] .. offsets[j+1]);
+ * offsets has s+1 entries, indices capacity >= number of kept rounds. keep may be NULL
+ * (all rounds kept). Assignment values outside [1, s] -> SSBH_INVALID_ARGUMENT. */
+ssbh_status ssbh_sift_partition(const uint8_t* keep, uint64_t n, const uint32_t* assignment,
+                                uint32_t n_subblocks, uint64_t* offsets, uint64_t* indices,
+                                uint64_t* max_len);
+
+/* Reference: block_limit / binomial_tail_bound / relative_entropy / abort_check —
+ * sampling.hpp:45-57, sampling.cpp:41-96. Host scalar numerics (not data-parallel). */
+ssbh_status ssbh_block_limit(uint64_t n_rounds, double p_sift, double eps_abort,
+                             uint64_t m_blocks, uint64_t* limit);
+ssbh_status ssbh_binomial_tail_bound(uint64_t n_rounds, uint64_t limit, double p_sift,
+                                     double* out);
+ssbh_status ssbh_relative_entropy(double x, double p, double* out);
+int ssbh_abort_check(const uint64_t* lengths, uint64_t count, uint64_t limit);
+
+/* ----------------------------------------------------------------- toeplitz */
+/* Reference: toeplitz_hash — proj/include/ssbh/toeplitz.hpp:27, proj/src/toeplitz.cpp:34-52
+ * (and ToeplitzSeed validation toeplitz.cpp:9-15): K = T x over GF(2) with
+ * T[i][j] = seed[(n-1)+i-j]; seed has m+n-1 bits, input n bits, out m bits (host words). */
+ssbh_status ssbh_toeplitz_hash(const uint64_t* seed, uint64_t m, uint64_t n,
+                               const uint64_t* input, uint64_t input_bits, uint64_t* out);
+
+/* Reference: blocked_toeplitz_hash — toeplitz.hpp:31-32, toeplitz.cpp:54-76. The product is
+ * bit-identical for every blocking; m_prime/n_prime are validated like the reference. */
+ssbh_status ssbh_blocked_toeplitz_hash(const uint64_t* seed, uint64_t m, uint64_t n,
+                                       const uint64_t* input, uint64_t input_bits,
+                                       uint64_t m_prime, uint64_t n_prime, uint64_t* out);
+
+/* Reference: cycle_estimate — toeplitz.hpp:36-37, toeplitz.cpp:78-89 (host scalar). */
+ssbh_status ssbh_cycle_estimate(uint64_t input_len, uint64_t output_len, uint64_t m_prime,
+                                uint64_t* out);
+
+/* Batched hash (the per-block loop of ssbh_main.cpp:328-336 / pipeline.cpp:129-136 in one
+ * launch): block b has input bits inputs[in_off[b]*64 ...] of length n[b], seed words
+ * seeds[seed_off[b] ...] of m+n[b]-1 bits; all blocks have m output bits; the results are
+ * concatenated (bitstring.cpp:42-47) into out (ceil(count*m/64) words). Host buffers. */
+ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, const uint64_t* n,
+                                     const uint64_t* inputs, const uint64_t* in_off,
+                                     const uint64_t* seeds, const uint64_t* seed_off,
+                                     uint64_t* out);
+
+/* -------------------------------------------------------- fused extraction */
+/* The whole file-mode hot path (ssbh_main.cpp:306-345 with distinct seeds):
+ * assign_subblocks(n, s, samp) -> sift (all kept, or keep mask) -> per block j gather ->
+ * seed = KeyedStream(hash, "hash-seed", per_block ? j : 0).bits(k + n_j - 1) ->
+ * toeplitz_hash -> concatenation in block order.
+ *
+ * Blocks [block_first, block_first + block_count) are produced (multi-GPU sharding:
+ * each rank owns a contiguous block range; block_count == 0 means all s blocks).
+ * block_limit != 0 enables the reference's strict abort (any n_j > block_limit ->
+ * SSBH_ABORT_OVERSIZE, key untouched). An empty owned sub-block -> SSBH_INVALID_ARGUMENT
+ * ("toeplitz: m and n must be positive", as ToeplitzSeed throws, toeplitz.cpp:11-12). */
+typedef struct {
+    uint64_t n_rounds;      /* n input bits */
+    uint32_t n_subblocks;   /* s */
+    uint32_t per_block_seed;/* 0: shared seed (sub 0); 1: sub = j (pipeline.cpp:132) */
+    uint64_t out_bits;      /* k output bits per sub-block */
+    uint64_t samp_key[4];   /* MasterSeed for "sampling" */
+    uint64_t hash_key[4];   /* MasterSeed for "hash-seed" */
+    uint32_t block_first;
+    uint32_t block_count;   /* 0 = all */
+    uint64_t block_limit;   /* 0 = no abort check */
+} ssbh_extract_params;
+
+typedef struct {
+    double ms_sample;       /* Threefry + count + scan (device, CUDA events) */
+    double ms_scatter;      /* stable partition + reversed bit pack */
+    double ms_seed;         /* Toeplitz seed generation */
+    double ms_hash;         /* GF(2) Toeplitz hash */
+    double ms_total;
+    uint64_t hash_word_ops; /* sum_j n_j * k / 32 over owned blocks (algorithmic LOP3) */
+    uint64_t max_len;       /* max owned n_j */
+    uint64_t min_len;       /* min owned n_j */
+    uint32_t hash_launches; /* kernel launches of the hash kernel */
+    uint32_t launches;      /* all kernel launches of the run */
+} ssbh_extract_stats;
+
+/* Opaque device plan: buffers sized once for (n, s, k, ownership), reused across runs. */
+typedef struct ssbh_plan ssbh_plan;
+
+ssbh_status ssbh_plan_create(const ssbh_extract_params* params, ssbh_plan** plan);
+ssbh_status ssbh_plan_destroy(ssbh_plan* plan);
+/* Device bytes held by the plan. */
+uint64_t ssbh_plan_device_bytes(const ssbh_plan* plan);
+
+/* Device-resident run on `stream` (cudaStream_t as void*; NULL = legacy default stream).
+ * d_input: ceil(n/32) uint32 words on the plan's device; d_key: output words
+ * (ceil(owned*k/32) uint32, written in full); d_lengths: owned n_j (uint64, may be NULL).
+ * Asynchronous: errors detected on the device are reported by ssbh_plan_check. The
+ * sampling / hash seeds may be changed per run (samp_key/hash_key may be NULL = plan's). */
+ssbh_status ssbh_plan_run_device(ssbh_plan* plan, const uint32_t* d_input, uint32_t* d_key,
+                                 uint64_t* d_lengths, const uint64_t* samp_key,
+                                 const uint64_t* hash_key, void* stream);
+/* Synchronizes the plan's last run and converts device-side flags to a status
+ * (empty block / oversize abort). Fills stats when non-NULL (timings need
+ * ssbh_plan_set_timing(plan, 1) before the run). */
+ssbh_status ssbh_plan_check(ssbh_plan* plan, ssbh_extract_stats* stats);
+ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
+
+/* Host-buffer entry point (what a reference caller binds): input host words (n bits),
+ * out_key host words (ceil(owned*k/64)), out_lengths host (owned entries, may be NULL).
+ * H2D, device run, D2H; synchronous. */
+ssbh_status ssbh_extract(const ssbh_extract_params* params, const uint64_t* input,
+                         uint64_t* out_key, uint64_t* out_lengths, ssbh_extract_stats* stats);
+/* Same through an existing plan (no re-allocation); copies through pinned staging. */
+ssbh_status ssbh_plan_run_host(ssbh_plan* plan, const uint64_t* input, uint64_t* out_key,
+                               uint64_t* out_lengths, ssbh_extract_stats* stats);
+
+/* Synthetic input on the device: p == 0.5 -> KeyedStream(key,"input").bits(n);
+ * else bit i = bernoulli(p, i) of the same stream. d_out: ceil(n/32) uint32 words. */
+ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbits,
+                                   uint32_t* d_out, void* stream);
+
+/* Diagnostics (not a reference interface): measured LOP3 lane-ops/s of the current device
+ * (the int-ALU roofline denominator of the hash kernel) over one timed launch. */
+ssbh_status ssbh_measure_lop3_peak(uint32_t iters, double* lop3_per_s, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSBH_CUDA_H */

@@ -1,0 +1,438 @@
+"""paper_2308_02856_b200 — B200-native sampled sub-block Toeplitz extractor.
+
+The product is two in-tree native libraries:
+
+* ``libssbh_cuda.so`` — hand-written sm_100a kernels behind the C-ABI declared in
+  ``include/ssbh_cuda.h`` (Threefry sampler, stable bit partition, GF(2) Toeplitz
+  hash, concatenation).
+* ``libssbh.so`` — the reference's C++ API (``include/ssbh/*.hpp``: ``BitString``,
+  ``KeyedStream``, ``assign_subblocks``, ``sift_partition``, ``toeplitz_hash`` …) as a
+  drop-in over that C-ABI.
+
+This module is a thin ``ctypes`` view of the C-ABI for the Python test-suite and
+``bench.py``. It never falls back to a CPU implementation: loading fails loudly when
+the CUDA library is missing, and compute calls raise ``NoDeviceError`` without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libssbh_cuda.so")
+CXX_LIB_PATH = os.path.join(HERE, "libssbh.so")
+
+U64P = C.POINTER(C.c_uint64)
+U32P = C.POINTER(C.c_uint32)
+U8P = C.POINTER(C.c_uint8)
+
+# status codes (include/ssbh_cuda.h)
+OK, INVALID_ARGUMENT, INFEASIBLE, OVERFLOW, IO, CUDA, NO_DEVICE, ABORT_OVERSIZE = range(8)
+
+# every exported symbol of include/ssbh_cuda.h
+ABI_SYMBOLS = (
+    "ssbh_abi_version", "ssbh_last_error", "ssbh_device_count", "ssbh_set_device",
+    "ssbh_prf_block", "ssbh_prf_tag", "ssbh_stream_bits", "ssbh_stream_words",
+    "ssbh_stream_uniform_below", "ssbh_stream_bernoulli", "ssbh_assign_subblocks",
+    "ssbh_sift_partition", "ssbh_block_limit", "ssbh_binomial_tail_bound",
+    "ssbh_relative_entropy", "ssbh_abort_check", "ssbh_toeplitz_hash",
+    "ssbh_blocked_toeplitz_hash", "ssbh_cycle_estimate", "ssbh_toeplitz_hash_batch",
+    "ssbh_plan_create", "ssbh_plan_destroy", "ssbh_plan_device_bytes", "ssbh_plan_run_device",
+    "ssbh_plan_check", "ssbh_plan_set_timing", "ssbh_extract", "ssbh_plan_run_host",
+    "ssbh_make_input_device", "ssbh_measure_lop3_peak",
+)
+
+
+class SsbhError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+        self.msg = msg
+
+
+class InvalidArgument(SsbhError, ValueError):
+    pass
+
+
+class Infeasible(SsbhError):
+    pass
+
+
+class OverflowErr(SsbhError, OverflowError):
+    pass
+
+
+class NoDeviceError(SsbhError):
+    pass
+
+
+class AbortOversize(SsbhError):
+    pass
+
+
+_EXC = {INVALID_ARGUMENT: InvalidArgument, INFEASIBLE: Infeasible, OVERFLOW: OverflowErr,
+        NO_DEVICE: NoDeviceError, ABORT_OVERSIZE: AbortOversize}
+
+
+class ExtractParams(C.Structure):
+    _fields_ = [("n_rounds", C.c_uint64), ("n_subblocks", C.c_uint32),
+                ("per_block_seed", C.c_uint32), ("out_bits", C.c_uint64),
+                ("samp_key", C.c_uint64 * 4), ("hash_key", C.c_uint64 * 4),
+                ("block_first", C.c_uint32), ("block_count", C.c_uint32),
+                ("block_limit", C.c_uint64)]
+
+
+class ExtractStats(C.Structure):
+    _fields_ = [("ms_sample", C.c_double), ("ms_scatter", C.c_double), ("ms_seed", C.c_double),
+                ("ms_hash", C.c_double), ("ms_total", C.c_double),
+                ("hash_word_ops", C.c_uint64), ("max_len", C.c_uint64),
+                ("min_len", C.c_uint64), ("hash_launches", C.c_uint32),
+                ("launches", C.c_uint32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (make) first — "
+                          "the B200 path has no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    st = C.c_int
+    L.ssbh_abi_version.restype = C.c_int
+    L.ssbh_last_error.restype = C.c_char_p
+    L.ssbh_device_count.restype = C.c_int
+    L.ssbh_set_device.restype = st
+    L.ssbh_set_device.argtypes = [C.c_int]
+    L.ssbh_prf_block.restype = st
+    L.ssbh_prf_block.argtypes = [U64P, U64P, U64P]
+    L.ssbh_prf_tag.restype = C.c_uint64
+    L.ssbh_prf_tag.argtypes = [C.c_char_p, C.c_size_t]
+    L.ssbh_stream_bits.restype = st
+    L.ssbh_stream_bits.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64, U64P]
+    L.ssbh_stream_words.restype = st
+    L.ssbh_stream_words.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, U64P]
+    L.ssbh_stream_uniform_below.restype = st
+    L.ssbh_stream_uniform_below.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64,
+                                            C.c_uint64, C.c_uint64, U64P]
+    L.ssbh_stream_bernoulli.restype = st
+    L.ssbh_stream_bernoulli.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
+                                        C.c_uint64, U64P]
+    L.ssbh_assign_subblocks.restype = st
+    L.ssbh_assign_subblocks.argtypes = [C.c_uint64, C.c_uint32, U64P, U32P, U64P]
+    L.ssbh_sift_partition.restype = st
+    L.ssbh_sift_partition.argtypes = [U8P, C.c_uint64, U32P, C.c_uint32, U64P, U64P, U64P]
+    L.ssbh_block_limit.restype = st
+    L.ssbh_block_limit.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, U64P]
+    L.ssbh_binomial_tail_bound.restype = st
+    L.ssbh_binomial_tail_bound.argtypes = [C.c_uint64, C.c_uint64, C.c_double,
+                                           C.POINTER(C.c_double)]
+    L.ssbh_relative_entropy.restype = st
+    L.ssbh_relative_entropy.argtypes = [C.c_double, C.c_double, C.POINTER(C.c_double)]
+    L.ssbh_abort_check.restype = C.c_int
+    L.ssbh_abort_check.argtypes = [U64P, C.c_uint64, C.c_uint64]
+    L.ssbh_toeplitz_hash.restype = st
+    L.ssbh_toeplitz_hash.argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64, U64P]
+    L.ssbh_blocked_toeplitz_hash.restype = st
+    L.ssbh_blocked_toeplitz_hash.argtypes = [U64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64,
+                                             C.c_uint64, C.c_uint64, U64P]
+    L.ssbh_cycle_estimate.restype = st
+    L.ssbh_cycle_estimate.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, U64P]
+    L.ssbh_toeplitz_hash_batch.restype = st
+    L.ssbh_toeplitz_hash_batch.argtypes = [C.c_uint64, C.c_uint64, U64P, U64P, U64P, U64P,
+                                           U64P, U64P]
+    L.ssbh_plan_create.restype = st
+    L.ssbh_plan_create.argtypes = [C.POINTER(ExtractParams), C.POINTER(C.c_void_p)]
+    L.ssbh_plan_destroy.restype = st
+    L.ssbh_plan_destroy.argtypes = [C.c_void_p]
+    L.ssbh_plan_device_bytes.restype = C.c_uint64
+    L.ssbh_plan_device_bytes.argtypes = [C.c_void_p]
+    L.ssbh_plan_run_device.restype = st
+    L.ssbh_plan_run_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, U64P,
+                                       U64P, C.c_void_p]
+    L.ssbh_plan_check.restype = st
+    L.ssbh_plan_check.argtypes = [C.c_void_p, C.POINTER(ExtractStats)]
+    L.ssbh_plan_set_timing.restype = st
+    L.ssbh_plan_set_timing.argtypes = [C.c_void_p, C.c_int]
+    L.ssbh_extract.restype = st
+    L.ssbh_extract.argtypes = [C.POINTER(ExtractParams), U64P, U64P, U64P,
+                               C.POINTER(ExtractStats)]
+    L.ssbh_plan_run_host.restype = st
+    L.ssbh_plan_run_host.argtypes = [C.c_void_p, U64P, U64P, U64P, C.POINTER(ExtractStats)]
+    L.ssbh_make_input_device.restype = st
+    L.ssbh_make_input_device.argtypes = [U64P, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.ssbh_measure_lop3_peak.restype = st
+    L.ssbh_measure_lop3_peak.argtypes = [C.c_uint32, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != OK:
+        msg = lib.ssbh_last_error().decode(errors="replace")
+        raise _EXC.get(status, SsbhError)(status, msg)
+
+
+def _p64(a):
+    return a.ctypes.data_as(U64P)
+
+
+def _p32(a):
+    return a.ctypes.data_as(U32P)
+
+
+def _p8(a):
+    return a.ctypes.data_as(U8P)
+
+
+def key_of(seed) -> np.ndarray:
+    """BASELINE integer seed N -> MasterSeed::from_hex('%064x' % N) = words {0,0,0,N}."""
+    if isinstance(seed, (list, tuple, np.ndarray)):
+        return np.ascontiguousarray(seed, dtype=np.uint64)
+    return np.array([0, 0, 0, int(seed)], dtype=np.uint64)
+
+
+def nwords(nbits: int) -> int:
+    return (int(nbits) + 63) // 64
+
+
+def device_count() -> int:
+    return int(lib.ssbh_device_count())
+
+
+def tag(purpose: str) -> int:
+    b = purpose.encode()
+    return int(lib.ssbh_prf_tag(b, len(b)))
+
+
+def prf_block(key, ctr) -> np.ndarray:
+    out = np.zeros(4, dtype=np.uint64)
+    _check(lib.ssbh_prf_block(_p64(key_of(key)), _p64(np.asarray(ctr, dtype=np.uint64)),
+                              _p64(out)))
+    return out
+
+
+def stream_bits(key, purpose: str, sub: int, nbits: int) -> np.ndarray:
+    out = np.zeros(max(nwords(nbits), 1), dtype=np.uint64)
+    _check(lib.ssbh_stream_bits(_p64(key_of(key)), tag(purpose), sub, nbits, _p64(out)))
+    return out[: nwords(nbits)]
+
+
+def stream_words(key, purpose, sub, first, count) -> np.ndarray:
+    out = np.zeros(max(count, 1), dtype=np.uint64)
+    _check(lib.ssbh_stream_words(_p64(key_of(key)), tag(purpose), sub, first, count, _p64(out)))
+    return out[:count]
+
+
+def stream_uniform_below(key, purpose, sub, bound, first, count) -> np.ndarray:
+    out = np.zeros(max(count, 1), dtype=np.uint64)
+    _check(lib.ssbh_stream_uniform_below(_p64(key_of(key)), tag(purpose), sub, bound, first,
+                                         count, _p64(out)))
+    return out[:count]
+
+
+def stream_bernoulli(key, purpose, sub, p, first, count) -> np.ndarray:
+    out = np.zeros(max(nwords(count), 1), dtype=np.uint64)
+    _check(lib.ssbh_stream_bernoulli(_p64(key_of(key)), tag(purpose), sub, p, first, count,
+                                     _p64(out)))
+    return out[: nwords(count)]
+
+
+def assign_subblocks(n: int, s: int, key):
+    a = np.zeros(max(n, 1), dtype=np.uint32)
+    c = np.zeros(max(s, 1), dtype=np.uint64)
+    _check(lib.ssbh_assign_subblocks(n, s, _p64(key_of(key)), _p32(a), _p64(c)))
+    return a[:n], c[:s]
+
+
+def sift_partition(keep, assignment, s: int):
+    assignment = np.ascontiguousarray(assignment, dtype=np.uint32)
+    n = len(assignment)
+    kp = None if keep is None else np.ascontiguousarray(keep, dtype=np.uint8)
+    if kp is not None and len(kp) != n:
+        raise InvalidArgument(INVALID_ARGUMENT,
+                              "sift_partition: flag count does not match partition")
+    off = np.zeros(s + 1, dtype=np.uint64)
+    idx = np.zeros(max(n, 1), dtype=np.uint64)
+    ml = np.zeros(1, dtype=np.uint64)
+    _check(lib.ssbh_sift_partition(None if kp is None else _p8(kp), n, _p32(assignment), s,
+                                   _p64(off), _p64(idx), _p64(ml)))
+    return off, idx[: int(off[-1])], int(ml[0])
+
+
+def toeplitz_hash(seed, m: int, n: int, x, input_bits: int | None = None) -> np.ndarray:
+    seed = np.ascontiguousarray(seed, dtype=np.uint64)
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+    _check(lib.ssbh_toeplitz_hash(_p64(seed), m, n, _p64(x), n if input_bits is None else
+                                  input_bits, _p64(out)))
+    return out[: nwords(m)]
+
+
+def blocked_toeplitz_hash(seed, m, n, x, mp, np_) -> np.ndarray:
+    seed = np.ascontiguousarray(seed, dtype=np.uint64)
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    out = np.zeros(max(nwords(m), 1), dtype=np.uint64)
+    _check(lib.ssbh_blocked_toeplitz_hash(_p64(seed), m, n, _p64(x), n, mp, np_, _p64(out)))
+    return out[: nwords(m)]
+
+
+def toeplitz_hash_batch(m: int, ns, inputs, in_off, seeds, seed_off) -> np.ndarray:
+    """Hash len(ns) blocks (each its own n and seed, common m); returns the concatenation."""
+    ns = np.ascontiguousarray(ns, dtype=np.uint64)
+    inputs = np.ascontiguousarray(inputs, dtype=np.uint64)
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    in_off = np.ascontiguousarray(in_off, dtype=np.uint64)
+    seed_off = np.ascontiguousarray(seed_off, dtype=np.uint64)
+    cnt = len(ns)
+    out = np.zeros(max(nwords(cnt * m), 1), dtype=np.uint64)
+    _check(lib.ssbh_toeplitz_hash_batch(cnt, m, _p64(ns), _p64(inputs), _p64(in_off),
+                                        _p64(seeds), _p64(seed_off), _p64(out)))
+    return out[: nwords(cnt * m)]
+
+
+def block_limit(n, p, eps, m) -> int:
+    out = np.zeros(1, dtype=np.uint64)
+    _check(lib.ssbh_block_limit(n, p, eps, m, _p64(out)))
+    return int(out[0])
+
+
+def binomial_tail_bound(n, L, p) -> float:
+    out = C.c_double(0)
+    _check(lib.ssbh_binomial_tail_bound(n, L, p, C.byref(out)))
+    return out.value
+
+
+def relative_entropy(x, p) -> float:
+    out = C.c_double(0)
+    _check(lib.ssbh_relative_entropy(x, p, C.byref(out)))
+    return out.value
+
+
+def abort_check(lengths, limit) -> bool:
+    a = np.ascontiguousarray(lengths, dtype=np.uint64)
+    return bool(lib.ssbh_abort_check(_p64(a) if len(a) else None, len(a), limit))
+
+
+def cycle_estimate(i, o, mp) -> int:
+    out = np.zeros(1, dtype=np.uint64)
+    _check(lib.ssbh_cycle_estimate(i, o, mp, _p64(out)))
+    return int(out[0])
+
+
+def make_params(n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0,
+                limit=0) -> ExtractParams:
+    p = ExtractParams()
+    p.n_rounds = n
+    p.n_subblocks = s
+    p.per_block_seed = 1 if per_block else 0
+    p.out_bits = k
+    p.samp_key[:] = [int(v) for v in key_of(samp)]
+    p.hash_key[:] = [int(v) for v in key_of(hsh)]
+    p.block_first = block_first
+    p.block_count = block_count
+    p.block_limit = limit
+    return p
+
+
+def extract(x, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0, limit=0):
+    """Host-buffer fused extraction (ssbh_extract). Returns (key words, n_j, stats)."""
+    params = make_params(n, s, k, samp, hsh, per_block, block_first, block_count, limit)
+    owned = block_count or s
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    key = np.zeros(max(nwords(owned * k), 1), dtype=np.uint64)
+    lens = np.zeros(owned, dtype=np.uint64)
+    st = ExtractStats()
+    _check(lib.ssbh_extract(C.byref(params), _p64(x), _p64(key), _p64(lens), C.byref(st)))
+    return key[: nwords(owned * k)], lens, st
+
+
+class Plan:
+    """Device plan (ssbh_plan_*): buffers sized once, reused across runs."""
+
+    def __init__(self, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0,
+                 limit=0):
+        self.params = make_params(n, s, k, samp, hsh, per_block, block_first, block_count,
+                                  limit)
+        self.owned = block_count or s
+        self.n, self.s, self.k = n, s, k
+        h = C.c_void_p()
+        _check(lib.ssbh_plan_create(C.byref(self.params), C.byref(h)))
+        self.h = h
+
+    @property
+    def device_bytes(self) -> int:
+        return int(lib.ssbh_plan_device_bytes(self.h))
+
+    def set_timing(self, on=True):
+        _check(lib.ssbh_plan_set_timing(self.h, 1 if on else 0))
+
+    def run_device(self, d_input_ptr: int, d_key_ptr: int, d_len_ptr: int = 0, stream: int = 0,
+                   samp=None, hsh=None):
+        sk = None if samp is None else _p64(key_of(samp))
+        hk = None if hsh is None else _p64(key_of(hsh))
+        _check(lib.ssbh_plan_run_device(self.h, C.c_void_p(d_input_ptr), C.c_void_p(d_key_ptr),
+                                        C.c_void_p(d_len_ptr or None), sk, hk,
+                                        C.c_void_p(stream or None)))
+
+    def check(self) -> ExtractStats:
+        st = ExtractStats()
+        _check(lib.ssbh_plan_check(self.h, C.byref(st)))
+        return st
+
+    def run_host(self, x_words, key_out=None, len_out=None):
+        x = np.ascontiguousarray(x_words, dtype=np.uint64)
+        key = key_out if key_out is not None else np.zeros(max(nwords(self.owned * self.k), 1),
+                                                           dtype=np.uint64)
+        lens = len_out if len_out is not None else np.zeros(self.owned, dtype=np.uint64)
+        st = ExtractStats()
+        _check(lib.ssbh_plan_run_host(self.h, _p64(x), _p64(key), _p64(lens), C.byref(st)))
+        return key, lens, st
+
+    def run_host_ptrs(self, x_ptr: int, key_ptr: int, len_ptr: int):
+        st = ExtractStats()
+        _check(lib.ssbh_plan_run_host(self.h, C.cast(x_ptr, U64P), C.cast(key_ptr, U64P),
+                                      C.cast(len_ptr, U64P) if len_ptr else None, C.byref(st)))
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ssbh_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_input_device(seed, p, nbits, d_out_ptr: int, stream: int = 0):
+    _check(lib.ssbh_make_input_device(_p64(key_of(seed)), float(p), nbits,
+                                      C.c_void_p(d_out_ptr), C.c_void_p(stream or None)))
+
+
+def measure_lop3_peak(iters: int = 20000):
+    """Measured LOP3 lane-ops/s of the current device (int-ALU roofline denominator)."""
+    r, ms = C.c_double(0), C.c_double(0)
+    _check(lib.ssbh_measure_lop3_peak(iters, C.byref(r), C.byref(ms)))
+    return r.value, ms.value
+
+
+# BASELINE.json configs (seeds per SURVEY §8a / Appendix A4)
+CONFIGS = {
+    1: dict(n=1 << 20, s=64, k=8192, p=0.5, seed_in=1, seed_samp=2, seed_hash=3, per_block=False),
+    2: dict(n=1 << 24, s=256, k=32768, p=0.3, seed_in=11, seed_samp=2, seed_hash=3,
+            per_block=False),
+    3: dict(n=1 << 30, s=1024, k=1 << 19, p=0.5, seed_in=1, seed_samp=2, seed_hash=3,
+            per_block=False),
+    4: dict(n=1 << 34, s=16384, k=3 << 18, p=0.4, seed_in=1, seed_samp=2, seed_hash=3,
+            per_block=True),
+    5: dict(n=1 << 37, s=32768, k=1 << 21, p=0.5, seed_in=1, seed_samp=2, seed_hash=3,
+            per_block=False),
+}

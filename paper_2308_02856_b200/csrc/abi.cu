@@ -1,0 +1,762 @@
+// abi.cu — the C-ABI (include/ssbh_cuda.h): argument validation with the reference's error
+// semantics, device buffer management (ssbh_plan), and the launch sequence of the fused
+// sample -> seed -> hash -> concatenate path. All compute goes to the GPU; there is no
+// CPU fallback (without a device every compute entry point returns SSBH_NO_DEVICE).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ssbh_cuda.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace ssbh_impl;
+
+namespace {
+
+thread_local std::string g_err;
+
+ssbh_status fail(ssbh_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+ssbh_status ok() {
+    g_err.clear();
+    return SSBH_OK;
+}
+
+#define CU(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(SSBH_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),  \
+                        __FILE__, __LINE__);                                                \
+    } while (0)
+
+ssbh_status check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SSBH_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+    return SSBH_OK;
+}
+
+int usable_devices() {
+    static int cached = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        int good = 0;
+        for (int d = 0; d < n; ++d) {
+            cudaDeviceProp p;
+            if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++good;
+        }
+        cached = good;
+    });
+    return cached;
+}
+
+ssbh_status need_device() {
+    if (usable_devices() <= 0)
+        return fail(SSBH_NO_DEVICE,
+                    "no sm_100 CUDA device available: the B200 path has no CPU fallback");
+    return SSBH_OK;
+}
+
+#define NEED_DEVICE()                              \
+    do {                                           \
+        ssbh_status s_ = need_device();            \
+        if (s_ != SSBH_OK) return s_;              \
+    } while (0)
+
+// RAII device buffer
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    cudaError_t alloc(size_t b) {
+        release();
+        bytes = b ? b : 16;
+        return cudaMalloc(&p, bytes);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+uint64_t words64(uint64_t bits) { return (bits + 63) / 64; }
+
+}  // namespace
+
+// ======================================================================== runtime
+extern "C" int ssbh_abi_version(void) { return SSBH_ABI_VERSION; }
+extern "C" const char* ssbh_last_error(void) { return g_err.c_str(); }
+extern "C" int ssbh_device_count(void) { return usable_devices(); }
+extern "C" ssbh_status ssbh_set_device(int device) {
+    NEED_DEVICE();
+    if (device < 0 || device >= usable_devices())
+        return fail(SSBH_INVALID_ARGUMENT, "set_device: device %d out of range", device);
+    CU(cudaSetDevice(device));
+    return ok();
+}
+
+// ======================================================================== PRF
+extern "C" ssbh_status ssbh_prf_block(const uint64_t key[4], const uint64_t ctr[4],
+                                      uint64_t out[4]) {
+    uint64_t ks[5];
+    ssbh_dev::threefry_ks(key, ks);
+    const ssbh_dev::U64x4 r = ssbh_dev::threefry(ks, ctr[0], ctr[1], ctr[2], ctr[3]);
+    for (int i = 0; i < 4; ++i) out[i] = r.v[i];
+    return ok();
+}
+
+extern "C" uint64_t ssbh_prf_tag(const char* purpose, size_t len) {
+    return ssbh_dev::fnv1a(purpose, len);
+}
+
+extern "C" ssbh_status ssbh_stream_bits(const uint64_t key[4], uint64_t tag, uint64_t sub,
+                                        uint64_t nbits, uint64_t* out_words) {
+    if (nbits == 0) return ok();
+    NEED_DEVICE();
+    const uint64_t w64 = words64(nbits);
+    DBuf d;
+    CU(d.alloc(w64 * 8));
+    CU(cudaMemset(d.p, 0, w64 * 8));
+    launch_stream_bits(key, tag, sub, nbits, d.as<uint32_t>(), 0);
+    if (auto s = check_launch("stream_bits")) return s;
+    CU(cudaMemcpy(out_words, d.p, w64 * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_stream_words(const uint64_t key[4], uint64_t tag, uint64_t sub,
+                                         uint64_t first, uint64_t count, uint64_t* out) {
+    if (count == 0) return ok();
+    NEED_DEVICE();
+    DBuf d;
+    CU(d.alloc(count * 8));
+    launch_stream_words(key, tag, sub, first, count, d.as<uint64_t>(), 0);
+    if (auto s = check_launch("stream_words")) return s;
+    CU(cudaMemcpy(out, d.p, count * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_stream_uniform_below(const uint64_t key[4], uint64_t tag,
+                                                 uint64_t sub, uint64_t bound, uint64_t first,
+                                                 uint64_t count, uint64_t* out) {
+    if (bound == 0) return fail(SSBH_INVALID_ARGUMENT, "uniform_below: bound must be positive");
+    if (count == 0) return ok();
+    NEED_DEVICE();
+    DBuf d;
+    CU(d.alloc(count * 8));
+    launch_stream_uniform(key, tag, sub, bound, first, count, d.as<uint64_t>(), 0);
+    if (auto s = check_launch("stream_uniform")) return s;
+    CU(cudaMemcpy(out, d.p, count * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_stream_bernoulli(const uint64_t key[4], uint64_t tag, uint64_t sub,
+                                             double p, uint64_t first, uint64_t count,
+                                             uint64_t* out_words) {
+    if (p < 0.0 || p > 1.0) return fail(SSBH_INVALID_ARGUMENT, "bernoulli: p outside [0,1]");
+    if (count == 0) return ok();
+    NEED_DEVICE();
+    const uint64_t w64 = words64(count);
+    DBuf d;
+    CU(d.alloc(w64 * 8));
+    CU(cudaMemset(d.p, 0, w64 * 8));
+    launch_stream_bernoulli(key, tag, sub, p, first, count, d.as<uint32_t>(), 0);
+    if (auto s = check_launch("stream_bernoulli")) return s;
+    CU(cudaMemcpy(out_words, d.p, w64 * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbits,
+                                              uint32_t* d_out, void* stream) {
+    if (p < 0.0 || p > 1.0) return fail(SSBH_INVALID_ARGUMENT, "bernoulli: p outside [0,1]");
+    NEED_DEVICE();
+    launch_make_input(key, p, nbits, d_out, static_cast<cudaStream_t>(stream));
+    return check_launch("make_input");
+}
+
+// ======================================================================== host scalars
+// sampling.cpp:41-96 restated (host numerics, not data-parallel).
+static ssbh_status rel_entropy(double x, double p, double* out) {
+    if (!(p > 0.0 && p < 1.0))
+        return fail(SSBH_INVALID_ARGUMENT, "relative_entropy: p must lie in (0,1)");
+    if (!(x >= 0.0 && x <= 1.0))
+        return fail(SSBH_INVALID_ARGUMENT, "relative_entropy: x must lie in [0,1]");
+    if (x == 0.0)
+        *out = std::log(1.0 / (1.0 - p));
+    else if (x == 1.0)
+        *out = std::log(1.0 / p);
+    else
+        *out = x * std::log(x / p) + (1.0 - x) * std::log((1.0 - x) / (1.0 - p));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_relative_entropy(double x, double p, double* out) {
+    return rel_entropy(x, p, out);
+}
+
+extern "C" ssbh_status ssbh_binomial_tail_bound(uint64_t n, uint64_t limit, double p,
+                                                double* out) {
+    const double x = (double)limit / (double)n;
+    double h = 0;
+    if (auto s = rel_entropy(x, p, &h)) return s;
+    const double arg = std::sqrt(2.0 * (double)n * h);
+    *out = 0.5 * std::erfc(arg / std::sqrt(2.0));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_block_limit(uint64_t n, double p, double eps, uint64_t m_blocks,
+                                        uint64_t* limit) {
+    if (n == 0) return fail(SSBH_INVALID_ARGUMENT, "block_limit: n_rounds must be positive");
+    if (!(p > 0.0 && p < 1.0))
+        return fail(SSBH_INVALID_ARGUMENT, "block_limit: p_sift must lie in (0,1)");
+    if (!(eps > 0.0 && eps < 1.0))
+        return fail(SSBH_INVALID_ARGUMENT, "block_limit: eps_abort must lie in (0,1)");
+    if (m_blocks == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "block_limit: m_blocks must be positive");
+    const double threshold = eps / (double)m_blocks;
+    if (threshold < 1e-300)
+        return fail(SSBH_INFEASIBLE, "block_limit: per-block budget below erfc resolution");
+    auto tail = [&](uint64_t L) {
+        double v = 0;
+        ssbh_binomial_tail_bound(n, L, p, &v);
+        return v;
+    };
+    const uint64_t lo0 = (uint64_t)std::ceil((double)n * p);
+    if (tail(n) > threshold)
+        return fail(SSBH_INFEASIBLE, "block_limit: bound not met even at L = n_rounds");
+    if (tail(lo0) <= threshold) {
+        *limit = lo0;
+        return ok();
+    }
+    uint64_t lo = lo0, hi = n;
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (tail(mid) <= threshold)
+            hi = mid;
+        else
+            lo = mid;
+    }
+    *limit = hi;
+    return ok();
+}
+
+extern "C" int ssbh_abort_check(const uint64_t* lengths, uint64_t count, uint64_t limit) {
+    for (uint64_t i = 0; i < count; ++i)
+        if (lengths[i] > limit) return 0;
+    return 1;
+}
+
+extern "C" ssbh_status ssbh_cycle_estimate(uint64_t input_len, uint64_t output_len,
+                                           uint64_t m_prime, uint64_t* out) {
+    if (m_prime == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "cycle_estimate: m_prime must be positive");
+    const uint64_t passes = (output_len + m_prime - 1) / m_prime;
+    const unsigned __int128 total = (unsigned __int128)input_len + output_len +
+                                    (unsigned __int128)(input_len + m_prime) * passes;
+    if (total > (unsigned __int128)~0ull)
+        return fail(SSBH_OVERFLOW, "cycle_estimate: result exceeds 64 bits");
+    *out = (uint64_t)total;
+    return ok();
+}
+
+// ======================================================================== device layout
+namespace {
+
+struct LayoutBufs {
+    DBuf nj, yoff, ypad, ktl, items, soff, stats;
+    cudaError_t alloc(uint32_t nown) {
+        cudaError_t e;
+        if ((e = nj.alloc((size_t)nown * 8 + 8))) return e;
+        if ((e = yoff.alloc((size_t)(nown + 1) * 8))) return e;
+        if ((e = ypad.alloc((size_t)nown * 4 + 4))) return e;
+        if ((e = ktl.alloc((size_t)nown * 4 + 4))) return e;
+        if ((e = items.alloc((size_t)(nown + 1) * 8))) return e;
+        if ((e = soff.alloc((size_t)(nown + 1) * 8))) return e;
+        if ((e = stats.alloc(sizeof(DevStats)))) return e;
+        return cudaSuccess;
+    }
+    Layout view() const {
+        Layout l;
+        l.nj = nj.as<unsigned long long>();
+        l.yoff = yoff.as<unsigned long long>();
+        l.ypad = ypad.as<uint32_t>();
+        l.ktl = ktl.as<uint32_t>();
+        l.items = items.as<unsigned long long>();
+        l.soff = soff.as<unsigned long long>();
+        l.stats = stats.as<DevStats>();
+        return l;
+    }
+};
+
+// Choose the k-tile so that the persistent grid gets enough items (>= ~16 per CTA)
+// while keeping tiles long enough to amortise per-item overhead.
+uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid) {
+    const uint64_t yw = std::max<uint64_t>(1, (mean_nj + 31) / 32);
+    uint64_t kt = kHashKTMax;
+    const uint64_t want_items = (uint64_t)grid * 16;
+    while (kt > 256) {
+        const uint64_t items = (uint64_t)rowtiles * nown * ((yw + kt - 1) / kt);
+        if (items >= want_items) break;
+        kt /= 2;
+    }
+    return (uint32_t)std::max<uint64_t>(kHashR, kt / kHashR * kHashR);
+}
+
+}  // namespace
+
+// ======================================================================== plan
+struct ssbh_plan {
+    ssbh_extract_params p{};
+    int device = 0;
+    uint32_t nown = 0;
+    SamplerGeom geom{};
+    uint32_t kw = 0, rowtiles = 0, kt = 0;
+    bool direct_out = true;
+    int grid = 0;
+    uint64_t ybuf_words = 0, sbuf_words = 0, key_words32 = 0;
+    DBuf payload, counts, gsum, ybuf, sbuf, scratch;
+    LayoutBufs lay;
+    DevStats* h_stats = nullptr;
+    bool timing = false;
+    cudaEvent_t ev[6]{};
+    cudaStream_t last_stream = nullptr;
+    uint32_t launches_per_run = 0;
+    // host-path staging
+    DBuf d_input, d_key, d_len;
+    cudaStream_t own_stream = nullptr;
+    uint64_t bytes = 0;
+};
+
+static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown) {
+    if (!p) return fail(SSBH_INVALID_ARGUMENT, "extract: null params");
+    if (p->n_subblocks == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "assign_subblocks: n_subblocks must be positive");
+    if (p->out_bits == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    if (p->n_subblocks > (1u << 30))
+        return fail(SSBH_INVALID_ARGUMENT, "extract: n_subblocks above 2^30 unsupported");
+    const uint32_t cnt = p->block_count ? p->block_count : p->n_subblocks;
+    if ((uint64_t)p->block_first + cnt > p->n_subblocks)
+        return fail(SSBH_INVALID_ARGUMENT, "extract: owned block range exceeds n_subblocks");
+    if (p->n_rounds == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    *nown = cnt;
+    return SSBH_OK;
+}
+
+extern "C" ssbh_status ssbh_plan_create(const ssbh_extract_params* params, ssbh_plan** out) {
+    uint32_t nown = 0;
+    if (auto s = validate_params(params, &nown)) return s;
+    NEED_DEVICE();
+    auto* pl = new ssbh_plan();
+    pl->p = *params;
+    pl->nown = nown;
+    CU(cudaGetDevice(&pl->device));
+    const uint64_t n = params->n_rounds, k = params->out_bits;
+    pl->geom = make_sampler_geom(n, params->n_subblocks, params->block_first, nown, false);
+    pl->kw = (uint32_t)((k + 31) / 32);
+    pl->rowtiles = (pl->kw + kHashRowWords - 1) / kHashRowWords;
+    pl->direct_out = (k % 32) == 0;
+    pl->grid = hash_grid_size(pl->device);
+    pl->kt = choose_kt(n / params->n_subblocks, nown, pl->rowtiles, pl->grid);
+    // buffer bounds (n_j unknown on the host until the device has sampled):
+    // sum_j round_up(ceil(n_j/32), R) <= n/32 + nown*R
+    const uint64_t ybound = (n + 31) / 32 + (uint64_t)nown * kHashR + 8;
+    pl->ybuf_words = round_up(ybound, 8);
+    const uint64_t seed_fixed = (uint64_t)pl->rowtiles * kHashRowWords + 8;
+    if (params->per_block_seed)
+        pl->sbuf_words = round_up((uint64_t)nown * (seed_fixed + 8) + ybound + 64, 8);
+    else
+        pl->sbuf_words = round_up(seed_fixed + round_up((n + 31) / 32, kHashR) + 64, 8);
+    pl->key_words32 = ((uint64_t)nown * k + 31) / 32;
+
+    auto alloc = [&](DBuf& b, size_t bytes) -> cudaError_t {
+        pl->bytes += bytes;
+        return b.alloc(bytes);
+    };
+    cudaError_t e = cudaSuccess;
+    if (!e) e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
+    if (!e) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
+    if (!e) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
+    if (!e) e = alloc(pl->ybuf, pl->ybuf_words * 4);
+    if (!e) e = alloc(pl->sbuf, pl->sbuf_words * 4);
+    if (!e && !pl->direct_out) e = alloc(pl->scratch, (size_t)nown * pl->kw * 4);
+    if (!e) e = pl->lay.alloc(nown);
+    if (!e) e = cudaMallocHost(&pl->h_stats, sizeof(DevStats));
+    for (int i = 0; i < 6 && !e; ++i) e = cudaEventCreate(&pl->ev[i]);
+    if (e) {
+        ssbh_plan_destroy(pl);
+        return fail(SSBH_CUDA, "plan_create: device allocation failed: %s", cudaGetErrorString(e));
+    }
+    *out = pl;
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
+    if (!pl) return ok();
+    for (auto& e : pl->ev)
+        if (e) cudaEventDestroy(e);
+    if (pl->h_stats) cudaFreeHost(pl->h_stats);
+    if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
+    delete pl;
+    return ok();
+}
+
+extern "C" uint64_t ssbh_plan_device_bytes(const ssbh_plan* pl) { return pl ? pl->bytes : 0; }
+
+extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
+    if (!pl) return fail(SSBH_INVALID_ARGUMENT, "null plan");
+    pl->timing = enable != 0;
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_input,
+                                            uint32_t* d_key, uint64_t* d_lengths,
+                                            const uint64_t* samp_key, const uint64_t* hash_key,
+                                            void* stream) {
+    if (!pl || !d_input || !d_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run: null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl->last_stream = st;
+    const uint64_t* sk = samp_key ? samp_key : pl->p.samp_key;
+    const uint64_t* hk = hash_key ? hash_key : pl->p.hash_key;
+    const Layout lay = pl->lay.view();
+    uint32_t launches = 0;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
+    // pass 1-2: sample + count + scan + layout
+    CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
+    launch_sample_count(pl->geom, sk, d_input, nullptr, pl->payload.p, pl->counts.as<uint32_t>(),
+                        nullptr, st);
+    launch_scan(pl->geom, pl->counts.as<uint32_t>(), pl->gsum.as<unsigned long long>(), lay.nj,
+                st);
+    launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
+                  pl->p.block_limit, st);
+    launches += 5;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[1], st));
+    // pass 3: stable scatter into reversed packed blocks
+    CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
+    launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
+                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
+    launches += 1;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[2], st));
+    // seeds
+    launch_seeds(hk, lay, pl->nown, pl->p.block_first, pl->p.per_block_seed, pl->sbuf_words,
+                 pl->sbuf.as<uint32_t>(), st);
+    launches += 1;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[3], st));
+    // hash
+    uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
+    CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
+    HashArgs a{};
+    a.ybuf = pl->ybuf.as<uint32_t>();
+    a.sbuf = pl->sbuf.as<uint32_t>();
+    a.out = out;
+    a.out_stride = pl->direct_out ? pl->p.out_bits / 32 : pl->kw;
+    a.lay = lay;
+    a.nown = pl->nown;
+    a.kw = pl->kw;
+    a.rowtiles = pl->rowtiles;
+    a.per_block_seed = pl->p.per_block_seed;
+    launch_hash(a, pl->grid, st);
+    launches += 1;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[4], st));
+    if (!pl->direct_out) {
+        launch_concat(pl->scratch.as<uint32_t>(), pl->kw, pl->nown, pl->p.out_bits, d_key, st);
+        launches += 1;
+    }
+    if (d_lengths)
+        CU(cudaMemcpyAsync(d_lengths, lay.nj, (size_t)pl->nown * 8, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(pl->h_stats, lay.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, st));
+    if (pl->timing) CU(cudaEventRecord(pl->ev[5], st));
+    pl->launches_per_run = launches;
+    return check_launch("plan_run");
+}
+
+extern "C" ssbh_status ssbh_plan_check(ssbh_plan* pl, ssbh_extract_stats* stats) {
+    if (!pl) return fail(SSBH_INVALID_ARGUMENT, "null plan");
+    CU(cudaStreamSynchronize(pl->last_stream));
+    const DevStats& d = *pl->h_stats;
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->hash_word_ops = d.hash_word_ops;
+        stats->max_len = d.max_nj;
+        stats->min_len = d.min_nj;
+        stats->hash_launches = 1;
+        stats->launches = pl->launches_per_run;
+        if (pl->timing) {
+            float ms[5] = {0, 0, 0, 0, 0};
+            for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], pl->ev[i], pl->ev[i + 1]);
+            cudaEventElapsedTime(&ms[4], pl->ev[0], pl->ev[5]);
+            stats->ms_sample = ms[0];
+            stats->ms_scatter = ms[1];
+            stats->ms_seed = ms[2];
+            stats->ms_hash = ms[3];
+            stats->ms_total = ms[4];
+        }
+    }
+    if (d.flags & kFlagTooLong)
+        return fail(SSBH_INVALID_ARGUMENT,
+                    "extract: sub-block of >= 2^32 bits is beyond the device path");
+    if (d.flags & kFlagOversize)
+        return fail(SSBH_ABORT_OVERSIZE, "abort: oversize_block (some n_j > block_limit %llu)",
+                    (unsigned long long)pl->p.block_limit);
+    if (d.flags & kFlagEmpty)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_plan_run_host(ssbh_plan* pl, const uint64_t* input, uint64_t* out_key,
+                                          uint64_t* out_lengths, ssbh_extract_stats* stats) {
+    if (!pl || !input || !out_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run_host: null argument");
+    CU(cudaSetDevice(pl->device));
+    if (!pl->own_stream) CU(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
+    const uint64_t in_w64 = words64(pl->p.n_rounds);
+    const uint64_t key_w64 = words64((uint64_t)pl->nown * pl->p.out_bits);
+    if (!pl->d_input.p) {
+        CU(pl->d_input.alloc(in_w64 * 8 + 16));
+        CU(pl->d_key.alloc(key_w64 * 8 + 16));
+        CU(pl->d_len.alloc((size_t)pl->nown * 8 + 8));
+    }
+    cudaStream_t st = pl->own_stream;
+    CU(cudaMemcpyAsync(pl->d_input.p, input, in_w64 * 8, cudaMemcpyHostToDevice, st));
+    // the key buffer's last u32 of an odd word count must read as zero in the u64 view
+    if ((pl->key_words32 & 1) != 0) CU(cudaMemsetAsync(pl->d_key.p, 0, key_w64 * 8, st));
+    if (auto s = ssbh_plan_run_device(pl, pl->d_input.as<uint32_t>(), pl->d_key.as<uint32_t>(),
+                                      pl->d_len.as<uint64_t>(), nullptr, nullptr, st))
+        return s;
+    if (auto s = ssbh_plan_check(pl, stats)) return s;
+    CU(cudaMemcpyAsync(out_key, pl->d_key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));
+    if (out_lengths)
+        CU(cudaMemcpyAsync(out_lengths, pl->d_len.p, (size_t)pl->nown * 8, cudaMemcpyDeviceToHost,
+                           st));
+    CU(cudaStreamSynchronize(st));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_extract(const ssbh_extract_params* params, const uint64_t* input,
+                                    uint64_t* out_key, uint64_t* out_lengths,
+                                    ssbh_extract_stats* stats) {
+    ssbh_plan* pl = nullptr;
+    if (auto s = ssbh_plan_create(params, &pl)) return s;
+    const ssbh_status s = ssbh_plan_run_host(pl, input, out_key, out_lengths, stats);
+    std::string msg = g_err;
+    ssbh_plan_destroy(pl);
+    g_err = msg;
+    return s;
+}
+
+// ======================================================================== sampler API
+extern "C" ssbh_status ssbh_assign_subblocks(uint64_t n, uint32_t s, const uint64_t key[4],
+                                             uint32_t* assignment, uint64_t* raw_counts) {
+    if (s == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "assign_subblocks: n_subblocks must be positive");
+    if (n == 0) {
+        std::memset(raw_counts, 0, (size_t)s * 8);
+        return ok();
+    }
+    NEED_DEVICE();
+    const SamplerGeom g = make_sampler_geom(n, s, 0, s, false);
+    DBuf assign, counts, gsum, nj;
+    CU(assign.alloc((size_t)n * 4));
+    CU(counts.alloc((size_t)g.nchunks * s * 4));
+    CU(gsum.alloc((size_t)g.ngroups * s * 8));
+    CU(nj.alloc((size_t)s * 8));
+    CU(cudaMemset(counts.p, 0, counts.bytes));
+    launch_sample_count(g, key, nullptr, nullptr, nullptr, counts.as<uint32_t>(),
+                        assign.as<uint32_t>(), 0);
+    launch_scan(g, counts.as<uint32_t>(), gsum.as<unsigned long long>(),
+                nj.as<unsigned long long>(), 0);
+    if (auto st = check_launch("assign_subblocks")) return st;
+    CU(cudaMemcpy(assignment, assign.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(raw_counts, nj.p, (size_t)s * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+namespace ssbh_impl {
+void launch_payload_from_assignment(const SamplerGeom& g, const uint32_t* d_assign,
+                                    const uint8_t* d_keep, uint32_t* d_payload,
+                                    uint32_t* d_counts, uint32_t* d_bad, cudaStream_t st);
+void launch_csr_offsets(const unsigned long long* d_nj, uint32_t nown,
+                        unsigned long long* d_off, cudaStream_t st);
+}  // namespace ssbh_impl
+
+extern "C" ssbh_status ssbh_sift_partition(const uint8_t* keep, uint64_t n,
+                                           const uint32_t* assignment, uint32_t s,
+                                           uint64_t* offsets, uint64_t* indices,
+                                           uint64_t* max_len) {
+    if (s == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "sift_partition: n_subblocks must be positive");
+    if (n == 0) {
+        std::memset(offsets, 0, ((size_t)s + 1) * 8);
+        if (max_len) *max_len = 0;
+        return ok();
+    }
+    NEED_DEVICE();
+    const SamplerGeom g = make_sampler_geom(n, s, 0, s, true);
+    DBuf dassign, dkeep, payload, counts, gsum, nj, off, idx, bad;
+    CU(dassign.alloc((size_t)n * 4));
+    CU(cudaMemcpy(dassign.p, assignment, (size_t)n * 4, cudaMemcpyHostToDevice));
+    if (keep) {
+        CU(dkeep.alloc((size_t)n));
+        CU(cudaMemcpy(dkeep.p, keep, (size_t)n, cudaMemcpyHostToDevice));
+    }
+    CU(payload.alloc((size_t)n * 4));
+    CU(counts.alloc((size_t)g.nchunks * s * 4));
+    CU(gsum.alloc((size_t)g.ngroups * s * 8));
+    CU(nj.alloc((size_t)s * 8));
+    CU(off.alloc(((size_t)s + 1) * 8));
+    CU(idx.alloc((size_t)n * 8));
+    CU(bad.alloc(4));
+    CU(cudaMemset(counts.p, 0, counts.bytes));
+    CU(cudaMemset(bad.p, 0, 4));
+    launch_payload_from_assignment(g, dassign.as<uint32_t>(), keep ? dkeep.as<uint8_t>() : nullptr,
+                                   payload.as<uint32_t>(), counts.as<uint32_t>(),
+                                   bad.as<uint32_t>(), 0);
+    uint32_t hbad = 0;
+    CU(cudaMemcpy(&hbad, bad.p, 4, cudaMemcpyDeviceToHost));
+    if (hbad)
+        return fail(SSBH_INVALID_ARGUMENT,
+                    "sift_partition: assignment value outside [1, n_subblocks]");
+    launch_scan(g, counts.as<uint32_t>(), gsum.as<unsigned long long>(),
+                nj.as<unsigned long long>(), 0);
+    launch_csr_offsets(nj.as<unsigned long long>(), s, off.as<unsigned long long>(), 0);
+    launch_scatter(g, payload.p, counts.as<uint32_t>(), nj.as<unsigned long long>(), nullptr,
+                   nullptr, idx.as<unsigned long long>(), off.as<unsigned long long>(), 0);
+    if (auto st = check_launch("sift_partition")) return st;
+    CU(cudaMemcpy(offsets, off.p, ((size_t)s + 1) * 8, cudaMemcpyDeviceToHost));
+    const uint64_t kept = offsets[s];
+    if (kept) CU(cudaMemcpy(indices, idx.p, kept * 8, cudaMemcpyDeviceToHost));
+    if (max_len) {
+        uint64_t m = 0;
+        for (uint32_t j = 0; j < s; ++j) m = std::max<uint64_t>(m, offsets[j + 1] - offsets[j]);
+        *max_len = m;
+    }
+    return ok();
+}
+
+// ======================================================================== toeplitz API
+namespace ssbh_impl {
+void launch_pack_blocks(const uint64_t* d_seeds, const unsigned long long* d_seed_off,
+                        const uint64_t* d_inputs, const unsigned long long* d_in_off,
+                        const Layout& lay, uint32_t count, uint64_t m, uint32_t* d_sbuf,
+                        uint32_t* d_ybuf, cudaStream_t st);
+}
+
+extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, const uint64_t* n,
+                                                const uint64_t* inputs, const uint64_t* in_off,
+                                                const uint64_t* seeds, const uint64_t* seed_off,
+                                                uint64_t* out) {
+    if (m == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    for (uint64_t b = 0; b < count; ++b)
+        if (n[b] == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    if (count == 0) return ok();
+    if (count > (1u << 30)) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: batch too large");
+    NEED_DEVICE();
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    const uint32_t nown = (uint32_t)count;
+    const uint32_t kw = (uint32_t)((m + 31) / 32);
+    const uint32_t rowtiles = (kw + kHashRowWords - 1) / kHashRowWords;
+    uint64_t in_words = 0, seed_words = 0, sum_n = 0, ybound = 8, sbound = 8;
+    for (uint64_t b = 0; b < count; ++b) {
+        in_words = std::max<uint64_t>(in_words, in_off[b] + words64(n[b]));
+        seed_words = std::max<uint64_t>(seed_words, seed_off[b] + words64(m + n[b] - 1));
+        sum_n += n[b];
+        const uint64_t yp = round_up((n[b] + 31) / 32, kHashR);
+        ybound += yp;
+        sbound += round_up((uint64_t)rowtiles * kHashRowWords + 8 + yp, 8);
+    }
+    LayoutBufs lb;
+    DBuf din, dseeds, dinoff, dseedoff, ybuf, sbuf, scratch, key;
+    CU(lb.alloc(nown));
+    CU(din.alloc(in_words * 8));
+    CU(dseeds.alloc(seed_words * 8));
+    CU(dinoff.alloc(count * 8));
+    CU(dseedoff.alloc(count * 8));
+    CU(ybuf.alloc(ybound * 4));
+    CU(sbuf.alloc(sbound * 4));
+    CU(scratch.alloc((size_t)nown * kw * 4));
+    const uint64_t key_w64 = words64(count * m);
+    CU(key.alloc(key_w64 * 8));
+    CU(cudaMemcpy(din.p, inputs, in_words * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dseeds.p, seeds, seed_words * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dinoff.p, in_off, count * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dseedoff.p, seed_off, count * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(lb.nj.p, n, count * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemset(ybuf.p, 0, ybuf.bytes));
+    CU(cudaMemset(sbuf.p, 0, sbuf.bytes));
+    CU(cudaMemset(scratch.p, 0, scratch.bytes));
+    CU(cudaMemset(key.p, 0, key.bytes));
+    const Layout lay = lb.view();
+    const int grid = hash_grid_size(dev);
+    const uint32_t kt = choose_kt(sum_n / count, nown, rowtiles, grid);
+    launch_layout(lay, nown, m, rowtiles, kt, 1, 0, 0);
+    launch_pack_blocks(dseeds.as<uint64_t>(), dseedoff.as<unsigned long long>(),
+                       din.as<uint64_t>(), dinoff.as<unsigned long long>(), lay, nown, m,
+                       sbuf.as<uint32_t>(), ybuf.as<uint32_t>(), 0);
+    HashArgs a{};
+    a.ybuf = ybuf.as<uint32_t>();
+    a.sbuf = sbuf.as<uint32_t>();
+    a.out = scratch.as<uint32_t>();
+    a.out_stride = kw;
+    a.lay = lay;
+    a.nown = nown;
+    a.kw = kw;
+    a.rowtiles = rowtiles;
+    a.per_block_seed = 1;
+    launch_hash(a, grid, 0);
+    launch_concat(scratch.as<uint32_t>(), kw, nown, m, key.as<uint32_t>(), 0);
+    if (auto st = check_launch("toeplitz_hash")) return st;
+    CU(cudaMemcpy(out, key.p, key_w64 * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_toeplitz_hash(const uint64_t* seed, uint64_t m, uint64_t n,
+                                          const uint64_t* input, uint64_t input_bits,
+                                          uint64_t* out) {
+    // ToeplitzSeed ctor (toeplitz.cpp:9-15) then check_input (toeplitz.cpp:19-22)
+    if (m == 0 || n == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    if (input_bits != n)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: input length does not match seed.n");
+    const uint64_t zero = 0;
+    return ssbh_toeplitz_hash_batch(1, m, &n, input, &zero, seed, &zero, out);
+}
+
+extern "C" ssbh_status ssbh_blocked_toeplitz_hash(const uint64_t* seed, uint64_t m, uint64_t n,
+                                                  const uint64_t* input, uint64_t input_bits,
+                                                  uint64_t m_prime, uint64_t n_prime,
+                                                  uint64_t* out) {
+    if (m == 0 || n == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    if (input_bits != n)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: input length does not match seed.n");
+    if (m_prime == 0 || n_prime == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: blocking dimensions must be positive");
+    // toeplitz.hpp:29-32: bit-for-bit identical to toeplitz_hash for every blocking; the
+    // GPU tiling is our own (row tiles x k tiles), so the blocking is validated only.
+    return ssbh_toeplitz_hash(seed, m, n, input, input_bits, out);
+}

@@ -1,0 +1,116 @@
+// internal.h — device-side data structures and kernel launchers shared by the .cu files.
+// Not part of the public ABI (include/ssbh_cuda.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ssbh_impl {
+
+// Hash-kernel tile geometry (see toeplitz.cu): each warp owns R consecutive 32-row output
+// words, a CTA has kHashWarps compute warps + 1 producer warp, a k-tile covers <= KT_MAX
+// words of the reversed input.
+constexpr int kHashR = 32;
+constexpr int kHashWarps = 4;
+constexpr int kHashRowWords = kHashR * kHashWarps;  // output words per row tile
+constexpr int kHashKTMax = 2048;                    // max y words per item
+constexpr int kHashStages = 2;
+
+// Device-side run statistics / error flags written by the layout kernel.
+struct DevStats {
+    unsigned long long max_nj;
+    unsigned long long min_nj;
+    unsigned long long total_items;
+    unsigned long long seed_words;     // shared mode: words of the shared seed region
+    unsigned long long hash_word_ops;  // sum n_j * k / 32
+    unsigned long long sum_nj;
+    uint32_t flags;                    // kFlag*
+    uint32_t pad;
+};
+constexpr uint32_t kFlagEmpty = 1u;     // some owned n_j == 0
+constexpr uint32_t kFlagOversize = 2u;  // some owned n_j > block_limit
+constexpr uint32_t kFlagTooLong = 4u;   // some owned n_j >= 2^32 (device path limit)
+
+// Per-owned-block layout arrays (device).
+struct Layout {
+    unsigned long long* nj;    // [nown]   block lengths (bits)
+    unsigned long long* yoff;  // [nown+1] u32-word offsets of reversed inputs in ybuf
+    uint32_t* ypad;            // [nown]   padded y words (multiple of kHashR)
+    uint32_t* ktl;             // [nown]   k-tile length (words, multiple of kHashR)
+    unsigned long long* items; // [nown+1] hash work-item prefix
+    unsigned long long* soff;  // [nown+1] u32-word offsets of per-block seeds (0 if shared)
+    DevStats* stats;
+};
+
+struct HashArgs {
+    const uint32_t* ybuf;
+    const uint32_t* sbuf;
+    uint32_t* out;           // out[jj * out_stride + word]
+    unsigned long long out_stride;
+    Layout lay;
+    uint32_t nown;
+    uint32_t kw;             // output words per block (ceil(k/32))
+    uint32_t rowtiles;       // ceil(kw / kHashRowWords)
+    uint32_t per_block_seed;
+};
+
+// ---- prf / input -------------------------------------------------------------------
+void launch_stream_words(const uint64_t key[4], uint64_t tag, uint64_t sub, uint64_t first,
+                         uint64_t count, uint64_t* d_out, cudaStream_t st);
+void launch_stream_uniform(const uint64_t key[4], uint64_t tag, uint64_t sub, uint64_t bound,
+                           uint64_t first, uint64_t count, uint64_t* d_out, cudaStream_t st);
+void launch_stream_bernoulli(const uint64_t key[4], uint64_t tag, uint64_t sub, double p,
+                             uint64_t first, uint64_t count, uint32_t* d_out32, cudaStream_t st);
+// bits(nbits) of (key, tag, sub) as u32 words; tail masked.
+void launch_stream_bits(const uint64_t key[4], uint64_t tag, uint64_t sub, uint64_t nbits,
+                        uint32_t* d_out32, cudaStream_t st);
+void launch_make_input(const uint64_t key[4], double p, uint64_t nbits, uint32_t* d_out32,
+                       cudaStream_t st);
+
+// ---- sampler -----------------------------------------------------------------------
+struct SamplerGeom {
+    uint64_t n;
+    uint64_t s;
+    uint32_t j_lo, nown;
+    int chunk_shift;       // warp-chunk = 2^chunk_shift rounds
+    uint64_t nchunks;
+    uint64_t group_chunks; // chunks per scan group
+    uint64_t ngroups;
+    int payload_bytes;     // 2 (u16: V | bit<<15) or 4 (u32: V | keep<<30 | bit<<31)
+};
+SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,
+                              bool has_keep);
+// Pass 1: V_i (Threefry), payload, per-(chunk, owned block) counts (counts pre-zeroed).
+void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
+                         const uint8_t* d_keep, void* d_payload, uint32_t* d_counts,
+                         uint32_t* d_assign_out, cudaStream_t st);
+// Pass 2: exclusive scan of counts along chunks (in place -> offsets), nj totals.
+void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d_gsum,
+                 unsigned long long* d_nj, cudaStream_t st);
+// Pass 3: stable scatter. ybuf mode: reversed bit pack into ybuf (pre-zeroed);
+// index mode (d_idx_out != null): CSR indices at csr_off[jj] + rank.
+void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
+                    const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                    uint32_t* d_ybuf, unsigned long long* d_idx_out,
+                    const unsigned long long* d_csr_off, cudaStream_t st);
+
+// ---- layout / seeds / hash -----------------------------------------------------------
+// Computes ypad/ktl/yoff/items/soff/stats from lay.nj for nown blocks.
+void launch_layout(const Layout& lay, uint32_t nown, uint64_t k, uint32_t rowtiles,
+                   uint32_t kt_target, int per_block_seed, uint64_t block_limit,
+                   cudaStream_t st);
+// Seeds: shared -> stats.seed_words words of stream (hash,"hash-seed",0);
+// per-block -> each region soff[jj].. of stream sub = j_lo + jj.
+void launch_seeds(const uint64_t key[4], const Layout& lay, uint32_t nown, uint32_t j_lo,
+                  int per_block_seed, uint64_t max_words_hint, uint32_t* d_sbuf,
+                  cudaStream_t st);
+// y[c] = x[n-1-c] for one block: writes ypad words at d_y (zero padded).
+void launch_reverse(const uint32_t* d_x32, uint64_t nbits, uint32_t* d_y, uint64_t ywords,
+                    cudaStream_t st);
+int hash_grid_size(int device);
+void launch_hash(const HashArgs& a, int grid, cudaStream_t st);
+// Concatenate nown blocks of k bits (block stride kw words) into key (bit offset jj*k).
+void launch_concat(const uint32_t* d_blocks, uint32_t kw, uint32_t nown, uint64_t k,
+                   uint32_t* d_key, cudaStream_t st);
+
+}  // namespace ssbh_impl

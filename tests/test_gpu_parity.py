@@ -1,0 +1,293 @@
+"""GPU parity: the B200 path (through the C-ABI) vs the CPU oracle / golden vectors.
+
+Bit-exact for everything (integer/bit work). Mirrors the reference's own tests
+(proj/tests/test_{prf,toeplitz,sampling,bitstring,pipeline}.cpp) and extends them to the
+BASELINE configs. Every call below runs sm_100a kernels; there is no CPU fallback.
+"""
+import numpy as np
+import pytest
+
+from conftest import words
+
+pytestmark = pytest.mark.gpu
+U64 = np.uint64
+
+
+def bits_to_words(bits):
+    n = len(bits)
+    w = np.zeros(max((n + 63) // 64, 1), dtype=U64)
+    for i, b in enumerate(bits):
+        if b:
+            w[i // 64] |= U64(1) << U64(i % 64)
+    return w[: (n + 63) // 64]
+
+
+def get_bit(w, i):
+    return (int(w[i // 64]) >> (i % 64)) & 1
+
+
+# ---------------------------------------------------------------------------------- PRF
+def test_prf_block_and_kat(dev, golden):
+    for c in golden["prf_block"]:
+        assert (dev.prf_block(words(c["key"]), words(c["ctr"])) == words(c["out"])).all()
+    w = dev.stream_words([0, 0, 0, 0], "kat", 0, 0, 2)  # test_prf.cpp:88-94
+    assert int(w[0]) == 0xCAEE3B9563A0641A and int(w[1]) == 0x33477B8A6E8573EE
+    for t, h in golden["tags"].items():
+        assert dev.tag(t) == int(h, 16)
+
+
+def test_stream_bits_golden(dev, golden, oracle):
+    for c in golden["stream_bits"]:
+        got = dev.stream_bits(words(c["key"]), c["purpose"], c["sub"], c["nbits"])
+        assert (got == words(c["words"])).all()
+    for nb in (1, 31, 32, 33, 255, 256, 257, 100003):
+        assert (dev.stream_bits(3, "hash-seed", 5, nb) == oracle.bits(3, "hash-seed", 5, nb)).all()
+
+
+def test_stream_uniform_bernoulli(dev, golden, oracle):
+    for c in golden["uniform_below"]:
+        got = dev.stream_uniform_below(words(c["key"]), c["purpose"], c["sub"], c["bound"], 0,
+                                       len(c["values"]))
+        assert [int(v) for v in got] == c["values"]
+    got = dev.stream_uniform_below(9, "u", 2, 1000003, 1 << 40, 4096)
+    want = [oracle.uniform_below(9, "u", 2, 1000003, (1 << 40) + i) for i in range(4096)]
+    assert [int(v) for v in got] == want
+    for c in golden["bernoulli"]:
+        got = dev.stream_bernoulli(words(c["key"]), c["purpose"], 0, c["p"], 0, 256)
+        assert "".join(str(get_bit(got, i)) for i in range(256)) == c["bits"]
+    with pytest.raises(ValueError):
+        dev.stream_uniform_below(0, "u", 0, 0, 0, 4)
+    with pytest.raises(ValueError):
+        dev.stream_bernoulli(0, "b", 0, 1.5, 0, 4)
+
+
+def test_make_input_device(dev, oracle, golden):
+    import torch
+
+    for c in golden["extract"].values():
+        if c["n"] > (1 << 24):
+            continue
+        buf = torch.zeros(((c["n"] + 63) // 64) * 2, dtype=torch.int32, device="cuda")
+        dev.make_input_device(c["seed_in"], c["p"], c["n"], buf.data_ptr())
+        torch.cuda.synchronize()
+        x = buf.cpu().numpy().view(np.uint64)
+        assert f"{oracle.fnv(x):016x}" == c["input_fnv"]
+
+
+# ----------------------------------------------------------------------------- Toeplitz
+def test_toeplitz_worked_example(dev):
+    seed, x = bits_to_words([1, 0, 1, 1]), bits_to_words([1, 1, 0])
+    out = dev.toeplitz_hash(seed, 2, 3, x)
+    assert int(out[0]) == 1  # (1, 0), zero tail
+
+
+def test_toeplitz_identity_and_zero(dev, oracle):
+    assert int(dev.toeplitz_hash(bits_to_words([1]), 1, 1, bits_to_words([1]))[0]) == 1
+    rng = np.random.default_rng(3)
+    for m, n in ((1, 1), (5, 9), (64, 33)):
+        x = oracle.bits(int(rng.integers(1 << 60)), "x", 0, n)
+        out = dev.toeplitz_hash(np.zeros((m + n - 1 + 63) // 64, dtype=U64), m, n, x)
+        assert int(np.unpackbits(out.view(np.uint8)).sum()) == 0
+
+
+def test_toeplitz_golden(dev, golden):
+    for c in golden["toeplitz"]:
+        got = dev.toeplitz_hash(words(c["seed"]), c["m"], c["n"], words(c["x"]))
+        assert (got == words(c["out"])).all(), (c["m"], c["n"])
+
+
+def _batch_check(dev, oracle, m, cases):
+    """cases: list of (seed_words, n, x_words); one GPU batch vs oracle per case."""
+    ns, ins, ioff, sds, soff = [], [], [], [], []
+    pos_i = pos_s = 0
+    for seed, n, x in cases:
+        ns.append(n)
+        ioff.append(pos_i)
+        soff.append(pos_s)
+        ins.append(x)
+        sds.append(seed)
+        pos_i += len(x)
+        pos_s += len(seed)
+    got = dev.toeplitz_hash_batch(m, ns, np.concatenate(ins), ioff, np.concatenate(sds), soff)
+    bits = np.unpackbits(got.view(np.uint8), bitorder="little")
+    for q, (seed, n, x) in enumerate(cases):
+        want = np.unpackbits(oracle.dense_toeplitz(seed, m, n, x).view(np.uint8),
+                             bitorder="little")[:m] if m * n <= 4096 else np.unpackbits(
+            oracle.toeplitz_hash(seed, m, n, x).view(np.uint8), bitorder="little")[:m]
+        assert (bits[q * m:(q + 1) * m] == want).all(), (m, n, q)
+
+
+def test_toeplitz_exhaustive_m_n_le_6(dev, oracle):
+    # SPEC.md:524 acceptance bar (exhaustive m, n <= 6), beyond test_toeplitz.cpp:51-73
+    for m in range(1, 7):
+        for n in range(1, 7):
+            cases = []
+            for sv in range(1 << (m + n - 1)):
+                for xv in range(1 << n):
+                    cases.append((np.array([sv], dtype=U64), n, np.array([xv], dtype=U64)))
+            _batch_check(dev, oracle, m, cases)
+
+
+def test_toeplitz_randomized_1000(dev, oracle):
+    # 1000 randomized cases, m <= 64, n <= 128 (test_toeplitz.cpp:75-87)
+    rng = np.random.default_rng(17)
+    by_m = {}
+    for _ in range(1000):
+        m, n = int(rng.integers(1, 65)), int(rng.integers(1, 129))
+        seed = oracle.bits(int(rng.integers(1 << 62)), "s", 0, m + n - 1)
+        x = oracle.bits(int(rng.integers(1 << 62)), "x", 0, n)
+        by_m.setdefault(m, []).append((seed, n, x))
+    for m, cases in by_m.items():
+        _batch_check(dev, oracle, m, cases)
+
+
+def test_toeplitz_large_shapes(dev, oracle):
+    rng = np.random.default_rng(23)
+    shapes = [(6300, 100000), (8192, 16384), (32768, 65536), (4097, 3), (3, 70001),
+              (100, 200000), (65536, 4096), (12345, 54321)]
+    for m, n in shapes:
+        seed = oracle.bits(int(rng.integers(1 << 62)), "s", 0, m + n - 1)
+        x = oracle.bits(int(rng.integers(1 << 62)), "x", 0, n)
+        want = oracle.toeplitz_hash(seed, m, n, x)
+        assert (dev.toeplitz_hash(seed, m, n, x) == want).all(), (m, n)
+        # production blocking (test_toeplitz.cpp:97-103): bit-identical
+        assert (dev.blocked_toeplitz_hash(seed, m, n, x, 2000, 1) == want).all()
+
+
+def test_toeplitz_linearity_and_columns(dev, oracle):
+    rng = np.random.default_rng(29)
+    for _ in range(10):
+        m, n = int(rng.integers(1, 5000)), int(rng.integers(1, 9000))
+        seed = oracle.bits(int(rng.integers(1 << 62)), "s", 0, m + n - 1)
+        x = oracle.bits(int(rng.integers(1 << 62)), "x", 0, n)
+        y = oracle.bits(int(rng.integers(1 << 62)), "y", 0, n)
+        hx, hy = dev.toeplitz_hash(seed, m, n, x), dev.toeplitz_hash(seed, m, n, y)
+        assert (dev.toeplitz_hash(seed, m, n, x ^ y) == (hx ^ hy)).all()
+    m, n = 9, 13  # unit vectors read out columns (test_toeplitz.cpp:121-132)
+    seed = oracle.bits(31, "s", 0, m + n - 1)
+    for j in range(n):
+        e = np.zeros(1, dtype=U64)
+        e[0] = U64(1) << U64(j)
+        col = dev.toeplitz_hash(seed, m, n, e)
+        for i in range(m):
+            assert get_bit(col, i) == get_bit(seed, n - 1 + i - j)
+
+
+def test_toeplitz_dimension_errors(dev):
+    # test_toeplitz.cpp:134-140
+    with pytest.raises(ValueError):
+        dev.toeplitz_hash(np.zeros(1, dtype=U64), 3, 3, np.zeros(1, dtype=U64), input_bits=4)
+    with pytest.raises(ValueError):
+        dev.blocked_toeplitz_hash(np.zeros(1, dtype=U64), 3, 3, np.zeros(1, dtype=U64), 0, 1)
+    with pytest.raises(ValueError):
+        dev.toeplitz_hash(np.zeros(1, dtype=U64), 0, 3, np.zeros(1, dtype=U64))
+
+
+# ------------------------------------------------------------------------------ sampler
+def test_assign_subblocks(dev, oracle, golden):
+    for c in golden["assign_subblocks"]:
+        a, cnt = dev.assign_subblocks(c["n"], c["s"], c["seed"])
+        assert [int(v) for v in a[:32]] == c["assign_head"]
+        assert f"{oracle.fnv(a.astype(U64)):016x}" == c["assign_fnv"]
+        assert f"{oracle.fnv(cnt):016x}" == c["raw_counts_fnv"]
+    for n, s in ((1 << 20, 1024), (123457, 17), (1, 1), (33, 3), (5000, 7)):
+        a, cnt = dev.assign_subblocks(n, s, 2)
+        ea, ec = oracle.assign_subblocks(n, s, 2)
+        assert (a == ea).all() and (cnt == ec).all()
+    with pytest.raises(ValueError):
+        dev.assign_subblocks(10, 0, 0)
+
+
+def test_sift_partition(dev, oracle):
+    rng = np.random.default_rng(5)
+    for n, s in ((10000, 4), (64, 4), (1 << 18, 1000), (77777, 33), (100, 1)):
+        a, _ = oracle.assign_subblocks(n, s, 0)
+        for keep in (np.ones(n, np.uint8), np.zeros(n, np.uint8),
+                     rng.integers(0, 2, n).astype(np.uint8)):
+            off, idx, ml = dev.sift_partition(keep, a, s)
+            eoff, eidx = oracle.sift_partition(keep, a, s)
+            assert (off == eoff).all() and (idx == eidx).all()
+            assert ml == (int(np.diff(eoff).max()) if s else 0)
+    a, _ = oracle.assign_subblocks(8, 2, 0)
+    with pytest.raises(ValueError):
+        dev.sift_partition(np.ones(7, np.uint8), a, 2)
+
+
+# ---------------------------------------------------------------------------- fused path
+@pytest.mark.parametrize("name", ["1", "2", "small_perblock", "small_k_odd", "small_k_32"])
+def test_extract_golden(dev, oracle, golden, name):
+    c = golden["extract"][name]
+    x = oracle.make_input(c["seed_in"], c["p"], c["n"])
+    key, nj, st = dev.extract(x, c["n"], c["s"], c["k"], c["seed_samp"], c["seed_hash"],
+                              per_block=bool(c["per_block"]))
+    assert f"{oracle.fnv(nj):016x}" == c["nj_fnv"]
+    assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
+    assert int(st.max_len) == c["nj_max"] and int(st.min_len) == c["nj_min"]
+    assert int(st.hash_word_ops) == c["n"] * c["k"] // 32
+
+
+def test_extract_random_vs_oracle(dev, oracle):
+    rng = np.random.default_rng(11)
+    for _ in range(12):
+        n = int(rng.integers(1000, 300000))
+        s = int(rng.choice([1, 2, 3, 8, 16, 50, 64, 100]))
+        k = int(rng.choice([1, 31, 32, 33, 64, 100, 512, 1024, 3000]))
+        pb = bool(rng.integers(0, 2))
+        x = oracle.make_input(int(rng.integers(100)), float(rng.choice([0.5, 0.1, 0.9])), n)
+        key, nj = oracle.extract(x, n, s, 21, 22, pb, k)
+        gkey, gnj, _ = dev.extract(x, n, s, k, 21, 22, per_block=pb)
+        assert (gnj == nj).all()
+        assert (gkey == key).all(), (n, s, k, pb)
+
+
+def test_extract_block_ranges_concatenate(dev, oracle):
+    # multi-GPU sharding: owned block ranges concatenate to the full key (k % 64 == 0)
+    n, s, k = 400000, 64, 1024
+    x = oracle.make_input(3, 0.5, n)
+    full, nj, _ = dev.extract(x, n, s, k, 2, 3)
+    parts, lens = [], []
+    for first, cnt in ((0, 16), (16, 16), (32, 20), (52, 12)):
+        kk, ll, _ = dev.extract(x, n, s, k, 2, 3, block_first=first, block_count=cnt)
+        parts.append(kk)
+        lens.append(ll)
+    assert (np.concatenate(parts) == full).all()
+    assert (np.concatenate(lens) == nj).all()
+
+
+def test_extract_empty_block_and_abort(dev, oracle):
+    x = oracle.make_input(1, 0.5, 64)
+    # 64 rounds into 1000 blocks: empty sub-blocks -> ToeplitzSeed throws (toeplitz.cpp:11-12)
+    with pytest.raises(ValueError):
+        dev.extract(x, 64, 1000, 8, 2, 3)
+    # strict abort (sampling.cpp:92-96): limit below max n_j -> oversize abort
+    x = oracle.make_input(1, 0.5, 100000)
+    _, nj, _ = dev.extract(x, 100000, 8, 64, 2, 3)
+    with pytest.raises(dev.AbortOversize):
+        dev.extract(x, 100000, 8, 64, 2, 3, limit=int(nj.max()) - 1)
+    key, _, _ = dev.extract(x, 100000, 8, 64, 2, 3, limit=int(nj.max()))
+    assert len(key) == 8
+
+
+def test_plan_reuse_and_device_path(dev, oracle, golden):
+    import torch
+
+    c = golden["extract"]["1"]
+    n, s, k = c["n"], c["s"], c["k"]
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"])
+    d_in = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+        plan.check()
+        key = d_key.cpu().numpy().view(np.uint64)
+        assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
+    # other seeds through the same plan
+    plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr(), samp=5, hsh=6)
+    plan.check()
+    x = d_in.cpu().numpy().view(np.uint64)
+    ekey, enj = oracle.extract(x, n, s, 5, 6, 0, k)
+    assert (d_key.cpu().numpy().view(np.uint64) == ekey).all()
+    assert (d_len.cpu().numpy().view(np.uint64) == enj).all()
+    plan.close()
