@@ -291,3 +291,34 @@ def test_plan_reuse_and_device_path(dev, oracle, golden):
     assert (d_key.cpu().numpy().view(np.uint64) == ekey).all()
     assert (d_len.cpu().numpy().view(np.uint64) == enj).all()
     plan.close()
+
+
+# ----------------------------------------------------------------- BASELINE full sizes
+# SURVEY §8a anchors (computed with the compiled reference); tests/golden/gen_golden.py
+# --config3 re-derives config 3 from the reference into golden.json.
+SURVEY_C3 = {"key_fnv": "ea34efc57d4887a3", "nj_min": 1045673, "nj_max": 1052053,
+             "nj_0": 1047749, "key_popcount": 268442266}
+
+
+@pytest.mark.slow
+def test_config3_full_key_digest(dev, oracle, golden):
+    import torch
+
+    c = dev.CONFIGS[3]
+    want = golden["extract"].get("3", SURVEY_C3)
+    n, s, k = c["n"], c["s"], c["k"]
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"])
+    d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+    plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+    st = plan.check()
+    key = d_key.cpu().numpy().view(np.uint64)
+    nj = d_len.cpu().numpy().view(np.uint64)
+    assert int(nj.min()) == want["nj_min"] and int(nj.max()) == want["nj_max"]
+    assert int(nj[0]) == want["nj_0"] and int(nj.sum()) == n
+    assert int(np.unpackbits(key.view(np.uint8)).sum()) == want["key_popcount"]
+    assert f"{oracle.fnv(key):016x}" == want["key_fnv"]
+    assert int(st.hash_word_ops) == n * k // 32
+    plan.close()
