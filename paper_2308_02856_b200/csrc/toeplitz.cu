@@ -21,6 +21,7 @@
 // the device (k_layout) and walked by a persistent grid, so no host sync is needed
 // between sampling and hashing.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -169,38 +170,54 @@ __global__ void __launch_bounds__(kLayoutThreads) k_layout(Layout lay, uint32_t 
 
 // ------------------------------------------------------------------------------------
 // Seeds: KeyedStream(hash, "hash-seed", sub).bits(...) (prf.cpp:104-115), u64 word w =
-// block({tag, sub, w/4, 1})[w%4] -> u32 words 8f..8f+7 of quad f. Whole regions are
-// filled with stream bits (prefix-stable: the first k+n_j-1 bits equal what the
-// reference builds; the rest only meet zero y bits).
+// block({tag, sub, w/4, 1})[w%4]. Whole regions are filled with stream bits (prefix-
+// stable: the first k+n_j-1 bits equal what the reference builds; the rest only meet zero
+// y bits). The buffer holds the seed PRE-SHIFTED by one bit, S'[b] = S[b-1] (S'[0] = 0):
+// the hash kernel then forms lane l's window with shift amount l+1 in [1, 32], i.e. with
+// the multiplier 2^(31-l) on the FMA pipe (see hash_tile).
+// Quad f (u32 words 8f..8f+7 of S') needs the top bit of stream block f-1: taken from the
+// neighbour lane by shuffle, recomputed by lane 0.
 // ------------------------------------------------------------------------------------
+__device__ __forceinline__ void write_shifted_quad(uint32_t* dst, const U64x4& r,
+                                                   uint32_t carry_in) {
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) w[e] = (uint32_t)(r.v[e >> 1] >> ((e & 1) * 32));
+    uint32_t o[8];
+    o[0] = (w[0] << 1) | carry_in;
+#pragma unroll
+    for (int e = 1; e < 8; ++e) o[e] = (w[e] << 1) | (w[e - 1] >> 31);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+__device__ __forceinline__ void seed_region(const Key& key, uint64_t sub, uint64_t nquads,
+                                            uint32_t* dst, uint64_t f0, uint64_t stride) {
+    const uint32_t lane = threadIdx.x & 31;
+    // all lanes of a warp walk the same trip count so the shuffle stays converged
+    for (uint64_t fb = f0 - lane; fb < nquads; fb += stride) {
+        const uint64_t f = fb + lane;
+        U64x4 r = {};
+        if (f < nquads) r = threefry(key.ks, kTagHashSeed, sub, f, 1);
+        uint32_t carry = __shfl_up_sync(0xffffffffu, (uint32_t)(r.v[3] >> 63), 1);
+        if (lane == 0) carry = f > 0 ? (uint32_t)(threefry(key.ks, kTagHashSeed, sub, f - 1, 1).v[3] >> 63) : 0u;
+        if (f < nquads) write_shifted_quad(dst + f * 8, r, carry);
+    }
+}
+
 __global__ void k_seeds_shared(Key key, const DevStats* __restrict__ st, uint32_t* sbuf) {
     const uint64_t nquads = st->seed_words / 8;
-    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nquads;
-         f += (uint64_t)gridDim.x * blockDim.x) {
-        const U64x4 r = threefry(key.ks, kTagHashSeed, 0, f, 1);
-        uint4* o = reinterpret_cast<uint4*>(sbuf + f * 8);
-        o[0] = make_uint4((uint32_t)r.v[0], (uint32_t)(r.v[0] >> 32), (uint32_t)r.v[1],
-                          (uint32_t)(r.v[1] >> 32));
-        o[1] = make_uint4((uint32_t)r.v[2], (uint32_t)(r.v[2] >> 32), (uint32_t)r.v[3],
-                          (uint32_t)(r.v[3] >> 32));
-    }
+    seed_region(key, 0, nquads, sbuf, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x,
+                (uint64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void k_seeds_per_block(Key key, const unsigned long long* __restrict__ soff,
                                   uint32_t j_lo, uint32_t* sbuf) {
     const uint32_t jj = blockIdx.y;
     const uint64_t w0 = soff[jj];
-    const uint64_t nquads = (soff[jj + 1] - w0) / 8;
-    const uint64_t sub = (uint64_t)j_lo + jj;
-    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nquads;
-         f += (uint64_t)gridDim.x * blockDim.x) {
-        const U64x4 r = threefry(key.ks, kTagHashSeed, sub, f, 1);
-        uint4* o = reinterpret_cast<uint4*>(sbuf + w0 + f * 8);
-        o[0] = make_uint4((uint32_t)r.v[0], (uint32_t)(r.v[0] >> 32), (uint32_t)r.v[1],
-                          (uint32_t)(r.v[1] >> 32));
-        o[1] = make_uint4((uint32_t)r.v[2], (uint32_t)(r.v[2] >> 32), (uint32_t)r.v[3],
-                          (uint32_t)(r.v[3] >> 32));
-    }
+    seed_region(key, (uint64_t)j_lo + jj, (soff[jj + 1] - w0) / 8, sbuf + w0,
+                blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
 }
 
 // ------------------------------------------------------------------------------------
@@ -244,12 +261,18 @@ __global__ void k_pack_blocks(const uint64_t* __restrict__ seeds,
     const uint64_t sbits = m + n - 1;
     const uint32_t* s32 = reinterpret_cast<const uint32_t*>(seeds + seed_off[jj]);
     uint32_t* dst = sbuf + lay.soff[jj];
+    // pre-shifted by one bit (S'[b] = S[b-1]), see the seed kernels
     const uint64_t sw = (sbits + 31) / 32;
-    for (uint64_t w = threadIdx.x; w < sw; w += blockDim.x) {
+    auto seed_word = [&](uint64_t w) {
         uint32_t v = s32[w];
         const uint64_t lo = w * 32;
         if (lo + 32 > sbits) v &= (1u << (uint32_t)(sbits - lo)) - 1u;
-        dst[w] = v;
+        return v;
+    };
+    for (uint64_t w = threadIdx.x; w <= sw; w += blockDim.x) {
+        const uint32_t cur = w < sw ? seed_word(w) : 0u;
+        const uint32_t prev = w ? seed_word(w - 1) : 0u;
+        dst[w] = (cur << 1) | (prev >> 31);
     }
     const uint32_t* x32 = reinterpret_cast<const uint32_t*>(inputs + in_off[jj]);
     uint32_t* y = ybuf + lay.yoff[jj];
@@ -272,12 +295,36 @@ constexpr int kStageWords = kHashKTMax + kSTileWords;
 constexpr size_t kHashSmem =
     (size_t)kHashStages * kStageWords * 4 + kHashStages * (sizeof(ItemDesc) + 16) + 64;
 
+// Lane l's 32-bit seed window starting at bit 32t + l, from the pre-shifted seed S':
+// funnelshift(S'[t], S'[t+1], l+1) = umulhi(S'[t], m) + S'[t+1] * m with m = 2^(31-l)
+// (the two products occupy disjoint bit ranges). Two IMADs on the otherwise idle FMA pipe
+// replace one SHF on the ALU pipe, which is left to the algorithmic LOP3s alone.
+// kWin selects how the window is formed (both read the pre-shifted seed S'):
+//   0: SHF  — __funnelshift_rc(S'[t], S'[t+1], l+1)  (one ALU-pipe instruction)
+//   1: IMAD — umulhi(S'[t], m) + S'[t+1]*m, m = 2^(31-l) (two FMA-pipe instructions)
+template <int kWin>
+__device__ __forceinline__ uint32_t window(uint32_t a, uint32_t b, uint32_t m) {
+    if constexpr (kWin == 0)
+        return __funnelshift_rc(a, b, m);
+    else
+        return __umulhi(a, m) + b * m;
+}
+
+// 2^(31-l) per lane, read from memory so ptxas cannot strength-reduce b * m back into an
+// ALU shift.
+__constant__ uint32_t c_lane_mult[32] = {
+    1u << 31, 1u << 30, 1u << 29, 1u << 28, 1u << 27, 1u << 26, 1u << 25, 1u << 24,
+    1u << 23, 1u << 22, 1u << 21, 1u << 20, 1u << 19, 1u << 18, 1u << 17, 1u << 16,
+    1u << 15, 1u << 14, 1u << 13, 1u << 12, 1u << 11, 1u << 10, 1u << 9,  1u << 8,
+    1u << 7,  1u << 6,  1u << 5,  1u << 4,  1u << 3,  1u << 2,  1u << 1,  1u << 0};
+
+template <int kWin>
 __device__ __forceinline__ void hash_tile(const uint32_t* __restrict__ Ys,
                                           const uint32_t* __restrict__ Sw, int L,
-                                          uint32_t lane, uint32_t (&acc)[R]) {
+                                          uint32_t m, uint32_t (&acc)[R]) {
     uint32_t win[R];
 #pragma unroll
-    for (int t = 0; t < R; ++t) win[t] = __funnelshift_r(Sw[t], Sw[t + 1], lane);
+    for (int t = 0; t < R; ++t) win[t] = window<kWin>(Sw[t], Sw[t + 1], m);
 #pragma unroll 1
     for (int T = 0; T < L; T += R) {
         const uint32_t* sb = Sw + T + R;
@@ -294,7 +341,7 @@ __device__ __forceinline__ void hash_tile(const uint32_t* __restrict__ Ys,
                 const int q = 4 * g + e;
 #pragma unroll
                 for (int r = 0; r < R; ++r) acc[r] ^= win[(q + r) % R] & yv[e];
-                win[q] = __funnelshift_r(sv[e], sv[e + 1], lane);
+                win[q] = window<kWin>(sv[e], sv[e + 1], m);
             }
         }
     }
@@ -323,6 +370,7 @@ __device__ __forceinline__ bool decode_item(const HashArgs& a, unsigned long lon
     return true;
 }
 
+template <int kWin>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint32_t* stage_base = reinterpret_cast<uint32_t*>(smem_raw);
@@ -374,6 +422,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) 
     }
 
     // -------------------- compute warps --------------------------------------------------
+    // per-lane window parameter: shift l+1 (SHF) or multiplier 2^(31-l) (IMAD)
+    const uint32_t lane_mult = kWin == 0 ? lane + 1 : c_lane_mult[lane];
     for (uint32_t it = 0;; ++it) {
         const int s = it % kHashStages;
         mbar_wait(&full[s], (it / kHashStages) & 1);
@@ -384,18 +434,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) 
         uint32_t acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0;
-        hash_tile(Ys, Ss + warp * R, (int)d.L, lane, acc);
+        hash_tile<kWin>(Ys, Ss + warp * R, (int)d.L, lane_mult, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // stage may be refilled
-        uint32_t mine = 0;
+        // lane r%32 collects output word r (R/32 words per lane, R a multiple of 32)
+        static_assert(R % 32 == 0, "R must be a multiple of 32");
+        uint32_t mine[R / 32];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t b = __ballot_sync(0xffffffffu, __popc(acc[r]) & 1u);
-            if (lane == (uint32_t)r) mine = b;
+            if (lane == (uint32_t)(r % 32)) mine[r / 32] = b;
         }
-        const uint32_t word = d.b0 + warp * R + lane;
-        if (lane < (uint32_t)R && word < a.kw)
-            atomicXor(a.out + (unsigned long long)d.jj * a.out_stride + word, mine);
+#pragma unroll
+        for (int q = 0; q < R / 32; ++q) {
+            const uint32_t word = d.b0 + warp * R + q * 32 + lane;
+            if (word < a.kw)
+                atomicXor(a.out + (unsigned long long)d.jj * a.out_stride + word, mine[q]);
+        }
     }
 }
 
@@ -467,25 +522,46 @@ void launch_reverse(const uint32_t* d_x32, uint64_t nbits, uint32_t* d_y, uint64
     k_reverse<<<(unsigned)blocks, 256, 0, st>>>(d_x32, nbits, d_y, ywords);
 }
 
-int hash_grid_size(int device) {
-    static int cached[64] = {0};
-    if (device >= 0 && device < 64 && cached[device]) return cached[device];
-    cudaFuncSetAttribute(k_toeplitz_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
+int hash_window_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = std::getenv("SSBH_HASH_WIN");  // dev switch for A/B measurements
+        mode = (e && *e == '1') ? 1 : 0;
+    }
+    return mode;
+}
+
+template <int kWin>
+int hash_grid_size_t(int device) {
+    cudaFuncSetAttribute(k_toeplitz_hash<kWin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHashSmem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_toeplitz_hash, (NW + 1) * 32,
-                                                  kHashSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_toeplitz_hash<kWin>,
+                                                  (NW + 1) * 32, kHashSmem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const int g = std::max(1, per_sm) * sms;
-    if (device >= 0 && device < 64) cached[device] = g;
+    return std::max(1, per_sm) * sms;
+}
+
+int hash_grid_size(int device) {
+    static int cached[2][64] = {};
+    const int w = hash_window_mode();
+    if (device >= 0 && device < 64 && cached[w][device]) return cached[w][device];
+    const int g = w ? hash_grid_size_t<1>(device) : hash_grid_size_t<0>(device);
+    if (device >= 0 && device < 64) cached[w][device] = g;
     return g;
 }
 
 void launch_hash(const HashArgs& a, int grid, cudaStream_t st) {
-    cudaFuncSetAttribute(k_toeplitz_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kHashSmem);
-    k_toeplitz_hash<<<grid, (NW + 1) * 32, kHashSmem, st>>>(a);
+    if (hash_window_mode() == 1) {
+        cudaFuncSetAttribute(k_toeplitz_hash<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kHashSmem);
+        k_toeplitz_hash<1><<<grid, (NW + 1) * 32, kHashSmem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_toeplitz_hash<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kHashSmem);
+        k_toeplitz_hash<0><<<grid, (NW + 1) * 32, kHashSmem, st>>>(a);
+    }
 }
 
 void launch_concat(const uint32_t* d_blocks, uint32_t kw, uint32_t nown, uint64_t k,
