@@ -237,7 +237,7 @@ def main():
     plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"],
                   block_first=first, block_count=count)
     plan.set_timing(True)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a capturable stream: the plan replays one CUDA graph per step
     d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
     P.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr(), stream.cuda_stream)
     key_words64 = (count * k + 63) // 64
@@ -264,7 +264,8 @@ def main():
           for _ in range(args.steps)]
     hash_ms, hash_ops, stats = [], 0, None
     for i in range(args.steps):
-        flush.fill_(i & 0xFF)  # evict L2 between steps (outside the step events)
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xFF)  # evict L2 between steps (outside the step events)
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)

@@ -3,6 +3,7 @@
 // sample -> seed -> hash -> concatenate path. All compute goes to the GPU; there is no
 // CPU fallback (without a device every compute entry point returns SSBH_NO_DEVICE).
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -320,7 +321,7 @@ uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid)
     const uint64_t yw = std::max<uint64_t>(1, (mean_nj + 31) / 32);
     uint64_t kt = kHashKTMax;
     const uint64_t want_items = (uint64_t)grid * 16;
-    while (kt > 256) {
+    while (kt > 64) {
         const uint64_t items = (uint64_t)rowtiles * nown * ((yw + kt - 1) / kt);
         if (items >= want_items) break;
         kt /= 2;
@@ -347,6 +348,15 @@ struct ssbh_plan {
     cudaEvent_t ev[6]{};
     cudaStream_t last_stream = nullptr;
     uint32_t launches_per_run = 0;
+    // CUDA graph of one run (captured per stream / buffers / seeds; replayed afterwards)
+    cudaGraphExec_t exec = nullptr;
+    struct GraphKey {
+        cudaStream_t st;
+        const void *in, *key, *len;
+        uint64_t sk[4], hk[4];
+        bool timing;
+        bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
+    } gkey{};
     // host-path staging
     DBuf d_input, d_key, d_len;
     cudaStream_t own_stream = nullptr;
@@ -424,6 +434,7 @@ extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
         if (e) cudaEventDestroy(e);
     if (pl->h_stats) cudaFreeHost(pl->h_stats);
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
+    if (pl->exec) cudaGraphExecDestroy(pl->exec);
     delete pl;
     return ok();
 }
@@ -436,15 +447,10 @@ extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
     return ok();
 }
 
-extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_input,
-                                            uint32_t* d_key, uint64_t* d_lengths,
-                                            const uint64_t* samp_key, const uint64_t* hash_key,
-                                            void* stream) {
-    if (!pl || !d_input || !d_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run: null argument");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    pl->last_stream = st;
-    const uint64_t* sk = samp_key ? samp_key : pl->p.samp_key;
-    const uint64_t* hk = hash_key ? hash_key : pl->p.hash_key;
+// Enqueue one fused run on `st` (directly, or into a graph being captured).
+static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, uint32_t* d_key,
+                                uint64_t* d_lengths, const uint64_t* sk, const uint64_t* hk,
+                                cudaStream_t st) {
     const Layout lay = pl->lay.view();
     uint32_t launches = 0;
     if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
@@ -495,6 +501,62 @@ extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_inp
     if (pl->timing) CU(cudaEventRecord(pl->ev[5], st));
     pl->launches_per_run = launches;
     return check_launch("plan_run");
+}
+
+static bool graphs_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("SSBH_NO_GRAPH");
+        on = (e && *e == '1') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_input,
+                                            uint32_t* d_key, uint64_t* d_lengths,
+                                            const uint64_t* samp_key, const uint64_t* hash_key,
+                                            void* stream) {
+    if (!pl || !d_input || !d_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run: null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl->last_stream = st;
+    const uint64_t* sk = samp_key ? samp_key : pl->p.samp_key;
+    const uint64_t* hk = hash_key ? hash_key : pl->p.hash_key;
+    // The legacy default stream cannot be captured, and per-phase event timing is only
+    // meaningful on direct launches: launch directly in those cases.
+    if (st == nullptr || pl->timing || !graphs_enabled())
+        return plan_enqueue(pl, d_input, d_key, d_lengths, sk, hk, st);
+    ssbh_plan::GraphKey key{};
+    key.st = st;
+    key.in = d_input;
+    key.key = d_key;
+    key.len = d_lengths;
+    std::memcpy(key.sk, sk, 32);
+    std::memcpy(key.hk, hk, 32);
+    key.timing = pl->timing;
+    if (!(pl->exec && key == pl->gkey)) {
+        if (pl->exec) {
+            cudaGraphExecDestroy(pl->exec);
+            pl->exec = nullptr;
+        }
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const ssbh_status s = plan_enqueue(pl, d_input, d_key, d_lengths, sk, hk, st);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (s != SSBH_OK) {
+            if (g) cudaGraphDestroy(g);
+            return s;
+        }
+        if (e != cudaSuccess) return fail(SSBH_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        const cudaError_t ie = cudaGraphInstantiate(&pl->exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            pl->exec = nullptr;
+            return fail(SSBH_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ie));
+        }
+        pl->gkey = key;
+    }
+    CU(cudaGraphLaunch(pl->exec, st));
+    return ok();
 }
 
 extern "C" ssbh_status ssbh_plan_check(ssbh_plan* pl, ssbh_extract_stats* stats) {

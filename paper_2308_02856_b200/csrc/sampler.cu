@@ -19,6 +19,7 @@
 //      see toeplitz.cu) with a red.or on a zeroed buffer — OR of distinct bits is order
 //      independent, so the result is deterministic.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -48,6 +49,79 @@ struct PayloadBits<uint32_t> {
     static constexpr uint32_t kVMask = 0x3fffffffu;
 };
 
+// One group of 32 consecutive rounds: V_i, payload / assignment write; returns the
+// owned-block index jj (or ~0 when the round is not counted).
+template <typename P, bool kPow2>
+__device__ __forceinline__ uint32_t sample_group(const Key& key, uint64_t n, uint64_t s,
+                                                 const uint32_t* __restrict__ in32,
+                                                 const uint8_t* __restrict__ keep, uint32_t j_lo,
+                                                 uint32_t nown, uint64_t g, uint32_t lane,
+                                                 P* __restrict__ payload,
+                                                 uint32_t* __restrict__ assign_out) {
+    using B = PayloadBits<P>;
+    const uint64_t i = g * 32 + lane;
+    const bool valid = i < n;
+    uint32_t v = 0;
+    if (valid) {
+        if (kPow2)
+            v = (uint32_t)(threefry_w0(key.ks, kTagSampling, 0, i, 0) & (s - 1));
+        else
+            v = (uint32_t)uniform_below(key.ks, kTagSampling, 0, s, i);
+    }
+    uint32_t bit = 0;
+    if (in32) bit = (__ldg(in32 + g) >> lane) & 1u;
+    bool kept = valid;
+    if (keep && valid) kept = keep[i] != 0;
+    if (valid) {
+        if (payload) {
+            uint32_t pv = v | (bit << B::kDataShift);
+            if (B::kKeepShift < 32 && !kept) pv |= 1u << (B::kKeepShift & 31);
+            payload[i] = (P)pv;
+        }
+        if (assign_out) assign_out[i] = v + 1;
+    }
+    const uint32_t jj = v - j_lo;
+    return (kept && jj < nown) ? jj : 0xffffffffu;
+}
+
+// Pass 1, small s: every warp counts one (chunk, part) range into a warp-private smem
+// histogram (match_any-aggregated plain read-modify-writes — the warp owns the row), then
+// flushes the non-zero bins to the global (chunk, block) table.
+template <typename P, bool kPow2>
+__global__ void __launch_bounds__(256) k_sample_count_rows(
+    Key key, uint64_t n, uint64_t s, const uint32_t* __restrict__ in32,
+    const uint8_t* __restrict__ keep, uint32_t j_lo, uint32_t nown, int cs, uint64_t nchunks,
+    uint32_t parts, P* __restrict__ payload, uint32_t* __restrict__ counts,
+    uint32_t* __restrict__ assign_out) {
+    extern __shared__ uint32_t hist_all[];
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t* hist = hist_all + (size_t)(threadIdx.x >> 5) * nown;
+    const uint64_t gpc = (1ull << cs) / 32;  // groups per chunk
+    const uint64_t ngroups = (n + 31) / 32;
+    const uint64_t total = nchunks * parts;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = warp; w < total; w += nwarps) {
+        const uint64_t c = w / parts, part = w % parts;
+        for (uint32_t t = lane; t < nown; t += 32) hist[t] = 0;
+        __syncwarp();
+        const uint64_t g0 = c * gpc + part * gpc / parts;
+        const uint64_t g1 = min(ngroups, c * gpc + (part + 1) * gpc / parts);
+        for (uint64_t g = g0; g < g1; ++g) {
+            const uint32_t jj = sample_group<P, kPow2>(key, n, s, in32, keep, j_lo, nown, g,
+                                                       lane, payload, assign_out);
+            const uint32_t peers = __match_any_sync(0xffffffffu, jj);
+            if (jj != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                hist[jj] += (uint32_t)__popc(peers);
+            __syncwarp();
+        }
+        for (uint32_t t = lane; t < nown; t += 32)
+            if (hist[t]) atomicAdd(counts + c * nown + t, hist[t]);
+        __syncwarp();
+    }
+}
+
+// Pass 1, large s: counts go straight to the global (chunk, block) table.
 template <typename P, bool kPow2>
 __global__ void __launch_bounds__(256) k_sample_count(Key key, uint64_t n, uint64_t s,
                                                       const uint32_t* __restrict__ in32,
@@ -56,38 +130,16 @@ __global__ void __launch_bounds__(256) k_sample_count(Key key, uint64_t n, uint6
                                                       P* __restrict__ payload,
                                                       uint32_t* __restrict__ counts,
                                                       uint32_t* __restrict__ assign_out) {
-    using B = PayloadBits<P>;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t ngroups = (n + 31) / 32;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t g = warp; g < ngroups; g += nwarps) {
-        const uint64_t i = g * 32 + lane;
-        const bool valid = i < n;
-        uint32_t v = 0;
-        if (valid) {
-            if (kPow2)
-                v = (uint32_t)(threefry_w0(key.ks, kTagSampling, 0, i, 0) & (s - 1));
-            else
-                v = (uint32_t)uniform_below(key.ks, kTagSampling, 0, s, i);
-        }
-        uint32_t bit = 0;
-        if (in32) bit = (__ldg(in32 + g) >> lane) & 1u;
-        bool kept = valid;
-        if (keep && valid) kept = keep[i] != 0;
-        if (valid) {
-            if (payload) {
-                uint32_t pv = v | (bit << B::kDataShift);
-                if (B::kKeepShift < 32 && !kept) pv |= 1u << (B::kKeepShift & 31);
-                payload[i] = (P)pv;
-            }
-            if (assign_out) assign_out[i] = v + 1;
-        }
-        const uint32_t jj = v - j_lo;
-        const bool in = kept && jj < nown;
-        const uint32_t peers = __match_any_sync(0xffffffffu, in ? jj : 0xffffffffu);
-        if (in && lane == (uint32_t)(__ffs(peers) - 1))
-            atomicAdd(counts + (i >> cs) * nown + jj, (uint32_t)__popc(peers));
+        const uint32_t jj = sample_group<P, kPow2>(key, n, s, in32, keep, j_lo, nown, g, lane,
+                                                   payload, assign_out);
+        const uint32_t peers = __match_any_sync(0xffffffffu, jj);
+        if (jj != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+            atomicAdd(counts + ((g * 32) >> cs) * nown + jj, (uint32_t)__popc(peers));
     }
 }
 
@@ -137,9 +189,21 @@ __global__ void k_scan_apply(uint32_t* __restrict__ counts, uint64_t nchunks, ui
     }
 }
 
-template <typename P, bool kSmemRow>
+// Mask of the lanes whose `in` is set and whose key equals this lane's key (kbits low
+// bits compared): one ballot per key bit.
+__device__ __forceinline__ uint32_t peers_by_ballot(uint32_t key, bool in, int kbits) {
+    uint32_t m = __ballot_sync(0xffffffffu, in);
+    for (int b = 0; b < kbits; ++b) {
+        const uint32_t kb = (key >> b) & 1u;
+        const uint32_t bb = __ballot_sync(0xffffffffu, kb);
+        m &= bb ^ (kb - 1u);  // kb ? bb : ~bb
+    }
+    return m;
+}
+
+template <typename P, bool kSmemRow, bool kMatch>
 __global__ void __launch_bounds__(256) k_scatter(const P* __restrict__ payload, uint64_t n,
-                                                 uint32_t j_lo, uint32_t nown, int cs,
+                                                 uint32_t j_lo, uint32_t nown, int kbits, int cs,
                                                  uint64_t nchunks, uint32_t* __restrict__ offs,
                                                  const unsigned long long* __restrict__ nj,
                                                  const unsigned long long* __restrict__ yoff,
@@ -147,10 +211,20 @@ __global__ void __launch_bounds__(256) k_scatter(const P* __restrict__ payload, 
                                                  unsigned long long* __restrict__ idx_out,
                                                  const unsigned long long* __restrict__ csr_off) {
     using B = PayloadBits<P>;
-    extern __shared__ uint32_t srow_all[];
+    constexpr int U = 4;  // groups of 32 rounds whose payloads are in flight per warp
+    extern __shared__ __align__(16) uint8_t scatter_smem[];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t wpb = blockDim.x >> 5;
+    // Rank `pos` of block jj lands on global y bit  yend[jj] - pos  (reversed packing).
+    unsigned long long* s_end = reinterpret_cast<unsigned long long*>(scatter_smem);
+    uint32_t* srow_all = reinterpret_cast<uint32_t*>(scatter_smem + (size_t)nown * 8);
+    if (kSmemRow) {
+        if (!idx_out)
+            for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
+                s_end[t] = yoff[t] * 32ull + nj[t] - 1ull;
+        __syncthreads();
+    }
     for (uint64_t c = blockIdx.x * (uint64_t)wpb + wib; c < nchunks;
          c += (uint64_t)gridDim.x * wpb) {
         uint32_t* row = offs + c * nown;
@@ -162,31 +236,63 @@ __global__ void __launch_bounds__(256) k_scatter(const P* __restrict__ payload, 
         }
         const uint64_t i0 = c << cs;
         const uint64_t i1 = min(n, (c + 1) << cs);
-        for (uint64_t ib = i0; ib < i1; ib += 32) {
-            const uint64_t i = ib + lane;
-            const bool valid = i < i1;
-            const uint32_t p = valid ? (uint32_t)payload[i] : 0u;
-            const uint32_t v = p & B::kVMask;
-            const uint32_t bit = (p >> B::kDataShift) & 1u;
-            bool kept = valid;
-            if (B::kKeepShift < 32) kept = kept && !((p >> (B::kKeepShift & 31)) & 1u);
-            const uint32_t jj = v - j_lo;
-            const bool in = kept && jj < nown;
-            const uint32_t peers = __match_any_sync(0xffffffffu, in ? jj : 0xffffffffu);
-            const uint32_t leader = __ffs(peers) - 1;
-            uint32_t base = 0;
-            if (in && lane == leader) base = atomicAdd(row + jj, (uint32_t)__popc(peers));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (in) {
-                const uint64_t pos = (uint64_t)base + __popc(peers & lanemask_lt());
-                if (idx_out) {
-                    idx_out[csr_off[jj] + pos] = i;
-                } else if (bit) {
-                    const uint64_t q = nj[jj] - 1 - pos;
-                    atomicOr(ybuf + yoff[jj] + (q >> 5), 1u << (q & 31));
-                }
+        uint32_t cur[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const uint64_t i = i0 + 32 * q + lane;
+            cur[q] = i < i1 ? (uint32_t)payload[i] : 0u;
+        }
+        for (uint64_t ib = i0; ib < i1; ib += 32 * U) {
+            // software pipeline: the next batch's payload loads are in flight while this
+            // batch is ranked (the ranking itself must stay in round order)
+            uint32_t nxt[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint64_t i = ib + 32 * (U + q) + lane;
+                nxt[q] = i < i1 ? (uint32_t)payload[i] : 0u;
             }
-            __syncwarp();
+            // (1) peer masks of the U groups: independent of the running ranks, so their
+            //     latency overlaps (MATCH.ANY x U in flight, or ballots per key bit)
+            uint32_t jjv[U], peers[U];
+            bool inv[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint64_t i = ib + 32 * q + lane;
+                const uint32_t p = cur[q];
+                bool kept = i < i1;
+                if (B::kKeepShift < 32) kept = kept && !((p >> (B::kKeepShift & 31)) & 1u);
+                jjv[q] = (p & B::kVMask) - j_lo;
+                inv[q] = kept && jjv[q] < nown;
+                if (kMatch)
+                    peers[q] = __match_any_sync(0xffffffffu, inv[q] ? jjv[q] : 0xffffffffu);
+                else
+                    peers[q] = peers_by_ballot(jjv[q], inv[q], kbits);
+            }
+            // (2) in round order: all peers read the running rank (same address: broadcast),
+            //     the highest peer writes it back. The warp owns `row` (no atomics); groups
+            //     are ordered by __syncwarp.
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint64_t i = ib + 32 * q + lane;
+                const uint32_t jj = jjv[q];
+                const uint32_t pm = peers[q];
+                if (inv[q]) {
+                    const uint32_t base = row[jj];
+                    if ((pm >> lane) == 1u) row[jj] = base + (uint32_t)__popc(pm);
+                    const uint64_t pos = (uint64_t)base + __popc(pm & lanemask_lt());
+                    if (idx_out) {
+                        idx_out[csr_off[jj] + pos] = i;
+                    } else if ((cur[q] >> B::kDataShift) & 1u) {
+                        const unsigned long long e =
+                            kSmemRow ? s_end[jj] : __ldg(yoff + jj) * 32ull + __ldg(nj + jj) - 1ull;
+                        const uint64_t qb = e - pos;
+                        atomicOr(ybuf + (qb >> 5), 1u << (qb & 31));
+                    }
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q) cur[q] = nxt[q];
         }
         __syncwarp();
     }
@@ -286,37 +392,55 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
     return g;
 }
 
+template <typename P, bool kPow2>
+static void sample_count_t(const SamplerGeom& g, const Key& k, const uint32_t* d_in32,
+                           const uint8_t* d_keep, P* pl, uint32_t* d_counts,
+                           uint32_t* d_assign_out, cudaStream_t st) {
+    const uint64_t groups = (g.n + 31) / 32;
+    const size_t row_bytes = (size_t)g.nown * 4;
+    if (row_bytes * 8 <= 96 * 1024) {
+        // enough (chunk, part) work units for ~2 waves of 64 warps per SM
+        const uint64_t gpc = (1ull << g.chunk_shift) / 32;
+        const uint64_t want = (uint64_t)sm_count() * 128;
+        const uint32_t parts =
+            (uint32_t)std::min<uint64_t>(gpc, std::max<uint64_t>(1, (want + g.nchunks - 1) / g.nchunks));
+        const uint64_t units = g.nchunks * parts;
+        const uint64_t blocks = std::min<uint64_t>((units + 7) / 8, (uint64_t)sm_count() * 8);
+        const size_t shm = row_bytes * 8;
+        auto kern = k_sample_count_rows<P, kPow2>;
+        if (shm > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
+            k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, g.nchunks, parts, pl,
+            d_counts, d_assign_out);
+        return;
+    }
+    uint64_t blocks = (groups + 7) / 8;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    k_sample_count<P, kPow2><<<(unsigned)blocks, 256, 0, st>>>(
+        k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, pl, d_counts, d_assign_out);
+}
+
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
                          const uint8_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st) {
     if (g.n == 0) return;
     Key k;
     threefry_ks(key, k.ks);
-    const uint64_t groups = (g.n + 31) / 32;
-    uint64_t blocks = (groups + 7) / 8;
-    const uint64_t cap = (uint64_t)sm_count() * 8;
-    if (blocks > cap) blocks = cap;
     const bool pow2 = (g.s & (g.s - 1)) == 0;
     if (g.payload_bytes == 2) {
         auto* pl = static_cast<uint16_t*>(d_payload);
         if (pow2)
-            k_sample_count<uint16_t, true><<<(unsigned)blocks, 256, 0, st>>>(
-                k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, pl, d_counts,
-                d_assign_out);
+            sample_count_t<uint16_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
         else
-            k_sample_count<uint16_t, false><<<(unsigned)blocks, 256, 0, st>>>(
-                k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, pl, d_counts,
-                d_assign_out);
+            sample_count_t<uint16_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
     } else {
         auto* pl = static_cast<uint32_t*>(d_payload);
         if (pow2)
-            k_sample_count<uint32_t, true><<<(unsigned)blocks, 256, 0, st>>>(
-                k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, pl, d_counts,
-                d_assign_out);
+            sample_count_t<uint32_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
         else
-            k_sample_count<uint32_t, false><<<(unsigned)blocks, 256, 0, st>>>(
-                k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, pl, d_counts,
-                d_assign_out);
+            sample_count_t<uint32_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
     }
 }
 
@@ -329,6 +453,15 @@ void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d
     k_scan_apply<<<grid, 256, 0, st>>>(d_counts, g.nchunks, g.nown, g.group_chunks, d_gsum);
 }
 
+static bool scatter_match() {  // dev switch for A/B: SSBH_SCATTER_PEERS=ballot|match
+    static int m = -1;
+    if (m < 0) {
+        const char* e = std::getenv("SSBH_SCATTER_PEERS");
+        m = (e && e[0] == 'm') ? 1 : 0;  // ballot default: 6.3 ms vs 8.6 ms (config 3)
+    }
+    return m == 1;
+}
+
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
                     const unsigned long long* d_nj, const unsigned long long* d_yoff,
                     uint32_t* d_ybuf, unsigned long long* d_idx_out,
@@ -338,19 +471,22 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
     const bool smem = row_bytes <= 32768;
     int wpb = 8;
     size_t shm = 0;
-    if (smem) {
+    if (smem) {  // per-warp running-rank rows + the per-block y end-bit table
         wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / row_bytes));
-        shm = row_bytes * wpb;
+        shm = row_bytes * wpb + (size_t)g.nown * 8;
     }
     uint64_t blocks = (g.nchunks + wpb - 1) / wpb;
     const int threads = wpb * 32;
+    int kbits = 1;
+    while ((1ull << kbits) < g.nown) ++kbits;
 #define SSBH_SCATTER(P, SM)                                                                   \
     do {                                                                                      \
-        auto kern = k_scatter<P, SM>;                                                         \
+        auto kern = scatter_match() ? k_scatter<P, SM, true> : k_scatter<P, SM, false>;       \
         if (shm > 48 * 1024)                                                                  \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm); \
         kern<<<(unsigned)blocks, threads, shm, st>>>(                                         \
-            static_cast<const P*>(d_payload), g.n, g.j_lo, g.nown, g.chunk_shift, g.nchunks,  \
+            static_cast<const P*>(d_payload), g.n, g.j_lo, g.nown, kbits, g.chunk_shift,      \
+            g.nchunks,                                                                        \
             d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);                           \
     } while (0)
     if (g.payload_bytes == 2) {

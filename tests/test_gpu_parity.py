@@ -290,6 +290,21 @@ def test_plan_reuse_and_device_path(dev, oracle, golden):
     ekey, enj = oracle.extract(x, n, s, 5, 6, 0, k)
     assert (d_key.cpu().numpy().view(np.uint64) == ekey).all()
     assert (d_len.cpu().numpy().view(np.uint64) == enj).all()
+    # CUDA-graph path (capturable stream, timing off): captured once, replayed, re-captured
+    # when the seeds change
+    stream = torch.cuda.Stream()
+    for seeds in ((c["seed_samp"], c["seed_hash"]), (c["seed_samp"], c["seed_hash"]), (5, 6)):
+        d_key.zero_()
+        torch.cuda.synchronize()
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream,
+                        samp=seeds[0], hsh=seeds[1])
+        plan.check()
+        want = ekey if seeds == (5, 6) else None
+        got = d_key.cpu().numpy().view(np.uint64)
+        if want is None:
+            assert f"{oracle.fnv(got):016x}" == c["key_fnv"]
+        else:
+            assert (got == want).all()
     plan.close()
 
 

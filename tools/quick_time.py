@@ -17,7 +17,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
-    tag = os.environ.get("SSBH_HASH_WIN", "default")
+    tag = os.environ.get("SSBH_HASH_WIN", "default") + ("/nograph" if os.environ.get("SSBH_NO_GRAPH") == "1" else "/graph")
     peak, _ = P.measure_lop3_peak(20000)
     print(json.dumps({"win": tag, "lop3_peak_T": round(peak / 1e12, 3)}), flush=True)
     for cid in [int(c) for c in args.configs.split(",")]:
@@ -29,8 +29,9 @@ def main():
         P.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
         d_key = torch.zeros((s * k + 63) // 64 * 2, dtype=torch.int32, device="cuda")
         torch.cuda.synchronize()
+        stream = torch.cuda.Stream()
         for r in range(args.reps + 1):
-            plan.run_device(d_in.data_ptr(), d_key.data_ptr())
+            plan.run_device(d_in.data_ptr(), d_key.data_ptr(), 0, stream.cuda_stream)
             st = plan.check()
             if r == 0:
                 continue  # warm-up
