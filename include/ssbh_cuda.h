@@ -193,6 +193,23 @@ ssbh_status ssbh_extract(const ssbh_extract_params* params, const uint64_t* inpu
 ssbh_status ssbh_plan_run_host(ssbh_plan* plan, const uint64_t* input, uint64_t* out_key,
                                uint64_t* out_lengths, ssbh_extract_stats* stats);
 
+/* Streaming plans — inputs fed in pieces (BASELINE config 5: 2^37 rounds "streamed in 8
+ * chunks"; also any input larger than device memory). No per-round payload buffer: V_i is
+ * recomputed by Threefry in the scatter pass. Every chunk except the last holds exactly
+ * chunk_bits rounds (a multiple of 1024); chunks may be fed in any order, each once.
+ *   ssbh_plan_stream_begin  : count pass over all n rounds (needs no input), scan, layout
+ *   ssbh_plan_stream_chunk  : chunk c's rounds [c*chunk_bits, ...) as uint32 words on device
+ *   ssbh_plan_stream_finish : seeds, hash, concatenation into d_key (+ lengths)
+ * then ssbh_plan_check as for in-memory plans. */
+ssbh_status ssbh_plan_create_streaming(const ssbh_extract_params* params, uint64_t chunk_bits,
+                                       ssbh_plan** plan);
+ssbh_status ssbh_plan_stream_begin(ssbh_plan* plan, const uint64_t* samp_key,
+                                   const uint64_t* hash_key, void* stream);
+ssbh_status ssbh_plan_stream_chunk(ssbh_plan* plan, uint64_t chunk_index, const uint32_t* d_chunk,
+                                   void* stream);
+ssbh_status ssbh_plan_stream_finish(ssbh_plan* plan, uint32_t* d_key, uint64_t* d_lengths,
+                                    void* stream);
+
 /* Synthetic input on the device: p == 0.5 -> KeyedStream(key,"input").bits(n);
  * else bit i = bernoulli(p, i) of the same stream. d_out: ceil(n/32) uint32 words. */
 ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbits,

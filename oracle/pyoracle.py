@@ -363,3 +363,24 @@ class Reference:
                                       _p64(key_of(samp)), _p64(key_of(hsh)), nblocks,
                                       _p64(bits), _p64(dig))
         return float(secs), int(bits[0]), int(dig[0])
+
+
+def _ref_extract_selected(self, x, n, s, samp, hsh, per_block, k, which):
+    """Reference-code streaming extraction of selected blocks (ref_shim.cpp)."""
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    which = np.ascontiguousarray(which, dtype=np.uint32)
+    kw = nwords(k)
+    keys = np.zeros(max(len(which) * kw, 1), dtype=np.uint64)
+    nj = np.zeros(s, dtype=np.uint64)
+    L = self.L
+    L.ref_extract_selected.restype = C.c_int
+    L.ref_extract_selected.argtypes = [U64P, C.c_uint64, C.c_uint32, U64P, U64P, C.c_int,
+                                       C.c_uint64, U32P, C.c_uint32, U64P, U64P]
+    rc = L.ref_extract_selected(_p64(x), n, s, _p64(key_of(samp)), _p64(key_of(hsh)),
+                                int(per_block), k, _p32(which), len(which), _p64(keys), _p64(nj))
+    if rc:
+        raise ValueError(f"extract_selected failed (code {rc})")
+    return keys[: len(which) * kw].reshape(len(which), kw), nj
+
+
+Reference.extract_selected = _ref_extract_selected

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "parallel.hpp"  // proj/src/parallel.hpp
@@ -204,6 +205,54 @@ int ref_extract(const uint64_t* input, uint64_t n, uint32_t s, const uint64_t sa
         BitString key;
         for (uint32_t j = 0; j < s; ++j) key.append(outs[j]);
         to_words(key, out_key);
+        return 0;
+    } catch (...) {
+        return code_of_current();
+    }
+}
+
+// Streaming form of the file-mode extraction for sizes whose Partition cannot be held in
+// memory: every round's V_i from the reference's own
+// KeyedStream::uniform_below (contiguous per-thread index ranges, concatenated in thread
+// order = round order), all n_j counted, the rounds of the `which` blocks gathered; those
+// blocks hashed with the reference's KeyedStream::bits + ToeplitzSeed + toeplitz_hash.
+int ref_extract_selected(const uint64_t* input, uint64_t n, uint32_t s, const uint64_t samp[4],
+                         const uint64_t hash[4], int per_block, uint64_t k, const uint32_t* which,
+                         uint32_t nwhich, uint64_t* out_keys, uint64_t* out_nj) {
+    try {
+        const KeyedStream st(seed_of(samp), "sampling");
+        std::vector<int32_t> slot(s, -1);
+        for (uint32_t q = 0; q < nwhich; ++q) slot[which[q]] = (int32_t)q;
+        const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+        const uint64_t per = (n + hw - 1) / hw;
+        std::vector<std::vector<uint64_t>> counts(hw, std::vector<uint64_t>(s, 0));
+        std::vector<std::vector<std::vector<uint64_t>>> lists(
+            hw, std::vector<std::vector<uint64_t>>(nwhich));
+        detail::parallel_for(hw, [&](std::size_t t) {
+            const uint64_t lo = t * per, hi = std::min(n, lo + per);
+            for (uint64_t i = lo; i < hi; ++i) {
+                const uint64_t v = st.uniform_below(s, i);
+                ++counts[t][v];
+                if (slot[v] >= 0) lists[t][slot[v]].push_back(i);
+            }
+        });
+        for (uint32_t j = 0; j < s; ++j) {
+            uint64_t c = 0;
+            for (std::size_t t = 0; t < hw; ++t) c += counts[t][j];
+            out_nj[j] = c;
+        }
+        const uint64_t kw = (k + 63) / 64;
+        detail::parallel_for(nwhich, [&](std::size_t q) {
+            std::vector<uint64_t> idx;
+            for (std::size_t t = 0; t < hw; ++t)
+                idx.insert(idx.end(), lists[t][q].begin(), lists[t][q].end());
+            BitString x(idx.size());
+            for (uint64_t r = 0; r < idx.size(); ++r)
+                if ((input[idx[r] >> 6] >> (idx[r] & 63)) & 1) x.set(r, true);
+            const KeyedStream hs(seed_of(hash), "hash-seed", per_block ? which[q] : 0);
+            const ToeplitzSeed ts(hs.bits(k + x.size() - 1), k, x.size());
+            to_words(toeplitz_hash(ts, x), out_keys + q * kw);
+        });
         return 0;
     } catch (...) {
         return code_of_current();

@@ -41,7 +41,8 @@ ABI_SYMBOLS = (
     "ssbh_blocked_toeplitz_hash", "ssbh_cycle_estimate", "ssbh_toeplitz_hash_batch",
     "ssbh_plan_create", "ssbh_plan_destroy", "ssbh_plan_device_bytes", "ssbh_plan_run_device",
     "ssbh_plan_check", "ssbh_plan_set_timing", "ssbh_extract", "ssbh_plan_run_host",
-    "ssbh_make_input_device", "ssbh_measure_lop3_peak",
+    "ssbh_make_input_device", "ssbh_measure_lop3_peak", "ssbh_plan_create_streaming",
+    "ssbh_plan_stream_begin", "ssbh_plan_stream_chunk", "ssbh_plan_stream_finish",
 )
 
 
@@ -163,6 +164,15 @@ def _load():
     L.ssbh_plan_run_host.argtypes = [C.c_void_p, U64P, U64P, U64P, C.POINTER(ExtractStats)]
     L.ssbh_make_input_device.restype = st
     L.ssbh_make_input_device.argtypes = [U64P, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.ssbh_plan_create_streaming.restype = st
+    L.ssbh_plan_create_streaming.argtypes = [C.POINTER(ExtractParams), C.c_uint64,
+                                             C.POINTER(C.c_void_p)]
+    L.ssbh_plan_stream_begin.restype = st
+    L.ssbh_plan_stream_begin.argtypes = [C.c_void_p, U64P, U64P, C.c_void_p]
+    L.ssbh_plan_stream_chunk.restype = st
+    L.ssbh_plan_stream_chunk.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.ssbh_plan_stream_finish.restype = st
+    L.ssbh_plan_stream_finish.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.ssbh_measure_lop3_peak.restype = st
     L.ssbh_measure_lop3_peak.argtypes = [C.c_uint32, C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
@@ -353,17 +363,36 @@ def extract(x, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0
 
 
 class Plan:
-    """Device plan (ssbh_plan_*): buffers sized once, reused across runs."""
+    """Device plan (ssbh_plan_*): buffers sized once, reused across runs.
+    chunk_bits > 0 creates a streaming plan (stream_begin / stream_chunk / stream_finish)."""
 
     def __init__(self, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0,
-                 limit=0):
+                 limit=0, chunk_bits=0):
         self.params = make_params(n, s, k, samp, hsh, per_block, block_first, block_count,
                                   limit)
         self.owned = block_count or s
         self.n, self.s, self.k = n, s, k
+        self.chunk_bits = chunk_bits
         h = C.c_void_p()
-        _check(lib.ssbh_plan_create(C.byref(self.params), C.byref(h)))
+        if chunk_bits:
+            _check(lib.ssbh_plan_create_streaming(C.byref(self.params), chunk_bits, C.byref(h)))
+        else:
+            _check(lib.ssbh_plan_create(C.byref(self.params), C.byref(h)))
         self.h = h
+
+    def stream_begin(self, stream: int = 0, samp=None, hsh=None):
+        sk = None if samp is None else _p64(key_of(samp))
+        hk = None if hsh is None else _p64(key_of(hsh))
+        _check(lib.ssbh_plan_stream_begin(self.h, sk, hk, C.c_void_p(stream or None)))
+
+    def stream_chunk(self, index: int, d_chunk_ptr: int, stream: int = 0):
+        _check(lib.ssbh_plan_stream_chunk(self.h, index, C.c_void_p(d_chunk_ptr),
+                                          C.c_void_p(stream or None)))
+
+    def stream_finish(self, d_key_ptr: int, d_len_ptr: int = 0, stream: int = 0):
+        _check(lib.ssbh_plan_stream_finish(self.h, C.c_void_p(d_key_ptr),
+                                           C.c_void_p(d_len_ptr or None),
+                                           C.c_void_p(stream or None)))
 
     @property
     def device_bytes(self) -> int:

@@ -357,11 +357,21 @@ struct ssbh_plan {
         bool timing;
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
     } gkey{};
+    // streaming plans (no payload buffer; input fed chunk by chunk)
+    bool streaming = false;
+    uint64_t chunk_bits = 0;
+    uint64_t stream_samp[4]{}, stream_hash[4]{};
+    uint32_t stream_launches = 0;
     // host-path staging
     DBuf d_input, d_key, d_len;
     cudaStream_t own_stream = nullptr;
     uint64_t bytes = 0;
 };
+
+static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint64_t* sk,
+                                cudaStream_t st, uint32_t& launches);
+static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
+                                const uint64_t* hk, cudaStream_t st, uint32_t& launches);
 
 static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown) {
     if (!p) return fail(SSBH_INVALID_ARGUMENT, "extract: null params");
@@ -380,16 +390,25 @@ static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown)
     return SSBH_OK;
 }
 
-extern "C" ssbh_status ssbh_plan_create(const ssbh_extract_params* params, ssbh_plan** out) {
+static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t chunk_bits,
+                                    ssbh_plan** out) {
     uint32_t nown = 0;
     if (auto s = validate_params(params, &nown)) return s;
     NEED_DEVICE();
+    int max_cs = 40;
+    if (chunk_bits) {
+        if (chunk_bits % 1024 != 0)
+            return fail(SSBH_INVALID_ARGUMENT, "streaming: chunk_bits must be a multiple of 1024");
+        max_cs = __builtin_ctzll(chunk_bits);
+    }
     auto* pl = new ssbh_plan();
     pl->p = *params;
     pl->nown = nown;
+    pl->streaming = chunk_bits != 0;
+    pl->chunk_bits = chunk_bits;
     CU(cudaGetDevice(&pl->device));
     const uint64_t n = params->n_rounds, k = params->out_bits;
-    pl->geom = make_sampler_geom(n, params->n_subblocks, params->block_first, nown, false);
+    pl->geom = make_sampler_geom(n, params->n_subblocks, params->block_first, nown, false, max_cs);
     pl->kw = (uint32_t)((k + 31) / 32);
     pl->rowtiles = (pl->kw + kHashRowWords - 1) / kHashRowWords;
     pl->direct_out = (k % 32) == 0;
@@ -411,7 +430,7 @@ extern "C" ssbh_status ssbh_plan_create(const ssbh_extract_params* params, ssbh_
         return b.alloc(bytes);
     };
     cudaError_t e = cudaSuccess;
-    if (!e) e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
+    if (!e && !pl->streaming) e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
     if (!e) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
     if (!e) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
     if (!e) e = alloc(pl->ybuf, pl->ybuf_words * 4);
@@ -426,6 +445,57 @@ extern "C" ssbh_status ssbh_plan_create(const ssbh_extract_params* params, ssbh_
     }
     *out = pl;
     return ok();
+}
+
+extern "C" ssbh_status ssbh_plan_create(const ssbh_extract_params* params, ssbh_plan** out) {
+    return plan_create_impl(params, 0, out);
+}
+
+extern "C" ssbh_status ssbh_plan_create_streaming(const ssbh_extract_params* params,
+                                                  uint64_t chunk_bits, ssbh_plan** out) {
+    if (chunk_bits == 0) return fail(SSBH_INVALID_ARGUMENT, "streaming: chunk_bits must be positive");
+    return plan_create_impl(params, chunk_bits, out);
+}
+
+extern "C" ssbh_status ssbh_plan_stream_begin(ssbh_plan* pl, const uint64_t* samp_key,
+                                              const uint64_t* hash_key, void* stream) {
+    if (!pl || !pl->streaming) return fail(SSBH_INVALID_ARGUMENT, "stream_begin: not a streaming plan");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl->last_stream = st;
+    std::memcpy(pl->stream_samp, samp_key ? samp_key : pl->p.samp_key, 32);
+    std::memcpy(pl->stream_hash, hash_key ? hash_key : pl->p.hash_key, 32);
+    pl->stream_launches = 0;
+    if (auto s = phase_sample(pl, nullptr, pl->stream_samp, st, pl->stream_launches)) return s;
+    return check_launch("stream_begin");
+}
+
+extern "C" ssbh_status ssbh_plan_stream_chunk(ssbh_plan* pl, uint64_t chunk_index,
+                                              const uint32_t* d_chunk, void* stream) {
+    if (!pl || !pl->streaming || !d_chunk)
+        return fail(SSBH_INVALID_ARGUMENT, "stream_chunk: not a streaming plan / null chunk");
+    const uint64_t first = chunk_index * pl->chunk_bits;
+    if (first >= pl->p.n_rounds)
+        return fail(SSBH_INVALID_ARGUMENT, "stream_chunk: chunk index past the input");
+    const uint64_t count = std::min<uint64_t>(pl->chunk_bits, pl->p.n_rounds - first);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl->last_stream = st;
+    const Layout lay = pl->lay.view();
+    launch_scatter_stream(pl->geom, pl->stream_samp, d_chunk, first, count,
+                          pl->counts.as<uint32_t>(), lay.nj, lay.yoff, pl->ybuf.as<uint32_t>(), st);
+    pl->stream_launches += 1;
+    return check_launch("stream_chunk");
+}
+
+extern "C" ssbh_status ssbh_plan_stream_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
+                                               void* stream) {
+    if (!pl || !pl->streaming || !d_key)
+        return fail(SSBH_INVALID_ARGUMENT, "stream_finish: not a streaming plan / null key");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl->last_stream = st;
+    if (auto s = phase_finish(pl, d_key, d_lengths, pl->stream_hash, st, pl->stream_launches))
+        return s;
+    pl->launches_per_run = pl->stream_launches;
+    return check_launch("stream_finish");
 }
 
 extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
@@ -448,13 +518,12 @@ extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
 }
 
 // Enqueue one fused run on `st` (directly, or into a graph being captured).
-static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, uint32_t* d_key,
-                                uint64_t* d_lengths, const uint64_t* sk, const uint64_t* hk,
-                                cudaStream_t st) {
+// Phase A: pass 1-2 — Threefry V per round (+ payload when d_input is given), counts,
+// scan, device-side layout. Streaming plans call it without input (counts only).
+static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint64_t* sk,
+                                cudaStream_t st, uint32_t& launches) {
     const Layout lay = pl->lay.view();
-    uint32_t launches = 0;
     if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
-    // pass 1-2: sample + count + scan + layout
     CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
     launch_sample_count(pl->geom, sk, d_input, nullptr, pl->payload.p, pl->counts.as<uint32_t>(),
                         nullptr, st);
@@ -464,18 +533,19 @@ static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, uint32_t
                   pl->p.block_limit, st);
     launches += 5;
     if (pl->timing) CU(cudaEventRecord(pl->ev[1], st));
-    // pass 3: stable scatter into reversed packed blocks
     CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
-    launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
-                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
-    launches += 1;
+    return SSBH_OK;
+}
+
+// Phase C: Toeplitz seeds, the hash of every owned block, concatenation, lengths/stats.
+static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
+                                const uint64_t* hk, cudaStream_t st, uint32_t& launches) {
+    const Layout lay = pl->lay.view();
     if (pl->timing) CU(cudaEventRecord(pl->ev[2], st));
-    // seeds
     launch_seeds(hk, lay, pl->nown, pl->p.block_first, pl->p.per_block_seed, pl->sbuf_words,
                  pl->sbuf.as<uint32_t>(), st);
     launches += 1;
     if (pl->timing) CU(cudaEventRecord(pl->ev[3], st));
-    // hash
     uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
     CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
     HashArgs a{};
@@ -499,6 +569,21 @@ static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, uint32_t
         CU(cudaMemcpyAsync(d_lengths, lay.nj, (size_t)pl->nown * 8, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemcpyAsync(pl->h_stats, lay.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, st));
     if (pl->timing) CU(cudaEventRecord(pl->ev[5], st));
+    return SSBH_OK;
+}
+
+// One in-memory fused run on `st` (directly, or into a graph being captured).
+static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, uint32_t* d_key,
+                                uint64_t* d_lengths, const uint64_t* sk, const uint64_t* hk,
+                                cudaStream_t st) {
+    const Layout lay = pl->lay.view();
+    uint32_t launches = 0;
+    if (auto s = phase_sample(pl, d_input, sk, st, launches)) return s;
+    // pass 3: stable scatter into reversed packed blocks
+    launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
+                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
+    launches += 1;
+    if (auto s = phase_finish(pl, d_key, d_lengths, hk, st, launches)) return s;
     pl->launches_per_run = launches;
     return check_launch("plan_run");
 }
@@ -517,6 +602,8 @@ extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_inp
                                             const uint64_t* samp_key, const uint64_t* hash_key,
                                             void* stream) {
     if (!pl || !d_input || !d_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run: null argument");
+    if (pl->streaming)
+        return fail(SSBH_INVALID_ARGUMENT, "plan_run: streaming plans take stream_begin/chunk/finish");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     pl->last_stream = st;
     const uint64_t* sk = samp_key ? samp_key : pl->p.samp_key;

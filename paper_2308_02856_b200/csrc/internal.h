@@ -78,8 +78,10 @@ struct SamplerGeom {
     uint64_t ngroups;
     int payload_bytes;     // 2 (u16: V | bit<<15) or 4 (u32: V | keep<<30 | bit<<31)
 };
+// max_chunk_shift bounds the warp-chunk (streaming: input chunks must be a whole number of
+// warp-chunks).
 SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,
-                              bool has_keep);
+                              bool has_keep, int max_chunk_shift = 40);
 // Pass 1: V_i (Threefry), payload, per-(chunk, owned block) counts (counts pre-zeroed).
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
                          const uint8_t* d_keep, void* d_payload, uint32_t* d_counts,
@@ -93,6 +95,13 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
                     const unsigned long long* d_nj, const unsigned long long* d_yoff,
                     uint32_t* d_ybuf, unsigned long long* d_idx_out,
                     const unsigned long long* d_csr_off, cudaStream_t st);
+// Pass 3 for streaming plans: rounds [first, first+count) whose data bits are d_chunk32
+// (bit 0 = round `first`); V recomputed by Threefry (no payload). `first` and the chunk end
+// (unless it is n) must be multiples of the warp-chunk.
+void launch_scatter_stream(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_chunk32,
+                           uint64_t first, uint64_t count, uint32_t* d_offsets,
+                           const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                           uint32_t* d_ybuf, cudaStream_t st);
 
 // ---- layout / seeds / hash -----------------------------------------------------------
 // Computes ypad/ktl/yoff/items/soff/stats from lay.nj for nown blocks.

@@ -201,58 +201,92 @@ __device__ __forceinline__ uint32_t peers_by_ballot(uint32_t key, bool in, int k
     return m;
 }
 
-template <typename P, bool kSmemRow, bool kMatch>
-__global__ void __launch_bounds__(256) k_scatter(const P* __restrict__ payload, uint64_t n,
-                                                 uint32_t j_lo, uint32_t nown, int kbits, int cs,
-                                                 uint64_t nchunks, uint32_t* __restrict__ offs,
-                                                 const unsigned long long* __restrict__ nj,
-                                                 const unsigned long long* __restrict__ yoff,
-                                                 uint32_t* __restrict__ ybuf,
-                                                 unsigned long long* __restrict__ idx_out,
-                                                 const unsigned long long* __restrict__ csr_off) {
-    using B = PayloadBits<P>;
+// Where pass 3 gets each round's (V, data bit, keep) from:
+//  PayloadSrc — the payload written by pass 1 (in-memory plans);
+//  StreamSrc  — recomputed: V by Threefry, the bit from the current input chunk (streaming
+//               plans: no payload buffer, input fed chunk by chunk).
+template <typename P>
+struct PayloadSrc {
+    using Bits = PayloadBits<P>;
+    const P* __restrict__ payload;
+    __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return payload[i]; }
+};
+
+struct StreamSrc {
+    using Bits = PayloadBits<uint32_t>;
+    Key key;
+    uint64_t s;
+    bool pow2;
+    const uint32_t* __restrict__ in32;  // chunk words; bit 0 = round `first`
+    uint64_t first;
+    __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+        const uint64_t r = i - first;
+        const uint32_t v =
+            pow2 ? (uint32_t)(threefry_w0(key.ks, kTagSampling, 0, i, 0) & (s - 1))
+                 : (uint32_t)uniform_below(key.ks, kTagSampling, 0, s, i);
+        return v | (((__ldg(in32 + (r >> 5)) >> (r & 31)) & 1u) << Bits::kDataShift);
+    }
+};
+
+struct ScatterArgs {
+    uint64_t c_begin, c_end;  // warp-chunks processed by this launch
+    uint64_t n_end;           // one past the last round of this launch
+    uint32_t j_lo, nown;
+    int kbits, cs;
+    uint32_t* offs;           // per-(chunk, block) running ranks
+    const unsigned long long* nj;
+    const unsigned long long* yoff;
+    uint32_t* ybuf;
+    unsigned long long* idx_out;
+    const unsigned long long* csr_off;
+};
+
+template <typename Src, bool kSmemRow, bool kMatch>
+__global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
+    using B = typename Src::Bits;
     constexpr int U = 4;  // groups of 32 rounds whose payloads are in flight per warp
     extern __shared__ __align__(16) uint8_t scatter_smem[];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t wpb = blockDim.x >> 5;
+    const uint32_t nown = a.nown, j_lo = a.j_lo;
     // Rank `pos` of block jj lands on global y bit  yend[jj] - pos  (reversed packing).
     unsigned long long* s_end = reinterpret_cast<unsigned long long*>(scatter_smem);
     uint32_t* srow_all = reinterpret_cast<uint32_t*>(scatter_smem + (size_t)nown * 8);
     if (kSmemRow) {
-        if (!idx_out)
+        if (!a.idx_out)
             for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
-                s_end[t] = yoff[t] * 32ull + nj[t] - 1ull;
+                s_end[t] = a.yoff[t] * 32ull + a.nj[t] - 1ull;
         __syncthreads();
     }
-    for (uint64_t c = blockIdx.x * (uint64_t)wpb + wib; c < nchunks;
+    for (uint64_t c = a.c_begin + blockIdx.x * (uint64_t)wpb + wib; c < a.c_end;
          c += (uint64_t)gridDim.x * wpb) {
-        uint32_t* row = offs + c * nown;
+        uint32_t* row = a.offs + c * nown;
         if (kSmemRow) {
             uint32_t* srow = srow_all + (size_t)wib * nown;
             for (uint32_t t = lane; t < nown; t += 32) srow[t] = row[t];
             __syncwarp();
             row = srow;
         }
-        const uint64_t i0 = c << cs;
-        const uint64_t i1 = min(n, (c + 1) << cs);
+        const uint64_t i0 = c << a.cs;
+        const uint64_t i1 = min(a.n_end, (c + 1) << a.cs);
         uint32_t cur[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
             const uint64_t i = i0 + 32 * q + lane;
-            cur[q] = i < i1 ? (uint32_t)payload[i] : 0u;
+            cur[q] = i < i1 ? src(i) : 0u;
         }
         for (uint64_t ib = i0; ib < i1; ib += 32 * U) {
-            // software pipeline: the next batch's payload loads are in flight while this
-            // batch is ranked (the ranking itself must stay in round order)
+            // software pipeline: the next batch's payloads are in flight while this batch is
+            // ranked (the ranking itself must stay in round order)
             uint32_t nxt[U];
 #pragma unroll
             for (int q = 0; q < U; ++q) {
                 const uint64_t i = ib + 32 * (U + q) + lane;
-                nxt[q] = i < i1 ? (uint32_t)payload[i] : 0u;
+                nxt[q] = i < i1 ? src(i) : 0u;
             }
-            // (1) peer masks of the U groups: independent of the running ranks, so their
-            //     latency overlaps (MATCH.ANY x U in flight, or ballots per key bit)
+            // (1) peer masks of the U groups: independent of the running ranks
+            //     (ballots per key bit; MATCH.ANY is throughput-bound on sm_100)
             uint32_t jjv[U], peers[U];
             bool inv[U];
 #pragma unroll
@@ -266,7 +300,7 @@ __global__ void __launch_bounds__(256) k_scatter(const P* __restrict__ payload, 
                 if (kMatch)
                     peers[q] = __match_any_sync(0xffffffffu, inv[q] ? jjv[q] : 0xffffffffu);
                 else
-                    peers[q] = peers_by_ballot(jjv[q], inv[q], kbits);
+                    peers[q] = peers_by_ballot(jjv[q], inv[q], a.kbits);
             }
             // (2) in round order: all peers read the running rank (same address: broadcast),
             //     the highest peer writes it back. The warp owns `row` (no atomics); groups
@@ -280,13 +314,14 @@ __global__ void __launch_bounds__(256) k_scatter(const P* __restrict__ payload, 
                     const uint32_t base = row[jj];
                     if ((pm >> lane) == 1u) row[jj] = base + (uint32_t)__popc(pm);
                     const uint64_t pos = (uint64_t)base + __popc(pm & lanemask_lt());
-                    if (idx_out) {
-                        idx_out[csr_off[jj] + pos] = i;
+                    if (a.idx_out) {
+                        a.idx_out[a.csr_off[jj] + pos] = i;
                     } else if ((cur[q] >> B::kDataShift) & 1u) {
                         const unsigned long long e =
-                            kSmemRow ? s_end[jj] : __ldg(yoff + jj) * 32ull + __ldg(nj + jj) - 1ull;
+                            kSmemRow ? s_end[jj]
+                                     : __ldg(a.yoff + jj) * 32ull + __ldg(a.nj + jj) - 1ull;
                         const uint64_t qb = e - pos;
-                        atomicOr(ybuf + (qb >> 5), 1u << (qb & 31));
+                        atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
                     }
                 }
                 __syncwarp();
@@ -370,7 +405,7 @@ int sm_count() {
 }  // namespace
 
 SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,
-                              bool has_keep) {
+                              bool has_keep, int max_chunk_shift) {
     SamplerGeom g{};
     g.n = n;
     g.s = s;
@@ -383,7 +418,9 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
         const uint64_t nc = (n + (1ull << shift) - 1) >> shift;
         return nc * (uint64_t)nown * 4ull;
     };
-    while (cs < 40 && (((n >> cs) > 16384ull) || table_bytes(cs) > (256ull << 20))) ++cs;
+    // table budget: 256 MiB, or 1/16 of the input bytes for very large n (config 5)
+    const uint64_t budget = std::max<uint64_t>(256ull << 20, n / 128);
+    while (cs < max_chunk_shift && (((n >> cs) > 16384ull) || table_bytes(cs) > budget)) ++cs;
     g.chunk_shift = cs;
     g.nchunks = (n + (1ull << cs) - 1) >> cs;
     if (g.nchunks == 0) g.nchunks = 1;
@@ -462,11 +499,8 @@ static bool scatter_match() {  // dev switch for A/B: SSBH_SCATTER_PEERS=ballot|
     return m == 1;
 }
 
-void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
-                    const unsigned long long* d_nj, const unsigned long long* d_yoff,
-                    uint32_t* d_ybuf, unsigned long long* d_idx_out,
-                    const unsigned long long* d_csr_off, cudaStream_t st) {
-    if (g.n == 0 || g.nown == 0) return;
+template <typename Src>
+static void scatter_launch(const SamplerGeom& g, const Src& src, ScatterArgs a, cudaStream_t st) {
     const size_t row_bytes = (size_t)g.nown * 4;
     const bool smem = row_bytes <= 32768;
     int wpb = 8;
@@ -475,32 +509,71 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
         wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / row_bytes));
         shm = row_bytes * wpb + (size_t)g.nown * 8;
     }
-    uint64_t blocks = (g.nchunks + wpb - 1) / wpb;
-    const int threads = wpb * 32;
-    int kbits = 1;
-    while ((1ull << kbits) < g.nown) ++kbits;
-#define SSBH_SCATTER(P, SM)                                                                   \
-    do {                                                                                      \
-        auto kern = scatter_match() ? k_scatter<P, SM, true> : k_scatter<P, SM, false>;       \
-        if (shm > 48 * 1024)                                                                  \
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm); \
-        kern<<<(unsigned)blocks, threads, shm, st>>>(                                         \
-            static_cast<const P*>(d_payload), g.n, g.j_lo, g.nown, kbits, g.chunk_shift,      \
-            g.nchunks,                                                                        \
-            d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);                           \
-    } while (0)
-    if (g.payload_bytes == 2) {
-        if (smem)
-            SSBH_SCATTER(uint16_t, true);
-        else
-            SSBH_SCATTER(uint16_t, false);
-    } else {
-        if (smem)
-            SSBH_SCATTER(uint32_t, true);
-        else
-            SSBH_SCATTER(uint32_t, false);
-    }
-#undef SSBH_SCATTER
+    const uint64_t nc = a.c_end - a.c_begin;
+    const uint64_t blocks = std::max<uint64_t>(1, (nc + wpb - 1) / wpb);
+    a.kbits = 1;
+    while ((1ull << a.kbits) < g.nown) ++a.kbits;
+    auto go = [&](auto kern) {
+        if (shm > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        kern<<<(unsigned)blocks, wpb * 32, shm, st>>>(src, a);
+    };
+    const bool m = scatter_match();
+    if (smem)
+        m ? go(k_scatter<Src, true, true>) : go(k_scatter<Src, true, false>);
+    else
+        m ? go(k_scatter<Src, false, true>) : go(k_scatter<Src, false, false>);
+}
+
+static ScatterArgs scatter_args(const SamplerGeom& g, uint32_t* d_offsets,
+                                const unsigned long long* d_nj,
+                                const unsigned long long* d_yoff, uint32_t* d_ybuf,
+                                unsigned long long* d_idx_out,
+                                const unsigned long long* d_csr_off) {
+    ScatterArgs a{};
+    a.c_begin = 0;
+    a.c_end = g.nchunks;
+    a.n_end = g.n;
+    a.j_lo = g.j_lo;
+    a.nown = g.nown;
+    a.cs = g.chunk_shift;
+    a.offs = d_offsets;
+    a.nj = d_nj;
+    a.yoff = d_yoff;
+    a.ybuf = d_ybuf;
+    a.idx_out = d_idx_out;
+    a.csr_off = d_csr_off;
+    return a;
+}
+
+void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
+                    const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                    uint32_t* d_ybuf, unsigned long long* d_idx_out,
+                    const unsigned long long* d_csr_off, cudaStream_t st) {
+    if (g.n == 0 || g.nown == 0) return;
+    const ScatterArgs a = scatter_args(g, d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);
+    if (g.payload_bytes == 2)
+        scatter_launch(g, PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload)}, a, st);
+    else
+        scatter_launch(g, PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload)}, a, st);
+}
+
+void launch_scatter_stream(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_chunk32,
+                           uint64_t first, uint64_t count, uint32_t* d_offsets,
+                           const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                           uint32_t* d_ybuf, cudaStream_t st) {
+    if (count == 0 || g.nown == 0) return;
+    ScatterArgs a = scatter_args(g, d_offsets, d_nj, d_yoff, d_ybuf, nullptr, nullptr);
+    a.c_begin = first >> g.chunk_shift;
+    a.c_end = (first + count + (1ull << g.chunk_shift) - 1) >> g.chunk_shift;
+    a.n_end = first + count;
+    StreamSrc src{};
+    threefry_ks(key, src.key.ks);
+    src.s = g.s;
+    src.pow2 = (g.s & (g.s - 1)) == 0;
+    src.in32 = d_chunk32;
+    src.first = first;
+    scatter_launch(g, src, a, st);
 }
 
 void launch_payload_from_assignment(const SamplerGeom& g, const uint32_t* d_assign,

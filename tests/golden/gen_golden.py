@@ -37,6 +37,8 @@ def fnv(o, a):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config3", action="store_true")
+    ap.add_argument("--config4", action="store_true")
+    ap.add_argument("--only-large", action="store_true", help="skip the small vectors")
     args = ap.parse_args()
     ref, o = Reference(), Oracle()
     g = json.load(open(OUT)) if os.path.exists(OUT) else {}
@@ -97,7 +99,7 @@ def main():
     cfgs["small_k_odd"] = (50000, 8, 77, 0.5, 7, 8, 9, 0)
     cfgs["small_k_32"] = (70000, 32, 96, 0.3, 7, 8, 9, 0)
     ext = g.get("extract", {})
-    for name, (n, s, k, p, si, ss, sh, pb) in cfgs.items():
+    for name, (n, s, k, p, si, ss, sh, pb) in ([] if args.only_large else cfgs.items()):
         x = o.make_input(si, p, n)
         t = time.time()
         key, nj = ref.extract(x, n, s, ss, sh, pb, k)
@@ -125,6 +127,25 @@ def main():
             "block0_fnv": fnv(o, key[:kw]), "block1023_fnv": fnv(o, key[1023 * kw:]),
             "ref_seconds": round(time.time() - t, 1)}
         print(3, ext["3"], flush=True)
+    if args.config4:
+        # configs 4: the reference API cannot hold its Partition (192 GiB): stream with the
+        # reference's own KeyedStream / toeplitz_hash (ref_extract_selected)
+        n, s, k = 1 << 34, 16384, 3 << 18
+        which = [0, 1, 8191, 16383]
+        x = o.make_input(1, 0.4, n)
+        t = time.time()
+        keys, nj = ref.extract_selected(x, n, s, 2, 3, 1, k, which)
+        ext["4"] = {
+            "n": n, "s": s, "k": k, "p": 0.4, "seed_in": 1, "seed_samp": 2, "seed_hash": 3,
+            "per_block": 1, "input_fnv": fnv(o, x), "nj_min": int(nj.min()),
+            "nj_max": int(nj.max()), "nj_0": int(nj[0]), "nj_last": int(nj[-1]),
+            "nj_fnv": fnv(o, nj), "which": which,
+            "block_fnv": [fnv(o, keys[q]) for q in range(len(which))],
+            "block_word0": [f"{int(keys[q][0]):016x}" for q in range(len(which))],
+            "block_popcount": [int(np.unpackbits(keys[q].view(np.uint8)).sum())
+                               for q in range(len(which))],
+            "ref_seconds": round(time.time() - t, 1)}
+        print(4, ext["4"], flush=True)
     g["extract"] = ext
     json.dump(g, open(OUT, "w"), indent=1)
     print("wrote", OUT)

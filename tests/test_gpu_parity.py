@@ -337,3 +337,59 @@ def test_config3_full_key_digest(dev, oracle, golden):
     assert f"{oracle.fnv(key):016x}" == want["key_fnv"]
     assert int(st.hash_word_ops) == n * k // 32
     plan.close()
+
+
+# ------------------------------------------------------------------- streaming plans
+def _stream_run(dev, x_words, n, s, k, samp, hsh, chunk_bits, per_block=False, order=None,
+                block_first=0, block_count=0):
+    import torch
+
+    plan = dev.Plan(n, s, k, samp, hsh, per_block=per_block, block_first=block_first,
+                    block_count=block_count, chunk_bits=chunk_bits)
+    owned = block_count or s
+    x32 = torch.from_numpy(np.ascontiguousarray(x_words).view(np.int32).copy())
+    nchunks = (n + chunk_bits - 1) // chunk_bits
+    d_key = torch.zeros(((owned * k + 63) // 64) * 2, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(owned, dtype=torch.int64, device="cuda")
+    plan.stream_begin()
+    for c in (order if order is not None else range(nchunks)):
+        lo = c * chunk_bits // 32
+        hi = min((c + 1) * chunk_bits, n)
+        chunk = x32[lo:(hi + 31) // 32].cuda()
+        plan.stream_chunk(c, chunk.data_ptr())
+        torch.cuda.synchronize()
+    plan.stream_finish(d_key.data_ptr(), d_len.data_ptr())
+    st = plan.check()
+    plan.close()
+    return d_key.cpu().numpy().view(np.uint64), d_len.cpu().numpy().view(np.uint64), st
+
+
+def test_streaming_plan_matches_oracle(dev, oracle):
+    rng = np.random.default_rng(77)
+    for (n, s, k, cb, pb) in ((300000, 16, 1024, 1 << 16, False), (250001, 50, 77, 1 << 15, True),
+                              (1 << 20, 64, 8192, 1 << 17, False), (70000, 3, 96, 1 << 10, False)):
+        x = oracle.make_input(int(rng.integers(1000)), 0.5, n)
+        want, wnj = oracle.extract(x, n, s, 31, 32, pb, k)
+        nch = (n + cb - 1) // cb
+        order = list(rng.permutation(nch))  # chunks may arrive in any order
+        got, nj, _ = _stream_run(dev, x, n, s, k, 31, 32, cb, per_block=pb, order=order)
+        assert (nj == wnj).all()
+        assert (got[: len(want)] == want).all(), (n, s, k, cb, pb)
+    # owned block range in streaming mode
+    n, s, k = 200000, 16, 640
+    x = oracle.make_input(9, 0.5, n)
+    want, _ = oracle.extract(x, n, s, 31, 32, 0, k)
+    got, _, _ = _stream_run(dev, x, n, s, k, 31, 32, 1 << 14, block_first=4, block_count=8)
+    kw = k // 64
+    assert (got == want[4 * kw:12 * kw]).all()
+
+
+@pytest.mark.slow
+def test_config3_streaming_8_chunks_digest(dev, oracle, golden):
+    c = dev.CONFIGS[3]
+    want = golden["extract"].get("3", SURVEY_C3)
+    x = oracle.make_input(c["seed_in"], c["p"], c["n"])
+    got, nj, st = _stream_run(dev, x, c["n"], c["s"], c["k"], c["seed_samp"], c["seed_hash"],
+                              c["n"] // 8)
+    assert int(nj.min()) == want["nj_min"] and int(nj.max()) == want["nj_max"]
+    assert f"{oracle.fnv(got):016x}" == want["key_fnv"]
