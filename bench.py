@@ -59,7 +59,8 @@ def config_dict(cid, c, world):
         "seed_mode": "per-block (hash-seed sub=j)" if c["per_block"] else "shared (hash-seed sub=0)",
         "seeds": {"input": c["seed_in"], "sampling": c["seed_samp"], "hash": c["seed_hash"]},
         "parallelism": f"sub-blocks sharded over {world} GPU(s), replicated input",
-        "l2": "L2 flushed between steps (256 MiB write); input 128 MiB and 2 GiB payload > L2",
+        "l2": "L2 (126 MB) flushed between steps by a 256 MiB write outside the step events"
+              + ("; input and payload exceed L2" if c["n"] >= (1 << 30) else ""),
     }
 
 
@@ -226,18 +227,27 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    P.lib.ssbh_set_device(local)
+    dev_index = local % max(1, torch.cuda.device_count())  # identity on a full box
+    torch.cuda.set_device(dev_index)
+    P.lib.ssbh_set_device(dev_index)
+    backend = os.environ.get("SSBH_DIST_BACKEND", "nccl")  # gloo: multi-rank test on 1 GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
+
+    from paper_2308_02856_b200.multigpu import owned_range
 
     n, s, k = c["n"], c["s"], c["k"]
-    first = rank * s // world
-    count = (rank + 1) * s // world - first
+    first, count = owned_range(rank, world, s)
+    streaming = cid == 5  # 2^37 rounds: input streamed in 8 chunks (BASELINE configs[4])
+    chunk_bits = n // 8 if streaming else 0
     plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"],
-                  block_first=first, block_count=count)
+                  block_first=first, block_count=count, chunk_bits=chunk_bits)
     plan.set_timing(True)
-    stream = torch.cuda.Stream()  # a capturable stream: the plan replays one CUDA graph per step
+    stream = torch.cuda.Stream()  # capturable: untimed runs replay one CUDA graph
     d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
     P.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr(), stream.cuda_stream)
     key_words64 = (count * k + 63) // 64
@@ -249,13 +259,20 @@ def main():
     peak, _ = P.measure_lop3_peak(20000)  # int-ALU roofline denominator (live)
 
     def step():
-        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream)
+        if not streaming:
+            plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr(),
+                            stream.cuda_stream)
+            return
+        plan.stream_begin(stream.cuda_stream)
+        for ci in range(8):
+            plan.stream_chunk(ci, d_in.data_ptr() + ci * (chunk_bits // 8), stream.cuda_stream)
+        plan.stream_finish(d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream)
 
     for _ in range(max(3, args.warmup)):
         step()
         plan.check()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     if world > 1:
         dist.barrier()
@@ -275,42 +292,54 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms = [a_.elapsed_time(b_) for a_, b_ in ev]
     total_ms = sum(step_ms)
     clk = clocks.stop()
 
     # ---- e2e through the public host API (pinned H2D of the input, D2H of the key) ------
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
-    x_host = d_in.cpu().view(torch.int64).pin_memory()
-    key_host = torch.empty(key_words64, dtype=torch.int64).pin_memory()
-    len_host = torch.empty(count, dtype=torch.int64).pin_memory()
-    plan.run_host_ptrs(x_host.data_ptr(), key_host.data_ptr(), len_host.data_ptr())  # warm
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        plan.run_host_ptrs(x_host.data_ptr(), key_host.data_ptr(), len_host.data_ptr())
-    e2e_s = time.perf_counter() - t0
-    same = bool(torch.equal(key_host.cuda().view(torch.int32), d_key))
-
-    vals = torch.tensor([total_ms, e2e_s, float(hash_ops), max(hash_ms)], dtype=torch.float64,
-                        device="cuda")
-    if world > 1:
-        mx = vals.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        tot_ops = torch.tensor([float(hash_ops)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tot_ops, op=dist.ReduceOp.SUM)
-        vals = mx
-        hash_ops_all = tot_ops.item()
+    e2e = None
+    same = None
+    if not streaming:
+        x_host = d_in.cpu().view(torch.int64).pin_memory()
+        key_host = torch.empty(key_words64, dtype=torch.int64).pin_memory()
+        len_host = torch.empty(count, dtype=torch.int64).pin_memory()
+        plan.run_host_ptrs(x_host.data_ptr(), key_host.data_ptr(), len_host.data_ptr())  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            plan.run_host_ptrs(x_host.data_ptr(), key_host.data_ptr(), len_host.data_ptr())
+        e2e_s = time.perf_counter() - t0
+        same = bool(torch.equal(key_host.cuda().view(torch.int32), d_key))
+        e2e = {"h2d": int(x_host.numel() * 8), "d2h": int(key_words64 * 8 + count * 8)}
     else:
-        hash_ops_all = float(hash_ops)
+        e2e_s = float("nan")
+
+    # ---- gather the owned key slices in block order (the only inter-GPU exchange) --------
+    import hashlib
+
+    if world > 1:
+        from paper_2308_02856_b200.multigpu import gather_key
+
+        full = gather_key(d_key.view(torch.int64)[:key_words64].to(coll_dev), s, k)
+    else:
+        full = d_key.view(torch.int64)[:key_words64].cpu().numpy().view("uint64")
+    key_sha = hashlib.sha256(full.tobytes()).hexdigest()[:16]
+
+    vals = torch.tensor([total_ms, e2e_s, max(hash_ms)], dtype=torch.float64, device=coll_dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     total_ms, e2e_s = vals[0].item(), vals[1].item()
 
     if rank == 0:
         value = n * args.steps / (total_ms * 1e-3) / 1e9
-        e2e_val = n * e2e_steps / e2e_s / 1e9
         avg_hash_ms = sum(hash_ms) / len(hash_ms)
         achieved = hash_ops / (avg_hash_ms * 1e-3)  # rank-0 owned blocks, rank-0 launches
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "hash_traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(f"config{cid}_n{world}")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup),
@@ -323,7 +352,8 @@ def main():
                 "bound": "int-alu (LOP3)", "kernel": "k_toeplitz_hash",
                 "achieved": achieved / 1e12, "peak": peak / 1e12,
                 "unit": "T LOP3 word-ops/s", "frac": achieved / peak,
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/)",
                 "algorithmic_per_launch": f"sum_j n_j*k/32 = {hash_ops} word-ops (owned blocks)",
                 "peak_source": "measured live in this run: k_lop3_peak (csrc/diag.cu), "
                                "148 SMs x 64 LOP3 lanes/clk at the running SM clock",
@@ -333,14 +363,19 @@ def main():
                                     "scatter": stats.ms_scatter, "seeds": stats.ms_seed,
                                     "hash": stats.ms_hash, "total": stats.ms_total},
             "hash_share_of_step": avg_hash_ms / (total_ms / args.steps),
-            "e2e": {"value": e2e_val, "unit": UNIT,
-                    "h2d_bytes_per_step": int(x_host.numel() * 8),
-                    "d2h_bytes_per_step": int(key_words64 * 8 + count * 8),
-                    "steps": e2e_steps, "api": "ssbh_plan_run_host (C-ABI)",
-                    "key_matches_device_run": same},
             "gpu_launches": int(stats.launches) * args.steps,
+            "key_sha256_16": key_sha,
             "clocks": clk,
         }
+        if e2e is not None:
+            line["e2e"] = {"value": n * e2e_steps / e2e_s / 1e9, "unit": UNIT,
+                           "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                           "steps": e2e_steps, "api": "ssbh_plan_run_host (C-ABI)",
+                           "key_matches_device_run": same}
+        else:
+            line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None,
+                           "d2h_bytes_per_step": None,
+                           "note": "streaming config: input resident in HBM only"}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline_leg(cid, c)
