@@ -397,7 +397,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) 
             uint32_t it = 0;
             for (unsigned long long item = blockIdx.x;; item += gridDim.x, ++it) {
                 const int s = it % kHashStages;
-                if (it >= (uint32_t)kHashStages) mbar_wait(&empty[s], ((it / kHashStages) - 1) & 1);
+                if (it >= (uint32_t)kHashStages) mbar_wait_sleep(&empty[s], ((it / kHashStages) - 1) & 1);
                 ItemDesc d;
                 unsigned long long sy, ss;
                 const bool ok = decode_item(a, item, jj_hint, d, sy, ss);
