@@ -193,6 +193,21 @@ ssbh_status ssbh_extract(const ssbh_extract_params* params, const uint64_t* inpu
 ssbh_status ssbh_plan_run_host(ssbh_plan* plan, const uint64_t* input, uint64_t* out_key,
                                uint64_t* out_lengths, ssbh_extract_stats* stats);
 
+/* Sifted runs (the reference's keep flags, sift_partition sampling.cpp:27-39 as used by
+ * run_extraction pipeline.cpp:109-112): only rounds with keep bit set join their sub-block;
+ * n_j counts kept rounds. keep is bit-packed like the input (bit i = keep[i]; device: uint32
+ * words, host: uint64 words); NULL keeps every round. */
+ssbh_status ssbh_plan_run_device_sifted(ssbh_plan* plan, const uint32_t* d_input,
+                                        const uint32_t* d_keep, uint32_t* d_key,
+                                        uint64_t* d_lengths, const uint64_t* samp_key,
+                                        const uint64_t* hash_key, void* stream);
+ssbh_status ssbh_plan_run_host_sifted(ssbh_plan* plan, const uint64_t* input,
+                                      const uint64_t* keep, uint64_t* out_key,
+                                      uint64_t* out_lengths, ssbh_extract_stats* stats);
+ssbh_status ssbh_extract_sifted(const ssbh_extract_params* params, const uint64_t* input,
+                                const uint64_t* keep, uint64_t* out_key, uint64_t* out_lengths,
+                                ssbh_extract_stats* stats);
+
 /* Streaming plans — inputs fed in pieces (BASELINE config 5: 2^37 rounds "streamed in 8
  * chunks"; also any input larger than device memory). No per-round payload buffer: V_i is
  * recomputed by Threefry in the scatter pass. Every chunk except the last holds exactly

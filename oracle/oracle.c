@@ -483,12 +483,24 @@ static void concat_blocks(const uint64_t* blocks, uint32_t s, uint64_t k, uint64
 int or_extract(const uint64_t* input, uint64_t n, uint32_t s, const uint64_t samp_key[4],
                const uint64_t hash_key[4], int per_block_seed, uint64_t k, uint64_t* out_key,
                uint64_t* out_nj, int nthreads) {
+    return or_extract_sifted(input, NULL, n, s, samp_key, hash_key, per_block_seed, k, out_key,
+                             out_nj, nthreads);
+}
+
+/* run_extraction's sift + hash loop (pipeline.cpp:109-136): keep_in (1 byte per round,
+ * NULL = all kept) selects the rounds that join their sub-block. */
+int or_extract_sifted(const uint64_t* input, const uint8_t* keep_in, uint64_t n, uint32_t s,
+                      const uint64_t samp_key[4], const uint64_t hash_key[4], int per_block_seed,
+                      uint64_t k, uint64_t* out_key, uint64_t* out_nj, int nthreads) {
     if (s == 0 || k == 0) return -1;
     uint32_t* assignment = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
     uint64_t* raw = (uint64_t*)malloc(sizeof(uint64_t) * s);
     or_assign_subblocks(n, s, samp_key, assignment, raw, nthreads);
     uint8_t* keep = (uint8_t*)malloc(n ? n : 1);
-    memset(keep, 1, n);
+    if (keep_in)
+        memcpy(keep, keep_in, n);
+    else
+        memset(keep, 1, n);
     uint64_t* offsets = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)s + 1));
     uint64_t* indices = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
     or_sift_partition(keep, n, assignment, s, offsets, indices);

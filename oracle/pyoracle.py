@@ -212,6 +212,21 @@ class Oracle:
             raise ValueError("toeplitz: m and n must be positive (empty sub-block)")
         return key[: nwords(s * k)], nj
 
+    def extract_sifted(self, x, keep_u8, n, s, samp, hsh, per_block, k, nthreads=0):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        kp = np.ascontiguousarray(keep_u8, dtype=np.uint8)
+        key = np.zeros(max(nwords(s * k), 1), dtype=np.uint64)
+        nj = np.zeros(s, dtype=np.uint64)
+        self.L.or_extract_sifted.restype = C.c_int
+        self.L.or_extract_sifted.argtypes = [U64P, U8P, C.c_uint64, C.c_uint32, U64P, U64P,
+                                             C.c_int, C.c_uint64, U64P, U64P, C.c_int]
+        rc = self.L.or_extract_sifted(_p64(x), _p8(kp), n, s, _p64(key_of(samp)),
+                                      _p64(key_of(hsh)), int(per_block), k, _p64(key), _p64(nj),
+                                      nthreads)
+        if rc:
+            raise ValueError("toeplitz: m and n must be positive (empty sub-block)")
+        return key[: nwords(s * k)], nj
+
     def extract_selected(self, x, n, s, samp, hsh, per_block, k, which, nthreads=0):
         x = np.ascontiguousarray(x, dtype=np.uint64)
         which = np.ascontiguousarray(which, dtype=np.uint32)

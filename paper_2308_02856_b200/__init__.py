@@ -43,6 +43,7 @@ ABI_SYMBOLS = (
     "ssbh_plan_check", "ssbh_plan_set_timing", "ssbh_extract", "ssbh_plan_run_host",
     "ssbh_make_input_device", "ssbh_measure_lop3_peak", "ssbh_plan_create_streaming",
     "ssbh_plan_stream_begin", "ssbh_plan_stream_chunk", "ssbh_plan_stream_finish",
+    "ssbh_plan_run_device_sifted", "ssbh_plan_run_host_sifted", "ssbh_extract_sifted",
 )
 
 
@@ -164,6 +165,15 @@ def _load():
     L.ssbh_plan_run_host.argtypes = [C.c_void_p, U64P, U64P, U64P, C.POINTER(ExtractStats)]
     L.ssbh_make_input_device.restype = st
     L.ssbh_make_input_device.argtypes = [U64P, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.ssbh_plan_run_device_sifted.restype = st
+    L.ssbh_plan_run_device_sifted.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, U64P, U64P, C.c_void_p]
+    L.ssbh_plan_run_host_sifted.restype = st
+    L.ssbh_plan_run_host_sifted.argtypes = [C.c_void_p, U64P, U64P, U64P, U64P,
+                                            C.POINTER(ExtractStats)]
+    L.ssbh_extract_sifted.restype = st
+    L.ssbh_extract_sifted.argtypes = [C.POINTER(ExtractParams), U64P, U64P, U64P, U64P,
+                                      C.POINTER(ExtractStats)]
     L.ssbh_plan_create_streaming.restype = st
     L.ssbh_plan_create_streaming.argtypes = [C.POINTER(ExtractParams), C.c_uint64,
                                              C.POINTER(C.c_void_p)]
@@ -350,15 +360,22 @@ def make_params(n, s, k, samp, hsh, per_block=False, block_first=0, block_count=
     return p
 
 
-def extract(x, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0, limit=0):
-    """Host-buffer fused extraction (ssbh_extract). Returns (key words, n_j, stats)."""
+def extract(x, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0, limit=0,
+            keep=None):
+    """Host-buffer fused extraction (ssbh_extract / ssbh_extract_sifted when `keep` — bit-packed
+    uint64 words, bit i = keep round i — is given). Returns (key words, n_j, stats)."""
     params = make_params(n, s, k, samp, hsh, per_block, block_first, block_count, limit)
     owned = block_count or s
     x = np.ascontiguousarray(x, dtype=np.uint64)
     key = np.zeros(max(nwords(owned * k), 1), dtype=np.uint64)
     lens = np.zeros(owned, dtype=np.uint64)
     st = ExtractStats()
-    _check(lib.ssbh_extract(C.byref(params), _p64(x), _p64(key), _p64(lens), C.byref(st)))
+    if keep is None:
+        _check(lib.ssbh_extract(C.byref(params), _p64(x), _p64(key), _p64(lens), C.byref(st)))
+    else:
+        kp = np.ascontiguousarray(keep, dtype=np.uint64)
+        _check(lib.ssbh_extract_sifted(C.byref(params), _p64(x), _p64(kp), _p64(key),
+                                       _p64(lens), C.byref(st)))
     return key[: nwords(owned * k)], lens, st
 
 

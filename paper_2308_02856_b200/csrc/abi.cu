@@ -352,7 +352,7 @@ struct ssbh_plan {
     cudaGraphExec_t exec = nullptr;
     struct GraphKey {
         cudaStream_t st;
-        const void *in, *key, *len;
+        const void *in, *keep, *key, *len;
         uint64_t sk[4], hk[4];
         bool timing;
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
@@ -363,13 +363,13 @@ struct ssbh_plan {
     uint64_t stream_samp[4]{}, stream_hash[4]{};
     uint32_t stream_launches = 0;
     // host-path staging
-    DBuf d_input, d_key, d_len;
+    DBuf d_input, d_key, d_len, d_keep;
     cudaStream_t own_stream = nullptr;
     uint64_t bytes = 0;
 };
 
-static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint64_t* sk,
-                                cudaStream_t st, uint32_t& launches);
+static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
+                                const uint64_t* sk, cudaStream_t st, uint32_t& launches);
 static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                                 const uint64_t* hk, cudaStream_t st, uint32_t& launches);
 
@@ -465,7 +465,8 @@ extern "C" ssbh_status ssbh_plan_stream_begin(ssbh_plan* pl, const uint64_t* sam
     std::memcpy(pl->stream_samp, samp_key ? samp_key : pl->p.samp_key, 32);
     std::memcpy(pl->stream_hash, hash_key ? hash_key : pl->p.hash_key, 32);
     pl->stream_launches = 0;
-    if (auto s = phase_sample(pl, nullptr, pl->stream_samp, st, pl->stream_launches)) return s;
+    if (auto s = phase_sample(pl, nullptr, nullptr, pl->stream_samp, st, pl->stream_launches))
+        return s;
     return check_launch("stream_begin");
 }
 
@@ -520,12 +521,12 @@ extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
 // Enqueue one fused run on `st` (directly, or into a graph being captured).
 // Phase A: pass 1-2 — Threefry V per round (+ payload when d_input is given), counts,
 // scan, device-side layout. Streaming plans call it without input (counts only).
-static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint64_t* sk,
-                                cudaStream_t st, uint32_t& launches) {
+static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
+                                const uint64_t* sk, cudaStream_t st, uint32_t& launches) {
     const Layout lay = pl->lay.view();
     if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
     CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
-    launch_sample_count(pl->geom, sk, d_input, nullptr, pl->payload.p, pl->counts.as<uint32_t>(),
+    launch_sample_count(pl->geom, sk, d_input, d_keep, pl->payload.p, pl->counts.as<uint32_t>(),
                         nullptr, st);
     launch_scan(pl->geom, pl->counts.as<uint32_t>(), pl->gsum.as<unsigned long long>(), lay.nj,
                 st);
@@ -573,12 +574,13 @@ static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_leng
 }
 
 // One in-memory fused run on `st` (directly, or into a graph being captured).
-static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, uint32_t* d_key,
+static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
+                                uint32_t* d_key,
                                 uint64_t* d_lengths, const uint64_t* sk, const uint64_t* hk,
                                 cudaStream_t st) {
     const Layout lay = pl->lay.view();
     uint32_t launches = 0;
-    if (auto s = phase_sample(pl, d_input, sk, st, launches)) return s;
+    if (auto s = phase_sample(pl, d_input, d_keep, sk, st, launches)) return s;
     // pass 3: stable scatter into reversed packed blocks
     launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
                    pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
@@ -601,6 +603,14 @@ extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_inp
                                             uint32_t* d_key, uint64_t* d_lengths,
                                             const uint64_t* samp_key, const uint64_t* hash_key,
                                             void* stream) {
+    return ssbh_plan_run_device_sifted(pl, d_input, nullptr, d_key, d_lengths, samp_key, hash_key,
+                                       stream);
+}
+
+extern "C" ssbh_status ssbh_plan_run_device_sifted(ssbh_plan* pl, const uint32_t* d_input,
+                                                   const uint32_t* d_keep, uint32_t* d_key,
+                                                   uint64_t* d_lengths, const uint64_t* samp_key,
+                                                   const uint64_t* hash_key, void* stream) {
     if (!pl || !d_input || !d_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run: null argument");
     if (pl->streaming)
         return fail(SSBH_INVALID_ARGUMENT, "plan_run: streaming plans take stream_begin/chunk/finish");
@@ -611,12 +621,13 @@ extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_inp
     // The legacy default stream cannot be captured, and per-phase event timing is only
     // meaningful on direct launches: launch directly in those cases.
     if (st == nullptr || pl->timing || !graphs_enabled())
-        return plan_enqueue(pl, d_input, d_key, d_lengths, sk, hk, st);
+        return plan_enqueue(pl, d_input, d_keep, d_key, d_lengths, sk, hk, st);
     ssbh_plan::GraphKey key{};
     key.st = st;
     key.in = d_input;
     key.key = d_key;
     key.len = d_lengths;
+    key.keep = d_keep;
     std::memcpy(key.sk, sk, 32);
     std::memcpy(key.hk, hk, 32);
     key.timing = pl->timing;
@@ -626,7 +637,7 @@ extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_inp
             pl->exec = nullptr;
         }
         CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        const ssbh_status s = plan_enqueue(pl, d_input, d_key, d_lengths, sk, hk, st);
+        const ssbh_status s = plan_enqueue(pl, d_input, d_keep, d_key, d_lengths, sk, hk, st);
         cudaGraph_t g = nullptr;
         const cudaError_t e = cudaStreamEndCapture(st, &g);
         if (s != SSBH_OK) {
@@ -681,7 +692,16 @@ extern "C" ssbh_status ssbh_plan_check(ssbh_plan* pl, ssbh_extract_stats* stats)
 
 extern "C" ssbh_status ssbh_plan_run_host(ssbh_plan* pl, const uint64_t* input, uint64_t* out_key,
                                           uint64_t* out_lengths, ssbh_extract_stats* stats) {
+    return ssbh_plan_run_host_sifted(pl, input, nullptr, out_key, out_lengths, stats);
+}
+
+extern "C" ssbh_status ssbh_plan_run_host_sifted(ssbh_plan* pl, const uint64_t* input,
+                                                 const uint64_t* keep, uint64_t* out_key,
+                                                 uint64_t* out_lengths,
+                                                 ssbh_extract_stats* stats) {
     if (!pl || !input || !out_key) return fail(SSBH_INVALID_ARGUMENT, "plan_run_host: null argument");
+    if (pl->streaming)
+        return fail(SSBH_INVALID_ARGUMENT, "plan_run_host: streaming plans take stream_begin/chunk/finish");
     CU(cudaSetDevice(pl->device));
     if (!pl->own_stream) CU(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
     const uint64_t in_w64 = words64(pl->p.n_rounds);
@@ -691,12 +711,16 @@ extern "C" ssbh_status ssbh_plan_run_host(ssbh_plan* pl, const uint64_t* input, 
         CU(pl->d_key.alloc(key_w64 * 8 + 16));
         CU(pl->d_len.alloc((size_t)pl->nown * 8 + 8));
     }
+    if (keep && !pl->d_keep.p) CU(pl->d_keep.alloc(in_w64 * 8 + 16));
     cudaStream_t st = pl->own_stream;
     CU(cudaMemcpyAsync(pl->d_input.p, input, in_w64 * 8, cudaMemcpyHostToDevice, st));
+    if (keep) CU(cudaMemcpyAsync(pl->d_keep.p, keep, in_w64 * 8, cudaMemcpyHostToDevice, st));
     // the key buffer's last u32 of an odd word count must read as zero in the u64 view
     if ((pl->key_words32 & 1) != 0) CU(cudaMemsetAsync(pl->d_key.p, 0, key_w64 * 8, st));
-    if (auto s = ssbh_plan_run_device(pl, pl->d_input.as<uint32_t>(), pl->d_key.as<uint32_t>(),
-                                      pl->d_len.as<uint64_t>(), nullptr, nullptr, st))
+    if (auto s = ssbh_plan_run_device_sifted(pl, pl->d_input.as<uint32_t>(),
+                                             keep ? pl->d_keep.as<uint32_t>() : nullptr,
+                                             pl->d_key.as<uint32_t>(), pl->d_len.as<uint64_t>(),
+                                             nullptr, nullptr, st))
         return s;
     if (auto s = ssbh_plan_check(pl, stats)) return s;
     CU(cudaMemcpyAsync(out_key, pl->d_key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));
@@ -710,9 +734,16 @@ extern "C" ssbh_status ssbh_plan_run_host(ssbh_plan* pl, const uint64_t* input, 
 extern "C" ssbh_status ssbh_extract(const ssbh_extract_params* params, const uint64_t* input,
                                     uint64_t* out_key, uint64_t* out_lengths,
                                     ssbh_extract_stats* stats) {
+    return ssbh_extract_sifted(params, input, nullptr, out_key, out_lengths, stats);
+}
+
+extern "C" ssbh_status ssbh_extract_sifted(const ssbh_extract_params* params,
+                                           const uint64_t* input, const uint64_t* keep,
+                                           uint64_t* out_key, uint64_t* out_lengths,
+                                           ssbh_extract_stats* stats) {
     ssbh_plan* pl = nullptr;
     if (auto s = ssbh_plan_create(params, &pl)) return s;
-    const ssbh_status s = ssbh_plan_run_host(pl, input, out_key, out_lengths, stats);
+    const ssbh_status s = ssbh_plan_run_host_sifted(pl, input, keep, out_key, out_lengths, stats);
     std::string msg = g_err;
     ssbh_plan_destroy(pl);
     g_err = msg;

@@ -83,8 +83,9 @@ struct SamplerGeom {
 SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,
                               bool has_keep, int max_chunk_shift = 40);
 // Pass 1: V_i (Threefry), payload, per-(chunk, owned block) counts (counts pre-zeroed).
+// d_keep: optional bit-packed sift mask (bit i = keep round i), like the reference's keep[i].
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
-                         const uint8_t* d_keep, void* d_payload, uint32_t* d_counts,
+                         const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st);
 // Pass 2: exclusive scan of counts along chunks (in place -> offsets), nj totals.
 void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d_gsum,

@@ -6,7 +6,7 @@
 //
 //  pass 1 (k_sample_count, int-ALU bound): V_i = uniform_below(s, i) from
 //      KeyedStream(seed, "sampling") — Threefry is counter based, so every round is
-//      independent. Emits a 2-byte payload V | x_i<<15 (4-byte when s > 2^15 or a keep
+//      independent. Emits a 2-byte payload V | x_i<<15 (4-byte when s >= 2^15 or a keep
 //      mask is given) and counts rounds per (warp-chunk, owned block) with
 //      __match_any_sync-aggregated atomics.
 //  pass 2 (k_scan_*, HBM/latency bound, tiny): exclusive scan of the count table along
@@ -54,7 +54,7 @@ struct PayloadBits<uint32_t> {
 template <typename P, bool kPow2>
 __device__ __forceinline__ uint32_t sample_group(const Key& key, uint64_t n, uint64_t s,
                                                  const uint32_t* __restrict__ in32,
-                                                 const uint8_t* __restrict__ keep, uint32_t j_lo,
+                                                 const uint32_t* __restrict__ keep32, uint32_t j_lo,
                                                  uint32_t nown, uint64_t g, uint32_t lane,
                                                  P* __restrict__ payload,
                                                  uint32_t* __restrict__ assign_out) {
@@ -71,11 +71,16 @@ __device__ __forceinline__ uint32_t sample_group(const Key& key, uint64_t n, uin
     uint32_t bit = 0;
     if (in32) bit = (__ldg(in32 + g) >> lane) & 1u;
     bool kept = valid;
-    if (keep && valid) kept = keep[i] != 0;
+    if (keep32 && valid) kept = ((__ldg(keep32 + g) >> lane) & 1u) != 0;
     if (valid) {
         if (payload) {
             uint32_t pv = v | (bit << B::kDataShift);
-            if (B::kKeepShift < 32 && !kept) pv |= 1u << (B::kKeepShift & 31);
+            if (!kept) {
+                if (B::kKeepShift < 32)
+                    pv |= 1u << (B::kKeepShift & 31);
+                else
+                    pv |= B::kVMask;  // u16 (s < 2^15): V = 0x7fff marks a sifted-out round
+            }
             payload[i] = (P)pv;
         }
         if (assign_out) assign_out[i] = v + 1;
@@ -90,7 +95,7 @@ __device__ __forceinline__ uint32_t sample_group(const Key& key, uint64_t n, uin
 template <typename P, bool kPow2>
 __global__ void __launch_bounds__(256) k_sample_count_rows(
     Key key, uint64_t n, uint64_t s, const uint32_t* __restrict__ in32,
-    const uint8_t* __restrict__ keep, uint32_t j_lo, uint32_t nown, int cs, uint64_t nchunks,
+    const uint32_t* __restrict__ keep, uint32_t j_lo, uint32_t nown, int cs, uint64_t nchunks,
     uint32_t parts, P* __restrict__ payload, uint32_t* __restrict__ counts,
     uint32_t* __restrict__ assign_out) {
     extern __shared__ uint32_t hist_all[];
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(256) k_sample_count_rows(
 template <typename P, bool kPow2>
 __global__ void __launch_bounds__(256) k_sample_count(Key key, uint64_t n, uint64_t s,
                                                       const uint32_t* __restrict__ in32,
-                                                      const uint8_t* __restrict__ keep,
+                                                      const uint32_t* __restrict__ keep,
                                                       uint32_t j_lo, uint32_t nown, int cs,
                                                       P* __restrict__ payload,
                                                       uint32_t* __restrict__ counts,
@@ -411,7 +416,8 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
     g.s = s;
     g.j_lo = j_lo;
     g.nown = nown;
-    g.payload_bytes = (!has_keep && s <= 32768) ? 2 : 4;
+    // u16 needs V <= 0x7ffe so that 0x7fff can mark sifted-out rounds
+    g.payload_bytes = (!has_keep && s < 32768) ? 2 : 4;
     // warp-chunk: enough chunks for latency hiding in the scatter pass, bounded count table
     int cs = 10;
     auto table_bytes = [&](int shift) {
@@ -431,7 +437,7 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
 
 template <typename P, bool kPow2>
 static void sample_count_t(const SamplerGeom& g, const Key& k, const uint32_t* d_in32,
-                           const uint8_t* d_keep, P* pl, uint32_t* d_counts,
+                           const uint32_t* d_keep, P* pl, uint32_t* d_counts,
                            uint32_t* d_assign_out, cudaStream_t st) {
     const uint64_t groups = (g.n + 31) / 32;
     const size_t row_bytes = (size_t)g.nown * 4;
@@ -460,7 +466,7 @@ static void sample_count_t(const SamplerGeom& g, const Key& k, const uint32_t* d
 }
 
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
-                         const uint8_t* d_keep, void* d_payload, uint32_t* d_counts,
+                         const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st) {
     if (g.n == 0) return;
     Key k;

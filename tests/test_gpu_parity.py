@@ -393,3 +393,23 @@ def test_config3_streaming_8_chunks_digest(dev, oracle, golden):
                               c["n"] // 8)
     assert int(nj.min()) == want["nj_min"] and int(nj.max()) == want["nj_max"]
     assert f"{oracle.fnv(got):016x}" == want["key_fnv"]
+
+
+# ------------------------------------------------------- sifted runs (keep flags)
+def test_extract_sifted_matches_oracle(dev, oracle):
+    rng = np.random.default_rng(21)
+    for n, s, k, pb, pk in ((300000, 16, 512, False, 0.5), (200000, 33, 96, True, 0.9),
+                            (150000, 5, 77, False, 0.2), (1 << 20, 32768, 64, False, 0.99)):
+        x = oracle.make_input(int(rng.integers(1000)), 0.5, n)
+        keep = (rng.random(n) < pk).astype(np.uint8)
+        keep_words = np.packbits(np.concatenate([keep, np.zeros((-n) % 64, np.uint8)]),
+                                 bitorder="little").view(np.uint64)
+        try:
+            want, wnj = oracle.extract_sifted(x, keep, n, s, 41, 42, pb, k)
+        except ValueError:
+            with pytest.raises(ValueError):  # an empty sifted sub-block, like ToeplitzSeed
+                dev.extract(x, n, s, k, 41, 42, per_block=pb, keep=keep_words)
+            continue
+        got, nj, _ = dev.extract(x, n, s, k, 41, 42, per_block=pb, keep=keep_words)
+        assert (nj == wnj).all()
+        assert (got == want).all(), (n, s, k, pb, pk)

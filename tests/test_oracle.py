@@ -168,6 +168,32 @@ def test_extract_selected_matches_full(oracle):
             assert (keys[q] == key[j * kw:(j + 1) * kw]).all()
 
 
+def test_extract_sifted_vs_reference_loop(oracle, reference):
+    # run_extraction's sift + per-block hash (pipeline.cpp:109-136) composed from the
+    # reference's own assign_subblocks / sift_partition / bits / toeplitz_hash
+    rng = np.random.default_rng(8)
+    for n, s, k, pb in ((30000, 4, 256, 1), (20000, 7, 100, 0)):
+        x = oracle.make_input(3, 0.5, n)
+        keep = rng.integers(0, 2, n).astype(np.uint8)
+        key, nj = oracle.extract_sifted(x, keep, n, s, 5, 6, pb, k)
+        a, _ = reference.assign_subblocks(n, s, 5)
+        off, idx, _ = reference.sift_partition(keep, a, s)
+        xbits = np.unpackbits(x.view(np.uint8), bitorder="little")
+        outbits = []
+        for j in range(s):
+            blk = idx[int(off[j]):int(off[j + 1])]
+            nb = len(blk)
+            assert nj[j] == nb
+            xb = np.packbits(np.concatenate([xbits[blk], np.zeros((-nb) % 64, np.uint8)]),
+                             bitorder="little").view(np.uint64)
+            seed = reference.bits(6, "hash-seed", j if pb else 0, k + nb - 1)
+            h = reference.toeplitz_hash(seed, k, nb, xb)
+            outbits.append(np.unpackbits(h.view(np.uint8), bitorder="little")[:k])
+        allb = np.concatenate(outbits)
+        got = np.unpackbits(key.view(np.uint8), bitorder="little")[: s * k]
+        assert (got == allb).all()
+
+
 def test_cycle_estimate(oracle, reference):
     assert oracle.cycle_estimate(123, 0, 2000) == (123, 0)
     assert oracle.cycle_estimate(2000, 2000, 2000) == (8000, 0)
