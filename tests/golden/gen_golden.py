@@ -38,6 +38,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config3", action="store_true")
     ap.add_argument("--config4", action="store_true")
+    ap.add_argument("--config5", action="store_true")
     ap.add_argument("--only-large", action="store_true", help="skip the small vectors")
     args = ap.parse_args()
     ref, o = Reference(), Oracle()
@@ -146,6 +147,25 @@ def main():
                                for q in range(len(which))],
             "ref_seconds": round(time.time() - t, 1)}
         print(4, ext["4"], flush=True)
+    if args.config5:
+        # config 5: 2^37 rounds (16 GiB input), s = 32768, shared seed, k = 2^21 —
+        # streaming with the reference's own KeyedStream / toeplitz_hash
+        n, s, k = 1 << 37, 32768, 1 << 21
+        which = [0, 32767]
+        x = o.make_input(1, 0.5, n)
+        t = time.time()
+        keys, nj = ref.extract_selected(x, n, s, 2, 3, 0, k, which)
+        ext["5"] = {
+            "n": n, "s": s, "k": k, "p": 0.5, "seed_in": 1, "seed_samp": 2, "seed_hash": 3,
+            "per_block": 0, "input_fnv": fnv(o, x), "nj_min": int(nj.min()),
+            "nj_max": int(nj.max()), "nj_0": int(nj[0]), "nj_last": int(nj[-1]),
+            "nj_fnv": fnv(o, nj), "which": which,
+            "block_fnv": [fnv(o, keys[q]) for q in range(len(which))],
+            "block_word0": [f"{int(keys[q][0]):016x}" for q in range(len(which))],
+            "block_popcount": [int(np.unpackbits(keys[q].view(np.uint8)).sum())
+                               for q in range(len(which))],
+            "ref_seconds": round(time.time() - t, 1)}
+        print(5, ext["5"], flush=True)
     g["extract"] = ext
     json.dump(g, open(OUT, "w"), indent=1)
     print("wrote", OUT)
