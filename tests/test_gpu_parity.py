@@ -395,6 +395,37 @@ def test_config3_streaming_8_chunks_digest(dev, oracle, golden):
     assert f"{oracle.fnv(got):016x}" == want["key_fnv"]
 
 
+# ------------------------------------------------ config 4 (per-block seeds, 2^34 rounds)
+@pytest.mark.slow
+def test_config4_full_blocks_vs_reference(dev, oracle, golden):
+    """BASELINE configs[3] on one GPU: all 16384 n_j and four sub-block keys against the
+    reference's own streaming computation (gen_golden.py --config4, ref_extract_selected)."""
+    import torch
+
+    want = golden["extract"].get("4")
+    if want is None:
+        pytest.skip("golden config-4 anchors not generated")
+    c = dev.CONFIGS[4]
+    n, s, k = c["n"], c["s"], c["k"]
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=True)
+    d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+    plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+    st = plan.check()
+    nj = d_len.cpu().numpy().view(np.uint64)
+    assert f"{oracle.fnv(nj):016x}" == want["nj_fnv"]
+    assert int(nj.min()) == want["nj_min"] and int(nj.max()) == want["nj_max"]
+    kw = k // 64
+    key64 = d_key.view(torch.int64)
+    for q, j in enumerate(want["which"]):
+        blk = key64[j * kw:(j + 1) * kw].cpu().numpy().view(np.uint64)
+        assert f"{oracle.fnv(blk):016x}" == want["block_fnv"][q], j
+    assert int(st.hash_word_ops) == n * k // 32
+    plan.close()
+
+
 # ------------------------------------------------------- sifted runs (keep flags)
 def test_extract_sifted_matches_oracle(dev, oracle):
     rng = np.random.default_rng(21)
