@@ -13,11 +13,15 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclu
 CU_SRCS  := $(CSRC)/prf.cu $(CSRC)/sampler.cu $(CSRC)/toeplitz.cu $(CSRC)/abi.cu $(CSRC)/diag.cu
 CU_HDRS  := $(CSRC)/common.cuh $(CSRC)/ptx.cuh $(CSRC)/internal.h include/ssbh_cuda.h
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
-HOST_SRCS:= $(wildcard $(CSRC)/host/*.cpp)
+HOST_SRCS:= $(CSRC)/host/ssbh_api.cpp
 HDRS_API := $(wildcard include/ssbh/*.hpp)
 CUDA_LIB := /usr/local/cuda/lib64
 
-all: $(PKG)/libssbh_cuda.so $(PKG)/libssbh.so oracle cpptests
+all: $(PKG)/libssbh_cuda.so $(PKG)/libssbh.so $(PKG)/ssbh-b200 oracle cpptests
+
+# CLI (file-mode extract + bench analogue of proj/tools/ssbh_main.cpp)
+$(PKG)/ssbh-b200: $(CSRC)/host/ssbh_cli.cpp $(HDRS_API) $(PKG)/libssbh.so
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(PKG) -lssbh -lssbh_cuda -Wl,-rpath,'$$ORIGIN'
 
 build/%.o: $(CSRC)/%.cu $(CU_HDRS)
 	@mkdir -p build

@@ -1,0 +1,213 @@
+// ssbh_cli.cpp — `ssbh-b200`, the B200 counterpart of the reference CLI's hot-path commands
+// (proj/tools/ssbh_main.cpp), on the drop-in API (libssbh.so -> libssbh_cuda.so):
+//
+//   ssbh-b200 extract --in FILE --in-bits N --out-bits L [--ns S] [--seed HEX64]
+//                     [--eps-abort E] [--out FILE] [--partition-csv FILE]
+//       file mode of cmd_extract (ssbh_main.cpp:306-345): the master seed keys both the
+//       sampling and the per-block "hash-seed" streams (sub = j), L/S bits per block, strict
+//       oversize abort against block_limit(N, 1/S, eps_abort, S) (N when S == 1).
+//   ssbh-b200 bench --sizes A,B,... [--ns S] [--seed HEX64] [--out-ratio R]
+//       cmd_bench (ssbh_main.cpp:368-426): direct hash of the whole input vs sub-block
+//       hashing, measured on the GPU, beside the FPGA cycle-model ratio
+//       (cycle_estimate / timing_model semantics, pipeline.cpp:142-163).
+//
+// Exit codes follow ssbh_main.cpp:26-33: 0 ok, 2 parse/invalid, 3 infeasible,
+// 4 oversize abort, 6 io; device failures exit 7.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "ssbh/bitstring.hpp"
+#include "ssbh/errors.hpp"
+#include "ssbh/extract.hpp"
+#include "ssbh/prf.hpp"
+#include "ssbh/sampling.hpp"
+#include "ssbh/toeplitz.hpp"
+
+using namespace ssbh;
+
+namespace {
+
+enum : int { kOk = 0, kParse = 2, kInfeasible = 3, kAbortOversize = 4, kIo = 6, kDevice = 7 };
+
+struct Args {
+    std::string cmd, in, out, partition_csv, seed_hex = std::string(64, '0');
+    std::uint64_t in_bits = 0, out_bits = 0;
+    std::uint32_t ns = 1;
+    double eps_abort = 1e-8, out_ratio = 0.06303;
+    std::vector<std::uint64_t> sizes;
+};
+
+std::uint64_t parse_u64(const std::string& s) {
+    std::size_t pos = 0;
+    const unsigned long long v = std::stoull(s, &pos);
+    if (pos != s.size()) throw std::invalid_argument("not an integer: " + s);
+    return v;
+}
+
+Args parse(int argc, char** argv) {
+    if (argc < 2) throw std::invalid_argument("usage: ssbh-b200 extract|bench [options]");
+    Args a;
+    a.cmd = argv[1];
+    for (int i = 2; i < argc; ++i) {
+        const std::string f = argv[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= argc) throw std::invalid_argument("missing value for " + f);
+            return argv[++i];
+        };
+        if (f == "--in") a.in = val();
+        else if (f == "--out") a.out = val();
+        else if (f == "--partition-csv") a.partition_csv = val();
+        else if (f == "--seed") a.seed_hex = val();
+        else if (f == "--in-bits") a.in_bits = parse_u64(val());
+        else if (f == "--out-bits") a.out_bits = parse_u64(val());
+        else if (f == "--ns") a.ns = static_cast<std::uint32_t>(parse_u64(val()));
+        else if (f == "--eps-abort") a.eps_abort = std::stod(val());
+        else if (f == "--out-ratio") a.out_ratio = std::stod(val());
+        else if (f == "--sizes") {
+            std::stringstream ss(val());
+            std::string tok;
+            while (std::getline(ss, tok, ',')) a.sizes.push_back(parse_u64(tok));
+        } else
+            throw std::invalid_argument("unknown flag " + f);
+    }
+    return a;
+}
+
+void emit(const std::string& path, const std::string& text) {
+    if (path.empty()) {
+        std::fwrite(text.data(), 1, text.size(), stdout);
+        return;
+    }
+    std::ofstream o(path, std::ios::binary);
+    if (!o) throw io_error("cannot open output: " + path);
+    o << text;
+}
+
+int cmd_extract(const Args& a) {
+    if (a.in.empty() || a.in_bits == 0)
+        throw std::invalid_argument("extract: need --in with --in-bits");
+    if (a.out_bits == 0) throw std::invalid_argument("extract: file mode needs --out-bits");
+    if (a.ns == 0) throw std::invalid_argument("assign_subblocks: n_subblocks must be positive");
+    const MasterSeed seed = MasterSeed::from_hex(a.seed_hex);
+    const BitString data = BitString::read_file(a.in, a.in_bits);
+    const std::uint64_t limit =
+        a.ns == 1 ? a.in_bits
+                  : block_limit(a.in_bits, 1.0 / static_cast<double>(a.ns), a.eps_abort, a.ns);
+    std::string report = "# b200: seed " + seed.to_hex() + ", ns " + std::to_string(a.ns) + "\n";
+    report += "mode: file\n";
+    report += "block_limit: " + std::to_string(limit) + "\n";
+    ExtractOptions opt;
+    opt.seed_mode = SeedMode::PerBlock;  // KeyedStream(seed, "hash-seed", j)
+    opt.block_limit = limit;
+    const auto t0 = std::chrono::steady_clock::now();
+    const ExtractResult r = extract(data, a.ns, a.out_bits / a.ns, seed, seed, opt);
+    const double secs =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (!a.partition_csv.empty()) {
+        const Partition part = assign_subblocks(a.in_bits, a.ns, seed);
+        std::string dump = "round_index,v_i,kept\n";
+        for (std::uint64_t i = 0; i < a.in_bits; ++i)
+            dump += std::to_string(i) + "," + std::to_string(part.assignment[i]) + ",1\n";
+        emit(a.partition_csv, dump);
+    }
+    if (r.aborted) {
+        report += "abort: oversize_block\n";
+        emit("", report);
+        return kAbortOversize;
+    }
+    report += "key_length_bits: " + std::to_string(r.key.size()) + "\n";
+    report += "hash_seconds: " + std::to_string(secs) + "\n";
+    report += "device_ms: " + std::to_string(r.device_ms) + "\n";
+    if (!a.out.empty()) r.key.write_file(a.out);
+    emit("", report);
+    return kOk;
+}
+
+// FPGA cycle model of the reference (pipeline.cpp:142-163): full vs splitting(ns), padded
+// to the abort limit.
+std::uint64_t model_cycles(std::uint64_t in, std::uint64_t out, std::uint32_t ns, double eps) {
+    const BlockingParams blk;
+    if (ns == 1) return cycle_estimate(in, out, blk.m_prime);
+    const std::uint64_t limit = block_limit(in, 1.0 / ns, eps, ns);
+    return ns * cycle_estimate(limit, (out + ns - 1) / ns, blk.m_prime);
+}
+
+int cmd_bench(const Args& a) {
+    if (a.sizes.empty()) throw std::invalid_argument("bench: --sizes required");
+    const MasterSeed seed = MasterSeed::from_hex(a.seed_hex);
+    std::string out = "size_bits,full_seconds,split_seconds,measured_ratio,modeled_ratio\n";
+    for (const std::uint64_t size : a.sizes) {
+        if (size == 0) throw std::invalid_argument("bench: sizes must be positive");
+        const std::uint64_t m_full =
+            std::max<std::uint64_t>(1, static_cast<std::uint64_t>(size * a.out_ratio));
+        const BitString input = KeyedStream(seed, "bench-input").bits(size);
+        const ToeplitzSeed fseed(KeyedStream(seed, "bench-seed-full").bits(m_full + size - 1),
+                                 m_full, size);
+        (void)toeplitz_hash(fseed, input);  // warm-up (module load, allocator)
+        auto t0 = std::chrono::steady_clock::now();
+        const BitString full = toeplitz_hash(fseed, input);
+        const double full_s =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        // split: partition + gather + per-block seeds untimed (ssbh_main.cpp:388-404), then
+        // the hashing of every block timed — one batched launch on the GPU (:405-410)
+        const std::uint64_t m_block = std::max<std::uint64_t>(1, m_full / a.ns);
+        const Partition part = assign_subblocks(size, a.ns, seed);
+        const SiftedPartition sifted =
+            sift_partition(std::vector<std::uint8_t>(size, 1), part);
+        std::vector<BitString> inputs(a.ns);
+        std::vector<ToeplitzSeed> seeds;
+        for (std::uint32_t j = 0; j < a.ns; ++j) {
+            inputs[j] = BitString(sifted.blocks[j].size());
+            for (std::uint64_t q = 0; q < sifted.blocks[j].size(); ++q)
+                if (input.get(sifted.blocks[j][q])) inputs[j].set(q, true);
+            seeds.emplace_back(KeyedStream(seed, "hash-seed", j).bits(m_block + inputs[j].size() - 1),
+                               m_block, inputs[j].size());
+        }
+        (void)toeplitz_hash_batch(seeds, inputs);  // warm-up
+        t0 = std::chrono::steady_clock::now();
+        const BitString split = toeplitz_hash_batch(seeds, inputs);
+        const double split_s =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        (void)split;
+        const double modeled = static_cast<double>(model_cycles(size, m_full, 1, a.eps_abort)) /
+                               static_cast<double>(model_cycles(size, m_block * a.ns, a.ns,
+                                                                a.eps_abort));
+        char line[256];
+        std::snprintf(line, sizeof line, "%llu,%.6g,%.6g,%.6g,%.6g\n",
+                      static_cast<unsigned long long>(size), full_s, split_s, full_s / split_s,
+                      modeled);
+        out += line;
+        (void)full;
+    }
+    emit(a.out, out);
+    return kOk;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    try {
+        const Args a = parse(argc, argv);
+        if (a.cmd == "extract") return cmd_extract(a);
+        if (a.cmd == "bench") return cmd_bench(a);
+        throw std::invalid_argument("unknown command " + a.cmd);
+    } catch (const infeasible_error& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return kInfeasible;
+    } catch (const io_error& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return kIo;
+    } catch (const device_error& e) {
+        std::fprintf(stderr, "device error: %s\n", e.what());
+        return kDevice;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return kParse;
+    }
+}

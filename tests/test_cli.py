@@ -1,0 +1,101 @@
+"""The `ssbh-b200` CLI (paper_2308_02856_b200/csrc/host/ssbh_cli.cpp) against the reference's
+file-mode semantics (proj/tools/ssbh_main.cpp:306-345; proj/tests/test_cli.cpp:162-224):
+one master seed keys sampling and the per-block hash seeds (sub = j), L/ns output bits per
+block, raw-bit files LSB first, strict oversize abort with exit code 4, partition CSV."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_2308_02856_b200", "ssbh-b200")
+SEED_HEX = "00000000000000000000000000000000000000000000000000000000000000" + "2a"
+SEED_KEY = [0, 0, 0, 0x2A]
+
+
+def run(*args, cwd):
+    return subprocess.run([CLI, *args], capture_output=True, text=True, cwd=cwd, timeout=600)
+
+
+def write_bits(path, words, nbits):
+    b = np.ascontiguousarray(words, dtype=np.uint64).view(np.uint8)[: (nbits + 7) // 8]
+    with open(path, "wb") as f:
+        f.write(b.tobytes())
+
+
+def read_bits(path, nbits):
+    raw = np.fromfile(path, dtype=np.uint8)
+    assert len(raw) == (nbits + 7) // 8
+    pad = np.zeros(((len(raw) + 7) // 8) * 8, np.uint8)
+    pad[: len(raw)] = raw
+    return pad.view(np.uint64)
+
+
+def test_cli_parse_and_io_errors(tmp_path):
+    assert run("nope", cwd=tmp_path).returncode == 2
+    assert run("extract", "--in", "x", cwd=tmp_path).returncode == 2  # --in-bits missing
+    r = run("extract", "--in", str(tmp_path / "missing.bin"), "--in-bits", "64",
+            "--out-bits", "8", cwd=tmp_path)
+    assert r.returncode == 6
+
+
+@pytest.mark.gpu
+def test_cli_file_mode_matches_oracle(tmp_path, oracle):
+    n, ns, L = 1 << 20, 64, 64 * 8192
+    x = oracle.make_input(5, 0.5, n)
+    write_bits(tmp_path / "in.bin", x, n)
+    r = run("extract", "--in", "in.bin", "--in-bits", str(n), "--out-bits", str(L), "--ns",
+            str(ns), "--seed", SEED_HEX, "--out", "key.bin", cwd=tmp_path)
+    assert r.returncode == 0, r.stderr
+    rep = dict(l.split(": ", 1) for l in r.stdout.splitlines() if ": " in l and l[0] != "#")
+    limit, err = oracle.block_limit(n, 1 / ns, 1e-8, ns)
+    assert err == 0 and int(rep["block_limit"]) == limit
+    assert int(rep["key_length_bits"]) == L
+    key = read_bits(tmp_path / "key.bin", L)
+    want, _ = oracle.extract(x, n, ns, SEED_KEY, SEED_KEY, 1, L // ns)
+    assert (key[: len(want)] == want).all()
+    # single block: the whole string hashed with hash-seed sub 0 (test_cli.cpp:162-181)
+    r = run("extract", "--in", "in.bin", "--in-bits", "100000", "--out-bits", "3000",
+            "--seed", SEED_HEX, "--out", "key1.bin", cwd=tmp_path)
+    assert r.returncode == 0, r.stderr
+    x1 = oracle.make_input(5, 0.5, n)
+    x1 = np.unpackbits(x1.view(np.uint8), bitorder="little")[:100000]
+    x1w = np.packbits(np.concatenate([x1, np.zeros((-100000) % 64, np.uint8)]),
+                      bitorder="little").view(np.uint64)
+    seed = oracle.bits(SEED_KEY, "hash-seed", 0, 3000 + 100000 - 1)
+    assert (read_bits(tmp_path / "key1.bin", 3000)[:47] == oracle.toeplitz_hash(seed, 3000, 100000,
+                                                                                x1w)).all()
+
+
+@pytest.mark.gpu
+def test_cli_abort_and_partition_csv(tmp_path, oracle):
+    n, ns = 50000, 8
+    x = oracle.make_input(6, 0.5, n)
+    write_bits(tmp_path / "in.bin", x, n)
+    # a loose abort budget puts the limit near the mean: some block overflows -> exit 4
+    r = run("extract", "--in", "in.bin", "--in-bits", str(n), "--out-bits", "800", "--ns",
+            str(ns), "--seed", SEED_HEX, "--eps-abort", "0.999", "--out", "k.bin",
+            "--partition-csv", "part.csv", cwd=tmp_path)
+    limit, _ = oracle.block_limit(n, 1 / ns, 0.999, ns)
+    a, counts = oracle.assign_subblocks(n, ns, SEED_KEY)
+    if int(counts.max()) > limit:
+        assert r.returncode == 4 and "abort: oversize_block" in r.stdout
+        assert not (tmp_path / "k.bin").exists()
+    else:
+        assert r.returncode == 0
+    rows = (tmp_path / "part.csv").read_text().splitlines()
+    assert rows[0] == "round_index,v_i,kept" and len(rows) == n + 1
+    assert all(int(rows[1 + i].split(",")[1]) == int(a[i]) for i in range(0, n, 997))
+
+
+@pytest.mark.gpu
+def test_cli_bench_runs(tmp_path):
+    r = run("bench", "--sizes", "20000000,40000000", "--ns", "16", "--seed", SEED_HEX,
+            cwd=tmp_path)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0] == "size_bits,full_seconds,split_seconds,measured_ratio,modeled_ratio"
+    for ln in lines[1:]:
+        size, full_s, split_s, meas, model = ln.split(",")
+        assert float(meas) > 1.0 and float(model) > 1.0
