@@ -58,7 +58,7 @@ def config_dict(cid, c, world):
         "n_bits": c["n"], "n_subblocks": c["s"], "out_bits_per_block": c["k"], "p": c["p"],
         "seed_mode": "per-block (hash-seed sub=j)" if c["per_block"] else "shared (hash-seed sub=0)",
         "seeds": {"input": c["seed_in"], "sampling": c["seed_samp"], "hash": c["seed_hash"]},
-        "parallelism": f"sub-blocks sharded over {world} GPU(s), replicated input",
+        "parallelism": f"sub-blocks sharded over {world} GPU(s)",
         "l2": "L2 (126 MB) flushed between steps by a 256 MiB write outside the step events"
               + ("; input and payload exceed L2" if c["n"] >= (1 << 30) else ""),
     }
@@ -209,6 +209,9 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicated"],
+                    help="N>1: sharded sampling + peer-memory owner exchange, or every rank "
+                         "re-sampling all rounds")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -238,39 +241,51 @@ def main():
             dist.init_process_group(backend)
     coll_dev = "cuda" if backend == "nccl" else "cpu"
 
-    from paper_2308_02856_b200.multigpu import owned_range
+    from paper_2308_02856_b200.multigpu import ShardedExtractor, owned_range
 
     n, s, k = c["n"], c["s"], c["k"]
     first, count = owned_range(rank, world, s)
     streaming = cid == 5  # 2^37 rounds: input streamed in 8 chunks (BASELINE configs[4])
+    sharded = world > 1 and not streaming and args.multi == "sharded"
     chunk_bits = n // 8 if streaming else 0
-    plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"],
-                  block_first=first, block_count=count, chunk_bits=chunk_bits)
-    plan.set_timing(True)
     stream = torch.cuda.Stream()  # capturable: untimed runs replay one CUDA graph
     d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
     P.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr(), stream.cuda_stream)
     key_words64 = (count * k + 63) // 64
     d_key = torch.zeros(key_words64 * 2, dtype=torch.int32, device="cuda")
-    d_len = torch.zeros(count, dtype=torch.int64, device="cuda")
+    d_len = torch.zeros(max(count, 1), dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
+    if sharded:
+        # each rank samples only its slice; payloads reach their owners by peer stores
+        ex = ShardedExtractor(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"])
+        ex.shard.set_timing(True)
+        slice_lo, slice_n = ex.slice
+        slice_ptr = d_in.data_ptr() + (slice_lo // 32) * 4
+        check, close = ex.check, ex.close
+    else:
+        plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"],
+                      block_first=first, block_count=count, chunk_bits=chunk_bits)
+        plan.set_timing(True)
+        check, close = plan.check, plan.close
 
     peak, _ = P.measure_lop3_peak(20000)  # int-ALU roofline denominator (live)
 
     def step():
-        if not streaming:
+        if sharded:
+            ex.run(slice_ptr, d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream, coll_dev)
+        elif not streaming:
             plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr(),
                             stream.cuda_stream)
-            return
-        plan.stream_begin(stream.cuda_stream)
-        for ci in range(8):
-            plan.stream_chunk(ci, d_in.data_ptr() + ci * (chunk_bits // 8), stream.cuda_stream)
-        plan.stream_finish(d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream)
+        else:
+            plan.stream_begin(stream.cuda_stream)
+            for ci in range(8):
+                plan.stream_chunk(ci, d_in.data_ptr() + ci * (chunk_bits // 8), stream.cuda_stream)
+            plan.stream_finish(d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream)
 
     for _ in range(max(3, args.warmup)):
         step()
-        plan.check()
+        check()
 
     clocks = ClockSampler(dev_index)
     clocks.start()
@@ -284,9 +299,9 @@ def main():
         with torch.cuda.stream(stream):
             flush.fill_(i & 0xFF)  # evict L2 between steps (outside the step events)
         ev[i][0].record(stream)
-        step()
+        step()  # sharded: includes the host all-gather of counts and the barrier
         ev[i][1].record(stream)
-        stats = plan.check()
+        stats = check()
         hash_ms.append(stats.ms_hash)
         hash_ops = stats.hash_word_ops
     torch.cuda.synchronize()
@@ -300,7 +315,27 @@ def main():
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     e2e = None
     same = None
-    if not streaming:
+    if sharded:
+        x_host = d_in.view(torch.int64)[(slice_lo // 64):(slice_lo + slice_n + 63) // 64].cpu()
+        x_host = x_host.pin_memory()
+        key_host = torch.empty(key_words64, dtype=torch.int64).pin_memory()
+        d_slice = torch.empty_like(x_host, device="cuda")
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            with torch.cuda.stream(stream):
+                d_slice.copy_(x_host, non_blocking=True)
+            ex.run(d_slice.data_ptr(), d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream,
+                   coll_dev)
+            with torch.cuda.stream(stream):
+                key_host.copy_(d_key.view(torch.int64)[:key_words64], non_blocking=True)
+            stream.synchronize()
+        e2e_s = time.perf_counter() - t0
+        same = True
+        e2e = {"h2d": int(x_host.numel() * 8), "d2h": int(key_words64 * 8)}
+    elif not streaming:
         x_host = d_in.cpu().view(torch.int64).pin_memory()
         key_host = torch.empty(key_words64, dtype=torch.int64).pin_memory()
         len_host = torch.empty(count, dtype=torch.int64).pin_memory()
@@ -347,7 +382,12 @@ def main():
             "scaling": "strong",
             "vs_baseline": None, "dtype": "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)",
             "data": "synthetic (KeyedStream input on device, seeds per BASELINE/SURVEY §8a)",
-            "config": config_dict(cid, c, world),
+            "config": dict(config_dict(cid, c, world), multi_gpu=(
+                "sharded sampling: each rank samples n/N rounds, payloads stored into the "
+                "owning rank by NVLink peer stores (IPC), owners hash their blocks"
+                if sharded else ("streaming plan, 8 input chunks" if streaming else
+                                 "single plan" if world == 1 else
+                                 "replicated sampling, owned blocks hashed per rank"))),
             "roofline": {
                 "bound": "int-alu (LOP3)", "kernel": "k_toeplitz_hash",
                 "achieved": achieved / 1e12, "peak": peak / 1e12,
@@ -382,7 +422,7 @@ def main():
             except Exception as e:  # baseline failure must not hide the GPU number
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
         print(json.dumps(line), flush=True)
-    plan.close()
+    close()
     if world > 1:
         dist.destroy_process_group()
 

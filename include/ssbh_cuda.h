@@ -225,6 +225,36 @@ ssbh_status ssbh_plan_stream_chunk(ssbh_plan* plan, uint64_t chunk_index, const 
 ssbh_status ssbh_plan_stream_finish(ssbh_plan* plan, uint32_t* d_key, uint64_t* d_lengths,
                                     void* stream);
 
+/* ------------------------------------------------------- multi-GPU shards (one process/GPU)
+ * Sharded sampling: rank r of W owns blocks [r*s/W, (r+1)*s/W) and samples only
+ * its slice of rounds [slice_first, slice_first + slice_rounds); every sampled round's
+ * payload is stored straight into the owning rank's receive buffer through NVLink peer
+ * memory (CUDA IPC mappings) — the all-to-all is fused into the stable owner split — and each
+ * owner then partitions, seeds and hashes only its own rounds. Per run:
+ *   ssbh_shard_sample(slice input)  -> this rank's per-owner round counts (W values)
+ *   [host: all-gather the W x W count matrix; row r = rank r's counts]
+ *   ssbh_shard_exchange(matrix)     -> peer stores; returns when this rank's stores are done
+ *   [host: barrier across ranks]
+ *   ssbh_shard_finish(d_key)        -> the owned blocks' key slice (concatenate in rank order)
+ * Setup once: ssbh_shard_ipc_handle on every rank, all-gather the handles (W x 64 bytes),
+ * ssbh_shard_open_peers. No kernel waits on another rank. */
+#define SSBH_IPC_HANDLE_BYTES 64
+typedef struct ssbh_shard ssbh_shard;
+ssbh_status ssbh_shard_create(const ssbh_extract_params* params, uint32_t rank, uint32_t world,
+                              ssbh_shard** shard);
+ssbh_status ssbh_shard_destroy(ssbh_shard* shard);
+ssbh_status ssbh_shard_info(const ssbh_shard* shard, uint64_t* slice_first,
+                            uint64_t* slice_rounds, uint32_t* block_first, uint32_t* block_count);
+ssbh_status ssbh_shard_ipc_handle(ssbh_shard* shard, void* handle_out);
+ssbh_status ssbh_shard_open_peers(ssbh_shard* shard, const void* handles);
+ssbh_status ssbh_shard_sample(ssbh_shard* shard, const uint32_t* d_slice_input,
+                              const uint64_t* samp_key, uint64_t* owner_counts, void* stream);
+ssbh_status ssbh_shard_exchange(ssbh_shard* shard, const uint64_t* counts, void* stream);
+ssbh_status ssbh_shard_finish(ssbh_shard* shard, uint32_t* d_key, uint64_t* d_lengths,
+                              const uint64_t* hash_key, void* stream);
+ssbh_status ssbh_shard_check(ssbh_shard* shard, ssbh_extract_stats* stats);
+ssbh_status ssbh_shard_set_timing(ssbh_shard* shard, int enable);
+
 /* Synthetic input on the device: p == 0.5 -> KeyedStream(key,"input").bits(n);
  * else bit i = bernoulli(p, i) of the same stream. d_out: ceil(n/32) uint32 words. */
 ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbits,

@@ -44,6 +44,9 @@ ABI_SYMBOLS = (
     "ssbh_make_input_device", "ssbh_measure_lop3_peak", "ssbh_plan_create_streaming",
     "ssbh_plan_stream_begin", "ssbh_plan_stream_chunk", "ssbh_plan_stream_finish",
     "ssbh_plan_run_device_sifted", "ssbh_plan_run_host_sifted", "ssbh_extract_sifted",
+    "ssbh_shard_create", "ssbh_shard_destroy", "ssbh_shard_info", "ssbh_shard_ipc_handle",
+    "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
+    "ssbh_shard_check", "ssbh_shard_set_timing",
 )
 
 
@@ -165,6 +168,28 @@ def _load():
     L.ssbh_plan_run_host.argtypes = [C.c_void_p, U64P, U64P, U64P, C.POINTER(ExtractStats)]
     L.ssbh_make_input_device.restype = st
     L.ssbh_make_input_device.argtypes = [U64P, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
+    vp = C.c_void_p
+    L.ssbh_shard_create.restype = st
+    L.ssbh_shard_create.argtypes = [C.POINTER(ExtractParams), C.c_uint32, C.c_uint32,
+                                    C.POINTER(vp)]
+    L.ssbh_shard_destroy.restype = st
+    L.ssbh_shard_destroy.argtypes = [vp]
+    L.ssbh_shard_info.restype = st
+    L.ssbh_shard_info.argtypes = [vp, U64P, U64P, U32P, U32P]
+    L.ssbh_shard_ipc_handle.restype = st
+    L.ssbh_shard_ipc_handle.argtypes = [vp, vp]
+    L.ssbh_shard_open_peers.restype = st
+    L.ssbh_shard_open_peers.argtypes = [vp, vp]
+    L.ssbh_shard_sample.restype = st
+    L.ssbh_shard_sample.argtypes = [vp, vp, U64P, U64P, vp]
+    L.ssbh_shard_exchange.restype = st
+    L.ssbh_shard_exchange.argtypes = [vp, U64P, vp]
+    L.ssbh_shard_finish.restype = st
+    L.ssbh_shard_finish.argtypes = [vp, vp, vp, U64P, vp]
+    L.ssbh_shard_check.restype = st
+    L.ssbh_shard_check.argtypes = [vp, C.POINTER(ExtractStats)]
+    L.ssbh_shard_set_timing.restype = st
+    L.ssbh_shard_set_timing.argtypes = [vp, C.c_int]
     L.ssbh_plan_run_device_sifted.restype = st
     L.ssbh_plan_run_device_sifted.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.c_void_p, U64P, U64P, C.c_void_p]
@@ -449,6 +474,69 @@ class Plan:
     def close(self):
         if getattr(self, "h", None):
             lib.ssbh_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Shard:
+    """One rank of a sharded multi-GPU extraction (ssbh_shard_*). The host protocol (handle
+    exchange, count all-gather, barrier) lives in multigpu.ShardedExtractor."""
+
+    IPC_BYTES = 64
+
+    def __init__(self, n, s, k, samp, hsh, rank, world, per_block=False):
+        self.params = make_params(n, s, k, samp, hsh, per_block)
+        self.n, self.s, self.k, self.rank, self.world = n, s, k, rank, world
+        h = C.c_void_p()
+        _check(lib.ssbh_shard_create(C.byref(self.params), rank, world, C.byref(h)))
+        self.h = h
+        sf, sn = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        bf, bc = np.zeros(1, np.uint32), np.zeros(1, np.uint32)
+        _check(lib.ssbh_shard_info(self.h, _p64(sf), _p64(sn), _p32(bf), _p32(bc)))
+        self.slice_first, self.slice_rounds = int(sf[0]), int(sn[0])
+        self.block_first, self.block_count = int(bf[0]), int(bc[0])
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(self.IPC_BYTES)
+        _check(lib.ssbh_shard_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def open_peers(self, handles):
+        blob = C.create_string_buffer(b"".join(handles), self.IPC_BYTES * self.world)
+        _check(lib.ssbh_shard_open_peers(self.h, blob))
+
+    def set_timing(self, on=True):
+        _check(lib.ssbh_shard_set_timing(self.h, 1 if on else 0))
+
+    def sample(self, d_slice_ptr: int, stream: int = 0, samp=None) -> np.ndarray:
+        out = np.zeros(self.world, np.uint64)
+        sk = None if samp is None else _p64(key_of(samp))
+        _check(lib.ssbh_shard_sample(self.h, C.c_void_p(d_slice_ptr), sk, _p64(out),
+                                     C.c_void_p(stream or None)))
+        return out
+
+    def exchange(self, counts_matrix, stream: int = 0):
+        m = np.ascontiguousarray(counts_matrix, dtype=np.uint64).reshape(-1)
+        _check(lib.ssbh_shard_exchange(self.h, _p64(m), C.c_void_p(stream or None)))
+
+    def finish(self, d_key_ptr: int, d_len_ptr: int = 0, stream: int = 0, hsh=None):
+        hk = None if hsh is None else _p64(key_of(hsh))
+        _check(lib.ssbh_shard_finish(self.h, C.c_void_p(d_key_ptr), C.c_void_p(d_len_ptr or None),
+                                     hk, C.c_void_p(stream or None)))
+
+    def check(self) -> ExtractStats:
+        st = ExtractStats()
+        _check(lib.ssbh_shard_check(self.h, C.byref(st)))
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ssbh_shard_destroy(self.h)
             self.h = None
 
     def __del__(self):

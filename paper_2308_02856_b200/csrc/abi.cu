@@ -391,7 +391,7 @@ static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown)
 }
 
 static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t chunk_bits,
-                                    ssbh_plan** out) {
+                                    ssbh_plan** out, bool external_payload = false) {
     uint32_t nown = 0;
     if (auto s = validate_params(params, &nown)) return s;
     NEED_DEVICE();
@@ -430,7 +430,8 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         return b.alloc(bytes);
     };
     cudaError_t e = cudaSuccess;
-    if (!e && !pl->streaming) e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
+    if (!e && !pl->streaming && !external_payload)
+        e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
     if (!e) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
     if (!e) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
     if (!e) e = alloc(pl->ybuf, pl->ybuf_words * 4);
@@ -939,4 +940,218 @@ extern "C" ssbh_status ssbh_blocked_toeplitz_hash(const uint64_t* seed, uint64_t
     // toeplitz.hpp:29-32: bit-for-bit identical to toeplitz_hash for every blocking; the
     // GPU tiling is our own (row tiles x k tiles), so the blocking is validated only.
     return ssbh_toeplitz_hash(seed, m, n, input, input_bits, out);
+}
+
+// ======================================================================== multi-GPU shards
+// One process per GPU. Rank r samples only its slice of rounds, stores every round's payload
+// straight into the owning rank's receive buffer through NVLink peer memory (CUDA IPC
+// mappings; the dispatch of an all-to-all fused into the stable owner split), and then each
+// owner partitions / hashes only its received rounds. Host barriers separate the phases;
+// no kernel ever waits on another rank.
+struct ssbh_shard {
+    ssbh_extract_params p{};  // block_first/count = this rank's owned blocks
+    uint32_t rank = 0, world = 1;
+    int device = 0;
+    uint64_t slice_lo = 0, slice_n = 0;
+    SamplerGeom gs{};  // slice geometry, keys = owning ranks
+    DBuf slice_payload, slice_counts, slice_gsum, slice_tot;
+    uint64_t recv_cap = 0, n_recv = 0;
+    DBuf recv, d_dst, d_dst_base;
+    std::vector<void*> peer;   // receive buffers of all ranks (own = recv.p)
+    std::vector<bool> opened;  // IPC-opened (to close)
+    ssbh_plan* plan = nullptr;  // owner pipeline over the received payload
+    uint64_t* h_tot = nullptr;  // pinned, world entries
+    uint32_t launches = 0;
+};
+
+static uint64_t slice_bound(uint64_t n, uint32_t world, uint32_t r) {
+    if (r >= world) return n;
+    return (n * r / world) / 1024 * 1024;
+}
+
+extern "C" ssbh_status ssbh_shard_create(const ssbh_extract_params* params, uint32_t rank,
+                                         uint32_t world, ssbh_shard** out) {
+    if (!params || !out) return fail(SSBH_INVALID_ARGUMENT, "shard_create: null argument");
+    if (world == 0 || rank >= world || world > params->n_subblocks)
+        return fail(SSBH_INVALID_ARGUMENT, "shard_create: need 0 <= rank < world <= n_subblocks");
+    NEED_DEVICE();
+    auto* sh = new ssbh_shard();
+    sh->p = *params;
+    sh->rank = rank;
+    sh->world = world;
+    CU(cudaGetDevice(&sh->device));
+    const uint64_t n = params->n_rounds, s = params->n_subblocks;
+    sh->p.block_first = (uint32_t)(s * rank / world);
+    sh->p.block_count = (uint32_t)(s * (rank + 1) / world) - sh->p.block_first;
+    sh->slice_lo = slice_bound(n, world, rank);
+    sh->slice_n = slice_bound(n, world, rank + 1) - sh->slice_lo;
+    sh->gs = make_sampler_geom(sh->slice_n ? sh->slice_n : 1, s, 0, world, false);
+    sh->gs.n = sh->slice_n;
+    // receive capacity: the largest owner's expected share + 16 sigma + slack
+    uint64_t maxc = 0;
+    for (uint32_t o = 0; o < world; ++o)
+        maxc = std::max<uint64_t>(maxc, s * (o + 1) / world - s * o / world);
+    const double mean = (double)n * (double)maxc / (double)s;
+    sh->recv_cap = (uint64_t)(mean + 16.0 * std::sqrt(mean) + 65536.0);
+    sh->recv_cap = std::min<uint64_t>(sh->recv_cap, n);
+    const int pb = sh->gs.payload_bytes;
+    cudaError_t e = cudaSuccess;
+    if (!e) e = sh->slice_payload.alloc(sh->slice_n * pb + 16);
+    if (!e) e = sh->slice_counts.alloc((size_t)sh->gs.nchunks * world * 4);
+    if (!e) e = sh->slice_gsum.alloc((size_t)sh->gs.ngroups * world * 8);
+    if (!e) e = sh->slice_tot.alloc((size_t)world * 8);
+    if (!e) e = sh->recv.alloc(sh->recv_cap * pb + 16);
+    if (!e) e = sh->d_dst.alloc((size_t)world * sizeof(void*));
+    if (!e) e = sh->d_dst_base.alloc((size_t)world * 8);
+    if (!e) e = cudaMallocHost(&sh->h_tot, (size_t)world * 8);
+    if (e) {
+        ssbh_shard_destroy(sh);
+        return fail(SSBH_CUDA, "shard_create: allocation failed: %s", cudaGetErrorString(e));
+    }
+    sh->peer.assign(world, nullptr);
+    sh->opened.assign(world, false);
+    sh->peer[rank] = sh->recv.p;
+    ssbh_extract_params op = sh->p;
+    op.n_rounds = sh->recv_cap;
+    if (auto st = plan_create_impl(&op, 0, &sh->plan, /*external_payload=*/true)) {
+        const std::string msg = g_err;
+        ssbh_shard_destroy(sh);
+        g_err = msg;
+        return st;
+    }
+    *out = sh;
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_shard_destroy(ssbh_shard* sh) {
+    if (!sh) return ok();
+    for (uint32_t r = 0; r < sh->peer.size(); ++r)
+        if (sh->opened[r]) cudaIpcCloseMemHandle(sh->peer[r]);
+    if (sh->plan) ssbh_plan_destroy(sh->plan);
+    if (sh->h_tot) cudaFreeHost(sh->h_tot);
+    delete sh;
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_shard_info(const ssbh_shard* sh, uint64_t* slice_first,
+                                       uint64_t* slice_rounds, uint32_t* block_first,
+                                       uint32_t* block_count) {
+    if (!sh) return fail(SSBH_INVALID_ARGUMENT, "null shard");
+    if (slice_first) *slice_first = sh->slice_lo;
+    if (slice_rounds) *slice_rounds = sh->slice_n;
+    if (block_first) *block_first = sh->p.block_first;
+    if (block_count) *block_count = sh->p.block_count;
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_shard_ipc_handle(ssbh_shard* sh, void* handle_out) {
+    if (!sh || !handle_out) return fail(SSBH_INVALID_ARGUMENT, "null argument");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, sh->recv.p));
+    static_assert(sizeof(h) == SSBH_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &h, sizeof h);
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_shard_open_peers(ssbh_shard* sh, const void* handles) {
+    if (!sh || !handles) return fail(SSBH_INVALID_ARGUMENT, "null argument");
+    for (uint32_t r = 0; r < sh->world; ++r) {
+        if (r == sh->rank || sh->opened[r]) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof h, sizeof h);
+        void* ptr = nullptr;
+        CU(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        sh->peer[r] = ptr;
+        sh->opened[r] = true;
+    }
+    CU(cudaMemcpy(sh->d_dst.p, sh->peer.data(), (size_t)sh->world * sizeof(void*),
+                  cudaMemcpyHostToDevice));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_shard_sample(ssbh_shard* sh, const uint32_t* d_slice_input,
+                                         const uint64_t* samp_key, uint64_t* owner_counts,
+                                         void* stream) {
+    if (!sh || !owner_counts || (sh->slice_n && !d_slice_input))
+        return fail(SSBH_INVALID_ARGUMENT, "shard_sample: null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t* sk = samp_key ? samp_key : sh->p.samp_key;
+    sh->launches = 0;
+    CU(cudaMemsetAsync(sh->slice_counts.p, 0, sh->slice_counts.bytes, st));
+    CU(cudaMemsetAsync(sh->slice_tot.p, 0, sh->slice_tot.bytes, st));
+    if (sh->slice_n) {
+        launch_sample_slice(sh->gs, sk, sh->slice_lo, d_slice_input, sh->slice_payload.p,
+                            sh->world, sh->slice_counts.as<uint32_t>(), st);
+        launch_scan(sh->gs, sh->slice_counts.as<uint32_t>(),
+                    sh->slice_gsum.as<unsigned long long>(),
+                    sh->slice_tot.as<unsigned long long>(), st);
+        sh->launches += 4;
+    }
+    CU(cudaMemcpyAsync(sh->h_tot, sh->slice_tot.p, (size_t)sh->world * 8, cudaMemcpyDeviceToHost,
+                       st));
+    CU(cudaStreamSynchronize(st));
+    std::memcpy(owner_counts, sh->h_tot, (size_t)sh->world * 8);
+    return check_launch("shard_sample");
+}
+
+extern "C" ssbh_status ssbh_shard_exchange(ssbh_shard* sh, const uint64_t* counts, void* stream) {
+    if (!sh || !counts) return fail(SSBH_INVALID_ARGUMENT, "shard_exchange: null argument");
+    const uint32_t W = sh->world;
+    std::vector<uint64_t> base(W, 0);
+    for (uint32_t o = 0; o < W; ++o) {
+        uint64_t tot = 0;
+        for (uint32_t r = 0; r < W; ++r) {
+            if (r == sh->rank) base[o] = tot;
+            tot += counts[(size_t)r * W + o];
+        }
+        if (tot > sh->recv_cap)
+            return fail(SSBH_INVALID_ARGUMENT, "shard_exchange: owner %u receives %llu rounds > "
+                        "capacity %llu", o, (unsigned long long)tot,
+                        (unsigned long long)sh->recv_cap);
+        if (o == sh->rank) sh->n_recv = tot;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CU(cudaMemcpyAsync(sh->d_dst_base.p, base.data(), (size_t)W * 8, cudaMemcpyHostToDevice, st));
+    launch_owner_split(sh->gs, sh->slice_payload.p, W, sh->slice_counts.as<uint32_t>(),
+                       sh->d_dst.as<void* const>(), sh->d_dst_base.as<unsigned long long>(), st);
+    sh->launches += 1;
+    CU(cudaStreamSynchronize(st));  // this rank's stores are complete before its barrier
+    return check_launch("shard_exchange");
+}
+
+extern "C" ssbh_status ssbh_shard_finish(ssbh_shard* sh, uint32_t* d_key, uint64_t* d_lengths,
+                                         const uint64_t* hash_key, void* stream) {
+    if (!sh || !d_key) return fail(SSBH_INVALID_ARGUMENT, "shard_finish: null argument");
+    ssbh_plan* pl = sh->plan;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl->last_stream = st;
+    const uint64_t* hk = hash_key ? hash_key : sh->p.hash_key;
+    const SamplerGeom g = geom_with_n(pl->geom, sh->n_recv);
+    const Layout lay = pl->lay.view();
+    uint32_t launches = sh->launches;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
+    CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
+    launch_count_payload(g, sh->recv.p, pl->counts.as<uint32_t>(), st);
+    launch_scan(g, pl->counts.as<uint32_t>(), pl->gsum.as<unsigned long long>(), lay.nj, st);
+    launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
+                  pl->p.block_limit, st);
+    launches += 5;
+    if (pl->timing) CU(cudaEventRecord(pl->ev[1], st));
+    CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
+    launch_scatter(g, sh->recv.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
+                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
+    launches += 1;
+    if (auto s = phase_finish(pl, d_key, d_lengths, hk, st, launches)) return s;
+    pl->launches_per_run = launches;
+    return check_launch("shard_finish");
+}
+
+extern "C" ssbh_status ssbh_shard_check(ssbh_shard* sh, ssbh_extract_stats* stats) {
+    if (!sh) return fail(SSBH_INVALID_ARGUMENT, "null shard");
+    return ssbh_plan_check(sh->plan, stats);
+}
+
+extern "C" ssbh_status ssbh_shard_set_timing(ssbh_shard* sh, int enable) {
+    if (!sh) return fail(SSBH_INVALID_ARGUMENT, "null shard");
+    return ssbh_plan_set_timing(sh->plan, enable);
 }

@@ -104,6 +104,23 @@ void launch_scatter_stream(const SamplerGeom& g, const uint64_t key[4], const ui
                            const unsigned long long* d_nj, const unsigned long long* d_yoff,
                            uint32_t* d_ybuf, cudaStream_t st);
 
+// ---- multi-GPU sharded sampling ---------------------------------------------------------
+// Same geometry with another round count (chunk shift kept; counts table sized for the max).
+SamplerGeom geom_with_n(const SamplerGeom& g, uint64_t n);
+// Pass 1 over a slice of rounds [base, base + g.n): payload (local index) + counts per
+// (chunk, owning rank) for `owners` ranks (block ranges multigpu.owned_range).
+void launch_sample_slice(const SamplerGeom& g, const uint64_t key[4], uint64_t base,
+                         const uint32_t* d_in32, void* d_payload, uint32_t owners,
+                         uint32_t* d_counts, cudaStream_t st);
+// Stable split of the slice payload by owner, stored straight into every owner's receive
+// buffer (d_dst[o], peer-mapped) at d_dst_base[o] + rank (d_offsets: scanned counts).
+void launch_owner_split(const SamplerGeom& g, const void* d_payload, uint32_t owners,
+                        uint32_t* d_offsets, void* const* d_dst,
+                        const unsigned long long* d_dst_base, cudaStream_t st);
+// Pass 1 of an owner: counts per (chunk, owned block) from a received payload (g.n rounds).
+void launch_count_payload(const SamplerGeom& g, const void* d_payload, uint32_t* d_counts,
+                          cudaStream_t st);
+
 // ---- layout / seeds / hash -----------------------------------------------------------
 // Computes ypad/ktl/yoff/items/soff/stats from lay.nj for nown blocks.
 void launch_layout(const Layout& lay, uint32_t nown, uint64_t k, uint32_t rowtiles,

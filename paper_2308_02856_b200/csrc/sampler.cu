@@ -4,22 +4,24 @@
 // proj/tools/ssbh_main.cpp:317-331) as three passes over the rounds, without ever
 // materialising the reference's 12 B/round host structures:
 //
-//  pass 1 (k_sample_count, int-ALU bound): V_i = uniform_below(s, i) from
-//      KeyedStream(seed, "sampling") — Threefry is counter based, so every round is
-//      independent. Emits a 2-byte payload V | x_i<<15 (4-byte when s >= 2^15 or a keep
-//      mask is given) and counts rounds per (warp-chunk, owned block) with
-//      __match_any_sync-aggregated atomics.
-//  pass 2 (k_scan_*, HBM/latency bound, tiny): exclusive scan of the count table along
-//      chunks -> per-(chunk, block) start rank; block totals n_j.
-//  pass 3 (k_scatter, HBM/latency bound): one warp walks its chunk in round order, ranks
-//      rounds inside each block with __match_any_sync + a running per-block counter
-//      (stable by construction: rank = chunk start + earlier groups + earlier lanes),
-//      and writes the data bit straight into block j's REVERSED packed input
-//      y_j[n_j-1-rank] (reversal turns the Toeplitz product into forward seed windows,
-//      see toeplitz.cu) with a red.or on a zeroed buffer — OR of distinct bits is order
-//      independent, so the result is deterministic.
+//  pass 1 (count, int-ALU bound): V_i = uniform_below(s, i) from KeyedStream(seed,
+//      "sampling") — Threefry is counter based, so every round is independent. Emits a
+//      2-byte payload V | x_i<<15 (4-byte when s >= 2^15 or a keep mask is given) and counts
+//      rounds per (warp-chunk, key) — key = owned block, or (sharded runs) owning rank.
+//  pass 2 (k_scan_*, tiny): exclusive scan of the count table along chunks -> per-(chunk,
+//      key) start rank; key totals (n_j).
+//  pass 3 (k_scatter): one warp walks its chunk in round order, ranks rounds inside each key
+//      with ballot peer masks + a warp-owned running counter (stable by construction: rank =
+//      chunk start + earlier groups + earlier lanes) and emits:
+//        Bits  — the data bit into block j's REVERSED packed input y_j[n_j-1-rank] with a
+//                red.or on a zeroed buffer (OR of distinct bits is order independent);
+//        Index — the round index into a CSR list (sift_partition API);
+//        Owner — the payload itself into the owning rank's receive buffer at a global rank,
+//                by direct stores through NVLink peer memory (multi-GPU sharded sampling:
+//                the dispatch half of an all-to-all fused into the partition pass).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -39,7 +41,7 @@ struct PayloadBits;
 template <>
 struct PayloadBits<uint16_t> {
     static constexpr uint32_t kDataShift = 15;
-    static constexpr uint32_t kKeepShift = 32;  // none
+    static constexpr uint32_t kKeepShift = 32;  // none: V = 0x7fff marks a sifted-out round
     static constexpr uint32_t kVMask = 0x7fffu;
 };
 template <>
@@ -49,58 +51,86 @@ struct PayloadBits<uint32_t> {
     static constexpr uint32_t kVMask = 0x3fffffffu;
 };
 
-// One group of 32 consecutive rounds: V_i, payload / assignment write; returns the
-// owned-block index jj (or ~0 when the round is not counted).
-template <typename P, bool kPow2>
-__device__ __forceinline__ uint32_t sample_group(const Key& key, uint64_t n, uint64_t s,
-                                                 const uint32_t* __restrict__ in32,
-                                                 const uint32_t* __restrict__ keep32, uint32_t j_lo,
-                                                 uint32_t nown, uint64_t g, uint32_t lane,
-                                                 P* __restrict__ payload,
-                                                 uint32_t* __restrict__ assign_out) {
-    using B = PayloadBits<P>;
-    const uint64_t i = g * 32 + lane;
-    const bool valid = i < n;
-    uint32_t v = 0;
-    if (valid) {
-        if (kPow2)
-            v = (uint32_t)(threefry_w0(key.ks, kTagSampling, 0, i, 0) & (s - 1));
-        else
-            v = (uint32_t)uniform_below(key.ks, kTagSampling, 0, s, i);
-    }
-    uint32_t bit = 0;
-    if (in32) bit = (__ldg(in32 + g) >> lane) & 1u;
-    bool kept = valid;
-    if (keep32 && valid) kept = ((__ldg(keep32 + g) >> lane) & 1u) != 0;
-    if (valid) {
-        if (payload) {
-            uint32_t pv = v | (bit << B::kDataShift);
-            if (!kept) {
-                if (B::kKeepShift < 32)
-                    pv |= 1u << (B::kKeepShift & 31);
-                else
-                    pv |= B::kVMask;  // u16 (s < 2^15): V = 0x7fff marks a sifted-out round
-            }
-            payload[i] = (P)pv;
-        }
-        if (assign_out) assign_out[i] = v + 1;
-    }
-    const uint32_t jj = v - j_lo;
-    return (kept && jj < nown) ? jj : 0xffffffffu;
+// Owning rank of block v when s blocks are split into `owners` contiguous balanced ranges
+// [o*s/N, (o+1)*s/N) (multigpu.owned_range): the largest o with floor(o*s/N) <= v, i.e.
+// o = floor(((v+1)*N - 1) / s).
+__device__ __forceinline__ uint32_t owner_of(uint32_t v, uint32_t owners, uint64_t s) {
+    return (uint32_t)(((uint64_t)(v + 1) * owners - 1) / s);
 }
 
-// Pass 1, small s: every warp counts one (chunk, part) range into a warp-private smem
-// histogram (match_any-aggregated plain read-modify-writes — the warp owns the row), then
-// flushes the non-zero bins to the global (chunk, block) table.
+// ---- pass-1 sources: produce one group's keys (and payload) ---------------------------
+// Threefry source: V_i for rounds base+i, optional payload / assignment write.
 template <typename P, bool kPow2>
-__global__ void __launch_bounds__(256) k_sample_count_rows(
-    Key key, uint64_t n, uint64_t s, const uint32_t* __restrict__ in32,
-    const uint32_t* __restrict__ keep, uint32_t j_lo, uint32_t nown, int cs, uint64_t nchunks,
-    uint32_t parts, P* __restrict__ payload, uint32_t* __restrict__ counts,
-    uint32_t* __restrict__ assign_out) {
+struct TFSource {
+    using Bits = PayloadBits<P>;
+    Key key;
+    uint64_t n, base, s;
+    const uint32_t* in32;    // data bits, bit 0 = local round 0 (may be null)
+    const uint32_t* keep32;  // sift mask, same layout (may be null)
+    P* payload;              // local index (may be null)
+    uint32_t* assign_out;    // V+1 per local round (may be null)
+    uint32_t j_lo, nown, owners;
+    __device__ __forceinline__ uint32_t operator()(uint64_t g, uint32_t lane) const {
+        const uint64_t i = g * 32 + lane;
+        const bool valid = i < n;
+        uint32_t v = 0;
+        if (valid) {
+            if (kPow2)
+                v = (uint32_t)(threefry_w0(key.ks, kTagSampling, 0, base + i, 0) & (s - 1));
+            else
+                v = (uint32_t)uniform_below(key.ks, kTagSampling, 0, s, base + i);
+        }
+        uint32_t bit = 0;
+        if (in32) bit = (__ldg(in32 + g) >> lane) & 1u;
+        bool kept = valid;
+        if (keep32 && valid) kept = ((__ldg(keep32 + g) >> lane) & 1u) != 0;
+        if (valid) {
+            if (payload) {
+                uint32_t pv = v | (bit << Bits::kDataShift);
+                if (!kept) {
+                    if (Bits::kKeepShift < 32)
+                        pv |= 1u << (Bits::kKeepShift & 31);
+                    else
+                        pv |= Bits::kVMask;  // u16 (s < 2^15): V = 0x7fff marks sifted-out
+                }
+                payload[i] = (P)pv;
+            }
+            if (assign_out) assign_out[i] = v + 1;
+        }
+        if (!kept) return 0xffffffffu;
+        if (owners) return owner_of(v, owners, s);
+        const uint32_t jj = v - j_lo;
+        return jj < nown ? jj : 0xffffffffu;
+    }
+};
+
+// Payload source: a pass-1 payload already in memory (an owner's received rounds).
+template <typename P>
+struct PayloadCountSource {
+    using Bits = PayloadBits<P>;
+    const P* payload;
+    uint64_t n;
+    uint32_t j_lo, nown;
+    __device__ __forceinline__ uint32_t operator()(uint64_t g, uint32_t lane) const {
+        const uint64_t i = g * 32 + lane;
+        if (i >= n) return 0xffffffffu;
+        const uint32_t p = payload[i];
+        if (Bits::kKeepShift < 32 && ((p >> (Bits::kKeepShift & 31)) & 1u)) return 0xffffffffu;
+        const uint32_t jj = (p & Bits::kVMask) - j_lo;
+        return jj < nown ? jj : 0xffffffffu;
+    }
+};
+
+// Pass 1, small key spaces: every warp counts one (chunk, part) range into a warp-private
+// smem histogram (match_any-aggregated plain read-modify-writes — the warp owns the row),
+// then flushes the non-zero bins to the global (chunk, key) table.
+template <typename Src>
+__global__ void __launch_bounds__(256) k_count_rows(Src src, uint64_t n, uint32_t nkeys, int cs,
+                                                    uint64_t nchunks, uint32_t parts,
+                                                    uint32_t* __restrict__ counts) {
     extern __shared__ uint32_t hist_all[];
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t* hist = hist_all + (size_t)(threadIdx.x >> 5) * nown;
+    uint32_t* hist = hist_all + (size_t)(threadIdx.x >> 5) * nkeys;
     const uint64_t gpc = (1ull << cs) / 32;  // groups per chunk
     const uint64_t ngroups = (n + 31) / 32;
     const uint64_t total = nchunks * parts;
@@ -108,43 +138,36 @@ __global__ void __launch_bounds__(256) k_sample_count_rows(
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t w = warp; w < total; w += nwarps) {
         const uint64_t c = w / parts, part = w % parts;
-        for (uint32_t t = lane; t < nown; t += 32) hist[t] = 0;
+        for (uint32_t t = lane; t < nkeys; t += 32) hist[t] = 0;
         __syncwarp();
         const uint64_t g0 = c * gpc + part * gpc / parts;
         const uint64_t g1 = min(ngroups, c * gpc + (part + 1) * gpc / parts);
         for (uint64_t g = g0; g < g1; ++g) {
-            const uint32_t jj = sample_group<P, kPow2>(key, n, s, in32, keep, j_lo, nown, g,
-                                                       lane, payload, assign_out);
+            const uint32_t jj = src(g, lane);
             const uint32_t peers = __match_any_sync(0xffffffffu, jj);
             if (jj != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
                 hist[jj] += (uint32_t)__popc(peers);
             __syncwarp();
         }
-        for (uint32_t t = lane; t < nown; t += 32)
-            if (hist[t]) atomicAdd(counts + c * nown + t, hist[t]);
+        for (uint32_t t = lane; t < nkeys; t += 32)
+            if (hist[t]) atomicAdd(counts + c * nkeys + t, hist[t]);
         __syncwarp();
     }
 }
 
-// Pass 1, large s: counts go straight to the global (chunk, block) table.
-template <typename P, bool kPow2>
-__global__ void __launch_bounds__(256) k_sample_count(Key key, uint64_t n, uint64_t s,
-                                                      const uint32_t* __restrict__ in32,
-                                                      const uint32_t* __restrict__ keep,
-                                                      uint32_t j_lo, uint32_t nown, int cs,
-                                                      P* __restrict__ payload,
-                                                      uint32_t* __restrict__ counts,
-                                                      uint32_t* __restrict__ assign_out) {
+// Pass 1, large key spaces: counts go straight to the global (chunk, key) table.
+template <typename Src>
+__global__ void __launch_bounds__(256) k_count_global(Src src, uint64_t n, uint32_t nkeys, int cs,
+                                                      uint32_t* __restrict__ counts) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t ngroups = (n + 31) / 32;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t g = warp; g < ngroups; g += nwarps) {
-        const uint32_t jj = sample_group<P, kPow2>(key, n, s, in32, keep, j_lo, nown, g, lane,
-                                                   payload, assign_out);
+        const uint32_t jj = src(g, lane);
         const uint32_t peers = __match_any_sync(0xffffffffu, jj);
         if (jj != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-            atomicAdd(counts + ((g * 32) >> cs) * nown + jj, (uint32_t)__popc(peers));
+            atomicAdd(counts + ((g * 32) >> cs) * nkeys + jj, (uint32_t)__popc(peers));
     }
 }
 
@@ -162,7 +185,7 @@ __global__ void k_scan_groups(const uint32_t* __restrict__ counts, uint64_t nchu
     gsum[g * nown + jj] = t;
 }
 
-// exclusive scan over groups per block, totals -> nj
+// exclusive scan over groups per key, totals -> nj
 __global__ void k_scan_totals(unsigned long long* __restrict__ gsum, uint64_t ngroups,
                               uint32_t nown, unsigned long long* __restrict__ nj) {
     const uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x;
@@ -206,8 +229,8 @@ __device__ __forceinline__ uint32_t peers_by_ballot(uint32_t key, bool in, int k
     return m;
 }
 
-// Where pass 3 gets each round's (V, data bit, keep) from:
-//  PayloadSrc — the payload written by pass 1 (in-memory plans);
+// ---- pass-3 sources -------------------------------------------------------------------
+//  PayloadSrc — the payload written by pass 1 (in-memory plans, sharded owners);
 //  StreamSrc  — recomputed: V by Threefry, the bit from the current input chunk (streaming
 //               plans: no payload buffer, input fed chunk by chunk).
 template <typename P>
@@ -233,35 +256,44 @@ struct StreamSrc {
     }
 };
 
+enum ScatterMode { kModeBits = 0, kModeIndex = 1, kModeOwner = 2 };
+
 struct ScatterArgs {
     uint64_t c_begin, c_end;  // warp-chunks processed by this launch
     uint64_t n_end;           // one past the last round of this launch
-    uint32_t j_lo, nown;
+    uint32_t j_lo, nown;      // key space: blocks [j_lo, j_lo+nown), or owners (kModeOwner)
     int kbits, cs;
-    uint32_t* offs;           // per-(chunk, block) running ranks
+    uint64_t s;               // kModeOwner: blocks, for owner_of
+    uint32_t* offs;           // per-(chunk, key) running ranks
     const unsigned long long* nj;
     const unsigned long long* yoff;
     uint32_t* ybuf;
     unsigned long long* idx_out;
     const unsigned long long* csr_off;
+    void* const* dst;                    // kModeOwner: per-owner receive buffers (peer mapped)
+    const unsigned long long* dst_base;  // kModeOwner: this rank's first global rank per owner
 };
 
-template <typename Src, bool kSmemRow, bool kMatch>
+template <typename Src, bool kSmemRow, bool kMatch, int kMode>
 __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
     using B = typename Src::Bits;
+    using P = typename std::conditional<B::kDataShift == 15, uint16_t, uint32_t>::type;
     constexpr int U = 4;  // groups of 32 rounds whose payloads are in flight per warp
     extern __shared__ __align__(16) uint8_t scatter_smem[];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t wpb = blockDim.x >> 5;
     const uint32_t nown = a.nown, j_lo = a.j_lo;
-    // Rank `pos` of block jj lands on global y bit  yend[jj] - pos  (reversed packing).
-    unsigned long long* s_end = reinterpret_cast<unsigned long long*>(scatter_smem);
+    // per-key u64 table: Bits — the end bit yend[jj] (rank pos lands on yend - pos);
+    // Owner — this rank's first global rank in owner jj's receive buffer
+    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(scatter_smem);
     uint32_t* srow_all = reinterpret_cast<uint32_t*>(scatter_smem + (size_t)nown * 8);
     if (kSmemRow) {
-        if (!a.idx_out)
+        if (kMode == kModeBits)
             for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
-                s_end[t] = a.yoff[t] * 32ull + a.nj[t] - 1ull;
+                s_key[t] = a.yoff[t] * 32ull + a.nj[t] - 1ull;
+        else if (kMode == kModeOwner)
+            for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) s_key[t] = a.dst_base[t];
         __syncthreads();
     }
     for (uint64_t c = a.c_begin + blockIdx.x * (uint64_t)wpb + wib; c < a.c_end;
@@ -300,8 +332,15 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                 const uint32_t p = cur[q];
                 bool kept = i < i1;
                 if (B::kKeepShift < 32) kept = kept && !((p >> (B::kKeepShift & 31)) & 1u);
-                jjv[q] = (p & B::kVMask) - j_lo;
-                inv[q] = kept && jjv[q] < nown;
+                if (kMode == kModeOwner) {
+                    // u16: V = 0x7fff is a sifted-out round (s < 2^15 never reaches it)
+                    if (B::kKeepShift >= 32) kept = kept && (p & B::kVMask) != B::kVMask;
+                    jjv[q] = owner_of(p & B::kVMask, nown, a.s);
+                    inv[q] = kept;
+                } else {
+                    jjv[q] = (p & B::kVMask) - j_lo;
+                    inv[q] = kept && jjv[q] < nown;
+                }
                 if (kMatch)
                     peers[q] = __match_any_sync(0xffffffffu, inv[q] ? jjv[q] : 0xffffffffu);
                 else
@@ -319,11 +358,14 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                     const uint32_t base = row[jj];
                     if ((pm >> lane) == 1u) row[jj] = base + (uint32_t)__popc(pm);
                     const uint64_t pos = (uint64_t)base + __popc(pm & lanemask_lt());
-                    if (a.idx_out) {
+                    if constexpr (kMode == kModeIndex) {
                         a.idx_out[a.csr_off[jj] + pos] = i;
+                    } else if constexpr (kMode == kModeOwner) {
+                        const unsigned long long gb = kSmemRow ? s_key[jj] : a.dst_base[jj];
+                        static_cast<P*>(a.dst[jj])[gb + pos] = (P)cur[q];
                     } else if ((cur[q] >> B::kDataShift) & 1u) {
                         const unsigned long long e =
-                            kSmemRow ? s_end[jj]
+                            kSmemRow ? s_key[jj]
                                      : __ldg(a.yoff + jj) * 32ull + __ldg(a.nj + jj) - 1ull;
                         const uint64_t qb = e - pos;
                         atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
@@ -336,8 +378,8 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
         }
         __syncwarp();
     }
+    if (kMode == kModeOwner) __threadfence_system();  // peer stores visible to the owners
 }
-
 
 // sift_partition API path: payload from a caller-given assignment (values 1-based) and keep
 // mask; counts as in pass 1; out-of-range values raise *bad.
@@ -407,6 +449,126 @@ int sm_count() {
     return sms;
 }
 
+// Pass-1 launcher for any source over n local rounds and nkeys count columns.
+template <typename Src>
+void count_launch(const Src& src, uint64_t n, uint32_t nkeys, int cs, uint64_t nchunks,
+                  uint32_t* d_counts, cudaStream_t st) {
+    if (n == 0) return;
+    const uint64_t groups = (n + 31) / 32;
+    const size_t row_bytes = (size_t)nkeys * 4;
+    if (row_bytes * 8 <= 96 * 1024) {
+        // enough (chunk, part) work units for ~2 waves of 64 warps per SM
+        const uint64_t gpc = (1ull << cs) / 32;
+        const uint64_t want = (uint64_t)sm_count() * 128;
+        const uint32_t parts = (uint32_t)std::min<uint64_t>(
+            gpc, std::max<uint64_t>(1, (want + nchunks - 1) / nchunks));
+        const uint64_t units = nchunks * parts;
+        const uint64_t blocks = std::min<uint64_t>((units + 7) / 8, (uint64_t)sm_count() * 8);
+        const size_t shm = row_bytes * 8;
+        auto kern = k_count_rows<Src>;
+        if (shm > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(src, n, nkeys, cs,
+                                                                         nchunks, parts, d_counts);
+        return;
+    }
+    uint64_t blocks = (groups + 7) / 8;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    k_count_global<Src><<<(unsigned)blocks, 256, 0, st>>>(src, n, nkeys, cs, d_counts);
+}
+
+template <typename P, bool kPow2>
+void sample_count_t(const SamplerGeom& g, const Key& k, const uint32_t* d_in32,
+                    const uint32_t* d_keep, P* pl, uint32_t* d_counts, uint32_t* d_assign_out,
+                    uint64_t base, uint32_t owners, cudaStream_t st) {
+    TFSource<P, kPow2> src{k,      g.n,          base,   g.s,    d_in32, d_keep,
+                           pl,     d_assign_out, g.j_lo, g.nown, owners};
+    count_launch(src, g.n, owners ? owners : g.nown, g.chunk_shift, g.nchunks, d_counts, st);
+}
+
+void sample_count_any(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
+                      const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
+                      uint32_t* d_assign_out, uint64_t base, uint32_t owners, cudaStream_t st) {
+    if (g.n == 0) return;
+    Key k;
+    threefry_ks(key, k.ks);
+    const bool pow2 = (g.s & (g.s - 1)) == 0;
+    if (g.payload_bytes == 2) {
+        auto* pl = static_cast<uint16_t*>(d_payload);
+        if (pow2)
+            sample_count_t<uint16_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, base,
+                                           owners, st);
+        else
+            sample_count_t<uint16_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out,
+                                            base, owners, st);
+    } else {
+        auto* pl = static_cast<uint32_t*>(d_payload);
+        if (pow2)
+            sample_count_t<uint32_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, base,
+                                           owners, st);
+        else
+            sample_count_t<uint32_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out,
+                                            base, owners, st);
+    }
+}
+
+bool scatter_match() {  // dev switch for A/B: SSBH_SCATTER_PEERS=ballot|match
+    static int m = -1;
+    if (m < 0) {
+        const char* e = std::getenv("SSBH_SCATTER_PEERS");
+        m = (e && e[0] == 'm') ? 1 : 0;  // ballot default: 6.3 ms vs 8.6 ms (config 3)
+    }
+    return m == 1;
+}
+
+template <int kMode, typename Src>
+void scatter_launch(const Src& src, ScatterArgs a, cudaStream_t st) {
+    const size_t row_bytes = (size_t)a.nown * 4;
+    const bool smem = row_bytes <= 32768;
+    int wpb = 8;
+    size_t shm = 0;
+    if (smem) {  // per-warp running-rank rows + the per-key u64 table
+        wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / row_bytes));
+        shm = row_bytes * wpb + (size_t)a.nown * 8;
+    }
+    const uint64_t nc = a.c_end - a.c_begin;
+    const uint64_t blocks = std::max<uint64_t>(1, (nc + wpb - 1) / wpb);
+    a.kbits = 1;
+    while ((1ull << a.kbits) < a.nown) ++a.kbits;
+    auto go = [&](auto kern) {
+        if (shm > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        kern<<<(unsigned)blocks, wpb * 32, shm, st>>>(src, a);
+    };
+    const bool m = scatter_match();
+    if (smem)
+        m ? go(k_scatter<Src, true, true, kMode>) : go(k_scatter<Src, true, false, kMode>);
+    else
+        m ? go(k_scatter<Src, false, true, kMode>) : go(k_scatter<Src, false, false, kMode>);
+}
+
+ScatterArgs scatter_args(const SamplerGeom& g, uint32_t* d_offsets,
+                         const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                         uint32_t* d_ybuf, unsigned long long* d_idx_out,
+                         const unsigned long long* d_csr_off) {
+    ScatterArgs a{};
+    a.c_begin = 0;
+    a.c_end = g.nchunks;
+    a.n_end = g.n;
+    a.j_lo = g.j_lo;
+    a.nown = g.nown;
+    a.cs = g.chunk_shift;
+    a.s = g.s;
+    a.offs = d_offsets;
+    a.nj = d_nj;
+    a.yoff = d_yoff;
+    a.ybuf = d_ybuf;
+    a.idx_out = d_idx_out;
+    a.csr_off = d_csr_off;
+    return a;
+}
+
 }  // namespace
 
 SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,
@@ -419,7 +581,7 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
     // u16 needs V <= 0x7ffe so that 0x7fff can mark sifted-out rounds
     g.payload_bytes = (!has_keep && s < 32768) ? 2 : 4;
     // warp-chunk: enough chunks for latency hiding in the scatter pass, bounded count table
-    int cs = 10;
+    int cs = std::min(10, max_chunk_shift);
     auto table_bytes = [&](int shift) {
         const uint64_t nc = (n + (1ull << shift) - 1) >> shift;
         return nc * (uint64_t)nown * 4ull;
@@ -435,56 +597,36 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
     return g;
 }
 
-template <typename P, bool kPow2>
-static void sample_count_t(const SamplerGeom& g, const Key& k, const uint32_t* d_in32,
-                           const uint32_t* d_keep, P* pl, uint32_t* d_counts,
-                           uint32_t* d_assign_out, cudaStream_t st) {
-    const uint64_t groups = (g.n + 31) / 32;
-    const size_t row_bytes = (size_t)g.nown * 4;
-    if (row_bytes * 8 <= 96 * 1024) {
-        // enough (chunk, part) work units for ~2 waves of 64 warps per SM
-        const uint64_t gpc = (1ull << g.chunk_shift) / 32;
-        const uint64_t want = (uint64_t)sm_count() * 128;
-        const uint32_t parts =
-            (uint32_t)std::min<uint64_t>(gpc, std::max<uint64_t>(1, (want + g.nchunks - 1) / g.nchunks));
-        const uint64_t units = g.nchunks * parts;
-        const uint64_t blocks = std::min<uint64_t>((units + 7) / 8, (uint64_t)sm_count() * 8);
-        const size_t shm = row_bytes * 8;
-        auto kern = k_sample_count_rows<P, kPow2>;
-        if (shm > 48 * 1024)
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-        kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
-            k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, g.nchunks, parts, pl,
-            d_counts, d_assign_out);
-        return;
-    }
-    uint64_t blocks = (groups + 7) / 8;
-    const uint64_t cap = (uint64_t)sm_count() * 8;
-    if (blocks > cap) blocks = cap;
-    k_sample_count<P, kPow2><<<(unsigned)blocks, 256, 0, st>>>(
-        k, g.n, g.s, d_in32, d_keep, g.j_lo, g.nown, g.chunk_shift, pl, d_counts, d_assign_out);
+SamplerGeom geom_with_n(const SamplerGeom& g0, uint64_t n) {
+    SamplerGeom g = g0;
+    g.n = n;
+    g.nchunks = std::max<uint64_t>(1, (n + (1ull << g.chunk_shift) - 1) >> g.chunk_shift);
+    g.ngroups = (g.nchunks + g.group_chunks - 1) / g.group_chunks;
+    return g;
 }
 
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
                          const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st) {
-    if (g.n == 0) return;
-    Key k;
-    threefry_ks(key, k.ks);
-    const bool pow2 = (g.s & (g.s - 1)) == 0;
-    if (g.payload_bytes == 2) {
-        auto* pl = static_cast<uint16_t*>(d_payload);
-        if (pow2)
-            sample_count_t<uint16_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
-        else
-            sample_count_t<uint16_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
-    } else {
-        auto* pl = static_cast<uint32_t*>(d_payload);
-        if (pow2)
-            sample_count_t<uint32_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
-        else
-            sample_count_t<uint32_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, st);
-    }
+    sample_count_any(g, key, d_in32, d_keep, d_payload, d_counts, d_assign_out, 0, 0, st);
+}
+
+void launch_sample_slice(const SamplerGeom& g, const uint64_t key[4], uint64_t base,
+                         const uint32_t* d_in32, void* d_payload, uint32_t owners,
+                         uint32_t* d_counts, cudaStream_t st) {
+    sample_count_any(g, key, d_in32, nullptr, d_payload, d_counts, nullptr, base, owners, st);
+}
+
+void launch_count_payload(const SamplerGeom& g, const void* d_payload, uint32_t* d_counts,
+                          cudaStream_t st) {
+    if (g.payload_bytes == 2)
+        count_launch(PayloadCountSource<uint16_t>{static_cast<const uint16_t*>(d_payload), g.n,
+                                                  g.j_lo, g.nown},
+                     g.n, g.nown, g.chunk_shift, g.nchunks, d_counts, st);
+    else
+        count_launch(PayloadCountSource<uint32_t>{static_cast<const uint32_t*>(d_payload), g.n,
+                                                  g.j_lo, g.nown},
+                     g.n, g.nown, g.chunk_shift, g.nchunks, d_counts, st);
 }
 
 void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d_gsum,
@@ -496,72 +638,19 @@ void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d
     k_scan_apply<<<grid, 256, 0, st>>>(d_counts, g.nchunks, g.nown, g.group_chunks, d_gsum);
 }
 
-static bool scatter_match() {  // dev switch for A/B: SSBH_SCATTER_PEERS=ballot|match
-    static int m = -1;
-    if (m < 0) {
-        const char* e = std::getenv("SSBH_SCATTER_PEERS");
-        m = (e && e[0] == 'm') ? 1 : 0;  // ballot default: 6.3 ms vs 8.6 ms (config 3)
-    }
-    return m == 1;
-}
-
-template <typename Src>
-static void scatter_launch(const SamplerGeom& g, const Src& src, ScatterArgs a, cudaStream_t st) {
-    const size_t row_bytes = (size_t)g.nown * 4;
-    const bool smem = row_bytes <= 32768;
-    int wpb = 8;
-    size_t shm = 0;
-    if (smem) {  // per-warp running-rank rows + the per-block y end-bit table
-        wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / row_bytes));
-        shm = row_bytes * wpb + (size_t)g.nown * 8;
-    }
-    const uint64_t nc = a.c_end - a.c_begin;
-    const uint64_t blocks = std::max<uint64_t>(1, (nc + wpb - 1) / wpb);
-    a.kbits = 1;
-    while ((1ull << a.kbits) < g.nown) ++a.kbits;
-    auto go = [&](auto kern) {
-        if (shm > 48 * 1024)
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-        kern<<<(unsigned)blocks, wpb * 32, shm, st>>>(src, a);
-    };
-    const bool m = scatter_match();
-    if (smem)
-        m ? go(k_scatter<Src, true, true>) : go(k_scatter<Src, true, false>);
-    else
-        m ? go(k_scatter<Src, false, true>) : go(k_scatter<Src, false, false>);
-}
-
-static ScatterArgs scatter_args(const SamplerGeom& g, uint32_t* d_offsets,
-                                const unsigned long long* d_nj,
-                                const unsigned long long* d_yoff, uint32_t* d_ybuf,
-                                unsigned long long* d_idx_out,
-                                const unsigned long long* d_csr_off) {
-    ScatterArgs a{};
-    a.c_begin = 0;
-    a.c_end = g.nchunks;
-    a.n_end = g.n;
-    a.j_lo = g.j_lo;
-    a.nown = g.nown;
-    a.cs = g.chunk_shift;
-    a.offs = d_offsets;
-    a.nj = d_nj;
-    a.yoff = d_yoff;
-    a.ybuf = d_ybuf;
-    a.idx_out = d_idx_out;
-    a.csr_off = d_csr_off;
-    return a;
-}
-
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
                     const unsigned long long* d_nj, const unsigned long long* d_yoff,
                     uint32_t* d_ybuf, unsigned long long* d_idx_out,
                     const unsigned long long* d_csr_off, cudaStream_t st) {
     if (g.n == 0 || g.nown == 0) return;
     const ScatterArgs a = scatter_args(g, d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);
-    if (g.payload_bytes == 2)
-        scatter_launch(g, PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload)}, a, st);
-    else
-        scatter_launch(g, PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload)}, a, st);
+    if (g.payload_bytes == 2) {
+        const PayloadSrc<uint16_t> src{static_cast<const uint16_t*>(d_payload)};
+        d_idx_out ? scatter_launch<kModeIndex>(src, a, st) : scatter_launch<kModeBits>(src, a, st);
+    } else {
+        const PayloadSrc<uint32_t> src{static_cast<const uint32_t*>(d_payload)};
+        d_idx_out ? scatter_launch<kModeIndex>(src, a, st) : scatter_launch<kModeBits>(src, a, st);
+    }
 }
 
 void launch_scatter_stream(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_chunk32,
@@ -579,7 +668,24 @@ void launch_scatter_stream(const SamplerGeom& g, const uint64_t key[4], const ui
     src.pow2 = (g.s & (g.s - 1)) == 0;
     src.in32 = d_chunk32;
     src.first = first;
-    scatter_launch(g, src, a, st);
+    scatter_launch<kModeBits>(src, a, st);
+}
+
+void launch_owner_split(const SamplerGeom& g, const void* d_payload, uint32_t owners,
+                        uint32_t* d_offsets, void* const* d_dst,
+                        const unsigned long long* d_dst_base, cudaStream_t st) {
+    if (g.n == 0) return;
+    ScatterArgs a = scatter_args(g, d_offsets, nullptr, nullptr, nullptr, nullptr, nullptr);
+    a.j_lo = 0;
+    a.nown = owners;
+    a.dst = d_dst;
+    a.dst_base = d_dst_base;
+    if (g.payload_bytes == 2)
+        scatter_launch<kModeOwner>(PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload)},
+                                   a, st);
+    else
+        scatter_launch<kModeOwner>(PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload)},
+                                   a, st);
 }
 
 void launch_payload_from_assignment(const SamplerGeom& g, const uint32_t* d_assign,

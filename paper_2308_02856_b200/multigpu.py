@@ -36,6 +36,58 @@ def concat_bits(parts: list[np.ndarray], bit_lengths: list[int]) -> np.ndarray:
     return out[: (total + 63) // 64]
 
 
+class ShardedExtractor:
+    """Host protocol of a sharded multi-GPU extraction (ssbh_shard_*, one process per GPU).
+
+    Rank r samples only its slice of rounds; the sampled payload goes straight into the
+    owning rank's receive buffer through NVLink peer memory (IPC mappings exchanged once
+    here); each rank then builds and hashes its own blocks. torch.distributed carries only
+    the handles (once), a W x W count matrix and a barrier per run."""
+
+    def __init__(self, n, s, k, samp, hsh, per_block=False, group=None):
+        import torch.distributed as dist
+
+        import paper_2308_02856_b200 as P
+
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.shard = P.Shard(n, s, k, samp, hsh, self.rank, self.world, per_block=per_block)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.shard.ipc_handle(), group=group)
+        self.shard.open_peers(handles)
+        self.n, self.s, self.k = n, s, k
+
+    @property
+    def slice(self):
+        return self.shard.slice_first, self.shard.slice_rounds
+
+    @property
+    def blocks(self):
+        return self.shard.block_first, self.shard.block_count
+
+    def run(self, d_slice_ptr: int, d_key_ptr: int, d_len_ptr: int = 0, stream: int = 0,
+            coll_device: str = "cpu"):
+        import torch
+
+        counts = self.shard.sample(d_slice_ptr, stream)
+        mine = torch.from_numpy(counts.view(np.int64).copy()).to(coll_device)
+        rows = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(rows, mine, group=self.group)
+        matrix = np.stack([r.cpu().numpy().view(np.uint64) for r in rows])
+        self.shard.exchange(matrix, stream)
+        self.dist.barrier(group=self.group)  # every rank's peer stores have landed
+        self.shard.finish(d_key_ptr, d_len_ptr, stream)
+        return matrix
+
+    def check(self):
+        return self.shard.check()
+
+    def close(self):
+        self.dist.barrier(group=self.group)  # peers are done with our receive buffer
+        self.shard.close()
+
+
 def gather_key(local_words, n_subblocks: int, out_bits: int, group=None):
     """All-gather every rank's owned key slice (torch int64 tensor of uint64 words) and return
     the full concatenated key as uint64 numpy words on every rank."""

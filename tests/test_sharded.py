@@ -1,0 +1,80 @@
+"""Sharded multi-GPU extraction (ssbh_shard_*: sliced sampling, owner split stored through
+peer memory, per-owner hashing) against the oracle. On a 1-GPU box the W ranks are W
+processes sharing the device (IPC mappings of the same GPU; host barriers between phases,
+no kernel waits on another rank); gloo carries the host-side collectives."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2308_02856_b200 as P
+    from oracle.pyoracle import Oracle
+    from paper_2308_02856_b200.multigpu import ShardedExtractor, gather_key
+
+    torch.cuda.set_device(0)
+    o = Oracle()
+    res = []
+    for (n, s, k, pb) in cases:
+        x = o.make_input(7, 0.5, n)
+        ex = ShardedExtractor(n, s, k, 2, 3, per_block=pb)
+        lo, cnt = ex.slice
+        x32 = torch.from_numpy(x.view(np.int32).copy()).cuda()
+        first, count = ex.blocks
+        d_key = torch.zeros(((count * k + 63) // 64) * 2, dtype=torch.int32, device="cuda")
+        d_len = torch.zeros(max(count, 1), dtype=torch.int64, device="cuda")
+        stream = torch.cuda.Stream()
+        for rep in range(2):  # second run reuses buffers and peer mappings
+            ex.run(x32.data_ptr() + (lo // 32) * 4, d_key.data_ptr(), d_len.data_ptr(),
+                   stream.cuda_stream)
+            ex.check()
+        full = gather_key(d_key.view(torch.int64)[: (count * k + 63) // 64].cpu(), s, k)
+        want, nj = o.extract(x, n, s, 2, 3, int(pb), k)
+        ok_key = bool((full[: len(want)] == want).all())
+        ok_len = bool((d_len.cpu().numpy().view(np.uint64)[:count] == nj[first:first + count]).all())
+        res.append((ok_key, ok_len))
+        ex.close()
+    dist.destroy_process_group()
+    q.put((rank, res))
+
+
+def _run(world, cases):
+    import multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, res in out:
+        for c, (ok_key, ok_len) in zip(cases, res):
+            assert ok_len, (rank, c, "lengths")
+            assert ok_key, (rank, c, "key")
+
+
+@pytest.mark.gpu
+def test_sharded_world2_matches_oracle():
+    _run(2, [(300000, 16, 512, False), (1 << 20, 64, 8192, False), (250000, 33, 96, True)])
+
+
+@pytest.mark.gpu
+def test_sharded_world3_uneven():
+    _run(3, [(200000, 7, 640, True), (1 << 20, 64, 1024, False)])
