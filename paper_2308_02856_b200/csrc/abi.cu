@@ -348,8 +348,9 @@ struct ssbh_plan {
     cudaEvent_t ev[6]{};
     cudaStream_t last_stream = nullptr;
     uint32_t launches_per_run = 0;
-    // CUDA graph of one run (captured per stream / buffers / seeds; replayed afterwards)
-    cudaGraphExec_t exec = nullptr;
+    // CUDA graph(s) of one run (captured per stream / buffers / seeds; replayed afterwards):
+    // one graph untimed, one per segment when timing
+    cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
     struct GraphKey {
         cudaStream_t st;
         const void *in, *keep, *key, *len;
@@ -506,7 +507,8 @@ extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
         if (e) cudaEventDestroy(e);
     if (pl->h_stats) cudaFreeHost(pl->h_stats);
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
-    if (pl->exec) cudaGraphExecDestroy(pl->exec);
+    for (auto x : pl->exec)
+        if (x) cudaGraphExecDestroy(x);
     delete pl;
     return ok();
 }
@@ -519,13 +521,20 @@ extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
     return ok();
 }
 
-// Enqueue one fused run on `st` (directly, or into a graph being captured).
-// Phase A: pass 1-2 — Threefry V per round (+ payload when d_input is given), counts,
-// scan, device-side layout. Streaming plans call it without input (counts only).
-static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
-                                const uint64_t* sk, cudaStream_t st, uint32_t& launches) {
+// ---- the run as four stream segments ---------------------------------------------------
+//  S0 sample: pass 1-2 (Threefry V per round + payload, counts, scan, device-side layout)
+//  S1 scatter: pass 3 (stable partition into reversed packed blocks)
+//  S2 seeds:   Toeplitz seed material
+//  S3 hash:    GF(2) hash, concatenation, lengths / stats copies
+// Timing events go BETWEEN segments: directly launched, or each segment replayed as its own
+// CUDA graph (events inside a captured graph cannot be timed).
+static void rec(ssbh_plan* pl, int i, cudaStream_t st) {
+    if (pl->timing) cudaEventRecord(pl->ev[i], st);
+}
+
+static ssbh_status seg_sample(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
+                              const uint64_t* sk, cudaStream_t st, uint32_t& launches) {
     const Layout lay = pl->lay.view();
-    if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
     CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
     launch_sample_count(pl->geom, sk, d_input, d_keep, pl->payload.p, pl->counts.as<uint32_t>(),
                         nullptr, st);
@@ -534,20 +543,29 @@ static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const ui
     launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
                   pl->p.block_limit, st);
     launches += 5;
-    if (pl->timing) CU(cudaEventRecord(pl->ev[1], st));
     CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
     return SSBH_OK;
 }
 
-// Phase C: Toeplitz seeds, the hash of every owned block, concatenation, lengths/stats.
-static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
-                                const uint64_t* hk, cudaStream_t st, uint32_t& launches) {
+static ssbh_status seg_scatter(ssbh_plan* pl, cudaStream_t st, uint32_t& launches) {
     const Layout lay = pl->lay.view();
-    if (pl->timing) CU(cudaEventRecord(pl->ev[2], st));
-    launch_seeds(hk, lay, pl->nown, pl->p.block_first, pl->p.per_block_seed, pl->sbuf_words,
-                 pl->sbuf.as<uint32_t>(), st);
+    launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
+                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
     launches += 1;
-    if (pl->timing) CU(cudaEventRecord(pl->ev[3], st));
+    return SSBH_OK;
+}
+
+static ssbh_status seg_seeds(ssbh_plan* pl, const uint64_t* hk, cudaStream_t st,
+                             uint32_t& launches) {
+    launch_seeds(hk, pl->lay.view(), pl->nown, pl->p.block_first, pl->p.per_block_seed,
+                 pl->sbuf_words, pl->sbuf.as<uint32_t>(), st);
+    launches += 1;
+    return SSBH_OK;
+}
+
+static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
+                            cudaStream_t st, uint32_t& launches) {
+    const Layout lay = pl->lay.view();
     uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
     CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
     HashArgs a{};
@@ -562,7 +580,6 @@ static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_leng
     a.per_block_seed = pl->p.per_block_seed;
     launch_hash(a, pl->grid, st);
     launches += 1;
-    if (pl->timing) CU(cudaEventRecord(pl->ev[4], st));
     if (!pl->direct_out) {
         launch_concat(pl->scratch.as<uint32_t>(), pl->kw, pl->nown, pl->p.out_bits, d_key, st);
         launches += 1;
@@ -570,23 +587,64 @@ static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_leng
     if (d_lengths)
         CU(cudaMemcpyAsync(d_lengths, lay.nj, (size_t)pl->nown * 8, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemcpyAsync(pl->h_stats, lay.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, st));
-    if (pl->timing) CU(cudaEventRecord(pl->ev[5], st));
     return SSBH_OK;
 }
 
-// One in-memory fused run on `st` (directly, or into a graph being captured).
-static ssbh_status plan_enqueue(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
-                                uint32_t* d_key,
-                                uint64_t* d_lengths, const uint64_t* sk, const uint64_t* hk,
-                                cudaStream_t st) {
-    const Layout lay = pl->lay.view();
+// Phase A (direct launches): S0 with its events. Streaming plans call it without input.
+static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
+                                const uint64_t* sk, cudaStream_t st, uint32_t& launches) {
+    rec(pl, 0, st);
+    if (auto s = seg_sample(pl, d_input, d_keep, sk, st, launches)) return s;
+    rec(pl, 1, st);
+    return SSBH_OK;
+}
+
+// Phase C (direct launches): S2 + S3 with their events.
+static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
+                                const uint64_t* hk, cudaStream_t st, uint32_t& launches) {
+    rec(pl, 2, st);
+    if (auto s = seg_seeds(pl, hk, st, launches)) return s;
+    rec(pl, 3, st);
+    if (auto s = seg_hash(pl, d_key, d_lengths, st, launches)) return s;
+    rec(pl, 4, st);
+    rec(pl, 5, st);
+    return SSBH_OK;
+}
+
+struct RunArgs {
+    const uint32_t* d_input;
+    const uint32_t* d_keep;
+    uint32_t* d_key;
+    uint64_t* d_lengths;
+    const uint64_t* sk;
+    const uint64_t* hk;
+};
+
+// Segments [s0, s1) of an in-memory run, without events.
+static ssbh_status enqueue_segments(ssbh_plan* pl, const RunArgs& r, int s0, int s1,
+                                    cudaStream_t st, uint32_t& launches) {
+    for (int sgi = s0; sgi < s1; ++sgi) {
+        ssbh_status s = SSBH_OK;
+        switch (sgi) {
+            case 0: s = seg_sample(pl, r.d_input, r.d_keep, r.sk, st, launches); break;
+            case 1: s = seg_scatter(pl, st, launches); break;
+            case 2: s = seg_seeds(pl, r.hk, st, launches); break;
+            default: s = seg_hash(pl, r.d_key, r.d_lengths, st, launches); break;
+        }
+        if (s) return s;
+    }
+    return SSBH_OK;
+}
+
+// One in-memory fused run launched directly on `st`, events between segments.
+static ssbh_status plan_enqueue(ssbh_plan* pl, const RunArgs& r, cudaStream_t st) {
     uint32_t launches = 0;
-    if (auto s = phase_sample(pl, d_input, d_keep, sk, st, launches)) return s;
-    // pass 3: stable scatter into reversed packed blocks
-    launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
-                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
-    launches += 1;
-    if (auto s = phase_finish(pl, d_key, d_lengths, hk, st, launches)) return s;
+    for (int sgi = 0; sgi < 4; ++sgi) {
+        rec(pl, sgi, st);
+        if (auto s = enqueue_segments(pl, r, sgi, sgi + 1, st, launches)) return s;
+    }
+    rec(pl, 4, st);
+    rec(pl, 5, st);
     pl->launches_per_run = launches;
     return check_launch("plan_run");
 }
@@ -598,6 +656,26 @@ static bool graphs_enabled() {
         on = (e && *e == '1') ? 0 : 1;
     }
     return on == 1;
+}
+
+static ssbh_status capture(ssbh_plan* pl, const RunArgs& r, int s0, int s1, cudaStream_t st,
+                           cudaGraphExec_t* exec, uint32_t& launches) {
+    CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const ssbh_status s = enqueue_segments(pl, r, s0, s1, st, launches);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (s != SSBH_OK) {
+        if (g) cudaGraphDestroy(g);
+        return s;
+    }
+    if (e != cudaSuccess) return fail(SSBH_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    const cudaError_t ie = cudaGraphInstantiate(exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+        *exec = nullptr;
+        return fail(SSBH_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ie));
+    }
+    return SSBH_OK;
 }
 
 extern "C" ssbh_status ssbh_plan_run_device(ssbh_plan* pl, const uint32_t* d_input,
@@ -617,44 +695,43 @@ extern "C" ssbh_status ssbh_plan_run_device_sifted(ssbh_plan* pl, const uint32_t
         return fail(SSBH_INVALID_ARGUMENT, "plan_run: streaming plans take stream_begin/chunk/finish");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     pl->last_stream = st;
-    const uint64_t* sk = samp_key ? samp_key : pl->p.samp_key;
-    const uint64_t* hk = hash_key ? hash_key : pl->p.hash_key;
-    // The legacy default stream cannot be captured, and per-phase event timing is only
-    // meaningful on direct launches: launch directly in those cases.
-    if (st == nullptr || pl->timing || !graphs_enabled())
-        return plan_enqueue(pl, d_input, d_keep, d_key, d_lengths, sk, hk, st);
+    const RunArgs r{d_input, d_keep, d_key, d_lengths, samp_key ? samp_key : pl->p.samp_key,
+                    hash_key ? hash_key : pl->p.hash_key};
+    // the legacy default stream cannot be captured: launch directly there
+    if (st == nullptr || !graphs_enabled()) return plan_enqueue(pl, r, st);
     ssbh_plan::GraphKey key{};
     key.st = st;
     key.in = d_input;
     key.key = d_key;
     key.len = d_lengths;
     key.keep = d_keep;
-    std::memcpy(key.sk, sk, 32);
-    std::memcpy(key.hk, hk, 32);
+    std::memcpy(key.sk, r.sk, 32);
+    std::memcpy(key.hk, r.hk, 32);
     key.timing = pl->timing;
-    if (!(pl->exec && key == pl->gkey)) {
-        if (pl->exec) {
-            cudaGraphExecDestroy(pl->exec);
-            pl->exec = nullptr;
+    // untimed: one graph for the whole run; timed: one graph per segment, events between
+    const int nseg = pl->timing ? 4 : 1;
+    if (!(pl->exec[0] && key == pl->gkey)) {
+        for (auto& x : pl->exec)
+            if (x) {
+                cudaGraphExecDestroy(x);
+                x = nullptr;
+            }
+        uint32_t launches = 0;
+        for (int sgi = 0; sgi < nseg; ++sgi) {
+            const int s0 = nseg == 1 ? 0 : sgi, s1 = nseg == 1 ? 4 : sgi + 1;
+            if (auto s = capture(pl, r, s0, s1, st, &pl->exec[sgi], launches)) return s;
         }
-        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        const ssbh_status s = plan_enqueue(pl, d_input, d_keep, d_key, d_lengths, sk, hk, st);
-        cudaGraph_t g = nullptr;
-        const cudaError_t e = cudaStreamEndCapture(st, &g);
-        if (s != SSBH_OK) {
-            if (g) cudaGraphDestroy(g);
-            return s;
-        }
-        if (e != cudaSuccess) return fail(SSBH_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
-        const cudaError_t ie = cudaGraphInstantiate(&pl->exec, g, 0);
-        cudaGraphDestroy(g);
-        if (ie != cudaSuccess) {
-            pl->exec = nullptr;
-            return fail(SSBH_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ie));
-        }
+        pl->launches_per_run = launches;
         pl->gkey = key;
     }
-    CU(cudaGraphLaunch(pl->exec, st));
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        if (nseg > 1) rec(pl, sgi, st);
+        CU(cudaGraphLaunch(pl->exec[sgi], st));
+    }
+    if (nseg > 1) {
+        rec(pl, 4, st);
+        rec(pl, 5, st);
+    }
     return ok();
 }
 
