@@ -181,6 +181,7 @@ __global__ void k_scan_groups(const uint32_t* __restrict__ counts, uint64_t nchu
     const uint64_t c0 = g * group_chunks;
     const uint64_t c1 = min(nchunks, c0 + group_chunks);
     unsigned long long t = 0;
+#pragma unroll 8  // independent loads in flight: the scan is latency-bound
     for (uint64_t c = c0; c < c1; ++c) t += counts[c * nown + jj];
     gsum[g * nown + jj] = t;
 }
@@ -191,6 +192,7 @@ __global__ void k_scan_totals(unsigned long long* __restrict__ gsum, uint64_t ng
     const uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x;
     if (jj >= nown) return;
     unsigned long long run = 0;
+#pragma unroll 8
     for (uint64_t g = 0; g < ngroups; ++g) {
         const unsigned long long t = gsum[g * nown + jj];
         gsum[g * nown + jj] = run;
@@ -210,6 +212,7 @@ __global__ void k_scan_apply(uint32_t* __restrict__ counts, uint64_t nchunks, ui
     const uint64_t c0 = g * group_chunks;
     const uint64_t c1 = min(nchunks, c0 + group_chunks);
     unsigned long long base = gsum[g * nown + jj];
+#pragma unroll 8
     for (uint64_t c = c0; c < c1; ++c) {
         const uint32_t t = counts[c * nown + jj];
         counts[c * nown + jj] = (uint32_t)base;
