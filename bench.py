@@ -14,9 +14,11 @@ s = 1024 sub-blocks, k = 2^19 output bits per sub-block, p = 0.5, seeds 1/2/3.
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 3]
     python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
 
-Multi-GPU: each rank owns a contiguous range of sub-blocks (no data-path collective;
-the input is replicated, sampling is recomputed per rank, owned blocks are hashed);
-timing is the max over ranks of the per-rank device time.
+Multi-GPU (default ``--multi sharded``): each rank owns a contiguous range of sub-blocks,
+samples only its n/N slice of rounds and stores each round's payload straight into the
+owning rank's receive buffer through NVLink peer memory; owners then hash their blocks.
+``--multi replicated`` re-samples all rounds on every rank instead. Timing is the max
+over ranks of the per-rank device time.
 ``--impl reference`` times the reference's own CPU implementation (oracle/_ref: the
 unmodified reference sources compiled by oracle/Makefile) on a bounded sample of the
 same workload on the host cores; rank 0 only.
@@ -37,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "input Gbit/s hashed (sample+Toeplitz)"
 UNIT = "Gbit/s"
+HBM_PEAK_GBS = 6531.6  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth on this pool's B200s)
 
 
 def cfg_desc(cid, c):
@@ -198,6 +201,21 @@ def cpu_baseline_leg(cid, c):
             "sample": f"{nb} sub-blocks of config{cid} shape (n_j~{c['n'] // c['s']}, k={c['k']}) "
                       f"from a {n_s}-round prefix: assign_subblocks + sift_partition + gather + "
                       f"toeplitz_hash, {secs:.1f} s on {min(nb, threads)} threads"}
+
+
+def sampler_line(n, world, stats, sharded):
+    """Sampler phases (Threefry count pass + scans + layout, then the scatter) as achieved HBM
+    GB/s over their algorithmic bytes per rank: input bits read (n/8), the 2 B/round payload
+    written and read back, the reversed sub-block words written (n/8). The count pass is
+    Threefry-bound on the integer ALU (~208 ALU instr/round, profiles/*ncu_sampler*)."""
+    rounds = n // world if sharded else n
+    ms = stats.ms_sample + stats.ms_scatter
+    bytes_ = rounds / 8 + 2 * rounds + 2 * rounds + rounds / 8
+    gbs = bytes_ / (ms * 1e-3) / 1e9 if ms > 0 else None
+    return {"ms": ms, "rounds": rounds, "rounds_per_s": rounds / (ms * 1e-3) if ms else None,
+            "hbm_bytes_algorithmic": int(bytes_), "achieved_gbs": gbs,
+            "hbm_frac": gbs / HBM_PEAK_GBS if gbs else None, "peak_gbs": HBM_PEAK_GBS,
+            "bound": "int-alu (Threefry4x64-20 per round), not HBM"}
 
 
 def main():
@@ -397,12 +415,13 @@ def main():
                 "algorithmic_per_launch": f"sum_j n_j*k/32 = {hash_ops} word-ops (owned blocks)",
                 "peak_source": "measured live in this run: k_lop3_peak (csrc/diag.cu), "
                                "148 SMs x 64 LOP3 lanes/clk at the running SM clock",
-                "hbm_term_ms": (n / 8 + count * k / 8) / 6531.6e9 * 1e3,
+                "hbm_term_ms": (n / 8 + count * k / 8) / (HBM_PEAK_GBS * 1e9) * 1e3,
             },
             "phases_ms_last_step": {"sample_count_scan_layout": stats.ms_sample,
                                     "scatter": stats.ms_scatter, "seeds": stats.ms_seed,
                                     "hash": stats.ms_hash, "total": stats.ms_total},
             "hash_share_of_step": avg_hash_ms / (total_ms / args.steps),
+            "sampler": sampler_line(n, world, stats, sharded),
             "gpu_launches": int(stats.launches) * args.steps,
             "key_sha256_16": key_sha,
             "clocks": clk,

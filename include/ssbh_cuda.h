@@ -255,6 +255,68 @@ ssbh_status ssbh_shard_finish(ssbh_shard* shard, uint32_t* d_key, uint64_t* d_le
 ssbh_status ssbh_shard_check(ssbh_shard* shard, ssbh_extract_stats* stats);
 ssbh_status ssbh_shard_set_timing(ssbh_shard* shard, int enable);
 
+/* ----------------------------------------- protocol rounds (run_extraction's hash stage)
+ * RoundRecord bytes (proj/include/ssbh/pipeline.hpp:15-38): bit 0 BasisAx, 1 BasisBx,
+ * 2 Detected, 3 BitA, 4 BitB, 5 IsTest; is_key_round = Detected && !BasisAx && !BasisBx. */
+typedef struct {
+    uint64_t n_rounds;
+    double p_x;   /* test-basis probability */
+    double e_ph;  /* phase error rate (X/X flips) */
+    double e_bit; /* bit error rate (Z/Z flips) */
+    double p_det; /* detection probability */
+} ssbh_round_params;
+
+/* Reference: simulate_rounds — pipeline.hpp:41, pipeline.cpp:20-55 (streams "basis-a",
+ * "basis-b", "detect", "bit-a", "noise" of `seed`). One byte per round; _device writes
+ * d_rounds on `stream` (asynchronous), the host form copies back (synchronous). Parameter
+ * ranges are the caller's (Bbm92Params::validate); probabilities outside [0,1] ->
+ * SSBH_INVALID_ARGUMENT as bernoulli throws (prf.cpp:97-98). */
+ssbh_status ssbh_simulate_rounds_device(const ssbh_round_params* params, const uint64_t seed[4],
+                                        uint8_t* d_rounds, void* stream);
+ssbh_status ssbh_simulate_rounds(const ssbh_round_params* params, const uint64_t seed[4],
+                                 uint8_t* rounds);
+
+/* run_extraction after the key-length solver (pipeline.cpp:84-136): statistics check on the
+ * test rounds, sift of the key rounds, assign_subblocks(n, s, seed), oversize abort,
+ * bits_per_block = key_length / s, per-block seeds KeyedStream(seed, "hash-seed", j),
+ * toeplitz_hash of gathered bit_a, concatenation. key_length is the caller's
+ * key_length(params, scenario).length (0 when infeasible): the finite-key solver is the
+ * reference's host code and stays there. */
+typedef struct {
+    uint32_t n_subblocks;   /* plan.n_subblocks */
+    uint32_t pad;
+    uint64_t block_limit;   /* plan.block_limit (must be set) */
+    uint64_t seed[4];       /* plan.seed: sampling and hash-seed streams */
+    double eps_abort;       /* plan.eps_abort */
+    double eps_sec, p_x, eta_tol, q_tol; /* Bbm92Params */
+    uint64_t key_length;    /* kl.length */
+} ssbh_extraction_params;
+
+typedef struct {
+    int32_t abort;          /* 0 None, 1 OversizeBlock, 2 Statistics (ExtractionReport::Abort) */
+    uint32_t pad;
+    uint64_t bits_per_block;
+    uint64_t key_bits;      /* bits written to out_key (s * bits_per_block, or 0) */
+    double total_epsilon;
+    double hash_seconds;    /* device time of seed generation + hash (CUDA events) */
+    uint64_t test_rounds;
+    uint64_t phase_errors;  /* c1: detected test rounds with bit_a != bit_b */
+    uint64_t no_detections; /* c2: undetected test rounds */
+    uint64_t key_rounds;    /* sifted length */
+    int32_t lengths_valid;  /* out_lengths written (not for a statistics abort) */
+    uint32_t pad2;
+} ssbh_extraction_result;
+
+/* Host rounds (n bytes); out_key capacity ceil(key_length_floor / 64) words where
+ * key_length_floor = s * (key_length / s); out_lengths has s entries. Synchronous. */
+ssbh_status ssbh_run_extraction(const uint8_t* rounds, uint64_t n_rounds,
+                                const ssbh_extraction_params* params, uint64_t* out_key,
+                                uint64_t* out_lengths, ssbh_extraction_result* result);
+/* Same from device-resident rounds (e.g. ssbh_simulate_rounds_device); host outputs. */
+ssbh_status ssbh_run_extraction_device(const uint8_t* d_rounds, uint64_t n_rounds,
+                                       const ssbh_extraction_params* params, uint64_t* out_key,
+                                       uint64_t* out_lengths, ssbh_extraction_result* result);
+
 /* Synthetic input on the device: p == 0.5 -> KeyedStream(key,"input").bits(n);
  * else bit i = bernoulli(p, i) of the same stream. d_out: ceil(n/32) uint32 words. */
 ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbits,

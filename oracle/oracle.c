@@ -630,3 +630,68 @@ void or_seed_from_int(uint64_t v, uint64_t key[4]) {
     key[2] = 0;
     key[3] = v;
 }
+
+/* ------------------------------------------------------------- protocol rounds */
+
+typedef struct {
+    const uint64_t* key;
+    uint64_t n;
+    double p_x, e_ph, e_bit, p_det;
+    uint64_t t_a, t_b, t_det, t_bit, t_noise;
+    uint8_t* out;
+} rounds_ctx;
+
+/* pipeline.cpp:31-53, one round at a time */
+static void rounds_range(void* arg, uint64_t lo, uint64_t hi, int tid) {
+    (void)tid;
+    const rounds_ctx* c = (const rounds_ctx*)arg;
+    for (uint64_t i = lo; i < hi && i < c->n; ++i) {
+        uint8_t r = 0;
+        const int ax = or_bernoulli(c->key, c->t_a, 0, c->p_x, i) == 1;
+        const int bx = or_bernoulli(c->key, c->t_b, 0, c->p_x, i) == 1;
+        if (ax) r |= 1;
+        if (bx) r |= 2;
+        if (ax && bx) r |= 32;
+        if (or_bernoulli(c->key, c->t_det, 0, c->p_det, i) == 1) {
+            r |= 4;
+            const uint64_t w = or_stream_word(c->key, c->t_bit, 0, i);
+            const int a = (int)(w & 1);
+            int b;
+            if (ax == bx)
+                b = a ^ (or_bernoulli(c->key, c->t_noise, 0, ax ? c->e_ph : c->e_bit, i) == 1);
+            else
+                b = (int)((w >> 1) & 1);
+            if (a) r |= 8;
+            if (b) r |= 16;
+        }
+        c->out[i] = r;
+    }
+}
+
+void or_simulate_rounds(uint64_t n, double p_x, double e_ph, double e_bit, double p_det,
+                        const uint64_t key[4], uint8_t* out, int nthreads) {
+    if (n == 0) return;
+    rounds_ctx c = {key, n, p_x, e_ph, e_bit, p_det, or_tag("basis-a"), or_tag("basis-b"),
+                    or_tag("detect"), or_tag("bit-a"), or_tag("noise"), out};
+    parallel_ranges(n, 1, nthreads, rounds_range, &c);
+}
+
+void or_rounds_split(const uint8_t* rounds, uint64_t n, uint64_t* bits, uint8_t* keep,
+                     uint64_t counts[4]) {
+    memset(bits, 0, sizeof(uint64_t) * ((n + 63) / 64));
+    counts[0] = counts[1] = counts[2] = counts[3] = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint8_t r = rounds[i];
+        const int det = (r >> 2) & 1, a = (r >> 3) & 1, b = (r >> 4) & 1, test = (r >> 5) & 1;
+        if (a) bits[i >> 6] |= 1ull << (i & 63);
+        keep[i] = det && !(r & 1) && !(r & 2);
+        if (test) {
+            ++counts[0];
+            if (!det)
+                ++counts[2];
+            else if (a != b)
+                ++counts[1];
+        }
+        counts[3] += keep[i];
+    }
+}

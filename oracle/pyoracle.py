@@ -399,3 +399,148 @@ def _ref_extract_selected(self, x, n, s, samp, hsh, per_block, k, which):
 
 
 Reference.extract_selected = _ref_extract_selected
+
+
+# ------------------------------------------------------------------ protocol rounds
+def _or_simulate_rounds(self, n, p_x, e_ph, e_bit, p_det, seed, nthreads=0):
+    """oracle.c restatement of simulate_rounds (pipeline.cpp:20-55)."""
+    L = self.L
+    L.or_simulate_rounds.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double,
+                                     U64P, U8P, C.c_int]
+    out = np.zeros(max(n, 1), dtype=np.uint8)
+    L.or_simulate_rounds(n, p_x, e_ph, e_bit, p_det, _p64(key_of(seed)), _p8(out), nthreads)
+    return out[:n]
+
+
+def _or_rounds_split(self, rounds):
+    """(bit_a words, is_key_round bytes, counts {test, c1, c2, key})."""
+    L = self.L
+    L.or_rounds_split.argtypes = [U8P, C.c_uint64, U64P, U8P, U64P]
+    r = np.ascontiguousarray(rounds, dtype=np.uint8)
+    n = len(r)
+    bits = np.zeros(max(nwords(n), 1), dtype=np.uint64)
+    keep = np.zeros(max(n, 1), dtype=np.uint8)
+    counts = np.zeros(4, dtype=np.uint64)
+    L.or_rounds_split(_p8(r), n, _p64(bits), _p8(keep), _p64(counts))
+    return bits[: nwords(n)], keep[:n], [int(c) for c in counts]
+
+
+def _or_run_extraction(self, rounds, ns, block_limit, seed, key_length, eps_sec, p_x, q_tol,
+                       eta_tol=1.0, eps_abort=1e-8):
+    """run_extraction's hash stage restated from the oracle's pieces (pipeline.cpp:84-136):
+    returns (abort, key words, block lengths, bits_per_block). abort: 0/1 oversize/2 stats."""
+    bits, keep, (_, c1, c2, _) = self.rounds_split(rounds)
+    n = len(rounds)
+    px2 = p_x * p_x
+    if c1 / n > px2 * eta_tol * q_tol or c2 / n > px2 * (1.0 - eta_tol):
+        return 2, np.zeros(0, np.uint64), None, 0
+    bpb = key_length // ns
+    a, _ = self.assign_subblocks(n, ns, seed)
+    offsets, _ = self.sift_partition(keep, a, ns)
+    lens = np.diff(offsets).astype(np.uint64)
+    if (lens > block_limit).any():
+        return 1, np.zeros(0, np.uint64), lens, bpb
+    if bpb == 0:
+        return 0, np.zeros(0, np.uint64), lens, 0
+    key, nj = self.extract_sifted(bits, keep, n, ns, seed, seed, True, bpb)
+    assert (nj == lens).all()
+    return 0, key, lens, bpb
+
+
+Oracle.simulate_rounds = _or_simulate_rounds
+Oracle.rounds_split = _or_rounds_split
+Oracle.run_extraction = _or_run_extraction
+
+
+class RefBbm92(C.Structure):
+    """ref_shim.cpp ref_bbm92: the Bbm92Params fields the tests vary (others default)."""
+    _fields_ = [("n_rounds", C.c_uint64), ("p_x", C.c_double), ("e_ph", C.c_double),
+                ("e_bit", C.c_double), ("q_tol", C.c_double), ("eta_tol", C.c_double),
+                ("f_ec", C.c_double), ("p_det", C.c_double), ("eps_sec", C.c_double),
+                ("eps_abort", C.c_double)]
+
+
+def bbm92(n_rounds, p_x=0.02, e_ph=0.0082, e_bit=0.058, q_tol=0.0082, eta_tol=1.0, f_ec=1.16,
+          p_det=1.0, eps_sec=1e-6, eps_abort=1e-8) -> RefBbm92:
+    """Bbm92Params with the reference defaults (bbm92.hpp:14-26)."""
+    return RefBbm92(n_rounds, p_x, e_ph, e_bit, q_tol, eta_tol, f_ec, p_det, eps_sec, eps_abort)
+
+
+def _ref_simulate_rounds(self, params: RefBbm92, seed):
+    L = self.L
+    L.ref_simulate_rounds.restype = C.c_int
+    L.ref_simulate_rounds.argtypes = [C.POINTER(RefBbm92), U64P, U8P]
+    out = np.zeros(max(params.n_rounds, 1), dtype=np.uint8)
+    rc = L.ref_simulate_rounds(C.byref(params), _p64(key_of(seed)), _p8(out))
+    if rc:
+        raise ValueError(f"simulate_rounds failed (code {rc})")
+    return out[: params.n_rounds]
+
+
+def _ref_key_length(self, params: RefBbm92, ns):
+    L = self.L
+    L.ref_key_length.restype = C.c_int
+    L.ref_key_length.argtypes = [C.POINTER(RefBbm92), C.c_uint32, U64P, C.POINTER(C.c_int)]
+    out = np.zeros(1, dtype=np.uint64)
+    feas = C.c_int(0)
+    rc = L.ref_key_length(C.byref(params), ns, _p64(out), C.byref(feas))
+    if rc:
+        raise ValueError(f"key_length failed (code {rc})")
+    return int(out[0]), bool(feas.value)
+
+
+def _ref_plan_block_limit(self, params: RefBbm92, ns):
+    L = self.L
+    L.ref_plan_block_limit.restype = C.c_int
+    L.ref_plan_block_limit.argtypes = [C.POINTER(RefBbm92), C.c_uint32, U64P]
+    out = np.zeros(1, dtype=np.uint64)
+    rc = L.ref_plan_block_limit(C.byref(params), ns, _p64(out))
+    if rc:
+        raise ValueError(f"block_limit failed (code {rc})")
+    return int(out[0])
+
+
+def _ref_run_extraction(self, rounds, params: RefBbm92, ns, block_limit, seed, m_prime=2000):
+    """The reference's run_extraction (pipeline.cpp:75-138). Returns a dict of the
+    ExtractionReport fields (key as uint64 words)."""
+    L = self.L
+    L.ref_run_extraction.restype = C.c_int
+    L.ref_run_extraction.argtypes = [U8P, C.POINTER(RefBbm92), C.c_uint32, C.c_uint64, U64P,
+                                     C.c_uint64, U64P, C.c_uint64, U64P, U64P,
+                                     C.POINTER(C.c_double)]
+    r = np.ascontiguousarray(rounds, dtype=np.uint8)
+    cap = nwords(len(r)) + 2
+    key = np.zeros(cap, dtype=np.uint64)
+    lens = np.zeros(max(ns, 1), dtype=np.uint64)
+    meta = np.zeros(5, dtype=np.uint64)
+    dmeta = (C.c_double * 2)()
+    rc = L.ref_run_extraction(_p8(r), C.byref(params), ns, block_limit, _p64(key_of(seed)),
+                              m_prime, _p64(key), cap, _p64(lens), _p64(meta), dmeta)
+    if rc:
+        raise ValueError(f"run_extraction failed (code {rc})")
+    nlen = int(meta[4])
+    return {"abort": int(meta[0]), "bits_per_block": int(meta[1]), "key_bits": int(meta[2]),
+            "cycle_count": int(meta[3]), "block_lengths": lens[:nlen].copy(),
+            "key": key[: nwords(int(meta[2]))].copy(), "total_epsilon": dmeta[0],
+            "wall_seconds": dmeta[1]}
+
+
+def _ref_timing_model(self, input_len, output_len, kind, ns=1, m_prime=2000, eps_abort=1e-8,
+                      limit_override=0, pad=True):
+    L = self.L
+    L.ref_timing_model.restype = C.c_int
+    L.ref_timing_model.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_uint32, C.c_uint64,
+                                   C.c_double, C.c_uint64, C.c_int, U64P]
+    out = np.zeros(1, dtype=np.uint64)
+    rc = L.ref_timing_model(input_len, output_len, kind, ns, m_prime, eps_abort, limit_override,
+                            int(pad), _p64(out))
+    if rc:
+        raise ValueError(f"timing_model failed (code {rc})")
+    return int(out[0])
+
+
+Reference.simulate_rounds = _ref_simulate_rounds
+Reference.key_length = _ref_key_length
+Reference.plan_block_limit = _ref_plan_block_limit
+Reference.run_extraction = _ref_run_extraction
+Reference.timing_model = _ref_timing_model

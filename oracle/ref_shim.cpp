@@ -1,7 +1,7 @@
 // ref_shim.cpp — extern "C" shim over the UNMODIFIED reference C++ API.
 // TEST / BASELINE INFRASTRUCTURE ONLY. Compiled by oracle/Makefile together with the
 // reference sources where they lie (/root/reference/proj/src/{bitstring,prf,sampling,
-// toeplitz}.cpp) into oracle/_ref/libssbh_ref.so. Nothing of the reference is copied
+// toeplitz,pipeline,bbm92,geat}.cpp) into oracle/_ref/libssbh_ref.so. Nothing of the reference is copied
 // into this repository; this file only calls its public API (proj/include/ssbh/*.hpp)
 // and its thread pool (proj/src/parallel.hpp:13-41).
 //
@@ -16,7 +16,9 @@
 
 #include "parallel.hpp"  // proj/src/parallel.hpp
 #include "ssbh/bitstring.hpp"
+#include "ssbh/bbm92.hpp"
 #include "ssbh/errors.hpp"
+#include "ssbh/pipeline.hpp"
 #include "ssbh/prf.hpp"
 #include "ssbh/sampling.hpp"
 #include "ssbh/toeplitz.hpp"
@@ -303,6 +305,119 @@ double ref_time_sample(uint64_t n_sample, uint32_t s_sample, uint64_t k, double 
         }
     *digest = h;
     return secs;
+}
+
+// ---- protocol rounds / run_extraction (pipeline.hpp:41-99) ------------------------------
+// Flat parameter block for ctypes; the remaining Bbm92Params fields keep their defaults.
+struct ref_bbm92 {
+    uint64_t n_rounds;
+    double p_x, e_ph, e_bit, q_tol, eta_tol, f_ec, p_det, eps_sec, eps_abort;
+};
+
+static Bbm92Params params_of(const ref_bbm92* r) {
+    Bbm92Params p;
+    p.n_rounds = r->n_rounds;
+    p.p_x = r->p_x;
+    p.e_ph = r->e_ph;
+    p.e_bit = r->e_bit;
+    p.q_tol = r->q_tol;
+    p.eta_tol = r->eta_tol;
+    p.f_ec = r->f_ec;
+    p.p_det = r->p_det;
+    p.eps_sec = r->eps_sec;
+    p.eps_abort = r->eps_abort;
+    return p;
+}
+
+int ref_simulate_rounds(const ref_bbm92* rp, const uint64_t seed[4], uint8_t* out) {
+    try {
+        const auto rounds = simulate_rounds(params_of(rp), seed_of(seed));
+        for (std::size_t i = 0; i < rounds.size(); ++i) out[i] = rounds[i].raw;
+        return 0;
+    } catch (...) {
+        return code_of_current();
+    }
+}
+
+// key_length(params, ns == 1 ? full : splitting(ns)) as run_extraction sizes it
+// (pipeline.cpp:115-117).
+int ref_key_length(const ref_bbm92* rp, uint32_t ns, uint64_t* length, int* feasible) {
+    try {
+        const KeyLengthResult kl =
+            key_length(params_of(rp), ns == 1 ? Scenario::full() : Scenario::splitting(ns));
+        *length = kl.length;
+        *feasible = kl.feasible;
+        return 0;
+    } catch (...) {
+        return code_of_current();
+    }
+}
+
+// The reference's plan_for (test_pipeline.cpp:27-35 / ssbh_main.cpp:276-282): block_limit of
+// the sifting probability p_z^2 p_det / ns.
+int ref_plan_block_limit(const ref_bbm92* rp, uint32_t ns, uint64_t* limit) {
+    try {
+        const Bbm92Params p = params_of(rp);
+        const double p_sift = p.p_z() * p.p_z() * p.p_det / static_cast<double>(ns);
+        *limit = block_limit(p.n_rounds, p_sift, p.eps_abort, ns);
+        return 0;
+    } catch (...) {
+        return code_of_current();
+    }
+}
+
+// run_extraction (pipeline.cpp:75-138) on caller rounds. out_key capacity key_cap_words;
+// meta = {abort, bits_per_block, key bits, cycle_count, block_lengths count};
+// dmeta = {total_epsilon, wall_seconds}.
+int ref_run_extraction(const uint8_t* rounds_raw, const ref_bbm92* rp, uint32_t ns,
+                       uint64_t block_limit_, const uint64_t seed[4], uint64_t m_prime,
+                       uint64_t* out_key, uint64_t key_cap_words, uint64_t* out_lengths,
+                       uint64_t meta[5], double dmeta[2]) {
+    try {
+        const Bbm92Params p = params_of(rp);
+        std::vector<RoundRecord> rounds(p.n_rounds);
+        for (uint64_t i = 0; i < p.n_rounds; ++i) rounds[i].raw = rounds_raw[i];
+        SamplingPlan plan;
+        plan.n_subblocks = ns;
+        plan.eps_abort = p.eps_abort;
+        plan.block_limit = block_limit_;
+        plan.seed = seed_of(seed);
+        BlockingParams blk;
+        blk.m_prime = m_prime;
+        const ExtractionReport rep = run_extraction(rounds, plan, p, blk);
+        meta[0] = static_cast<uint64_t>(rep.abort);
+        meta[1] = rep.bits_per_block;
+        meta[2] = rep.key.size();
+        meta[3] = rep.cycle_count;
+        meta[4] = rep.block_lengths.size();
+        dmeta[0] = rep.total_epsilon;
+        dmeta[1] = rep.wall_seconds;
+        if ((rep.key.size() + 63) / 64 > key_cap_words) return 8;
+        to_words(rep.key, out_key);
+        for (std::size_t j = 0; j < rep.block_lengths.size(); ++j)
+            out_lengths[j] = rep.block_lengths[j];
+        return 0;
+    } catch (...) {
+        return code_of_current();
+    }
+}
+
+// timing_model (pipeline.hpp:60-62, pipeline.cpp:139-160). kind: 0 full, 1 splitting,
+// 2 small-block.
+int ref_timing_model(uint64_t input_len, uint64_t output_len, int kind, uint32_t ns,
+                     uint64_t m_prime, double eps_abort, uint64_t limit_override, int pad,
+                     uint64_t* out) {
+    try {
+        const Scenario sc = kind == 0   ? Scenario::full()
+                            : kind == 1 ? Scenario::splitting(ns)
+                                        : Scenario::small_block(ns);
+        BlockingParams blk;
+        blk.m_prime = m_prime;
+        *out = timing_model(input_len, output_len, sc, blk, eps_abort, limit_override, pad != 0);
+        return 0;
+    } catch (...) {
+        return code_of_current();
+    }
 }
 
 }  // extern "C"

@@ -46,7 +46,8 @@ ABI_SYMBOLS = (
     "ssbh_plan_run_device_sifted", "ssbh_plan_run_host_sifted", "ssbh_extract_sifted",
     "ssbh_shard_create", "ssbh_shard_destroy", "ssbh_shard_info", "ssbh_shard_ipc_handle",
     "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
-    "ssbh_shard_check", "ssbh_shard_set_timing",
+    "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
+    "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
 )
 
 
@@ -98,6 +99,29 @@ class ExtractStats(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class RoundParams(C.Structure):
+    _fields_ = [("n_rounds", C.c_uint64), ("p_x", C.c_double), ("e_ph", C.c_double),
+                ("e_bit", C.c_double), ("p_det", C.c_double)]
+
+
+class ExtractionParams(C.Structure):
+    _fields_ = [("n_subblocks", C.c_uint32), ("pad", C.c_uint32), ("block_limit", C.c_uint64),
+                ("seed", C.c_uint64 * 4), ("eps_abort", C.c_double), ("eps_sec", C.c_double),
+                ("p_x", C.c_double), ("eta_tol", C.c_double), ("q_tol", C.c_double),
+                ("key_length", C.c_uint64)]
+
+
+class ExtractionResult(C.Structure):
+    _fields_ = [("abort", C.c_int32), ("pad", C.c_uint32), ("bits_per_block", C.c_uint64),
+                ("key_bits", C.c_uint64), ("total_epsilon", C.c_double),
+                ("hash_seconds", C.c_double), ("test_rounds", C.c_uint64),
+                ("phase_errors", C.c_uint64), ("no_detections", C.c_uint64),
+                ("key_rounds", C.c_uint64), ("lengths_valid", C.c_int32), ("pad2", C.c_uint32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if not f.startswith("pad")}
 
 
 def _load():
@@ -211,6 +235,17 @@ def _load():
     L.ssbh_measure_lop3_peak.restype = st
     L.ssbh_measure_lop3_peak.argtypes = [C.c_uint32, C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
+    L.ssbh_simulate_rounds_device.restype = st
+    L.ssbh_simulate_rounds_device.argtypes = [C.POINTER(RoundParams), U64P, C.c_void_p,
+                                              C.c_void_p]
+    L.ssbh_simulate_rounds.restype = st
+    L.ssbh_simulate_rounds.argtypes = [C.POINTER(RoundParams), U64P, U8P]
+    L.ssbh_run_extraction.restype = st
+    L.ssbh_run_extraction.argtypes = [U8P, C.c_uint64, C.POINTER(ExtractionParams), U64P, U64P,
+                                      C.POINTER(ExtractionResult)]
+    L.ssbh_run_extraction_device.restype = st
+    L.ssbh_run_extraction_device.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(ExtractionParams),
+                                             U64P, U64P, C.POINTER(ExtractionResult)]
     return L
 
 
@@ -402,6 +437,57 @@ def extract(x, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0
         _check(lib.ssbh_extract_sifted(C.byref(params), _p64(x), _p64(kp), _p64(key),
                                        _p64(lens), C.byref(st)))
     return key[: nwords(owned * k)], lens, st
+
+
+# ------------------------------------------------------------ protocol rounds (pipeline.hpp)
+def round_params(n, p_x, e_ph, e_bit, p_det=1.0) -> RoundParams:
+    rp = RoundParams()
+    rp.n_rounds, rp.p_x, rp.e_ph, rp.e_bit, rp.p_det = n, p_x, e_ph, e_bit, p_det
+    return rp
+
+
+def simulate_rounds(n, p_x, e_ph, e_bit, p_det, seed) -> np.ndarray:
+    """simulate_rounds (pipeline.cpp:20-55) on the GPU: one RoundRecord byte per round."""
+    out = np.zeros(max(int(n), 1), dtype=np.uint8)
+    k = key_of(seed)
+    _check(lib.ssbh_simulate_rounds(C.byref(round_params(n, p_x, e_ph, e_bit, p_det)), _p64(k),
+                                    _p8(out)))
+    return out[:n]
+
+
+def simulate_rounds_device(n, p_x, e_ph, e_bit, p_det, seed, d_rounds_ptr, stream=0):
+    k = key_of(seed)
+    _check(lib.ssbh_simulate_rounds_device(C.byref(round_params(n, p_x, e_ph, e_bit, p_det)),
+                                           _p64(k), C.c_void_p(d_rounds_ptr),
+                                           C.c_void_p(stream)))
+
+
+def extraction_params(ns, block_limit, seed, key_length, eps_sec, p_x, q_tol, eta_tol=1.0,
+                      eps_abort=1e-8) -> ExtractionParams:
+    ep = ExtractionParams()
+    ep.n_subblocks, ep.block_limit, ep.key_length = ns, block_limit, key_length
+    ep.seed[:] = [int(v) for v in key_of(seed)]
+    ep.eps_abort, ep.eps_sec, ep.p_x, ep.eta_tol, ep.q_tol = eps_abort, eps_sec, p_x, eta_tol, q_tol
+    return ep
+
+
+def run_extraction(rounds, params: ExtractionParams, d_rounds_ptr: int | None = None,
+                   n: int | None = None):
+    """run_extraction's statistics check + sift + sample + per-block hash on the GPU
+    (ssbh_run_extraction). Returns (key words, block lengths, result)."""
+    ns = params.n_subblocks
+    key_bits = ns * (params.key_length // ns) if ns else 0
+    key = np.zeros(max(nwords(key_bits), 1), dtype=np.uint64)
+    lens = np.zeros(max(ns, 1), dtype=np.uint64)
+    res = ExtractionResult()
+    if d_rounds_ptr is None:
+        r = np.ascontiguousarray(rounds, dtype=np.uint8)
+        _check(lib.ssbh_run_extraction(_p8(r) if len(r) else None, len(r), C.byref(params),
+                                       _p64(key), _p64(lens), C.byref(res)))
+    else:
+        _check(lib.ssbh_run_extraction_device(C.c_void_p(d_rounds_ptr), n, C.byref(params),
+                                              _p64(key), _p64(lens), C.byref(res)))
+    return key[: nwords(res.key_bits)], lens[:ns], res
 
 
 class Plan:

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1231,4 +1232,141 @@ extern "C" ssbh_status ssbh_shard_check(ssbh_shard* sh, ssbh_extract_stats* stat
 extern "C" ssbh_status ssbh_shard_set_timing(ssbh_shard* sh, int enable) {
     if (!sh) return fail(SSBH_INVALID_ARGUMENT, "null shard");
     return ssbh_plan_set_timing(sh->plan, enable);
+}
+
+// ======================================================================== protocol rounds
+static ssbh_status check_round_params(const ssbh_round_params* p) {
+    if (!p) return fail(SSBH_INVALID_ARGUMENT, "simulate_rounds: null params");
+    const double ps[4] = {p->p_x, p->e_ph, p->e_bit, p->p_det};
+    for (double v : ps)
+        if (!(v >= 0.0 && v <= 1.0)) return fail(SSBH_INVALID_ARGUMENT, "bernoulli: p outside [0,1]");
+    return SSBH_OK;
+}
+
+extern "C" ssbh_status ssbh_simulate_rounds_device(const ssbh_round_params* params,
+                                                   const uint64_t seed[4], uint8_t* d_rounds,
+                                                   void* stream) {
+    if (auto s = check_round_params(params)) return s;
+    if (params->n_rounds == 0) return ok();
+    if (!seed || !d_rounds) return fail(SSBH_INVALID_ARGUMENT, "simulate_rounds: null argument");
+    NEED_DEVICE();
+    launch_simulate_rounds(seed, params->n_rounds, params->p_x, params->e_ph, params->e_bit,
+                           params->p_det, d_rounds, static_cast<cudaStream_t>(stream));
+    return check_launch("simulate_rounds");
+}
+
+extern "C" ssbh_status ssbh_simulate_rounds(const ssbh_round_params* params,
+                                            const uint64_t seed[4], uint8_t* rounds) {
+    if (auto s = check_round_params(params)) return s;
+    if (params->n_rounds == 0) return ok();
+    if (!seed || !rounds) return fail(SSBH_INVALID_ARGUMENT, "simulate_rounds: null argument");
+    NEED_DEVICE();
+    DBuf d;
+    CU(d.alloc(params->n_rounds));
+    if (auto s = ssbh_simulate_rounds_device(params, seed, d.as<uint8_t>(), nullptr)) return s;
+    CU(cudaMemcpy(rounds, d.p, params->n_rounds, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+// pipeline.cpp:84-136 from device-resident RoundRecord bytes. The two host decisions of the
+// reference (statistics abort, then oversize abort / bits_per_block) need the counters and
+// the block lengths, so the call synchronises twice.
+extern "C" ssbh_status ssbh_run_extraction_device(const uint8_t* d_rounds, uint64_t n,
+                                                  const ssbh_extraction_params* p,
+                                                  uint64_t* out_key, uint64_t* out_lengths,
+                                                  ssbh_extraction_result* res) {
+    if (!p || !res) return fail(SSBH_INVALID_ARGUMENT, "run_extraction: null argument");
+    if (p->n_subblocks == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "run_extraction: plan.n_subblocks must be positive");
+    if (p->block_limit == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "run_extraction: plan.block_limit must be set");
+    if (n == 0 || !d_rounds)
+        return fail(SSBH_INVALID_ARGUMENT, "run_extraction: round count does not match params");
+    NEED_DEVICE();
+    std::memset(res, 0, sizeof *res);
+    const uint32_t ns = p->n_subblocks;
+    // pipeline.cpp:86-88, same operation order
+    res->total_epsilon = static_cast<double>(ns) * (p->eps_sec - p->eps_abort) /
+                             static_cast<double>(ns) +
+                         p->eps_abort;
+
+    const uint64_t w32 = (n + 31) / 32;
+    DBuf bits, keep, cnt;
+    CU(bits.alloc(round_up(w32, 2) * 4));
+    CU(keep.alloc(round_up(w32, 2) * 4));
+    CU(cnt.alloc(4 * 8));
+    CU(cudaMemset(cnt.p, 0, 4 * 8));
+    launch_rounds_split(d_rounds, n, bits.as<uint32_t>(), keep.as<uint32_t>(),
+                        cnt.as<unsigned long long>(), nullptr);
+    if (auto s = check_launch("rounds_split")) return s;
+    uint64_t c[4];
+    CU(cudaMemcpy(c, cnt.p, sizeof c, cudaMemcpyDeviceToHost));
+    res->test_rounds = c[0];
+    res->phase_errors = c[1];
+    res->no_detections = c[2];
+    res->key_rounds = c[3];
+
+    // statistics check (pipeline.cpp:90-104)
+    const double nd = static_cast<double>(n);
+    const double px2 = p->p_x * p->p_x;
+    if (static_cast<double>(c[1]) / nd > px2 * p->eta_tol * p->q_tol ||
+        static_cast<double>(c[2]) / nd > px2 * (1.0 - p->eta_tol)) {
+        res->abort = 2;
+        return ok();
+    }
+
+    // sift + sample + abort_check + per-block seeds + hash (pipeline.cpp:107-136)
+    const uint64_t bpb = p->key_length / ns;
+    res->bits_per_block = bpb;
+    ssbh_extract_params ep{};
+    ep.n_rounds = n;
+    ep.n_subblocks = ns;
+    ep.per_block_seed = 1;
+    ep.out_bits = bpb ? bpb : 32;  // bpb == 0: lengths only, the hash output is discarded
+    std::memcpy(ep.samp_key, p->seed, 32);
+    std::memcpy(ep.hash_key, p->seed, 32);
+    ep.block_limit = p->block_limit;
+    ssbh_plan* pl = nullptr;
+    if (auto s = ssbh_plan_create(&ep, &pl)) return s;
+    std::unique_ptr<ssbh_plan, ssbh_status (*)(ssbh_plan*)> guard(pl, ssbh_plan_destroy);
+    ssbh_plan_set_timing(pl, 1);
+    DBuf key, len;
+    const uint64_t key_w64 = words64((uint64_t)ns * ep.out_bits);
+    CU(key.alloc(key_w64 * 8 + 16));
+    CU(len.alloc((size_t)ns * 8));
+    CU(cudaMemset(key.p, 0, key_w64 * 8 + 16));
+    if (auto s = ssbh_plan_run_device_sifted(pl, bits.as<uint32_t>(), keep.as<uint32_t>(),
+                                             key.as<uint32_t>(), len.as<uint64_t>(), nullptr,
+                                             nullptr, nullptr))
+        return s;
+    ssbh_extract_stats st{};
+    ssbh_status s = ssbh_plan_check(pl, &st);
+    if (s == SSBH_ABORT_OVERSIZE) {
+        res->abort = 1;
+        res->bits_per_block = 0;  // the reference returns before sizing the key
+        s = SSBH_OK;
+    } else if (s == SSBH_INVALID_ARGUMENT && bpb == 0 && st.min_len == 0) {
+        s = SSBH_OK;  // no hashing when nothing is extractable: empty blocks are fine
+    }
+    if (s != SSBH_OK) return s;
+    if (out_lengths) CU(cudaMemcpy(out_lengths, len.p, (size_t)ns * 8, cudaMemcpyDeviceToHost));
+    res->lengths_valid = out_lengths != nullptr;
+    if (res->abort || bpb == 0) return ok();
+    res->key_bits = (uint64_t)ns * bpb;
+    res->hash_seconds = (st.ms_seed + st.ms_hash) * 1e-3;
+    if (out_key) CU(cudaMemcpy(out_key, key.p, words64(res->key_bits) * 8, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_run_extraction(const uint8_t* rounds, uint64_t n,
+                                           const ssbh_extraction_params* p, uint64_t* out_key,
+                                           uint64_t* out_lengths, ssbh_extraction_result* res) {
+    if (!p || !res) return fail(SSBH_INVALID_ARGUMENT, "run_extraction: null argument");
+    if (n == 0 || !rounds)
+        return fail(SSBH_INVALID_ARGUMENT, "run_extraction: round count does not match params");
+    NEED_DEVICE();
+    DBuf d;
+    CU(d.alloc(n));
+    CU(cudaMemcpy(d.p, rounds, n, cudaMemcpyHostToDevice));
+    return ssbh_run_extraction_device(d.as<uint8_t>(), n, p, out_key, out_lengths, res);
 }

@@ -67,6 +67,14 @@ void launch_stream_bits(const uint64_t key[4], uint64_t tag, uint64_t sub, uint6
 void launch_make_input(const uint64_t key[4], double p, uint64_t nbits, uint32_t* d_out32,
                        cudaStream_t st);
 
+// ---- protocol rounds (run_extraction front end, rounds.cu) ----------------------------
+void launch_simulate_rounds(const uint64_t key[4], uint64_t n, double p_x, double e_ph,
+                            double e_bit, double p_det, uint8_t* d_rounds, cudaStream_t st);
+// bits32 = bit_a, keep32 = is_key_round (ceil(n/32) words each); d_counts4 (pre-zeroed):
+// test rounds, test rounds with bit_a != bit_b, undetected test rounds, key rounds.
+void launch_rounds_split(const uint8_t* d_rounds, uint64_t n, uint32_t* d_bits32,
+                         uint32_t* d_keep32, unsigned long long* d_counts4, cudaStream_t st);
+
 // ---- sampler -----------------------------------------------------------------------
 struct SamplerGeom {
     uint64_t n;

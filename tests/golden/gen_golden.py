@@ -21,7 +21,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from oracle.pyoracle import Oracle, Reference, key_of, nwords  # noqa: E402
+from oracle.pyoracle import Oracle, Reference, bbm92, key_of, nwords  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
 
@@ -34,11 +34,59 @@ def fnv(o, a):
     return f"{o.fnv(np.asarray(a, dtype=np.uint64)):016x}"
 
 
+def sim_params(n, **kw):
+    """test_pipeline.cpp:14-25 desk-scale simulation point."""
+    d = dict(p_x=0.05, e_ph=0.0082, e_bit=0.02, q_tol=0.02, eps_sec=1e-5, eps_abort=1e-8)
+    d.update(kw)
+    return bbm92(n, **d)
+
+
+def pipeline_cases(ref, o):
+    """run_extraction cases of test_pipeline.cpp (deterministic, sized by the reference's own
+    key-length solver, oversize and statistics aborts) plus two infeasible/large-ns points."""
+    aa, bb = [0xAAAAAAAAAAAAAAAA] * 4, [0xBBBBBBBBBBBBBBBB] * 4
+    cases = [  # name, sim params, extraction params, ns, seed, block_limit override
+        ("deterministic_ns4", sim_params(1000000), None, 4, aa, 0),
+        ("single_block", sim_params(300000), None, 1, bb, 0),
+        ("oversize", sim_params(50000), None, 4, 0, 10),
+        ("statistics", sim_params(200000, e_ph=0.4, q_tol=0.4), sim_params(200000), 4, 0, 0),
+        ("infeasible_ns16", sim_params(1000000), None, 16, aa, 0),
+        ("ns64", sim_params(8000000, p_x=0.03), None, 64, 5, 0),
+        ("p_det_eta", sim_params(1000000, p_det=0.7, eta_tol=0.6), None, 2, 6, 0),
+        ("ns3_nonpow2", sim_params(1500000), None, 3, 9, 0),
+    ]
+    out = {}
+    for name, sim, hon, ns, seed, lim_over in cases:
+        hon = hon or sim
+        t = time.time()
+        rounds = ref.simulate_rounds(sim, seed)
+        lim = lim_over or ref.plan_block_limit(hon, ns)
+        kl, feas = ref.key_length(hon, ns)
+        rep = ref.run_extraction(rounds, hon, ns, lim, seed)
+        pad = np.zeros(nwords(len(rounds) * 8) * 8, dtype=np.uint8)
+        pad[: len(rounds)] = rounds
+        out[name] = {
+            "sim": {f: getattr(sim, f) for f, _ in sim._fields_},
+            "params": {f: getattr(hon, f) for f, _ in hon._fields_},
+            "ns": ns, "seed": hexw(key_of(seed)), "block_limit": lim,
+            "key_length": kl if feas else 0, "feasible": feas,
+            "rounds_fnv": fnv(o, pad.view(np.uint64)),
+            "abort": rep["abort"], "bits_per_block": rep["bits_per_block"],
+            "key_bits": rep["key_bits"], "key_fnv": fnv(o, rep["key"]),
+            "cycle_count": rep["cycle_count"], "total_epsilon": rep["total_epsilon"],
+            "block_lengths": [int(v) for v in rep["block_lengths"]],
+            "ref_seconds": round(time.time() - t, 2)}
+        print(name, {k: v for k, v in out[name].items() if k != "block_lengths"}, flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config3", action="store_true")
     ap.add_argument("--config4", action="store_true")
     ap.add_argument("--config5", action="store_true")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="run_extraction / simulate_rounds cases (pipeline.cpp)")
     ap.add_argument("--only-large", action="store_true", help="skip the small vectors")
     args = ap.parse_args()
     ref, o = Reference(), Oracle()
@@ -167,6 +215,8 @@ def main():
             "ref_seconds": round(time.time() - t, 1)}
         print(5, ext["5"], flush=True)
     g["extract"] = ext
+    if args.pipeline:
+        g["pipeline"] = pipeline_cases(ref, o)
     json.dump(g, open(OUT, "w"), indent=1)
     print("wrote", OUT)
 

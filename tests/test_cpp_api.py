@@ -11,7 +11,8 @@ BIN = os.path.join(ROOT, "tests", "cpp", "bin")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["test_prf", "test_toeplitz", "test_sampling", "test_extract"])
+@pytest.mark.parametrize("suite", ["test_prf", "test_toeplitz", "test_sampling", "test_extract",
+                                   "test_pipeline"])
 def test_cpp_suite(suite):
     exe = os.path.join(BIN, suite)
     if not os.path.exists(exe):

@@ -4,6 +4,8 @@ Bit-exact for everything (integer/bit work). Mirrors the reference's own tests
 (proj/tests/test_{prf,toeplitz,sampling,bitstring,pipeline}.cpp) and extends them to the
 BASELINE configs. Every call below runs sm_100a kernels; there is no CPU fallback.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -426,6 +428,45 @@ def test_config4_full_blocks_vs_reference(dev, oracle, golden):
     plan.close()
 
 
+# ------------------------------------- config 5 (2^37 rounds streamed in 8 chunks, k = 2^21)
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("SSBH_RUN_CONFIG5") != "1",
+                    reason="~9 min on one B200: set SSBH_RUN_CONFIG5=1")
+def test_config5_streamed_vs_reference(dev, oracle, golden):
+    """BASELINE configs[4] on one GPU through the streaming plan (8 input chunks of 2^34
+    rounds): all 32768 n_j and sub-blocks 0 and 32767 against the reference's own streaming
+    computation (gen_golden.py --config5, 1728 s of reference CPU time)."""
+    import torch
+
+    want = golden["extract"].get("5")
+    if want is None:
+        pytest.skip("golden config-5 anchors not generated")
+    c = dev.CONFIGS[5]
+    n, s, k = c["n"], c["s"], c["k"]
+    chunk = n // 8
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=False, chunk_bits=chunk)
+    d_in = torch.zeros(n // 32, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+    plan.stream_begin()
+    for ci in range(8):
+        plan.stream_chunk(ci, d_in.data_ptr() + ci * (chunk // 8))
+    plan.stream_finish(d_key.data_ptr(), d_len.data_ptr())
+    st = plan.check()
+    nj = d_len.cpu().numpy().view(np.uint64)
+    assert f"{oracle.fnv(nj):016x}" == want["nj_fnv"]
+    assert int(nj.min()) == want["nj_min"] and int(nj.max()) == want["nj_max"]
+    assert int(nj[0]) == want["nj_0"] and int(nj[-1]) == want["nj_last"]
+    kw = k // 64
+    key64 = d_key.view(torch.int64)
+    for q, j in enumerate(want["which"]):
+        blk = key64[j * kw:(j + 1) * kw].cpu().numpy().view(np.uint64)
+        assert f"{oracle.fnv(blk):016x}" == want["block_fnv"][q], j
+    assert int(st.hash_word_ops) == n * k // 32
+    plan.close()
+
+
 # ------------------------------------------------------- sifted runs (keep flags)
 def test_extract_sifted_matches_oracle(dev, oracle):
     rng = np.random.default_rng(21)
@@ -444,3 +485,110 @@ def test_extract_sifted_matches_oracle(dev, oracle):
         got, nj, _ = dev.extract(x, n, s, k, 41, 42, per_block=pb, keep=keep_words)
         assert (nj == wnj).all()
         assert (got == want).all(), (n, s, k, pb, pk)
+
+
+# --------------------------------------- protocol rounds + run_extraction (pipeline.cpp)
+def _rounds_fnv(oracle, rounds):
+    pad = np.zeros((len(rounds) + 7) // 8 * 8, dtype=np.uint8)
+    pad[: len(rounds)] = rounds
+    return f"{oracle.fnv(pad.view(np.uint64)):016x}"
+
+
+def test_simulate_rounds_gpu(dev, oracle, golden):
+    """GPU simulate_rounds vs the reference's rounds (golden) and the oracle, host and
+    device entry points, aligned and unaligned device buffers, ragged lengths."""
+    import torch
+
+    for name, c in golden["pipeline"].items():
+        sp = c["sim"]
+        r = dev.simulate_rounds(sp["n_rounds"], sp["p_x"], sp["e_ph"], sp["e_bit"], sp["p_det"],
+                                words(c["seed"]))
+        assert _rounds_fnv(oracle, r) == c["rounds_fnv"], name
+    rng = np.random.default_rng(71)
+    for n in (1, 3, 4, 31, 33, 1000, 65537):
+        args = (n, float(rng.uniform(0.01, 0.9)), float(rng.uniform(0, 0.3)),
+                float(rng.uniform(0, 0.5)), float(rng.uniform(0, 1)))
+        seed = [int(v) for v in rng.integers(0, 1 << 62, 4)]
+        want = oracle.simulate_rounds(*args, seed)
+        assert (dev.simulate_rounds(*args, seed) == want).all(), n
+        buf = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+        for off in (0, 1, 3):
+            buf.zero_()
+            dev.simulate_rounds_device(*args, seed, buf.data_ptr() + off)
+            torch.cuda.synchronize()
+            got = buf.cpu().numpy()
+            assert (got[off:off + n] == want).all() and not got[:off].any(), (n, off)
+            assert not got[off + n:].any(), (n, off)
+    with pytest.raises(ValueError):
+        dev.simulate_rounds(10, 1.5, 0.0, 0.0, 1.0, 0)
+
+
+def _extraction_params(dev, c):
+    hp = c["params"]
+    return dev.extraction_params(c["ns"], c["block_limit"], words(c["seed"]), c["key_length"],
+                                 hp["eps_sec"], hp["p_x"], hp["q_tol"], hp["eta_tol"],
+                                 hp["eps_abort"])
+
+
+def test_run_extraction_gpu_golden(dev, oracle, golden):
+    """ssbh_run_extraction vs the reference's ExtractionReport (run_extraction,
+    pipeline.cpp:75-138): abort kind, bits_per_block, block lengths, key digest, epsilon."""
+    for name, c in golden["pipeline"].items():
+        sp = c["sim"]
+        rounds = oracle.simulate_rounds(sp["n_rounds"], sp["p_x"], sp["e_ph"], sp["e_bit"],
+                                        sp["p_det"], words(c["seed"]))
+        key, lens, res = dev.run_extraction(rounds, _extraction_params(dev, c))
+        assert res.abort == c["abort"], name
+        assert res.bits_per_block == c["bits_per_block"], name
+        assert res.total_epsilon == c["total_epsilon"], name
+        if c["abort"] != 2:
+            assert res.lengths_valid and [int(v) for v in lens] == c["block_lengths"], name
+        assert res.key_bits == c["key_bits"], name
+        assert f"{oracle.fnv(key):016x}" == c["key_fnv"], name
+
+
+def test_run_extraction_gpu_device_rounds(dev, oracle, golden):
+    """Device-resident rounds (simulate_rounds_device -> run_extraction_device), including an
+    unaligned rounds pointer (byte-wise split path), vs the oracle's restatement."""
+    import torch
+
+    c = golden["pipeline"]["deterministic_ns4"]
+    sp = c["sim"]
+    n = sp["n_rounds"]
+    want = oracle.simulate_rounds(n, sp["p_x"], sp["e_ph"], sp["e_bit"], sp["p_det"],
+                                  words(c["seed"]))
+    for off in (0, 5):
+        buf = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+        dev.simulate_rounds_device(n, sp["p_x"], sp["e_ph"], sp["e_bit"], sp["p_det"],
+                                   words(c["seed"]), buf.data_ptr() + off)
+        torch.cuda.synchronize()
+        key, lens, res = dev.run_extraction(None, _extraction_params(dev, c),
+                                            d_rounds_ptr=buf.data_ptr() + off, n=n)
+        assert f"{oracle.fnv(key):016x}" == c["key_fnv"], off
+        assert [int(v) for v in lens] == c["block_lengths"]
+        _, _, counts = oracle.rounds_split(want)
+        assert [res.test_rounds, res.phase_errors, res.no_detections, res.key_rounds] == counts
+        assert res.hash_seconds > 0
+
+
+def test_run_extraction_gpu_random_vs_oracle(dev, oracle):
+    """Random shapes (non-power-of-two s, p_det < 1, eta_tol < 1, odd bit counts) vs the
+    oracle's restatement of the hash stage."""
+    rng = np.random.default_rng(73)
+    for trial in range(6):
+        n = int(rng.integers(20000, 400000))
+        ns = int(rng.choice([1, 2, 3, 5, 8, 13]))
+        p_x, p_det = float(rng.uniform(0.02, 0.2)), float(rng.uniform(0.6, 1.0))
+        eta = float(rng.uniform(0.3, 1.0)) if trial % 2 else 1.0
+        seed = [int(v) for v in rng.integers(0, 1 << 62, 4)]
+        rounds = oracle.simulate_rounds(n, p_x, 0.01, 0.02, p_det, seed)
+        kl = int(rng.integers(0, 4000))
+        lim = n  # generous cap
+        args = (ns, lim, seed, kl, 1e-6, p_x, 0.05, eta, 1e-8)
+        want_abort, want_key, want_lens, want_bpb = oracle.run_extraction(rounds, *args)
+        key, lens, res = dev.run_extraction(rounds, dev.extraction_params(*args))
+        assert res.abort == want_abort, trial
+        assert res.bits_per_block == want_bpb, trial
+        if want_abort != 2:
+            assert (lens == want_lens).all(), trial
+        assert (key == want_key).all(), trial

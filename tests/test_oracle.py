@@ -200,3 +200,51 @@ def test_cycle_estimate(oracle, reference):
     # proj/tests/reference_values.hpp:84
     assert oracle.cycle_estimate(96040000, 6054000, 2000)[0] == 290821228000
     assert reference.cycle_estimate(96040000, 6054000, 2000)[0] == 290821228000
+
+
+# ------------------------------------------------- protocol rounds / run_extraction (pipeline)
+def _rounds_fnv(oracle, rounds):
+    pad = np.zeros((len(rounds) + 7) // 8 * 8, dtype=np.uint8)
+    pad[: len(rounds)] = rounds
+    return f"{oracle.fnv(pad.view(np.uint64)):016x}"
+
+
+def test_simulate_rounds_golden(oracle, golden):
+    """oracle.c simulate_rounds vs rounds frozen from the reference (gen_golden --pipeline)."""
+    for name, c in golden["pipeline"].items():
+        sp = c["sim"]
+        r = oracle.simulate_rounds(sp["n_rounds"], sp["p_x"], sp["e_ph"], sp["e_bit"],
+                                   sp["p_det"], words(c["seed"]))
+        assert _rounds_fnv(oracle, r) == c["rounds_fnv"], name
+
+
+def test_simulate_rounds_vs_reference(oracle, reference):
+    from oracle.pyoracle import bbm92
+
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        n = int(rng.integers(1, 70000))
+        p = bbm92(n, p_x=float(rng.uniform(0.01, 0.9)), e_ph=float(rng.uniform(0, 0.3)),
+                  e_bit=float(rng.uniform(0, 0.5)), q_tol=0.45,
+                  p_det=float(rng.uniform(0, 1)))
+        seed = [int(v) for v in rng.integers(0, 1 << 62, 4)]
+        want = reference.simulate_rounds(p, seed)
+        got = oracle.simulate_rounds(n, p.p_x, p.e_ph, p.e_bit, p.p_det, seed)
+        assert (want == got).all()
+
+
+def test_run_extraction_golden(oracle, golden):
+    """run_extraction's hash stage restated (pyoracle Oracle.run_extraction) vs the
+    reference's ExtractionReport frozen by gen_golden --pipeline."""
+    for name, c in golden["pipeline"].items():
+        sp, hp = c["sim"], c["params"]
+        r = oracle.simulate_rounds(sp["n_rounds"], sp["p_x"], sp["e_ph"], sp["e_bit"],
+                                   sp["p_det"], words(c["seed"]))
+        abort, key, lens, bpb = oracle.run_extraction(
+            r, c["ns"], c["block_limit"], words(c["seed"]), c["key_length"], hp["eps_sec"],
+            hp["p_x"], hp["q_tol"], hp["eta_tol"], hp["eps_abort"])
+        assert abort == c["abort"], name
+        assert bpb == c["bits_per_block"], name
+        if abort != 2:
+            assert [int(v) for v in lens] == c["block_lengths"], name
+        assert f"{oracle.fnv(key):016x}" == c["key_fnv"], name
