@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) k_rounds_split(const uint8_t* __restrict_
             rec[4] = b.x; rec[5] = b.y; rec[6] = b.z; rec[7] = b.w;
         } else {
             for (int q = 0; q < 8; ++q) rec[q] = 0;
-            for (uint64_t i = w * 32; i < n; ++i)
+            for (uint64_t i = w * 32; i < n && i < (w + 1) * 32; ++i)
                 rec[(i & 31) >> 2] |= (uint32_t)rounds[i] << (8 * (i & 3));
         }
         uint32_t bw = 0, kw = 0;
