@@ -172,6 +172,13 @@ __global__ void __launch_bounds__(256) k_count_global(Src src, uint64_t n, uint3
 }
 
 // counts[c][jj] -> group sums gsum[g][jj] (u64)
+// The count table is scanned along chunks per key in three steps: group sums, an
+// exclusive scan of the group sums (one warp per key), and the in-place rewrite of every
+// count to its chunk's start rank. Loads are issued in batches of kScanBatch before any
+// store: the compiler cannot hoist a load of counts[c+1] above the store to counts[c]
+// (same array), which serialised the rewrite on DRAM latency.
+constexpr int kScanBatch = 8;
+
 __global__ void k_scan_groups(const uint32_t* __restrict__ counts, uint64_t nchunks,
                               uint32_t nown, uint64_t group_chunks,
                               unsigned long long* __restrict__ gsum) {
@@ -181,24 +188,51 @@ __global__ void k_scan_groups(const uint32_t* __restrict__ counts, uint64_t nchu
     const uint64_t c0 = g * group_chunks;
     const uint64_t c1 = min(nchunks, c0 + group_chunks);
     unsigned long long t = 0;
-#pragma unroll 8  // independent loads in flight: the scan is latency-bound
-    for (uint64_t c = c0; c < c1; ++c) t += counts[c * nown + jj];
+    for (uint64_t c = c0; c < c1; c += kScanBatch) {
+        uint32_t v[kScanBatch];
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) v[e] = c + e < c1 ? counts[(c + e) * nown + jj] : 0u;
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) t += v[e];
+    }
     gsum[g * nown + jj] = t;
 }
 
-// exclusive scan over groups per key, totals -> nj
+// exclusive scan over groups per key (one warp per key, lane-contiguous group ranges),
+// totals -> nj
 __global__ void k_scan_totals(unsigned long long* __restrict__ gsum, uint64_t ngroups,
                               uint32_t nown, unsigned long long* __restrict__ nj) {
-    const uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x;
-    if (jj >= nown) return;
-    unsigned long long run = 0;
-#pragma unroll 8
-    for (uint64_t g = 0; g < ngroups; ++g) {
-        const unsigned long long t = gsum[g * nown + jj];
-        gsum[g * nown + jj] = run;
-        run += t;
+    const uint32_t jj = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (jj >= nown) return;  // warp-uniform
+    const uint64_t per = (ngroups + 31) / 32;
+    const uint64_t g0 = min(ngroups, lane * per), g1 = min(ngroups, g0 + per);
+    unsigned long long mine = 0;
+    for (uint64_t g = g0; g < g1; g += kScanBatch) {
+        unsigned long long v[kScanBatch];
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) v[e] = g + e < g1 ? gsum[(g + e) * nown + jj] : 0ull;
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) mine += v[e];
     }
-    nj[jj] = run;
+    unsigned long long inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+    }
+    unsigned long long run = inc - mine;
+    if (lane == 31) nj[jj] = inc;
+    for (uint64_t g = g0; g < g1; g += kScanBatch) {
+        unsigned long long v[kScanBatch];
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) v[e] = g + e < g1 ? gsum[(g + e) * nown + jj] : 0ull;
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) {
+            if (g + e < g1) gsum[(g + e) * nown + jj] = run;
+            run += v[e];
+        }
+    }
 }
 
 // counts -> per-chunk start ranks (in place, u32: device path limits n_j < 2^32, checked
@@ -212,11 +246,15 @@ __global__ void k_scan_apply(uint32_t* __restrict__ counts, uint64_t nchunks, ui
     const uint64_t c0 = g * group_chunks;
     const uint64_t c1 = min(nchunks, c0 + group_chunks);
     unsigned long long base = gsum[g * nown + jj];
-#pragma unroll 8
-    for (uint64_t c = c0; c < c1; ++c) {
-        const uint32_t t = counts[c * nown + jj];
-        counts[c * nown + jj] = (uint32_t)base;
-        base += t;
+    for (uint64_t c = c0; c < c1; c += kScanBatch) {
+        uint32_t v[kScanBatch];
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) v[e] = c + e < c1 ? counts[(c + e) * nown + jj] : 0u;
+#pragma unroll
+        for (int e = 0; e < kScanBatch; ++e) {
+            if (c + e < c1) counts[(c + e) * nown + jj] = (uint32_t)base;
+            base += v[e];
+        }
     }
 }
 
@@ -460,11 +498,14 @@ void count_launch(const Src& src, uint64_t n, uint32_t nkeys, int cs, uint64_t n
     const uint64_t groups = (n + 31) / 32;
     const size_t row_bytes = (size_t)nkeys * 4;
     if (row_bytes * 8 <= 96 * 1024) {
-        // enough (chunk, part) work units for ~2 waves of 64 warps per SM
+        // enough (chunk, part) work units for ~2 waves of 64 warps per SM, but every unit
+        // keeps >= max(8, nkeys/8) 32-round groups so that zeroing and flushing its
+        // nkeys-bin histogram stays small against the Threefry work
         const uint64_t gpc = (1ull << cs) / 32;
         const uint64_t want = (uint64_t)sm_count() * 128;
+        const uint64_t gmin = std::max<uint64_t>(8, nkeys / 8);
         const uint32_t parts = (uint32_t)std::min<uint64_t>(
-            gpc, std::max<uint64_t>(1, (want + nchunks - 1) / nchunks));
+            std::max<uint64_t>(1, gpc / gmin), std::max<uint64_t>(1, (want + nchunks - 1) / nchunks));
         const uint64_t units = nchunks * parts;
         const uint64_t blocks = std::min<uint64_t>((units + 7) / 8, (uint64_t)sm_count() * 8);
         const size_t shm = row_bytes * 8;
@@ -584,7 +625,8 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
     // u16 needs V <= 0x7ffe so that 0x7fff can mark sifted-out rounds
     g.payload_bytes = (!has_keep && s < 32768) ? 2 : 4;
     // warp-chunk: enough chunks for latency hiding in the scatter pass, bounded count table
-    int cs = std::min(10, max_chunk_shift);
+    // (256-round chunks at the low end: small inputs still spread over every SM)
+    int cs = std::min(8, max_chunk_shift);
     auto table_bytes = [&](int shift) {
         const uint64_t nc = (n + (1ull << shift) - 1) >> shift;
         return nc * (uint64_t)nown * 4ull;
@@ -637,7 +679,7 @@ void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d
     if (g.nown == 0) return;
     const dim3 grid((g.nown + 255) / 256, (unsigned)g.ngroups);
     k_scan_groups<<<grid, 256, 0, st>>>(d_counts, g.nchunks, g.nown, g.group_chunks, d_gsum);
-    k_scan_totals<<<(g.nown + 255) / 256, 256, 0, st>>>(d_gsum, g.ngroups, g.nown, d_nj);
+    k_scan_totals<<<(g.nown + 7) / 8, 256, 0, st>>>(d_gsum, g.ngroups, g.nown, d_nj);
     k_scan_apply<<<grid, 256, 0, st>>>(d_counts, g.nchunks, g.nown, g.group_chunks, d_gsum);
 }
 

@@ -147,11 +147,22 @@ __global__ void __launch_bounds__(kLayoutThreads) k_layout(Layout lay, uint32_t 
         }
         __syncthreads();
     }
-    atomicMax(&s_max, my_max);
-    atomicMin(&s_min, my_min);
-    atomicAdd(&s_ops, my_ops);
-    atomicAdd(&s_sum, my_sum);
-    atomicOr(&s_flags, my_flags);
+    // warp reductions first: 64-bit shared atomicMax/Min are CAS loops, 1024-way contended
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
+        my_min = min(my_min, __shfl_xor_sync(0xffffffffu, my_min, o));
+        my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
+        my_sum += __shfl_xor_sync(0xffffffffu, my_sum, o);
+        my_flags |= __shfl_xor_sync(0xffffffffu, my_flags, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&s_max, my_max);
+        atomicMin(&s_min, my_min);
+        atomicAdd(&s_ops, my_ops);
+        atomicAdd(&s_sum, my_sum);
+        atomicOr(&s_flags, my_flags);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         lay.yoff[nown] = carry[0];
