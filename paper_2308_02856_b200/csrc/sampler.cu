@@ -142,13 +142,20 @@ __global__ void __launch_bounds__(256) k_count_rows(Src src, uint64_t n, uint32_
         __syncwarp();
         const uint64_t g0 = c * gpc + part * gpc / parts;
         const uint64_t g1 = min(ngroups, c * gpc + (part + 1) * gpc / parts);
-        for (uint64_t g = g0; g < g1; ++g) {
-            const uint32_t jj = src(g, lane);
+        auto tally = [&](uint32_t jj) {
             const uint32_t peers = __match_any_sync(0xffffffffu, jj);
             if (jj != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
                 hist[jj] += (uint32_t)__popc(peers);
             __syncwarp();
+        };
+        uint64_t g = g0;
+        for (; g + 1 < g1; g += 2) {  // two independent Threefry chains per lane (ILP)
+            const uint32_t ja = src(g, lane);
+            const uint32_t jb = src(g + 1, lane);
+            tally(ja);
+            tally(jb);
         }
+        if (g < g1) tally(src(g, lane));
         for (uint32_t t = lane; t < nkeys; t += 32)
             if (hist[t]) atomicAdd(counts + c * nkeys + t, hist[t]);
         __syncwarp();
@@ -637,7 +644,9 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
     g.chunk_shift = cs;
     g.nchunks = (n + (1ull << cs) - 1) >> cs;
     if (g.nchunks == 0) g.nchunks = 1;
-    g.group_chunks = 64;
+    // scan groups: enough (group, key) threads to fill the GPU, at most 64 chunks deep
+    g.group_chunks = std::min<uint64_t>(
+        64, std::max<uint64_t>(8, g.nchunks * (uint64_t)std::max<uint32_t>(nown, 1) / (148ull * 2048)));
     g.ngroups = (g.nchunks + g.group_chunks - 1) / g.group_chunks;
     return g;
 }
