@@ -6,13 +6,22 @@
 //       file mode of cmd_extract (ssbh_main.cpp:306-345): the master seed keys both the
 //       sampling and the per-block "hash-seed" streams (sub = j), L/S bits per block, strict
 //       oversize abort against block_limit(N, 1/S, eps_abort, S) (N when S == 1).
+//   ssbh-b200 extract --simulate --n-rounds N --key-length L [--ns S] [--seed HEX64]
+//                     [--p-x P] [--e-ph E] [--e-bit E] [--q-tol Q] [--eta-tol T] [--p-det D]
+//                     [--eps-sec E] [--eps-abort E] [--out FILE] [--partition-csv FILE]
+//       simulate mode of cmd_extract (ssbh_main.cpp:274-303): simulate_rounds + run_extraction
+//       on the GPU. L is key_length(params, scenario).length from the reference's finite-key
+//       solver (out of scope here, see pipeline.hpp); the block cap is block_limit(N,
+//       p_z^2 p_det / S, eps_abort, S) as the reference derives it.
+//   ssbh-b200 limit --n N --p-sift P --eps-abort E [--m M]
+//       cmd_limit (ssbh_main.cpp:435-440): prints block_limit(N, P, E, M).
 //   ssbh-b200 bench --sizes A,B,... [--ns S] [--seed HEX64] [--out-ratio R]
 //       cmd_bench (ssbh_main.cpp:368-426): direct hash of the whole input vs sub-block
 //       hashing, measured on the GPU, beside the FPGA cycle-model ratio
 //       (cycle_estimate / timing_model semantics, pipeline.cpp:142-163).
 //
 // Exit codes follow ssbh_main.cpp:26-33: 0 ok, 2 parse/invalid, 3 infeasible,
-// 4 oversize abort, 6 io; device failures exit 7.
+// 4 oversize abort, 5 statistics abort, 6 io; device failures exit 7.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +34,7 @@
 #include "ssbh/bitstring.hpp"
 #include "ssbh/errors.hpp"
 #include "ssbh/extract.hpp"
+#include "ssbh/pipeline.hpp"
 #include "ssbh/prf.hpp"
 #include "ssbh/sampling.hpp"
 #include "ssbh/toeplitz.hpp"
@@ -33,7 +43,15 @@ using namespace ssbh;
 
 namespace {
 
-enum : int { kOk = 0, kParse = 2, kInfeasible = 3, kAbortOversize = 4, kIo = 6, kDevice = 7 };
+enum : int {
+    kOk = 0,
+    kParse = 2,
+    kInfeasible = 3,
+    kAbortOversize = 4,
+    kAbortStats = 5,
+    kIo = 6,
+    kDevice = 7
+};
 
 struct Args {
     std::string cmd, in, out, partition_csv, seed_hex = std::string(64, '0');
@@ -41,6 +59,12 @@ struct Args {
     std::uint32_t ns = 1;
     double eps_abort = 1e-8, out_ratio = 0.06303;
     std::vector<std::uint64_t> sizes;
+    // simulate mode (Bbm92Params defaults, bbm92.hpp:14-26) and limit
+    bool simulate = false;
+    Bbm92Params params;
+    std::uint64_t key_length = 0, limit_n = 0, limit_m = 1;
+    bool have_key_length = false;
+    double p_sift = 0;
 };
 
 std::uint64_t parse_u64(const std::string& s) {
@@ -51,7 +75,7 @@ std::uint64_t parse_u64(const std::string& s) {
 }
 
 Args parse(int argc, char** argv) {
-    if (argc < 2) throw std::invalid_argument("usage: ssbh-b200 extract|bench [options]");
+    if (argc < 2) throw std::invalid_argument("usage: ssbh-b200 extract|limit|bench [options]");
     Args a;
     a.cmd = argv[1];
     for (int i = 2; i < argc; ++i) {
@@ -69,6 +93,21 @@ Args parse(int argc, char** argv) {
         else if (f == "--ns") a.ns = static_cast<std::uint32_t>(parse_u64(val()));
         else if (f == "--eps-abort") a.eps_abort = std::stod(val());
         else if (f == "--out-ratio") a.out_ratio = std::stod(val());
+        else if (f == "--simulate") a.simulate = true;
+        else if (f == "--n-rounds") a.params.n_rounds = parse_u64(val());
+        else if (f == "--p-x") a.params.p_x = std::stod(val());
+        else if (f == "--e-ph") a.params.e_ph = std::stod(val());
+        else if (f == "--e-bit") a.params.e_bit = std::stod(val());
+        else if (f == "--q-tol") a.params.q_tol = std::stod(val());
+        else if (f == "--eta-tol") a.params.eta_tol = std::stod(val());
+        else if (f == "--p-det") a.params.p_det = std::stod(val());
+        else if (f == "--eps-sec") a.params.eps_sec = std::stod(val());
+        else if (f == "--key-length") {
+            a.key_length = parse_u64(val());
+            a.have_key_length = true;
+        } else if (f == "--n") a.limit_n = parse_u64(val());
+        else if (f == "--m") a.limit_m = parse_u64(val());
+        else if (f == "--p-sift") a.p_sift = std::stod(val());
         else if (f == "--sizes") {
             std::stringstream ss(val());
             std::string tok;
@@ -109,17 +148,17 @@ int cmd_extract(const Args& a) {
     const ExtractResult r = extract(data, a.ns, a.out_bits / a.ns, seed, seed, opt);
     const double secs =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (r.aborted) {  // no partition dump on an abort (ssbh_main.cpp:347-357)
+        report += "abort: oversize_block\n";
+        emit("", report);
+        return kAbortOversize;
+    }
     if (!a.partition_csv.empty()) {
         const Partition part = assign_subblocks(a.in_bits, a.ns, seed);
         std::string dump = "round_index,v_i,kept\n";
         for (std::uint64_t i = 0; i < a.in_bits; ++i)
             dump += std::to_string(i) + "," + std::to_string(part.assignment[i]) + ",1\n";
         emit(a.partition_csv, dump);
-    }
-    if (r.aborted) {
-        report += "abort: oversize_block\n";
-        emit("", report);
-        return kAbortOversize;
     }
     report += "key_length_bits: " + std::to_string(r.key.size()) + "\n";
     report += "hash_seconds: " + std::to_string(secs) + "\n";
@@ -129,13 +168,71 @@ int cmd_extract(const Args& a) {
     return kOk;
 }
 
-// FPGA cycle model of the reference (pipeline.cpp:142-163): full vs splitting(ns), padded
-// to the abort limit.
+// simulate mode (ssbh_main.cpp:274-303): rounds and the extraction's data path on the GPU
+int cmd_extract_simulate(const Args& a) {
+    if (!a.have_key_length)
+        throw std::invalid_argument(
+            "extract --simulate: --key-length required (the finite-key solver stays host-side)");
+    if (a.ns == 0) throw std::invalid_argument("scenario: n_subblocks must be positive");
+    const MasterSeed seed = MasterSeed::from_hex(a.seed_hex);
+    Bbm92Params p = a.params;
+    p.eps_abort = a.eps_abort;
+    const auto rounds = simulate_rounds(p, seed);
+    SamplingPlan plan;
+    plan.n_subblocks = a.ns;
+    plan.eps_abort = p.eps_abort;
+    const double p_sift = p.p_z() * p.p_z() * p.p_det / static_cast<double>(a.ns);
+    plan.block_limit = block_limit(p.n_rounds, p_sift, plan.eps_abort, a.ns);
+    plan.seed = seed;
+    const ExtractionReport rep = run_extraction(rounds, plan, p, a.key_length);
+    std::string report = "# b200: seed " + seed.to_hex() + ", ns " + std::to_string(a.ns) + "\n";
+    report += "mode: simulate\n";
+    report += "block_limit: " + std::to_string(plan.block_limit) + "\n";
+    report += "bits_per_block: " + std::to_string(rep.bits_per_block) + "\n";
+    report += "key_length_bits: " + std::to_string(rep.key.size()) + "\n";
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.17g", rep.total_epsilon);
+    report += std::string("total_epsilon: ") + buf + "\n";
+    report += "modeled_cycles: " + std::to_string(rep.cycle_count) + "\n";
+    std::snprintf(buf, sizeof buf, "%.6g", rep.wall_seconds);
+    report += std::string("hash_seconds: ") + buf + "\n";
+    report += "block_lengths:";
+    for (const auto b : rep.block_lengths) report += " " + std::to_string(b);
+    report += "\n";
+    if (rep.abort == ExtractionReport::Abort::OversizeBlock) {
+        report += "abort: oversize_block\n";
+        emit("", report);
+        return kAbortOversize;
+    }
+    if (rep.abort == ExtractionReport::Abort::Statistics) {
+        report += "abort: statistics\n";
+        emit("", report);
+        return kAbortStats;
+    }
+    if (!a.partition_csv.empty()) {
+        const Partition part = assign_subblocks(p.n_rounds, a.ns, seed);
+        std::string dump = "round_index,v_i,kept\n";
+        for (std::uint64_t i = 0; i < rounds.size(); ++i)
+            dump += std::to_string(i) + "," + std::to_string(part.assignment[i]) + "," +
+                    (rounds[i].is_key_round() ? "1" : "0") + "\n";
+        emit(a.partition_csv, dump);
+    }
+    if (!a.out.empty()) rep.key.write_file(a.out);
+    emit("", report);
+    return kOk;
+}
+
+int cmd_limit(const Args& a) {
+    std::printf("%llu\n", static_cast<unsigned long long>(
+                               block_limit(a.limit_n, a.p_sift, a.eps_abort, a.limit_m)));
+    return kOk;
+}
+
+// FPGA cycle model of the reference: full vs splitting(ns) padded to the abort limit
+// (timing_model, pipeline.cpp:139-160).
 std::uint64_t model_cycles(std::uint64_t in, std::uint64_t out, std::uint32_t ns, double eps) {
     const BlockingParams blk;
-    if (ns == 1) return cycle_estimate(in, out, blk.m_prime);
-    const std::uint64_t limit = block_limit(in, 1.0 / ns, eps, ns);
-    return ns * cycle_estimate(limit, (out + ns - 1) / ns, blk.m_prime);
+    return timing_model(in, out, ns == 1 ? Scenario::full() : Scenario::splitting(ns), blk, eps);
 }
 
 int cmd_bench(const Args& a) {
@@ -194,7 +291,8 @@ int cmd_bench(const Args& a) {
 int main(int argc, char** argv) {
     try {
         const Args a = parse(argc, argv);
-        if (a.cmd == "extract") return cmd_extract(a);
+        if (a.cmd == "extract") return a.simulate ? cmd_extract_simulate(a) : cmd_extract(a);
+        if (a.cmd == "limit") return cmd_limit(a);
         if (a.cmd == "bench") return cmd_bench(a);
         throw std::invalid_argument("unknown command " + a.cmd);
     } catch (const infeasible_error& e) {

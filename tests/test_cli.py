@@ -79,14 +79,61 @@ def test_cli_abort_and_partition_csv(tmp_path, oracle):
             "--partition-csv", "part.csv", cwd=tmp_path)
     limit, _ = oracle.block_limit(n, 1 / ns, 0.999, ns)
     a, counts = oracle.assign_subblocks(n, ns, SEED_KEY)
-    if int(counts.max()) > limit:
-        assert r.returncode == 4 and "abort: oversize_block" in r.stdout
-        assert not (tmp_path / "k.bin").exists()
-    else:
-        assert r.returncode == 0
+    assert int(counts.max()) > limit
+    assert r.returncode == 4 and "abort: oversize_block" in r.stdout
+    # an abort writes neither the key nor the partition table (ssbh_main.cpp:347-357)
+    assert not (tmp_path / "k.bin").exists() and not (tmp_path / "part.csv").exists()
+    r = run("extract", "--in", "in.bin", "--in-bits", str(n), "--out-bits", "800", "--ns",
+            str(ns), "--seed", SEED_HEX, "--out", "k.bin", "--partition-csv", "part.csv",
+            cwd=tmp_path)
+    assert r.returncode == 0, r.stderr
     rows = (tmp_path / "part.csv").read_text().splitlines()
     assert rows[0] == "round_index,v_i,kept" and len(rows) == n + 1
     assert all(int(rows[1 + i].split(",")[1]) == int(a[i]) for i in range(0, n, 997))
+
+
+def test_cli_limit_matches_reference(tmp_path, oracle):
+    # cmd_limit (ssbh_main.cpp:435-440): host scalar, no GPU needed
+    for n, p, eps, m in ((1000000, 0.2256, 1e-8, 4), (96040000, 0.05, 1e-8, 20),
+                         (5000, 0.5, 0.1, 1)):
+        r = run("limit", "--n", str(n), "--p-sift", repr(p), "--eps-abort", repr(eps), "--m",
+                str(m), cwd=tmp_path)
+        assert r.returncode == 0, r.stderr
+        want, err = oracle.block_limit(n, p, eps, m)
+        assert err == 0 and int(r.stdout) == want
+
+
+@pytest.mark.gpu
+def test_cli_simulate_matches_reference_report(tmp_path, oracle, golden):
+    """extract --simulate (ssbh_main.cpp:274-303) on the reference's deterministic case, and
+    the statistics abort (exit 5), against golden.json["pipeline"]."""
+    c = golden["pipeline"]["deterministic_ns4"]
+    sp = c["sim"]
+    args = ["extract", "--simulate", "--n-rounds", str(sp["n_rounds"]), "--p-x", repr(sp["p_x"]),
+            "--e-ph", repr(sp["e_ph"]), "--e-bit", repr(sp["e_bit"]), "--q-tol",
+            repr(sp["q_tol"]), "--eps-sec", repr(sp["eps_sec"]), "--ns", str(c["ns"]),
+            "--seed", "a" * 64, "--key-length", str(c["key_length"])]
+    r = run(*args, "--out", "key.bin", "--partition-csv", "part.csv", cwd=tmp_path)
+    assert r.returncode == 0, r.stderr
+    rep = dict(l.split(": ", 1) for l in r.stdout.splitlines() if ": " in l and l[0] != "#")
+    assert int(rep["block_limit"]) == c["block_limit"]
+    assert int(rep["bits_per_block"]) == c["bits_per_block"]
+    assert int(rep["key_length_bits"]) == c["key_bits"]
+    assert int(rep["modeled_cycles"]) == c["cycle_count"]
+    assert float(rep["total_epsilon"]) == c["total_epsilon"]
+    assert [int(v) for v in rep["block_lengths"].split()] == c["block_lengths"]
+    key = read_bits(tmp_path / "key.bin", c["key_bits"])
+    assert f"{oracle.fnv(key[: (c['key_bits'] + 63) // 64]):016x}" == c["key_fnv"]
+    rows = (tmp_path / "part.csv").read_text().splitlines()
+    assert len(rows) == sp["n_rounds"] + 1
+    # half the test rounds undetected against a 0.9 transmission tolerance: c2/n ~ p_x^2/2 >
+    # p_x^2 (1 - eta_tol) -> statistics abort, exit 5, no key / partition written
+    r = run("extract", "--simulate", "--n-rounds", "200000", "--p-x", "0.05", "--p-det", "0.5",
+            "--eta-tol", "0.9", "--ns", "4", "--key-length", "1000", "--out", "k2.bin",
+            "--partition-csv", "p2.csv", cwd=tmp_path)
+    assert r.returncode == 5 and "abort: statistics" in r.stdout, r.stdout + r.stderr
+    assert not (tmp_path / "k2.bin").exists() and not (tmp_path / "p2.csv").exists()
+    assert run("extract", "--simulate", "--n-rounds", "1000", cwd=tmp_path).returncode == 2
 
 
 @pytest.mark.gpu
