@@ -57,7 +57,9 @@ def log2s(v):
 def config_dict(cid, c, world):
     return {
         "workload": f"config{cid}: n={log2s(c['n'])} rounds, s={c['s']} sub-blocks, "
-                    f"k={c['k']} out bits/sub-block, p={c['p']} ({cfg_desc(cid, c)})",
+                    f"k={c['k']} out bits/sub-block, p={c['p']} ({cfg_desc(cid, c)})"
+                    + (" [n OVERRIDDEN by --rounds: not a BASELINE shape]"
+                       if c.get("rounds_override") else ""),
         "n_bits": c["n"], "n_subblocks": c["s"], "out_bits_per_block": c["k"], "p": c["p"],
         "seed_mode": "per-block (hash-seed sub=j)" if c["per_block"] else "shared (hash-seed sub=0)",
         "seeds": {"input": c["seed_in"], "sampling": c["seed_samp"], "hash": c["seed_hash"]},
@@ -230,6 +232,8 @@ def main():
     ap.add_argument("--multi", default="sharded", choices=["sharded", "replicated"],
                     help="N>1: sharded sampling + peer-memory owner exchange, or every rank "
                          "re-sampling all rounds")
+    ap.add_argument("--rounds", type=int, default=0,
+                    help="testing aid: override n (the line's config then names the override)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -239,7 +243,10 @@ def main():
     import paper_2308_02856_b200 as P
 
     cid = args.config
-    c = P.CONFIGS[cid]
+    c = dict(P.CONFIGS[cid])
+    if args.rounds:
+        c["n"] = args.rounds
+        c["rounds_override"] = True
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, cid, c)
@@ -352,7 +359,8 @@ def main():
             stream.synchronize()
         e2e_s = time.perf_counter() - t0
         same = True
-        e2e = {"h2d": int(x_host.numel() * 8), "d2h": int(key_words64 * 8)}
+        e2e = {"h2d": int(x_host.numel() * 8), "d2h": int(key_words64 * 8),
+               "api": "ssbh_shard_sample/exchange/finish (C-ABI) via multigpu.ShardedExtractor"}
     elif not streaming:
         x_host = d_in.cpu().view(torch.int64).pin_memory()
         key_host = torch.empty(key_words64, dtype=torch.int64).pin_memory()
@@ -365,9 +373,40 @@ def main():
             plan.run_host_ptrs(x_host.data_ptr(), key_host.data_ptr(), len_host.data_ptr())
         e2e_s = time.perf_counter() - t0
         same = bool(torch.equal(key_host.cuda().view(torch.int32), d_key))
-        e2e = {"h2d": int(x_host.numel() * 8), "d2h": int(key_words64 * 8 + count * 8)}
+        e2e = {"h2d": int(x_host.numel() * 8), "d2h": int(key_words64 * 8 + count * 8),
+               "api": "ssbh_plan_run_host (C-ABI)"}
     else:
-        e2e_s = float("nan")
+        # streaming (config 5): the 16 GiB input stays in host memory; each step stages every
+        # chunk through one pinned buffer (host copy + H2D inside the region) and reads the key
+        # back, so the host<->device traffic of the whole job is timed
+        cw = chunk_bits // 32
+        x_host = d_in.cpu()
+        pinned = torch.empty(cw, dtype=torch.int32).pin_memory()
+        d_chunk = torch.empty(cw, dtype=torch.int32, device="cuda")
+        key_host = torch.empty(key_words64, dtype=torch.int64)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            plan.stream_begin(stream.cuda_stream)
+            for ci in range(8):
+                pinned.copy_(x_host[ci * cw:(ci + 1) * cw])
+                with torch.cuda.stream(stream):
+                    d_chunk.copy_(pinned, non_blocking=True)
+                plan.stream_chunk(ci, d_chunk.data_ptr(), stream.cuda_stream)
+                stream.synchronize()  # pinned buffer reused by the next chunk
+            plan.stream_finish(d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                key_host.copy_(d_key.view(torch.int64)[:key_words64])
+            stream.synchronize()
+        e2e_s = time.perf_counter() - t0
+        check()
+        same = bool(torch.equal(key_host.cuda().view(torch.int32), d_key))
+        e2e = {"h2d": int(n // 8), "d2h": int(key_words64 * 8),
+               "api": "ssbh_plan_stream_begin/chunk/finish (C-ABI), chunks staged through "
+                      "pinned memory"}
+        del x_host
 
     # ---- gather the owned key slices in block order (the only inter-GPU exchange) --------
     import hashlib
@@ -429,12 +468,8 @@ def main():
         if e2e is not None:
             line["e2e"] = {"value": n * e2e_steps / e2e_s / 1e9, "unit": UNIT,
                            "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
-                           "steps": e2e_steps, "api": "ssbh_plan_run_host (C-ABI)",
+                           "steps": e2e_steps, "api": e2e["api"],
                            "key_matches_device_run": same}
-        else:
-            line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None,
-                           "d2h_bytes_per_step": None,
-                           "note": "streaming config: input resident in HBM only"}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline_leg(cid, c)
