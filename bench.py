@@ -383,7 +383,7 @@ def main():
         x_host = d_in.cpu()
         pinned = torch.empty(cw, dtype=torch.int32).pin_memory()
         d_chunk = torch.empty(cw, dtype=torch.int32, device="cuda")
-        key_host = torch.empty(key_words64, dtype=torch.int64)
+        key_host = torch.empty(key_words64, dtype=torch.int64).pin_memory()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
