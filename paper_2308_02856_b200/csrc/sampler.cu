@@ -620,6 +620,25 @@ ScatterArgs scatter_args(const SamplerGeom& g, uint32_t* d_offsets,
     return a;
 }
 
+// Count-table geometry knobs (dev A/B switches; defaults are the measured choice).
+int table_budget_shift() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("SSBH_TABLE_BUDGET_SHIFT");
+        v = e ? std::atoi(e) : 7;
+    }
+    return v;
+}
+
+uint64_t max_table_chunks() {
+    static uint64_t v = 0;
+    if (!v) {
+        const char* e = std::getenv("SSBH_MAX_CHUNKS");
+        v = e ? std::strtoull(e, nullptr, 10) : 16384ull;
+    }
+    return v;
+}
+
 }  // namespace
 
 SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,
@@ -638,9 +657,10 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
         const uint64_t nc = (n + (1ull << shift) - 1) >> shift;
         return nc * (uint64_t)nown * 4ull;
     };
-    // table budget: 256 MiB, or 1/16 of the input bytes for very large n (config 5)
-    const uint64_t budget = std::max<uint64_t>(256ull << 20, n / 128);
-    while (cs < max_chunk_shift && (((n >> cs) > 16384ull) || table_bytes(cs) > budget)) ++cs;
+    // table budget: 256 MiB, or n / 2^budget_shift bytes for very large n (configs 4-5)
+    const uint64_t budget = std::max<uint64_t>(256ull << 20, n >> table_budget_shift());
+    const uint64_t max_chunks = max_table_chunks();
+    while (cs < max_chunk_shift && (((n >> cs) > max_chunks) || table_bytes(cs) > budget)) ++cs;
     g.chunk_shift = cs;
     g.nchunks = (n + (1ull << cs) - 1) >> cs;
     if (g.nchunks == 0) g.nchunks = 1;
