@@ -129,8 +129,13 @@ class ClockSampler:
 
 def cpu_sample_shape(cid, c, threads):
     """Bounded CPU sample of the workload: T sub-blocks of the config's shape drawn by the
-    reference sampler from a T*(n/s)-round prefix, hashed on T threads."""
+    reference sampler from a T*m-round prefix, hashed on T threads. The reference's hash costs
+    ~k/128 u64 XORs per input bit whatever n_j is, so the per-bit rate is kept while m is cut
+    to ~20 s of work per thread for large k (m = n/s up to config 3; 2^19 for config 4, 2^18
+    for config 5)."""
     m = c["n"] // c["s"]
+    while m > 1024 and m * (c["k"] / 128) / 3e8 > 20:
+        m //= 2
     t = max(1, min(threads, 64, c["s"]))
     return t * m, t, t  # n_sample, s_sample, nblocks
 
@@ -144,7 +149,7 @@ def run_reference(args, cid, c):
     except FileNotFoundError:
         ref, kind = None, "port"
     n_s, s_s, nb = cpu_sample_shape(cid, c, threads)
-    sample = (f"{nb} sub-blocks of config{cid} shape (n_j~{c['n'] // c['s']}, k={c['k']}) sampled "
+    sample = (f"{nb} sub-blocks (n_j~{n_s // s_s}, k={c['k']}: config{cid}'s k) sampled "
               f"by assign_subblocks from a {n_s}-round prefix; assign_subblocks + sift_partition "
               f"+ gather + toeplitz_hash on {min(nb, threads)} threads")
 
@@ -200,7 +205,7 @@ def cpu_baseline_leg(cid, c):
         o.extract(x, n_s, s_s, c["seed_samp"], c["seed_hash"], c["per_block"], c["k"])
         secs, bits, kind = time.perf_counter() - t0, n_s, "port"
     return {"value": bits / secs / 1e9, "unit": UNIT, "cores": min(nb, threads), "kind": kind,
-            "sample": f"{nb} sub-blocks of config{cid} shape (n_j~{c['n'] // c['s']}, k={c['k']}) "
+            "sample": f"{nb} sub-blocks (n_j~{n_s // s_s}, k={c['k']}: config{cid}'s k) "
                       f"from a {n_s}-round prefix: assign_subblocks + sift_partition + gather + "
                       f"toeplitz_hash, {secs:.1f} s on {min(nb, threads)} threads"}
 
