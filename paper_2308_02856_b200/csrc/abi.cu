@@ -359,6 +359,10 @@ struct ssbh_plan {
         bool timing;
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
     } gkey{};
+    // two-level split (large key spaces, see internal.h BucketGeom)
+    bool bucketed = false;
+    BucketGeom bg{};
+    DBuf counts_a, gsum_a, tot_a, staging, counts_b, gsum_b, nj_b;
     // streaming plans (no payload buffer; input fed chunk by chunk)
     bool streaming = false;
     uint64_t chunk_bits = 0;
@@ -374,6 +378,9 @@ static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const ui
                                 const uint64_t* sk, cudaStream_t st, uint32_t& launches);
 static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                                 const uint64_t* hk, cudaStream_t st, uint32_t& launches);
+static ssbh_status bucket_passes(ssbh_plan* pl, const SamplerGeom& ga, const uint64_t* sk,
+                                 uint64_t base, const uint32_t* d_input, const uint32_t* d_keep,
+                                 const void* d_payload_src, cudaStream_t st, uint32_t& launches);
 
 static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown) {
     if (!p) return fail(SSBH_INVALID_ARGUMENT, "extract: null params");
@@ -427,15 +434,46 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         pl->sbuf_words = round_up(seed_fixed + round_up((n + 31) / 32, kHashR) + 64, 8);
     pl->key_words32 = ((uint64_t)nown * k + 31) / 32;
 
+    // two-level split for large key spaces (SSBH_BUCKETS=0 disables it, =1 forces it)
+    const char* be = std::getenv("SSBH_BUCKETS");
+    pl->bucketed = be && *be ? *be == '1' : nown >= kBucketMinBlocks;
+    if (pl->bucketed) {
+        const uint64_t n_src = pl->streaming ? chunk_bits : n;
+        const double mean = (double)n / (double)(external_payload ? nown : params->n_subblocks);
+        pl->bg = make_bucket_geom(n_src, params->n_subblocks, params->block_first, nown,
+                                  pl->streaming ? (double)chunk_bits / params->n_subblocks : mean,
+                                  false, max_cs);
+        // pass-A payload: the received payload's type for shard owners; u16 whenever V fits
+        // 15 bits and no keep marker can occur (streaming runs take no keep mask)
+        pl->bg.a.payload_bytes = external_payload ? pl->geom.payload_bytes
+                                 : (params->n_subblocks < 32768 ||
+                                    (pl->streaming && params->n_subblocks == 32768)) ? 2 : 4;
+    }
+    const BucketGeom& bg = pl->bg;
+
     auto alloc = [&](DBuf& b, size_t bytes) -> cudaError_t {
         pl->bytes += bytes;
         return b.alloc(bytes);
     };
     cudaError_t e = cudaSuccess;
-    if (!e && !pl->streaming && !external_payload)
-        e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
-    if (!e) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
-    if (!e) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
+    if (!pl->bucketed) {
+        if (!e && !pl->streaming && !external_payload)
+            e = alloc(pl->payload, (size_t)n * pl->geom.payload_bytes);
+    } else {
+        if (!e && !external_payload)
+            e = alloc(pl->payload, (size_t)bg.a.n * bg.a.payload_bytes + 16);
+        if (!e) e = alloc(pl->counts_a, (size_t)bg.a.nchunks * bg.nbuckets * 4);
+        if (!e) e = alloc(pl->gsum_a, (size_t)bg.a.ngroups * bg.nbuckets * 8);
+        if (!e) e = alloc(pl->tot_a, (size_t)bg.nbuckets * 8);
+        if (!e) e = alloc(pl->staging, (size_t)bg.b.n * 2);
+        if (!e) e = alloc(pl->counts_b, (size_t)bg.b.nchunks * bg.b.nown * 4);
+        if (!e) e = alloc(pl->gsum_b, (size_t)bg.b.ngroups * bg.b.nown * 8);
+        if (!e) e = alloc(pl->nj_b, (size_t)bg.nbuckets * bg.b.nown * 8);
+    }
+    // single-level count table (bucketed streaming plans keep it: its scanned rows give every
+    // block's rank at the start of each input chunk)
+    if (!e && (!pl->bucketed || pl->streaming)) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
+    if (!e && (!pl->bucketed || pl->streaming)) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
     if (!e) e = alloc(pl->ybuf, pl->ybuf_words * 4);
     if (!e) e = alloc(pl->sbuf, pl->sbuf_words * 4);
     if (!e && !pl->direct_out) e = alloc(pl->scratch, (size_t)nown * pl->kw * 4);
@@ -484,6 +522,20 @@ extern "C" ssbh_status ssbh_plan_stream_chunk(ssbh_plan* pl, uint64_t chunk_inde
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     pl->last_stream = st;
     const Layout lay = pl->lay.view();
+    if (pl->bucketed) {
+        // two-level split of this chunk; ranks continue from the block's rounds in earlier
+        // chunks = the scanned single-level table's row at the chunk start
+        const SamplerGeom ga = geom_with_n(pl->bg.a, count);
+        if (auto s = bucket_passes(pl, ga, pl->stream_samp, first, d_chunk, nullptr, nullptr, st,
+                                   pl->stream_launches))
+            return s;
+        const uint32_t* rank_base =
+            pl->counts.as<uint32_t>() + (first >> pl->geom.chunk_shift) * (uint64_t)pl->nown;
+        launch_bucket_scatter(pl->bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(),
+                              lay.nj, lay.yoff, pl->ybuf.as<uint32_t>(), rank_base, st);
+        pl->stream_launches += 1;
+        return check_launch("stream_chunk");
+    }
     launch_scatter_stream(pl->geom, pl->stream_samp, d_chunk, first, count,
                           pl->counts.as<uint32_t>(), lay.nj, lay.yoff, pl->ybuf.as<uint32_t>(), st);
     pl->stream_launches += 1;
@@ -533,12 +585,56 @@ static void rec(ssbh_plan* pl, int i, cudaStream_t st) {
     if (pl->timing) cudaEventRecord(pl->ev[i], st);
 }
 
+// Two-level passes from a pass-A payload (or Threefry when d_input is given): bucket counts,
+// scan, split into the staging regions, pass-B counts and per-region scan (-> nj_b).
+static ssbh_status bucket_passes(ssbh_plan* pl, const SamplerGeom& ga, const uint64_t* sk,
+                                 uint64_t base, const uint32_t* d_input, const uint32_t* d_keep,
+                                 const void* d_payload_src, cudaStream_t st, uint32_t& launches) {
+    const BucketGeom& bg = pl->bg;
+    const Layout lay = pl->lay.view();
+    uint32_t* flags = &lay.stats->pad;
+    CU(cudaMemsetAsync(pl->counts_a.p, 0, pl->counts_a.bytes, st));
+    if (d_payload_src) {
+        launch_count_payload(ga, d_payload_src, pl->counts_a.as<uint32_t>(), st, bg.shift);
+    } else {
+        launch_sample_buckets(bg, ga, sk, base, d_input, d_keep, pl->payload.p,
+                              pl->counts_a.as<uint32_t>(), st);
+        d_payload_src = pl->payload.p;
+    }
+    launch_scan(with_keys(ga, bg.nbuckets), pl->counts_a.as<uint32_t>(),
+                pl->gsum_a.as<unsigned long long>(), pl->tot_a.as<unsigned long long>(), st);
+    CU(cudaMemsetAsync(pl->staging.p, 0xff, pl->staging.bytes, st));
+    launch_bucket_split(bg, ga, d_payload_src, pl->counts_a.as<uint32_t>(),
+                        pl->staging.as<uint16_t>(), flags, st);
+    CU(cudaMemsetAsync(pl->counts_b.p, 0, pl->counts_b.bytes, st));
+    launch_bucket_count(bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(), st);
+    launch_scan(bg.b, pl->counts_b.as<uint32_t>(), pl->gsum_b.as<unsigned long long>(),
+                pl->nj_b.as<unsigned long long>(), st, bg.gps);
+    launches += 10;
+    return SSBH_OK;
+}
+
 static ssbh_status seg_sample(ssbh_plan* pl, const uint32_t* d_input, const uint32_t* d_keep,
                               const uint64_t* sk, cudaStream_t st, uint32_t& launches) {
     const Layout lay = pl->lay.view();
+    if (pl->bucketed || pl->streaming)
+        CU(cudaMemsetAsync(&lay.stats->pad, 0, 4, st));  // kFlagBucketOverflow of this run
+    if (pl->bucketed && !pl->streaming) {
+        if (auto s = bucket_passes(pl, pl->bg.a, sk, 0, d_input, d_keep, nullptr, st, launches))
+            return s;
+        // block lengths: the per-region totals of the first nown local keys
+        CU(cudaMemcpyAsync(lay.nj, pl->nj_b.p, (size_t)pl->nown * 8, cudaMemcpyDeviceToDevice,
+                           st));
+        launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
+                      pl->p.block_limit, st);
+        launches += 1;
+        CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
+        return SSBH_OK;
+    }
     CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
-    launch_sample_count(pl->geom, sk, d_input, d_keep, pl->payload.p, pl->counts.as<uint32_t>(),
-                        nullptr, st);
+    // streaming: count only (a bucketed streaming plan's payload buffer holds one chunk)
+    launch_sample_count(pl->geom, sk, d_input, d_keep, pl->streaming ? nullptr : pl->payload.p,
+                        pl->counts.as<uint32_t>(), nullptr, st);
     launch_scan(pl->geom, pl->counts.as<uint32_t>(), pl->gsum.as<unsigned long long>(), lay.nj,
                 st);
     launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
@@ -550,6 +646,12 @@ static ssbh_status seg_sample(ssbh_plan* pl, const uint32_t* d_input, const uint
 
 static ssbh_status seg_scatter(ssbh_plan* pl, cudaStream_t st, uint32_t& launches) {
     const Layout lay = pl->lay.view();
+    if (pl->bucketed) {
+        launch_bucket_scatter(pl->bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(),
+                              lay.nj, lay.yoff, pl->ybuf.as<uint32_t>(), nullptr, st);
+        launches += 1;
+        return SSBH_OK;
+    }
     launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
                    pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
     launches += 1;
@@ -758,6 +860,9 @@ extern "C" ssbh_status ssbh_plan_check(ssbh_plan* pl, ssbh_extract_stats* stats)
             stats->ms_total = ms[4];
         }
     }
+    if (d.pad & kFlagBucketOverflow)
+        return fail(SSBH_CUDA, "extract: a two-level staging region overflowed (> mean + 16 "
+                               "sigma rounds in one bucket)");
     if (d.flags & kFlagTooLong)
         return fail(SSBH_INVALID_ARGUMENT,
                     "extract: sub-block of >= 2^32 bits is beyond the device path");
@@ -1208,16 +1313,31 @@ extern "C" ssbh_status ssbh_shard_finish(ssbh_shard* sh, uint32_t* d_key, uint64
     const Layout lay = pl->lay.view();
     uint32_t launches = sh->launches;
     if (pl->timing) CU(cudaEventRecord(pl->ev[0], st));
-    CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
-    launch_count_payload(g, sh->recv.p, pl->counts.as<uint32_t>(), st);
-    launch_scan(g, pl->counts.as<uint32_t>(), pl->gsum.as<unsigned long long>(), lay.nj, st);
+    if (pl->bucketed) {
+        // many owned blocks: two-level split of the received rounds (see BucketGeom)
+        CU(cudaMemsetAsync(&lay.stats->pad, 0, 4, st));
+        if (auto s = bucket_passes(pl, geom_with_n(pl->bg.a, sh->n_recv), nullptr, 0, nullptr,
+                                   nullptr, sh->recv.p, st, launches))
+            return s;
+        CU(cudaMemcpyAsync(lay.nj, pl->nj_b.p, (size_t)pl->nown * 8, cudaMemcpyDeviceToDevice,
+                           st));
+    } else {
+        CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
+        launch_count_payload(g, sh->recv.p, pl->counts.as<uint32_t>(), st);
+        launch_scan(g, pl->counts.as<uint32_t>(), pl->gsum.as<unsigned long long>(), lay.nj, st);
+        launches += 4;
+    }
     launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
                   pl->p.block_limit, st);
-    launches += 5;
+    launches += 1;
     if (pl->timing) CU(cudaEventRecord(pl->ev[1], st));
     CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
-    launch_scatter(g, sh->recv.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
-                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
+    if (pl->bucketed)
+        launch_bucket_scatter(pl->bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(),
+                              lay.nj, lay.yoff, pl->ybuf.as<uint32_t>(), nullptr, st);
+    else
+        launch_scatter(g, sh->recv.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
+                       pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
     launches += 1;
     if (auto s = phase_finish(pl, d_key, d_lengths, hk, st, launches)) return s;
     pl->launches_per_run = launches;

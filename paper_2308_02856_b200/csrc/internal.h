@@ -30,6 +30,7 @@ struct DevStats {
 constexpr uint32_t kFlagEmpty = 1u;     // some owned n_j == 0
 constexpr uint32_t kFlagOversize = 2u;  // some owned n_j > block_limit
 constexpr uint32_t kFlagTooLong = 4u;   // some owned n_j >= 2^32 (device path limit)
+constexpr uint32_t kFlagBucketOverflow = 8u;  // a two-level staging region overflowed
 
 // Per-owned-block layout arrays (device).
 struct Layout {
@@ -96,8 +97,10 @@ void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint
                          const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st);
 // Pass 2: exclusive scan of counts along chunks (in place -> offsets), nj totals.
+// seg_groups > 0: the scan restarts every seg_groups groups (two-level pass B); nj gets one
+// row of g.nown totals per segment.
 void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d_gsum,
-                 unsigned long long* d_nj, cudaStream_t st);
+                 unsigned long long* d_nj, cudaStream_t st, uint64_t seg_groups = 0);
 // Pass 3: stable scatter. ybuf mode: reversed bit pack into ybuf (pre-zeroed);
 // index mode (d_idx_out != null): CSR indices at csr_off[jj] + rank.
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
@@ -126,8 +129,52 @@ void launch_owner_split(const SamplerGeom& g, const void* d_payload, uint32_t ow
                         uint32_t* d_offsets, void* const* d_dst,
                         const unsigned long long* d_dst_base, cudaStream_t st);
 // Pass 1 of an owner: counts per (chunk, owned block) from a received payload (g.n rounds).
+// bshift > 0: keys are buckets of 2^bshift owned blocks (two-level pass A).
 void launch_count_payload(const SamplerGeom& g, const void* d_payload, uint32_t* d_counts,
-                          cudaStream_t st);
+                          cudaStream_t st, uint32_t bshift = 0);
+
+// ---- two-level split for large key spaces ---------------------------------------------
+// With thousands of owned blocks one warp-chunk touches every block, so the running-rank rows
+// no longer fit shared memory and the data bits land on random words of a y buffer far larger
+// than L2. Pass A splits the rounds stably by bucket (2^shift consecutive blocks) into a
+// staging buffer with one fixed-capacity region per bucket (mean + 16 sigma); pass B counts,
+// scans (restarting per region) and scatters the staged rounds with 2^shift keys, so each
+// warp's rank row lives in shared memory and its y writes stay within one bucket's blocks.
+constexpr uint32_t kBucketShift = 7;           // 128 blocks per bucket
+constexpr uint32_t kBucketMinBlocks = 4096;    // below: single-level scatter
+struct BucketGeom {
+    uint32_t shift;       // log2 blocks per bucket
+    uint32_t nbuckets;
+    uint64_t cap;         // staged rounds per bucket region
+    uint64_t cpb;         // pass-B chunks per region
+    uint64_t gps;         // pass-B scan groups per region
+    SamplerGeom a;        // pass A over the source rounds (nown = owned blocks)
+    SamplerGeom b;        // pass B over nbuckets * cap staged rounds (nown = 2^shift), u16
+};
+inline SamplerGeom with_keys(SamplerGeom g, uint32_t nkeys) {
+    g.nown = nkeys;
+    return g;
+}
+// mean_per_block: expected rounds per owned block among the n_src source rounds.
+BucketGeom make_bucket_geom(uint64_t n_src, uint64_t s, uint32_t j_lo, uint32_t nown,
+                            double mean_per_block, bool has_keep, int max_chunk_shift = 40);
+// Pass A from Threefry (rounds base + [0, ga.n)): payload + per-(chunk, bucket) counts.
+void launch_sample_buckets(const BucketGeom& bg, const SamplerGeom& ga, const uint64_t key[4],
+                           uint64_t base, const uint32_t* d_in32, const uint32_t* d_keep,
+                           void* d_payload, uint32_t* d_counts, cudaStream_t st);
+// Pass A split: payload -> staging regions (u16 local block | bit << 15), using the scanned
+// pass-A table; a full region raises kFlagBucketOverflow in *d_flags.
+void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void* d_payload,
+                         uint32_t* d_offsets_a, uint16_t* d_staging, uint32_t* d_flags,
+                         cudaStream_t st);
+// Pass B counts over the staging regions (empty slots hold 0xffff).
+void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_counts_b,
+                         cudaStream_t st);
+// Pass B scatter into the reversed blocks; d_rank_base (per owned block, may be null) is
+// added to every rank (streaming: the block's rounds in earlier input chunks).
+void launch_bucket_scatter(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_offsets_b,
+                           const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                           uint32_t* d_ybuf, const uint32_t* d_rank_base, cudaStream_t st);
 
 // ---- layout / seeds / hash -----------------------------------------------------------
 // Computes ypad/ktl/yoff/items/soff/stats from lay.nj for nown blocks.

@@ -20,6 +20,7 @@
 //                by direct stores through NVLink peer memory (multi-GPU sharded sampling:
 //                the dispatch half of an all-to-all fused into the partition pass).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
@@ -70,6 +71,7 @@ struct TFSource {
     P* payload;              // local index (may be null)
     uint32_t* assign_out;    // V+1 per local round (may be null)
     uint32_t j_lo, nown, owners;
+    uint32_t bshift;         // > 0: keys are buckets of 2^bshift owned blocks (two-level split)
     __device__ __forceinline__ uint32_t operator()(uint64_t g, uint32_t lane) const {
         const uint64_t i = g * 32 + lane;
         const bool valid = i < n;
@@ -100,7 +102,7 @@ struct TFSource {
         if (!kept) return 0xffffffffu;
         if (owners) return owner_of(v, owners, s);
         const uint32_t jj = v - j_lo;
-        return jj < nown ? jj : 0xffffffffu;
+        return jj < nown ? jj >> bshift : 0xffffffffu;
     }
 };
 
@@ -111,13 +113,14 @@ struct PayloadCountSource {
     const P* payload;
     uint64_t n;
     uint32_t j_lo, nown;
+    uint32_t bshift;  // > 0: bucket keys (see TFSource)
     __device__ __forceinline__ uint32_t operator()(uint64_t g, uint32_t lane) const {
         const uint64_t i = g * 32 + lane;
         if (i >= n) return 0xffffffffu;
         const uint32_t p = payload[i];
         if (Bits::kKeepShift < 32 && ((p >> (Bits::kKeepShift & 31)) & 1u)) return 0xffffffffu;
         const uint32_t jj = (p & Bits::kVMask) - j_lo;
-        return jj < nown ? jj : 0xffffffffu;
+        return jj < nown ? jj >> bshift : 0xffffffffu;
     }
 };
 
@@ -189,9 +192,11 @@ constexpr int kScanBatch = 8;
 __global__ void k_scan_groups(const uint32_t* __restrict__ counts, uint64_t nchunks,
                               uint32_t nown, uint64_t group_chunks,
                               unsigned long long* __restrict__ gsum) {
-    const uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x;
+    // flat grid: (group, 256-key slice) — a grid's y extent is capped at 65535 groups
+    const uint32_t kslices = (nown + blockDim.x - 1) / blockDim.x;
+    const uint64_t g = blockIdx.x / kslices;
+    const uint32_t jj = (blockIdx.x % kslices) * blockDim.x + threadIdx.x;
     if (jj >= nown) return;
-    const uint64_t g = blockIdx.y;
     const uint64_t c0 = g * group_chunks;
     const uint64_t c1 = min(nchunks, c0 + group_chunks);
     unsigned long long t = 0;
@@ -206,14 +211,20 @@ __global__ void k_scan_groups(const uint32_t* __restrict__ counts, uint64_t nchu
 }
 
 // exclusive scan over groups per key (one warp per key, lane-contiguous group ranges),
-// totals -> nj
+// totals -> nj. Segmented (two-level split, pass B): every `gps` consecutive groups form one
+// bucket region whose scan restarts at 0; warp (seg, key) writes nj[seg * nown + key].
 __global__ void k_scan_totals(unsigned long long* __restrict__ gsum, uint64_t ngroups,
-                              uint32_t nown, unsigned long long* __restrict__ nj) {
-    const uint32_t jj = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                              uint32_t nown, unsigned long long* __restrict__ nj,
+                              uint64_t gps, uint64_t nseg) {
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    if (jj >= nown) return;  // warp-uniform
-    const uint64_t per = (ngroups + 31) / 32;
-    const uint64_t g0 = min(ngroups, lane * per), g1 = min(ngroups, g0 + per);
+    if (wid >= nseg * nown) return;  // warp-uniform
+    const uint32_t jj = (uint32_t)(wid % nown);
+    const uint64_t seg = wid / nown;
+    const uint64_t gbeg = seg * gps, gend = min(ngroups, gbeg + gps);
+    const uint64_t span = gend > gbeg ? gend - gbeg : 0;
+    const uint64_t per = (span + 31) / 32;
+    const uint64_t g0 = min(gend, gbeg + lane * per), g1 = min(gend, g0 + per);
     unsigned long long mine = 0;
     for (uint64_t g = g0; g < g1; g += kScanBatch) {
         unsigned long long v[kScanBatch];
@@ -229,7 +240,7 @@ __global__ void k_scan_totals(unsigned long long* __restrict__ gsum, uint64_t ng
         if (lane >= (uint32_t)o) inc += y;
     }
     unsigned long long run = inc - mine;
-    if (lane == 31) nj[jj] = inc;
+    if (lane == 31) nj[seg * nown + jj] = inc;
     for (uint64_t g = g0; g < g1; g += kScanBatch) {
         unsigned long long v[kScanBatch];
 #pragma unroll
@@ -247,9 +258,11 @@ __global__ void k_scan_totals(unsigned long long* __restrict__ gsum, uint64_t ng
 __global__ void k_scan_apply(uint32_t* __restrict__ counts, uint64_t nchunks, uint32_t nown,
                              uint64_t group_chunks,
                              const unsigned long long* __restrict__ gsum) {
-    const uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x;
+    // flat grid: (group, 256-key slice) — a grid's y extent is capped at 65535 groups
+    const uint32_t kslices = (nown + blockDim.x - 1) / blockDim.x;
+    const uint64_t g = blockIdx.x / kslices;
+    const uint32_t jj = (blockIdx.x % kslices) * blockDim.x + threadIdx.x;
     if (jj >= nown) return;
-    const uint64_t g = blockIdx.y;
     const uint64_t c0 = g * group_chunks;
     const uint64_t c1 = min(nchunks, c0 + group_chunks);
     unsigned long long base = gsum[g * nown + jj];
@@ -304,12 +317,15 @@ struct StreamSrc {
     }
 };
 
-enum ScatterMode { kModeBits = 0, kModeIndex = 1, kModeOwner = 2 };
+// Bucket — two-level split, pass A: the round goes to its bucket's staging region (rank =
+//          position inside the region) as a u16 (local block index | bit << 15).
+enum ScatterMode { kModeBits = 0, kModeIndex = 1, kModeOwner = 2, kModeBucket = 3 };
 
 struct ScatterArgs {
     uint64_t c_begin, c_end;  // warp-chunks processed by this launch
     uint64_t n_end;           // one past the last round of this launch
-    uint32_t j_lo, nown;      // key space: blocks [j_lo, j_lo+nown), or owners (kModeOwner)
+    uint32_t j_lo, nown;      // key space: blocks [j_lo, j_lo+nown), or owners (kModeOwner),
+                              // or buckets (kModeBucket), or local blocks (staged kModeBits)
     int kbits, cs;
     uint64_t s;               // kModeOwner: blocks, for owner_of
     uint32_t* offs;           // per-(chunk, key) running ranks
@@ -320,6 +336,14 @@ struct ScatterArgs {
     const unsigned long long* csr_off;
     void* const* dst;                    // kModeOwner: per-owner receive buffers (peer mapped)
     const unsigned long long* dst_base;  // kModeOwner: this rank's first global rank per owner
+    // two-level split
+    uint32_t bshift;            // log2 blocks per bucket
+    uint32_t nblocks;           // kModeBucket: owned blocks
+    uint64_t cap;               // kModeBucket: staged rounds per bucket region
+    uint16_t* staging;          // kModeBucket: destination regions
+    uint32_t* flags;            // kModeBucket: kFlagBucketOverflow on a full region
+    uint64_t cpb;               // staged kModeBits: chunks per bucket region (0: not staged)
+    const uint32_t* rank_base;  // staged kModeBits: per-block rank offset (streaming) or null
 };
 
 template <typename Src, bool kSmemRow, bool kMatch, int kMode>
@@ -337,7 +361,7 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
     unsigned long long* s_key = reinterpret_cast<unsigned long long*>(scatter_smem);
     uint32_t* srow_all = reinterpret_cast<uint32_t*>(scatter_smem + (size_t)nown * 8);
     if (kSmemRow) {
-        if (kMode == kModeBits)
+        if (kMode == kModeBits && !a.cpb)
             for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
                 s_key[t] = a.yoff[t] * 32ull + a.nj[t] - 1ull;
         else if (kMode == kModeOwner)
@@ -385,6 +409,11 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                     if (B::kKeepShift >= 32) kept = kept && (p & B::kVMask) != B::kVMask;
                     jjv[q] = owner_of(p & B::kVMask, nown, a.s);
                     inv[q] = kept;
+                } else if (kMode == kModeBucket) {
+                    // pass-A payloads carry no u16 marker (a keep mask forces u32 payloads)
+                    const uint32_t jb = (p & B::kVMask) - j_lo;
+                    jjv[q] = jb >> a.bshift;
+                    inv[q] = kept && jb < a.nblocks;
                 } else {
                     jjv[q] = (p & B::kVMask) - j_lo;
                     inv[q] = kept && jjv[q] < nown;
@@ -411,12 +440,28 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                     } else if constexpr (kMode == kModeOwner) {
                         const unsigned long long gb = kSmemRow ? s_key[jj] : a.dst_base[jj];
                         static_cast<P*>(a.dst[jj])[gb + pos] = (P)cur[q];
+                    } else if constexpr (kMode == kModeBucket) {
+                        const uint32_t p = cur[q];
+                        const uint32_t local = ((p & B::kVMask) - j_lo) & ((1u << a.bshift) - 1u);
+                        if (pos < a.cap)
+                            a.staging[jj * a.cap + pos] =
+                                (uint16_t)(local | (((p >> B::kDataShift) & 1u) << 15));
+                        else
+                            atomicOr(a.flags, kFlagBucketOverflow);
                     } else if ((cur[q] >> B::kDataShift) & 1u) {
-                        const unsigned long long e =
-                            kSmemRow ? s_key[jj]
-                                     : __ldg(a.yoff + jj) * 32ull + __ldg(a.nj + jj) - 1ull;
-                        const uint64_t qb = e - pos;
-                        atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
+                        if (a.cpb) {  // staged rounds: chunk c lies in bucket c / cpb
+                            const uint32_t jf = (uint32_t)((c / a.cpb) << a.bshift) + jj;
+                            const uint64_t r = pos + (a.rank_base ? __ldg(a.rank_base + jf) : 0u);
+                            const uint64_t qb =
+                                __ldg(a.yoff + jf) * 32ull + __ldg(a.nj + jf) - 1ull - r;
+                            atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
+                        } else {
+                            const unsigned long long e =
+                                kSmemRow ? s_key[jj]
+                                         : __ldg(a.yoff + jj) * 32ull + __ldg(a.nj + jj) - 1ull;
+                            const uint64_t qb = e - pos;
+                            atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
+                        }
                     }
                 }
                 __syncwarp();
@@ -532,15 +577,17 @@ void count_launch(const Src& src, uint64_t n, uint32_t nkeys, int cs, uint64_t n
 template <typename P, bool kPow2>
 void sample_count_t(const SamplerGeom& g, const Key& k, const uint32_t* d_in32,
                     const uint32_t* d_keep, P* pl, uint32_t* d_counts, uint32_t* d_assign_out,
-                    uint64_t base, uint32_t owners, cudaStream_t st) {
-    TFSource<P, kPow2> src{k,      g.n,          base,   g.s,    d_in32, d_keep,
-                           pl,     d_assign_out, g.j_lo, g.nown, owners};
-    count_launch(src, g.n, owners ? owners : g.nown, g.chunk_shift, g.nchunks, d_counts, st);
+                    uint64_t base, uint32_t owners, uint32_t bshift, cudaStream_t st) {
+    TFSource<P, kPow2> src{k,  g.n,          base,   g.s,    d_in32, d_keep,
+                           pl, d_assign_out, g.j_lo, g.nown, owners, bshift};
+    const uint32_t nkeys = owners ? owners : (bshift ? ((g.nown - 1) >> bshift) + 1 : g.nown);
+    count_launch(src, g.n, nkeys, g.chunk_shift, g.nchunks, d_counts, st);
 }
 
 void sample_count_any(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
                       const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
-                      uint32_t* d_assign_out, uint64_t base, uint32_t owners, cudaStream_t st) {
+                      uint32_t* d_assign_out, uint64_t base, uint32_t owners, uint32_t bshift,
+                      cudaStream_t st) {
     if (g.n == 0) return;
     Key k;
     threefry_ks(key, k.ks);
@@ -549,18 +596,18 @@ void sample_count_any(const SamplerGeom& g, const uint64_t key[4], const uint32_
         auto* pl = static_cast<uint16_t*>(d_payload);
         if (pow2)
             sample_count_t<uint16_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, base,
-                                           owners, st);
+                                           owners, bshift, st);
         else
             sample_count_t<uint16_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out,
-                                            base, owners, st);
+                                            base, owners, bshift, st);
     } else {
         auto* pl = static_cast<uint32_t*>(d_payload);
         if (pow2)
             sample_count_t<uint32_t, true>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out, base,
-                                           owners, st);
+                                           owners, bshift, st);
         else
             sample_count_t<uint32_t, false>(g, k, d_in32, d_keep, pl, d_counts, d_assign_out,
-                                            base, owners, st);
+                                            base, owners, bshift, st);
     }
 }
 
@@ -682,34 +729,118 @@ SamplerGeom geom_with_n(const SamplerGeom& g0, uint64_t n) {
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
                          const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st) {
-    sample_count_any(g, key, d_in32, d_keep, d_payload, d_counts, d_assign_out, 0, 0, st);
+    sample_count_any(g, key, d_in32, d_keep, d_payload, d_counts, d_assign_out, 0, 0, 0, st);
 }
 
 void launch_sample_slice(const SamplerGeom& g, const uint64_t key[4], uint64_t base,
                          const uint32_t* d_in32, void* d_payload, uint32_t owners,
                          uint32_t* d_counts, cudaStream_t st) {
-    sample_count_any(g, key, d_in32, nullptr, d_payload, d_counts, nullptr, base, owners, st);
+    sample_count_any(g, key, d_in32, nullptr, d_payload, d_counts, nullptr, base, owners, 0, st);
+}
+
+void launch_sample_buckets(const BucketGeom& bg, const SamplerGeom& ga, const uint64_t key[4],
+                           uint64_t base, const uint32_t* d_in32, const uint32_t* d_keep,
+                           void* d_payload, uint32_t* d_counts, cudaStream_t st) {
+    sample_count_any(ga, key, d_in32, d_keep, d_payload, d_counts, nullptr, base, 0, bg.shift,
+                     st);
 }
 
 void launch_count_payload(const SamplerGeom& g, const void* d_payload, uint32_t* d_counts,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint32_t bshift) {
+    const uint32_t nkeys = bshift ? ((g.nown - 1) >> bshift) + 1 : g.nown;
     if (g.payload_bytes == 2)
         count_launch(PayloadCountSource<uint16_t>{static_cast<const uint16_t*>(d_payload), g.n,
-                                                  g.j_lo, g.nown},
-                     g.n, g.nown, g.chunk_shift, g.nchunks, d_counts, st);
+                                                  g.j_lo, g.nown, bshift},
+                     g.n, nkeys, g.chunk_shift, g.nchunks, d_counts, st);
     else
         count_launch(PayloadCountSource<uint32_t>{static_cast<const uint32_t*>(d_payload), g.n,
-                                                  g.j_lo, g.nown},
-                     g.n, g.nown, g.chunk_shift, g.nchunks, d_counts, st);
+                                                  g.j_lo, g.nown, bshift},
+                     g.n, nkeys, g.chunk_shift, g.nchunks, d_counts, st);
 }
 
 void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d_gsum,
-                 unsigned long long* d_nj, cudaStream_t st) {
+                 unsigned long long* d_nj, cudaStream_t st, uint64_t seg_groups) {
     if (g.nown == 0) return;
-    const dim3 grid((g.nown + 255) / 256, (unsigned)g.ngroups);
+    const uint64_t gps = seg_groups ? seg_groups : g.ngroups;
+    const uint64_t nseg = (g.ngroups + gps - 1) / gps;
+    const unsigned grid = (unsigned)(((g.nown + 255) / 256) * g.ngroups);
     k_scan_groups<<<grid, 256, 0, st>>>(d_counts, g.nchunks, g.nown, g.group_chunks, d_gsum);
-    k_scan_totals<<<(g.nown + 7) / 8, 256, 0, st>>>(d_gsum, g.ngroups, g.nown, d_nj);
+    k_scan_totals<<<(unsigned)((nseg * g.nown + 7) / 8), 256, 0, st>>>(d_gsum, g.ngroups, g.nown,
+                                                                       d_nj, gps, nseg);
     k_scan_apply<<<grid, 256, 0, st>>>(d_counts, g.nchunks, g.nown, g.group_chunks, d_gsum);
+}
+
+// ---- two-level split for large key spaces ---------------------------------------------
+BucketGeom make_bucket_geom(uint64_t n_src, uint64_t s, uint32_t j_lo, uint32_t nown,
+                            double mean_per_block, bool has_keep, int max_chunk_shift) {
+    BucketGeom bg{};
+    bg.shift = kBucketShift;
+    const uint32_t bb = 1u << bg.shift;
+    bg.nbuckets = (nown + bb - 1) / bb;
+    // pass A: keys = buckets; u16 payload whenever V fits 15 bits (no keep marker needed)
+    bg.a = make_sampler_geom(n_src ? n_src : 1, s, j_lo, bg.nbuckets, has_keep, max_chunk_shift);
+    bg.a.n = n_src;
+    bg.a.nown = nown;
+    bg.a.payload_bytes = (!has_keep && s <= 32768) ? 2 : 4;
+    // pass B: one fixed region per bucket = mean + 16 sigma (+ slack), in whole scan groups of
+    // 2^cs chunks; count table <= max(64 MiB, n/16 bytes)
+    const double mean = mean_per_block * bb;
+    const uint64_t cap0 = (uint64_t)(mean + 16.0 * std::sqrt(mean) + 4096.0);
+    const uint64_t budget = std::max<uint64_t>(64ull << 20, n_src / 16);
+    int cs = 10;
+    while (cs < 20 && (uint64_t)bg.nbuckets * (cap0 >> cs) * bb * 4 > budget) ++cs;
+    const uint64_t gc = 16;
+    const uint64_t span = (1ull << cs) * gc;
+    bg.cap = (cap0 + span - 1) / span * span;
+    bg.cpb = bg.cap >> cs;
+    bg.gps = bg.cpb / gc;
+    SamplerGeom& b = bg.b;
+    b.n = (uint64_t)bg.nbuckets * bg.cap;
+    b.s = s;
+    b.j_lo = 0;
+    b.nown = bb;
+    b.chunk_shift = cs;
+    b.nchunks = (uint64_t)bg.nbuckets * bg.cpb;
+    b.group_chunks = gc;
+    b.ngroups = (uint64_t)bg.nbuckets * bg.gps;
+    b.payload_bytes = 2;
+    return bg;
+}
+
+void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void* d_payload,
+                         uint32_t* d_offsets_a, uint16_t* d_staging, uint32_t* d_flags,
+                         cudaStream_t st) {
+    if (ga.n == 0) return;
+    ScatterArgs a = scatter_args(ga, d_offsets_a, nullptr, nullptr, nullptr, nullptr, nullptr);
+    a.nown = bg.nbuckets;
+    a.nblocks = ga.nown;
+    a.bshift = bg.shift;
+    a.cap = bg.cap;
+    a.staging = d_staging;
+    a.flags = d_flags;
+    if (ga.payload_bytes == 2)
+        scatter_launch<kModeBucket>(PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload)},
+                                    a, st);
+    else
+        scatter_launch<kModeBucket>(PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload)},
+                                    a, st);
+}
+
+void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_counts_b,
+                         cudaStream_t st) {
+    const SamplerGeom& b = bg.b;
+    count_launch(PayloadCountSource<uint16_t>{d_staging, b.n, 0, b.nown, 0}, b.n, b.nown,
+                 b.chunk_shift, b.nchunks, d_counts_b, st);
+}
+
+void launch_bucket_scatter(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_offsets_b,
+                           const unsigned long long* d_nj, const unsigned long long* d_yoff,
+                           uint32_t* d_ybuf, const uint32_t* d_rank_base, cudaStream_t st) {
+    ScatterArgs a = scatter_args(bg.b, d_offsets_b, d_nj, d_yoff, d_ybuf, nullptr, nullptr);
+    a.bshift = bg.shift;
+    a.cpb = bg.cpb;
+    a.rank_base = d_rank_base;
+    scatter_launch<kModeBits>(PayloadSrc<uint16_t>{d_staging}, a, st);
 }
 
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,

@@ -224,8 +224,8 @@ __global__ void k_seeds_shared(Key key, const DevStats* __restrict__ st, uint32_
 }
 
 __global__ void k_seeds_per_block(Key key, const unsigned long long* __restrict__ soff,
-                                  uint32_t j_lo, uint32_t* sbuf) {
-    const uint32_t jj = blockIdx.y;
+                                  uint32_t j_lo, uint32_t jj0, uint32_t* sbuf) {
+    const uint32_t jj = jj0 + blockIdx.y;
     const uint64_t w0 = soff[jj];
     seed_region(key, (uint64_t)j_lo + jj, (soff[jj + 1] - w0) / 8, sbuf + w0,
                 blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
@@ -521,8 +521,11 @@ void launch_seeds(const uint64_t key[4], const Layout& lay, uint32_t nown, uint3
     } else if (nown) {
         const uint64_t per = max_words_hint / 8 + 1;  // quads per block (upper bound)
         unsigned gx = (unsigned)std::min<uint64_t>((per + 255) / 256, 8);
-        k_seeds_per_block<<<dim3(std::max(gx, 1u), nown), 256, 0, st>>>(kk, lay.soff, j_lo,
-                                                                         d_sbuf);
+        for (uint32_t jj0 = 0; jj0 < nown; jj0 += 65535u) {  // grid y extent <= 65535
+            const uint32_t cnt = std::min<uint32_t>(65535u, nown - jj0);
+            k_seeds_per_block<<<dim3(std::max(gx, 1u), cnt), 256, 0, st>>>(kk, lay.soff, j_lo,
+                                                                           jj0, d_sbuf);
+        }
     }
 }
 

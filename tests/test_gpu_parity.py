@@ -592,3 +592,77 @@ def test_run_extraction_gpu_random_vs_oracle(dev, oracle):
         if want_abort != 2:
             assert (lens == want_lens).all(), trial
         assert (key == want_key).all(), trial
+
+
+# ------------------------------------------- two-level split (large key spaces, BucketGeom)
+# Plans with >= 4096 owned blocks split rounds by bucket (128 blocks) into staging regions
+# first; SSBH_BUCKETS=1 forces that path at small sizes so every case is checked against the
+# oracle: several buckets and a partial last one, non-power-of-two s, per-block seeds,
+# k % 32 != 0, owned block ranges, keep masks, streaming chunks in any order, graph replay.
+@pytest.fixture
+def two_level(monkeypatch):
+    monkeypatch.setenv("SSBH_BUCKETS", "1")
+
+
+def test_two_level_extract_vs_oracle(dev, oracle, two_level):
+    rng = np.random.default_rng(91)
+    cases = [(300000, 1000, 64, False), (500000, 4096, 32, True), (250000, 333, 77, True),
+             (400000, 129, 1024, False), (100000, 7, 96, False)]
+    for n, s, k, pb in cases:
+        x = oracle.make_input(int(rng.integers(100)), float(rng.choice([0.5, 0.3])), n)
+        want, wnj = oracle.extract(x, n, s, 21, 22, pb, k)
+        got, nj, _ = dev.extract(x, n, s, k, 21, 22, per_block=pb)
+        assert (nj == wnj).all(), (n, s, k, pb)
+        assert (got == want).all(), (n, s, k, pb)
+    for name in ("1", "2"):
+        c = __import__("json").load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                                      "golden.json")))["extract"][name]
+        x = oracle.make_input(c["seed_in"], c["p"], c["n"])
+        key, nj, _ = dev.extract(x, c["n"], c["s"], c["k"], c["seed_samp"], c["seed_hash"])
+        assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
+
+
+def test_two_level_ranges_keep_and_graph(dev, oracle, two_level):
+    import torch
+
+    n, s, k = 600000, 1000, 64
+    x = oracle.make_input(4, 0.5, n)
+    full, nj, _ = dev.extract(x, n, s, k, 2, 3)
+    kk, ll, _ = dev.extract(x, n, s, k, 2, 3, block_first=300, block_count=500)
+    assert (ll == nj[300:800]).all()
+    assert (kk == full[300 * k // 64:800 * k // 64]).all()
+    rng = np.random.default_rng(5)
+    keep = (rng.random(n) < 0.7).astype(np.uint8)
+    kw = np.packbits(np.concatenate([keep, np.zeros((-n) % 64, np.uint8)]),
+                     bitorder="little").view(np.uint64)
+    want, wnj = oracle.extract_sifted(x, keep, n, s, 2, 3, True, k)
+    got, gnj, _ = dev.extract(x, n, s, k, 2, 3, per_block=True, keep=kw)
+    assert (gnj == wnj).all() and (got == want).all()
+    # device plan: graph capture / replay with changing seeds
+    plan = dev.Plan(n, s, k, 2, 3)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.Stream()
+    for seeds in ((2, 3), (2, 3), (8, 9)):
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), 0, stream.cuda_stream, samp=seeds[0],
+                        hsh=seeds[1])
+        plan.check()
+        ref = full if seeds == (2, 3) else oracle.extract(x, n, s, 8, 9, 0, k)[0]
+        assert (d_key.cpu().numpy().view(np.uint64) == ref).all(), seeds
+    plan.close()
+
+
+def test_two_level_streaming(dev, oracle, two_level):
+    rng = np.random.default_rng(93)
+    for (n, s, k, cb, pb) in ((600000, 1000, 64, 1 << 16, False), (300001, 257, 96, 1 << 15, True)):
+        x = oracle.make_input(int(rng.integers(1000)), 0.5, n)
+        want, wnj = oracle.extract(x, n, s, 31, 32, pb, k)
+        order = list(rng.permutation((n + cb - 1) // cb))
+        got, nj, _ = _stream_run(dev, x, n, s, k, 31, 32, cb, per_block=pb, order=order)
+        assert (nj == wnj).all()
+        assert (got[: len(want)] == want).all(), (n, s, k, cb, pb)
+    n, s, k = 400000, 600, 64
+    x = oracle.make_input(9, 0.5, n)
+    want, _ = oracle.extract(x, n, s, 31, 32, 0, k)
+    got, _, _ = _stream_run(dev, x, n, s, k, 31, 32, 1 << 14, block_first=100, block_count=300)
+    assert (got == want[100:400]).all()

@@ -78,3 +78,11 @@ def test_sharded_world2_matches_oracle():
 @pytest.mark.gpu
 def test_sharded_world3_uneven():
     _run(3, [(200000, 7, 640, True), (1 << 20, 64, 1024, False)])
+
+
+@pytest.mark.gpu
+def test_sharded_world2_two_level(monkeypatch):
+    # owners forced onto the two-level split (SSBH_BUCKETS=1 reaches the spawned ranks):
+    # several buckets per owner, a partial last bucket, per-block seeds
+    monkeypatch.setenv("SSBH_BUCKETS", "1")
+    _run(2, [(600000, 600, 320, True), (400000, 300, 96, False)])

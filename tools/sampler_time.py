@@ -52,7 +52,7 @@ def main():
                           "ms_sample": round(st.ms_sample, 3), "ms_scatter": round(st.ms_scatter, 3),
                           "ms_hash": round(st.ms_hash, 3), "ms_total": round(st.ms_total, 3),
                           "chunk_scatter_ms": [round(x, 2) for x in chunk_ms] if chunk_ms else None,
-                          "bytes": plan.device_bytes()}), flush=True)
+                          "bytes": plan.device_bytes}), flush=True)
     plan.close()
 
 
