@@ -605,7 +605,7 @@ static ssbh_status bucket_passes(ssbh_plan* pl, const SamplerGeom& ga, const uin
                 pl->gsum_a.as<unsigned long long>(), pl->tot_a.as<unsigned long long>(), st);
     CU(cudaMemsetAsync(pl->staging.p, 0xff, pl->staging.bytes, st));
     launch_bucket_split(bg, ga, d_payload_src, pl->counts_a.as<uint32_t>(),
-                        pl->staging.as<uint16_t>(), flags, st);
+                        pl->tot_a.as<unsigned long long>(), pl->staging.as<uint16_t>(), flags, st);
     CU(cudaMemsetAsync(pl->counts_b.p, 0, pl->counts_b.bytes, st));
     launch_bucket_count(bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(), st);
     launch_scan(bg.b, pl->counts_b.as<uint32_t>(), pl->gsum_b.as<unsigned long long>(),

@@ -140,7 +140,8 @@ void launch_count_payload(const SamplerGeom& g, const void* d_payload, uint32_t*
 // staging buffer with one fixed-capacity region per bucket (mean + 16 sigma); pass B counts,
 // scans (restarting per region) and scatters the staged rounds with 2^shift keys, so each
 // warp's rank row lives in shared memory and its y writes stay within one bucket's blocks.
-constexpr uint32_t kBucketShift = 7;           // 128 blocks per bucket
+constexpr uint32_t kBucketShift = 7;           // >= 128 blocks per bucket
+constexpr uint32_t kMaxBuckets = 64;           // <= 64 buckets (8 KB of split sectors per warp)
 constexpr uint32_t kBucketMinBlocks = 4096;    // below: single-level scatter
 struct BucketGeom {
     uint32_t shift;       // log2 blocks per bucket
@@ -165,8 +166,8 @@ void launch_sample_buckets(const BucketGeom& bg, const SamplerGeom& ga, const ui
 // Pass A split: payload -> staging regions (u16 local block | bit << 15), using the scanned
 // pass-A table; a full region raises kFlagBucketOverflow in *d_flags.
 void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void* d_payload,
-                         uint32_t* d_offsets_a, uint16_t* d_staging, uint32_t* d_flags,
-                         cudaStream_t st);
+                         uint32_t* d_offsets_a, const unsigned long long* d_tot_a,
+                         uint16_t* d_staging, uint32_t* d_flags, cudaStream_t st);
 // Pass B counts over the staging regions (empty slots hold 0xffff).
 void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_counts_b,
                          cudaStream_t st);

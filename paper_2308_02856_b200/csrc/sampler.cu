@@ -145,11 +145,10 @@ __global__ void __launch_bounds__(256) k_count_rows(Src src, uint64_t n, uint32_
         __syncwarp();
         const uint64_t g0 = c * gpc + part * gpc / parts;
         const uint64_t g1 = min(ngroups, c * gpc + (part + 1) * gpc / parts);
+        // shared-memory atomics into the warp's own histogram (MATCH.ANY aggregation is
+        // throughput-bound on sm_100; lanes rarely collide on a bin)
         auto tally = [&](uint32_t jj) {
-            const uint32_t peers = __match_any_sync(0xffffffffu, jj);
-            if (jj != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-                hist[jj] += (uint32_t)__popc(peers);
-            __syncwarp();
+            if (jj != 0xffffffffu) atomicAdd(&hist[jj], 1u);
         };
         uint64_t g = g0;
         for (; g + 1 < g1; g += 2) {  // two independent Threefry chains per lane (ILP)
@@ -159,6 +158,7 @@ __global__ void __launch_bounds__(256) k_count_rows(Src src, uint64_t n, uint32_
             tally(jb);
         }
         if (g < g1) tally(src(g, lane));
+        __syncwarp();
         for (uint32_t t = lane; t < nkeys; t += 32)
             if (hist[t]) atomicAdd(counts + c * nkeys + t, hist[t]);
         __syncwarp();
@@ -342,6 +342,7 @@ struct ScatterArgs {
     uint64_t cap;               // kModeBucket: staged rounds per bucket region
     uint16_t* staging;          // kModeBucket: destination regions
     uint32_t* flags;            // kModeBucket: kFlagBucketOverflow on a full region
+    const unsigned long long* tot;  // kModeBucket: rounds per bucket (end of the last chunk)
     uint64_t cpb;               // staged kModeBits: chunks per bucket region (0: not staged)
     const uint32_t* rank_base;  // staged kModeBits: per-block rank offset (streaming) or null
 };
@@ -360,6 +361,15 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
     // Owner — this rank's first global rank in owner jj's receive buffer
     unsigned long long* s_key = reinterpret_cast<unsigned long long*>(scatter_smem);
     uint32_t* srow_all = reinterpret_cast<uint32_t*>(scatter_smem + (size_t)nown * 8);
+    // kModeBucket: per-warp write combining — a region's staged stream is contiguous per
+    // chunk, so every completed 32-B sector leaves as two 16-B stores. Each bucket has a ring
+    // of 64 u16 slots (4 sectors, slot = position & 63): one group gives a bucket <= 32
+    // consecutive positions, i.e. <= 3 sectors including the one still filling from earlier
+    // groups, so no two live elements share a slot; a sector is flushed (after the group's
+    // writes) in the group that completes it, before any later group can reuse its slots.
+    uint16_t* wb = reinterpret_cast<uint16_t*>(
+        scatter_smem + (((size_t)nown * 8 + (size_t)wpb * nown * 4 + 15) & ~(size_t)15) +
+        (size_t)wib * nown * 128);
     if (kSmemRow) {
         if (kMode == kModeBits && !a.cpb)
             for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
@@ -431,10 +441,11 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                 const uint64_t i = ib + 32 * q + lane;
                 const uint32_t jj = jjv[q];
                 const uint32_t pm = peers[q];
+                uint64_t pos = 0;
                 if (inv[q]) {
                     const uint32_t base = row[jj];
                     if ((pm >> lane) == 1u) row[jj] = base + (uint32_t)__popc(pm);
-                    const uint64_t pos = (uint64_t)base + __popc(pm & lanemask_lt());
+                    pos = (uint64_t)base + __popc(pm & lanemask_lt());
                     if constexpr (kMode == kModeIndex) {
                         a.idx_out[a.csr_off[jj] + pos] = i;
                     } else if constexpr (kMode == kModeOwner) {
@@ -443,11 +454,13 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                     } else if constexpr (kMode == kModeBucket) {
                         const uint32_t p = cur[q];
                         const uint32_t local = ((p & B::kVMask) - j_lo) & ((1u << a.bshift) - 1u);
-                        if (pos < a.cap)
-                            a.staging[jj * a.cap + pos] =
-                                (uint16_t)(local | (((p >> B::kDataShift) & 1u) << 15));
-                        else
+                        const uint16_t v = (uint16_t)(local | (((p >> B::kDataShift) & 1u) << 15));
+                        if (pos >= a.cap)
                             atomicOr(a.flags, kFlagBucketOverflow);
+                        else if (kSmemRow)
+                            wb[jj * 64 + (uint32_t)(pos & 63)] = v;
+                        else
+                            a.staging[jj * a.cap + pos] = v;
                     } else if ((cur[q] >> B::kDataShift) & 1u) {
                         if (a.cpb) {  // staged rounds: chunk c lies in bucket c / cpb
                             const uint32_t jf = (uint32_t)((c / a.cpb) << a.bshift) + jj;
@@ -465,6 +478,35 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                     }
                 }
                 __syncwarp();
+                if constexpr (kMode == kModeBucket && kSmemRow) {
+                    // flush a sector when this round completes it, or ends the chunk's range
+                    // in the bucket; sectors shared with a neighbouring chunk go element-wise
+                    if (inv[q] && pos < a.cap) {
+                        const uint32_t slot = (uint32_t)(pos & 15);
+                        bool flush = slot == 15;
+                        if (!flush) {
+                            const uint64_t end = c + 1 < a.c_end ? a.offs[(c + 1) * nown + jj]
+                                                                 : a.tot[jj];
+                            flush = pos + 1 == end;
+                        }
+                        if (flush) {
+                            const uint64_t start = a.offs[c * nown + jj];  // global row: unchanged
+                            const uint64_t s0 = pos & ~15ull;
+                            uint16_t* dst = a.staging + jj * a.cap;
+                            const uint16_t* w = wb + jj * 64;
+                            if (slot == 15 && s0 >= start) {
+                                uint4* d4 = reinterpret_cast<uint4*>(dst + s0);
+                                const uint4* w4 = reinterpret_cast<const uint4*>(w + (s0 & 63));
+                                d4[0] = w4[0];
+                                d4[1] = w4[1];
+                            } else {
+                                for (uint64_t t = s0 > start ? s0 : start; t <= pos; ++t)
+                                    dst[t] = w[t & 63];
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
             }
 #pragma unroll
             for (int q = 0; q < U; ++q) cur[q] = nxt[q];
@@ -622,13 +664,14 @@ bool scatter_match() {  // dev switch for A/B: SSBH_SCATTER_PEERS=ballot|match
 
 template <int kMode, typename Src>
 void scatter_launch(const Src& src, ScatterArgs a, cudaStream_t st) {
-    const size_t row_bytes = (size_t)a.nown * 4;
+    // per-warp bytes: running-rank row (+ write-combining sectors for the bucket split)
+    const size_t row_bytes = (size_t)a.nown * 4 + (kMode == kModeBucket ? (size_t)a.nown * 128 : 0);
     const bool smem = row_bytes <= 32768;
     int wpb = 8;
     size_t shm = 0;
-    if (smem) {  // per-warp running-rank rows + the per-key u64 table
+    if (smem) {  // per-warp rows (+ sectors) + the per-key u64 table
         wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / row_bytes));
-        shm = row_bytes * wpb + (size_t)a.nown * 8;
+        shm = row_bytes * wpb + (size_t)a.nown * 8 + 16;
     }
     const uint64_t nc = a.c_end - a.c_begin;
     const uint64_t blocks = std::max<uint64_t>(1, (nc + wpb - 1) / wpb);
@@ -774,7 +817,10 @@ void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d
 BucketGeom make_bucket_geom(uint64_t n_src, uint64_t s, uint32_t j_lo, uint32_t nown,
                             double mean_per_block, bool has_keep, int max_chunk_shift) {
     BucketGeom bg{};
+    // >= 128 blocks per bucket and <= kMaxBuckets buckets (the split's per-warp shared memory
+    // grows with the bucket count)
     bg.shift = kBucketShift;
+    while (((uint64_t)nown + (1ull << bg.shift) - 1) >> bg.shift > kMaxBuckets) ++bg.shift;
     const uint32_t bb = 1u << bg.shift;
     bg.nbuckets = (nown + bb - 1) / bb;
     // pass A: keys = buckets; u16 payload whenever V fits 15 bits (no keep marker needed)
@@ -808,8 +854,8 @@ BucketGeom make_bucket_geom(uint64_t n_src, uint64_t s, uint32_t j_lo, uint32_t 
 }
 
 void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void* d_payload,
-                         uint32_t* d_offsets_a, uint16_t* d_staging, uint32_t* d_flags,
-                         cudaStream_t st) {
+                         uint32_t* d_offsets_a, const unsigned long long* d_tot_a,
+                         uint16_t* d_staging, uint32_t* d_flags, cudaStream_t st) {
     if (ga.n == 0) return;
     ScatterArgs a = scatter_args(ga, d_offsets_a, nullptr, nullptr, nullptr, nullptr, nullptr);
     a.nown = bg.nbuckets;
@@ -818,6 +864,7 @@ void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void
     a.cap = bg.cap;
     a.staging = d_staging;
     a.flags = d_flags;
+    a.tot = d_tot_a;
     if (ga.payload_bytes == 2)
         scatter_launch<kModeBucket>(PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload)},
                                     a, st);

@@ -595,7 +595,7 @@ def test_run_extraction_gpu_random_vs_oracle(dev, oracle):
 
 
 # ------------------------------------------- two-level split (large key spaces, BucketGeom)
-# Plans with >= 4096 owned blocks split rounds by bucket (128 blocks) into staging regions
+# Plans with >= 4096 owned blocks split rounds by bucket (>= 128 blocks, <= 64 buckets) into staging regions
 # first; SSBH_BUCKETS=1 forces that path at small sizes so every case is checked against the
 # oracle: several buckets and a partial last one, non-power-of-two s, per-block seeds,
 # k % 32 != 0, owned block ranges, keep masks, streaming chunks in any order, graph replay.
@@ -607,6 +607,7 @@ def two_level(monkeypatch):
 def test_two_level_extract_vs_oracle(dev, oracle, two_level):
     rng = np.random.default_rng(91)
     cases = [(300000, 1000, 64, False), (500000, 4096, 32, True), (250000, 333, 77, True),
+             (2000000, 20000, 32, False),
              (400000, 129, 1024, False), (100000, 7, 96, False)]
     for n, s, k, pb in cases:
         x = oracle.make_input(int(rng.integers(100)), float(rng.choice([0.5, 0.3])), n)
