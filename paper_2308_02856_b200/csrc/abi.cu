@@ -321,7 +321,11 @@ struct LayoutBufs {
 uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid) {
     const uint64_t yw = std::max<uint64_t>(1, (mean_nj + 31) / 32);
     uint64_t kt = kHashKTMax;
-    const uint64_t want_items = (uint64_t)grid * 16;
+    static const uint64_t per_cta = [] {  // dev A/B knob: SSBH_KT_ITEMS_PER_CTA
+        const char* e = std::getenv("SSBH_KT_ITEMS_PER_CTA");
+        return e ? std::strtoull(e, nullptr, 10) : 8ull;  // 8: config 2 hash 0.870 -> 0.888
+    }();
+    const uint64_t want_items = (uint64_t)grid * per_cta;
     while (kt > 64) {
         const uint64_t items = (uint64_t)rowtiles * nown * ((yw + kt - 1) / kt);
         if (items >= want_items) break;
