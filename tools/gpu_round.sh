@@ -13,3 +13,8 @@ timeout 300 $CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__t
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_hash -s 3 -c 1 -o gpurun_out/hash_c3 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_count_rows|k_scatter" -s 6 -c 2 -o gpurun_out/sampler_c3 $CMD > gpurun_out/ncu_sampler.log 2>&1; echo ncu3 rc=$?
 ls -la gpurun_out
+# two-level split at the config-4 shape (k = 64 isolates the sampler): launch list + full capture
+SCMD="python tools/sampler_time.py --log2n 34 --s 16384 --reps 1"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4_sampler.csv $SCMD > gpurun_out/ncu_c4list.log 2>&1; echo ncu4 rc=$?
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_count_rows" -c 4 -o gpurun_out/sampler_c4 $SCMD > gpurun_out/ncu_c4full.log 2>&1; echo ncu5 rc=$?
+ls -la gpurun_out
