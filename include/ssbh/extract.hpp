@@ -25,6 +25,9 @@ struct ExtractOptions {
     std::uint32_t block_count = 0;  ///< 0 = all blocks
     std::uint64_t block_limit = 0;  ///< 0 = no abort check; else strict n_j > limit aborts
     int device = -1;                ///< CUDA device, -1 = current
+    /// > 1 entries: one process over these GPUs (sharded sampling, owner split through peer
+    /// memory; the whole key — block_first/block_count must be 0). Entries may repeat.
+    std::vector<int> devices;
 };
 
 struct ExtractResult {

@@ -255,6 +255,16 @@ ssbh_status ssbh_shard_finish(ssbh_shard* shard, uint32_t* d_key, uint64_t* d_le
 ssbh_status ssbh_shard_check(ssbh_shard* shard, ssbh_extract_stats* stats);
 ssbh_status ssbh_shard_set_timing(ssbh_shard* shard, int enable);
 
+/* The same sharded extraction driven from ONE process over several GPUs (the reference's
+ * callers are single-process C++): rank r runs on devices[r] (entries may repeat), receive
+ * buffers are exchanged as device pointers with peer access enabled between distinct devices,
+ * one host thread per rank, thread joins as the barriers. Host input / key / lengths as in
+ * ssbh_extract; the whole key (block_first = 0, all blocks). ndev == 1 is ssbh_extract on
+ * devices[0]. stats: hash_word_ops and min/max length over all blocks. */
+ssbh_status ssbh_extract_multi(const ssbh_extract_params* params, const uint64_t* input,
+                               const int* devices, uint32_t ndev, uint64_t* out_key,
+                               uint64_t* out_lengths, ssbh_extract_stats* stats);
+
 /* ----------------------------------------- protocol rounds (run_extraction's hash stage)
  * RoundRecord bytes (proj/include/ssbh/pipeline.hpp:15-38): bit 0 BasisAx, 1 BasisBx,
  * 2 Detected, 3 BitA, 4 BitB, 5 IsTest; is_key_round = Detected && !BasisAx && !BasisBx. */

@@ -48,6 +48,7 @@ ABI_SYMBOLS = (
     "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
     "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
+    "ssbh_extract_multi",
 )
 
 
@@ -246,6 +247,9 @@ def _load():
     L.ssbh_run_extraction_device.restype = st
     L.ssbh_run_extraction_device.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(ExtractionParams),
                                              U64P, U64P, C.POINTER(ExtractionResult)]
+    L.ssbh_extract_multi.restype = st
+    L.ssbh_extract_multi.argtypes = [C.POINTER(ExtractParams), U64P, C.POINTER(C.c_int), C.c_uint32,
+                                     U64P, U64P, C.POINTER(ExtractStats)]
     return L
 
 
@@ -437,6 +441,20 @@ def extract(x, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0
         _check(lib.ssbh_extract_sifted(C.byref(params), _p64(x), _p64(kp), _p64(key),
                                        _p64(lens), C.byref(st)))
     return key[: nwords(owned * k)], lens, st
+
+
+def extract_multi(x, n, s, k, samp, hsh, devices, per_block=False, limit=0):
+    """One process over several GPUs (ssbh_extract_multi: sharded sampling, owner split through
+    peer memory, one host thread per device). Returns (key words, n_j, stats)."""
+    params = make_params(n, s, k, samp, hsh, per_block, 0, 0, limit)
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    key = np.zeros(max(nwords(s * k), 1), dtype=np.uint64)
+    lens = np.zeros(s, dtype=np.uint64)
+    st = ExtractStats()
+    devs = (C.c_int * len(devices))(*devices)
+    _check(lib.ssbh_extract_multi(C.byref(params), _p64(x), devs, len(devices), _p64(key),
+                                  _p64(lens), C.byref(st)))
+    return key[: nwords(s * k)], lens, st
 
 
 # ------------------------------------------------------------ protocol rounds (pipeline.hpp)

@@ -10,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ssbh_cuda.h"
@@ -1493,4 +1494,181 @@ extern "C" ssbh_status ssbh_run_extraction(const uint8_t* rounds, uint64_t n,
     CU(d.alloc(n));
     CU(cudaMemcpy(d.p, rounds, n, cudaMemcpyHostToDevice));
     return ssbh_run_extraction_device(d.as<uint8_t>(), n, p, out_key, out_lengths, res);
+}
+
+// ======================================================================== in-process multi-GPU
+namespace {
+
+// dst bits [off, off + nbits) |= src bits [0, nbits) (dst pre-zeroed; host words)
+void or_bits(uint64_t* dst, uint64_t off, const uint64_t* src, uint64_t nbits) {
+    const uint64_t nw = words64(nbits);
+    const unsigned sh = (unsigned)(off & 63);
+    uint64_t* d = dst + (off >> 6);
+    for (uint64_t w = 0; w < nw; ++w) {
+        uint64_t v = src[w];
+        if (w + 1 == nw && (nbits & 63)) v &= (1ull << (nbits & 63)) - 1;
+        d[w] |= v << sh;
+        if (sh && (w + 1 < nw || ((nbits & 63) == 0 ? 64 : (nbits & 63)) + sh > 64))
+            d[w + 1] |= v >> (64 - sh);
+    }
+}
+
+struct RankRun {
+    ssbh_shard* sh = nullptr;
+    int device = 0;
+    cudaStream_t st = nullptr;
+    DBuf slice, key, len;
+    std::vector<uint64_t> counts, key_host, len_host;
+    ssbh_status status = SSBH_OK;
+    std::string msg;
+};
+
+// Runs fn(rank) on one host thread per rank (each bound to its device); the first failure's
+// status and message become the caller's.
+template <class Fn>
+ssbh_status on_ranks(std::vector<RankRun>& rr, Fn fn) {
+    std::vector<std::thread> th;
+    for (size_t r = 0; r < rr.size(); ++r)
+        th.emplace_back([&, r] {
+            if (cudaSetDevice(rr[r].device) != cudaSuccess) {
+                rr[r].status = SSBH_CUDA;
+                rr[r].msg = "set_device failed";
+                return;
+            }
+            rr[r].status = fn(r);
+            if (rr[r].status != SSBH_OK) rr[r].msg = g_err;
+        });
+    for (auto& t : th) t.join();
+    for (auto& x : rr)
+        if (x.status != SSBH_OK) return fail(x.status, "%s", x.msg.c_str());
+    return SSBH_OK;
+}
+
+}  // namespace
+
+// One process driving several GPUs: the sharded protocol of ssbh_shard_* with the receive
+// buffers exchanged as plain device pointers (peer access enabled between distinct devices)
+// and the three phases separated by thread joins instead of torch.distributed.
+extern "C" ssbh_status ssbh_extract_multi(const ssbh_extract_params* params, const uint64_t* input,
+                                          const int* devices, uint32_t ndev, uint64_t* out_key,
+                                          uint64_t* out_lengths, ssbh_extract_stats* stats) {
+    if (!params || !input || !out_key || !devices || ndev == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "extract_multi: null argument / no devices");
+    if (params->block_first != 0 || (params->block_count && params->block_count != params->n_subblocks))
+        return fail(SSBH_INVALID_ARGUMENT, "extract_multi: produces the whole key (block range 0, all)");
+    NEED_DEVICE();
+    for (uint32_t r = 0; r < ndev; ++r)
+        if (devices[r] < 0 || devices[r] >= usable_devices())
+            return fail(SSBH_INVALID_ARGUMENT, "extract_multi: device %d out of range", devices[r]);
+    int prev = 0;
+    CU(cudaGetDevice(&prev));
+    if (ndev == 1) {
+        CU(cudaSetDevice(devices[0]));
+        const ssbh_status s = ssbh_extract(params, input, out_key, out_lengths, stats);
+        cudaSetDevice(prev);
+        return s;
+    }
+    const uint64_t n = params->n_rounds, k = params->out_bits, s = params->n_subblocks;
+    std::vector<RankRun> rr(ndev);
+    for (uint32_t r = 0; r < ndev; ++r) rr[r].device = devices[r];
+    auto cleanup = [&] {
+        for (auto& x : rr) {
+            cudaSetDevice(x.device);
+            if (x.sh) ssbh_shard_destroy(x.sh);
+            if (x.st) cudaStreamDestroy(x.st);
+            x.slice.release();
+            x.key.release();
+            x.len.release();
+        }
+        cudaSetDevice(prev);
+    };
+    ssbh_status st = on_ranks(rr, [&](size_t r) -> ssbh_status {
+        if (auto e = ssbh_shard_create(params, (uint32_t)r, ndev, &rr[r].sh)) return e;
+        CU(cudaStreamCreateWithFlags(&rr[r].st, cudaStreamNonBlocking));
+        return SSBH_OK;
+    });
+    if (st == SSBH_OK) {
+        // receive buffers as plain pointers; peer access between distinct devices
+        for (uint32_t r = 0; r < ndev; ++r) {
+            cudaSetDevice(rr[r].device);
+            for (uint32_t q = 0; q < ndev; ++q) {
+                rr[r].sh->peer[q] = rr[q].sh->recv.p;
+                if (rr[q].device != rr[r].device) {
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(rr[q].device, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else if (e != cudaSuccess) {
+                        st = fail(SSBH_CUDA, "extract_multi: peer access %d -> %d: %s", rr[r].device,
+                                  rr[q].device, cudaGetErrorString(e));
+                        break;
+                    }
+                }
+            }
+            if (st != SSBH_OK) break;
+            if (cudaMemcpy(rr[r].sh->d_dst.p, rr[r].sh->peer.data(), (size_t)ndev * sizeof(void*),
+                           cudaMemcpyHostToDevice) != cudaSuccess) {
+                st = fail(SSBH_CUDA, "extract_multi: peer table upload failed");
+                break;
+            }
+        }
+    }
+    // phase 1: each rank samples its slice of rounds
+    if (st == SSBH_OK)
+        st = on_ranks(rr, [&](size_t r) -> ssbh_status {
+            RankRun& x = rr[r];
+            const uint64_t lo = x.sh->slice_lo, cnt = x.sh->slice_n;
+            const uint64_t w0 = lo / 64, w1 = words64(lo + cnt);
+            CU(x.slice.alloc((w1 - w0) * 8 + 16));
+            if (cnt)
+                CU(cudaMemcpyAsync(x.slice.p, input + w0, (w1 - w0) * 8, cudaMemcpyHostToDevice,
+                                   x.st));
+            x.counts.assign(ndev, 0);
+            return ssbh_shard_sample(x.sh, x.slice.as<uint32_t>(), nullptr, x.counts.data(), x.st);
+        });
+    // phase 2: owner split through peer memory (every rank needs every rank's counts)
+    std::vector<uint64_t> matrix((size_t)ndev * ndev);
+    for (uint32_t r = 0; r < ndev && st == SSBH_OK; ++r)
+        std::memcpy(matrix.data() + (size_t)r * ndev, rr[r].counts.data(), (size_t)ndev * 8);
+    if (st == SSBH_OK)
+        st = on_ranks(rr, [&](size_t r) -> ssbh_status {
+            return ssbh_shard_exchange(rr[r].sh, matrix.data(), rr[r].st);
+        });
+    // phase 3 (after the join = barrier): owners hash their blocks
+    if (st == SSBH_OK)
+        st = on_ranks(rr, [&](size_t r) -> ssbh_status {
+            RankRun& x = rr[r];
+            const uint64_t cnt = x.sh->p.block_count;
+            const uint64_t kw64 = words64(cnt * k);
+            CU(x.key.alloc(kw64 * 8 + 16));
+            CU(x.len.alloc(cnt * 8 + 8));
+            CU(cudaMemsetAsync(x.key.p, 0, kw64 * 8 + 16, x.st));
+            if (auto e = ssbh_shard_finish(x.sh, x.key.as<uint32_t>(), x.len.as<uint64_t>(), nullptr,
+                                           x.st))
+                return e;
+            if (auto e = ssbh_shard_check(x.sh, nullptr)) return e;
+            x.key_host.resize(kw64 + 1);
+            x.len_host.resize(cnt + 1);
+            CU(cudaMemcpy(x.key_host.data(), x.key.p, kw64 * 8, cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(x.len_host.data(), x.len.p, cnt * 8, cudaMemcpyDeviceToHost));
+            return SSBH_OK;
+        });
+    if (st == SSBH_OK) {
+        std::memset(out_key, 0, words64(s * k) * 8);
+        ssbh_extract_stats agg{};
+        agg.min_len = ~0ull;
+        for (auto& x : rr) {
+            const uint64_t first = x.sh->p.block_first, cnt = x.sh->p.block_count;
+            or_bits(out_key, first * k, x.key_host.data(), cnt * k);
+            if (out_lengths) std::memcpy(out_lengths + first, x.len_host.data(), cnt * 8);
+            for (uint64_t i = 0; i < cnt; ++i) {
+                agg.max_len = std::max<uint64_t>(agg.max_len, x.len_host[i]);
+                agg.min_len = std::min<uint64_t>(agg.min_len, x.len_host[i]);
+                agg.hash_word_ops += x.len_host[i] * k / 32;
+            }
+        }
+        agg.hash_launches = ndev;
+        if (stats) *stats = agg;
+        (void)n;
+    }
+    cleanup();
+    return st == SSBH_OK ? ok() : st;
 }

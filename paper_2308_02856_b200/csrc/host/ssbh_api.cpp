@@ -296,7 +296,12 @@ ExtractResult extract(const BitString& input, std::uint32_t n_subblocks,
     BitString key(owned * out_bits_per_block);
     ssbh_extract_stats st{};
     const ssbh_status s =
-        ssbh_extract(&p, input.words().data(), key.words().data(), r.block_lengths.data(), &st);
+        opt.devices.size() > 1
+            ? ssbh_extract_multi(&p, input.words().data(), opt.devices.data(),
+                                 static_cast<std::uint32_t>(opt.devices.size()), key.words().data(),
+                                 r.block_lengths.data(), &st)
+            : ssbh_extract(&p, input.words().data(), key.words().data(), r.block_lengths.data(),
+                           &st);
     if (s == SSBH_ABORT_OVERSIZE) {
         r.aborted = true;
         return r;

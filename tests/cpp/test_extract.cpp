@@ -96,3 +96,29 @@ TEST_CASE("owned block ranges, abort and empty blocks") {
     CHECK_FALSE(extract(data, 16, 512, seed_n(4), seed_n(5), lim).aborted);
     CHECK_THROWS_AS(extract(BitString(64), 1000, 8, seed_n(1), seed_n(2)), std::invalid_argument);
 }
+
+TEST_CASE("one process over several devices equals one device") {
+    // ssbh_extract_multi with ranks on repeated device ids (a 1-GPU box): sharded sampling,
+    // owner split through device pointers, per-owner hashing, bit-offset concatenation
+    const BitString data = KeyedStream(seed_n(6), "input").bits(300001);
+    for (std::uint64_t k : {512ull, 77ull}) {
+        ExtractOptions pb;
+        pb.seed_mode = SeedMode::PerBlock;
+        const ExtractResult one = extract(data, 33, k, seed_n(7), seed_n(8), pb);
+        for (std::size_t nd : {2u, 3u}) {
+            ExtractOptions m = pb;
+            m.devices.assign(nd, 0);
+            const ExtractResult multi = extract(data, 33, k, seed_n(7), seed_n(8), m);
+            CHECK(multi.key == one.key);
+            CHECK(multi.block_lengths == one.block_lengths);
+            CHECK(multi.hash_word_ops > 0);
+        }
+    }
+    std::uint64_t mx = 0;
+    const ExtractResult full = extract(data, 33, 512, seed_n(7), seed_n(8));
+    for (auto l : full.block_lengths) mx = std::max(mx, l);
+    ExtractOptions lim;
+    lim.devices = {0, 0};
+    lim.block_limit = mx - 1;
+    CHECK(extract(data, 33, 512, seed_n(7), seed_n(8), lim).aborted);
+}

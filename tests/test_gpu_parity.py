@@ -667,3 +667,28 @@ def test_two_level_streaming(dev, oracle, two_level):
     want, _ = oracle.extract(x, n, s, 31, 32, 0, k)
     got, _, _ = _stream_run(dev, x, n, s, k, 31, 32, 1 << 14, block_first=100, block_count=300)
     assert (got == want[100:400]).all()
+
+
+# ------------------------------------------------ one process over several GPUs (C-ABI)
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_extract_multi_vs_oracle(dev, oracle, ndev):
+    """ssbh_extract_multi with ranks on repeated device ids (1-GPU box): same key and n_j as
+    the oracle, including bit-offset concatenation (k % 64 != 0) and per-block seeds."""
+    rng = np.random.default_rng(101 + ndev)
+    for n, s, k, pb in ((300000, 16, 512, False), (250001, 33, 77, True), (1 << 20, 64, 8192, False)):
+        x = oracle.make_input(int(rng.integers(1000)), 0.5, n)
+        want, wnj = oracle.extract(x, n, s, 2, 3, pb, k)
+        got, nj, st = dev.extract_multi(x, n, s, k, 2, 3, [0] * ndev, per_block=pb)
+        assert (nj == wnj).all(), (n, s, k, ndev)
+        assert (got == want).all(), (n, s, k, ndev)
+        assert int(st.hash_word_ops) > 0
+    with pytest.raises(ValueError):
+        dev.extract_multi(x, n, s, k, 2, 3, [0, 99])
+
+
+def test_extract_multi_two_level_owners(dev, oracle, two_level):
+    n, s, k = 600000, 900, 64
+    x = oracle.make_input(12, 0.5, n)
+    want, wnj = oracle.extract(x, n, s, 2, 3, True, k)
+    got, nj, _ = dev.extract_multi(x, n, s, k, 2, 3, [0, 0], per_block=True)
+    assert (nj == wnj).all() and (got == want).all()
