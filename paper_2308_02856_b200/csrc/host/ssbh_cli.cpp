@@ -2,10 +2,11 @@
 // (proj/tools/ssbh_main.cpp), on the drop-in API (libssbh.so -> libssbh_cuda.so):
 //
 //   ssbh-b200 extract --in FILE --in-bits N --out-bits L [--ns S] [--seed HEX64]
-//                     [--eps-abort E] [--out FILE] [--partition-csv FILE]
+//                     [--eps-abort E] [--out FILE] [--partition-csv FILE] [--gpus G]
 //       file mode of cmd_extract (ssbh_main.cpp:306-345): the master seed keys both the
 //       sampling and the per-block "hash-seed" streams (sub = j), L/S bits per block, strict
 //       oversize abort against block_limit(N, 1/S, eps_abort, S) (N when S == 1).
+//       --gpus G > 1: one process over GPUs 0..G-1 (ssbh_extract_multi).
 //   ssbh-b200 extract --simulate --n-rounds N --key-length L [--ns S] [--seed HEX64]
 //                     [--p-x P] [--e-ph E] [--e-bit E] [--q-tol Q] [--eta-tol T] [--p-det D]
 //                     [--eps-sec E] [--eps-abort E] [--out FILE] [--partition-csv FILE]
@@ -56,7 +57,7 @@ enum : int {
 struct Args {
     std::string cmd, in, out, partition_csv, seed_hex = std::string(64, '0');
     std::uint64_t in_bits = 0, out_bits = 0;
-    std::uint32_t ns = 1;
+    std::uint32_t ns = 1, gpus = 1;
     double eps_abort = 1e-8, out_ratio = 0.06303;
     std::vector<std::uint64_t> sizes;
     // simulate mode (Bbm92Params defaults, bbm92.hpp:14-26) and limit
@@ -91,6 +92,7 @@ Args parse(int argc, char** argv) {
         else if (f == "--in-bits") a.in_bits = parse_u64(val());
         else if (f == "--out-bits") a.out_bits = parse_u64(val());
         else if (f == "--ns") a.ns = static_cast<std::uint32_t>(parse_u64(val()));
+        else if (f == "--gpus") a.gpus = static_cast<std::uint32_t>(parse_u64(val()));
         else if (f == "--eps-abort") a.eps_abort = std::stod(val());
         else if (f == "--out-ratio") a.out_ratio = std::stod(val());
         else if (f == "--simulate") a.simulate = true;
@@ -144,6 +146,8 @@ int cmd_extract(const Args& a) {
     ExtractOptions opt;
     opt.seed_mode = SeedMode::PerBlock;  // KeyedStream(seed, "hash-seed", j)
     opt.block_limit = limit;
+    for (std::uint32_t g = 0; a.gpus > 1 && g < a.gpus; ++g)  // one process over N GPUs
+        opt.devices.push_back(static_cast<int>(g));
     const auto t0 = std::chrono::steady_clock::now();
     const ExtractResult r = extract(data, a.ns, a.out_bits / a.ns, seed, seed, opt);
     const double secs =
