@@ -404,8 +404,11 @@ static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown)
     return SSBH_OK;
 }
 
+// external_payload: the plan consumes a payload it does not own (shard owners), whose element
+// size is external_payload_bytes.
 static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t chunk_bits,
-                                    ssbh_plan** out, bool external_payload = false) {
+                                    ssbh_plan** out, bool external_payload = false,
+                                    int external_payload_bytes = 0) {
     uint32_t nown = 0;
     if (auto s = validate_params(params, &nown)) return s;
     NEED_DEVICE();
@@ -423,6 +426,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     CU(cudaGetDevice(&pl->device));
     const uint64_t n = params->n_rounds, k = params->out_bits;
     pl->geom = make_sampler_geom(n, params->n_subblocks, params->block_first, nown, false, max_cs);
+    if (external_payload && external_payload_bytes) pl->geom.payload_bytes = external_payload_bytes;
     pl->kw = (uint32_t)((k + 31) / 32);
     pl->rowtiles = (pl->kw + kHashRowWords - 1) / kHashRowWords;
     pl->direct_out = (k % 32) == 0;
@@ -1175,6 +1179,8 @@ extern "C" ssbh_status ssbh_shard_create(const ssbh_extract_params* params, uint
     sh->slice_n = slice_bound(n, world, rank + 1) - sh->slice_lo;
     sh->gs = make_sampler_geom(sh->slice_n ? sh->slice_n : 1, s, 0, world, false);
     sh->gs.n = sh->slice_n;
+    // shards take no keep mask, so no u16 sift marker: V up to 0x7fff fits (s <= 2^15)
+    sh->gs.payload_bytes = s <= 32768 ? 2 : 4;
     // receive capacity: the largest owner's expected share + 16 sigma + slack
     uint64_t maxc = 0;
     for (uint32_t o = 0; o < world; ++o)
@@ -1201,7 +1207,7 @@ extern "C" ssbh_status ssbh_shard_create(const ssbh_extract_params* params, uint
     sh->peer[rank] = sh->recv.p;
     ssbh_extract_params op = sh->p;
     op.n_rounds = sh->recv_cap;
-    if (auto st = plan_create_impl(&op, 0, &sh->plan, /*external_payload=*/true)) {
+    if (auto st = plan_create_impl(&op, 0, &sh->plan, /*external_payload=*/true, pb)) {
         const std::string msg = g_err;
         ssbh_shard_destroy(sh);
         g_err = msg;

@@ -415,8 +415,8 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                 bool kept = i < i1;
                 if (B::kKeepShift < 32) kept = kept && !((p >> (B::kKeepShift & 31)) & 1u);
                 if (kMode == kModeOwner) {
-                    // u16: V = 0x7fff is a sifted-out round (s < 2^15 never reaches it)
-                    if (B::kKeepShift >= 32) kept = kept && (p & B::kVMask) != B::kVMask;
+                    // shard payloads carry no sift marker (no keep mask on that path), so a
+                    // u16 V may be 0x7fff (s = 2^15)
                     jjv[q] = owner_of(p & B::kVMask, nown, a.s);
                     inv[q] = kept;
                 } else if (kMode == kModeBucket) {

@@ -86,3 +86,10 @@ def test_sharded_world2_two_level(monkeypatch):
     # several buckets per owner, a partial last bucket, per-block seeds
     monkeypatch.setenv("SSBH_BUCKETS", "1")
     _run(2, [(600000, 600, 320, True), (400000, 300, 96, False)])
+
+
+@pytest.mark.gpu
+def test_sharded_world2_s32768_u16():
+    # s = 2^15: shard payloads stay u16 (no sift marker on that path), V = 0x7fff included;
+    # owners of 16384 blocks run the two-level split
+    _run(2, [(1 << 22, 32768, 64, False)])
