@@ -184,6 +184,20 @@ ssbh_status ssbh_plan_run_device(ssbh_plan* plan, const uint32_t* d_input, uint3
 ssbh_status ssbh_plan_check(ssbh_plan* plan, ssbh_extract_stats* stats);
 ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
 
+/* Hash engine of a plan (not a reference interface: the reference has one CPU loop).
+ *   SSBH_ENGINE_LOP3   : GF(2) product on the integer ALUs (LOP3/SHF/POPC) — every plan.
+ *   SSBH_ENGINE_TENSOR : shared-seed plans only: all blocks share one Hankel matrix, so the
+ *                        hash is one u8 GEMM mod 2 on the tcgen05 tensor cores (kind::i8).
+ *   SSBH_ENGINE_AUTO   : the plan's default (LOP3; environment SSBH_HASH_ENGINE=tensor
+ *                        selects the tensor engine for shared-seed plans).
+ * Both engines produce identical keys. TENSOR on a per-block-seed plan ->
+ * SSBH_INVALID_ARGUMENT. ssbh_plan_engine returns the engine in use. */
+#define SSBH_ENGINE_AUTO 0
+#define SSBH_ENGINE_LOP3 1
+#define SSBH_ENGINE_TENSOR 2
+ssbh_status ssbh_plan_set_engine(ssbh_plan* plan, int engine);
+int ssbh_plan_engine(const ssbh_plan* plan);
+
 /* Host-buffer entry point (what a reference caller binds): input host words (n bits),
  * out_key host words (ceil(owned*k/64)), out_lengths host (owned entries, may be NULL).
  * H2D, device run, D2H; synchronous. */

@@ -48,8 +48,10 @@ ABI_SYMBOLS = (
     "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
     "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
-    "ssbh_extract_multi",
+    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine",
 )
+
+ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
 
 
 class SsbhError(RuntimeError):
@@ -138,6 +140,10 @@ def _load():
     L.ssbh_set_device.argtypes = [C.c_int]
     L.ssbh_prf_block.restype = st
     L.ssbh_prf_block.argtypes = [U64P, U64P, U64P]
+    L.ssbh_plan_set_engine.restype = st
+    L.ssbh_plan_set_engine.argtypes = [C.c_void_p, C.c_int]
+    L.ssbh_plan_engine.restype = C.c_int
+    L.ssbh_plan_engine.argtypes = [C.c_void_p]
     L.ssbh_prf_tag.restype = C.c_uint64
     L.ssbh_prf_tag.argtypes = [C.c_char_p, C.c_size_t]
     L.ssbh_stream_bits.restype = st
@@ -513,7 +519,7 @@ class Plan:
     chunk_bits > 0 creates a streaming plan (stream_begin / stream_chunk / stream_finish)."""
 
     def __init__(self, n, s, k, samp, hsh, per_block=False, block_first=0, block_count=0,
-                 limit=0, chunk_bits=0):
+                 limit=0, chunk_bits=0, engine=ENGINE_AUTO):
         self.params = make_params(n, s, k, samp, hsh, per_block, block_first, block_count,
                                   limit)
         self.owned = block_count or s
@@ -525,6 +531,16 @@ class Plan:
         else:
             _check(lib.ssbh_plan_create(C.byref(self.params), C.byref(h)))
         self.h = h
+        if engine != ENGINE_AUTO:
+            self.set_engine(engine)
+
+    def set_engine(self, engine: int):
+        """ENGINE_LOP3 (integer ALUs) or ENGINE_TENSOR (tcgen05 u8 GEMM mod 2, shared seed)."""
+        _check(lib.ssbh_plan_set_engine(self.h, engine))
+
+    @property
+    def engine(self) -> int:
+        return int(lib.ssbh_plan_engine(self.h))
 
     def stream_begin(self, stream: int = 0, samp=None, hsh=None):
         sk = None if samp is None else _p64(key_of(samp))

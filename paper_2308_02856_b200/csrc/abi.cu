@@ -337,6 +337,14 @@ uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid)
 
 }  // namespace
 
+// Engine of a new plan: SSBH_HASH_ENGINE=lop3|tensor overrides; per-block seeds always LOP3.
+static int default_engine(uint32_t per_block_seed) {
+    if (per_block_seed) return kEngineLop3;
+    const char* e = std::getenv("SSBH_HASH_ENGINE");
+    if (e && std::strcmp(e, "tensor") == 0) return kEngineMma;
+    return kEngineLop3;
+}
+
 // ======================================================================== plan
 struct ssbh_plan {
     ssbh_extract_params p{};
@@ -373,6 +381,10 @@ struct ssbh_plan {
     uint64_t chunk_bits = 0;
     uint64_t stream_samp[4]{}, stream_hash[4]{};
     uint32_t stream_launches = 0;
+    // hash engine (shared-seed plans may run on the tensor cores, toeplitz_mma.cu)
+    int engine = kEngineLop3;
+    MmaGeom mma{};
+    DBuf mt_words;
     // host-path staging
     DBuf d_input, d_key, d_len, d_keep;
     cudaStream_t own_stream = nullptr;
@@ -442,6 +454,8 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     else
         pl->sbuf_words = round_up(seed_fixed + round_up((n + 31) / 32, kHashR) + 64, 8);
     pl->key_words32 = ((uint64_t)nown * k + 31) / 32;
+    pl->engine = default_engine(params->per_block_seed);
+    pl->mma = make_mma_geom(nown, pl->kw, n / params->n_subblocks, pl->device);
 
     // two-level split for large key spaces (SSBH_BUCKETS=0 disables it, =1 forces it)
     const char* be = std::getenv("SSBH_BUCKETS");
@@ -486,6 +500,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     if (!e) e = alloc(pl->ybuf, pl->ybuf_words * 4);
     if (!e) e = alloc(pl->sbuf, pl->sbuf_words * 4);
     if (!e && !pl->direct_out) e = alloc(pl->scratch, (size_t)nown * pl->kw * 4);
+    if (!e && !params->per_block_seed) e = alloc(pl->mt_words, (size_t)pl->mma.mtiles * 4);
     if (!e) e = pl->lay.alloc(nown);
     if (!e) e = cudaMallocHost(&pl->h_stats, sizeof(DevStats));
     for (int i = 0; i < 6 && !e; ++i) e = cudaEventCreate(&pl->ev[i]);
@@ -576,6 +591,28 @@ extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
 }
 
 extern "C" uint64_t ssbh_plan_device_bytes(const ssbh_plan* pl) { return pl ? pl->bytes : 0; }
+
+extern "C" ssbh_status ssbh_plan_set_engine(ssbh_plan* pl, int engine) {
+    if (!pl) return fail(SSBH_INVALID_ARGUMENT, "null plan");
+    if (engine < SSBH_ENGINE_AUTO || engine > SSBH_ENGINE_TENSOR)
+        return fail(SSBH_INVALID_ARGUMENT, "set_engine: unknown engine %d", engine);
+    int e = engine == SSBH_ENGINE_AUTO ? default_engine(pl->p.per_block_seed) : engine;
+    if (e == SSBH_ENGINE_TENSOR && pl->p.per_block_seed)
+        return fail(SSBH_INVALID_ARGUMENT,
+                    "set_engine: the tensor-core engine needs a shared seed (per-block seeds are "
+                    "one matrix-vector product per block)");
+    if (e != pl->engine) {
+        pl->engine = e;
+        for (auto& x : pl->exec)  // captured graphs hold the other engine's launches
+            if (x) {
+                cudaGraphExecDestroy(x);
+                x = nullptr;
+            }
+    }
+    return ok();
+}
+
+extern "C" int ssbh_plan_engine(const ssbh_plan* pl) { return pl ? pl->engine : -1; }
 
 extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
     if (!pl) return fail(SSBH_INVALID_ARGUMENT, "null plan");
@@ -680,6 +717,22 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
     const Layout lay = pl->lay.view();
     uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
     CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
+    if (pl->engine == kEngineMma) {
+        MmaHashArgs m{};
+        m.ybuf = pl->ybuf.as<uint32_t>();
+        m.sbuf = pl->sbuf.as<uint32_t>();
+        m.out = out;
+        m.out_stride = pl->direct_out ? pl->p.out_bits / 32 : pl->kw;
+        m.lay = lay;
+        m.nown = pl->nown;
+        m.kw = pl->kw;
+        m.ntiles = pl->mma.ntiles;
+        m.ksplit = pl->mma.ksplit;
+        m.items = pl->mma.items;
+        m.mt_words = pl->mt_words.as<uint32_t>();
+        launch_hash_mma(m, pl->mma, st);
+        launches += 2;
+    } else {
     HashArgs a{};
     a.ybuf = pl->ybuf.as<uint32_t>();
     a.sbuf = pl->sbuf.as<uint32_t>();
@@ -692,6 +745,7 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
     a.per_block_seed = pl->p.per_block_seed;
     launch_hash(a, pl->grid, st);
     launches += 1;
+    }
     if (!pl->direct_out) {
         launch_concat(pl->scratch.as<uint32_t>(), pl->kw, pl->nown, pl->p.out_bits, d_key, st);
         launches += 1;

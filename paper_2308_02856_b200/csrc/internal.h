@@ -192,6 +192,33 @@ void launch_reverse(const uint32_t* d_x32, uint64_t nbits, uint32_t* d_y, uint64
                     cudaStream_t st);
 int hash_grid_size(int device);
 void launch_hash(const HashArgs& a, int grid, cudaStream_t st);
+// Tensor-core engine for shared-seed plans (toeplitz_mma.cu): the hash of all owned blocks
+// as one u8 GEMM mod 2 (tcgen05.mma kind::i8). Same inputs/outputs as launch_hash.
+enum HashEngine : int { kEngineAuto = 0, kEngineLop3 = 1, kEngineMma = 2 };
+struct MmaGeom {
+    uint32_t mtiles;   // ceil(nown / 128)
+    uint32_t ntiles;   // ceil(kw / 8): 256 output rows per tile
+    uint32_t ksplit;   // K parts per (M, N) tile (red.xor when > 1)
+    uint32_t grid;     // persistent CTAs (one per SM)
+    uint64_t items;    // mtiles * ntiles * ksplit
+};
+struct MmaHashArgs {
+    const uint32_t* ybuf;
+    const uint32_t* sbuf;    // shared seed, pre-shifted by one bit (see launch_seeds)
+    uint32_t* out;           // out[jj * out_stride + word], zeroed when ksplit > 1
+    unsigned long long out_stride;
+    Layout lay;
+    uint32_t nown;
+    uint32_t kw;
+    uint32_t ntiles, ksplit;
+    uint64_t items;
+    uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
+};
+uint32_t mma_mtiles(uint32_t nown);
+MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
+size_t mma_hash_smem();
+void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st);
+
 // Concatenate nown blocks of k bits (block stride kw words) into key (bit offset jj*k).
 void launch_concat(const uint32_t* d_blocks, uint32_t kw, uint32_t nown, uint64_t k,
                    uint32_t* d_key, cudaStream_t st);

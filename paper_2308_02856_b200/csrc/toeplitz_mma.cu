@@ -1,0 +1,447 @@
+// toeplitz_mma.cu — shared-seed GF(2) Toeplitz hash on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM). Same product as k_toeplitz_hash
+// (proj/src/toeplitz.cpp:34-52), different engine; selected per plan (ssbh_plan_set_engine).
+//
+// Why a tensor-core engine exists. With the input reversed (y_j[c] = x_j[n_j-1-c]) block j's
+// output is K_j[i] = XOR_c S[i+c] y_j[c] (toeplitz.cu). With ONE shared seed every block
+// multiplies the SAME Hankel matrix H[i][c] = S[i+c], so the whole hash is a GF(2) matrix
+// product D = Y * H^T (blocks x input positions times input positions x output rows), and a
+// GF(2) product is an integer product mod 2: D[j][i] = (sum_c y_j[c] * S[i+c]) mod 2. The
+// u8 tensor-core path computes the integer sums exactly (s32 accumulators wrap mod 2^32,
+// which keeps the parity) at ~4x the bit-ops/s of the LOP3 engine. Per-block seeds
+// (config 4) have one matrix per block — a matrix-vector product — and stay on LOP3.
+//
+// Operands carry one bit per byte, in the byte's LSB; the other 7 bits may hold anything,
+// because they only add even multiples to the sum (a = a0 + 2a', b = b0 + 2b' gives
+// ab = a0 b0 + 2(...)). That makes both operands cheap to form in shared memory:
+//
+// * K order inside a 256-bit pipeline stage: byte (chunk q = 8g + kc, word w, byte b) of a
+//   K-major row is input position 128g + kc + 8b + 32w (any permutation of K is allowed as
+//   long as both operands use it).
+// * A = Y (M = 128 blocks): chunk q word w of block j is y-word (4g + w) >> kc — one shift
+//   per 4 bytes, canonical no-swizzle K-major layout (8-row core matrices, LBO 128 B along
+//   K, SBO 2048 B along M).
+// * B = Hankel (N = 256 output rows): with that K order, row r chunk (g, kc) holds S bits
+//   i0 + c0 + (r + kc + 128g) + 8b + 32w — a function of the UNIT index u = r + kc + 128g
+//   alone. So the operand is a table of 16-byte units, unit u word w = the 32-bit seed
+//   window starting at bit i0 + c0 + u + 32w (one funnel shift), and the descriptor walks
+//   it with LBO = 16 B (next K chunk = next unit) and SBO = 128 B (8 rows = 8 units):
+//   rows overlap in memory exactly as Hankel rows overlap in the seed. 392 units (6 KB)
+//   cover a 256-row x 256-position stage.
+//
+// Kernel: persistent, one CTA per SM (213 KB shared memory, 512 TMEM columns = two
+// 128 x 256 s32 accumulators). Work item = (M tile of 128 owned blocks, K part, N tile of
+// 256 output rows); every CTA walks items blockIdx.x, +grid, ... with N tiles innermost,
+// so concurrently running CTAs stream the same blocks' y words (L2 reuse). Warp roles:
+//   warps 0-3  epilogue: tcgen05.ld 32x32b (lane = block, 32 columns = 32 rows) -> parity
+//              bits -> one key word per load (st.global, or red.xor when K is split)
+//   warp 4     MMA issuer: 8 x tcgen05.mma (128x256x32) per stage, commit -> empty slot,
+//              last stage -> accumulator full (double-buffered accumulators)
+//   warps 5-8  A producers: block row jl, cp.async of its 32 y bytes 4 stages ahead, 16
+//              STS.128 of shifted words per stage
+//   warps 9-12 B producers: cp.async of 128 B of seed per stage, 392 units per stage
+// Ring of 5 stages (38 KB each) between producers and the MMA warp (mbarriers).
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace ssbh_impl {
+using namespace ssbh_dev;
+
+namespace {
+
+constexpr int kM = 128;                      // blocks per M tile (= TMEM lanes)
+constexpr int kN = 256;                      // output rows per N tile (= accumulator columns)
+constexpr int kMmaK = 32;                    // K bytes per tcgen05.mma kind::i8
+constexpr int kStageK = 256;                 // input positions per pipeline stage
+constexpr int kStageMmas = kStageK / kMmaK;  // 8
+constexpr int kGUnits = kN + 7 + 128 + 1;    // 392 Hankel units per stage
+constexpr int kStages = 5;
+constexpr int kPre = 4;                      // cp.async prefetch depth (stages)
+constexpr int kYBytes = kM * kStageK;        // 32768: A operand of one stage
+constexpr int kGBytes = kGUnits * 16;        // 6272: B operand of one stage
+constexpr int kSlotBytes = kYBytes + kGBytes;
+constexpr int kRawYBytes = kPre * kM * 32;   // y words staged by cp.async
+constexpr int kRawSBytes = 4 * kPre * 128;   // seed words staged by cp.async (per B warp)
+constexpr int kEpiWarps = 4, kMmaWarp = 4, kYWarp0 = 5, kGWarp0 = 9, kWarps = 13;
+constexpr int kThreads = kWarps * 32;
+constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps
+constexpr size_t kBarOff = (size_t)kStages * kSlotBytes + kRawYBytes + kRawSBytes;
+constexpr size_t kSmemBytes = kBarOff + (2 * kStages + 4) * 8 + 16;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+static_assert(kSlotBytes % 128 == 0, "slot alignment");
+
+// ------------------------------------------------------------------ tcgen05 / cp.async
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// Shared-memory matrix descriptor, SWIZZLE_NONE, version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// kind::i8 instruction descriptor: s32 accumulate, u8 x u8, both K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+#define SSBH_TMEM_LD32(taddr, v)                                                                 \
+    asm volatile(                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),             \
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),          \
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),          \
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),          \
+          "=r"(v[31])                                                                            \
+        : "r"(taddr))
+
+// ------------------------------------------------------------------ work items
+struct Item {
+    uint32_t mt, nt;     // M tile (128 owned blocks), N tile (256 output rows)
+    uint32_t st0, nst;   // stage range [st0, st0 + nst) of this K part
+};
+
+__device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item& d) {
+    if (item >= a.items) return false;
+    d.nt = item % a.ntiles;
+    const uint32_t r = item / a.ntiles;
+    const uint32_t kp = r % a.ksplit;
+    d.mt = r / a.ksplit;
+    const uint32_t ns = a.mt_words[d.mt] / (kStageK / 32);
+    const uint32_t lo = (uint32_t)((uint64_t)ns * kp / a.ksplit);
+    d.st0 = lo;
+    d.nst = (uint32_t)((uint64_t)ns * (kp + 1) / a.ksplit) - lo;
+    return true;
+}
+
+// Walks (item, stage) pairs of this CTA in order; used by the producers twice (consume and
+// prefetch kPre stages ahead).
+struct StageIt {
+    uint32_t item;
+    uint32_t s;      // stage within the item
+    Item d;
+    bool valid;
+    __device__ void start(const MmaHashArgs& a) {
+        item = blockIdx.x;
+        s = 0;
+        valid = decode(a, item, d);
+        skip_empty(a);
+    }
+    __device__ void skip_empty(const MmaHashArgs& a) {
+        while (valid && s >= d.nst) {
+            item += gridDim.x;
+            s = 0;
+            valid = decode(a, item, d);
+        }
+    }
+    __device__ void next(const MmaHashArgs& a) {
+        ++s;
+        skip_empty(a);
+    }
+};
+
+// A producer (one block row jl): stage the row's 256 y bits by cp.async (zero-filled past
+// the block's padded length or past the owned blocks).
+__device__ __forceinline__ void y_prefetch(const MmaHashArgs& a, const StageIt& p, uint32_t jl,
+                                           uint32_t* raw) {
+    const uint32_t* src = a.ybuf;
+    uint32_t bytes = 0;
+    if (p.valid) {
+        const uint32_t jj = p.d.mt * kM + jl;
+        const uint64_t w0 = (uint64_t)(p.d.st0 + p.s) * (kStageK / 32);
+        if (jj < a.nown && w0 < a.lay.ypad[jj]) {
+            src = a.ybuf + a.lay.yoff[jj] + w0;
+            bytes = 16;
+        }
+    }
+    cp_async16(raw, src, bytes);
+    cp_async16(raw + 4, src + 4, bytes);
+}
+
+// B producer warp: stage 32 seed words (pre-shifted seed S', S'[b] = S[b-1]) covering the
+// stage's windows; lanes 0-7 copy 16 B each.
+__device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& p, uint32_t lane,
+                                           uint32_t* raw) {
+    if (lane < 8) {
+        uint64_t q0a = 0;
+        if (p.valid) {
+            const uint64_t b1 = (uint64_t)p.d.nt * kN + (uint64_t)(p.d.st0 + p.s) * kStageK + 1;
+            q0a = (b1 >> 5) & ~3ull;
+        }
+        cp_async16(raw + 4 * lane, a.sbuf + q0a + 4 * lane, p.valid ? 16u : 0u);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* slots = smem;
+    uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kStages * kSlotBytes);
+    uint32_t* raw_s = raw_y + kRawYBytes / 4;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], kFullArrivals);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEpiWarps);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kEpiWarps) {
+        // ---------------------------------------------------------------- epilogue
+        uint32_t t = 0;
+        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
+            Item d;
+            if (!decode(a, item, d)) break;
+            const uint32_t ab = t & 1;
+            mbar_wait(&tfull[ab], (t >> 1) & 1);
+            tc_fence_after();
+            if (d.nst) {
+                const uint32_t jj = d.mt * kM + warp * 32 + lane;
+                const bool row_ok = jj < a.nown;
+                uint32_t* dst = a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32);
+#pragma unroll 1
+                for (int q = 0; q < kN / 32; ++q) {
+                    uint32_t v[32];
+                    SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kN + 32u * q, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) w |= (v[e] & 1u) << e;
+                    if (row_ok && d.nt * (kN / 32) + q < a.kw) {
+                        if (a.ksplit == 1)
+                            dst[q] = w;
+                        else
+                            atomicXor(dst + q, w);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------------------------------------------------------- MMA issuer
+        uint32_t g = 0, t = 0;
+        const uint32_t base_y = smem_u32(slots), base_g = base_y + kYBytes;
+        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
+            Item d;
+            if (!decode(a, item, d)) break;
+            const uint32_t ab = t & 1;
+            if (t >= 2) mbar_wait(&tempty[ab], ((t >> 1) - 1) & 1);
+            tc_fence_after();
+            if (d.nst == 0) {
+                if (lane == 0) mbar_arrive(&tfull[ab]);
+                continue;
+            }
+            for (uint32_t s = 0; s < d.nst; ++s, ++g) {
+                const uint32_t slot = g % kStages;
+                mbar_wait(&full[slot], (g / kStages) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t ya = base_y + slot * kSlotBytes;
+                    const uint32_t ga = base_g + slot * kSlotBytes;
+#pragma unroll
+                    for (int m = 0; m < kStageMmas; ++m) {
+                        const uint64_t adesc = sdesc(ya + 256u * m, 128, 2048);
+                        const uint32_t unit = 2u * (m & 3) + 128u * (m >> 2);
+                        const uint64_t bdesc = sdesc(ga + 16u * unit, 16, 128);
+                        mma_i8(tmem + ab * kN, adesc, bdesc, (s | (uint32_t)m) != 0);
+                    }
+                    mma_commit(&empty[slot]);
+                    if (s + 1 == d.nst) mma_commit(&tfull[ab]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp < kGWarp0) {
+        // ---------------------------------------------------------------- A producers
+        const uint32_t jl = threadIdx.x - kYWarp0 * 32;  // block row 0..127
+        uint32_t* raw = raw_y + jl * 8;                   // + slot * kM * 8
+        StageIt cur, pre;
+        cur.start(a);
+        pre.start(a);
+        for (int i = 0; i < kPre; ++i) {
+            y_prefetch(a, pre, jl, raw + i * kM * 8);
+            cp_async_commit();
+            if (pre.valid) pre.next(a);
+        }
+        const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
+        for (uint32_t g = 0; cur.valid; ++g, cur.next(a)) {
+            const uint32_t rs = g % kPre;
+            cp_async_wait<kPre - 1>();
+            const uint4 x0 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8);
+            const uint4 x1 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8 + 4);
+            const uint32_t slot = g % kStages;
+            if (g >= (uint32_t)kStages) mbar_wait(&empty[slot], ((g / kStages) - 1) & 1);
+            uint8_t* ys = slots + (size_t)slot * kSlotBytes + row_off;
+#pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                *reinterpret_cast<uint4*>(ys + kc * 128) =
+                    make_uint4(x0.x >> kc, x0.y >> kc, x0.z >> kc, x0.w >> kc);
+                *reinterpret_cast<uint4*>(ys + (8 + kc) * 128) =
+                    make_uint4(x1.x >> kc, x1.y >> kc, x1.z >> kc, x1.w >> kc);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[slot]);
+            // refill the raw slot just consumed (its values are in registers and stored)
+            y_prefetch(a, pre, jl, raw + rs * kM * 8);
+            cp_async_commit();
+            if (pre.valid) pre.next(a);
+        }
+        cp_async_wait<0>();
+    } else {
+        // ---------------------------------------------------------------- B producers
+        const uint32_t gw = warp - kGWarp0;                // 0..3
+        const uint32_t gt = threadIdx.x - kGWarp0 * 32;    // 0..127
+        uint32_t* raw = raw_s + gw * kPre * 32;
+        StageIt cur, pre;
+        cur.start(a);
+        pre.start(a);
+        for (int i = 0; i < kPre; ++i) {
+            s_prefetch(a, pre, lane, raw + i * 32);
+            cp_async_commit();
+            if (pre.valid) pre.next(a);
+        }
+        for (uint32_t g = 0; cur.valid; ++g, cur.next(a)) {
+            const uint32_t rs = g % kPre;
+            cp_async_wait<kPre - 1>();
+            __syncwarp();  // the warp's copies are visible to every lane
+            const uint32_t* sw = raw + rs * 32;
+            const uint64_t b1 =
+                (uint64_t)cur.d.nt * kN + (uint64_t)(cur.d.st0 + cur.s) * kStageK + 1;
+            const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));  // < 128
+            const uint32_t slot = g % kStages;
+            if (g >= (uint32_t)kStages) mbar_wait(&empty[slot], ((g / kStages) - 1) & 1);
+            uint8_t* gs = slots + (size_t)slot * kSlotBytes + kYBytes;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t u = gt + 128u * r;
+                if (u < (uint32_t)kGUnits) {
+                    const uint32_t rel = rel0 + u;
+                    const uint32_t q = rel >> 5, sh = rel & 31;
+                    const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3],
+                                   w4 = sw[q + 4];
+                    *reinterpret_cast<uint4*>(gs + 16 * u) =
+                        make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh),
+                                   __funnelshift_r(w2, w3, sh), __funnelshift_r(w3, w4, sh));
+                }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();  // every lane is done with raw slot rs before it is refilled
+            if (lane == 0) mbar_arrive(&full[slot]);
+            s_prefetch(a, pre, lane, raw + rs * 32);
+            cp_async_commit();
+            if (pre.valid) pre.next(a);
+        }
+        cp_async_wait<0>();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// Per M tile: the largest padded y length (u32 words) of its owned blocks.
+__global__ void k_mma_tiles(const uint32_t* __restrict__ ypad, uint32_t nown,
+                            uint32_t* __restrict__ mt_words) {
+    const uint32_t jj = blockIdx.x * kM + threadIdx.x;
+    uint32_t v = jj < nown ? ypad[jj] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __shared__ uint32_t wmax[kM / 32];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t m = 0;
+        for (int w = 0; w < kM / 32; ++w) m = max(m, wmax[w]);
+        mt_words[blockIdx.x] = m;
+    }
+}
+
+}  // namespace
+
+uint32_t mma_mtiles(uint32_t nown) { return (nown + kM - 1) / kM; }
+
+MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) {
+    MmaGeom g{};
+    g.mtiles = mma_mtiles(nown);
+    g.ntiles = (kw + kN / 32 - 1) / (kN / 32);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    g.grid = sms;
+    const uint64_t mean_stages = std::max<uint64_t>(1, (mean_nj + kStageK - 1) / kStageK);
+    g.ksplit = 1;
+    while ((uint64_t)g.mtiles * g.ntiles * g.ksplit < 2ull * sms &&
+           mean_stages / (2ull * g.ksplit) >= 8)
+        g.ksplit *= 2;
+    g.items = (uint64_t)g.mtiles * g.ntiles * g.ksplit;
+    return g;
+}
+
+size_t mma_hash_smem() { return kSmemBytes; }
+
+void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st) {
+    if (!a.nown || !g.items) return;
+    k_mma_tiles<<<g.mtiles, kM, 0, st>>>(a.lay.ypad, a.nown, a.mt_words);
+    cudaFuncSetAttribute(k_toeplitz_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemBytes);
+    const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
+    k_toeplitz_mma<<<grid, kThreads, kSmemBytes, st>>>(a);
+}
+
+}  // namespace ssbh_impl

@@ -1,0 +1,140 @@
+"""GPU parity of the tensor-core hash engine (csrc/toeplitz_mma.cu, SSBH_ENGINE_TENSOR).
+
+Shared-seed plans can hash every block as one u8 GEMM mod 2 on tcgen05. The keys must be
+bit-identical to the reference's toeplitz_hash (proj/src/toeplitz.cpp:34-52) — checked here
+against the oracle restatement, the golden digests made by the compiled reference, and the
+LOP3 engine on the same plan. Every call runs sm_100a kernels through the C-ABI.
+"""
+import numpy as np
+import pytest
+
+from test_gpu_parity import SURVEY_C3, _stream_run
+
+pytestmark = pytest.mark.gpu
+U64 = np.uint64
+
+
+def _run_plan(dev, x, n, s, k, samp, hsh, engine, **kw):
+    plan = dev.Plan(n, s, k, samp, hsh, engine=engine, **kw)
+    assert plan.engine == engine
+    key, nj, st = plan.run_host(x)
+    plan.close()
+    return key, nj, st
+
+
+def test_tensor_engine_random_shapes_vs_oracle(dev, oracle):
+    rng = np.random.default_rng(2308)
+    shapes = [(1000, 1, 1), (5000, 3, 31), (70000, 8, 256), (300000, 64, 1024),
+              (200000, 100, 33), (250000, 130, 512), (400000, 200, 96), (123457, 7, 3000),
+              (1 << 20, 64, 8192), (90000, 129, 64), (60000, 2, 257), (500000, 256, 160)]
+    for (n, s, k) in shapes:
+        x = oracle.make_input(int(rng.integers(1000)), float(rng.choice([0.5, 0.2, 0.9])), n)
+        want, wnj = oracle.extract(x, n, s, 41, 42, 0, k)
+        got, nj, st = _run_plan(dev, x, n, s, k, 41, 42, dev.ENGINE_TENSOR)
+        assert (nj == wnj).all()
+        assert (got == want).all(), (n, s, k)
+        assert int(st.hash_word_ops) == n * k // 32
+
+
+def test_tensor_engine_all_ones_input(dev, oracle):
+    # every operand byte saturated (0xff >> kc): the s32 sums wrap many times; the parity
+    # must still be exact
+    for (n, s, k) in ((1 << 18, 4, 4096), (1 << 20, 16, 2048)):
+        x = np.full((n + 63) // 64, np.iinfo(np.uint64).max, dtype=U64)
+        want, _ = oracle.extract(x, n, s, 5, 6, 0, k)
+        got, _, _ = _run_plan(dev, x, n, s, k, 5, 6, dev.ENGINE_TENSOR)
+        assert (got == want).all(), (n, s, k)
+
+
+@pytest.mark.parametrize("name", ["1", "2", "small_k_odd", "small_k_32"])
+def test_tensor_engine_golden(dev, oracle, golden, name):
+    c = golden["extract"][name]
+    assert not c["per_block"]
+    x = oracle.make_input(c["seed_in"], c["p"], c["n"])
+    key, nj, _ = _run_plan(dev, x, c["n"], c["s"], c["k"], c["seed_samp"], c["seed_hash"],
+                           dev.ENGINE_TENSOR)
+    assert f"{oracle.fnv(nj):016x}" == c["nj_fnv"]
+    assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
+
+
+def test_tensor_engine_switch_graph_and_ranges(dev, oracle):
+    import torch
+
+    n, s, k = 600000, 200, 2048
+    x = oracle.make_input(4, 0.5, n)
+    want, wnj = oracle.extract(x, n, s, 7, 8, 0, k)
+    plan = dev.Plan(n, s, k, 7, 8)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.Stream()
+    for engine in (dev.ENGINE_LOP3, dev.ENGINE_TENSOR, dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
+        plan.set_engine(engine)
+        d_key.zero_()
+        torch.cuda.synchronize()
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), 0, stream.cuda_stream)  # graph path
+        plan.check()
+        assert (d_key.cpu().numpy().view(U64) == want).all(), engine
+    plan.close()
+    # owned block ranges (multi-GPU shards) on the tensor engine
+    kw = k // 64
+    for first, cnt in ((0, 77), (77, 123), (190, 10)):
+        got, nj, _ = _run_plan(dev, x, n, s, k, 7, 8, dev.ENGINE_TENSOR, block_first=first,
+                               block_count=cnt)
+        assert (got == want[first * kw:(first + cnt) * kw]).all(), (first, cnt)
+        assert (nj == wnj[first:first + cnt]).all()
+
+
+def test_tensor_engine_streaming(dev, oracle):
+    n, s, k, cb = 700000, 40, 1536, 1 << 16
+    x = oracle.make_input(12, 0.5, n)
+    want, _ = oracle.extract(x, n, s, 31, 32, 0, k)
+    import paper_2308_02856_b200 as P
+
+    orig = P.Plan.__init__
+
+    def init(self, *a, **kw):
+        orig(self, *a, **kw)
+        self.set_engine(P.ENGINE_TENSOR)
+
+    P.Plan.__init__ = init
+    try:
+        got, _, _ = _stream_run(dev, x, n, s, k, 31, 32, cb)
+    finally:
+        P.Plan.__init__ = orig
+    assert (got[: len(want)] == want).all()
+
+
+def test_tensor_engine_rejects_per_block_seeds(dev):
+    plan = dev.Plan(100000, 8, 64, 2, 3, per_block=True)
+    with pytest.raises(ValueError):
+        plan.set_engine(dev.ENGINE_TENSOR)
+    assert plan.engine == dev.ENGINE_LOP3
+    plan.close()
+
+
+def test_tensor_engine_empty_block_semantics(dev, oracle):
+    x = oracle.make_input(1, 0.5, 64)
+    plan = dev.Plan(64, 1000, 8, 2, 3, engine=dev.ENGINE_TENSOR)
+    with pytest.raises(ValueError):  # ToeplitzSeed throws for n_j = 0 (toeplitz.cpp:11-12)
+        plan.run_host(x)
+    plan.close()
+
+
+@pytest.mark.slow
+def test_tensor_engine_config3_full_key_digest(dev, oracle, golden):
+    import torch
+
+    c = dev.CONFIGS[3]
+    want = golden["extract"].get("3", SURVEY_C3)
+    n, s, k = c["n"], c["s"], c["k"]
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], engine=dev.ENGINE_TENSOR)
+    d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+    plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+    plan.check()
+    key = d_key.cpu().numpy().view(U64)
+    assert int(np.unpackbits(key.view(np.uint8)).sum()) == want["key_popcount"]
+    assert f"{oracle.fnv(key):016x}" == want["key_fnv"]
+    plan.close()

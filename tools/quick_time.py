@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--engine", default="auto", choices=["auto", "lop3", "tensor"])
     args = ap.parse_args()
     tag = os.environ.get("SSBH_HASH_WIN", "default") + ("/nograph" if os.environ.get("SSBH_NO_GRAPH") == "1" else "/graph")
     peak, _ = P.measure_lop3_peak(20000)
@@ -24,6 +25,8 @@ def main():
         c = P.CONFIGS[cid]
         n, s, k = c["n"], c["s"], c["k"]
         plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"])
+        if args.engine != "auto" and not c["per_block"]:
+            plan.set_engine(P.ENGINE_LOP3 if args.engine == "lop3" else P.ENGINE_TENSOR)
         plan.set_timing(True)
         d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
         P.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
@@ -42,7 +45,10 @@ def main():
                 "frac": round(st.hash_word_ops / (st.ms_hash * 1e-3) / peak, 4),
                 "gbit_s": round(n / (st.ms_total * 1e-3) / 1e9, 4)}), flush=True)
         sample = d_key[:8].cpu().tolist()
-        print(json.dumps({"win": tag, "config": cid, "key_head": sample}), flush=True)
+        import hashlib
+        dig = hashlib.sha256(d_key.cpu().numpy().tobytes()).hexdigest()[:16]
+        print(json.dumps({"win": tag, "engine": plan.engine, "config": cid, "key_head": sample,
+                          "key_sha": dig}), flush=True)
         plan.close()
         del d_in, d_key
         torch.cuda.empty_cache()
