@@ -349,6 +349,10 @@ ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbi
 /* Diagnostics (not a reference interface): measured LOP3 lane-ops/s of the current device
  * (the int-ALU roofline denominator of the hash kernel) over one timed launch. */
 ssbh_status ssbh_measure_lop3_peak(uint32_t iters, double* lop3_per_s, double* ms);
+/* Diagnostics: measured tcgen05.mma kind::i8 MAC/s of the current device (the roofline
+ * denominator of the tensor hash engine): one CTA per SM issuing back-to-back 128x256x32
+ * MMAs. layout 0 = the hash kernel's operand layouts, 1 = plain K-major tiles. */
+ssbh_status ssbh_measure_mma_i8_peak(uint32_t iters, int layout, double* macs_per_s, double* ms);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,7 @@
 //   warps 9-12 B producers: cp.async of 128 B of seed per stage, 392 units per stage
 // Ring of 5 stages (38 KB each) between producers and the MMA warp (mbarriers).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -186,7 +187,7 @@ __device__ __forceinline__ void y_prefetch(const MmaHashArgs& a, const StageIt& 
         }
     }
     cp_async16(raw, src, bytes);
-    cp_async16(raw + 4, src + 4, bytes);
+    cp_async16(raw + kM * 4, src + 4, bytes);
 }
 
 // B producer warp: stage 32 seed words (pre-shifted seed S', S'[b] = S[b-1]) covering the
@@ -203,7 +204,11 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
     }
 }
 
+// kMask: clear the 7 don't-care bits of every operand byte (0/1 bytes) — the sums are the
+// same mod 2; fewer toggling multiplier bits cost less tensor-core power.
+template <bool kMask>
 __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
+    constexpr uint32_t M8 = kMask ? 0x01010101u : 0xFFFFFFFFu;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* slots = smem;
     uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kStages * kSlotBytes);
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             Item d;
             if (!decode(a, item, d)) break;
             const uint32_t ab = t & 1;
-            mbar_wait(&tfull[ab], (t >> 1) & 1);
+            mbar_wait_sleep(&tfull[ab], (t >> 1) & 1);
             tc_fence_after();
             if (d.nst) {
                 const uint32_t jj = d.mt * kM + warp * 32 + lane;
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             Item d;
             if (!decode(a, item, d)) break;
             const uint32_t ab = t & 1;
-            if (t >= 2) mbar_wait(&tempty[ab], ((t >> 1) - 1) & 1);
+            if (t >= 2) mbar_wait_sleep(&tempty[ab], ((t >> 1) - 1) & 1);
             tc_fence_after();
             if (d.nst == 0) {
                 if (lane == 0) mbar_arrive(&tfull[ab]);
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             }
             for (uint32_t s = 0; s < d.nst; ++s, ++g) {
                 const uint32_t slot = g % kStages;
-                mbar_wait(&full[slot], (g / kStages) & 1);
+                mbar_wait_sleep(&full[slot], (g / kStages) & 1);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t ya = base_y + slot * kSlotBytes;
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
     } else if (warp < kGWarp0) {
         // ---------------------------------------------------------------- A producers
         const uint32_t jl = threadIdx.x - kYWarp0 * 32;  // block row 0..127
-        uint32_t* raw = raw_y + jl * 8;                   // + slot * kM * 8
+        uint32_t* raw = raw_y + jl * 4;  // [slot][half][jl][4 words]: warp reads contiguous
         StageIt cur, pre;
         cur.start(a);
         pre.start(a);
@@ -321,16 +326,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             const uint32_t rs = g % kPre;
             cp_async_wait<kPre - 1>();
             const uint4 x0 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8);
-            const uint4 x1 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8 + 4);
+            const uint4 x1 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8 + kM * 4);
             const uint32_t slot = g % kStages;
-            if (g >= (uint32_t)kStages) mbar_wait(&empty[slot], ((g / kStages) - 1) & 1);
+            if (g >= (uint32_t)kStages) mbar_wait_sleep(&empty[slot], ((g / kStages) - 1) & 1);
             uint8_t* ys = slots + (size_t)slot * kSlotBytes + row_off;
 #pragma unroll
             for (int kc = 0; kc < 8; ++kc) {
                 *reinterpret_cast<uint4*>(ys + kc * 128) =
-                    make_uint4(x0.x >> kc, x0.y >> kc, x0.z >> kc, x0.w >> kc);
+                    make_uint4((x0.x >> kc) & M8, (x0.y >> kc) & M8, (x0.z >> kc) & M8,
+                               (x0.w >> kc) & M8);
                 *reinterpret_cast<uint4*>(ys + (8 + kc) * 128) =
-                    make_uint4(x1.x >> kc, x1.y >> kc, x1.z >> kc, x1.w >> kc);
+                    make_uint4((x1.x >> kc) & M8, (x1.y >> kc) & M8, (x1.z >> kc) & M8,
+                               (x1.w >> kc) & M8);
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
                 (uint64_t)cur.d.nt * kN + (uint64_t)(cur.d.st0 + cur.s) * kStageK + 1;
             const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));  // < 128
             const uint32_t slot = g % kStages;
-            if (g >= (uint32_t)kStages) mbar_wait(&empty[slot], ((g / kStages) - 1) & 1);
+            if (g >= (uint32_t)kStages) mbar_wait_sleep(&empty[slot], ((g / kStages) - 1) & 1);
             uint8_t* gs = slots + (size_t)slot * kSlotBytes + kYBytes;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -374,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
                     const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3],
                                    w4 = sw[q + 4];
                     *reinterpret_cast<uint4*>(gs + 16 * u) =
-                        make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh),
-                                   __funnelshift_r(w2, w3, sh), __funnelshift_r(w3, w4, sh));
+                        make_uint4(__funnelshift_r(w0, w1, sh) & M8, __funnelshift_r(w1, w2, sh) & M8,
+                                   __funnelshift_r(w2, w3, sh) & M8, __funnelshift_r(w3, w4, sh) & M8);
                 }
             }
             fence_proxy_async_smem();
@@ -438,10 +445,20 @@ size_t mma_hash_smem() { return kSmemBytes; }
 void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st) {
     if (!a.nown || !g.items) return;
     k_mma_tiles<<<g.mtiles, kM, 0, st>>>(a.lay.ypad, a.nown, a.mt_words);
-    cudaFuncSetAttribute(k_toeplitz_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
-    k_toeplitz_mma<<<grid, kThreads, kSmemBytes, st>>>(a);
+    static const int mask = [] {  // dev A/B knob: SSBH_MMA_MASK=0 keeps the don't-care bits
+        const char* e = std::getenv("SSBH_MMA_MASK");
+        return e && *e == '0' ? 0 : 1;
+    }();
+    if (mask) {
+        cudaFuncSetAttribute(k_toeplitz_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSmemBytes);
+        k_toeplitz_mma<true><<<grid, kThreads, kSmemBytes, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_toeplitz_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSmemBytes);
+        k_toeplitz_mma<false><<<grid, kThreads, kSmemBytes, st>>>(a);
+    }
 }
 
 }  // namespace ssbh_impl
