@@ -245,6 +245,11 @@ def main():
     ap.add_argument("--multi", default="sharded", choices=["sharded", "replicated"],
                     help="N>1: sharded sampling + peer-memory owner exchange, or every rank "
                          "re-sampling all rounds")
+    ap.add_argument("--engine", default="auto", choices=["auto", "lop3", "tensor"],
+                    help="hash engine of shared-seed plans (auto = tensor; per-block seeds "
+                         "always run the LOP3 engine)")
+    ap.add_argument("--no-lop3-compare", action="store_true",
+                    help="skip the extra LOP3-engine step reported beside a tensor-engine line")
     ap.add_argument("--rounds", type=int, default=0,
                     help="testing aid: override n (the line's config then names the override)")
     args = ap.parse_args()
@@ -265,6 +270,8 @@ def main():
             run_reference(args, cid, c)
         return
 
+    if args.engine == "lop3":  # read by every plan this process creates (shard owners too)
+        os.environ["SSBH_HASH_ENGINE"] = "lop3"
     import torch
     import torch.distributed as dist
 
@@ -304,10 +311,16 @@ def main():
     else:
         plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"],
                       block_first=first, block_count=count, chunk_bits=chunk_bits)
+        if args.engine == "tensor" and not c["per_block"]:
+            plan.set_engine(P.ENGINE_TENSOR)
         plan.set_timing(True)
         check, close = plan.check, plan.close
+    tensor = not c["per_block"] and args.engine != "lop3"
 
-    peak, _ = P.measure_lop3_peak(20000)  # int-ALU roofline denominator (live)
+    # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
+    # tcgen05 kind::i8 MAC rate with the tensor engine's operand layouts
+    peak, _ = P.measure_lop3_peak(20000)
+    tc_peak = P.measure_mma_i8_peak(100000, 0)[0] if tensor else None
 
     def step():
         if sharded:
@@ -348,6 +361,36 @@ def main():
     step_ms = [a_.elapsed_time(b_) for a_, b_ in ev]
     total_ms = sum(step_ms)
     clk = clocks.stop()
+
+    # ---- the north_star LOP3 kernel on the same workload, beside a tensor-engine line ------
+    lop3_cmp = None
+    if tensor and world == 1 and not streaming and not sharded and not args.no_lop3_compare:
+        import hashlib as _h
+
+        ref_key = _h.sha256(d_key.cpu().numpy().tobytes()).hexdigest()
+        plan.set_engine(P.ENGINE_LOP3)
+        step()
+        check()  # warm (captures the LOP3 graph)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        st3 = check()
+        torch.cuda.synchronize()
+        ms3 = e0.elapsed_time(e1)
+        lop3_cmp = {
+            "engine": "lop3 (k_toeplitz_hash, integer ALU; north_star's kernel)", "steps": 1,
+            "ms_per_step": ms3, "value": n / (ms3 * 1e-3) / 1e9, "unit": UNIT,
+            "hash_ms": st3.ms_hash,
+            "roofline": {"bound": "int-alu (LOP3)", "achieved": st3.hash_word_ops / (st3.ms_hash * 1e-3) / 1e12,
+                         "peak": peak / 1e12, "unit": "T LOP3 word-ops/s",
+                         "frac": st3.hash_word_ops / (st3.ms_hash * 1e-3) / peak},
+            "key_matches_tensor_engine":
+                _h.sha256(d_key.cpu().numpy().tobytes()).hexdigest() == ref_key,
+        }
+        plan.set_engine(P.ENGINE_TENSOR)
+        step()
+        check()
 
     # ---- e2e through the public host API (pinned H2D of the input, D2H of the key) ------
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
@@ -444,21 +487,33 @@ def main():
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "hash_traffic.json")
         if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get(f"config{cid}_n{world}")
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(3, args.warmup),
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong",
-            "vs_baseline": None, "dtype": "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)",
-            "data": "synthetic (KeyedStream input on device, seeds per BASELINE/SURVEY §8a)",
-            "config": dict(config_dict(cid, c, world), multi_gpu=(
-                "sharded sampling: each rank samples n/N rounds, payloads stored into the "
-                "owning rank by NVLink peer stores (IPC), owners hash their blocks"
-                if sharded else ("streaming plan, 8 input chunks" if streaming else
-                                 "single plan" if world == 1 else
-                                 "replicated sampling, owned blocks hashed per rank"))),
-            "roofline": {
+            traffic = json.load(open(tpath)).get(
+                f"config{cid}_n{world}" + ("_tensor" if tensor else ""))
+        hbm_ms = (n / 8 + count * k / 8) / (HBM_PEAK_GBS * 1e9) * 1e3
+        if tensor:
+            macs = hash_ops * 32  # sum_j n_j * k bit products = u8 tensor MACs doing useful work
+            roof = {
+                "bound": "tensor (tcgen05 kind::i8)", "kernel": "k_toeplitz_mma",
+                "achieved": macs / (avg_hash_ms * 1e-3) / 1e12, "peak": tc_peak / 1e12,
+                "unit": "T MAC/s (u8 x u8 -> s32; one MAC = one GF(2) bit product)",
+                "frac": macs / (avg_hash_ms * 1e-3) / tc_peak,
+                "traffic": traffic,
+                "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/)",
+                "algorithmic_per_launch": f"sum_j n_j*k = {macs} bit products (owned blocks; "
+                                          f"the LOP3 engine's {hash_ops} word-ops x 32)",
+                "peak_source": "measured live in this run: k_i8_peak (csrc/diag.cu), one CTA "
+                               "per SM issuing back-to-back 128x256x32 kind::i8 MMAs with the "
+                               "hash kernel's operand layouts",
+                "int_alu_equivalent": {"achieved": achieved / 1e12, "peak": peak / 1e12,
+                                       "unit": "T LOP3 word-ops/s",
+                                       "frac": achieved / peak,
+                                       "note": "the same work counted as the north_star LOP3 "
+                                               "roofline; > 1 because the tensor cores do "
+                                               "the GF(2) product ~3.6x faster than the ALUs"},
+                "hbm_term_ms": hbm_ms,
+            }
+        else:
+            roof = {
                 "bound": "int-alu (LOP3)", "kernel": "k_toeplitz_hash",
                 "achieved": achieved / 1e12, "peak": peak / 1e12,
                 "unit": "T LOP3 word-ops/s", "frac": achieved / peak,
@@ -467,8 +522,26 @@ def main():
                 "algorithmic_per_launch": f"sum_j n_j*k/32 = {hash_ops} word-ops (owned blocks)",
                 "peak_source": "measured live in this run: k_lop3_peak (csrc/diag.cu), "
                                "148 SMs x 64 LOP3 lanes/clk at the running SM clock",
-                "hbm_term_ms": (n / 8 + count * k / 8) / (HBM_PEAK_GBS * 1e9) * 1e3,
-            },
+                "hbm_term_ms": hbm_ms,
+            }
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": ("u8 (one GF(2) bit per byte) on tcgen05 kind::i8, s32 accumulate, parity "
+                      "= sum mod 2; bit-exact" if tensor else
+                      "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)"),
+            "hash_engine": "tensor" if tensor else "lop3",
+            "data": "synthetic (KeyedStream input on device, seeds per BASELINE/SURVEY §8a)",
+            "config": dict(config_dict(cid, c, world), multi_gpu=(
+                "sharded sampling: each rank samples n/N rounds, payloads stored into the "
+                "owning rank by NVLink peer stores (IPC), owners hash their blocks"
+                if sharded else ("streaming plan, 8 input chunks" if streaming else
+                                 "single plan" if world == 1 else
+                                 "replicated sampling, owned blocks hashed per rank"))),
+            "roofline": roof,
             "phases_ms_last_step": {"sample_count_scan_layout": stats.ms_sample,
                                     "scatter": stats.ms_scatter, "seeds": stats.ms_seed,
                                     "hash": stats.ms_hash, "total": stats.ms_total},
@@ -478,6 +551,8 @@ def main():
             "key_sha256_16": key_sha,
             "clocks": clk,
         }
+        if lop3_cmp is not None:
+            line["lop3_engine"] = lop3_cmp
         if e2e is not None:
             line["e2e"] = {"value": n * e2e_steps / e2e_s / 1e9, "unit": UNIT,
                            "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],

@@ -188,8 +188,9 @@ ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
  *   SSBH_ENGINE_LOP3   : GF(2) product on the integer ALUs (LOP3/SHF/POPC) — every plan.
  *   SSBH_ENGINE_TENSOR : shared-seed plans only: all blocks share one Hankel matrix, so the
  *                        hash is one u8 GEMM mod 2 on the tcgen05 tensor cores (kind::i8).
- *   SSBH_ENGINE_AUTO   : the plan's default (LOP3; environment SSBH_HASH_ENGINE=tensor
- *                        selects the tensor engine for shared-seed plans).
+ *   SSBH_ENGINE_AUTO   : the plan's default: TENSOR for shared-seed plans, LOP3 for
+ *                        per-block seeds (environment SSBH_HASH_ENGINE=lop3 keeps shared-seed
+ *                        plans on LOP3).
  * Both engines produce identical keys. TENSOR on a per-block-seed plan ->
  * SSBH_INVALID_ARGUMENT. ssbh_plan_engine returns the engine in use. */
 #define SSBH_ENGINE_AUTO 0

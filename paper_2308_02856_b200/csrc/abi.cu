@@ -337,12 +337,13 @@ uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid)
 
 }  // namespace
 
-// Engine of a new plan: SSBH_HASH_ENGINE=lop3|tensor overrides; per-block seeds always LOP3.
+// Engine of a new plan: shared seeds run on the tensor cores (toeplitz_mma.cu), per-block seeds
+// on the integer ALUs; SSBH_HASH_ENGINE=lop3 keeps shared-seed plans on the ALUs too.
 static int default_engine(uint32_t per_block_seed) {
     if (per_block_seed) return kEngineLop3;
     const char* e = std::getenv("SSBH_HASH_ENGINE");
-    if (e && std::strcmp(e, "tensor") == 0) return kEngineMma;
-    return kEngineLop3;
+    if (e && std::strcmp(e, "lop3") == 0) return kEngineLop3;
+    return kEngineMma;
 }
 
 // ======================================================================== plan

@@ -1,9 +1,11 @@
-"""GPU parity of the tensor-core hash engine (csrc/toeplitz_mma.cu, SSBH_ENGINE_TENSOR).
+"""GPU parity of both hash engines of shared-seed plans.
 
-Shared-seed plans can hash every block as one u8 GEMM mod 2 on tcgen05. The keys must be
-bit-identical to the reference's toeplitz_hash (proj/src/toeplitz.cpp:34-52) — checked here
-against the oracle restatement, the golden digests made by the compiled reference, and the
-LOP3 engine on the same plan. Every call runs sm_100a kernels through the C-ABI.
+Shared-seed plans hash every block as one u8 GEMM mod 2 on tcgen05 by default
+(csrc/toeplitz_mma.cu, SSBH_ENGINE_TENSOR); SSBH_ENGINE_LOP3 keeps them on the integer ALUs
+(csrc/toeplitz.cu). The keys must be bit-identical to the reference's toeplitz_hash
+(proj/src/toeplitz.cpp:34-52) — checked here against the oracle restatement, the golden
+digests made by the compiled reference, and each other. Every call runs sm_100a kernels
+through the C-ABI. (The rest of the GPU suite runs shared-seed plans on the default engine.)
 """
 import numpy as np
 import pytest
@@ -22,7 +24,24 @@ def _run_plan(dev, x, n, s, k, samp, hsh, engine, **kw):
     return key, nj, st
 
 
-def test_tensor_engine_random_shapes_vs_oracle(dev, oracle):
+ENGINES = pytest.mark.parametrize("engine", [1, 2], ids=["lop3", "tensor"])
+
+
+def test_default_engine_is_tensor_for_shared_seeds(dev):
+    plan = dev.Plan(100000, 8, 64, 2, 3)
+    assert plan.engine == dev.ENGINE_TENSOR
+    plan.set_engine(dev.ENGINE_LOP3)
+    assert plan.engine == dev.ENGINE_LOP3
+    plan.set_engine(dev.ENGINE_AUTO)
+    assert plan.engine == dev.ENGINE_TENSOR
+    plan.close()
+    plan = dev.Plan(100000, 8, 64, 2, 3, per_block=True)
+    assert plan.engine == dev.ENGINE_LOP3
+    plan.close()
+
+
+@ENGINES
+def test_engine_random_shapes_vs_oracle(dev, oracle, engine):
     rng = np.random.default_rng(2308)
     shapes = [(1000, 1, 1), (5000, 3, 31), (70000, 8, 256), (300000, 64, 1024),
               (200000, 100, 33), (250000, 130, 512), (400000, 200, 96), (123457, 7, 3000),
@@ -30,7 +49,7 @@ def test_tensor_engine_random_shapes_vs_oracle(dev, oracle):
     for (n, s, k) in shapes:
         x = oracle.make_input(int(rng.integers(1000)), float(rng.choice([0.5, 0.2, 0.9])), n)
         want, wnj = oracle.extract(x, n, s, 41, 42, 0, k)
-        got, nj, st = _run_plan(dev, x, n, s, k, 41, 42, dev.ENGINE_TENSOR)
+        got, nj, st = _run_plan(dev, x, n, s, k, 41, 42, engine)
         assert (nj == wnj).all()
         assert (got == want).all(), (n, s, k)
         assert int(st.hash_word_ops) == n * k // 32
@@ -46,13 +65,14 @@ def test_tensor_engine_all_ones_input(dev, oracle):
         assert (got == want).all(), (n, s, k)
 
 
+@ENGINES
 @pytest.mark.parametrize("name", ["1", "2", "small_k_odd", "small_k_32"])
-def test_tensor_engine_golden(dev, oracle, golden, name):
+def test_engine_golden(dev, oracle, golden, name, engine):
     c = golden["extract"][name]
     assert not c["per_block"]
     x = oracle.make_input(c["seed_in"], c["p"], c["n"])
     key, nj, _ = _run_plan(dev, x, c["n"], c["s"], c["k"], c["seed_samp"], c["seed_hash"],
-                           dev.ENGINE_TENSOR)
+                           engine)
     assert f"{oracle.fnv(nj):016x}" == c["nj_fnv"]
     assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
 
@@ -84,7 +104,8 @@ def test_tensor_engine_switch_graph_and_ranges(dev, oracle):
         assert (nj == wnj[first:first + cnt]).all()
 
 
-def test_tensor_engine_streaming(dev, oracle):
+@ENGINES
+def test_engine_streaming(dev, oracle, engine):
     n, s, k, cb = 700000, 40, 1536, 1 << 16
     x = oracle.make_input(12, 0.5, n)
     want, _ = oracle.extract(x, n, s, 31, 32, 0, k)
@@ -94,7 +115,7 @@ def test_tensor_engine_streaming(dev, oracle):
 
     def init(self, *a, **kw):
         orig(self, *a, **kw)
-        self.set_engine(P.ENGINE_TENSOR)
+        self.set_engine(engine)
 
     P.Plan.__init__ = init
     try:
@@ -121,13 +142,15 @@ def test_tensor_engine_empty_block_semantics(dev, oracle):
 
 
 @pytest.mark.slow
-def test_tensor_engine_config3_full_key_digest(dev, oracle, golden):
+def test_lop3_engine_config3_full_key_digest(dev, oracle, golden):
+    """The integer-ALU engine (north_star's kernel) on BASELINE config 3; the default-engine
+    run is test_gpu_parity.py::test_config3_full_key_digest."""
     import torch
 
     c = dev.CONFIGS[3]
     want = golden["extract"].get("3", SURVEY_C3)
     n, s, k = c["n"], c["s"], c["k"]
-    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], engine=dev.ENGINE_TENSOR)
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], engine=dev.ENGINE_LOP3)
     d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
     dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
     d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
