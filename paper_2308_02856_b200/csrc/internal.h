@@ -213,6 +213,7 @@ struct MmaHashArgs {
     uint32_t ntiles, ksplit;
     uint64_t items;
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
+    uint32_t spin;           // dev knob: MMA warp spins instead of suspending on its waits
 };
 uint32_t mma_mtiles(uint32_t nown);
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);

@@ -59,7 +59,8 @@ constexpr int kMmaK = 32;                    // K bytes per tcgen05.mma kind::i8
 constexpr int kStageK = 256;                 // input positions per pipeline stage
 constexpr int kStageMmas = kStageK / kMmaK;  // 8
 constexpr int kGUnits = kN + 7 + 128 + 1;    // 392 Hankel units per stage
-constexpr int kStages = 5;
+constexpr int kStages = 5;                   // A in shared memory: 5 x 38 KB
+constexpr int kStagesAT = 4;                 // A in TMEM: 4 x 64 columns next to the accumulator
 constexpr int kPre = 4;                      // cp.async prefetch depth (stages)
 constexpr int kYBytes = kM * kStageK;        // 32768: A operand of one stage
 constexpr int kGBytes = kGUnits * 16;        // 6272: B operand of one stage
@@ -69,9 +70,6 @@ constexpr int kRawSBytes = 4 * kPre * 128;   // seed words staged by cp.async (p
 constexpr int kEpiWarps = 4, kMmaWarp = 4, kYWarp0 = 5, kGWarp0 = 9, kWarps = 13;
 constexpr int kThreads = kWarps * 32;
 constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps
-constexpr size_t kBarOff = (size_t)kStages * kSlotBytes + kRawYBytes + kRawSBytes;
-constexpr size_t kSmemBytes = kBarOff + (2 * kStages + 4) * 8 + 16;
-static_assert(kSmemBytes <= 232448, "shared memory budget");
 static_assert(kSlotBytes % 128 == 0, "slot alignment");
 
 // ------------------------------------------------------------------ tcgen05 / cp.async
@@ -97,6 +95,18 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
         "}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(kIdesc), "r"(accum)
+        : "memory");
+}
+// A operand from TMEM (columns a_tmem .. +8: lane = row, 4 K bytes per 32-bit column).
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                          uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(kIdesc), "r"(accum)
         : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -126,6 +136,17 @@ __device__ __forceinline__ void cp_async_wait() {
           "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),          \
           "=r"(v[31])                                                                            \
         : "r"(taddr))
+
+#define SSBH_TMEM_ST32(taddr, v)                                                                 \
+    asm volatile(                                                                                \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"   \
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"      \
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),          \
+        "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),          \
+        "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]),      \
+        "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),      \
+        "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                               \
+        : "memory")
 
 // ------------------------------------------------------------------ work items
 struct Item {
@@ -204,24 +225,39 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
     }
 }
 
-// kMask: clear the 7 don't-care bits of every operand byte (0/1 bytes) — the sums are the
-// same mod 2; fewer toggling multiplier bits cost less tensor-core power.
-template <bool kMask>
+// Operand bytes are masked to 0/1 (M8): the 7 don't-care bits would not change the sums mod 2,
+// but toggling them drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965).
+// kAT: the A operand (y bits) lives in TMEM (tcgen05.st from the producers' registers, one
+// 128 x 256 accumulator + a 4-stage A ring) instead of shared memory (two accumulators).
+template <bool kAT>
+struct Geo {
+    static constexpr int stages = kAT ? kStagesAT : kStages;
+    static constexpr int slot = kAT ? kGBytes : kSlotBytes;  // shared-memory bytes per stage
+    static constexpr int goff = kAT ? 0 : kYBytes;           // B tile offset in a slot
+    static constexpr int nacc = kAT ? 1 : 2;                 // accumulators
+    static constexpr size_t bar = (size_t)stages * slot + kRawYBytes + kRawSBytes;
+    static constexpr size_t smem = bar + (2 * stages + 4) * 8 + 16;
+};
+static_assert(Geo<false>::smem <= 232448 && Geo<true>::smem <= 232448, "smem budget");
+
+template <bool kAT>
 __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
-    constexpr uint32_t M8 = kMask ? 0x01010101u : 0xFFFFFFFFu;
+    using G = Geo<kAT>;
+    constexpr int kS = G::stages;
+    constexpr uint32_t M8 = 0x01010101u;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* slots = smem;
-    uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kStages * kSlotBytes);
+    uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kS * G::slot);
     uint32_t* raw_s = raw_y + kRawYBytes / 4;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::bar);
+    uint64_t* empty = full + kS;
+    uint64_t* tfull = empty + kS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], kFullArrivals);
             mbar_init(&empty[s], 1);
         }
@@ -248,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
         for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
             Item d;
             if (!decode(a, item, d)) break;
-            const uint32_t ab = t & 1;
-            mbar_wait_sleep(&tfull[ab], (t >> 1) & 1);
+            const uint32_t ab = t % G::nacc;
+            mbar_wait_sleep(&tfull[ab], (t / G::nacc) & 1);
             tc_fence_after();
             if (d.nst) {
                 const uint32_t jj = d.mt * kM + warp * 32 + lane;
@@ -278,30 +314,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
     } else if (warp == kMmaWarp) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
-        const uint32_t base_y = smem_u32(slots), base_g = base_y + kYBytes;
+        const uint32_t base_y = smem_u32(slots), base_g = base_y + G::goff;
         for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
             Item d;
             if (!decode(a, item, d)) break;
-            const uint32_t ab = t & 1;
-            if (t >= 2) mbar_wait_sleep(&tempty[ab], ((t >> 1) - 1) & 1);
+            const uint32_t ab = t % G::nacc;
+            if (t >= (uint32_t)G::nacc) mbar_wait_sleep(&tempty[ab], ((t / G::nacc) - 1) & 1);
             tc_fence_after();
             if (d.nst == 0) {
                 if (lane == 0) mbar_arrive(&tfull[ab]);
                 continue;
             }
             for (uint32_t s = 0; s < d.nst; ++s, ++g) {
-                const uint32_t slot = g % kStages;
-                mbar_wait_sleep(&full[slot], (g / kStages) & 1);
+                const uint32_t slot = g % kS;
+                if (a.spin)
+                    mbar_wait(&full[slot], (g / kS) & 1);
+                else
+                    mbar_wait_sleep(&full[slot], (g / kS) & 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t ya = base_y + slot * kSlotBytes;
-                    const uint32_t ga = base_g + slot * kSlotBytes;
+                    const uint32_t ya = base_y + slot * G::slot;
+                    const uint32_t ga = base_g + slot * G::slot;
 #pragma unroll
                     for (int m = 0; m < kStageMmas; ++m) {
-                        const uint64_t adesc = sdesc(ya + 256u * m, 128, 2048);
                         const uint32_t unit = 2u * (m & 3) + 128u * (m >> 2);
                         const uint64_t bdesc = sdesc(ga + 16u * unit, 16, 128);
-                        mma_i8(tmem + ab * kN, adesc, bdesc, (s | (uint32_t)m) != 0);
+                        if constexpr (kAT)
+                            mma_i8_ts(tmem, tmem + kN + 64u * slot + 8u * m, bdesc,
+                                      (s | (uint32_t)m) != 0);
+                        else
+                            mma_i8(tmem + ab * kN, sdesc(ya + 256u * m, 128, 2048), bdesc,
+                                   (s | (uint32_t)m) != 0);
                     }
                     mma_commit(&empty[slot]);
                     if (s + 1 == d.nst) mma_commit(&tfull[ab]);
@@ -311,7 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
         }
     } else if (warp < kGWarp0) {
         // ---------------------------------------------------------------- A producers
-        const uint32_t jl = threadIdx.x - kYWarp0 * 32;  // block row 0..127
+        // block row: TMEM lane quadrant 32*(warp%4) is the only one this warp may access
+        const uint32_t jl = kAT ? 32u * (warp & 3) + lane : threadIdx.x - kYWarp0 * 32;
         uint32_t* raw = raw_y + jl * 4;  // [slot][half][jl][4 words]: warp reads contiguous
         StageIt cur, pre;
         cur.start(a);
@@ -327,19 +371,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             cp_async_wait<kPre - 1>();
             const uint4 x0 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8);
             const uint4 x1 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8 + kM * 4);
-            const uint32_t slot = g % kStages;
-            if (g >= (uint32_t)kStages) mbar_wait_sleep(&empty[slot], ((g / kStages) - 1) & 1);
-            uint8_t* ys = slots + (size_t)slot * kSlotBytes + row_off;
-#pragma unroll
-            for (int kc = 0; kc < 8; ++kc) {
-                *reinterpret_cast<uint4*>(ys + kc * 128) =
-                    make_uint4((x0.x >> kc) & M8, (x0.y >> kc) & M8, (x0.z >> kc) & M8,
-                               (x0.w >> kc) & M8);
-                *reinterpret_cast<uint4*>(ys + (8 + kc) * 128) =
-                    make_uint4((x1.x >> kc) & M8, (x1.y >> kc) & M8, (x1.z >> kc) & M8,
-                               (x1.w >> kc) & M8);
+            const uint32_t slot = g % kS;
+            if (g >= (uint32_t)kS) {
+                if (a.spin >= 2)
+                    mbar_wait(&empty[slot], ((g / kS) - 1) & 1);
+                else
+                    mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
             }
-            fence_proxy_async_smem();
+            if constexpr (kAT) {
+                // TMEM column 8m + c of the stage = chunk 2m + c/4, word c%4 (K bytes 4c..4c+3
+                // of MMA m, the order of the K-major smem chunks)
+                tc_fence_after();
+                const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                const uint32_t taddr = tmem + ((32u * (warp & 3)) << 16) + kN + 64u * slot;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t v[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int col = 32 * h + e, m = col >> 3, c = col & 7;
+                        const int q = 2 * m + (c >> 2), w = c & 3;
+                        v[e] = (xs[4 * (q >> 3) + w] >> (q & 7)) & M8;
+                    }
+                    SSBH_TMEM_ST32(taddr + 32u * h, v);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+            } else {
+                uint8_t* ys = slots + (size_t)slot * G::slot + row_off;
+#pragma unroll
+                for (int kc = 0; kc < 8; ++kc) {
+                    *reinterpret_cast<uint4*>(ys + kc * 128) =
+                        make_uint4((x0.x >> kc) & M8, (x0.y >> kc) & M8, (x0.z >> kc) & M8,
+                                   (x0.w >> kc) & M8);
+                    *reinterpret_cast<uint4*>(ys + (8 + kc) * 128) =
+                        make_uint4((x1.x >> kc) & M8, (x1.y >> kc) & M8, (x1.z >> kc) & M8,
+                                   (x1.w >> kc) & M8);
+                }
+                fence_proxy_async_smem();
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
             // refill the raw slot just consumed (its values are in registers and stored)
@@ -369,9 +439,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             const uint64_t b1 =
                 (uint64_t)cur.d.nt * kN + (uint64_t)(cur.d.st0 + cur.s) * kStageK + 1;
             const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));  // < 128
-            const uint32_t slot = g % kStages;
-            if (g >= (uint32_t)kStages) mbar_wait_sleep(&empty[slot], ((g / kStages) - 1) & 1);
-            uint8_t* gs = slots + (size_t)slot * kSlotBytes + kYBytes;
+            const uint32_t slot = g % kS;
+            if (g >= (uint32_t)kS) {
+                if (a.spin >= 2)
+                    mbar_wait(&empty[slot], ((g / kS) - 1) & 1);
+                else
+                    mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+            }
+            uint8_t* gs = slots + (size_t)slot * G::slot + G::goff;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const uint32_t u = gt + 128u * r;
@@ -440,24 +515,33 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     return g;
 }
 
-size_t mma_hash_smem() { return kSmemBytes; }
+size_t mma_hash_smem() { return Geo<true>::smem; }
 
-void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st) {
-    if (!a.nown || !g.items) return;
-    k_mma_tiles<<<g.mtiles, kM, 0, st>>>(a.lay.ypad, a.nown, a.mt_words);
+void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
+    if (!a0.nown || !g.items) return;
+    k_mma_tiles<<<g.mtiles, kM, 0, st>>>(a0.lay.ypad, a0.nown, a0.mt_words);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
-    static const int mask = [] {  // dev A/B knob: SSBH_MMA_MASK=0 keeps the don't-care bits
-        const char* e = std::getenv("SSBH_MMA_MASK");
+    // MMA warp: spinning on its stage barriers measured 2 % faster than suspending (config 3
+    // hash 285.4 -> 279.2 ms). Dev A/B knob SSBH_MMA_SPIN: 0 = suspend, 1 = MMA warp spins
+    // (default), 2 = producers spin on their slot barriers too.
+    static const int spin = [] {
+        const char* e = std::getenv("SSBH_MMA_SPIN");
+        return e && *e ? *e - '0' : 1;
+    }();
+    MmaHashArgs a = a0;
+    a.spin = spin;
+    static const int atmem = [] {  // dev A/B knob: SSBH_MMA_ATMEM=0 stages A in shared memory
+        const char* e = std::getenv("SSBH_MMA_ATMEM");
         return e && *e == '0' ? 0 : 1;
     }();
-    if (mask) {
+    if (atmem) {
         cudaFuncSetAttribute(k_toeplitz_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kSmemBytes);
-        k_toeplitz_mma<true><<<grid, kThreads, kSmemBytes, st>>>(a);
+                             (int)Geo<true>::smem);
+        k_toeplitz_mma<true><<<grid, kThreads, Geo<true>::smem, st>>>(a);
     } else {
         cudaFuncSetAttribute(k_toeplitz_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kSmemBytes);
-        k_toeplitz_mma<false><<<grid, kThreads, kSmemBytes, st>>>(a);
+                             (int)Geo<false>::smem);
+        k_toeplitz_mma<false><<<grid, kThreads, Geo<false>::smem, st>>>(a);
     }
 }
 
