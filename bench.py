@@ -290,7 +290,11 @@ def main():
 
     n, s, k = c["n"], c["s"], c["k"]
     first, count = owned_range(rank, world, s)
-    streaming = cid == 5  # 2^37 rounds: input streamed in 8 chunks (BASELINE configs[4])
+    # config 5 (2^37 rounds, "~2 GiB of input per GPU" on 8 GPUs): with >= 8 ranks each rank
+    # samples its own 2^34-round input chunk and ships payloads to the owners (sharded, ~100 GB
+    # per rank); with fewer ranks a rank cannot hold its 1/N slice's payloads, so every rank
+    # runs a streaming plan over the 8 input chunks and keeps only its own blocks
+    streaming = cid == 5 and not (world >= 8 and args.multi == "sharded")
     sharded = world > 1 and not streaming and args.multi == "sharded"
     chunk_bits = n // 8 if streaming else 0
     stream = torch.cuda.Stream()  # capturable: untimed runs replay one CUDA graph
