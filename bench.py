@@ -324,7 +324,7 @@ def main():
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
     # tcgen05 kind::i8 MAC rate with the tensor engine's operand layouts
     peak, _ = P.measure_lop3_peak(20000)
-    tc_peak = P.measure_mma_i8_peak(100000, 0)[0] if tensor else None
+    tc_peak = P.measure_mma_i8_peak(200000, 0)[0] if tensor else None  # ~120 ms: sustained
 
     def step():
         if sharded:

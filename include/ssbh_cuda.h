@@ -354,6 +354,8 @@ ssbh_status ssbh_measure_lop3_peak(uint32_t iters, double* lop3_per_s, double* m
  * denominator of the tensor hash engine): one CTA per SM issuing back-to-back 128x256x32
  * MMAs. layout 0 = the hash kernel's operand layouts, 1 = plain K-major tiles. */
 ssbh_status ssbh_measure_mma_i8_peak(uint32_t iters, int layout, double* macs_per_s, double* ms);
+/* Same with CTA pairs (cta_group::2, M = 256 across two SMs). */
+ssbh_status ssbh_measure_mma_i8_peak2(uint32_t iters, int layout, double* macs_per_s, double* ms);
 
 #ifdef __cplusplus
 }

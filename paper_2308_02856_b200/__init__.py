@@ -48,7 +48,7 @@ ABI_SYMBOLS = (
     "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
     "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
-    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak",
+    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
@@ -144,6 +144,9 @@ def _load():
     L.ssbh_plan_set_engine.argtypes = [C.c_void_p, C.c_int]
     L.ssbh_plan_engine.restype = C.c_int
     L.ssbh_plan_engine.argtypes = [C.c_void_p]
+    L.ssbh_measure_mma_i8_peak2.restype = st
+    L.ssbh_measure_mma_i8_peak2.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_double)]
     L.ssbh_measure_mma_i8_peak.restype = st
     L.ssbh_measure_mma_i8_peak.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                            C.POINTER(C.c_double)]
@@ -681,10 +684,12 @@ def measure_lop3_peak(iters: int = 20000):
     return r.value, ms.value
 
 
-def measure_mma_i8_peak(iters: int = 4000, layout: int = 0):
-    """Measured tcgen05 kind::i8 MAC/s of the current device (tensor-engine roofline)."""
+def measure_mma_i8_peak(iters: int = 4000, layout: int = 0, pairs: bool = False):
+    """Measured tcgen05 kind::i8 MAC/s of the current device (tensor-engine roofline);
+    pairs=True: CTA pairs (cta_group::2, M = 256)."""
     r, ms = C.c_double(0), C.c_double(0)
-    _check(lib.ssbh_measure_mma_i8_peak(iters, layout, C.byref(r), C.byref(ms)))
+    f = lib.ssbh_measure_mma_i8_peak2 if pairs else lib.ssbh_measure_mma_i8_peak
+    _check(f(iters, layout, C.byref(r), C.byref(ms)))
     return r.value, ms.value
 
 

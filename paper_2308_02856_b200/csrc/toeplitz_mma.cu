@@ -67,8 +67,11 @@ constexpr int kGBytes = kGUnits * 16;        // 6272: B operand of one stage
 constexpr int kSlotBytes = kYBytes + kGBytes;
 constexpr int kRawYBytes = kPre * kM * 32;   // y words staged by cp.async
 constexpr int kRawSBytes = 4 * kPre * 128;   // seed words staged by cp.async (per B warp)
-constexpr int kEpiWarps = 4, kMmaWarp = 4, kYWarp0 = 5, kGWarp0 = 9, kWarps = 13;
-constexpr int kThreads = kWarps * 32;
+// warps 0-3 epilogue, 4 MMA, then kSets producer sets of 4 A warps + 4 B warps; set q fills
+// the stages g with g % kSets == q, so a set has kSets stage-times per stage (its per-stage
+// chain of cp.async wait -> expand -> tcgen05.st / STS -> wait::st -> arrive is latency-bound)
+constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5;
+constexpr int threads_for(int sets) { return (kProdWarp0 + 8 * sets) * 32; }
 constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps
 static_assert(kSlotBytes % 128 == 0, "slot alignment");
 
@@ -191,6 +194,10 @@ struct StageIt {
         ++s;
         skip_empty(a);
     }
+    // skip over the stages other producer sets fill
+    __device__ void advance(const MmaHashArgs& a, int count) {
+        for (int i = 0; i < count && valid; ++i) next(a);
+    }
 };
 
 // A producer (one block row jl): stage the row's 256 y bits by cp.async (zero-filled past
@@ -229,26 +236,26 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
 // but toggling them drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965).
 // kAT: the A operand (y bits) lives in TMEM (tcgen05.st from the producers' registers, one
 // 128 x 256 accumulator + a 4-stage A ring) instead of shared memory (two accumulators).
-template <bool kAT>
+template <bool kAT, int kSets>
 struct Geo {
     static constexpr int stages = kAT ? kStagesAT : kStages;
     static constexpr int slot = kAT ? kGBytes : kSlotBytes;  // shared-memory bytes per stage
     static constexpr int goff = kAT ? 0 : kYBytes;           // B tile offset in a slot
     static constexpr int nacc = kAT ? 1 : 2;                 // accumulators
-    static constexpr size_t bar = (size_t)stages * slot + kRawYBytes + kRawSBytes;
+    static constexpr size_t bar = (size_t)stages * slot + kSets * (kRawYBytes + kRawSBytes);
     static constexpr size_t smem = bar + (2 * stages + 4) * 8 + 16;
 };
-static_assert(Geo<false>::smem <= 232448 && Geo<true>::smem <= 232448, "smem budget");
+static_assert(Geo<false, 1>::smem <= 232448 && Geo<true, 2>::smem <= 232448, "smem budget");
 
-template <bool kAT>
-__global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
-    using G = Geo<kAT>;
+template <bool kAT, int kSets>
+__global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_mma(MmaHashArgs a) {
+    using G = Geo<kAT, kSets>;
     constexpr int kS = G::stages;
     constexpr uint32_t M8 = 0x01010101u;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* slots = smem;
     uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kS * G::slot);
-    uint32_t* raw_s = raw_y + kRawYBytes / 4;
+    uint32_t* raw_s = raw_y + kSets * (kRawYBytes / 4);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::bar);
     uint64_t* empty = full + kS;
     uint64_t* tfull = empty + kS;
@@ -352,22 +359,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
                 __syncwarp();
             }
         }
-    } else if (warp < kGWarp0) {
+    } else if (((warp - kProdWarp0) & 7) < 4) {
         // ---------------------------------------------------------------- A producers
         // block row: TMEM lane quadrant 32*(warp%4) is the only one this warp may access
-        const uint32_t jl = kAT ? 32u * (warp & 3) + lane : threadIdx.x - kYWarp0 * 32;
-        uint32_t* raw = raw_y + jl * 4;  // [slot][half][jl][4 words]: warp reads contiguous
+        const uint32_t set = (warp - kProdWarp0) >> 3;
+        const uint32_t jl = kAT ? 32u * (warp & 3) + lane : 32u * ((warp - kProdWarp0) & 3) + lane;
+        // [slot][half][jl][4 words] per set: a warp's reads are contiguous
+        uint32_t* raw = raw_y + set * (kRawYBytes / 4) + jl * 4;
         StageIt cur, pre;
         cur.start(a);
-        pre.start(a);
+        cur.advance(a, set);
+        pre = cur;
         for (int i = 0; i < kPre; ++i) {
             y_prefetch(a, pre, jl, raw + i * kM * 8);
             cp_async_commit();
-            if (pre.valid) pre.next(a);
+            pre.advance(a, kSets);
         }
         const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
-        for (uint32_t g = 0; cur.valid; ++g, cur.next(a)) {
-            const uint32_t rs = g % kPre;
+        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
+            const uint32_t rs = i % kPre;
             cp_async_wait<kPre - 1>();
             const uint4 x0 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8);
             const uint4 x1 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8 + kM * 4);
@@ -415,24 +425,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             // refill the raw slot just consumed (its values are in registers and stored)
             y_prefetch(a, pre, jl, raw + rs * kM * 8);
             cp_async_commit();
-            if (pre.valid) pre.next(a);
+            pre.advance(a, kSets);
         }
         cp_async_wait<0>();
     } else {
         // ---------------------------------------------------------------- B producers
-        const uint32_t gw = warp - kGWarp0;                // 0..3
-        const uint32_t gt = threadIdx.x - kGWarp0 * 32;    // 0..127
-        uint32_t* raw = raw_s + gw * kPre * 32;
+        const uint32_t set = (warp - kProdWarp0) >> 3;
+        const uint32_t gw = ((warp - kProdWarp0) & 7) - 4;  // 0..3
+        const uint32_t gt = gw * 32 + lane;                 // 0..127
+        uint32_t* raw = raw_s + set * (kRawSBytes / 4) + gw * kPre * 32;
         StageIt cur, pre;
         cur.start(a);
-        pre.start(a);
+        cur.advance(a, set);
+        pre = cur;
         for (int i = 0; i < kPre; ++i) {
             s_prefetch(a, pre, lane, raw + i * 32);
             cp_async_commit();
-            if (pre.valid) pre.next(a);
+            pre.advance(a, kSets);
         }
-        for (uint32_t g = 0; cur.valid; ++g, cur.next(a)) {
-            const uint32_t rs = g % kPre;
+        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
+            const uint32_t rs = i % kPre;
             cp_async_wait<kPre - 1>();
             __syncwarp();  // the warp's copies are visible to every lane
             const uint32_t* sw = raw + rs * 32;
@@ -465,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_toeplitz_mma(MmaHashArgs a) {
             if (lane == 0) mbar_arrive(&full[slot]);
             s_prefetch(a, pre, lane, raw + rs * 32);
             cp_async_commit();
-            if (pre.valid) pre.next(a);
+            pre.advance(a, kSets);
         }
         cp_async_wait<0>();
     }
@@ -515,7 +527,7 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     return g;
 }
 
-size_t mma_hash_smem() { return Geo<true>::smem; }
+size_t mma_hash_smem() { return Geo<true, 2>::smem; }
 
 void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     if (!a0.nown || !g.items) return;
@@ -530,18 +542,31 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     }();
     MmaHashArgs a = a0;
     a.spin = spin;
-    static const int atmem = [] {  // dev A/B knob: SSBH_MMA_ATMEM=0 stages A in shared memory
+    // dev A/B knobs: SSBH_MMA_ATMEM=0 stages A in shared memory (one producer set);
+    // SSBH_MMA_SETS=1|2 producer sets with A in TMEM (default 2)
+    static const int atmem = [] {
         const char* e = std::getenv("SSBH_MMA_ATMEM");
         return e && *e == '0' ? 0 : 1;
     }();
-    if (atmem) {
-        cudaFuncSetAttribute(k_toeplitz_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)Geo<true>::smem);
-        k_toeplitz_mma<true><<<grid, kThreads, Geo<true>::smem, st>>>(a);
+    static const int sets = [] {
+        const char* e = std::getenv("SSBH_MMA_SETS");
+        return e && *e == '1' ? 1 : 2;
+    }();
+    if (!atmem) {
+        using G = Geo<false, 1>;
+        cudaFuncSetAttribute(k_toeplitz_mma<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)G::smem);
+        k_toeplitz_mma<false, 1><<<grid, threads_for(1), G::smem, st>>>(a);
+    } else if (sets == 1) {
+        using G = Geo<true, 1>;
+        cudaFuncSetAttribute(k_toeplitz_mma<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)G::smem);
+        k_toeplitz_mma<true, 1><<<grid, threads_for(1), G::smem, st>>>(a);
     } else {
-        cudaFuncSetAttribute(k_toeplitz_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)Geo<false>::smem);
-        k_toeplitz_mma<false><<<grid, kThreads, Geo<false>::smem, st>>>(a);
+        using G = Geo<true, 2>;
+        cudaFuncSetAttribute(k_toeplitz_mma<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)G::smem);
+        k_toeplitz_mma<true, 2><<<grid, threads_for(2), G::smem, st>>>(a);
     }
 }
 

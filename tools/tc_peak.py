@@ -34,10 +34,12 @@ def sampled(fn):
     return r, clocks
 
 
-for layout in (0, 1):
+for pairs in (False, True):
+  for layout in (0, 1):
     for iters in (20000, 200000):
-        (rate, ms), clk = sampled(lambda: P.measure_mma_i8_peak(iters, layout))
-        print(json.dumps({"probe": "i8", "layout": layout, "iters": iters, "ms": round(ms, 2),
+        (rate, ms), clk = sampled(lambda: P.measure_mma_i8_peak(iters, layout, pairs))
+        print(json.dumps({"probe": "i8", "pairs": pairs, "layout": layout, "iters": iters,
+                          "ms": round(ms, 2),
                           "T_mac_s": round(rate / 1e12, 1), "T_ops": round(2 * rate / 1e12, 1),
                           "sm_mhz": sorted(c for c, _ in clk)[len(clk) // 2] if clk else None,
                           "power_w_max": max((p for _, p in clk), default=None)}), flush=True)
