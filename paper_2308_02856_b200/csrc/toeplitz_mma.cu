@@ -19,8 +19,9 @@
 //   K-major row is input position 128g + kc + 8b + 32w (any permutation of K is allowed as
 //   long as both operands use it).
 // * A = Y (M = 128 blocks): chunk q word w of block j is y-word (4g + w) >> kc — one shift
-//   per 4 bytes, canonical no-swizzle K-major layout (8-row core matrices, LBO 128 B along
-//   K, SBO 2048 B along M).
+//   per 4 bytes. Default: written into TMEM by the producers (tcgen05.st, lane = block row,
+//   column 8m + c = chunk 2m + c/4, word c%4 of MMA m); fallback (SSBH_MMA_ATMEM=0): the
+//   canonical no-swizzle K-major smem layout (LBO 128 B along K, SBO 2048 B along M).
 // * B = Hankel (N = 256 output rows): with that K order, row r chunk (g, kc) holds S bits
 //   i0 + c0 + (r + kc + 128g) + 8b + 32w — a function of the UNIT index u = r + kc + 128g
 //   alone. So the operand is a table of 16-byte units, unit u word w = the 32-bit seed
@@ -28,19 +29,23 @@
 //   it with LBO = 16 B (next K chunk = next unit) and SBO = 128 B (8 rows = 8 units):
 //   rows overlap in memory exactly as Hankel rows overlap in the seed. 392 units (6 KB)
 //   cover a 256-row x 256-position stage.
+// Operand bytes are masked to 0/1 anyway: the don't-care bits toggling in the multipliers
+// drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965).
 //
-// Kernel: persistent, one CTA per SM (213 KB shared memory, 512 TMEM columns = two
-// 128 x 256 s32 accumulators). Work item = (M tile of 128 owned blocks, K part, N tile of
-// 256 output rows); every CTA walks items blockIdx.x, +grid, ... with N tiles innermost,
-// so concurrently running CTAs stream the same blocks' y words (L2 reuse). Warp roles:
+// Kernel: persistent, one CTA per SM, TMEM = one 128 x 256 s32 accumulator + a 4-stage ring
+// of A operands (smem-A fallback: two accumulators). Work item = (M tile of 128 owned blocks,
+// K part, N tile of 256 output rows); every CTA walks items blockIdx.x, +grid, ... with N
+// tiles innermost, so concurrently running CTAs stream the same blocks' y words (L2 reuse).
+// Warp roles:
 //   warps 0-3  epilogue: tcgen05.ld 32x32b (lane = block, 32 columns = 32 rows) -> parity
 //              bits -> one key word per load (st.global, or red.xor when K is split)
-//   warp 4     MMA issuer: 8 x tcgen05.mma (128x256x32) per stage, commit -> empty slot,
-//              last stage -> accumulator full (double-buffered accumulators)
-//   warps 5-8  A producers: block row jl, cp.async of its 32 y bytes 4 stages ahead, 16
-//              STS.128 of shifted words per stage
-//   warps 9-12 B producers: cp.async of 128 B of seed per stage, 392 units per stage
-// Ring of 5 stages (38 KB each) between producers and the MMA warp (mbarriers).
+//   warp 4     MMA issuer: 8 x tcgen05.mma (128x256x32) per stage, commit -> stage barrier,
+//              last stage of an item -> accumulator barrier
+//   then two producer sets (set q fills the stages g with g % 2 == q), each of
+//     4 A warps: block row jl, cp.async of its 32 y bytes 4 own stages ahead, 64 columns
+//     4 B warps: cp.async of 128 B of seed per stage, 392 units per stage
+// mbarriers between the roles; one producer set alone left the tensor core ~10 % idle (its
+// per-stage chain is latency-bound), two reach the sustained kind::i8 probe rate.
 #include <algorithm>
 #include <cstdlib>
 
