@@ -246,8 +246,8 @@ def main():
                     help="N>1: sharded sampling + peer-memory owner exchange, or every rank "
                          "re-sampling all rounds")
     ap.add_argument("--engine", default="auto", choices=["auto", "lop3", "tensor"],
-                    help="hash engine of shared-seed plans (auto = tensor; per-block seeds "
-                         "always run the LOP3 engine)")
+                    help="hash engine (auto = tensor: tcgen05 u8 MMAs mod 2; lop3 = the "
+                         "integer-ALU kernel)")
     ap.add_argument("--no-lop3-compare", action="store_true",
                     help="skip the extra LOP3-engine step reported beside a tensor-engine line")
     ap.add_argument("--rounds", type=int, default=0,
@@ -315,11 +315,11 @@ def main():
     else:
         plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"],
                       block_first=first, block_count=count, chunk_bits=chunk_bits)
-        if args.engine == "tensor" and not c["per_block"]:
+        if args.engine == "tensor":
             plan.set_engine(P.ENGINE_TENSOR)
         plan.set_timing(True)
         check, close = plan.check, plan.close
-    tensor = not c["per_block"] and args.engine != "lop3"
+    tensor = args.engine != "lop3"
 
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
     # tcgen05 kind::i8 MAC rate with the tensor engine's operand layouts
@@ -497,7 +497,8 @@ def main():
         if tensor:
             macs = hash_ops * 32  # sum_j n_j * k bit products = u8 tensor MACs doing useful work
             roof = {
-                "bound": "tensor (tcgen05 kind::i8)", "kernel": "k_toeplitz_mma",
+                "bound": "tensor (tcgen05 kind::i8)",
+                "kernel": "k_toeplitz_mma_pb" if c["per_block"] else "k_toeplitz_mma",
                 "achieved": macs / (avg_hash_ms * 1e-3) / 1e12, "peak": tc_peak / 1e12,
                 "unit": "T MAC/s (u8 x u8 -> s32; one MAC = one GF(2) bit product)",
                 "frac": macs / (avg_hash_ms * 1e-3) / tc_peak,

@@ -185,14 +185,14 @@ ssbh_status ssbh_plan_check(ssbh_plan* plan, ssbh_extract_stats* stats);
 ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
 
 /* Hash engine of a plan (not a reference interface: the reference has one CPU loop).
- *   SSBH_ENGINE_LOP3   : GF(2) product on the integer ALUs (LOP3/SHF/POPC) — every plan.
- *   SSBH_ENGINE_TENSOR : shared-seed plans only: all blocks share one Hankel matrix, so the
- *                        hash is one u8 GEMM mod 2 on the tcgen05 tensor cores (kind::i8).
- *   SSBH_ENGINE_AUTO   : the plan's default: TENSOR for shared-seed plans, LOP3 for
- *                        per-block seeds (environment SSBH_HASH_ENGINE=lop3 keeps shared-seed
- *                        plans on LOP3).
- * Both engines produce identical keys. TENSOR on a per-block-seed plan ->
- * SSBH_INVALID_ARGUMENT. ssbh_plan_engine returns the engine in use. */
+ *   SSBH_ENGINE_LOP3   : GF(2) product on the integer ALUs (LOP3/SHF/POPC).
+ *   SSBH_ENGINE_TENSOR : the product as u8 MMAs mod 2 on the tcgen05 tensor cores (kind::i8):
+ *                        shared seeds = one GEMM of all blocks against the one Hankel matrix,
+ *                        per-block seeds = each block's matrix-vector product tiled into
+ *                        128 x 128 Hankel blocks.
+ *   SSBH_ENGINE_AUTO   : the plan's default: TENSOR (environment SSBH_HASH_ENGINE=lop3 makes it
+ *                        LOP3).
+ * Both engines produce identical keys. ssbh_plan_engine returns the engine in use. */
 #define SSBH_ENGINE_AUTO 0
 #define SSBH_ENGINE_LOP3 1
 #define SSBH_ENGINE_TENSOR 2

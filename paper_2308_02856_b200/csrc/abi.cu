@@ -337,10 +337,11 @@ uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid)
 
 }  // namespace
 
-// Engine of a new plan: shared seeds run on the tensor cores (toeplitz_mma.cu), per-block seeds
-// on the integer ALUs; SSBH_HASH_ENGINE=lop3 keeps shared-seed plans on the ALUs too.
+// Engine of a new plan: the tensor cores (toeplitz_mma.cu: shared seeds as one GEMM over all
+// blocks, per-block seeds as tiled matrix-vector products) unless SSBH_HASH_ENGINE=lop3 keeps
+// the plan on the integer ALUs (toeplitz.cu).
 static int default_engine(uint32_t per_block_seed) {
-    if (per_block_seed) return kEngineLop3;
+    (void)per_block_seed;
     const char* e = std::getenv("SSBH_HASH_ENGINE");
     if (e && std::strcmp(e, "lop3") == 0) return kEngineLop3;
     return kEngineMma;
@@ -385,6 +386,7 @@ struct ssbh_plan {
     // hash engine (shared-seed plans may run on the tensor cores, toeplitz_mma.cu)
     int engine = kEngineLop3;
     MmaGeom mma{};
+    PbGeom pb{};
     DBuf mt_words;
     // host-path staging
     DBuf d_input, d_key, d_len, d_keep;
@@ -457,6 +459,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     pl->key_words32 = ((uint64_t)nown * k + 31) / 32;
     pl->engine = default_engine(params->per_block_seed);
     pl->mma = make_mma_geom(nown, pl->kw, n / params->n_subblocks, pl->device);
+    pl->pb = make_pb_geom(nown, pl->kw, pl->device);
 
     // two-level split for large key spaces (SSBH_BUCKETS=0 disables it, =1 forces it)
     const char* be = std::getenv("SSBH_BUCKETS");
@@ -598,10 +601,6 @@ extern "C" ssbh_status ssbh_plan_set_engine(ssbh_plan* pl, int engine) {
     if (engine < SSBH_ENGINE_AUTO || engine > SSBH_ENGINE_TENSOR)
         return fail(SSBH_INVALID_ARGUMENT, "set_engine: unknown engine %d", engine);
     int e = engine == SSBH_ENGINE_AUTO ? default_engine(pl->p.per_block_seed) : engine;
-    if (e == SSBH_ENGINE_TENSOR && pl->p.per_block_seed)
-        return fail(SSBH_INVALID_ARGUMENT,
-                    "set_engine: the tensor-core engine needs a shared seed (per-block seeds are "
-                    "one matrix-vector product per block)");
     if (e != pl->engine) {
         pl->engine = e;
         for (auto& x : pl->exec)  // captured graphs hold the other engine's launches
@@ -718,7 +717,21 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
     const Layout lay = pl->lay.view();
     uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
     CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
-    if (pl->engine == kEngineMma) {
+    if (pl->engine == kEngineMma && pl->p.per_block_seed) {
+        PbHashArgs m{};
+        m.ybuf = pl->ybuf.as<uint32_t>();
+        m.sbuf = pl->sbuf.as<uint32_t>();
+        m.out = out;
+        m.out_stride = pl->direct_out ? pl->p.out_bits / 32 : pl->kw;
+        m.lay = lay;
+        m.nown = pl->nown;
+        m.kw = pl->kw;
+        m.ntiles = pl->pb.ntiles;
+        m.nwin = pl->pb.nwin;
+        m.items = pl->pb.items;
+        launch_hash_mma_pb(m, pl->pb, st);
+        launches += 1;
+    } else if (pl->engine == kEngineMma) {
         MmaHashArgs m{};
         m.ybuf = pl->ybuf.as<uint32_t>();
         m.sbuf = pl->sbuf.as<uint32_t>();
@@ -1147,17 +1160,33 @@ extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, cons
     launch_pack_blocks(dseeds.as<uint64_t>(), dseedoff.as<unsigned long long>(),
                        din.as<uint64_t>(), dinoff.as<unsigned long long>(), lay, nown, m,
                        sbuf.as<uint32_t>(), ybuf.as<uint32_t>(), 0);
-    HashArgs a{};
-    a.ybuf = ybuf.as<uint32_t>();
-    a.sbuf = sbuf.as<uint32_t>();
-    a.out = scratch.as<uint32_t>();
-    a.out_stride = kw;
-    a.lay = lay;
-    a.nown = nown;
-    a.kw = kw;
-    a.rowtiles = rowtiles;
-    a.per_block_seed = 1;
-    launch_hash(a, grid, 0);
+    if (default_engine(1) == kEngineMma) {  // every block its own matrix: tiled matvec MMAs
+        const PbGeom pg = make_pb_geom(nown, kw, dev);
+        PbHashArgs a{};
+        a.ybuf = ybuf.as<uint32_t>();
+        a.sbuf = sbuf.as<uint32_t>();
+        a.out = scratch.as<uint32_t>();
+        a.out_stride = kw;
+        a.lay = lay;
+        a.nown = nown;
+        a.kw = kw;
+        a.ntiles = pg.ntiles;
+        a.nwin = pg.nwin;
+        a.items = pg.items;
+        launch_hash_mma_pb(a, pg, 0);
+    } else {
+        HashArgs a{};
+        a.ybuf = ybuf.as<uint32_t>();
+        a.sbuf = sbuf.as<uint32_t>();
+        a.out = scratch.as<uint32_t>();
+        a.out_stride = kw;
+        a.lay = lay;
+        a.nown = nown;
+        a.kw = kw;
+        a.rowtiles = rowtiles;
+        a.per_block_seed = 1;
+        launch_hash(a, grid, 0);
+    }
     launch_concat(scratch.as<uint32_t>(), kw, nown, m, key.as<uint32_t>(), 0);
     if (auto st = check_launch("toeplitz_hash")) return st;
     CU(cudaMemcpy(out, key.p, key_w64 * 8, cudaMemcpyDeviceToHost));

@@ -215,6 +215,26 @@ struct MmaHashArgs {
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
     uint32_t spin;           // dev knob: MMA warp spins instead of suspending on its waits
 };
+// Per-block seeds on the tensor cores: work item = (owned block, window of 256 row tiles of
+// 128 rows); see toeplitz_mma.cu.
+struct PbGeom {
+    uint32_t ntiles;   // ceil(kw / 4): 128-row tiles per block
+    uint32_t nwin;     // ceil(ntiles / 256)
+    uint32_t grid;
+    uint64_t items;    // nown * nwin
+};
+struct PbHashArgs {
+    const uint32_t* ybuf;
+    const uint32_t* sbuf;    // per-block seed regions at lay.soff[jj], pre-shifted by one bit
+    uint32_t* out;           // out[jj * out_stride + word], every word written once
+    unsigned long long out_stride;
+    Layout lay;
+    uint32_t nown, kw;
+    uint32_t ntiles, nwin;
+    uint64_t items;
+};
+PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device);
+void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
 size_t mma_hash_smem();

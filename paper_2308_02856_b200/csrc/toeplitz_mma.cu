@@ -495,6 +495,240 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_mma(MmaHashA
     }
 }
 
+// =========================================================================================
+// Per-block seeds: one Toeplitz matrix per block, i.e. one matrix-VECTOR product per block —
+// no second block shares the matrix. The product still maps onto the tensor cores by tiling
+// both the rows and the input into 128-wide pieces, i = 128 I + r, c = 128 C + t:
+//     K[128 I + r] = sum_C sum_t S[128 (I + C) + r + t] y[128 C + t] = sum_C (H_{I+C} y_C)[r]
+// with the 128 x 128 Hankel block H_D[r][t] = S[128 D + r + t]. For one D, the same H_D
+// multiplies every pair (I, C = D - I): a work item owns a window of 256 row tiles
+// I = I0 + n and walks D; each D step is one 128 x 256 x 128 u8 MMA
+//     acc[r][n] += sum_t H_D[r][t] * Y[n][t],   Y[n] = y chunk D - I0 - n (zero outside)
+// accumulated in TMEM over all D, so the work is exactly k * n_j MACs plus the ramp of the
+// window (< 3 % at config 4). Operands (K order within a 128-position chunk as in the shared
+// kernel: byte (kc, w, b) = position kc + 8b + 32w):
+//   A = H_D: 136 Hankel units of 16 B in shared memory (unit u word w = seed window at bit
+//       128 D + u + 32 w), LBO 16 B, SBO 128 B — generated per D step.
+//   B = Y:   column n's chunk moves by one each D step, so the y chunks are laid out in
+//       REVERSE order in a shared buffer of 8 K-chunk planes x 512 units (unit (kc, P) =
+//       chunk Ctop - P, word w = (y word (4C + w) >> kc) & 0x01010101): column n of step D is
+//       unit P = (D's start) + n, i.e. rows 16 B apart (SBO 128 B), planes 8 KB apart (LBO),
+//       and stepping D moves the descriptor's start address back by 16 B. One buffer serves
+//       256 D steps (511 chunks); two alternate.
+// Epilogue: lane = row r, registers = 32 row tiles n -> one __ballot_sync per tile gives the
+// key word of rows 128 (I0 + n) + 32 e .. + 31.
+constexpr int kPbWin = 256;                  // row tiles per work item (accumulator columns)
+constexpr int kPbL = 256;                    // D steps per y buffer
+constexpr int kPbUnits = 512;                // units per K-chunk plane of a y buffer
+constexpr int kPbYBytes = 8 * kPbUnits * 16; // 64 KB
+constexpr int kPbHUnits = 136;               // Hankel units per D step (128 rows + 7 + pad)
+constexpr int kPbHBytes = kPbHUnits * 16;    // 2176
+constexpr int kPbHStages = 8;
+constexpr int kPbThreads = 13 * 32;          // 4 epilogue, 1 MMA, 4 y, 4 Hankel warps
+constexpr size_t kPbBar = 2 * (size_t)kPbYBytes + (size_t)kPbHStages * kPbHBytes;
+constexpr size_t kPbSmem = kPbBar + (2 * kPbHStages + 8) * 8 + 16;
+// kind::i8, M = 128, N = 256 (same instruction descriptor as the shared kernel)
+
+struct PbItem {
+    uint32_t jj, I0, ncols;   // block, first row tile, valid row tiles in the window
+    uint32_t nD;              // D steps: ncols + nC - 1
+    uint32_t nC;              // y chunks of 128 positions
+};
+
+__device__ __forceinline__ bool pb_decode(const PbHashArgs& a, uint32_t item, PbItem& d) {
+    if (item >= a.items) return false;
+    d.jj = item / a.nwin;
+    const uint32_t w = item - d.jj * a.nwin;
+    d.I0 = w * kPbWin;
+    d.ncols = min((uint32_t)kPbWin, a.ntiles - d.I0);
+    d.nC = a.lay.ypad[d.jj] / 4;
+    d.nD = d.nC ? d.ncols + d.nC - 1 : 0;
+    return true;
+}
+
+__global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* ybufs = smem;                                  // 2 x 64 KB
+    uint8_t* hst = smem + 2 * (size_t)kPbYBytes;            // kPbHStages x 2176 B
+    uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + kPbBar);
+    uint64_t* hempty = hfull + kPbHStages;
+    uint64_t* yfull = hempty + kPbHStages;
+    uint64_t* yempty = yfull + 2;
+    uint64_t* tfull = yempty + 2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    constexpr uint32_t M8 = 0x01010101u;
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPbHStages; ++s) {
+            mbar_init(&hfull[s], 4);
+            mbar_init(&hempty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&yfull[b], 4);
+            mbar_init(&yempty[b], 1);
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEpiWarps);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kEpiWarps) {
+        // ------------------------------------------------------------------ epilogue
+        uint32_t t = 0;
+        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
+            PbItem d;
+            if (!pb_decode(a, item, d)) break;
+            const uint32_t ab = t & 1;
+            mbar_wait_sleep(&tfull[ab], (t >> 1) & 1);
+            tc_fence_after();
+            if (d.nD) {
+                uint32_t* dst = a.out + (unsigned long long)d.jj * a.out_stride;
+#pragma unroll 1
+                for (int q = 0; q < kPbWin / 32; ++q) {
+                    uint32_t v[32];
+                    SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kPbWin + 32u * q, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const uint32_t wd = __ballot_sync(0xffffffffu, v[e] & 1u);
+                        if (lane == (uint32_t)e) mine = wd;
+                    }
+                    const uint32_t n = 32u * q + lane;
+                    const uint32_t word = 4u * (d.I0 + n) + warp;  // rows 128 I + 32 warp ..
+                    if (n < d.ncols && word < a.kw) dst[word] = mine;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+        }
+    } else if (warp == kMmaWarp) {
+        // ------------------------------------------------------------------ MMA issuer
+        uint32_t hs = 0, yb = 0, t = 0;
+        const uint32_t ybase = smem_u32(ybufs), hbase = smem_u32(hst);
+        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
+            PbItem d;
+            if (!pb_decode(a, item, d)) break;
+            const uint32_t ab = t & 1;
+            if (t >= 2) mbar_wait_sleep(&tempty[ab], ((t >> 1) - 1) & 1);
+            tc_fence_after();
+            if (d.nD == 0) {
+                if (lane == 0) mbar_arrive(&tfull[ab]);
+                continue;
+            }
+            for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
+                const uint32_t b = yb & 1;
+                mbar_wait(&yfull[b], (yb >> 1) & 1);
+                tc_fence_after();
+                const uint32_t steps = min((uint32_t)kPbL, d.nD - D0);
+                for (uint32_t s = 0; s < steps; ++s, ++hs) {
+                    const uint32_t slot = hs % kPbHStages;
+                    mbar_wait(&hfull[slot], (hs / kPbHStages) & 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t ha = hbase + slot * kPbHBytes;
+                        // column n of step D0+s is unit (kPbL - 1 - s) + n of the buffer
+                        const uint32_t ya = ybase + b * kPbYBytes + 16u * (kPbL - 1 - s);
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const uint64_t adesc = sdesc(ha + 32u * m, 16, 128);
+                            const uint64_t bdesc = sdesc(ya + 2u * m * (kPbUnits * 16), kPbUnits * 16, 128);
+                            mma_i8(tmem + ab * kPbWin, adesc, bdesc, (D0 | s | (uint32_t)m) != 0);
+                        }
+                        mma_commit(&hempty[slot]);
+                        if (s + 1 == steps) mma_commit(&yempty[b]);
+                        if (D0 + s + 1 == d.nD) mma_commit(&tfull[ab]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp < kProdWarp0 + 4) {
+        // ------------------------------------------------------------------ y buffers
+        const uint32_t yt = threadIdx.x - kProdWarp0 * 32;  // 0..127
+        uint32_t yb = 0;
+        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
+            PbItem d;
+            if (!pb_decode(a, item, d)) break;
+            const uint32_t* y = a.ybuf + a.lay.yoff[d.jj];
+            for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
+                const uint32_t b = yb & 1;
+                if (yb >= 2) mbar_wait_sleep(&yempty[b], ((yb >> 1) - 1) & 1);
+                uint8_t* buf = ybufs + b * kPbYBytes;
+                // unit P holds chunk C = D0 + kPbL - 1 - P (the buffer's D steps D0 .. +255
+                // read units kPbL - 1 - s + n, n < 256)
+#pragma unroll 1
+                for (uint32_t P = yt; P < kPbUnits - 1; P += 128) {
+                    const int64_t C = (int64_t)D0 + kPbL - 1 - P;
+                    uint4 x = make_uint4(0, 0, 0, 0);
+                    if (C >= 0 && C < (int64_t)d.nC) x = __ldg(reinterpret_cast<const uint4*>(y) + C);
+#pragma unroll
+                    for (int kc = 0; kc < 8; ++kc)
+                        *reinterpret_cast<uint4*>(buf + (kc * kPbUnits + P) * 16) =
+                            make_uint4((x.x >> kc) & M8, (x.y >> kc) & M8, (x.z >> kc) & M8,
+                                       (x.w >> kc) & M8);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&yfull[b]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ Hankel units
+        const uint32_t ht = threadIdx.x - (kProdWarp0 + 4) * 32;  // 0..127
+        uint32_t hs = 0;
+        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
+            PbItem d;
+            if (!pb_decode(a, item, d)) break;
+            const uint32_t* sw = a.sbuf + a.lay.soff[d.jj];  // pre-shifted: S'[b + 1] = S[b]
+            for (uint32_t s = 0; s < d.nD; ++s, ++hs) {
+                const uint32_t slot = hs % kPbHStages;
+                if (hs >= (uint32_t)kPbHStages)
+                    mbar_wait_sleep(&hempty[slot], ((hs / kPbHStages) - 1) & 1);
+                // step s of the item is D = I0 + s - (kPbL... ) : D = I0 + s (C = D - I0 - n)
+                const uint64_t wbase = 4ull * (d.I0 + s);  // word of S' bit 128 D
+                uint8_t* hsm = hst + slot * kPbHBytes;
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t u = ht + 128u * r;
+                    if (u < (uint32_t)kPbHUnits) {
+                        const uint32_t rel = u + 1, q = rel >> 5, sh = rel & 31;
+                        const uint32_t* p = sw + wbase + q;
+                        const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2),
+                                       w3 = __ldg(p + 3), w4 = __ldg(p + 4);
+                        *reinterpret_cast<uint4*>(hsm + 16 * u) = make_uint4(
+                            __funnelshift_r(w0, w1, sh) & M8, __funnelshift_r(w1, w2, sh) & M8,
+                            __funnelshift_r(w2, w3, sh) & M8, __funnelshift_r(w3, w4, sh) & M8);
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&hfull[slot]);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 // Per M tile: the largest padded y length (u32 words) of its owned blocks.
 __global__ void k_mma_tiles(const uint32_t* __restrict__ ypad, uint32_t nown,
                             uint32_t* __restrict__ mt_words) {
@@ -530,6 +764,25 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
         g.ksplit *= 2;
     g.items = (uint64_t)g.mtiles * g.ntiles * g.ksplit;
     return g;
+}
+
+PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device) {
+    PbGeom g{};
+    g.ntiles = (kw + 3) / 4;  // 128-row tiles
+    g.nwin = (g.ntiles + kPbWin - 1) / kPbWin;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    g.grid = sms;
+    g.items = (uint64_t)nown * g.nwin;
+    return g;
+}
+
+void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st) {
+    if (!a.nown || !g.items) return;
+    cudaFuncSetAttribute(k_toeplitz_mma_pb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kPbSmem);
+    const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
+    k_toeplitz_mma_pb<<<grid, kPbThreads, kPbSmem, st>>>(a);
 }
 
 size_t mma_hash_smem() { return Geo<true, 2>::smem; }

@@ -1,7 +1,8 @@
-"""GPU parity of both hash engines of shared-seed plans.
+"""GPU parity of both hash engines.
 
-Shared-seed plans hash every block as one u8 GEMM mod 2 on tcgen05 by default
-(csrc/toeplitz_mma.cu, SSBH_ENGINE_TENSOR); SSBH_ENGINE_LOP3 keeps them on the integer ALUs
+Plans hash on the tcgen05 tensor cores by default (csrc/toeplitz_mma.cu, SSBH_ENGINE_TENSOR):
+shared seeds as one u8 GEMM mod 2 over all blocks, per-block seeds as matrix-vector products
+tiled into 128 x 128 Hankel blocks; SSBH_ENGINE_LOP3 keeps a plan on the integer ALUs
 (csrc/toeplitz.cu). The keys must be bit-identical to the reference's toeplitz_hash
 (proj/src/toeplitz.cpp:34-52) — checked here against the oracle restatement, the golden
 digests made by the compiled reference, and each other. Every call runs sm_100a kernels
@@ -27,7 +28,7 @@ def _run_plan(dev, x, n, s, k, samp, hsh, engine, **kw):
 ENGINES = pytest.mark.parametrize("engine", [1, 2], ids=["lop3", "tensor"])
 
 
-def test_default_engine_is_tensor_for_shared_seeds(dev):
+def test_default_engine_is_tensor(dev):
     plan = dev.Plan(100000, 8, 64, 2, 3)
     assert plan.engine == dev.ENGINE_TENSOR
     plan.set_engine(dev.ENGINE_LOP3)
@@ -36,6 +37,8 @@ def test_default_engine_is_tensor_for_shared_seeds(dev):
     assert plan.engine == dev.ENGINE_TENSOR
     plan.close()
     plan = dev.Plan(100000, 8, 64, 2, 3, per_block=True)
+    assert plan.engine == dev.ENGINE_TENSOR
+    plan.set_engine(dev.ENGINE_LOP3)
     assert plan.engine == dev.ENGINE_LOP3
     plan.close()
 
@@ -125,12 +128,39 @@ def test_engine_streaming(dev, oracle, engine):
     assert (got[: len(want)] == want).all()
 
 
-def test_tensor_engine_rejects_per_block_seeds(dev):
-    plan = dev.Plan(100000, 8, 64, 2, 3, per_block=True)
-    with pytest.raises(ValueError):
-        plan.set_engine(dev.ENGINE_TENSOR)
-    assert plan.engine == dev.ENGINE_LOP3
-    plan.close()
+@ENGINES
+def test_per_block_seeds_random_shapes_vs_oracle(dev, oracle, engine):
+    """Per-block seeds (KeyedStream(hash, "hash-seed", j), pipeline.cpp:132): on the tensor
+    engine every block is a matrix-vector product tiled into 128 x 128 Hankel blocks (row
+    windows of 256 tiles; k = 70000 spans three windows)."""
+    rng = np.random.default_rng(4)
+    shapes = [(1000, 1, 1), (5000, 3, 31), (70000, 8, 256), (300000, 16, 1024),
+              (200000, 10, 33), (123457, 7, 3000), (90000, 3, 70000), (400000, 40, 4096),
+              (60000, 2, 257), (250000, 5, 32896)]
+    for (n, s, k) in shapes:
+        x = oracle.make_input(int(rng.integers(1000)), 0.5, n)
+        want, wnj = oracle.extract(x, n, s, 51, 52, 1, k)
+        got, nj, st = _run_plan(dev, x, n, s, k, 51, 52, engine, per_block=True)
+        assert (nj == wnj).all()
+        assert (got == want).all(), (n, s, k)
+
+
+@ENGINES
+def test_per_block_golden_and_ranges(dev, oracle, golden, engine):
+    c = golden["extract"]["small_perblock"]
+    x = oracle.make_input(c["seed_in"], c["p"], c["n"])
+    key, nj, _ = _run_plan(dev, x, c["n"], c["s"], c["k"], c["seed_samp"], c["seed_hash"],
+                           engine, per_block=True)
+    assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
+    # owned block ranges: block j keeps its own seed stream sub = j
+    n, s, k = 300000, 12, 1536
+    x = oracle.make_input(8, 0.4, n)
+    want, _ = oracle.extract(x, n, s, 3, 4, 1, k)
+    kw = k // 64
+    for first, cnt in ((0, 5), (5, 7)):
+        got, _, _ = _run_plan(dev, x, n, s, k, 3, 4, engine, per_block=True, block_first=first,
+                              block_count=cnt)
+        assert (got == want[first * kw:(first + cnt) * kw]).all()
 
 
 def test_tensor_engine_empty_block_semantics(dev, oracle):

@@ -25,7 +25,7 @@ def main():
         c = P.CONFIGS[cid]
         n, s, k = c["n"], c["s"], c["k"]
         plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"])
-        if args.engine != "auto" and not c["per_block"]:
+        if args.engine != "auto":
             plan.set_engine(P.ENGINE_LOP3 if args.engine == "lop3" else P.ENGINE_TENSOR)
         plan.set_timing(True)
         d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
