@@ -17,12 +17,15 @@ def main():
     ap.add_argument("--configs", default="1,2,3")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--engine", default="auto", choices=["auto", "lop3", "tensor"])
+    ap.add_argument("--per-block", action="store_true", help="force per-block seeds")
     args = ap.parse_args()
     tag = os.environ.get("SSBH_HASH_WIN", "default") + ("/nograph" if os.environ.get("SSBH_NO_GRAPH") == "1" else "/graph")
     peak, _ = P.measure_lop3_peak(20000)
     print(json.dumps({"win": tag, "lop3_peak_T": round(peak / 1e12, 3)}), flush=True)
     for cid in [int(c) for c in args.configs.split(",")]:
-        c = P.CONFIGS[cid]
+        c = dict(P.CONFIGS[cid])
+        if args.per_block:
+            c["per_block"] = True
         n, s, k = c["n"], c["s"], c["k"]
         plan = P.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"])
         if args.engine != "auto":
