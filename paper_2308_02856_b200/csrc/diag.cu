@@ -166,7 +166,146 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     }
 }
 
+// Block-scaled FP4 probe (kind::mxf4, E2M1 operands, every UE8M0 scale = 1.0): rate of
+// 128x256x64 MMAs and exactness of the f32 accumulation of integer sums. mode 0: A and B all
+// 1.0 (rate); mode 1: A all 1.0, B one 1.0 per row, so every MMA adds exactly 1 and the
+// accumulator must read `iters` (checked per element, mismatches counted into *bad).
+__global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, uint32_t* bad) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+    for (uint32_t i = threadIdx.x; i < 4096 / 4; i += blockDim.x) w[i] = 0x22222222u;  // A
+    for (uint32_t i = threadIdx.x; i < 8192 / 4; i += blockDim.x) {
+        // B: row n occupies bytes (n%8)*16 + (n/8)*256 + kc*128 (kc = 0, 1); one 1.0 per row
+        uint32_t v = 0x22222222u;
+        if (mode == 1) {
+            const uint32_t byte = i * 4, kc = (byte >> 7) & 1, inrow = byte & 15;
+            v = (kc == 0 && inrow == 0) ? 0x00000002u : 0u;
+        }
+        w[1024 + i] = v;
+    }
+    const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tslot;
+    {   // scale factors: columns 256..287 of every lane = 0x7f (UE8M0 2^0)
+        const uint32_t v = 0x7F7F7F7Fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+            "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                tmem + ((32u * warp) << 16) + 256u),
+            "r"(v)
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x == 0) {
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+        const uint32_t idesc = (1u << 7) | (1u << 10) | (32u << 17) | (1u << 23) | (8u << 24);
+        auto desc = [](uint32_t a, uint32_t lbo, uint32_t sbo) {
+            return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+                   ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+        };
+        const uint64_t a = desc(base, 128, 256);
+        const uint64_t b = desc(base + 4096u, 128, 256);
+        for (uint32_t it = 0; it < iters; ++it) {
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
+                ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(it), "r"(tmem + 256u),
+                "r"(tmem + 264u)
+                : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         bar_a)
+                     : "memory");
+    }
+    asm volatile(
+        "{\n.reg .pred P1;\nW:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(bar_a)
+        : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (mode == 1) {
+        uint32_t nbad = 0;
+        for (int q = 0; q < 8; ++q) {
+            uint32_t v[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+                "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                  "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                  "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                  "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                  "=r"(v[30]), "=r"(v[31])
+                : "r"(tmem + ((32u * warp) << 16) + 32u * q));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int e = 0; e < 32; ++e) nbad += __uint_as_float(v[e]) != (float)iters;
+            if (blockIdx.x == 0 && threadIdx.x == 0 && q == 0) bad[1] = v[0];
+        }
+        if (nbad) atomicAdd(bad, nbad);
+    }
+    (void)lane;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 }  // namespace
+
+// Diagnostic for a possible FP4 engine (not used by the hash): rate (MAC/s) and exactness.
+extern "C" ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_per_s,
+                                         double* ms_out, uint32_t* mismatches,
+                                         uint32_t* sample_bits) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SSBH_NO_DEVICE;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int smem = 120 * 1024;
+    cudaFuncSetAttribute(k_f4_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    uint32_t* bad = nullptr;
+    if (cudaMalloc(&bad, 8) != cudaSuccess) return SSBH_CUDA;
+    cudaMemset(bad, 0, 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k_f4_probe<<<sms, 128, smem>>>(iters, mode, bad);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    uint32_t hb[2] = {0, 0};
+    cudaMemcpy(hb, bad, 8, cudaMemcpyDeviceToHost);
+    cudaFree(bad);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
+    if (macs_per_s) *macs_per_s = (double)sms * iters * 128.0 * 256.0 * 64.0 / (ms * 1e-3);
+    if (ms_out) *ms_out = ms;
+    if (mismatches) *mismatches = hb[0];
+    if (sample_bits) *sample_bits = hb[1];
+    return SSBH_OK;
+}
 
 extern "C" ssbh_status ssbh_measure_mma_i8_peak2(uint32_t iters, int layout, double* macs_per_s,
                                                  double* ms_out) {
