@@ -214,6 +214,7 @@ struct MmaHashArgs {
     uint64_t items;
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
     uint32_t spin;           // dev knob: MMA warp spins instead of suspending on its waits
+    uint32_t stage_bits;     // input positions per pipeline stage (set by launch_hash_mma)
 };
 // Per-block seeds on the tensor cores: work item = (owned block, window of 256 row tiles of
 // 128 rows); see toeplitz_mma.cu.

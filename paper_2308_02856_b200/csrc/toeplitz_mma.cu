@@ -168,7 +168,7 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
     const uint32_t r = item / a.ntiles;
     const uint32_t kp = r % a.ksplit;
     d.mt = r / a.ksplit;
-    const uint32_t ns = a.mt_words[d.mt] / (kStageK / 32);
+    const uint32_t ns = a.mt_words[d.mt] / (a.stage_bits / 32);
     const uint32_t lo = (uint32_t)((uint64_t)ns * kp / a.ksplit);
     d.st0 = lo;
     d.nst = (uint32_t)((uint64_t)ns * (kp + 1) / a.ksplit) - lo;
@@ -230,7 +230,7 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
     if (lane < 8) {
         uint64_t q0a = 0;
         if (p.valid) {
-            const uint64_t b1 = (uint64_t)p.d.nt * kN + (uint64_t)(p.d.st0 + p.s) * kStageK + 1;
+            const uint64_t b1 = (uint64_t)p.d.nt * kN + (uint64_t)(p.d.st0 + p.s) * a.stage_bits + 1;
             q0a = (b1 >> 5) & ~3ull;
         }
         cp_async16(raw + 4 * lane, a.sbuf + q0a + 4 * lane, p.valid ? 16u : 0u);
@@ -483,6 +483,293 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_mma(MmaHashA
             s_prefetch(a, pre, lane, raw + rs * 32);
             cp_async_commit();
             pre.advance(a, kSets);
+        }
+        cp_async_wait<0>();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// =========================================================================================
+// Shared seeds on FP4 operands (tcgen05.mma kind::mxf4, block-scaled E2M1, every UE8M0 scale
+// 1.0): the same Y * H^T product at twice the kind::i8 MAC rate (measured 4.46 vs 2.10 P MAC/s,
+// tools/f4_probe.py). Every operand element is 0 or 1.0 (nibble 0b0010), so every product is
+// 0 or 1 and the f32 accumulator holds the exact integer count while it stays below 2^24
+// (verified by the probe); items longer than kF4MaxStages stages are accumulated in several
+// rounds whose parities are XORed (parity of a sum = XOR of the parities of its parts).
+// K order inside a 512-position stage: chunk q = 4g + kc (16 B = 32 nibbles), word w,
+// nibble i <-> position 128g + kc + 4i + 32w, so
+//   A (y, M = 128 blocks, shared memory): chunk (g, kc) word w = ((y word 4g + w) >> kc << 1)
+//     & 0x22222222 — one shift and one mask per 8 elements, as in the i8 engine;
+//   B (Hankel, N = 256 rows): row r chunk (g, kc) = unit r + kc + 128g, unit u word w =
+//     (seed window at bit base + u + 32w << 1) & 0x22222222; 643 units per stage,
+//     LBO 16 B, SBO 128 B.
+// Block-scaled kinds take A from shared memory only, so both operands are staged in shared
+// memory (4 stages x 42 KB); TMEM = one 128 x 256 f32 accumulator + the constant scale
+// factors. Warp roles as in k_toeplitz_mma (two producer sets alternating stages).
+constexpr int kF4StageK = 512;                    // input positions per stage (8 MMAs, K = 64)
+constexpr int kF4GUnits = kN + 3 + 384 + 1;       // 643 Hankel units per stage
+constexpr int kF4YBytes = kM * kF4StageK / 2;     // 32768
+constexpr int kF4GBytes = ((kF4GUnits * 16 + 127) / 128) * 128;  // 10368
+constexpr int kF4Slot = kF4YBytes + kF4GBytes;
+constexpr int kF4Stages = 4;
+constexpr int kF4Pre = 2;                         // cp.async prefetch depth per set
+constexpr int kF4RawY = kF4Pre * kM * 64;         // per set
+constexpr int kF4RawS = 4 * kF4Pre * 128;         // per set
+constexpr size_t kF4Bar = (size_t)kF4Stages * kF4Slot + 2 * (kF4RawY + kF4RawS);
+constexpr size_t kF4Smem = kF4Bar + (2 * kF4Stages + 4) * 8 + 16;
+static_assert(kF4Smem <= 232448, "f4 smem budget");
+constexpr uint32_t kF4MaxStages = (1u << 24) / kF4StageK;  // exact f32 counts per round
+constexpr uint32_t kF4SfCol = kN;                            // scale factors: columns 256..287
+// kind::mxf4 instruction descriptor: E2M1 x E2M1, UE8M0 scales, K-major, M = 128, N = 256
+constexpr uint32_t kF4Idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) | (1u << 23) |
+                              ((uint32_t)(kM >> 4) << 24);
+
+__device__ __forceinline__ void mma_f4(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t sf,
+                                       uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kF4Idesc), "r"(accum), "r"(sf)
+        : "memory");
+}
+
+__device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageIt& p,
+                                              uint32_t jl, uint32_t* raw) {
+    const uint32_t* src = a.ybuf;
+    uint32_t bytes = 0;
+    if (p.valid) {
+        const uint32_t jj = p.d.mt * kM + jl;
+        const uint64_t w0 = (uint64_t)(p.d.st0 + p.s) * (kF4StageK / 32);
+        if (jj < a.nown && w0 < a.lay.ypad[jj]) {
+            src = a.ybuf + a.lay.yoff[jj] + w0;
+            bytes = 16;
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
+}
+
+__global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a) {
+    constexpr int kS = kF4Stages;
+    constexpr uint32_t M2 = 0x22222222u;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* slots = smem;
+    uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kS * kF4Slot);
+    uint32_t* raw_s = raw_y + 2 * (kF4RawY / 4);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kF4Bar);
+    uint64_t* empty = full + kS;
+    uint64_t* tfull = empty + kS;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kS; ++s) {
+            mbar_init(&full[s], kFullArrivals);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tempty[0], kEpiWarps);
+        fence_barrier_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp < kEpiWarps) {  // constant scale factors: 0x7f = 2^0 in every byte
+        uint32_t v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0x7F7F7F7Fu;
+        SSBH_TMEM_ST32(tmem + ((warp * 32u) << 16) + kF4SfCol, v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp < kEpiWarps) {
+        // ---------------------------------------------------------------- epilogue
+        uint32_t t = 0;  // accumulation rounds consumed
+        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
+            Item d;
+            if (!decode(a, item, d)) break;
+            const uint32_t rounds = d.nst ? (d.nst + kF4MaxStages - 1) / kF4MaxStages : 1;
+            uint32_t acc_w[kN / 32];
+#pragma unroll
+            for (int q = 0; q < kN / 32; ++q) acc_w[q] = 0;
+            for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
+                mbar_wait_sleep(&tfull[0], t & 1);
+                tc_fence_after();
+                if (d.nst) {
+#pragma unroll 1
+                    for (int q = 0; q < kN / 32; ++q) {
+                        uint32_t v[32];
+                        SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + 32u * q, v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        uint32_t w = 0;
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) w |= (__float2uint_rz(__uint_as_float(v[e])) & 1u) << e;
+                        acc_w[q] ^= w;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[0]);
+            }
+            const uint32_t jj = d.mt * kM + warp * 32 + lane;
+            if (d.nst && jj < a.nown) {
+                uint32_t* dst = a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32);
+#pragma unroll
+                for (int q = 0; q < kN / 32; ++q)
+                    if (d.nt * (kN / 32) + q < a.kw) {
+                        if (a.ksplit == 1)
+                            dst[q] = acc_w[q];
+                        else
+                            atomicXor(dst + q, acc_w[q]);
+                    }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------------------------------------------------------- MMA issuer
+        uint32_t g = 0, t = 0;
+        const uint32_t base_y = smem_u32(slots), base_g = base_y + kF4YBytes;
+        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
+            Item d;
+            if (!decode(a, item, d)) break;
+            if (d.nst == 0) {
+                if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
+                if (lane == 0) mbar_arrive(&tfull[0]);
+                ++t;
+                continue;
+            }
+            for (uint32_t s0 = 0; s0 < d.nst; s0 += kF4MaxStages, ++t) {
+                if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
+                tc_fence_after();
+                const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
+                for (uint32_t s = s0; s < s1; ++s, ++g) {
+                    const uint32_t slot = g % kS;
+                    mbar_wait(&full[slot], (g / kS) & 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t ya = base_y + slot * kF4Slot;
+                        const uint32_t ga = base_g + slot * kF4Slot;
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const uint32_t unit = 2u * (m & 1) + 128u * (m >> 1);
+                            mma_f4(tmem, sdesc(ya + 256u * m, 128, 2048),
+                                   sdesc(ga + 16u * unit, 16, 128), tmem + kF4SfCol,
+                                   ((s - s0) | (uint32_t)m) != 0);
+                        }
+                        mma_commit(&empty[slot]);
+                        if (s + 1 == s1) mma_commit(&tfull[0]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (((warp - kProdWarp0) & 7) < 4) {
+        // ---------------------------------------------------------------- A producers
+        const uint32_t set = (warp - kProdWarp0) >> 3;
+        const uint32_t jl = 32u * ((warp - kProdWarp0) & 3) + lane;
+        uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
+        StageIt cur, pre;
+        cur.start(a);
+        cur.advance(a, set);
+        pre = cur;
+        for (int i = 0; i < kF4Pre; ++i) {
+            y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
+            cp_async_commit();
+            pre.advance(a, 2);
+        }
+        const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
+        for (uint32_t g = set, i = 0; cur.valid; g += 2, ++i, cur.advance(a, 2)) {
+            const uint32_t rs = i % kF4Pre;
+            cp_async_wait<kF4Pre - 1>();
+            uint4 x[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + h * kM * 4);
+            const uint32_t slot = g % kS;
+            if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+            uint8_t* ys = slots + (size_t)slot * kF4Slot + row_off;
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+#pragma unroll
+                for (int kc = 0; kc < 4; ++kc)
+                    *reinterpret_cast<uint4*>(ys + (4 * gg + kc) * 128) =
+                        make_uint4(((x[gg].x >> kc) << 1) & M2, ((x[gg].y >> kc) << 1) & M2,
+                                   ((x[gg].z >> kc) << 1) & M2, ((x[gg].w >> kc) << 1) & M2);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[slot]);
+            y_prefetch_f4(a, pre, jl, raw + rs * kM * 16);
+            cp_async_commit();
+            pre.advance(a, 2);
+        }
+        cp_async_wait<0>();
+    } else {
+        // ---------------------------------------------------------------- B producers
+        const uint32_t set = (warp - kProdWarp0) >> 3;
+        const uint32_t gw = ((warp - kProdWarp0) & 7) - 4;
+        const uint32_t gt = gw * 32 + lane;
+        uint32_t* raw = raw_s + set * (kF4RawS / 4) + gw * kF4Pre * 32;
+        StageIt cur, pre;
+        cur.start(a);
+        cur.advance(a, set);
+        pre = cur;
+        for (int i = 0; i < kF4Pre; ++i) {
+            s_prefetch(a, pre, lane, raw + i * 32);
+            cp_async_commit();
+            pre.advance(a, 2);
+        }
+        for (uint32_t g = set, i = 0; cur.valid; g += 2, ++i, cur.advance(a, 2)) {
+            const uint32_t rs = i % kF4Pre;
+            cp_async_wait<kF4Pre - 1>();
+            __syncwarp();
+            const uint32_t* sw = raw + rs * 32;
+            const uint64_t b1 =
+                (uint64_t)cur.d.nt * kN + (uint64_t)(cur.d.st0 + cur.s) * kF4StageK + 1;
+            const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));
+            const uint32_t slot = g % kS;
+            if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+            uint8_t* gs = slots + (size_t)slot * kF4Slot + kF4YBytes;
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                const uint32_t u = gt + 128u * r;
+                if (u < (uint32_t)kF4GUnits) {
+                    const uint32_t rel = rel0 + u;
+                    const uint32_t q = rel >> 5, sh = rel & 31;
+                    const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3],
+                                   w4 = sw[q + 4];
+                    *reinterpret_cast<uint4*>(gs + 16 * u) =
+                        make_uint4((__funnelshift_r(w0, w1, sh) << 1) & M2,
+                                   (__funnelshift_r(w1, w2, sh) << 1) & M2,
+                                   (__funnelshift_r(w2, w3, sh) << 1) & M2,
+                                   (__funnelshift_r(w3, w4, sh) << 1) & M2);
+                }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[slot]);
+            s_prefetch(a, pre, lane, raw + rs * 32);
+            cp_async_commit();
+            pre.advance(a, 2);
         }
         cp_async_wait<0>();
     }
@@ -800,6 +1087,19 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     }();
     MmaHashArgs a = a0;
     a.spin = spin;
+    a.stage_bits = kStageK;
+    // SSBH_MMA_FP4=1: the FP4 (kind::mxf4) variant, 2x the i8 MAC rate
+    static const int fp4 = [] {
+        const char* e = std::getenv("SSBH_MMA_FP4");
+        return e && *e == '1' ? 1 : 0;
+    }();
+    if (fp4) {
+        a.stage_bits = kF4StageK;
+        cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kF4Smem);
+        k_toeplitz_f4<<<grid, threads_for(2), kF4Smem, st>>>(a);
+        return;
+    }
     // dev A/B knobs: SSBH_MMA_ATMEM=0 stages A in shared memory (one producer set);
     // SSBH_MMA_SETS=1|2 producer sets with A in TMEM (default 2)
     static const int atmem = [] {

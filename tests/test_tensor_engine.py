@@ -68,6 +68,17 @@ def test_tensor_engine_all_ones_input(dev, oracle):
         assert (got == want).all(), (n, s, k)
 
 
+def test_tensor_engine_block_longer_than_2p24(dev, oracle):
+    """A shared-seed block of more than 2^24 input bits: the FP4 variant's f32 accumulator
+    counts exactly only below 2^24, so such items accumulate in rounds whose parities XOR."""
+    n, s, k = (1 << 25) + 12345, 1, 96
+    x = oracle.make_input(6, 0.5, n)
+    want, _ = oracle.extract(x, n, s, 7, 8, 0, k)
+    got, nj, _ = _run_plan(dev, x, n, s, k, 7, 8, dev.ENGINE_TENSOR)
+    assert int(nj[0]) == n
+    assert (got == want).all()
+
+
 @ENGINES
 @pytest.mark.parametrize("name", ["1", "2", "small_k_odd", "small_k_32"])
 def test_engine_golden(dev, oracle, golden, name, engine):
