@@ -1088,10 +1088,11 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     MmaHashArgs a = a0;
     a.spin = spin;
     a.stage_bits = kStageK;
-    // SSBH_MMA_FP4=1: the FP4 (kind::mxf4) variant, 2x the i8 MAC rate
+    // FP4 (kind::mxf4) operands: 2x the kind::i8 MAC rate (default); SSBH_MMA_FP4=0 keeps the
+    // i8 variant (dev A/B knob)
     static const int fp4 = [] {
         const char* e = std::getenv("SSBH_MMA_FP4");
-        return e && *e == '1' ? 1 : 0;
+        return e && *e == '0' ? 0 : 1;
     }();
     if (fp4) {
         a.stage_bits = kF4StageK;
