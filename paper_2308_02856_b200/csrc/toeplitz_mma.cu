@@ -707,13 +707,15 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
             uint8_t* ys = slots + (size_t)slot * kF4Slot + row_off;
+            // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0
 #pragma unroll
             for (int gg = 0; gg < 4; ++gg) {
 #pragma unroll
-                for (int kc = 0; kc < 4; ++kc)
+                for (int kc = 0; kc < 4; ++kc) {
+                    auto f = [&](uint32_t v) { return (kc ? v >> (kc - 1) : v << 1) & M2; };
                     *reinterpret_cast<uint4*>(ys + (4 * gg + kc) * 128) =
-                        make_uint4(((x[gg].x >> kc) << 1) & M2, ((x[gg].y >> kc) << 1) & M2,
-                                   ((x[gg].z >> kc) << 1) & M2, ((x[gg].w >> kc) << 1) & M2);
+                        make_uint4(f(x[gg].x), f(x[gg].y), f(x[gg].z), f(x[gg].w));
+                }
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -753,15 +755,15 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
             for (int r = 0; r < 6; ++r) {
                 const uint32_t u = gt + 128u * r;
                 if (u < (uint32_t)kF4GUnits) {
-                    const uint32_t rel = rel0 + u;
+                    // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
+                    // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position
+                    const uint32_t rel = rel0 + u - 1;
                     const uint32_t q = rel >> 5, sh = rel & 31;
                     const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3],
                                    w4 = sw[q + 4];
                     *reinterpret_cast<uint4*>(gs + 16 * u) =
-                        make_uint4((__funnelshift_r(w0, w1, sh) << 1) & M2,
-                                   (__funnelshift_r(w1, w2, sh) << 1) & M2,
-                                   (__funnelshift_r(w2, w3, sh) << 1) & M2,
-                                   (__funnelshift_r(w3, w4, sh) << 1) & M2);
+                        make_uint4(__funnelshift_r(w0, w1, sh) & M2, __funnelshift_r(w1, w2, sh) & M2,
+                                   __funnelshift_r(w2, w3, sh) & M2, __funnelshift_r(w3, w4, sh) & M2);
                 }
             }
             fence_proxy_async_smem();
