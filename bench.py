@@ -320,11 +320,22 @@ def main():
         plan.set_timing(True)
         check, close = plan.check, plan.close
     tensor = args.engine != "lop3"
+    if not tensor:
+        hash_kernel = "k_toeplitz_hash"
+    elif c["per_block"]:
+        hash_kernel = "k_toeplitz_mma_pb"
+    elif sharded:
+        hash_kernel = "k_toeplitz_mma" if os.environ.get("SSBH_MMA_FP4") == "0" else "k_toeplitz_f4"
+    else:
+        hash_kernel = plan.hash_kernel
+    fp4 = hash_kernel == "k_toeplitz_f4"
 
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
-    # tcgen05 kind::i8 MAC rate with the tensor engine's operand layouts
+    # the tcgen05 MAC rate (kind::mxf4 or kind::i8) with the hash kernel's operand layouts
     peak, _ = P.measure_lop3_peak(20000)
-    tc_peak = P.measure_mma_i8_peak(200000, 0)[0] if tensor else None  # ~120 ms: sustained
+    tc_peak = None
+    if tensor:  # ~120-140 ms probes: the sustained rate
+        tc_peak = P.measure_mma_f4_peak(200000)[0] if fp4 else P.measure_mma_i8_peak(200000, 0)[0]
 
     def step():
         if sharded:
@@ -497,24 +508,29 @@ def main():
         if tensor:
             macs = hash_ops * 32  # sum_j n_j * k bit products = u8 tensor MACs doing useful work
             roof = {
-                "bound": "tensor (tcgen05 kind::i8)",
-                "kernel": "k_toeplitz_mma_pb" if c["per_block"] else "k_toeplitz_mma",
+                "bound": "tensor (tcgen05 kind::mxf4)" if fp4 else "tensor (tcgen05 kind::i8)",
+                "kernel": hash_kernel,
                 "achieved": macs / (avg_hash_ms * 1e-3) / 1e12, "peak": tc_peak / 1e12,
-                "unit": "T MAC/s (u8 x u8 -> s32; one MAC = one GF(2) bit product)",
+                "unit": ("T MAC/s (E2M1 0/1.0 x 0/1.0 -> f32 exact integer counts; one MAC = "
+                         "one GF(2) bit product)" if fp4 else
+                         "T MAC/s (u8 x u8 -> s32; one MAC = one GF(2) bit product)"),
                 "frac": macs / (avg_hash_ms * 1e-3) / tc_peak,
                 "traffic": traffic,
                 "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/)",
                 "algorithmic_per_launch": f"sum_j n_j*k = {macs} bit products (owned blocks; "
                                           f"the LOP3 engine's {hash_ops} word-ops x 32)",
-                "peak_source": "measured live in this run: k_i8_peak (csrc/diag.cu), one CTA "
-                               "per SM issuing back-to-back 128x256x32 kind::i8 MMAs with the "
-                               "hash kernel's operand layouts",
+                "peak_source": ("measured live in this run: k_f4_probe mode 2 (csrc/diag.cu), "
+                                "one CTA per SM issuing back-to-back 128x256x64 kind::mxf4 "
+                                "MMAs with the hash kernel's operand layouts" if fp4 else
+                                "measured live in this run: k_i8_peak (csrc/diag.cu), one CTA "
+                                "per SM issuing back-to-back 128x256x32 kind::i8 MMAs with the "
+                                "hash kernel's operand layouts"),
                 "int_alu_equivalent": {"achieved": achieved / 1e12, "peak": peak / 1e12,
                                        "unit": "T LOP3 word-ops/s",
                                        "frac": achieved / peak,
                                        "note": "the same work counted as the north_star LOP3 "
                                                "roofline; > 1 because the tensor cores do "
-                                               "the GF(2) product ~3.6x faster than the ALUs"},
+                                               "the GF(2) product faster than the ALUs"},
                 "hbm_term_ms": hbm_ms,
             }
         else:
@@ -535,7 +551,10 @@ def main():
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": ("u8 (one GF(2) bit per byte) on tcgen05 kind::i8, s32 accumulate, parity "
+            "dtype": ("e2m1 (one GF(2) bit per element as 0 / 1.0) on tcgen05 kind::mxf4, "
+                      "f32 accumulate of exact integer counts, parity = count mod 2; bit-exact"
+                      if fp4 else
+                      "u8 (one GF(2) bit per byte) on tcgen05 kind::i8, s32 accumulate, parity "
                       "= sum mod 2; bit-exact" if tensor else
                       "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)"),
             "hash_engine": "tensor" if tensor else "lop3",

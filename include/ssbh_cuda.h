@@ -198,6 +198,10 @@ ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
 #define SSBH_ENGINE_TENSOR 2
 ssbh_status ssbh_plan_set_engine(ssbh_plan* plan, int engine);
 int ssbh_plan_engine(const ssbh_plan* plan);
+/* Name of the hash kernel a plan launches: "k_toeplitz_f4" (shared seeds, FP4 operands),
+ * "k_toeplitz_mma" (shared seeds, u8; SSBH_MMA_FP4=0), "k_toeplitz_mma_pb" (per-block
+ * seeds) or "k_toeplitz_hash" (LOP3). */
+const char* ssbh_plan_hash_kernel(const ssbh_plan* plan);
 
 /* Host-buffer entry point (what a reference caller binds): input host words (n bits),
  * out_key host words (ceil(owned*k/64)), out_lengths host (owned entries, may be NULL).
@@ -354,6 +358,14 @@ ssbh_status ssbh_measure_lop3_peak(uint32_t iters, double* lop3_per_s, double* m
  * denominator of the tensor hash engine): one CTA per SM issuing back-to-back 128x256x32
  * MMAs. layout 0 = the hash kernel's operand layouts, 1 = plain K-major tiles. */
 ssbh_status ssbh_measure_mma_i8_peak(uint32_t iters, int layout, double* macs_per_s, double* ms);
+/* FP4 roofline of the shared-seed tensor kernel: tcgen05.mma kind::mxf4 (E2M1, unit UE8M0
+ * scales) 128x256x64 back to back with the hash kernel's operand layouts. */
+ssbh_status ssbh_measure_mma_f4_peak(uint32_t iters, double* macs_per_s, double* ms);
+/* FP4 probe: mode 0 = rate (plain tiles), 1 = exactness (every MMA adds exactly 1 to every f32
+ * accumulator; *mismatches counts elements != iters after `iters` MMAs, *sample_bits = one
+ * accumulator's bits), 2 = rate with the hash kernel's layouts. */
+ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_per_s, double* ms,
+                              uint32_t* mismatches, uint32_t* sample_bits);
 /* Same with CTA pairs (cta_group::2, M = 256 across two SMs). */
 ssbh_status ssbh_measure_mma_i8_peak2(uint32_t iters, int layout, double* macs_per_s, double* ms);
 

@@ -48,7 +48,8 @@ ABI_SYMBOLS = (
     "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
     "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
-    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2",
+    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2", "ssbh_measure_mma_f4_peak",
+    "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
@@ -144,6 +145,10 @@ def _load():
     L.ssbh_plan_set_engine.argtypes = [C.c_void_p, C.c_int]
     L.ssbh_plan_engine.restype = C.c_int
     L.ssbh_plan_engine.argtypes = [C.c_void_p]
+    L.ssbh_measure_mma_f4_peak.restype = st
+    L.ssbh_measure_mma_f4_peak.argtypes = [C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ssbh_plan_hash_kernel.restype = C.c_char_p
+    L.ssbh_plan_hash_kernel.argtypes = [C.c_void_p]
     L.ssbh_measure_mma_i8_peak2.restype = st
     L.ssbh_measure_mma_i8_peak2.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                             C.POINTER(C.c_double)]
@@ -548,6 +553,11 @@ class Plan:
     def engine(self) -> int:
         return int(lib.ssbh_plan_engine(self.h))
 
+    @property
+    def hash_kernel(self) -> str:
+        """Name of the hash kernel this plan launches (k_toeplitz_f4 / _mma / _mma_pb / _hash)."""
+        return lib.ssbh_plan_hash_kernel(self.h).decode()
+
     def stream_begin(self, stream: int = 0, samp=None, hsh=None):
         sk = None if samp is None else _p64(key_of(samp))
         hk = None if hsh is None else _p64(key_of(hsh))
@@ -690,6 +700,13 @@ def measure_mma_i8_peak(iters: int = 4000, layout: int = 0, pairs: bool = False)
     r, ms = C.c_double(0), C.c_double(0)
     f = lib.ssbh_measure_mma_i8_peak2 if pairs else lib.ssbh_measure_mma_i8_peak
     _check(f(iters, layout, C.byref(r), C.byref(ms)))
+    return r.value, ms.value
+
+
+def measure_mma_f4_peak(iters: int = 200000):
+    """Measured tcgen05 kind::mxf4 MAC/s with the FP4 hash kernel's operand layouts."""
+    r, ms = C.c_double(0), C.c_double(0)
+    _check(lib.ssbh_measure_mma_f4_peak(iters, C.byref(r), C.byref(ms)))
     return r.value, ms.value
 
 

@@ -614,6 +614,13 @@ extern "C" ssbh_status ssbh_plan_set_engine(ssbh_plan* pl, int engine) {
 
 extern "C" int ssbh_plan_engine(const ssbh_plan* pl) { return pl ? pl->engine : -1; }
 
+extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
+    if (!pl) return "";
+    if (pl->engine != kEngineMma) return "k_toeplitz_hash";
+    if (pl->p.per_block_seed) return "k_toeplitz_mma_pb";
+    return mma_uses_fp4() ? "k_toeplitz_f4" : "k_toeplitz_mma";
+}
+
 extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
     if (!pl) return fail(SSBH_INVALID_ARGUMENT, "null plan");
     pl->timing = enable != 0;

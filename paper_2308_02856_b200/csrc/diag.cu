@@ -176,8 +176,10 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
     __shared__ uint32_t tslot;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+    if (mode == 2)  // hash-kernel layouts: 32 KB A tile + Hankel units after it
+        for (uint32_t i = threadIdx.x; i < 45056 / 4; i += blockDim.x) w[i] = 0x22222222u;
     for (uint32_t i = threadIdx.x; i < 4096 / 4; i += blockDim.x) w[i] = 0x22222222u;  // A
-    for (uint32_t i = threadIdx.x; i < 8192 / 4; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; mode != 2 && i < 8192 / 4; i += blockDim.x) {
         // B: row n occupies bytes (n%8)*16 + (n/8)*256 + kc*128 (kc = 0, 1); one 1.0 per row
         uint32_t v = 0x22222222u;
         if (mode == 1) {
@@ -222,9 +224,12 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
             return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
                    ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
         };
-        const uint64_t a = desc(base, 128, 256);
-        const uint64_t b = desc(base + 4096u, 128, 256);
         for (uint32_t it = 0; it < iters; ++it) {
+            const uint32_t m = it & 7;
+            const uint64_t a = mode == 2 ? desc(base + 256u * m, 128, 2048) : desc(base, 128, 256);
+            const uint64_t b = mode == 2
+                ? desc(base + 32768u + 16u * (2u * (m & 1) + 128u * (m >> 1)), 16, 128)
+                : desc(base + 4096u, 128, 256);
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
@@ -273,7 +278,8 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
 
 }  // namespace
 
-// Diagnostic for a possible FP4 engine (not used by the hash): rate (MAC/s) and exactness.
+// FP4 probe: rate (MAC/s) and exactness (modes above; mode 2 = rate with the hash kernel's
+// operand layouts, the roofline denominator of k_toeplitz_f4).
 extern "C" ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_per_s,
                                          double* ms_out, uint32_t* mismatches,
                                          uint32_t* sample_bits) {
@@ -305,6 +311,11 @@ extern "C" ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_
     if (mismatches) *mismatches = hb[0];
     if (sample_bits) *sample_bits = hb[1];
     return SSBH_OK;
+}
+
+extern "C" ssbh_status ssbh_measure_mma_f4_peak(uint32_t iters, double* macs_per_s,
+                                                double* ms_out) {
+    return ssbh_probe_mma_f4(iters, 2, macs_per_s, ms_out, nullptr, nullptr);
 }
 
 extern "C" ssbh_status ssbh_measure_mma_i8_peak2(uint32_t iters, int layout, double* macs_per_s,

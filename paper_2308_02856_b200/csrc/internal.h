@@ -237,6 +237,7 @@ struct PbHashArgs {
 PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device);
 void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
+bool mma_uses_fp4();
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
 size_t mma_hash_smem();
 void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st);

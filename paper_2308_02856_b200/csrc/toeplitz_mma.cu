@@ -1039,6 +1039,16 @@ __global__ void k_mma_tiles(const uint32_t* __restrict__ ypad, uint32_t nown,
 
 uint32_t mma_mtiles(uint32_t nown) { return (nown + kM - 1) / kM; }
 
+// FP4 (kind::mxf4) operands for shared seeds: 2x the kind::i8 MAC rate (default);
+// SSBH_MMA_FP4=0 keeps the i8 variant (dev A/B knob).
+bool mma_uses_fp4() {
+    static const int fp4 = [] {
+        const char* e = std::getenv("SSBH_MMA_FP4");
+        return e && *e == '0' ? 0 : 1;
+    }();
+    return fp4 != 0;
+}
+
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) {
     MmaGeom g{};
     g.mtiles = mma_mtiles(nown);
@@ -1090,13 +1100,7 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     MmaHashArgs a = a0;
     a.spin = spin;
     a.stage_bits = kStageK;
-    // FP4 (kind::mxf4) operands: 2x the kind::i8 MAC rate (default); SSBH_MMA_FP4=0 keeps the
-    // i8 variant (dev A/B knob)
-    static const int fp4 = [] {
-        const char* e = std::getenv("SSBH_MMA_FP4");
-        return e && *e == '0' ? 0 : 1;
-    }();
-    if (fp4) {
+    if (mma_uses_fp4()) {
         a.stage_bits = kF4StageK;
         cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kF4Smem);
