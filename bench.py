@@ -320,15 +320,14 @@ def main():
         plan.set_timing(True)
         check, close = plan.check, plan.close
     tensor = args.engine != "lop3"
-    if not tensor:
-        hash_kernel = "k_toeplitz_hash"
-    elif c["per_block"]:
-        hash_kernel = "k_toeplitz_mma_pb"
-    elif sharded:
-        hash_kernel = "k_toeplitz_mma" if os.environ.get("SSBH_MMA_FP4") == "0" else "k_toeplitz_f4"
-    else:
+    if not sharded:
         hash_kernel = plan.hash_kernel
-    fp4 = hash_kernel == "k_toeplitz_f4"
+    else:
+        i8 = os.environ.get("SSBH_MMA_FP4") == "0"
+        hash_kernel = ("k_toeplitz_hash" if not tensor else
+                       ("k_toeplitz_mma_pb<i8>" if i8 else "k_toeplitz_mma_pb<f4>")
+                       if c["per_block"] else ("k_toeplitz_mma" if i8 else "k_toeplitz_f4"))
+    fp4 = hash_kernel in ("k_toeplitz_f4", "k_toeplitz_mma_pb<f4>")
 
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
     # the tcgen05 MAC rate (kind::mxf4 or kind::i8) with the hash kernel's operand layouts

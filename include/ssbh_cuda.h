@@ -199,8 +199,8 @@ ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
 ssbh_status ssbh_plan_set_engine(ssbh_plan* plan, int engine);
 int ssbh_plan_engine(const ssbh_plan* plan);
 /* Name of the hash kernel a plan launches: "k_toeplitz_f4" (shared seeds, FP4 operands),
- * "k_toeplitz_mma" (shared seeds, u8; SSBH_MMA_FP4=0), "k_toeplitz_mma_pb" (per-block
- * seeds) or "k_toeplitz_hash" (LOP3). */
+ * "k_toeplitz_mma" (shared seeds, u8; SSBH_MMA_FP4=0), "k_toeplitz_mma_pb<f4>" /
+ * "k_toeplitz_mma_pb<i8>" (per-block seeds) or "k_toeplitz_hash" (LOP3). */
 const char* ssbh_plan_hash_kernel(const ssbh_plan* plan);
 
 /* Host-buffer entry point (what a reference caller binds): input host words (n bits),

@@ -617,7 +617,7 @@ extern "C" int ssbh_plan_engine(const ssbh_plan* pl) { return pl ? pl->engine : 
 extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
     if (!pl) return "";
     if (pl->engine != kEngineMma) return "k_toeplitz_hash";
-    if (pl->p.per_block_seed) return "k_toeplitz_mma_pb";
+    if (pl->p.per_block_seed) return mma_uses_fp4() ? "k_toeplitz_mma_pb<f4>" : "k_toeplitz_mma_pb<i8>";
     return mma_uses_fp4() ? "k_toeplitz_f4" : "k_toeplitz_mma";
 }
 
@@ -1147,7 +1147,7 @@ extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, cons
     CU(dinoff.alloc(count * 8));
     CU(dseedoff.alloc(count * 8));
     CU(ybuf.alloc(ybound * 4));
-    CU(sbuf.alloc(sbound * 4));
+    CU(sbuf.alloc((sbound + 64) * 4));  // + the tensor kernels' read-ahead of unused units
     CU(scratch.alloc((size_t)nown * kw * 4));
     const uint64_t key_w64 = words64(count * m);
     CU(key.alloc(key_w64 * 8));

@@ -809,13 +809,10 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
 constexpr int kPbWin = 256;                  // row tiles per work item (accumulator columns)
 constexpr int kPbL = 256;                    // D steps per y buffer
 constexpr int kPbUnits = 512;                // units per K-chunk plane of a y buffer
-constexpr int kPbYBytes = 8 * kPbUnits * 16; // 64 KB
 constexpr int kPbHUnits = 136;               // Hankel units per D step (128 rows + 7 + pad)
 constexpr int kPbHBytes = kPbHUnits * 16;    // 2176
 constexpr int kPbHStages = 8;
 constexpr int kPbThreads = 13 * 32;          // 4 epilogue, 1 MMA, 4 y, 4 Hankel warps
-constexpr size_t kPbBar = 2 * (size_t)kPbYBytes + (size_t)kPbHStages * kPbHBytes;
-constexpr size_t kPbSmem = kPbBar + (2 * kPbHStages + 8) * 8 + 16;
 // kind::i8, M = 128, N = 256 (same instruction descriptor as the shared kernel)
 
 struct PbItem {
@@ -835,18 +832,44 @@ __device__ __forceinline__ bool pb_decode(const PbHashArgs& a, uint32_t item, Pb
     return true;
 }
 
+// kF4: the same tiling on FP4 operands (kind::mxf4, E2M1 0 / 1.0, unit scales; 2x the MAC
+// rate). A D step is then 2 MMAs of K = 64; the y buffer has 4 K-chunk planes (position
+// kc + 4i + 32w of the 128-chunk, word w = ((y word >> kc) << 1) & 0x22222222) and the Hankel
+// unit u word w = (S' window at bit 128 D + u + 32 w) & 0x22222222. TMEM: one f32 accumulator
+// + the constant scale factors; the f32 counts are exact below 2^24, so longer rows of D
+// steps accumulate in rounds of 2^17 steps whose parities are XORed.
+// A pipeline stage is kSD consecutive D steps (8 MMAs): H_{D+1} is H_D shifted by 128 units, so
+// 128 kSD + 8 units cover all of them and the per-stage barrier work is amortised.
+template <bool kF4>
+struct PbGeo {
+    static constexpr int planes = kF4 ? 4 : 8;      // K-chunk planes of a y buffer
+    static constexpr int mmas = kF4 ? 2 : 4;        // MMAs per D step (K = 128 positions)
+    static constexpr int sd = kF4 ? 4 : 2;          // D steps per stage
+    static constexpr int hunits = 128 * sd + 8;
+    static constexpr int hbytes = hunits * 16;
+    static constexpr int ybytes = planes * kPbUnits * 16;
+    static constexpr int nacc = kF4 ? 1 : 2;
+    static constexpr size_t bar = 2 * (size_t)ybytes + (size_t)kPbHStages * hbytes;
+    static constexpr size_t smem = bar + (2 * kPbHStages + 8) * 8 + 16;
+    static_assert(kPbL % sd == 0, "stages must not straddle y buffers");
+};
+constexpr uint32_t kPbF4MaxSteps = (1u << 24) / 128;  // D steps per f32-exact round
+
+template <bool kF4>
 __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a) {
+    using G = PbGeo<kF4>;
+    constexpr uint32_t kRound = kF4 ? kPbF4MaxSteps : 0xFFFFFFFFu;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* ybufs = smem;                                  // 2 x 64 KB
-    uint8_t* hst = smem + 2 * (size_t)kPbYBytes;            // kPbHStages x 2176 B
-    uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + kPbBar);
+    uint8_t* ybufs = smem;                                  // 2 y buffers
+    uint8_t* hst = smem + 2 * (size_t)G::ybytes;            // kPbHStages x G::hbytes
+    uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + G::bar);
     uint64_t* hempty = hfull + kPbHStages;
     uint64_t* yfull = hempty + kPbHStages;
     uint64_t* yempty = yfull + 2;
     uint64_t* tfull = yempty + 2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    constexpr uint32_t M8 = 0x01010101u;
+    constexpr uint32_t M8 = 0x01010101u, M2 = 0x22222222u;
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -872,77 +895,120 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if constexpr (kF4) {
+        if (warp < kEpiWarps) {  // constant scale factors 0x7f = 2^0
+            uint32_t v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0x7F7F7F7Fu;
+            SSBH_TMEM_ST32(tmem + ((warp * 32u) << 16) + kF4SfCol, v);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
 
     if (warp < kEpiWarps) {
         // ------------------------------------------------------------------ epilogue
-        uint32_t t = 0;
-        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
+        uint32_t t = 0;  // accumulation rounds consumed
+        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
             PbItem d;
             if (!pb_decode(a, item, d)) break;
-            const uint32_t ab = t & 1;
-            mbar_wait_sleep(&tfull[ab], (t >> 1) & 1);
-            tc_fence_after();
+            const uint32_t rounds = d.nD ? (d.nD - 1) / kRound + 1 : 1;
+            uint32_t acc[kPbWin / 32];
+#pragma unroll
+            for (int q = 0; q < kPbWin / 32; ++q) acc[q] = 0;
+            for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
+                const uint32_t ab = t % G::nacc;
+                mbar_wait_sleep(&tfull[ab], (t / G::nacc) & 1);
+                tc_fence_after();
+                if (d.nD) {
+#pragma unroll 1
+                    for (int q = 0; q < kPbWin / 32; ++q) {
+                        uint32_t v[32];
+                        SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kPbWin + 32u * q, v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        uint32_t mine = 0;
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            const uint32_t bit = kF4 ? __float2uint_rz(__uint_as_float(v[e])) & 1u
+                                                     : v[e] & 1u;
+                            const uint32_t wd = __ballot_sync(0xffffffffu, bit);
+                            if (lane == (uint32_t)e) mine = wd;
+                        }
+                        acc[q] ^= mine;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[ab]);
+            }
             if (d.nD) {
                 uint32_t* dst = a.out + (unsigned long long)d.jj * a.out_stride;
 #pragma unroll 1
                 for (int q = 0; q < kPbWin / 32; ++q) {
-                    uint32_t v[32];
-                    SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kPbWin + 32u * q, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    uint32_t mine = 0;
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const uint32_t wd = __ballot_sync(0xffffffffu, v[e] & 1u);
-                        if (lane == (uint32_t)e) mine = wd;
-                    }
                     const uint32_t n = 32u * q + lane;
                     const uint32_t word = 4u * (d.I0 + n) + warp;  // rows 128 I + 32 warp ..
-                    if (n < d.ncols && word < a.kw) dst[word] = mine;
+                    if (n < d.ncols && word < a.kw) dst[word] = acc[q];
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ab]);
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------------ MMA issuer
         uint32_t hs = 0, yb = 0, t = 0;
         const uint32_t ybase = smem_u32(ybufs), hbase = smem_u32(hst);
-        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
+        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
             PbItem d;
             if (!pb_decode(a, item, d)) break;
-            const uint32_t ab = t & 1;
-            if (t >= 2) mbar_wait_sleep(&tempty[ab], ((t >> 1) - 1) & 1);
-            tc_fence_after();
             if (d.nD == 0) {
+                const uint32_t ab = t % G::nacc;
+                if (t >= (uint32_t)G::nacc) mbar_wait_sleep(&tempty[ab], ((t / G::nacc) - 1) & 1);
                 if (lane == 0) mbar_arrive(&tfull[ab]);
+                ++t;
                 continue;
             }
+            uint32_t ab = 0, round_end = 0;
             for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
+                if (D0 % kRound == 0) {  // a new accumulation round (kRound is a multiple of kPbL)
+                    ab = t % G::nacc;
+                    if (t >= (uint32_t)G::nacc) mbar_wait_sleep(&tempty[ab], ((t / G::nacc) - 1) & 1);
+                    tc_fence_after();
+                    round_end = kF4 ? min(d.nD, D0 + kRound) : d.nD;
+                }
                 const uint32_t b = yb & 1;
                 mbar_wait(&yfull[b], (yb >> 1) & 1);
                 tc_fence_after();
                 const uint32_t steps = min((uint32_t)kPbL, d.nD - D0);
-                for (uint32_t s = 0; s < steps; ++s, ++hs) {
+                for (uint32_t sb = 0; sb < steps; sb += G::sd, ++hs) {
                     const uint32_t slot = hs % kPbHStages;
                     mbar_wait(&hfull[slot], (hs / kPbHStages) & 1);
                     tc_fence_after();
+                    const uint32_t nst = min((uint32_t)G::sd, steps - sb);
                     if (lane == 0) {
-                        const uint32_t ha = hbase + slot * kPbHBytes;
-                        // column n of step D0+s is unit (kPbL - 1 - s) + n of the buffer
-                        const uint32_t ya = ybase + b * kPbYBytes + 16u * (kPbL - 1 - s);
+                        const uint32_t ha = hbase + slot * G::hbytes;
+                        for (uint32_t j = 0; j < nst; ++j) {
+                            const uint32_t s = sb + j;
+                            // column n of step D0+s is unit (kPbL - 1 - s) + n of the buffer;
+                            // H of step j of the stage starts at unit 128 j
+                            const uint32_t ya = ybase + b * G::ybytes + 16u * (kPbL - 1 - s);
+                            const uint32_t first = (D0 % kRound) | s;
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const uint64_t adesc = sdesc(ha + 32u * m, 16, 128);
-                            const uint64_t bdesc = sdesc(ya + 2u * m * (kPbUnits * 16), kPbUnits * 16, 128);
-                            mma_i8(tmem + ab * kPbWin, adesc, bdesc, (D0 | s | (uint32_t)m) != 0);
+                            for (int m = 0; m < G::mmas; ++m) {
+                                const uint64_t adesc = sdesc(ha + 2048u * j + 32u * m, 16, 128);
+                                const uint64_t bdesc = sdesc(ya + 2u * m * (kPbUnits * 16), kPbUnits * 16, 128);
+                                if constexpr (kF4)
+                                    mma_f4(tmem, adesc, bdesc, tmem + kF4SfCol, (first | (uint32_t)m) != 0);
+                                else
+                                    mma_i8(tmem + ab * kPbWin, adesc, bdesc, (first | (uint32_t)m) != 0);
+                            }
                         }
                         mma_commit(&hempty[slot]);
-                        if (s + 1 == steps) mma_commit(&yempty[b]);
-                        if (D0 + s + 1 == d.nD) mma_commit(&tfull[ab]);
+                        if (sb + nst == steps) mma_commit(&yempty[b]);
+                        if (D0 + sb + nst == round_end) mma_commit(&tfull[ab]);
                     }
                     __syncwarp();
                 }
+                if (D0 + steps == round_end) ++t;
             }
         }
     } else if (warp < kProdWarp0 + 4) {
@@ -956,7 +1022,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
             for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
                 const uint32_t b = yb & 1;
                 if (yb >= 2) mbar_wait_sleep(&yempty[b], ((yb >> 1) - 1) & 1);
-                uint8_t* buf = ybufs + b * kPbYBytes;
+                uint8_t* buf = ybufs + b * G::ybytes;
                 // unit P holds chunk C = D0 + kPbL - 1 - P (the buffer's D steps D0 .. +255
                 // read units kPbL - 1 - s + n, n < 256)
 #pragma unroll 1
@@ -965,10 +1031,14 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                     uint4 x = make_uint4(0, 0, 0, 0);
                     if (C >= 0 && C < (int64_t)d.nC) x = __ldg(reinterpret_cast<const uint4*>(y) + C);
 #pragma unroll
-                    for (int kc = 0; kc < 8; ++kc)
+                    for (int kc = 0; kc < G::planes; ++kc) {
+                        auto f = [&](uint32_t v) {
+                            if constexpr (kF4) return (kc ? v >> (kc - 1) : v << 1) & M2;
+                            else return (v >> kc) & M8;
+                        };
                         *reinterpret_cast<uint4*>(buf + (kc * kPbUnits + P) * 16) =
-                            make_uint4((x.x >> kc) & M8, (x.y >> kc) & M8, (x.z >> kc) & M8,
-                                       (x.w >> kc) & M8);
+                            make_uint4(f(x.x), f(x.y), f(x.z), f(x.w));
+                    }
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -983,24 +1053,28 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
             PbItem d;
             if (!pb_decode(a, item, d)) break;
             const uint32_t* sw = a.sbuf + a.lay.soff[d.jj];  // pre-shifted: S'[b + 1] = S[b]
-            for (uint32_t s = 0; s < d.nD; ++s, ++hs) {
+            // stages never straddle y buffers: kSD steps from every multiple of kSD
+            for (uint32_t s = 0; s < d.nD; s += G::sd, ++hs) {
                 const uint32_t slot = hs % kPbHStages;
                 if (hs >= (uint32_t)kPbHStages)
                     mbar_wait_sleep(&hempty[slot], ((hs / kPbHStages) - 1) & 1);
-                // step s of the item is D = I0 + s - (kPbL... ) : D = I0 + s (C = D - I0 - n)
+                // D = I0 + s (column n reads chunk C = D - I0 - n)
                 const uint64_t wbase = 4ull * (d.I0 + s);  // word of S' bit 128 D
-                uint8_t* hsm = hst + slot * kPbHBytes;
+                uint8_t* hsm = hst + slot * G::hbytes;
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
+                for (int r = 0; r < (G::hunits + 127) / 128; ++r) {
                     const uint32_t u = ht + 128u * r;
-                    if (u < (uint32_t)kPbHUnits) {
-                        const uint32_t rel = u + 1, q = rel >> 5, sh = rel & 31;
+                    if (u < (uint32_t)G::hunits) {
+                        // i8: S bit 128D + u + 32w + 8b at bit 8b (S' window one bit up);
+                        // f4: S bit 128D + u + 32w + 4i at bit 4i + 1 (S' window at the bit)
+                        const uint32_t rel = kF4 ? u : u + 1, q = rel >> 5, sh = rel & 31;
+                        const uint32_t mk = kF4 ? M2 : M8;
                         const uint32_t* p = sw + wbase + q;
                         const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2),
                                        w3 = __ldg(p + 3), w4 = __ldg(p + 4);
                         *reinterpret_cast<uint4*>(hsm + 16 * u) = make_uint4(
-                            __funnelshift_r(w0, w1, sh) & M8, __funnelshift_r(w1, w2, sh) & M8,
-                            __funnelshift_r(w2, w3, sh) & M8, __funnelshift_r(w3, w4, sh) & M8);
+                            __funnelshift_r(w0, w1, sh) & mk, __funnelshift_r(w1, w2, sh) & mk,
+                            __funnelshift_r(w2, w3, sh) & mk, __funnelshift_r(w3, w4, sh) & mk);
                     }
                 }
                 fence_proxy_async_smem();
@@ -1078,10 +1152,16 @@ PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device) {
 
 void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st) {
     if (!a.nown || !g.items) return;
-    cudaFuncSetAttribute(k_toeplitz_mma_pb, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kPbSmem);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
-    k_toeplitz_mma_pb<<<grid, kPbThreads, kPbSmem, st>>>(a);
+    if (mma_uses_fp4()) {
+        cudaFuncSetAttribute(k_toeplitz_mma_pb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)PbGeo<true>::smem);
+        k_toeplitz_mma_pb<true><<<grid, kPbThreads, PbGeo<true>::smem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_toeplitz_mma_pb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)PbGeo<false>::smem);
+        k_toeplitz_mma_pb<false><<<grid, kPbThreads, PbGeo<false>::smem, st>>>(a);
+    }
 }
 
 size_t mma_hash_smem() { return Geo<true, 2>::smem; }
