@@ -521,9 +521,9 @@ constexpr int kF4Stages = 4;
 constexpr int kF4Pre = 2;                         // cp.async prefetch depth per set
 constexpr int kF4RawY = kF4Pre * kM * 64;         // per set
 constexpr int kF4RawS = 4 * kF4Pre * 128;         // per set
-constexpr size_t kF4Bar = (size_t)kF4Stages * kF4Slot + 2 * (kF4RawY + kF4RawS);
-constexpr size_t kF4Smem = kF4Bar + (2 * kF4Stages + 4) * 8 + 16;
-static_assert(kF4Smem <= 232448, "f4 smem budget");
+__host__ __device__ constexpr size_t f4_bar(int sets) { return (size_t)kF4Stages * kF4Slot + sets * (kF4RawY + kF4RawS); }
+__host__ __device__ constexpr size_t f4_smem(int sets) { return f4_bar(sets) + (2 * kF4Stages + 4) * 8 + 16; }
+static_assert(f4_smem(3) <= 232448, "f4 smem budget");
 constexpr uint32_t kF4MaxStages = (1u << 24) / kF4StageK;  // exact f32 counts per round
 constexpr uint32_t kF4SfCol = kN;                            // scale factors: columns 256..287
 // kind::mxf4 instruction descriptor: E2M1 x E2M1, UE8M0 scales, K-major, M = 128, N = 256
@@ -558,14 +558,15 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
     for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
 }
 
-__global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a) {
+template <int kSets>
+__global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashArgs a) {
     constexpr int kS = kF4Stages;
     constexpr uint32_t M2 = 0x22222222u;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* slots = smem;
     uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kS * kF4Slot);
-    uint32_t* raw_s = raw_y + 2 * (kF4RawY / 4);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kF4Bar);
+    uint32_t* raw_s = raw_y + kSets * (kF4RawY / 4);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + f4_bar(kSets));
     uint64_t* empty = full + kS;
     uint64_t* tfull = empty + kS;
     uint64_t* tempty = tfull + 2;
@@ -694,10 +695,10 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
         for (int i = 0; i < kF4Pre; ++i) {
             y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
             cp_async_commit();
-            pre.advance(a, 2);
+            pre.advance(a, kSets);
         }
         const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
-        for (uint32_t g = set, i = 0; cur.valid; g += 2, ++i, cur.advance(a, 2)) {
+        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
             uint4 x[4];
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
             if (lane == 0) mbar_arrive(&full[slot]);
             y_prefetch_f4(a, pre, jl, raw + rs * kM * 16);
             cp_async_commit();
-            pre.advance(a, 2);
+            pre.advance(a, kSets);
         }
         cp_async_wait<0>();
     } else {
@@ -738,9 +739,9 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
         for (int i = 0; i < kF4Pre; ++i) {
             s_prefetch(a, pre, lane, raw + i * 32);
             cp_async_commit();
-            pre.advance(a, 2);
+            pre.advance(a, kSets);
         }
-        for (uint32_t g = set, i = 0; cur.valid; g += 2, ++i, cur.advance(a, 2)) {
+        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
             __syncwarp();
@@ -771,7 +772,7 @@ __global__ void __launch_bounds__(threads_for(2), 1) k_toeplitz_f4(MmaHashArgs a
             if (lane == 0) mbar_arrive(&full[slot]);
             s_prefetch(a, pre, lane, raw + rs * 32);
             cp_async_commit();
-            pre.advance(a, 2);
+            pre.advance(a, kSets);
         }
         cp_async_wait<0>();
     }
@@ -1182,9 +1183,20 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     a.stage_bits = kStageK;
     if (mma_uses_fp4()) {
         a.stage_bits = kF4StageK;
-        cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kF4Smem);
-        k_toeplitz_f4<<<grid, threads_for(2), kF4Smem, st>>>(a);
+        // producer sets (dev A/B knob SSBH_MMA_F4_SETS=2|3)
+        static const int sets = [] {
+            const char* e = std::getenv("SSBH_MMA_F4_SETS");
+            return e && *e == '2' ? 2 : 3;
+        }();
+        if (sets == 2) {
+            cudaFuncSetAttribute(k_toeplitz_f4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)f4_smem(2));
+            k_toeplitz_f4<2><<<grid, threads_for(2), f4_smem(2), st>>>(a);
+        } else {
+            cudaFuncSetAttribute(k_toeplitz_f4<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)f4_smem(3));
+            k_toeplitz_f4<3><<<grid, threads_for(3), f4_smem(3), st>>>(a);
+        }
         return;
     }
     // dev A/B knobs: SSBH_MMA_ATMEM=0 stages A in shared memory (one producer set);
