@@ -1183,10 +1183,10 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     a.stage_bits = kStageK;
     if (mma_uses_fp4()) {
         a.stage_bits = kF4StageK;
-        // producer sets (dev A/B knob SSBH_MMA_F4_SETS=2|3)
+        // producer sets (dev A/B knob SSBH_MMA_F4_SETS=2|3; default 2)
         static const int sets = [] {
             const char* e = std::getenv("SSBH_MMA_F4_SETS");
-            return e && *e == '2' ? 2 : 3;
+            return e && *e == '3' ? 3 : 2;  // 3 sets measured no faster (157-158 ms)
         }();
         if (sets == 2) {
             cudaFuncSetAttribute(k_toeplitz_f4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
