@@ -387,6 +387,7 @@ struct ssbh_plan {
     int engine = kEngineLop3;
     MmaGeom mma{};
     PbGeom pb{};
+    bool shared_pb = false;  // shared seed hashed by the tiled matrix-vector kernel (long blocks)
     DBuf mt_words;
     // host-path staging
     DBuf d_input, d_key, d_len, d_keep;
@@ -460,6 +461,16 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     pl->engine = default_engine(params->per_block_seed);
     pl->mma = make_mma_geom(nown, pl->kw, n / params->n_subblocks, pl->device);
     pl->pb = make_pb_geom(nown, pl->kw, pl->device);
+    // Long shared-seed blocks: the tiled matrix-vector kernel keeps each block's y chunks in
+    // shared memory for 256 D steps instead of re-expanding them for every 256-row tile (config
+    // 3: hash 155 -> 145 ms); its window ramp (255 D steps per item) costs < 5 % once the mean
+    // block has > 620 K bits. SSBH_MMA_SHARED_PB=0/1 overrides (dev A/B knob).
+    {
+        const char* e = std::getenv("SSBH_MMA_SHARED_PB");
+        const uint64_t mean_nj = n / params->n_subblocks;
+        pl->shared_pb = !params->per_block_seed &&
+                        (e && *e ? *e == '1' : mean_nj >= (uint64_t)620000);
+    }
 
     // two-level split for large key spaces (SSBH_BUCKETS=0 disables it, =1 forces it)
     const char* be = std::getenv("SSBH_BUCKETS");
@@ -617,7 +628,8 @@ extern "C" int ssbh_plan_engine(const ssbh_plan* pl) { return pl ? pl->engine : 
 extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
     if (!pl) return "";
     if (pl->engine != kEngineMma) return "k_toeplitz_hash";
-    if (pl->p.per_block_seed) return mma_uses_fp4() ? "k_toeplitz_mma_pb<f4>" : "k_toeplitz_mma_pb<i8>";
+    if (pl->p.per_block_seed || pl->shared_pb)
+        return mma_uses_fp4() ? "k_toeplitz_mma_pb<f4>" : "k_toeplitz_mma_pb<i8>";
     return mma_uses_fp4() ? "k_toeplitz_f4" : "k_toeplitz_mma";
 }
 
@@ -724,7 +736,7 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
     const Layout lay = pl->lay.view();
     uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
     CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
-    if (pl->engine == kEngineMma && pl->p.per_block_seed) {
+    if (pl->engine == kEngineMma && (pl->p.per_block_seed || pl->shared_pb)) {
         PbHashArgs m{};
         m.ybuf = pl->ybuf.as<uint32_t>();
         m.sbuf = pl->sbuf.as<uint32_t>();

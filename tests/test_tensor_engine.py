@@ -68,6 +68,22 @@ def test_tensor_engine_all_ones_input(dev, oracle):
         assert (got == want).all(), (n, s, k)
 
 
+def test_shared_seed_long_blocks_use_the_tiled_kernel(dev, oracle):
+    """Shared seeds with long blocks (mean n_j >= 620 K bits) run the tiled matrix-vector kernel
+    (y chunks reused for 256 D steps) instead of the all-blocks GEMM; same key."""
+    n, s, k = 1 << 22, 4, 4096
+    x = oracle.make_input(13, 0.5, n)
+    want, _ = oracle.extract(x, n, s, 9, 10, 0, k)
+    plan = dev.Plan(n, s, k, 9, 10)
+    assert plan.hash_kernel.startswith("k_toeplitz_mma_pb")
+    got, _, _ = plan.run_host(x)
+    plan.close()
+    assert (got == want).all()
+    plan = dev.Plan(1 << 20, 64, 8192, 2, 3)  # config 1: short blocks keep the GEMM kernel
+    assert plan.hash_kernel in ("k_toeplitz_f4", "k_toeplitz_mma")
+    plan.close()
+
+
 def test_tensor_engine_block_longer_than_2p24(dev, oracle):
     """A shared-seed block of more than 2^24 input bits: the FP4 variant's f32 accumulator
     counts exactly only below 2^24, so such items accumulate in rounds whose parities XOR."""
