@@ -21,7 +21,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libssbh_cuda.so")
+# SSBH_CUDA_LIB: dev A/B of an alternative build of the same library (tools/); default in-tree
+LIB_PATH = os.environ.get("SSBH_CUDA_LIB") or os.path.join(HERE, "libssbh_cuda.so")
 CXX_LIB_PATH = os.path.join(HERE, "libssbh.so")
 
 U64P = C.POINTER(C.c_uint64)

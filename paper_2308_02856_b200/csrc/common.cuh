@@ -31,11 +31,31 @@ SSBH_HD void threefry_ks(const uint64_t key[4], uint64_t ks[5]) {
     ks[4] = 0x1BD11BDAA9FC1A22ull ^ key[0] ^ key[1] ^ key[2] ^ key[3];
 }
 
+// SSBH_TF_IMAD (dev A/B build): 64-bit adds as IMAD.WIDE.U32 + IMAD on the FMA pipe (the
+// Threefry pass is ALU-bound on the rotations and XORs).
+#if defined(SSBH_TF_IMAD)
+static __constant__ uint32_t c_tf_one = 1;
+#endif
+#if defined(__CUDA_ARCH__) && defined(SSBH_TF_IMAD)
+__device__ __forceinline__ uint64_t tf_add(uint64_t a, uint64_t b) {
+    const uint32_t one = c_tf_one;
+    uint64_t t;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(t) : "r"((uint32_t)a), "r"(one), "l"(b));
+    uint32_t hi;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"((uint32_t)(a >> 32)), "r"(one),
+        "r"((uint32_t)(t >> 32)));
+    return ((uint64_t)hi << 32) | (uint32_t)t;
+}
+#define SSBH_ADD(a, b) tf_add((a), (b))
+#else
+#define SSBH_ADD(a, b) ((a) + (b))
+#endif
+
 #define SSBH_TF_ROUND(RA, RB)                         \
     do {                                              \
-        x0 += x1;                                     \
+        x0 = SSBH_ADD(x0, x1);                        \
         x1 = rotl<RA>(x1) ^ x0;                       \
-        x2 += x3;                                     \
+        x2 = SSBH_ADD(x2, x3);                        \
         x3 = rotl<RB>(x3) ^ x2;                       \
         const uint64_t t_ = x1;                       \
         x1 = x3;                                      \
@@ -44,10 +64,10 @@ SSBH_HD void threefry_ks(const uint64_t key[4], uint64_t ks[5]) {
 
 #define SSBH_TF_INJECT(S)                             \
     do {                                              \
-        x0 += ks[(S) % 5];                            \
-        x1 += ks[((S) + 1) % 5];                      \
-        x2 += ks[((S) + 2) % 5];                      \
-        x3 += ks[((S) + 3) % 5] + (uint64_t)(S);      \
+        x0 = SSBH_ADD(x0, ks[(S) % 5]);               \
+        x1 = SSBH_ADD(x1, ks[((S) + 1) % 5]);         \
+        x2 = SSBH_ADD(x2, ks[((S) + 2) % 5]);         \
+        x3 = SSBH_ADD(x3, ks[((S) + 3) % 5] + (uint64_t)(S)); \
     } while (0)
 
 SSBH_HD U64x4 threefry(const uint64_t ks[5], uint64_t c0, uint64_t c1, uint64_t c2,

@@ -810,8 +810,6 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
 constexpr int kPbWin = 256;                  // row tiles per work item (accumulator columns)
 constexpr int kPbL = 256;                    // D steps per y buffer
 constexpr int kPbUnits = 512;                // units per K-chunk plane of a y buffer
-constexpr int kPbHUnits = 136;               // Hankel units per D step (128 rows + 7 + pad)
-constexpr int kPbHBytes = kPbHUnits * 16;    // 2176
 constexpr int kPbHStages = 8;
 constexpr int kPbThreads = 13 * 32;          // 4 epilogue, 1 MMA, 4 y, 4 Hankel warps
 // kind::i8, M = 128, N = 256 (same instruction descriptor as the shared kernel)
