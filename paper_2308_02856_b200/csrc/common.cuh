@@ -31,25 +31,9 @@ SSBH_HD void threefry_ks(const uint64_t key[4], uint64_t ks[5]) {
     ks[4] = 0x1BD11BDAA9FC1A22ull ^ key[0] ^ key[1] ^ key[2] ^ key[3];
 }
 
-// SSBH_TF_IMAD (dev A/B build): 64-bit adds as IMAD.WIDE.U32 + IMAD on the FMA pipe (the
-// Threefry pass is ALU-bound on the rotations and XORs).
-#if defined(SSBH_TF_IMAD)
-static __constant__ uint32_t c_tf_one = 1;
-#endif
-#if defined(__CUDA_ARCH__) && defined(SSBH_TF_IMAD)
-__device__ __forceinline__ uint64_t tf_add(uint64_t a, uint64_t b) {
-    const uint32_t one = c_tf_one;
-    uint64_t t;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(t) : "r"((uint32_t)a), "r"(one), "l"(b));
-    uint32_t hi;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"((uint32_t)(a >> 32)), "r"(one),
-        "r"((uint32_t)(t >> 32)));
-    return ((uint64_t)hi << 32) | (uint32_t)t;
-}
-#define SSBH_ADD(a, b) tf_add((a), (b))
-#else
+// 64-bit adds stay IADD3 pairs: moving them to the FMA pipe (IMAD.WIDE.U32 + IMAD, a dev A/B
+// build) made the Threefry count pass slower (config 3: 14.9 -> 19.2 ms).
 #define SSBH_ADD(a, b) ((a) + (b))
-#endif
 
 #define SSBH_TF_ROUND(RA, RB)                         \
     do {                                              \
