@@ -1129,12 +1129,27 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     g.grid = sms;
-    const uint64_t mean_stages = std::max<uint64_t>(1, (mean_nj + kStageK - 1) / kStageK);
+    // K split: the smallest split whose item count leaves the last wave >= 90 % full (or gives
+    // >= 8 waves), keeping >= 8 stages per part (FP4 stages are 512 positions)
+    const uint64_t stage_bits = mma_uses_fp4() ? 512 : kStageK;
+    const uint64_t mean_stages = std::max<uint64_t>(1, (mean_nj + stage_bits - 1) / stage_bits);
+    const uint64_t base = (uint64_t)g.mtiles * g.ntiles;
     g.ksplit = 1;
-    while ((uint64_t)g.mtiles * g.ntiles * g.ksplit < 2ull * sms &&
-           mean_stages / (2ull * g.ksplit) >= 8)
-        g.ksplit *= 2;
-    g.items = (uint64_t)g.mtiles * g.ntiles * g.ksplit;
+    static const uint32_t forced = [] {  // dev knob SSBH_MMA_KSPLIT
+        const char* e = std::getenv("SSBH_MMA_KSPLIT");
+        return e ? (uint32_t)std::strtoul(e, nullptr, 10) : 0u;
+    }();
+    if (forced) {
+        g.ksplit = forced;
+    } else {
+        for (uint32_t ks = 1; ks <= 16; ++ks) {
+            if (ks > 1 && mean_stages / ks < 8) break;
+            g.ksplit = ks;
+            const uint64_t items = base * ks, waves = (items + sms - 1) / sms;
+            if (waves >= 8 || (double)items / (double)(waves * sms) >= 0.9) break;
+        }
+    }
+    g.items = base * g.ksplit;
     return g;
 }
 
