@@ -58,7 +58,7 @@ def config_dict(cid, c, world):
     return {
         "workload": f"config{cid}: n={log2s(c['n'])} rounds, s={c['s']} sub-blocks, "
                     f"k={c['k']} out bits/sub-block, p={c['p']} ({cfg_desc(cid, c)})"
-                    + (" [n OVERRIDDEN by --rounds: not a BASELINE shape]"
+                    + (" [n/k OVERRIDDEN by --rounds/--out-bits: not a BASELINE shape]"
                        if c.get("rounds_override") else ""),
         "n_bits": c["n"], "n_subblocks": c["s"], "out_bits_per_block": c["k"], "p": c["p"],
         "seed_mode": "per-block (hash-seed sub=j)" if c["per_block"] else "shared (hash-seed sub=0)",
@@ -252,6 +252,8 @@ def main():
                     help="skip the extra LOP3-engine step reported beside a tensor-engine line")
     ap.add_argument("--rounds", type=int, default=0,
                     help="testing aid: override n (the line's config then names the override)")
+    ap.add_argument("--out-bits", type=int, default=0,
+                    help="testing aid: override k (the line's config then names the override)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -264,6 +266,9 @@ def main():
     c = dict(P.CONFIGS[cid])
     if args.rounds:
         c["n"] = args.rounds
+        c["rounds_override"] = True
+    if args.out_bits:
+        c["k"] = args.out_bits
         c["rounds_override"] = True
     if args.impl == "reference":
         if rank == 0:
