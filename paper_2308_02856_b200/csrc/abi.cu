@@ -389,8 +389,13 @@ struct ssbh_plan {
     PbGeom pb{};
     bool shared_pb = false;  // shared seed hashed by the tiled matrix-vector kernel (long blocks)
     DBuf mt_words;
-    // host-path staging
+    // host-path staging; late input: during a host run the input is copied on copy_stream while
+    // the count pass (which needs only the round indices) runs, and the passes that read the
+    // data bits wait for late_ev
     DBuf d_input, d_key, d_len, d_keep;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t late_ev = nullptr, prev_ev = nullptr;
+    const uint32_t* late_input = nullptr;
     cudaStream_t own_stream = nullptr;
     uint64_t bytes = 0;
 };
@@ -599,6 +604,9 @@ extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
         if (e) cudaEventDestroy(e);
     if (pl->h_stats) cudaFreeHost(pl->h_stats);
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
+    if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
+    if (pl->late_ev) cudaEventDestroy(pl->late_ev);
+    if (pl->prev_ev) cudaEventDestroy(pl->prev_ev);
     for (auto x : pl->exec)
         if (x) cudaGraphExecDestroy(x);
     delete pl;
@@ -669,8 +677,10 @@ static ssbh_status bucket_passes(ssbh_plan* pl, const SamplerGeom& ga, const uin
     launch_scan(with_keys(ga, bg.nbuckets), pl->counts_a.as<uint32_t>(),
                 pl->gsum_a.as<unsigned long long>(), pl->tot_a.as<unsigned long long>(), st);
     CU(cudaMemsetAsync(pl->staging.p, 0xff, pl->staging.bytes, st));
+    if (pl->late_input) CU(cudaStreamWaitEvent(st, pl->late_ev, 0));
     launch_bucket_split(bg, ga, d_payload_src, pl->counts_a.as<uint32_t>(),
-                        pl->tot_a.as<unsigned long long>(), pl->staging.as<uint16_t>(), flags, st);
+                        pl->tot_a.as<unsigned long long>(), pl->staging.as<uint16_t>(), flags, st,
+                        pl->late_input);
     CU(cudaMemsetAsync(pl->counts_b.p, 0, pl->counts_b.bytes, st));
     launch_bucket_count(bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(), st);
     launch_scan(bg.b, pl->counts_b.as<uint32_t>(), pl->gsum_b.as<unsigned long long>(),
@@ -684,6 +694,7 @@ static ssbh_status seg_sample(ssbh_plan* pl, const uint32_t* d_input, const uint
     const Layout lay = pl->lay.view();
     if (pl->bucketed || pl->streaming)
         CU(cudaMemsetAsync(&lay.stats->pad, 0, 4, st));  // kFlagBucketOverflow of this run
+    if (pl->late_input) d_input = nullptr;  // the data bits join in the split / scatter
     if (pl->bucketed && !pl->streaming) {
         if (auto s = bucket_passes(pl, pl->bg.a, sk, 0, d_input, d_keep, nullptr, st, launches))
             return s;
@@ -717,8 +728,9 @@ static ssbh_status seg_scatter(ssbh_plan* pl, cudaStream_t st, uint32_t& launche
         launches += 1;
         return SSBH_OK;
     }
+    if (pl->late_input) CU(cudaStreamWaitEvent(st, pl->late_ev, 0));
     launch_scatter(pl->geom, pl->payload.p, pl->counts.as<uint32_t>(), lay.nj, lay.yoff,
-                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st);
+                   pl->ybuf.as<uint32_t>(), nullptr, nullptr, st, pl->late_input);
     launches += 1;
     return SSBH_OK;
 }
@@ -993,14 +1005,39 @@ extern "C" ssbh_status ssbh_plan_run_host_sifted(ssbh_plan* pl, const uint64_t* 
     }
     if (keep && !pl->d_keep.p) CU(pl->d_keep.alloc(in_w64 * 8 + 16));
     cudaStream_t st = pl->own_stream;
-    CU(cudaMemcpyAsync(pl->d_input.p, input, in_w64 * 8, cudaMemcpyHostToDevice, st));
-    if (keep) CU(cudaMemcpyAsync(pl->d_keep.p, keep, in_w64 * 8, cudaMemcpyHostToDevice, st));
+    // large inputs without a keep mask: copy the input on a second stream while the count pass
+    // runs (it needs only the round indices); the split / scatter wait for the copy
+    const bool late = !keep && pl->p.n_rounds >= (1ull << 26);
+    if (late) {
+        if (!pl->copy_stream) {
+            CU(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&pl->late_ev, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&pl->prev_ev, cudaEventDisableTiming));
+        }
+        CU(cudaEventRecord(pl->prev_ev, st));  // the previous run is done with d_input
+        CU(cudaStreamWaitEvent(pl->copy_stream, pl->prev_ev, 0));
+        CU(cudaMemcpyAsync(pl->d_input.p, input, in_w64 * 8, cudaMemcpyHostToDevice,
+                           pl->copy_stream));
+        CU(cudaEventRecord(pl->late_ev, pl->copy_stream));
+    } else {
+        CU(cudaMemcpyAsync(pl->d_input.p, input, in_w64 * 8, cudaMemcpyHostToDevice, st));
+        if (keep) CU(cudaMemcpyAsync(pl->d_keep.p, keep, in_w64 * 8, cudaMemcpyHostToDevice, st));
+    }
     // the key buffer's last u32 of an odd word count must read as zero in the u64 view
     if ((pl->key_words32 & 1) != 0) CU(cudaMemsetAsync(pl->d_key.p, 0, key_w64 * 8, st));
-    if (auto s = ssbh_plan_run_device_sifted(pl, pl->d_input.as<uint32_t>(),
-                                             keep ? pl->d_keep.as<uint32_t>() : nullptr,
-                                             pl->d_key.as<uint32_t>(), pl->d_len.as<uint64_t>(),
-                                             nullptr, nullptr, st))
+    if (late) {  // direct launches: the cross-stream wait is not part of a captured graph
+        pl->late_input = pl->d_input.as<uint32_t>();
+        pl->last_stream = st;
+        const RunArgs r{pl->d_input.as<uint32_t>(), nullptr, pl->d_key.as<uint32_t>(),
+                        pl->d_len.as<uint64_t>(), pl->p.samp_key, pl->p.hash_key};
+        const ssbh_status s = plan_enqueue(pl, r, st);
+        pl->late_input = nullptr;
+        if (s) return s;
+    } else if (auto s = ssbh_plan_run_device_sifted(pl, pl->d_input.as<uint32_t>(),
+                                                    keep ? pl->d_keep.as<uint32_t>() : nullptr,
+                                                    pl->d_key.as<uint32_t>(),
+                                                    pl->d_len.as<uint64_t>(), nullptr, nullptr,
+                                                    st))
         return s;
     if (auto s = ssbh_plan_check(pl, stats)) return s;
     CU(cudaMemcpyAsync(out_key, pl->d_key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));

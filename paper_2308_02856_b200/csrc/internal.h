@@ -103,10 +103,12 @@ void launch_scan(const SamplerGeom& g, uint32_t* d_counts, unsigned long long* d
                  unsigned long long* d_nj, cudaStream_t st, uint64_t seg_groups = 0);
 // Pass 3: stable scatter. ybuf mode: reversed bit pack into ybuf (pre-zeroed);
 // index mode (d_idx_out != null): CSR indices at csr_off[jj] + rank.
+// d_in32_late: the payload holds V only; the data bits are read from these input words.
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
                     const unsigned long long* d_nj, const unsigned long long* d_yoff,
                     uint32_t* d_ybuf, unsigned long long* d_idx_out,
-                    const unsigned long long* d_csr_off, cudaStream_t st);
+                    const unsigned long long* d_csr_off, cudaStream_t st,
+                    const uint32_t* d_in32_late = nullptr);
 // Pass 3 for streaming plans: rounds [first, first+count) whose data bits are d_chunk32
 // (bit 0 = round `first`); V recomputed by Threefry (no payload). `first` and the chunk end
 // (unless it is n) must be multiples of the warp-chunk.
@@ -167,7 +169,8 @@ void launch_sample_buckets(const BucketGeom& bg, const SamplerGeom& ga, const ui
 // pass-A table; a full region raises kFlagBucketOverflow in *d_flags.
 void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void* d_payload,
                          uint32_t* d_offsets_a, const unsigned long long* d_tot_a,
-                         uint16_t* d_staging, uint32_t* d_flags, cudaStream_t st);
+                         uint16_t* d_staging, uint32_t* d_flags, cudaStream_t st,
+                         const uint32_t* d_in32_late = nullptr);
 // Pass B counts over the staging regions (empty slots hold 0xffff).
 void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_counts_b,
                          cudaStream_t st);

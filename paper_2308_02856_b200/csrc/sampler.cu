@@ -298,7 +298,14 @@ template <typename P>
 struct PayloadSrc {
     using Bits = PayloadBits<P>;
     const P* __restrict__ payload;
-    __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return payload[i]; }
+    // non-null: the payload carries V only and the data bit comes from the input words (the
+    // host path copies the input while the count pass runs, which does not need it)
+    const uint32_t* __restrict__ in32 = nullptr;
+    __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+        uint32_t v = payload[i];
+        if (in32) v |= ((__ldg(in32 + (i >> 5)) >> (i & 31)) & 1u) << Bits::kDataShift;
+        return v;
+    }
 };
 
 struct StreamSrc {
@@ -855,7 +862,8 @@ BucketGeom make_bucket_geom(uint64_t n_src, uint64_t s, uint32_t j_lo, uint32_t 
 
 void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void* d_payload,
                          uint32_t* d_offsets_a, const unsigned long long* d_tot_a,
-                         uint16_t* d_staging, uint32_t* d_flags, cudaStream_t st) {
+                         uint16_t* d_staging, uint32_t* d_flags, cudaStream_t st,
+                         const uint32_t* d_in32_late) {
     if (ga.n == 0) return;
     ScatterArgs a = scatter_args(ga, d_offsets_a, nullptr, nullptr, nullptr, nullptr, nullptr);
     a.nown = bg.nbuckets;
@@ -866,11 +874,11 @@ void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void
     a.flags = d_flags;
     a.tot = d_tot_a;
     if (ga.payload_bytes == 2)
-        scatter_launch<kModeBucket>(PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload)},
-                                    a, st);
+        scatter_launch<kModeBucket>(
+            PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload), d_in32_late}, a, st);
     else
-        scatter_launch<kModeBucket>(PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload)},
-                                    a, st);
+        scatter_launch<kModeBucket>(
+            PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload), d_in32_late}, a, st);
 }
 
 void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_counts_b,
@@ -893,14 +901,15 @@ void launch_bucket_scatter(const BucketGeom& bg, const uint16_t* d_staging, uint
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,
                     const unsigned long long* d_nj, const unsigned long long* d_yoff,
                     uint32_t* d_ybuf, unsigned long long* d_idx_out,
-                    const unsigned long long* d_csr_off, cudaStream_t st) {
+                    const unsigned long long* d_csr_off, cudaStream_t st,
+                    const uint32_t* d_in32_late) {
     if (g.n == 0 || g.nown == 0) return;
     const ScatterArgs a = scatter_args(g, d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);
     if (g.payload_bytes == 2) {
-        const PayloadSrc<uint16_t> src{static_cast<const uint16_t*>(d_payload)};
+        const PayloadSrc<uint16_t> src{static_cast<const uint16_t*>(d_payload), d_in32_late};
         d_idx_out ? scatter_launch<kModeIndex>(src, a, st) : scatter_launch<kModeBits>(src, a, st);
     } else {
-        const PayloadSrc<uint32_t> src{static_cast<const uint32_t*>(d_payload)};
+        const PayloadSrc<uint32_t> src{static_cast<const uint32_t*>(d_payload), d_in32_late};
         d_idx_out ? scatter_launch<kModeIndex>(src, a, st) : scatter_launch<kModeBits>(src, a, st);
     }
 }

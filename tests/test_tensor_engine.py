@@ -87,6 +87,29 @@ def test_shared_seed_long_blocks_use_the_tiled_kernel(dev, oracle):
         plan.close()
 
 
+@pytest.mark.parametrize("s,k", [(64, 1024), (4096, 256)], ids=["single-level", "two-level"])
+def test_host_run_overlaps_input_copy(dev, oracle, s, k):
+    """Host runs of >= 2^26 rounds copy the input on a second stream while the count pass runs
+    (it needs only the round indices); the scatter / bucket split take the data bits from the
+    input. Same key and lengths as the oracle, and as the device-resident run."""
+    import torch
+
+    n = (1 << 26) + 12345
+    x = oracle.make_input(17, 0.5, n)
+    want, wnj = oracle.extract(x, n, s, 3, 4, 0, k)
+    plan = dev.Plan(n, s, k, 3, 4)
+    for _ in range(2):  # plan reuse: the second copy waits for the first run
+        got, nj, _ = plan.run_host(x)
+        assert (nj == wnj).all()
+        assert (got == want).all()
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    d_key = torch.zeros(((s * k + 63) // 64) * 2, dtype=torch.int32, device="cuda")
+    plan.run_device(d_in.data_ptr(), d_key.data_ptr())
+    plan.check()
+    assert (d_key.cpu().numpy().view(U64)[: len(want)] == want).all()
+    plan.close()
+
+
 def test_tensor_engine_block_longer_than_2p24(dev, oracle):
     """A shared-seed block of more than 2^24 input bits: the FP4 variant's f32 accumulator
     counts exactly only below 2^24, so such items accumulate in rounds whose parities XOR."""
