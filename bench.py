@@ -325,13 +325,7 @@ def main():
         plan.set_timing(True)
         check, close = plan.check, plan.close
     tensor = args.engine != "lop3"
-    if not sharded:
-        hash_kernel = plan.hash_kernel
-    else:
-        i8 = os.environ.get("SSBH_MMA_FP4") == "0"
-        hash_kernel = ("k_toeplitz_hash" if not tensor else
-                       ("k_toeplitz_mma_pb<i8>" if i8 else "k_toeplitz_mma_pb<f4>")
-                       if c["per_block"] else ("k_toeplitz_mma" if i8 else "k_toeplitz_f4"))
+    hash_kernel = ex.shard.hash_kernel if sharded else plan.hash_kernel
     fp4 = hash_kernel in ("k_toeplitz_f4", "k_toeplitz_mma_pb<f4>")
 
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and

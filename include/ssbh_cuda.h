@@ -273,6 +273,8 @@ ssbh_status ssbh_shard_finish(ssbh_shard* shard, uint32_t* d_key, uint64_t* d_le
                               const uint64_t* hash_key, void* stream);
 ssbh_status ssbh_shard_check(ssbh_shard* shard, ssbh_extract_stats* stats);
 ssbh_status ssbh_shard_set_timing(ssbh_shard* shard, int enable);
+/* Hash kernel of the shard's owner plan (see ssbh_plan_hash_kernel). */
+const char* ssbh_shard_hash_kernel(const ssbh_shard* shard);
 
 /* The same sharded extraction driven from ONE process over several GPUs (the reference's
  * callers are single-process C++): rank r runs on devices[r] (entries may repeat), receive

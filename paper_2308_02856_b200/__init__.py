@@ -50,7 +50,7 @@ ABI_SYMBOLS = (
     "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
     "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2", "ssbh_measure_mma_f4_peak",
-    "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel",
+    "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel", "ssbh_shard_hash_kernel",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
@@ -150,6 +150,8 @@ def _load():
     L.ssbh_measure_mma_f4_peak.argtypes = [C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.ssbh_plan_hash_kernel.restype = C.c_char_p
     L.ssbh_plan_hash_kernel.argtypes = [C.c_void_p]
+    L.ssbh_shard_hash_kernel.restype = C.c_char_p
+    L.ssbh_shard_hash_kernel.argtypes = [C.c_void_p]
     L.ssbh_measure_mma_i8_peak2.restype = st
     L.ssbh_measure_mma_i8_peak2.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                             C.POINTER(C.c_double)]
@@ -637,6 +639,10 @@ class Shard:
         _check(lib.ssbh_shard_info(self.h, _p64(sf), _p64(sn), _p32(bf), _p32(bc)))
         self.slice_first, self.slice_rounds = int(sf[0]), int(sn[0])
         self.block_first, self.block_count = int(bf[0]), int(bc[0])
+
+    @property
+    def hash_kernel(self) -> str:
+        return lib.ssbh_shard_hash_kernel(self.h).decode()
 
     def ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(self.IPC_BYTES)

@@ -452,7 +452,11 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     pl->rowtiles = (pl->kw + kHashRowWords - 1) / kHashRowWords;
     pl->direct_out = (k % 32) == 0;
     pl->grid = hash_grid_size(pl->device);
-    pl->kt = choose_kt(n / params->n_subblocks, nown, pl->rowtiles, pl->grid);
+    // expected block length: shard owners see only their received rounds (n = the receive
+    // capacity, spread over the owned blocks); other plans the whole input over all s blocks
+    const uint64_t mean_nj = external_payload ? n / std::max<uint32_t>(nown, 1)
+                                              : n / params->n_subblocks;
+    pl->kt = choose_kt(mean_nj, nown, pl->rowtiles, pl->grid);
     // buffer bounds (n_j unknown on the host until the device has sampled):
     // sum_j round_up(ceil(n_j/32), R) <= n/32 + nown*R
     const uint64_t ybound = (n + 31) / 32 + (uint64_t)nown * kHashR + 8;
@@ -464,7 +468,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         pl->sbuf_words = round_up(seed_fixed + round_up((n + 31) / 32, kHashR) + 64, 8);
     pl->key_words32 = ((uint64_t)nown * k + 31) / 32;
     pl->engine = default_engine(params->per_block_seed);
-    pl->mma = make_mma_geom(nown, pl->kw, n / params->n_subblocks, pl->device);
+    pl->mma = make_mma_geom(nown, pl->kw, mean_nj, pl->device);
     pl->pb = make_pb_geom(nown, pl->kw, pl->device);
     // Long shared-seed blocks: the tiled matrix-vector kernel keeps each block's y chunks in
     // shared memory for 256 D steps instead of re-expanding them for every 256-row tile (config
@@ -472,7 +476,6 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     // block has > 620 K bits. SSBH_MMA_SHARED_PB=0/1 overrides (dev A/B knob).
     {
         const char* e = std::getenv("SSBH_MMA_SHARED_PB");
-        const uint64_t mean_nj = n / params->n_subblocks;
         pl->shared_pb = !params->per_block_seed &&
                         (e && *e ? *e == '1' : mean_nj >= (uint64_t)620000);
     }
@@ -1355,6 +1358,10 @@ extern "C" ssbh_status ssbh_shard_create(const ssbh_extract_params* params, uint
     }
     *out = sh;
     return ok();
+}
+
+extern "C" const char* ssbh_shard_hash_kernel(const ssbh_shard* sh) {
+    return sh ? ssbh_plan_hash_kernel(sh->plan) : "";
 }
 
 extern "C" ssbh_status ssbh_shard_destroy(ssbh_shard* sh) {
