@@ -1,15 +1,19 @@
-// toeplitz_mma.cu — shared-seed GF(2) Toeplitz hash on the 5th-generation tensor cores
-// (tcgen05.mma kind::i8, accumulators in TMEM). Same product as k_toeplitz_hash
-// (proj/src/toeplitz.cpp:34-52), different engine; selected per plan (ssbh_plan_set_engine).
+// toeplitz_mma.cu — the GF(2) Toeplitz hash on the 5th-generation tensor cores (tcgen05.mma,
+// accumulators in TMEM). Same product as k_toeplitz_hash (proj/src/toeplitz.cpp:34-52),
+// different engine; selected per plan (ssbh_plan_set_engine, ssbh_plan_hash_kernel names it).
 //
 // Why a tensor-core engine exists. With the input reversed (y_j[c] = x_j[n_j-1-c]) block j's
 // output is K_j[i] = XOR_c S[i+c] y_j[c] (toeplitz.cu). With ONE shared seed every block
 // multiplies the SAME Hankel matrix H[i][c] = S[i+c], so the whole hash is a GF(2) matrix
 // product D = Y * H^T (blocks x input positions times input positions x output rows), and a
-// GF(2) product is an integer product mod 2: D[j][i] = (sum_c y_j[c] * S[i+c]) mod 2. The
-// u8 tensor-core path computes the integer sums exactly (s32 accumulators wrap mod 2^32,
-// which keeps the parity) at ~4x the bit-ops/s of the LOP3 engine. Per-block seeds
-// (config 4) have one matrix per block — a matrix-vector product — and stay on LOP3.
+// GF(2) product is an integer product mod 2: D[j][i] = (sum_c y_j[c] * S[i+c]) mod 2. Per-block
+// seeds (and long shared blocks) tile each block's matrix-vector product into 128 x 128 Hankel
+// blocks instead (k_toeplitz_mma_pb, below). Kernels in this file:
+//   k_toeplitz_mma<AT, sets>  shared seeds, u8 operands (kind::i8, s32 sums wrap mod 2^32)
+//   k_toeplitz_f4<sets>       shared seeds, FP4 operands (kind::mxf4, exact f32 counts), default
+//                             for short blocks
+//   k_toeplitz_mma_pb<F4>     tiled matrix-vector products: per-block seeds, long shared blocks
+// The first is described here; the others where they are defined.
 //
 // Operands carry one bit per byte, in the byte's LSB; the other 7 bits may hold anything,
 // because they only add even multiples to the sum (a = a0 + 2a', b = b0 + 2b' gives
