@@ -176,10 +176,10 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
     __shared__ uint32_t tslot;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* w = reinterpret_cast<uint32_t*>(smem);
-    if (mode == 2)  // hash-kernel layouts: 32 KB A tile + Hankel units after it
+    if (mode >= 2)  // hash-kernel layouts / K96 tiles: fill the first 44 KB
         for (uint32_t i = threadIdx.x; i < 45056 / 4; i += blockDim.x) w[i] = 0x22222222u;
     for (uint32_t i = threadIdx.x; i < 4096 / 4; i += blockDim.x) w[i] = 0x22222222u;  // A
-    for (uint32_t i = threadIdx.x; mode != 2 && i < 8192 / 4; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; mode < 2 && i < 8192 / 4; i += blockDim.x) {
         // B: row n occupies bytes (n%8)*16 + (n/8)*256 + kc*128 (kc = 0, 1); one 1.0 per row
         uint32_t v = 0x22222222u;
         if (mode == 1) {
@@ -219,17 +219,20 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (threadIdx.x == 0) {
         const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
-        const uint32_t idesc = (1u << 7) | (1u << 10) | (32u << 17) | (1u << 23) | (8u << 24);
+        // mode 3: the K = 96 form of kind::mxf4 (instruction descriptor bit 31), rate only
+        const uint32_t idesc = (1u << 7) | (1u << 10) | (32u << 17) | (1u << 23) | (8u << 24) |
+                               (mode == 3 ? (1u << 31) : 0u);
         auto desc = [](uint32_t a, uint32_t lbo, uint32_t sbo) {
             return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
                    ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
         };
         for (uint32_t it = 0; it < iters; ++it) {
             const uint32_t m = it & 7;
-            const uint64_t a = mode == 2 ? desc(base + 256u * m, 128, 2048) : desc(base, 128, 256);
+            const uint64_t a = mode == 2 ? desc(base + 256u * m, 128, 2048)
+                               : mode == 3 ? desc(base, 128, 384) : desc(base, 128, 256);
             const uint64_t b = mode == 2
                 ? desc(base + 32768u + 16u * (2u * (m & 1) + 128u * (m >> 1)), 16, 128)
-                : desc(base + 4096u, 128, 256);
+                : mode == 3 ? desc(base + 8192u, 128, 384) : desc(base + 4096u, 128, 256);
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
@@ -306,7 +309,8 @@ extern "C" ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
-    if (macs_per_s) *macs_per_s = (double)sms * iters * 128.0 * 256.0 * 64.0 / (ms * 1e-3);
+    if (macs_per_s)
+        *macs_per_s = (double)sms * iters * 128.0 * 256.0 * (mode == 3 ? 96.0 : 64.0) / (ms * 1e-3);
     if (ms_out) *ms_out = ms;
     if (mismatches) *mismatches = hb[0];
     if (sample_bits) *sample_bits = hb[1];

@@ -298,13 +298,19 @@ template <typename P>
 struct PayloadSrc {
     using Bits = PayloadBits<P>;
     const P* __restrict__ payload;
-    // non-null: the payload carries V only and the data bit comes from the input words (the
-    // host path copies the input while the count pass runs, which does not need it)
-    const uint32_t* __restrict__ in32 = nullptr;
+    __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return payload[i]; }
+};
+
+// The payload carries V only and the data bit comes from the input words (the host path copies
+// the input while the count pass runs, which needs only the round indices). A separate type,
+// so the default scatter keeps its inner loop free of the extra branch.
+template <class P>
+struct PayloadInSrc {
+    using Bits = PayloadBits<P>;
+    const P* __restrict__ payload;
+    const uint32_t* __restrict__ in32;
     __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-        uint32_t v = payload[i];
-        if (in32) v |= ((__ldg(in32 + (i >> 5)) >> (i & 31)) & 1u) << Bits::kDataShift;
-        return v;
+        return payload[i] | (((__ldg(in32 + (i >> 5)) >> (i & 31)) & 1u) << Bits::kDataShift);
     }
 };
 
@@ -873,12 +879,18 @@ void launch_bucket_split(const BucketGeom& bg, const SamplerGeom& ga, const void
     a.staging = d_staging;
     a.flags = d_flags;
     a.tot = d_tot_a;
-    if (ga.payload_bytes == 2)
-        scatter_launch<kModeBucket>(
-            PayloadSrc<uint16_t>{static_cast<const uint16_t*>(d_payload), d_in32_late}, a, st);
-    else
-        scatter_launch<kModeBucket>(
-            PayloadSrc<uint32_t>{static_cast<const uint32_t*>(d_payload), d_in32_late}, a, st);
+    const auto* p16 = static_cast<const uint16_t*>(d_payload);
+    const auto* p32 = static_cast<const uint32_t*>(d_payload);
+    if (d_in32_late) {
+        if (ga.payload_bytes == 2)
+            scatter_launch<kModeBucket>(PayloadInSrc<uint16_t>{p16, d_in32_late}, a, st);
+        else
+            scatter_launch<kModeBucket>(PayloadInSrc<uint32_t>{p32, d_in32_late}, a, st);
+    } else if (ga.payload_bytes == 2) {
+        scatter_launch<kModeBucket>(PayloadSrc<uint16_t>{p16}, a, st);
+    } else {
+        scatter_launch<kModeBucket>(PayloadSrc<uint32_t>{p32}, a, st);
+    }
 }
 
 void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_counts_b,
@@ -905,11 +917,20 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
                     const uint32_t* d_in32_late) {
     if (g.n == 0 || g.nown == 0) return;
     const ScatterArgs a = scatter_args(g, d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);
+    if (d_in32_late) {  // host runs: data bits from the input (no index mode there)
+        if (g.payload_bytes == 2)
+            scatter_launch<kModeBits>(
+                PayloadInSrc<uint16_t>{static_cast<const uint16_t*>(d_payload), d_in32_late}, a, st);
+        else
+            scatter_launch<kModeBits>(
+                PayloadInSrc<uint32_t>{static_cast<const uint32_t*>(d_payload), d_in32_late}, a, st);
+        return;
+    }
     if (g.payload_bytes == 2) {
-        const PayloadSrc<uint16_t> src{static_cast<const uint16_t*>(d_payload), d_in32_late};
+        const PayloadSrc<uint16_t> src{static_cast<const uint16_t*>(d_payload)};
         d_idx_out ? scatter_launch<kModeIndex>(src, a, st) : scatter_launch<kModeBits>(src, a, st);
     } else {
-        const PayloadSrc<uint32_t> src{static_cast<const uint32_t*>(d_payload), d_in32_late};
+        const PayloadSrc<uint32_t> src{static_cast<const uint32_t*>(d_payload)};
         d_idx_out ? scatter_launch<kModeIndex>(src, a, st) : scatter_launch<kModeBits>(src, a, st);
     }
 }

@@ -12,7 +12,8 @@ f = P.lib.ssbh_probe_mma_f4
 f.restype = C.c_int
 f.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
               C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
-for mode, iters in ((0, 20000), (0, 200000), (1, 1000), (1, (1 << 20) + 3), (1, (1 << 24) + 5)):
+for mode, iters in ((0, 20000), (0, 200000), (2, 200000), (3, 200000), (1, 1000),
+                    (1, (1 << 20) + 3), (1, (1 << 24) + 5)):
     r, ms, bad, smp = C.c_double(), C.c_double(), C.c_uint32(), C.c_uint32()
     st = f(iters, mode, C.byref(r), C.byref(ms), C.byref(bad), C.byref(smp))
     val = C.c_float.from_buffer(C.c_uint32(smp.value)).value
