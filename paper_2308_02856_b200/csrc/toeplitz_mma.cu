@@ -814,7 +814,13 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
 constexpr int kPbWin = 256;                  // row tiles per work item (accumulator columns)
 constexpr int kPbL = 256;                    // D steps per y buffer
 constexpr int kPbUnits = 512;                // units per K-chunk plane of a y buffer
-constexpr int kPbHStages = 8;
+#ifndef SSBH_PB_SD_F4
+#define SSBH_PB_SD_F4 8  // 8 D steps (16 MMAs) per stage: config 3 hash 144.6 -> 137.6 ms vs 4
+#endif
+#ifndef SSBH_PB_HST
+#define SSBH_PB_HST 8
+#endif
+constexpr int kPbHStages = SSBH_PB_HST;
 constexpr int kPbThreads = 13 * 32;          // 4 epilogue, 1 MMA, 4 y, 4 Hankel warps
 // kind::i8, M = 128, N = 256 (same instruction descriptor as the shared kernel)
 
@@ -847,7 +853,7 @@ template <bool kF4>
 struct PbGeo {
     static constexpr int planes = kF4 ? 4 : 8;      // K-chunk planes of a y buffer
     static constexpr int mmas = kF4 ? 2 : 4;        // MMAs per D step (K = 128 positions)
-    static constexpr int sd = kF4 ? 4 : 2;          // D steps per stage
+    static constexpr int sd = kF4 ? SSBH_PB_SD_F4 : 2;  // D steps per stage
     static constexpr int hunits = 128 * sd + 8;
     static constexpr int hbytes = hunits * 16;
     static constexpr int ybytes = planes * kPbUnits * 16;
