@@ -10,7 +10,7 @@ PKG      := paper_2308_02856_b200
 CSRC     := $(PKG)/csrc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclude
-CU_SRCS  := $(CSRC)/prf.cu $(CSRC)/sampler.cu $(CSRC)/toeplitz.cu $(CSRC)/toeplitz_mma.cu $(CSRC)/abi.cu $(CSRC)/diag.cu $(CSRC)/rounds.cu
+CU_SRCS  := $(CSRC)/prf.cu $(CSRC)/sampler.cu $(CSRC)/toeplitz.cu $(CSRC)/toeplitz_mma.cu $(CSRC)/toeplitz_split.cu $(CSRC)/abi.cu $(CSRC)/diag.cu $(CSRC)/rounds.cu
 CU_HDRS  := $(CSRC)/common.cuh $(CSRC)/ptx.cuh $(CSRC)/internal.h include/ssbh_cuda.h
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HOST_SRCS:= $(CSRC)/host/ssbh_api.cpp $(CSRC)/host/ssbh_pipeline.cpp

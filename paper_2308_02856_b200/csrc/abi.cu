@@ -388,6 +388,12 @@ struct ssbh_plan {
     MmaGeom mma{};
     PbGeom pb{};
     bool shared_pb = false;  // shared seed hashed by the tiled matrix-vector kernel (long blocks)
+    // 3-for-4 split of the long shared-seed squares (toeplitz_split.cu)
+    bool split = false;
+    SplitGeom sg{};
+    PbGeom pbv{};
+    DBuf vs, vy, vout, vrem;
+    LayoutBufs vlay, rlay;
     DBuf mt_words;
     // host-path staging; late input: during a host run the input is copied on copy_stream while
     // the count pass (which needs only the round indices) runs, and the passes that read the
@@ -478,6 +484,14 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         const char* e = std::getenv("SSBH_MMA_SHARED_PB");
         pl->shared_pb = !params->per_block_seed &&
                         (e && *e ? *e == '1' : mean_nj >= (uint64_t)620000);
+        const char* se = std::getenv("SSBH_MMA_SPLIT");  // levels of the 3-for-4 split
+        const uint32_t L = se && *se ? (uint32_t)std::strtoul(se, nullptr, 10) : 0u;
+        pl->split = pl->shared_pb && pl->engine == kEngineMma && mma_uses_fp4() &&
+                    split_applicable(k, mean_nj, L);
+        if (pl->split) {
+            pl->sg = make_split_geom(nown, k, mean_nj, L);
+            pl->pbv = make_pb_geom((uint32_t)pl->sg.nvirt, (uint32_t)(pl->sg.sL / 32), pl->device);
+        }
     }
 
     // two-level split for large key spaces (SSBH_BUCKETS=0 disables it, =1 forces it)
@@ -524,6 +538,15 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     if (!e) e = alloc(pl->sbuf, pl->sbuf_words * 4);
     if (!e && !pl->direct_out) e = alloc(pl->scratch, (size_t)nown * pl->kw * 4);
     if (!e && !params->per_block_seed) e = alloc(pl->mt_words, (size_t)pl->mma.mtiles * 4);
+    if (!e && pl->split) {
+        const SplitGeom& g = pl->sg;
+        e = alloc(pl->vs, ((size_t)g.T * g.leaves * g.seed_words + 256) * 4);
+        if (!e) e = alloc(pl->vy, (size_t)g.nvirt * (g.sL / 8) + 16);
+        if (!e) e = alloc(pl->vout, (size_t)g.nvirt * (g.sL / 8) + 16);
+        if (!e) e = alloc(pl->vrem, (size_t)nown * pl->kw * 4 + 16);
+        if (!e) e = pl->vlay.alloc((uint32_t)g.nvirt);
+        if (!e) e = pl->rlay.alloc(nown);
+    }
     if (!e) e = pl->lay.alloc(nown);
     if (!e) e = cudaMallocHost(&pl->h_stats, sizeof(DevStats));
     for (int i = 0; i < 6 && !e; ++i) e = cudaEventCreate(&pl->ev[i]);
@@ -639,6 +662,7 @@ extern "C" int ssbh_plan_engine(const ssbh_plan* pl) { return pl ? pl->engine : 
 extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
     if (!pl) return "";
     if (pl->engine != kEngineMma) return "k_toeplitz_hash";
+    if (pl->split) return "k_toeplitz_mma_pb<f4>+split";  // engine checked above
     if (pl->p.per_block_seed || pl->shared_pb)
         return mma_uses_fp4() ? "k_toeplitz_mma_pb<f4>" : "k_toeplitz_mma_pb<i8>";
     return mma_uses_fp4() ? "k_toeplitz_f4" : "k_toeplitz_mma";
@@ -751,7 +775,42 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
     const Layout lay = pl->lay.view();
     uint32_t* out = pl->direct_out ? d_key : pl->scratch.as<uint32_t>();
     CU(cudaMemsetAsync(out, 0, pl->direct_out ? pl->key_words32 * 4 : pl->scratch.bytes, st));
-    if (pl->engine == kEngineMma && (pl->p.per_block_seed || pl->shared_pb)) {
+    if (pl->split && pl->engine == kEngineMma) {
+        // leaves of the 3-for-4 split + the remainder past T k, then the XOR combine
+        const SplitGeom& g = pl->sg;
+        const Layout vlay = pl->vlay.view(), rlay = pl->rlay.view();
+        launch_split_prep(pl->sbuf.as<uint32_t>(), pl->sbuf_words, pl->ybuf.as<uint32_t>(), lay,
+                          pl->nown, g, pl->vs.as<uint32_t>(), pl->vy.as<uint32_t>(), vlay, rlay,
+                          st);
+        CU(cudaMemsetAsync(pl->vrem.p, 0, pl->vrem.bytes, st));
+        PbHashArgs r{};
+        r.ybuf = pl->ybuf.as<uint32_t>();
+        r.sbuf = pl->sbuf.as<uint32_t>();
+        r.out = pl->vrem.as<uint32_t>();
+        r.out_stride = pl->kw;
+        r.lay = rlay;
+        r.nown = pl->nown;
+        r.kw = pl->kw;
+        r.ntiles = pl->pb.ntiles;
+        r.nwin = pl->pb.nwin;
+        r.items = pl->pb.items;
+        launch_hash_mma_pb(r, pl->pb, st);
+        PbHashArgs v{};
+        v.ybuf = pl->vy.as<uint32_t>();
+        v.sbuf = pl->vs.as<uint32_t>();
+        v.out = pl->vout.as<uint32_t>();
+        v.out_stride = g.sL / 32;
+        v.lay = vlay;
+        v.nown = (uint32_t)g.nvirt;
+        v.kw = (uint32_t)(g.sL / 32);
+        v.ntiles = pl->pbv.ntiles;
+        v.nwin = pl->pbv.nwin;
+        v.items = pl->pbv.items;
+        launch_hash_mma_pb(v, pl->pbv, st);
+        launch_split_combine(pl->vout.as<uint32_t>(), pl->vrem.as<uint32_t>(), pl->nown, pl->kw, g,
+                             out, pl->direct_out ? pl->p.out_bits / 32 : pl->kw, st);
+        launches += 6;
+    } else if (pl->engine == kEngineMma && (pl->p.per_block_seed || pl->shared_pb)) {
         PbHashArgs m{};
         m.ybuf = pl->ybuf.as<uint32_t>();
         m.sbuf = pl->sbuf.as<uint32_t>();

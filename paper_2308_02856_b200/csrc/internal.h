@@ -239,6 +239,25 @@ struct PbHashArgs {
 };
 PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device);
 void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st);
+// 3-for-4 split of long shared-seed squares (toeplitz_split.cu): T squares of k x k per block,
+// each split L times into 3^L Hankel leaves of size k / 2^L run by the tiled kernel.
+struct SplitGeom {
+    uint32_t L, T, leaves;   // levels, squares per block, 3^L
+    uint64_t k, sL;          // square size (= rows), leaf size
+    uint64_t nvirt;          // leaves over all owned blocks: nown * T * 3^L
+    uint64_t seed_words;     // u32 words per leaf seed region
+};
+SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L);
+bool split_applicable(uint64_t k, uint64_t mean_nj, uint32_t L);
+// leaf seeds (d_vs), leaf inputs (d_vy), leaf layout (vlay: yoff/ypad/soff) and the remainder
+// layout (rlay: the original input from position T k, seed offset T k)
+void launch_split_prep(const uint32_t* d_sbuf, uint64_t sbuf_words, const uint32_t* d_ybuf,
+                       const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t* d_vs,
+                       uint32_t* d_vy, const Layout& vlay, const Layout& rlay, cudaStream_t st);
+// out[jj * out_stride + w] = rem[jj * kw + w] ^ the leaves reaching word w
+void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t nown,
+                          uint32_t kw, const SplitGeom& g, uint32_t* d_out, uint64_t out_stride,
+                          cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
 bool mma_uses_fp4();
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);

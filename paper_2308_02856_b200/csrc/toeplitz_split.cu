@@ -1,0 +1,210 @@
+// toeplitz_split.cu — fewer MACs than n·k: the 3-for-4 split of a Toeplitz/Hankel
+// matrix-vector product, on top of the tiled tensor-core kernel (k_toeplitz_mma_pb).
+//
+// A shared-seed block computes K[i] = XOR_c S[i+c] y[c] for i < k (toeplitz.cu). Cut the input
+// into T segments of k positions (t k .. t k + k) plus a remainder: each segment is a square
+// k x k Hankel product H_t y_t with H_t[i][c] = S[t k + i + c]. Split a square of size 2m into
+// m x m blocks: the Hankel structure gives blocks B_d = window of S at offset d m (d = a + b),
+//     K_lo = B0 x0 + B1 x1,  K_hi = B1 x0 + B2 x1,
+// and over GF(2)
+//     P = B1 (x0 ^ x1),  Q = (B0 ^ B1) x0,  R = (B2 ^ B1) x1,  K_lo = P ^ Q,  K_hi = P ^ R:
+// three half-size Hankel products instead of four, with seeds that are XORs of windows of S.
+// Applied L times, every square becomes 3^L leaves of size k / 2^L: (3/4)^L of the MACs. The
+// leaves are "virtual blocks" of the tiled kernel — each with its own seed region (an XOR of up
+// to 2^L windows of the shared seed) and its own input (an XOR of up to 2^L pieces of the block's
+// reversed input) — so the hash kernel itself is unchanged. The remainder (positions >= T k)
+// runs as a second tiled launch on the original input; a combine pass XORs, for every output
+// word, the 2^L leaves per segment (P and, per level, Q or R by the row's half) and the
+// remainder.
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ssbh_impl {
+
+namespace {
+
+constexpr int kMaxL = 3;
+
+// Offsets (bits) whose windows / pieces a leaf XORs. seed: S windows; input: y pieces.
+__device__ __forceinline__ int leaf_offsets(uint32_t path, uint32_t L, uint64_t k, uint64_t base,
+                                            bool seed, uint64_t* off) {
+    int n = 1;
+    off[0] = base;
+    uint64_t m = k;
+    for (uint32_t l = 0; l < L; ++l) {
+        m >>= 1;
+        // digit l of the path (most significant = level 0)
+        uint32_t p = path;
+        for (uint32_t q = l + 1; q < L; ++q) p /= 3;
+        const uint32_t d = p % 3;  // 0 = P, 1 = Q, 2 = R
+        const int n0 = n;
+        if (seed) {
+            if (d == 0) {
+                for (int e = 0; e < n0; ++e) off[e] += m;                       // B1
+            } else if (d == 1) {
+                for (int e = 0; e < n0; ++e) off[n0 + e] = off[e] + m;          // B0 ^ B1
+                n = 2 * n0;
+            } else {
+                for (int e = 0; e < n0; ++e) { off[n0 + e] = off[e] + m; off[e] += 2 * m; }  // B2 ^ B1
+                n = 2 * n0;
+            }
+        } else {
+            if (d == 0) {
+                for (int e = 0; e < n0; ++e) off[n0 + e] = off[e] + m;          // x0 ^ x1
+                n = 2 * n0;
+            } else if (d == 2) {
+                for (int e = 0; e < n0; ++e) off[e] += m;                       // x1
+            }                                                                   // Q: x0
+        }
+    }
+    return n;
+}
+
+// Leaf seed regions (pre-shifted seed S': an XOR of word-aligned windows stays pre-shifted).
+__global__ void k_split_seeds(const uint32_t* __restrict__ sbuf, uint64_t sbuf_words, SplitGeom g,
+                              uint32_t* __restrict__ vs) {
+    const uint32_t r = blockIdx.y;  // t * leaves + path
+    const uint32_t t = r / g.leaves, path = r % g.leaves;
+    uint64_t off[1 << kMaxL];
+    const int n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, true, off);
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < g.seed_words;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int e = 0; e < n; ++e) {
+            const uint64_t q = off[e] / 32 + w;
+            if (q < sbuf_words) v ^= sbuf[q];
+        }
+        vs[(uint64_t)r * g.seed_words + w] = v;
+    }
+}
+
+// Leaf inputs: block j's reversed input pieces, zero past its padded length.
+__global__ void k_split_inputs(const uint32_t* __restrict__ ybuf, Layout lay, SplitGeom g,
+                               uint32_t* __restrict__ vy) {
+    const uint64_t lw = g.sL / 32;
+    const uint64_t v = blockIdx.y + (uint64_t)blockIdx.z * 65535u;  // virtual block
+    if (v >= g.nvirt) return;
+    const uint32_t jj = (uint32_t)(v / ((uint64_t)g.T * g.leaves));
+    const uint32_t r = (uint32_t)(v % ((uint64_t)g.T * g.leaves));
+    const uint32_t t = r / g.leaves, path = r % g.leaves;
+    uint64_t off[1 << kMaxL];
+    const int n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, false, off);
+    const uint32_t* y = ybuf + lay.yoff[jj];
+    const uint64_t yp = lay.ypad[jj];
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < lw;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t x = 0;
+        for (int e = 0; e < n; ++e) {
+            const uint64_t q = off[e] / 32 + w;
+            if (q < yp) x ^= y[q];
+        }
+        vy[v * lw + w] = x;
+    }
+}
+
+// Virtual layouts: leaves (inputs in vy, seeds in vs) and the remainder (original input from
+// position T k, seed window at T k).
+__global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vlay, Layout rlay) {
+    const uint64_t lw = g.sL / 32;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.nvirt;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = (uint32_t)(v % ((uint64_t)g.T * g.leaves));
+        vlay.yoff[v] = v * lw;
+        vlay.ypad[v] = (uint32_t)lw;
+        vlay.soff[v] = (uint64_t)r * g.seed_words;
+    }
+    const uint64_t tw = (uint64_t)g.T * g.k / 32;
+    for (uint64_t jj = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jj < nown;
+         jj += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t yp = lay.ypad[jj];
+        rlay.yoff[jj] = lay.yoff[jj] + tw;
+        rlay.ypad[jj] = yp > tw ? (uint32_t)(yp - tw) : 0u;
+        rlay.soff[jj] = tw;
+    }
+}
+
+// key word w of block jj = remainder ^ XOR over segments of the leaves that reach word w.
+__global__ void k_split_combine(const uint32_t* __restrict__ vout, const uint32_t* __restrict__ rem,
+                                uint32_t nown, uint32_t kw, SplitGeom g, uint32_t* __restrict__ out,
+                                unsigned long long out_stride) {
+    const uint64_t lw = g.sL / 32;
+    const uint64_t total = (uint64_t)nown * kw;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t jj = (uint32_t)(e / kw), w = (uint32_t)(e % kw);
+        uint32_t acc = rem[e];
+        // the word's half at each level selects Q (low) or R (high) next to P
+        uint32_t hsel = 0;  // bit l set: high half at level l
+        uint64_t i = (uint64_t)w * 32, m = g.k;
+        for (uint32_t l = 0; l < g.L; ++l) {
+            m >>= 1;
+            if (i >= m) {
+                hsel |= 1u << l;
+                i -= m;
+            }
+        }
+        const uint64_t wl = i / 32;  // word inside a leaf
+        for (uint32_t t = 0; t < g.T; ++t) {
+            for (uint32_t sub = 0; sub < (1u << g.L); ++sub) {  // bit l: P (0) or Q/R (1)
+                uint32_t path = 0;
+                for (uint32_t l = 0; l < g.L; ++l) {
+                    const uint32_t d = (sub >> l & 1u) ? ((hsel >> l & 1u) ? 2u : 1u) : 0u;
+                    path = path * 3 + d;
+                }
+                const uint64_t v = ((uint64_t)jj * g.T + t) * g.leaves + path;
+                acc ^= vout[v * lw + wl];
+            }
+        }
+        out[(unsigned long long)jj * out_stride + w] = acc;
+    }
+}
+
+}  // namespace
+
+SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L) {
+    SplitGeom g{};
+    g.L = L;
+    g.k = k;
+    g.T = (uint32_t)(mean_nj / k);
+    g.leaves = 1;
+    for (uint32_t l = 0; l < L; ++l) g.leaves *= 3;
+    g.sL = k >> L;
+    g.nvirt = (uint64_t)nown * g.T * g.leaves;
+    g.seed_words = 2 * g.sL / 32 + 64;
+    return g;
+}
+
+bool split_applicable(uint64_t k, uint64_t mean_nj, uint32_t L) {
+    if (L == 0 || L > (uint32_t)kMaxL) return false;
+    // leaves: whole 128-row tiles and word-aligned offsets; at least one full square
+    return k % (256ull << L) == 0 && mean_nj >= k;
+}
+
+void launch_split_prep(const uint32_t* d_sbuf, uint64_t sbuf_words, const uint32_t* d_ybuf,
+                       const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t* d_vs,
+                       uint32_t* d_vy, const Layout& vlay, const Layout& rlay, cudaStream_t st) {
+    const unsigned rs = g.T * g.leaves;
+    k_split_seeds<<<dim3((unsigned)std::min<uint64_t>((g.seed_words + 255) / 256, 64), rs), 256, 0,
+                    st>>>(d_sbuf, sbuf_words, g, d_vs);
+    const uint64_t lw = g.sL / 32;
+    const unsigned gz = (unsigned)((g.nvirt + 65534) / 65535);
+    const unsigned gy = (unsigned)std::min<uint64_t>(g.nvirt, 65535);
+    k_split_inputs<<<dim3((unsigned)std::min<uint64_t>((lw + 255) / 256, 16), gy, gz), 256, 0,
+                     st>>>(d_ybuf, lay, g, d_vy);
+    k_split_layout<<<(unsigned)std::min<uint64_t>((std::max<uint64_t>(g.nvirt, nown) + 255) / 256,
+                                                  1184),
+                     256, 0, st>>>(lay, nown, g, vlay, rlay);
+}
+
+void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t nown,
+                          uint32_t kw, const SplitGeom& g, uint32_t* d_out, uint64_t out_stride,
+                          cudaStream_t st) {
+    const uint64_t total = (uint64_t)nown * kw;
+    if (!total) return;
+    k_split_combine<<<(unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16), 256, 0, st>>>(
+        d_vout, d_rem, nown, kw, g, d_out, out_stride);
+}
+
+}  // namespace ssbh_impl

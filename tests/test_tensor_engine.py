@@ -110,6 +110,36 @@ def test_host_run_overlaps_input_copy(dev, oracle, s, k):
     plan.close()
 
 
+@pytest.mark.parametrize("levels", [1, 2])
+def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, monkeypatch):
+    """3-for-4 split (toeplitz_split.cu): many small squares vs the oracle, and BASELINE-sized
+    squares with a remainder vs the LOP3 engine on the same input."""
+    import torch
+
+    monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
+    n, s, k = (1 << 22) + 4321, 4, 4096  # T = 256 squares of 4096 per block
+    x = oracle.make_input(21, 0.5, n)
+    want, wnj = oracle.extract(x, n, s, 5, 6, 0, k)
+    plan = dev.Plan(n, s, k, 5, 6)
+    assert plan.hash_kernel.endswith("+split")
+    got, nj, _ = plan.run_host(x)
+    plan.close()
+    assert (nj == wnj).all()
+    assert (got == want).all()
+    n, s, k = (1 << 24) + 777, 16, 1 << 19  # T = 2 squares of 2^19 per block + remainder
+    x = oracle.make_input(22, 0.5, n)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    keys = []
+    for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
+        plan = dev.Plan(n, s, k, 7, 8, engine=engine)
+        d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr())
+        plan.check()
+        keys.append(d_key.cpu().numpy())
+        plan.close()
+    assert (keys[0] == keys[1]).all()
+
+
 def test_tensor_engine_block_longer_than_2p24(dev, oracle):
     """A shared-seed block of more than 2^24 input bits: the FP4 variant's f32 accumulator
     counts exactly only below 2^24, so such items accumulate in rounds whose parities XOR."""
