@@ -326,7 +326,7 @@ def main():
         check, close = plan.check, plan.close
     tensor = args.engine != "lop3"
     hash_kernel = ex.shard.hash_kernel if sharded else plan.hash_kernel
-    fp4 = hash_kernel in ("k_toeplitz_f4", "k_toeplitz_mma_pb<f4>")
+    fp4 = hash_kernel.split("+")[0] in ("k_toeplitz_f4", "k_toeplitz_mma_pb<f4>")
 
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
     # the tcgen05 MAC rate (kind::mxf4 or kind::i8) with the hash kernel's operand layouts
@@ -503,8 +503,26 @@ def main():
             traffic = json.load(open(tpath)).get(
                 f"config{cid}_n{world}" + ("_tensor" if tensor else ""))
         hbm_ms = (n / 8 + count * k / 8) / (HBM_PEAK_GBS * 1e9) * 1e3
+        split = (ex.shard if sharded else plan).split_geometry if tensor else (0, 0, 0)
         if tensor:
             macs = hash_ops * 32  # sum_j n_j * k bit products = u8 tensor MACs doing useful work
+            direct_macs = macs
+            split_info = None
+            if split[0]:
+                # 3-for-4 split: T*3^L leaf products of (k/2^L)^2 per block + the remainder
+                lv, sq, batch = split
+                nj = d_len[:count].cpu()
+                rem = int(torch.clamp(nj - sq * k, min=0).sum().item()) * k
+                macs = count * sq * 3 ** lv * (k >> lv) ** 2 + rem
+                split_info = {
+                    "levels": lv, "squares_per_block": sq, "blocks_per_leaf_batch": batch,
+                    "leaf_macs": macs - rem, "remainder_macs": rem,
+                    "direct_bit_products": direct_macs,
+                    "direct_equivalent_rate": direct_macs / (avg_hash_ms * 1e-3) / 1e12,
+                    "note": "the hash computes the same key with (3/4)^L of the bit products "
+                            "(csrc/toeplitz_split.cu); achieved/frac count the MACs it executes, "
+                            "direct_equivalent_rate the sum_j n_j*k products of the direct form "
+                            "per second (can exceed the MMA peak)"}
             roof = {
                 "bound": "tensor (tcgen05 kind::mxf4)" if fp4 else "tensor (tcgen05 kind::i8)",
                 "kernel": hash_kernel,
@@ -515,8 +533,12 @@ def main():
                 "frac": macs / (avg_hash_ms * 1e-3) / tc_peak,
                 "traffic": traffic,
                 "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/)",
-                "algorithmic_per_launch": f"sum_j n_j*k = {macs} bit products (owned blocks; "
-                                          f"the LOP3 engine's {hash_ops} word-ops x 32)",
+                "algorithmic_per_launch": (
+                    f"sum_j n_j*k = {macs} bit products (owned blocks; the LOP3 engine's "
+                    f"{hash_ops} word-ops x 32)" if not split[0] else
+                    f"{macs} MACs of the split (leaves + remainder) over the whole hash phase "
+                    f"(leaf prep, leaf and remainder launches, combine)"),
+                "split": split_info,
                 "peak_source": ("measured live in this run: k_f4_probe mode 2 (csrc/diag.cu), "
                                 "one CTA per SM issuing back-to-back 128x256x64 kind::mxf4 "
                                 "MMAs with the hash kernel's operand layouts" if fp4 else

@@ -202,6 +202,12 @@ int ssbh_plan_engine(const ssbh_plan* plan);
  * "k_toeplitz_mma" (shared seeds, u8; SSBH_MMA_FP4=0), "k_toeplitz_mma_pb<f4>" /
  * "k_toeplitz_mma_pb<i8>" (per-block seeds) or "k_toeplitz_hash" (LOP3). */
 const char* ssbh_plan_hash_kernel(const ssbh_plan* plan);
+/* 3-for-4 Toeplitz split of long shared-seed blocks (csrc/toeplitz_split.cu; a B200 addition,
+   no reference counterpart): levels L (0 = direct product), squares T of k positions per block,
+   owned blocks per leaf batch. The hash then runs T*3^L leaf products of k/2^L per block plus
+   the remainder past T*k. */
+ssbh_status ssbh_plan_split_geometry(const ssbh_plan* plan, uint32_t* levels, uint32_t* squares,
+                                     uint32_t* batch_blocks);
 
 /* Host-buffer entry point (what a reference caller binds): input host words (n bits),
  * out_key host words (ceil(owned*k/64)), out_lengths host (owned entries, may be NULL).
@@ -275,6 +281,9 @@ ssbh_status ssbh_shard_check(ssbh_shard* shard, ssbh_extract_stats* stats);
 ssbh_status ssbh_shard_set_timing(ssbh_shard* shard, int enable);
 /* Hash kernel of the shard's owner plan (see ssbh_plan_hash_kernel). */
 const char* ssbh_shard_hash_kernel(const ssbh_shard* shard);
+/* Split geometry of the shard's owner plan (see ssbh_plan_split_geometry). */
+ssbh_status ssbh_shard_split_geometry(const ssbh_shard* shard, uint32_t* levels,
+                                      uint32_t* squares, uint32_t* batch_blocks);
 
 /* The same sharded extraction driven from ONE process over several GPUs (the reference's
  * callers are single-process C++): rank r runs on devices[r] (entries may repeat), receive

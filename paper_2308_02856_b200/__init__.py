@@ -51,6 +51,7 @@ ABI_SYMBOLS = (
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
     "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2", "ssbh_measure_mma_f4_peak",
     "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel", "ssbh_shard_hash_kernel",
+    "ssbh_plan_split_geometry", "ssbh_shard_split_geometry",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
@@ -150,6 +151,10 @@ def _load():
     L.ssbh_measure_mma_f4_peak.argtypes = [C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.ssbh_plan_hash_kernel.restype = C.c_char_p
     L.ssbh_plan_hash_kernel.argtypes = [C.c_void_p]
+    L.ssbh_plan_split_geometry.restype = st
+    L.ssbh_plan_split_geometry.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint32)] * 3
+    L.ssbh_shard_split_geometry.restype = st
+    L.ssbh_shard_split_geometry.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint32)] * 3
     L.ssbh_shard_hash_kernel.restype = C.c_char_p
     L.ssbh_shard_hash_kernel.argtypes = [C.c_void_p]
     L.ssbh_measure_mma_i8_peak2.restype = st
@@ -561,6 +566,14 @@ class Plan:
         """Name of the hash kernel this plan launches (k_toeplitz_f4 / _mma / _mma_pb / _hash)."""
         return lib.ssbh_plan_hash_kernel(self.h).decode()
 
+    @property
+    def split_geometry(self):
+        """(levels, squares per block, blocks per leaf batch) of the 3-for-4 split; levels 0 =
+        direct tiled product."""
+        v = [C.c_uint32() for _ in range(3)]
+        _check(lib.ssbh_plan_split_geometry(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
     def stream_begin(self, stream: int = 0, samp=None, hsh=None):
         sk = None if samp is None else _p64(key_of(samp))
         hk = None if hsh is None else _p64(key_of(hsh))
@@ -643,6 +656,12 @@ class Shard:
     @property
     def hash_kernel(self) -> str:
         return lib.ssbh_shard_hash_kernel(self.h).decode()
+
+    @property
+    def split_geometry(self):
+        v = [C.c_uint32() for _ in range(3)]
+        _check(lib.ssbh_shard_split_geometry(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
 
     def ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(self.IPC_BYTES)

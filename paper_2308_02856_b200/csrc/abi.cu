@@ -395,6 +395,9 @@ struct ssbh_plan {
     DBuf vs, vy, vout, vrem;
     LayoutBufs vlay, rlay;
     DBuf mt_words;
+    DBuf vmt;        // split leaves on the GEMM kernel: max ypad per virtual M tile
+    MmaGeom mmv{};   // split leaves on the GEMM kernel
+    MmaGeom mmr{};   // split remainder on the GEMM kernel (shared seed)
     // host-path staging; late input: during a host run the input is copied on copy_stream while
     // the count pass (which needs only the round indices) runs, and the passes that read the
     // data bits wait for late_ev
@@ -484,13 +487,30 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         const char* e = std::getenv("SSBH_MMA_SHARED_PB");
         pl->shared_pb = !params->per_block_seed &&
                         (e && *e ? *e == '1' : mean_nj >= (uint64_t)620000);
-        const char* se = std::getenv("SSBH_MMA_SPLIT");  // levels of the 3-for-4 split
-        const uint32_t L = se && *se ? (uint32_t)std::strtoul(se, nullptr, 10) : 0u;
-        pl->split = pl->shared_pb && pl->engine == kEngineMma && mma_uses_fp4() &&
-                    split_applicable(k, mean_nj, L);
+        // 3-for-4 split (toeplitz_split.cu) of long blocks: levels by split_levels;
+        // SSBH_MMA_SPLIT=L forces (0 disables). Shared-seed leaves run on the all-blocks GEMM
+        // (default) or the tiled kernel (SSBH_MMA_SPLIT_LEAF=pb, dev A/B knob).
+        const char* sl = std::getenv("SSBH_MMA_SPLIT_LEAF");
+        const bool gemm = !params->per_block_seed && !(sl && std::strcmp(sl, "pb") == 0);
+        const char* se = std::getenv("SSBH_MMA_SPLIT");
+        const uint32_t L =
+            se && *se ? (uint32_t)std::strtoul(se, nullptr, 10) : split_levels(k, gemm);
+        pl->split = (gemm || pl->shared_pb || params->per_block_seed) &&
+                    pl->engine == kEngineMma && mma_uses_fp4() && split_applicable(k, mean_nj, L);
         if (pl->split) {
-            pl->sg = make_split_geom(nown, k, mean_nj, L);
-            pl->pbv = make_pb_geom((uint32_t)pl->sg.nvirt, (uint32_t)(pl->sg.sL / 32), pl->device);
+            const char* sb = std::getenv("SSBH_MMA_SPLIT_MB");  // leaf buffer budget, default 8 GB
+            const uint64_t budget =
+                (sb && *sb ? (uint64_t)std::strtoull(sb, nullptr, 10) : 8192ull) << 20;
+            pl->sg = make_split_geom(nown, k, mean_nj, L, params->per_block_seed != 0, gemm,
+                                     budget);
+            const uint32_t lw = (uint32_t)(pl->sg.sL / 32);
+            if (pl->sg.gemm) {
+                pl->mmv = make_mma_geom((uint32_t)pl->sg.nvirt, lw, pl->sg.sL, pl->device);
+                const uint64_t tk = (uint64_t)pl->sg.T * k;  // remainder: one GEMM as well
+                pl->mmr = make_mma_geom(nown, pl->kw, mean_nj > tk ? mean_nj - tk : 1, pl->device);
+            }
+            else
+                pl->pbv = make_pb_geom((uint32_t)pl->sg.nvirt, lw, pl->device);
         }
     }
 
@@ -540,11 +560,13 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     if (!e && !params->per_block_seed) e = alloc(pl->mt_words, (size_t)pl->mma.mtiles * 4);
     if (!e && pl->split) {
         const SplitGeom& g = pl->sg;
-        e = alloc(pl->vs, ((size_t)g.T * g.leaves * g.seed_words + 256) * 4);
-        if (!e) e = alloc(pl->vy, (size_t)g.nvirt * (g.sL / 8) + 16);
+        e = alloc(pl->vs,
+                  ((g.per_block ? g.nvirt : (size_t)g.T * g.leaves) * g.seed_words + 256) * 4);
+        if (!e) e = alloc(pl->vy, (size_t)g.nvirt * g.vlw * 4 + 16);
         if (!e) e = alloc(pl->vout, (size_t)g.nvirt * (g.sL / 8) + 16);
         if (!e) e = alloc(pl->vrem, (size_t)nown * pl->kw * 4 + 16);
         if (!e) e = pl->vlay.alloc((uint32_t)g.nvirt);
+        if (!e && g.gemm) e = alloc(pl->vmt, (size_t)pl->mmv.mtiles * 4);
         if (!e) e = pl->rlay.alloc(nown);
     }
     if (!e) e = pl->lay.alloc(nown);
@@ -662,10 +684,21 @@ extern "C" int ssbh_plan_engine(const ssbh_plan* pl) { return pl ? pl->engine : 
 extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
     if (!pl) return "";
     if (pl->engine != kEngineMma) return "k_toeplitz_hash";
-    if (pl->split) return "k_toeplitz_mma_pb<f4>+split";  // engine checked above
+    if (pl->split)  // engine checked above
+        return pl->sg.gemm ? "k_toeplitz_f4+split" : "k_toeplitz_mma_pb<f4>+split";
     if (pl->p.per_block_seed || pl->shared_pb)
         return mma_uses_fp4() ? "k_toeplitz_mma_pb<f4>" : "k_toeplitz_mma_pb<i8>";
     return mma_uses_fp4() ? "k_toeplitz_f4" : "k_toeplitz_mma";
+}
+
+extern "C" ssbh_status ssbh_plan_split_geometry(const ssbh_plan* pl, uint32_t* levels,
+                                                uint32_t* squares, uint32_t* batch_blocks) {
+    if (!pl) return fail(SSBH_INVALID_ARGUMENT, "null plan");
+    const bool on = pl->split && pl->engine == kEngineMma;
+    if (levels) *levels = on ? pl->sg.L : 0u;
+    if (squares) *squares = on ? pl->sg.T : 0u;
+    if (batch_blocks) *batch_blocks = on ? pl->sg.batch : 0u;
+    return ok();
 }
 
 extern "C" ssbh_status ssbh_plan_set_timing(ssbh_plan* pl, int enable) {
@@ -779,37 +812,79 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
         // leaves of the 3-for-4 split + the remainder past T k, then the XOR combine
         const SplitGeom& g = pl->sg;
         const Layout vlay = pl->vlay.view(), rlay = pl->rlay.view();
-        launch_split_prep(pl->sbuf.as<uint32_t>(), pl->sbuf_words, pl->ybuf.as<uint32_t>(), lay,
-                          pl->nown, g, pl->vs.as<uint32_t>(), pl->vy.as<uint32_t>(), vlay, rlay,
-                          st);
+        launch_split_setup(pl->sbuf.as<uint32_t>(), pl->sbuf_words, g, pl->vs.as<uint32_t>(), lay,
+                           pl->nown, vlay, rlay, st);
         CU(cudaMemsetAsync(pl->vrem.p, 0, pl->vrem.bytes, st));
-        PbHashArgs r{};
-        r.ybuf = pl->ybuf.as<uint32_t>();
-        r.sbuf = pl->sbuf.as<uint32_t>();
-        r.out = pl->vrem.as<uint32_t>();
-        r.out_stride = pl->kw;
-        r.lay = rlay;
-        r.nown = pl->nown;
-        r.kw = pl->kw;
-        r.ntiles = pl->pb.ntiles;
-        r.nwin = pl->pb.nwin;
-        r.items = pl->pb.items;
-        launch_hash_mma_pb(r, pl->pb, st);
-        PbHashArgs v{};
-        v.ybuf = pl->vy.as<uint32_t>();
-        v.sbuf = pl->vs.as<uint32_t>();
-        v.out = pl->vout.as<uint32_t>();
-        v.out_stride = g.sL / 32;
-        v.lay = vlay;
-        v.nown = (uint32_t)g.nvirt;
-        v.kw = (uint32_t)(g.sL / 32);
-        v.ntiles = pl->pbv.ntiles;
-        v.nwin = pl->pbv.nwin;
-        v.items = pl->pbv.items;
-        launch_hash_mma_pb(v, pl->pbv, st);
-        launch_split_combine(pl->vout.as<uint32_t>(), pl->vrem.as<uint32_t>(), pl->nown, pl->kw, g,
-                             out, pl->direct_out ? pl->p.out_bits / 32 : pl->kw, st);
-        launches += 6;
+        if (g.gemm) {  // shared seed: the remainders are one short GEMM (seed offset T k)
+            MmaHashArgs r{};
+            r.ybuf = pl->ybuf.as<uint32_t>();
+            r.sbuf = pl->sbuf.as<uint32_t>();
+            r.out = pl->vrem.as<uint32_t>();
+            r.out_stride = pl->kw;
+            r.lay = rlay;
+            r.nown = pl->nown;
+            r.kw = pl->kw;
+            r.ntiles = pl->mmr.ntiles;
+            r.ksplit = pl->mmr.ksplit;
+            r.items = pl->mmr.items;
+            r.mt_words = pl->mt_words.as<uint32_t>();
+            launch_hash_mma(r, pl->mmr, st);
+            launches += 5;
+        } else {
+            PbHashArgs r{};
+            r.ybuf = pl->ybuf.as<uint32_t>();
+            r.sbuf = pl->sbuf.as<uint32_t>();
+            r.out = pl->vrem.as<uint32_t>();
+            r.out_stride = pl->kw;
+            r.lay = rlay;
+            r.nown = pl->nown;
+            r.kw = pl->kw;
+            r.ntiles = pl->pb.ntiles;
+            r.nwin = pl->pb.nwin;
+            r.items = pl->pb.items;
+            launch_hash_mma_pb(r, pl->pb, st);
+            launches += 4;
+        }
+        for (uint32_t jj0 = 0; jj0 < pl->nown; jj0 += g.batch) {  // leaf batches
+            const uint32_t cnt = std::min<uint32_t>(g.batch, pl->nown - jj0);
+            launch_split_batch(pl->ybuf.as<uint32_t>(), pl->sbuf.as<uint32_t>(), pl->sbuf_words,
+                               lay, pl->nown, g, jj0, pl->vy.as<uint32_t>(),
+                               pl->vs.as<uint32_t>(), st);
+            launches += g.per_block ? 1 : 0;
+            if (g.gemm) {
+                MmaHashArgs v{};
+                v.ybuf = pl->vy.as<uint32_t>();
+                v.sbuf = pl->vs.as<uint32_t>();
+                v.out = pl->vout.as<uint32_t>();
+                v.out_stride = g.sL / 32;
+                v.lay = vlay;  // soff per 128-block M tile = the group's leaf seed
+                v.nown = (uint32_t)g.nvirt;
+                v.kw = (uint32_t)(g.sL / 32);
+                v.ntiles = pl->mmv.ntiles;
+                v.ksplit = pl->mmv.ksplit;
+                v.items = pl->mmv.items;
+                v.mt_words = pl->vmt.as<uint32_t>();
+                if (pl->mmv.ksplit > 1) CU(cudaMemsetAsync(pl->vout.p, 0, pl->vout.bytes, st));
+                launch_hash_mma(v, pl->mmv, st);
+                launches += 1;  // + k_mma_tiles
+            } else {
+                PbHashArgs v{};
+                v.ybuf = pl->vy.as<uint32_t>();
+                v.sbuf = pl->vs.as<uint32_t>();
+                v.out = pl->vout.as<uint32_t>();
+                v.out_stride = g.sL / 32;
+                v.lay = vlay;
+                v.nown = (uint32_t)g.nvirt;
+                v.kw = (uint32_t)(g.sL / 32);
+                v.ntiles = pl->pbv.ntiles;
+                v.nwin = pl->pbv.nwin;
+                v.items = pl->pbv.items;
+                launch_hash_mma_pb(v, pl->pbv, st);
+            }
+            launch_split_combine(pl->vout.as<uint32_t>(), pl->vrem.as<uint32_t>(), jj0, cnt,
+                                 pl->kw, g, out, pl->direct_out ? pl->p.out_bits / 32 : pl->kw, st);
+            launches += 3;
+        }
     } else if (pl->engine == kEngineMma && (pl->p.per_block_seed || pl->shared_pb)) {
         PbHashArgs m{};
         m.ybuf = pl->ybuf.as<uint32_t>();
@@ -1421,6 +1496,12 @@ extern "C" ssbh_status ssbh_shard_create(const ssbh_extract_params* params, uint
 
 extern "C" const char* ssbh_shard_hash_kernel(const ssbh_shard* sh) {
     return sh ? ssbh_plan_hash_kernel(sh->plan) : "";
+}
+
+extern "C" ssbh_status ssbh_shard_split_geometry(const ssbh_shard* sh, uint32_t* levels,
+                                                 uint32_t* squares, uint32_t* batch_blocks) {
+    if (!sh) return fail(SSBH_INVALID_ARGUMENT, "null shard");
+    return ssbh_plan_split_geometry(sh->plan, levels, squares, batch_blocks);
 }
 
 extern "C" ssbh_status ssbh_shard_destroy(ssbh_shard* sh) {

@@ -244,20 +244,32 @@ void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st);
 struct SplitGeom {
     uint32_t L, T, leaves;   // levels, squares per block, 3^L
     uint64_t k, sL;          // square size (= rows), leaf size
-    uint64_t nvirt;          // leaves over all owned blocks: nown * T * 3^L
+    uint32_t batch;          // owned blocks per leaf batch (memory budget)
+    uint64_t nvirt;          // leaves of one batch: batch * T * 3^L
     uint64_t seed_words;     // u32 words per leaf seed region
+    bool per_block;          // per-block seeds: leaf seeds per batch leaf (else per (t, path))
+    bool gemm;               // leaves hashed by the all-blocks GEMM (shared seed) or tiled kernel
+    uint32_t gpad;           // virtual blocks per (t, path) group: batch, 128-aligned for gemm;
+                             // virtual block v = (t * leaves + path) * gpad + jl
+    uint64_t vlw;            // u32 words per leaf input (sL / 32, 16-aligned for gemm)
 };
-SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L);
+uint32_t split_levels(uint64_t k, bool gemm);  // 0 = not worth it
+SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L,
+                          bool per_block, bool gemm_leaves, uint64_t budget_bytes);
 bool split_applicable(uint64_t k, uint64_t mean_nj, uint32_t L);
-// leaf seeds (d_vs), leaf inputs (d_vy), leaf layout (vlay: yoff/ypad/soff) and the remainder
-// layout (rlay: the original input from position T k, seed offset T k)
-void launch_split_prep(const uint32_t* d_sbuf, uint64_t sbuf_words, const uint32_t* d_ybuf,
-                       const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t* d_vs,
-                       uint32_t* d_vy, const Layout& vlay, const Layout& rlay, cudaStream_t st);
-// out[jj * out_stride + w] = rem[jj * kw + w] ^ the leaves reaching word w
-void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t nown,
-                          uint32_t kw, const SplitGeom& g, uint32_t* d_out, uint64_t out_stride,
-                          cudaStream_t st);
+// the batch-relative leaf layout (vlay: yoff/ypad/soff), the remainder layout (rlay: the
+// original input from position T k, seed offset T k) and, for a shared seed, the leaf seeds
+void launch_split_setup(const uint32_t* d_sbuf, uint64_t sbuf_words, const SplitGeom& g,
+                        uint32_t* d_vs, const Layout& lay, uint32_t nown, const Layout& vlay,
+                        const Layout& rlay, cudaStream_t st);
+// leaf inputs (and per-block leaf seeds) of blocks [jj0, jj0 + batch)
+void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t sbuf_words,
+                        const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t jj0,
+                        uint32_t* d_vy, uint32_t* d_vs, cudaStream_t st);
+// out[jj * out_stride + w] = rem[jj * kw + w] ^ the leaves reaching word w, blocks jj0 + [0, count)
+void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t jj0,
+                          uint32_t count, uint32_t kw, const SplitGeom& g, uint32_t* d_out,
+                          uint64_t out_stride, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
 bool mma_uses_fp4();
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);

@@ -164,6 +164,8 @@ __device__ __forceinline__ void cp_async_wait() {
 struct Item {
     uint32_t mt, nt;     // M tile (128 owned blocks), N tile (256 output rows)
     uint32_t st0, nst;   // stage range [st0, st0 + nst) of this K part
+    uint64_t soff;       // seed offset (u32 words) of the M tile's first block: 0 for a plan's
+                         // shared seed; the split's leaf groups (128-aligned) each have their own
 };
 
 __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item& d) {
@@ -172,6 +174,7 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
     const uint32_t r = item / a.ntiles;
     const uint32_t kp = r % a.ksplit;
     d.mt = r / a.ksplit;
+    d.soff = a.lay.soff[(uint64_t)d.mt * kM];
     const uint32_t ns = a.mt_words[d.mt] / (a.stage_bits / 32);
     const uint32_t lo = (uint32_t)((uint64_t)ns * kp / a.ksplit);
     d.st0 = lo;
@@ -237,7 +240,8 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
             const uint64_t b1 = (uint64_t)p.d.nt * kN + (uint64_t)(p.d.st0 + p.s) * a.stage_bits + 1;
             q0a = (b1 >> 5) & ~3ull;
         }
-        cp_async16(raw + 4 * lane, a.sbuf + q0a + 4 * lane, p.valid ? 16u : 0u);
+        cp_async16(raw + 4 * lane, a.sbuf + (p.valid ? p.d.soff : 0ull) + q0a + 4 * lane,
+                   p.valid ? 16u : 0u);
     }
 }
 

@@ -25,7 +25,7 @@ namespace ssbh_impl {
 
 namespace {
 
-constexpr int kMaxL = 3;
+constexpr int kMaxL = 7;
 
 // Offsets (bits) whose windows / pieces a leaf XORs. seed: S windows; input: y pieces.
 __device__ __forceinline__ int leaf_offsets(uint32_t path, uint32_t L, uint64_t k, uint64_t base,
@@ -63,44 +63,64 @@ __device__ __forceinline__ int leaf_offsets(uint32_t path, uint32_t L, uint64_t 
 }
 
 // Leaf seed regions (pre-shifted seed S': an XOR of word-aligned windows stays pre-shifted).
-__global__ void k_split_seeds(const uint32_t* __restrict__ sbuf, uint64_t sbuf_words, SplitGeom g,
+// Shared seed: one region per (segment, path), r = blockIdx.y, source sbuf[0, sbuf_words).
+// Per-block seeds: one per leaf of the batch, v = blockIdx.y + 65535 blockIdx.z, source the
+// block's region sbuf[soff[jj], soff[jj + 1]) (zero past it: those positions meet zero input).
+__global__ void k_split_seeds(const uint32_t* __restrict__ sbuf, uint64_t sbuf_words, Layout lay,
+                              SplitGeom g, uint32_t jj0, uint32_t nown,
                               uint32_t* __restrict__ vs) {
-    const uint32_t r = blockIdx.y;  // t * leaves + path
+    const uint64_t v = blockIdx.y + (uint64_t)blockIdx.z * 65535u;
+    const uint32_t rs = g.T * g.leaves;
+    if (v >= (g.per_block ? g.nvirt : (uint64_t)rs)) return;
+    const uint32_t r = g.per_block ? (uint32_t)(v / g.gpad) : (uint32_t)v;  // t * leaves + path
     const uint32_t t = r / g.leaves, path = r % g.leaves;
+    const uint32_t* src = sbuf;
+    uint64_t bound = sbuf_words;
+    if (g.per_block) {
+        const uint32_t jl = (uint32_t)(v % g.gpad), jj = jj0 + jl;
+        if (jl < g.batch && jj < nown) {
+            src = sbuf + lay.soff[jj];
+            bound = lay.soff[jj + 1] - lay.soff[jj];
+        } else {
+            bound = 0;  // past the last block of a partial batch
+        }
+    }
     uint64_t off[1 << kMaxL];
     const int n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, true, off);
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < g.seed_words;
          w += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t v = 0;
+        uint32_t x = 0;
         for (int e = 0; e < n; ++e) {
             const uint64_t q = off[e] / 32 + w;
-            if (q < sbuf_words) v ^= sbuf[q];
+            if (q < bound) x ^= src[q];
         }
-        vs[(uint64_t)r * g.seed_words + w] = v;
+        vs[v * g.seed_words + w] = x;
     }
 }
 
 // Leaf inputs: block j's reversed input pieces, zero past its padded length.
 __global__ void k_split_inputs(const uint32_t* __restrict__ ybuf, Layout lay, SplitGeom g,
-                               uint32_t* __restrict__ vy) {
+                               uint32_t jj0, uint32_t nown, uint32_t* __restrict__ vy) {
     const uint64_t lw = g.sL / 32;
-    const uint64_t v = blockIdx.y + (uint64_t)blockIdx.z * 65535u;  // virtual block
+    const uint64_t v = blockIdx.y + (uint64_t)blockIdx.z * 65535u;  // virtual block of the batch
     if (v >= g.nvirt) return;
-    const uint32_t jj = (uint32_t)(v / ((uint64_t)g.T * g.leaves));
-    const uint32_t r = (uint32_t)(v % ((uint64_t)g.T * g.leaves));
+    const uint32_t jl = (uint32_t)(v % g.gpad), jj = jj0 + jl;
+    if (jl >= g.batch) return;  // group padding: ypad 0, never read
+    const uint32_t r = (uint32_t)(v / g.gpad);
     const uint32_t t = r / g.leaves, path = r % g.leaves;
     uint64_t off[1 << kMaxL];
     const int n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, false, off);
-    const uint32_t* y = ybuf + lay.yoff[jj];
-    const uint64_t yp = lay.ypad[jj];
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < lw;
+    const bool live = jj < nown;  // the last batch may be partial
+    const uint32_t* y = live ? ybuf + lay.yoff[jj] : ybuf;
+    const uint64_t yp = live ? lay.ypad[jj] : 0;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < g.vlw;
          w += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t x = 0;
-        for (int e = 0; e < n; ++e) {
+        for (int e = 0; e < n && w < lw; ++e) {
             const uint64_t q = off[e] / 32 + w;
             if (q < yp) x ^= y[q];
         }
-        vy[v * lw + w] = x;
+        vy[v * g.vlw + w] = x;  // zero past the leaf: padding to the GEMM's 512-bit stages
     }
 }
 
@@ -110,10 +130,10 @@ __global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vl
     const uint64_t lw = g.sL / 32;
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.nvirt;
          v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t r = (uint32_t)(v % ((uint64_t)g.T * g.leaves));
-        vlay.yoff[v] = v * lw;
-        vlay.ypad[v] = (uint32_t)lw;
-        vlay.soff[v] = (uint64_t)r * g.seed_words;
+        const uint32_t r = (uint32_t)(v / g.gpad);
+        vlay.yoff[v] = v * g.vlw;
+        vlay.ypad[v] = v % g.gpad < g.batch ? (uint32_t)g.vlw : 0u;
+        vlay.soff[v] = (g.per_block ? v : (uint64_t)r) * g.seed_words;
     }
     const uint64_t tw = (uint64_t)g.T * g.k / 32;
     for (uint64_t jj = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jj < nown;
@@ -121,20 +141,20 @@ __global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vl
         const uint64_t yp = lay.ypad[jj];
         rlay.yoff[jj] = lay.yoff[jj] + tw;
         rlay.ypad[jj] = yp > tw ? (uint32_t)(yp - tw) : 0u;
-        rlay.soff[jj] = tw;
+        rlay.soff[jj] = (g.per_block ? lay.soff[jj] : 0ull) + tw;
     }
 }
 
 // key word w of block jj = remainder ^ XOR over segments of the leaves that reach word w.
 __global__ void k_split_combine(const uint32_t* __restrict__ vout, const uint32_t* __restrict__ rem,
-                                uint32_t nown, uint32_t kw, SplitGeom g, uint32_t* __restrict__ out,
-                                unsigned long long out_stride) {
+                                uint32_t jj0, uint32_t count, uint32_t kw, SplitGeom g,
+                                uint32_t* __restrict__ out, unsigned long long out_stride) {
     const uint64_t lw = g.sL / 32;
-    const uint64_t total = (uint64_t)nown * kw;
+    const uint64_t total = (uint64_t)count * kw;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
          e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t jj = (uint32_t)(e / kw), w = (uint32_t)(e % kw);
-        uint32_t acc = rem[e];
+        const uint32_t jl = (uint32_t)(e / kw), w = (uint32_t)(e % kw);  // block jj0 + jl
+        uint32_t acc = rem[(uint64_t)(jj0 + jl) * kw + w];
         // the word's half at each level selects Q (low) or R (high) next to P
         uint32_t hsel = 0;  // bit l set: high half at level l
         uint64_t i = (uint64_t)w * 32, m = g.k;
@@ -153,26 +173,70 @@ __global__ void k_split_combine(const uint32_t* __restrict__ vout, const uint32_
                     const uint32_t d = (sub >> l & 1u) ? ((hsel >> l & 1u) ? 2u : 1u) : 0u;
                     path = path * 3 + d;
                 }
-                const uint64_t v = ((uint64_t)jj * g.T + t) * g.leaves + path;
+                const uint64_t v = ((uint64_t)t * g.leaves + path) * g.gpad + jl;
                 acc ^= vout[v * lw + wl];
             }
         }
-        out[(unsigned long long)jj * out_stride + w] = acc;
+        out[(unsigned long long)(jj0 + jl) * out_stride + w] = acc;
     }
 }
 
 }  // namespace
 
-SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L) {
+// Levels. Tiled-kernel leaves (per-block seeds): the leaf work (3/4)^L grows by the window ramp
+// (255 D steps per 256-tile window over the leaf's k / 2^L / 128 chunks); L minimises the
+// product, a deeper level only when it gains > 8 % (its prep and combine passes grow as 2^L;
+// config 4: modelled L = 4 6 % better than L = 3, measured 2.80 vs 2.56 s).
+// GEMM leaves (shared seed): no ramp — the deepest level whose leaves keep >= 2^14 positions
+// (32 FP4 stages per work item; the per-item epilogue and the 2^L prep / combine passes make
+// shorter leaves slower: config 3 hash L = 3 / 4 / 5 / 6 = 69.2 / 55.5 / 48.0 / 48.7 ms).
+uint32_t split_levels(uint64_t k, bool gemm) {
+    uint32_t best = 0;
+    double best_cost = 1.0;
+    double f = 1.0;
+    for (uint32_t L = 1; L <= (uint32_t)kMaxL; ++L) {
+        f *= 0.75;
+        if (k % (256ull << L) != 0) break;
+        const double nc = (double)(k >> L) / 128.0;
+        if (nc < 64) break;
+        if (gemm) {
+            if ((k >> L) < (1ull << 14)) break;
+            best = L;
+            continue;
+        }
+        const double cost = f * (255.0 + nc) / nc;
+        if (cost < best_cost * 0.92) {
+            best_cost = cost;
+            best = L;
+        }
+    }
+    return best;
+}
+
+SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L,
+                          bool per_block, bool gemm_leaves, uint64_t budget_bytes) {
     SplitGeom g{};
     g.L = L;
+    g.per_block = per_block;
     g.k = k;
     g.T = (uint32_t)(mean_nj / k);
     g.leaves = 1;
     for (uint32_t l = 0; l < L; ++l) g.leaves *= 3;
     g.sL = k >> L;
-    g.nvirt = (uint64_t)nown * g.T * g.leaves;
     g.seed_words = 2 * g.sL / 32 + 64;
+    // shared seed: the leaves of one (segment, path) share a seed across blocks -> one GEMM of
+    // them against that leaf matrix (k_toeplitz_f4, no window ramp); groups padded to 128-block
+    // M tiles, leaf inputs to the GEMM's 512-bit stages. Per-block seeds: every leaf is its own
+    // matrix-vector product (tiled kernel).
+    g.gemm = !per_block && gemm_leaves;
+    g.vlw = g.gemm ? (g.sL / 32 + 15) / 16 * 16 : g.sL / 32;
+    // blocks per batch: leaf inputs + leaf outputs (+ leaf seeds) within the budget
+    const uint64_t per_blk = (uint64_t)g.T * g.leaves *
+                             (g.vlw * 4 + g.sL / 8 + (per_block ? g.seed_words * 4 : 0));
+    g.batch = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nown, budget_bytes / per_blk));
+    if (g.gemm && g.batch < nown && g.batch >= 128) g.batch = g.batch / 128 * 128;
+    g.gpad = g.gemm ? (g.batch + 127) / 128 * 128 : g.batch;
+    g.nvirt = (uint64_t)g.gpad * g.T * g.leaves;
     return g;
 }
 
@@ -182,29 +246,44 @@ bool split_applicable(uint64_t k, uint64_t mean_nj, uint32_t L) {
     return k % (256ull << L) == 0 && mean_nj >= k;
 }
 
-void launch_split_prep(const uint32_t* d_sbuf, uint64_t sbuf_words, const uint32_t* d_ybuf,
-                       const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t* d_vs,
-                       uint32_t* d_vy, const Layout& vlay, const Layout& rlay, cudaStream_t st) {
-    const unsigned rs = g.T * g.leaves;
-    k_split_seeds<<<dim3((unsigned)std::min<uint64_t>((g.seed_words + 255) / 256, 64), rs), 256, 0,
-                    st>>>(d_sbuf, sbuf_words, g, d_vs);
-    const uint64_t lw = g.sL / 32;
-    const unsigned gz = (unsigned)((g.nvirt + 65534) / 65535);
-    const unsigned gy = (unsigned)std::min<uint64_t>(g.nvirt, 65535);
-    k_split_inputs<<<dim3((unsigned)std::min<uint64_t>((lw + 255) / 256, 16), gy, gz), 256, 0,
-                     st>>>(d_ybuf, lay, g, d_vy);
+static void split_seeds(const uint32_t* d_sbuf, uint64_t sbuf_words, const Layout& lay,
+                        uint32_t nown, const SplitGeom& g, uint32_t jj0, uint32_t* d_vs,
+                        cudaStream_t st) {
+    const uint64_t rows = g.per_block ? g.nvirt : (uint64_t)g.T * g.leaves;
+    const unsigned gz = (unsigned)((rows + 65534) / 65535);
+    const unsigned gy = (unsigned)std::min<uint64_t>(rows, 65535);
+    const unsigned gx =
+        (unsigned)std::min<uint64_t>((g.seed_words + 255) / 256, g.per_block ? 8 : 64);
+    k_split_seeds<<<dim3(gx, gy, gz), 256, 0, st>>>(d_sbuf, sbuf_words, lay, g, jj0, nown, d_vs);
+}
+
+void launch_split_setup(const uint32_t* d_sbuf, uint64_t sbuf_words, const SplitGeom& g,
+                        uint32_t* d_vs, const Layout& lay, uint32_t nown, const Layout& vlay,
+                        const Layout& rlay, cudaStream_t st) {
+    if (!g.per_block) split_seeds(d_sbuf, sbuf_words, lay, nown, g, 0, d_vs, st);
     k_split_layout<<<(unsigned)std::min<uint64_t>((std::max<uint64_t>(g.nvirt, nown) + 255) / 256,
                                                   1184),
                      256, 0, st>>>(lay, nown, g, vlay, rlay);
 }
 
-void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t nown,
-                          uint32_t kw, const SplitGeom& g, uint32_t* d_out, uint64_t out_stride,
-                          cudaStream_t st) {
-    const uint64_t total = (uint64_t)nown * kw;
+void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t sbuf_words,
+                        const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t jj0,
+                        uint32_t* d_vy, uint32_t* d_vs, cudaStream_t st) {
+    const uint64_t lw = g.vlw;
+    const unsigned gz = (unsigned)((g.nvirt + 65534) / 65535);
+    const unsigned gy = (unsigned)std::min<uint64_t>(g.nvirt, 65535);
+    k_split_inputs<<<dim3((unsigned)std::min<uint64_t>((lw + 255) / 256, 16), gy, gz), 256, 0,
+                     st>>>(d_ybuf, lay, g, jj0, nown, d_vy);
+    if (g.per_block) split_seeds(d_sbuf, sbuf_words, lay, nown, g, jj0, d_vs, st);
+}
+
+void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t jj0,
+                          uint32_t count, uint32_t kw, const SplitGeom& g, uint32_t* d_out,
+                          uint64_t out_stride, cudaStream_t st) {
+    const uint64_t total = (uint64_t)count * kw;
     if (!total) return;
     k_split_combine<<<(unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16), 256, 0, st>>>(
-        d_vout, d_rem, nown, kw, g, d_out, out_stride);
+        d_vout, d_rem, jj0, count, kw, g, d_out, out_stride);
 }
 
 }  // namespace ssbh_impl

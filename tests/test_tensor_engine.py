@@ -110,18 +110,36 @@ def test_host_run_overlaps_input_copy(dev, oracle, s, k):
     plan.close()
 
 
-@pytest.mark.parametrize("levels", [1, 2])
-def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, monkeypatch):
-    """3-for-4 split (toeplitz_split.cu): many small squares vs the oracle, and BASELINE-sized
+def _split_possible():
+    """The split runs on FP4 operands in the tiled kernel (dev knobs can turn either off)."""
+    return (os.environ.get("SSBH_MMA_FP4", "1") != "0"
+            and os.environ.get("SSBH_MMA_SHARED_PB", "") != "0")
+
+
+@pytest.mark.parametrize("levels,budget_mb", [(1, None), (1, 1), (2, 1), (3, None), (4, 1),
+                                              (None, None)],
+                         ids=["L1", "L1-batched", "L2-batched", "L3", "L4-batched", "auto"])
+def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, budget_mb, monkeypatch):
+    """3-for-4 split (toeplitz_split.cu): many small squares vs the oracle (leaf buffers in
+    batches of blocks when the budget is small, the last batch partial), and BASELINE-sized
     squares with a remainder vs the LOP3 engine on the same input."""
     import torch
 
-    monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
-    n, s, k = (1 << 22) + 4321, 4, 4096  # T = 256 squares of 4096 per block
+    if levels is None:
+        monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)  # levels by the cost model
+    else:
+        monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
+    if budget_mb is None:
+        monkeypatch.delenv("SSBH_MMA_SPLIT_MB", raising=False)
+    else:
+        monkeypatch.setenv("SSBH_MMA_SPLIT_MB", str(budget_mb))
+    n, s, k = (1 << 22) + 4321, 5, 4096  # T = 204 squares of 4096 per block + remainder
     x = oracle.make_input(21, 0.5, n)
     want, wnj = oracle.extract(x, n, s, 5, 6, 0, k)
     plan = dev.Plan(n, s, k, 5, 6)
-    assert plan.hash_kernel.endswith("+split")
+    # the cost model splits only squares of >= ~2^18 (window ramp vs saved MACs)
+    if _split_possible() and os.environ.get("SSBH_HASH_ENGINE") != "lop3":
+        assert plan.hash_kernel.endswith("+split") == (levels is not None)
     got, nj, _ = plan.run_host(x)
     plan.close()
     assert (nj == wnj).all()
@@ -132,12 +150,93 @@ def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, monkeypatch):
     keys = []
     for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
         plan = dev.Plan(n, s, k, 7, 8, engine=engine)
+        if engine == dev.ENGINE_TENSOR and _split_possible():
+            assert plan.hash_kernel.endswith("+split")
         d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
         plan.run_device(d_in.data_ptr(), d_key.data_ptr())
         plan.check()
         keys.append(d_key.cpu().numpy())
         plan.close()
     assert (keys[0] == keys[1]).all()
+
+
+@pytest.mark.parametrize("levels,leaf", [(5, "gemm"), (6, "gemm"), (2, "pb")])
+def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, monkeypatch):
+    """Shared-seed leaves run as one GEMM per leaf matrix (k_toeplitz_f4, 128-block groups,
+    512-bit padded leaf inputs) by default, or on the tiled kernel (SSBH_MMA_SPLIT_LEAF=pb):
+    deep splits and both leaf kernels vs the LOP3 engine on T = 2 squares of 2^19 + remainder."""
+    import torch
+
+    monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
+    monkeypatch.setenv("SSBH_MMA_SPLIT_LEAF", leaf)
+    n, s, k = (1 << 24) + 4097, 16, 1 << 19
+    x = oracle.make_input(25, 0.5, n)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    keys = []
+    for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
+        plan = dev.Plan(n, s, k, 13, 14, engine=engine)
+        if engine == dev.ENGINE_TENSOR and _split_possible():
+            want = "k_toeplitz_f4+split" if leaf == "gemm" else "k_toeplitz_mma_pb<f4>+split"
+            assert plan.hash_kernel == want
+            assert plan.split_geometry[:2] == (levels, 2)
+        d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr())
+        plan.check()
+        keys.append(d_key.cpu().numpy())
+        plan.close()
+    assert (keys[0] == keys[1]).all()
+
+
+@pytest.mark.parametrize("levels,budget_mb", [(1, None), (3, 2), (4, None), (None, None)],
+                         ids=["L1", "L3-batched", "L4", "auto"])
+def test_split_per_block_seeds(dev, oracle, levels, budget_mb, monkeypatch):
+    """The split with per-block seeds (config-4 style): leaf seeds are XORs of windows of each
+    block's own seed region, made per leaf batch. Small squares vs the oracle; a config-4-like
+    shape (k = 3 * 2^17, T = 2 squares + a remainder) vs the LOP3 engine."""
+    import torch
+
+    if levels is None:
+        monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)
+    else:
+        monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
+    if budget_mb is None:
+        monkeypatch.delenv("SSBH_MMA_SPLIT_MB", raising=False)
+    else:
+        monkeypatch.setenv("SSBH_MMA_SPLIT_MB", str(budget_mb))
+    if levels is not None:
+        n, s, k = (1 << 21) + 999, 7, 4096
+        x = oracle.make_input(23, 0.5, n)
+        want, wnj = oracle.extract(x, n, s, 9, 10, 1, k)
+        plan = dev.Plan(n, s, k, 9, 10, per_block=True)
+        if _split_possible() and os.environ.get("SSBH_HASH_ENGINE") != "lop3":
+            assert plan.hash_kernel.endswith("+split")
+            assert plan.split_geometry[0] == levels
+        got, nj, _ = plan.run_host(x)
+        plan.close()
+        assert (nj == wnj).all()
+        assert (got == want).all()
+    n, s, k = (1 << 24) + 777, 16, 3 << 17
+    x = oracle.make_input(24, 0.5, n)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    keys = []
+    for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
+        plan = dev.Plan(n, s, k, 11, 12, per_block=True, engine=engine)
+        if engine == dev.ENGINE_TENSOR and os.environ.get("SSBH_MMA_FP4", "1") != "0":
+            assert plan.hash_kernel.endswith("+split")
+        d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr())
+        plan.check()
+        keys.append(d_key.cpu().numpy())
+        plan.close()
+    assert (keys[0] == keys[1]).all()
+
+
+def test_split_disabled_by_env(dev, monkeypatch):
+    """SSBH_MMA_SPLIT=0 keeps long shared blocks on the direct tiled kernel."""
+    monkeypatch.setenv("SSBH_MMA_SPLIT", "0")
+    plan = dev.Plan((1 << 22) + 4321, 5, 4096, 5, 6)
+    assert not plan.hash_kernel.endswith("+split")
+    plan.close()
 
 
 def test_tensor_engine_block_longer_than_2p24(dev, oracle):
