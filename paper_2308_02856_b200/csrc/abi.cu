@@ -881,9 +881,10 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 v.items = pl->pbv.items;
                 launch_hash_mma_pb(v, pl->pbv, st);
             }
-            launch_split_combine(pl->vout.as<uint32_t>(), pl->vrem.as<uint32_t>(), jj0, cnt,
-                                 pl->kw, g, out, pl->direct_out ? pl->p.out_bits / 32 : pl->kw, st);
-            launches += 3;
+            launches += 2 + launch_split_combine(pl->vout.as<uint32_t>(), pl->vy.as<uint32_t>(),
+                                                 pl->vrem.as<uint32_t>(), jj0, cnt, pl->kw, g, out,
+                                                 pl->direct_out ? pl->p.out_bits / 32 : pl->kw,
+                                                 st);
         }
     } else if (pl->engine == kEngineMma && (pl->p.per_block_seed || pl->shared_pb)) {
         PbHashArgs m{};

@@ -267,9 +267,10 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
                         const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t jj0,
                         uint32_t* d_vy, uint32_t* d_vs, cudaStream_t st);
 // out[jj * out_stride + w] = rem[jj * kw + w] ^ the leaves reaching word w, blocks jj0 + [0, count)
-void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t jj0,
-                          uint32_t count, uint32_t kw, const SplitGeom& g, uint32_t* d_out,
-                          uint64_t out_stride, cudaStream_t st);
+// returns the launches made; d_tmp (>= the leaf outputs) holds intermediate levels
+uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
+                              uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
+                              uint32_t* d_out, uint64_t out_stride, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
 bool mma_uses_fp4();
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);

@@ -532,7 +532,9 @@ constexpr int kF4RawS = 4 * kF4Pre * 128;         // per set
 __host__ __device__ constexpr size_t f4_bar(int sets) { return (size_t)kF4Stages * kF4Slot + sets * (kF4RawY + kF4RawS); }
 __host__ __device__ constexpr size_t f4_smem(int sets) { return f4_bar(sets) + (2 * kF4Stages + 4) * 8 + 16; }
 static_assert(f4_smem(3) <= 232448, "f4 smem budget");
-constexpr uint32_t kF4MaxStages = (1u << 24) / kF4StageK;  // exact f32 counts per round
+// exact f32 counts per round, < 2^23 so that the epilogue's parity read (count + 2^23: the
+// integer lands in the low mantissa bits, FADD instead of the slower F2I) stays exact
+constexpr uint32_t kF4MaxStages = (1u << 23) / kF4StageK;
 constexpr uint32_t kF4SfCol = kN;                            // scale factors: columns 256..287
 // kind::mxf4 instruction descriptor: E2M1 x E2M1, UE8M0 scales, K-major, M = 128, N = 256
 constexpr uint32_t kF4Idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) | (1u << 23) |
@@ -632,7 +634,8 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         uint32_t w = 0;
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) w |= (__float2uint_rz(__uint_as_float(v[e])) & 1u) << e;
+                        for (int e = 0; e < 32; ++e)
+                            w |= (__float_as_uint(__uint_as_float(v[e]) + 8388608.0f) & 1u) << e;
                         acc_w[q] ^= w;
                     }
                 }

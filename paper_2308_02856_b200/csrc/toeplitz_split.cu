@@ -17,6 +17,8 @@
 // word, the 2^L leaves per segment (P and, per level, Q or R by the row's half) and the
 // remainder.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.h"
@@ -98,29 +100,46 @@ __global__ void k_split_seeds(const uint32_t* __restrict__ sbuf, uint64_t sbuf_w
     }
 }
 
-// Leaf inputs: block j's reversed input pieces, zero past its padded length.
-__global__ void k_split_inputs(const uint32_t* __restrict__ ybuf, Layout lay, SplitGeom g,
-                               uint32_t jj0, uint32_t nown, uint32_t* __restrict__ vy) {
+// Leaf inputs: block j's reversed input pieces, zero past its padded length. One CTA per leaf:
+// its (up to 2^L) piece offsets are computed once into shared memory, then the CTA streams the
+// leaf's words (coalesced reads of every piece, one coalesced write).
+__global__ void __launch_bounds__(256) k_split_inputs(const uint32_t* __restrict__ ybuf,
+                                                      Layout lay, SplitGeom g, uint32_t jj0,
+                                                      uint32_t nown, uint32_t* __restrict__ vy) {
+    __shared__ uint64_t s_off[1 << kMaxL];
+    __shared__ int s_n;
     const uint64_t lw = g.sL / 32;
-    const uint64_t v = blockIdx.y + (uint64_t)blockIdx.z * 65535u;  // virtual block of the batch
-    if (v >= g.nvirt) return;
-    const uint32_t jl = (uint32_t)(v % g.gpad), jj = jj0 + jl;
+    // grid index -> (block, leaf) with the leaf fastest, so that the leaves of one block (which
+    // all read its input) run together and re-read it from L2
+    const uint64_t idx = blockIdx.x + (uint64_t)blockIdx.y * 65535u;
+    if (idx >= g.nvirt) return;
+    const uint32_t rs = g.T * g.leaves;
+    const uint32_t jl = (uint32_t)(idx / rs), jj = jj0 + jl;
+    const uint32_t r = (uint32_t)(idx % rs);
     if (jl >= g.batch) return;  // group padding: ypad 0, never read
-    const uint32_t r = (uint32_t)(v / g.gpad);
+    const uint64_t v = (uint64_t)r * g.gpad + jl;  // virtual block
     const uint32_t t = r / g.leaves, path = r % g.leaves;
-    uint64_t off[1 << kMaxL];
-    const int n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, false, off);
+    if (threadIdx.x == 0) {
+        uint64_t off[1 << kMaxL];
+        s_n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, false, off);
+        for (int e = 0; e < s_n; ++e) s_off[e] = off[e] / 32;
+    }
+    __syncthreads();
+    const int n = s_n;
     const bool live = jj < nown;  // the last batch may be partial
     const uint32_t* y = live ? ybuf + lay.yoff[jj] : ybuf;
     const uint64_t yp = live ? lay.ypad[jj] : 0;
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < g.vlw;
-         w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t* dst = vy + v * g.vlw;
+    for (uint64_t w = threadIdx.x; w < g.vlw; w += blockDim.x) {
         uint32_t x = 0;
-        for (int e = 0; e < n && w < lw; ++e) {
-            const uint64_t q = off[e] / 32 + w;
-            if (q < yp) x ^= y[q];
+        if (w < lw) {
+#pragma unroll 4
+            for (int e = 0; e < n; ++e) {
+                const uint64_t q = s_off[e] + w;
+                if (q < yp) x ^= __ldg(y + q);
+            }
         }
-        vy[v * g.vlw + w] = x;  // zero past the leaf: padding to the GEMM's 512-bit stages
+        dst[w] = x;  // zero past the leaf: padding to the GEMM's 512-bit stages
     }
 }
 
@@ -181,6 +200,55 @@ __global__ void k_split_combine(const uint32_t* __restrict__ vout, const uint32_
     }
 }
 
+// Hierarchical combine, one level per launch: the nodes of level l - 1 from their children at
+// level l (child size m = k >> l bits, cw = m / 32 words): node = [P ^ Q | P ^ R]. Node
+// (t, p, jl) of level l sits at ((t * 3^l + p) * gpad + jl) * (k >> l) / 32. Reads 2 words per
+// word written, (3/2)^l k bits per square at level l — instead of the flat combine's 2^L reads
+// per key word.
+__global__ void k_split_level(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                              uint32_t l, uint32_t count, SplitGeom g) {
+    const uint64_t cw = (g.k >> l) / 32, pw = 2 * cw;
+    uint32_t n_par = 1;  // 3^(l - 1)
+    for (uint32_t q = 1; q < l; ++q) n_par *= 3;
+    const uint64_t per_t = (uint64_t)n_par * count * pw;
+    const uint64_t total = (uint64_t)g.T * per_t;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = e % pw;
+        const uint64_t r = e / pw;  // (t * n_par + p) * count + jl
+        const uint32_t jl = (uint32_t)(r % count);
+        const uint64_t tp = r / count;  // t * n_par + p
+        const bool hi = w >= cw;
+        const uint64_t wl = hi ? w - cw : w;
+        const uint64_t child0 = tp * 3;  // t * 3^l + 3 p
+        const uint32_t p0 = src[((child0 + 0) * g.gpad + jl) * cw + wl];
+        const uint32_t px = src[((child0 + (hi ? 2 : 1)) * g.gpad + jl) * cw + wl];
+        dst[(tp * g.gpad + jl) * pw + w] = p0 ^ px;
+    }
+}
+
+// Root: key word w of block jj0 + jl = remainder ^ XOR over squares t of [P ^ Q | P ^ R] from the
+// level-1 nodes (t, 0..2).
+__global__ void k_split_root(const uint32_t* __restrict__ src, const uint32_t* __restrict__ rem,
+                             uint32_t jj0, uint32_t count, uint32_t kw, SplitGeom g,
+                             uint32_t* __restrict__ out, unsigned long long out_stride) {
+    const uint64_t cw = (g.k >> 1) / 32;
+    const uint64_t total = (uint64_t)count * kw;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t jl = (uint32_t)(e / kw), w = (uint32_t)(e % kw);
+        uint32_t acc = rem[(uint64_t)(jj0 + jl) * kw + w];
+        const bool hi = w >= cw;
+        const uint64_t wl = hi ? w - cw : w;
+        for (uint32_t t = 0; t < g.T; ++t) {
+            const uint64_t c0 = (uint64_t)t * 3;
+            acc ^= src[((c0 + 0) * g.gpad + jl) * cw + wl] ^
+                   src[((c0 + (hi ? 2 : 1)) * g.gpad + jl) * cw + wl];
+        }
+        out[(unsigned long long)(jj0 + jl) * out_stride + w] = acc;
+    }
+}
+
 }  // namespace
 
 // Levels. Tiled-kernel leaves (per-block seeds): the leaf work (3/4)^L grows by the window ramp
@@ -200,7 +268,8 @@ uint32_t split_levels(uint64_t k, bool gemm) {
         const double nc = (double)(k >> L) / 128.0;
         if (nc < 64) break;
         if (gemm) {
-            if ((k >> L) < (1ull << 14)) break;
+            // config 2 (k = 2^15, L = 1) measured no gain: short keys keep the direct GEMM
+            if (k < (1ull << 18) || (k >> L) < (1ull << 14)) break;
             best = L;
             continue;
         }
@@ -269,21 +338,40 @@ void launch_split_setup(const uint32_t* d_sbuf, uint64_t sbuf_words, const Split
 void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t sbuf_words,
                         const Layout& lay, uint32_t nown, const SplitGeom& g, uint32_t jj0,
                         uint32_t* d_vy, uint32_t* d_vs, cudaStream_t st) {
-    const uint64_t lw = g.vlw;
-    const unsigned gz = (unsigned)((g.nvirt + 65534) / 65535);
-    const unsigned gy = (unsigned)std::min<uint64_t>(g.nvirt, 65535);
-    k_split_inputs<<<dim3((unsigned)std::min<uint64_t>((lw + 255) / 256, 16), gy, gz), 256, 0,
-                     st>>>(d_ybuf, lay, g, jj0, nown, d_vy);
+    const unsigned gy = (unsigned)((g.nvirt + 65534) / 65535);
+    const unsigned gx = (unsigned)std::min<uint64_t>(g.nvirt, 65535);
+    k_split_inputs<<<dim3(gx, gy), 256, 0, st>>>(d_ybuf, lay, g, jj0, nown, d_vy);
     if (g.per_block) split_seeds(d_sbuf, sbuf_words, lay, nown, g, jj0, d_vs, st);
 }
 
-void launch_split_combine(const uint32_t* d_vout, const uint32_t* d_rem, uint32_t jj0,
-                          uint32_t count, uint32_t kw, const SplitGeom& g, uint32_t* d_out,
-                          uint64_t out_stride, cudaStream_t st) {
+uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
+                              uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
+                              uint32_t* d_out, uint64_t out_stride, cudaStream_t st) {
     const uint64_t total = (uint64_t)count * kw;
-    if (!total) return;
-    k_split_combine<<<(unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16), 256, 0, st>>>(
-        d_vout, d_rem, jj0, count, kw, g, d_out, out_stride);
+    if (!total) return 0;
+    const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    // flat (one pass, 2^L reads per key word) or level by level (default; dev A/B knob
+    // SSBH_MMA_SPLIT_COMBINE=flat)
+    static const bool flat = [] {
+        const char* e = std::getenv("SSBH_MMA_SPLIT_COMBINE");
+        return e && std::strcmp(e, "flat") == 0;
+    }();
+    if (flat || g.L == 1) {
+        if (g.L == 1)
+            k_split_root<<<grid, 256, 0, st>>>(d_vout, d_rem, jj0, count, kw, g, d_out, out_stride);
+        else
+            k_split_combine<<<grid, 256, 0, st>>>(d_vout, d_rem, jj0, count, kw, g, d_out,
+                                                  out_stride);
+        return 1;
+    }
+    uint32_t* src = d_vout;
+    uint32_t* dst = d_tmp;
+    for (uint32_t l = g.L; l >= 2; --l) {  // level l children -> level l - 1 nodes
+        k_split_level<<<grid, 256, 0, st>>>(src, dst, l, count, g);
+        std::swap(src, dst);
+    }
+    k_split_root<<<grid, 256, 0, st>>>(src, d_rem, jj0, count, kw, g, d_out, out_stride);
+    return g.L;
 }
 
 }  // namespace ssbh_impl

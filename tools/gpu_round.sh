@@ -17,7 +17,9 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 # launch list of the default bench command (tensor engine; the LOP3 comparison step is in it)
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo ncu1 rc=$?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_mma_pb -s 3 -c 1 -o gpurun_out/mma_c3 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
+# the split's leaf GEMM (per step: remainder GEMM, then the leaf GEMM) and the direct tiled kernel
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_f4 -s 3 -c 1 -o gpurun_out/leaf_c3 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
+SSBH_MMA_SPLIT=0 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_mma_pb -s 3 -c 1 -o gpurun_out/mma_c3 $CMD > gpurun_out/ncu_full_pb.log 2>&1; echo ncu2b rc=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_hash -c 1 -o gpurun_out/hash_c3 $CMD > gpurun_out/ncu_full_lop3.log 2>&1; echo ncu3 rc=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_count_rows|k_scatter" -s 6 -c 2 -o gpurun_out/sampler_c3 $CMD > gpurun_out/ncu_sampler.log 2>&1; echo ncu4 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_split -s 3 -c 3 -o gpurun_out/split_c3 $CMD > gpurun_out/ncu_split.log 2>&1; echo ncu5 rc=$?
