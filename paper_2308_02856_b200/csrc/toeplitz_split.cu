@@ -87,14 +87,22 @@ __global__ void k_split_seeds(const uint32_t* __restrict__ sbuf, uint64_t sbuf_w
             bound = 0;  // past the last block of a partial batch
         }
     }
-    uint64_t off[1 << kMaxL];
-    const int n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, true, off);
+    __shared__ uint64_t s_off[1 << kMaxL];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) {
+        uint64_t off[1 << kMaxL];
+        s_n = leaf_offsets(path, g.L, g.k, (uint64_t)t * g.k, true, off);
+        for (int e = 0; e < s_n; ++e) s_off[e] = off[e] / 32;
+    }
+    __syncthreads();
+    const int n = s_n;
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < g.seed_words;
          w += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t x = 0;
+#pragma unroll 4
         for (int e = 0; e < n; ++e) {
-            const uint64_t q = off[e] / 32 + w;
-            if (q < bound) x ^= src[q];
+            const uint64_t q = s_off[e] + w;
+            if (q < bound) x ^= __ldg(src + q);
         }
         vs[v * g.seed_words + w] = x;
     }

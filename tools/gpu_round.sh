@@ -23,4 +23,6 @@ SSBH_MMA_SPLIT=0 timeout 1200 ncu --set full --clock-control none --import-sourc
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_hash -c 1 -o gpurun_out/hash_c3 $CMD > gpurun_out/ncu_full_lop3.log 2>&1; echo ncu3 rc=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_count_rows|k_scatter" -s 6 -c 2 -o gpurun_out/sampler_c3 $CMD > gpurun_out/ncu_sampler.log 2>&1; echo ncu4 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_split -s 3 -c 3 -o gpurun_out/split_c3 $CMD > gpurun_out/ncu_split.log 2>&1; echo ncu5 rc=$?
+# config 5 launch list (one timed step after the warm-up; split leaf batches visible)
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python bench.py --config 5 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_list_c5.log 2>&1; echo ncu6 rc=$?
 ls -la gpurun_out
