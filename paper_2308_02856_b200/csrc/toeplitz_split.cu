@@ -1,5 +1,7 @@
 // toeplitz_split.cu — fewer MACs than n·k: the 3-for-4 split of a Toeplitz/Hankel
-// matrix-vector product, on top of the tiled tensor-core kernel (k_toeplitz_mma_pb).
+// matrix-vector product, on top of the tensor-core hash kernels (toeplitz_mma.cu). A B200-side
+// algorithmic change with no reference counterpart: the keys equal toeplitz_hash's
+// (proj/src/toeplitz.cpp:34-52) bit for bit; only the number of bit products drops.
 //
 // A shared-seed block computes K[i] = XOR_c S[i+c] y[c] for i < k (toeplitz.cu). Cut the input
 // into T segments of k positions (t k .. t k + k) plus a remainder: each segment is a square
@@ -10,12 +12,14 @@
 //     P = B1 (x0 ^ x1),  Q = (B0 ^ B1) x0,  R = (B2 ^ B1) x1,  K_lo = P ^ Q,  K_hi = P ^ R:
 // three half-size Hankel products instead of four, with seeds that are XORs of windows of S.
 // Applied L times, every square becomes 3^L leaves of size k / 2^L: (3/4)^L of the MACs. The
-// leaves are "virtual blocks" of the tiled kernel — each with its own seed region (an XOR of up
-// to 2^L windows of the shared seed) and its own input (an XOR of up to 2^L pieces of the block's
-// reversed input) — so the hash kernel itself is unchanged. The remainder (positions >= T k)
-// runs as a second tiled launch on the original input; a combine pass XORs, for every output
-// word, the 2^L leaves per segment (P and, per level, Q or R by the row's half) and the
-// remainder.
+// leaves are "virtual blocks" of the hash kernels — each with its own seed region (an XOR of up
+// to 2^L windows of the seed) and its own input (an XOR of up to 2^L pieces of the block's
+// reversed input). Shared seed: the leaves of one (segment, path) share their matrix across
+// blocks, so each such group is one all-blocks GEMM (k_toeplitz_f4, seed offset per M tile).
+// Per-block seeds: every leaf is a matrix-vector product on the tiled kernel
+// (k_toeplitz_mma_pb). The remainder (positions >= T k) runs as one more launch on the original
+// input; the combine goes up the tree level by level (node = [P ^ Q | P ^ R]) and XORs the
+// segments and the remainder into the key. Leaf buffers are batched over blocks (memory budget).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
