@@ -568,7 +568,25 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
     for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
 }
 
-template <int kSets>
+// kRegY variant of the A producers: the row's 512 y bits go global -> registers (one stage ahead)
+// instead of global -> shared (cp.async) -> registers, taking 16 KB per stage of shared-memory
+// traffic off the pipe the producers' operand stores and the MMA's operand reads share.
+__device__ __forceinline__ void y_load_f4(const MmaHashArgs& a, const StageIt& p, uint32_t jl,
+                                          uint4 (&x)[4]) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) x[h] = make_uint4(0u, 0u, 0u, 0u);
+    if (p.valid) {
+        const uint32_t jj = p.d.mt * kM + jl;
+        const uint64_t w0 = (uint64_t)(p.d.st0 + p.s) * (kF4StageK / 32);
+        if (jj < a.nown && w0 < a.lay.ypad[jj]) {
+            const uint4* src = reinterpret_cast<const uint4*>(a.ybuf + a.lay.yoff[jj] + w0);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) x[h] = __ldg(src + h);
+        }
+    }
+}
+
+template <int kSets, bool kRegY>
 __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashArgs a) {
     constexpr int kS = kF4Stages;
     constexpr uint32_t M2 = 0x22222222u;
@@ -698,28 +716,10 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
         // ---------------------------------------------------------------- A producers
         const uint32_t set = (warp - kProdWarp0) >> 3;
         const uint32_t jl = 32u * ((warp - kProdWarp0) & 3) + lane;
-        uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
-        StageIt cur, pre;
-        cur.start(a);
-        cur.advance(a, set);
-        pre = cur;
-        for (int i = 0; i < kF4Pre; ++i) {
-            y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
-            cp_async_commit();
-            pre.advance(a, kSets);
-        }
         const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
-        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
-            const uint32_t rs = i % kF4Pre;
-            cp_async_wait<kF4Pre - 1>();
-            uint4 x[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h)
-                x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + h * kM * 4);
-            const uint32_t slot = g % kS;
-            if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+        // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0
+        auto expand = [&](const uint4 (&x)[4], uint32_t slot) {
             uint8_t* ys = slots + (size_t)slot * kF4Slot + row_off;
-            // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0
 #pragma unroll
             for (int gg = 0; gg < 4; ++gg) {
 #pragma unroll
@@ -732,11 +732,48 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
+        };
+        StageIt cur, pre;
+        cur.start(a);
+        cur.advance(a, set);
+        pre = cur;
+        if constexpr (kRegY) {
+            uint4 x[4];
+            y_load_f4(a, pre, jl, x);
+            pre.advance(a, kSets);
+            for (uint32_t g = set; cur.valid; g += kSets, cur.advance(a, kSets)) {
+                uint4 nx[4];
+                y_load_f4(a, pre, jl, nx);  // next stage's bits in flight while this one is stored
+                pre.advance(a, kSets);
+                const uint32_t slot = g % kS;
+                if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+                expand(x, slot);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) x[h] = nx[h];
+            }
+        } else {
+        uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
+        for (int i = 0; i < kF4Pre; ++i) {
+            y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
+            cp_async_commit();
+            pre.advance(a, kSets);
+        }
+        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
+            const uint32_t rs = i % kF4Pre;
+            cp_async_wait<kF4Pre - 1>();
+            uint4 x[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + h * kM * 4);
+            const uint32_t slot = g % kS;
+            if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+            expand(x, slot);
             y_prefetch_f4(a, pre, jl, raw + rs * kM * 16);
             cp_async_commit();
             pre.advance(a, kSets);
         }
         cp_async_wait<0>();
+        }
     } else {
         // ---------------------------------------------------------------- B producers
         const uint32_t set = (warp - kProdWarp0) >> 3;
@@ -1213,20 +1250,24 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     a.stage_bits = kStageK;
     if (mma_uses_fp4()) {
         a.stage_bits = kF4StageK;
-        // producer sets (dev A/B knob SSBH_MMA_F4_SETS=2|3; default 2)
+        // producer sets (dev A/B knob SSBH_MMA_F4_SETS=2|3; default 2); A producers' y path
+        // (dev A/B knob SSBH_MMA_F4_REGY=1: global -> registers, 0: cp.async staging)
         static const int sets = [] {
             const char* e = std::getenv("SSBH_MMA_F4_SETS");
             return e && *e == '3' ? 3 : 2;  // 3 sets measured no faster (157-158 ms)
         }();
-        if (sets == 2) {
-            cudaFuncSetAttribute(k_toeplitz_f4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)f4_smem(2));
-            k_toeplitz_f4<2><<<grid, threads_for(2), f4_smem(2), st>>>(a);
-        } else {
-            cudaFuncSetAttribute(k_toeplitz_f4<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)f4_smem(3));
-            k_toeplitz_f4<3><<<grid, threads_for(3), f4_smem(3), st>>>(a);
-        }
+        static const bool regy = [] {
+            const char* e = std::getenv("SSBH_MMA_F4_REGY");
+            return e && *e == '1';
+        }();
+        auto go = [&](auto kern, int s) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f4_smem(s));
+            kern<<<grid, threads_for(s), f4_smem(s), st>>>(a);
+        };
+        if (sets == 2)
+            regy ? go(k_toeplitz_f4<2, true>, 2) : go(k_toeplitz_f4<2, false>, 2);
+        else
+            regy ? go(k_toeplitz_f4<3, true>, 3) : go(k_toeplitz_f4<3, false>, 3);
         return;
     }
     // dev A/B knobs: SSBH_MMA_ATMEM=0 stages A in shared memory (one producer set);
