@@ -693,7 +693,12 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
                 const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
                 for (uint32_t s = s0; s < s1; ++s, ++g) {
                     const uint32_t slot = g % kS;
-                    mbar_wait(&full[slot], (g / kS) & 1);
+                    // default (SSBH_MMA_F4_SPIN unset): hardware-suspended wait, no try_wait polls
+                    // on the L1 data pipe the producers' stores and the MMA operand reads share
+                    if (a.spin)
+                        mbar_wait(&full[slot], (g / kS) & 1);
+                    else
+                        mbar_wait_sleep(&full[slot], (g / kS) & 1);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t ya = base_y + slot * kF4Slot;
@@ -1256,6 +1261,14 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
             const char* e = std::getenv("SSBH_MMA_F4_SETS");
             return e && *e == '3' ? 3 : 2;  // 3 sets measured no faster (157-158 ms)
         }();
+        // MMA-warp stage wait (dev A/B knob SSBH_MMA_F4_SPIN=1: poll): the hardware-suspended
+        // wait measured 1.1 % faster on the split's leaf GEMM (config 3 hash 45.13 -> 44.65 ms,
+        // profiles/r01_ab_leaf_gemm.md) — polls compete for the L1 data pipe with the producers
+        static const int f4spin = [] {
+            const char* e = std::getenv("SSBH_MMA_F4_SPIN");
+            return e && *e == '1' ? 1 : 0;
+        }();
+        a.spin = f4spin;
         static const bool regy = [] {
             const char* e = std::getenv("SSBH_MMA_F4_REGY");
             return e && *e == '1';
