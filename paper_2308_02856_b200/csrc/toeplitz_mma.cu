@@ -805,19 +805,23 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
             uint8_t* gs = slots + (size_t)slot * kF4Slot + kF4YBytes;
+            // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
+            // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position. Unit u + 128 starts 4
+            // words later with the same shift, so its first word is this unit's last: 4 shared
+            // loads per unit instead of 5 (the L1 data pipe is the leaf GEMM's contended resource)
+            const uint32_t rel = rel0 + gt - 1;
+            const uint32_t q0 = rel >> 5, sh = rel & 31;
+            uint32_t w0 = sw[q0];
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
                 const uint32_t u = gt + 128u * r;
                 if (u < (uint32_t)kF4GUnits) {
-                    // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
-                    // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position
-                    const uint32_t rel = rel0 + u - 1;
-                    const uint32_t q = rel >> 5, sh = rel & 31;
-                    const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3],
-                                   w4 = sw[q + 4];
+                    const uint32_t q = q0 + 4u * r;
+                    const uint32_t w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3], w4 = sw[q + 4];
                     *reinterpret_cast<uint4*>(gs + 16 * u) =
                         make_uint4(__funnelshift_r(w0, w1, sh) & M2, __funnelshift_r(w1, w2, sh) & M2,
                                    __funnelshift_r(w2, w3, sh) & M2, __funnelshift_r(w3, w4, sh) & M2);
+                    w0 = w4;
                 }
             }
             fence_proxy_async_smem();
