@@ -568,33 +568,6 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
     for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
 }
 
-// Coalesced y staging for the A producers: a warp's 32 rows are fetched 8 rows per cp.async
-// instruction (4 lanes x 16 B per row, 8 cache lines per instruction instead of 32 — the L1 data
-// pipe is the leaf GEMM's contended resource), the row's 16-B chunks XOR-swizzled so that both
-// these writes and the per-row reads (lane = row) are conflict-free.
-__device__ __forceinline__ uint32_t f4_raw_off(uint32_t row, uint32_t h) {
-    return row * 16 + ((h ^ ((row >> 1) & 3)) * 4);  // u32 words within a [kM rows x 16] slot
-}
-__device__ __forceinline__ void y_prefetch_f4c(const MmaHashArgs& a, const StageIt& p,
-                                               uint32_t wrow0, uint32_t lane, uint32_t* rawslot) {
-    const uint32_t h = lane & 3;
-    const uint64_t w0 = p.valid ? (uint64_t)(p.d.st0 + p.s) * (kF4StageK / 32) : 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t row = wrow0 + (lane >> 2) + 8u * i;
-        const uint32_t* src = a.ybuf;
-        uint32_t bytes = 0;
-        if (p.valid) {
-            const uint32_t jj = p.d.mt * kM + row;
-            if (jj < a.nown && w0 < a.lay.ypad[jj]) {
-                src = a.ybuf + a.lay.yoff[jj] + w0 + 4 * h;
-                bytes = 16;
-            }
-        }
-        cp_async16(rawslot + f4_raw_off(row, h), src, bytes);
-    }
-}
-
 // kRegY variant of the A producers: the row's 512 y bits go global -> registers (one stage ahead)
 // instead of global -> shared (cp.async) -> registers, taking 16 KB per stage of shared-memory
 // traffic off the pipe the producers' operand stores and the MMA's operand reads share.
@@ -784,25 +757,23 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
                 for (int h = 0; h < 4; ++h) x[h] = nx[h];
             }
         } else {
-        uint32_t* raw = raw_y + set * (kF4RawY / 4);  // [slot][kM rows][16 words, swizzled]
-        const uint32_t wrow0 = jl & ~31u;
+        uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
         for (int i = 0; i < kF4Pre; ++i) {
-            y_prefetch_f4c(a, pre, wrow0, lane, raw + i * kM * 16);
+            y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
             cp_async_commit();
             pre.advance(a, kSets);
         }
         for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
-            __syncwarp();  // the row was fetched by 4 other lanes of this warp
             uint4 x[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h)
-                x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + f4_raw_off(jl, h));
+                x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + h * kM * 4);
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
-            expand(x, slot);  // ends in __syncwarp: every lane has read raw slot rs
-            y_prefetch_f4c(a, pre, wrow0, lane, raw + rs * kM * 16);
+            expand(x, slot);
+            y_prefetch_f4(a, pre, jl, raw + rs * kM * 16);
             cp_async_commit();
             pre.advance(a, kSets);
         }
