@@ -526,12 +526,15 @@ constexpr int kF4YBytes = kM * kF4StageK / 2;     // 32768
 constexpr int kF4GBytes = ((kF4GUnits * 16 + 127) / 128) * 128;  // 10368
 constexpr int kF4Slot = kF4YBytes + kF4GBytes;
 constexpr int kF4Stages = 4;
-constexpr int kF4Pre = 2;                         // cp.async prefetch depth per set
+#ifndef SSBH_F4_PRE
+#define SSBH_F4_PRE 2
+#endif
+constexpr int kF4Pre = SSBH_F4_PRE;               // cp.async prefetch depth per set
 constexpr int kF4RawY = kF4Pre * kM * 64;         // per set
 constexpr int kF4RawS = 4 * kF4Pre * 128;         // per set
 __host__ __device__ constexpr size_t f4_bar(int sets) { return (size_t)kF4Stages * kF4Slot + sets * (kF4RawY + kF4RawS); }
 __host__ __device__ constexpr size_t f4_smem(int sets) { return f4_bar(sets) + (2 * kF4Stages + 4) * 8 + 16; }
-static_assert(f4_smem(3) <= 232448, "f4 smem budget");
+static_assert(f4_smem(SSBH_F4_PRE > 2 ? 2 : 3) <= 232448, "f4 smem budget");
 // exact f32 counts per round, < 2^23 so that the epilogue's parity read (count + 2^23: the
 // integer lands in the low mantissa bits, FADD instead of the slower F2I) stays exact
 constexpr uint32_t kF4MaxStages = (1u << 23) / kF4StageK;
