@@ -589,8 +589,13 @@ __device__ __forceinline__ void y_load_f4(const MmaHashArgs& a, const StageIt& p
     }
 }
 
-template <int kSets, bool kRegY>
-__global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashArgs a) {
+// kE epilogue warps: 4 (one per TMEM sub-partition) or 8 (two per sub-partition, half of the
+// 256 accumulator columns each: a shorter drain of the single accumulator between work items)
+constexpr int f4_threads(int sets, int epi) { return (epi + 1 + 8 * sets) * 32; }
+template <int kSets, bool kRegY, int kE>
+__global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHashArgs a) {
+    constexpr int kEpiW = kE, kMmaW = kE, kProd0 = kE + 1;
+    constexpr int kQW = (kN / 32) / (kE / 4);  // accumulator column groups per epilogue warp
     constexpr int kS = kF4Stages;
     constexpr uint32_t M2 = 0x22222222u;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
             mbar_init(&empty[s], 1);
         }
         mbar_init(&tfull[0], 1);
-        mbar_init(&tempty[0], kEpiWarps);
+        mbar_init(&tempty[0], kEpiW);
         fence_barrier_init();
     }
     if (warp == 0) {
@@ -623,7 +628,7 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (warp < kEpiWarps) {  // constant scale factors: 0x7f = 2^0 in every byte
+    if (warp < 4) {  // constant scale factors: 0x7f = 2^0 in every byte
         uint32_t v[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = 0x7F7F7F7Fu;
@@ -634,24 +639,25 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
     __syncthreads();
     tc_fence_after();
 
-    if (warp < kEpiWarps) {
+    if (warp < kEpiW) {
         // ---------------------------------------------------------------- epilogue
+        const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;  // TMEM sub-partition, columns
         uint32_t t = 0;  // accumulation rounds consumed
         for (uint32_t item = blockIdx.x;; item += gridDim.x) {
             Item d;
             if (!decode(a, item, d)) break;
             const uint32_t rounds = d.nst ? (d.nst + kF4MaxStages - 1) / kF4MaxStages : 1;
-            uint32_t acc_w[kN / 32];
+            uint32_t acc_w[kQW];
 #pragma unroll
-            for (int q = 0; q < kN / 32; ++q) acc_w[q] = 0;
+            for (int q = 0; q < kQW; ++q) acc_w[q] = 0;
             for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
                 mbar_wait_sleep(&tfull[0], t & 1);
                 tc_fence_after();
                 if (d.nst) {
 #pragma unroll 1
-                    for (int q = 0; q < kN / 32; ++q) {
+                    for (int q = 0; q < kQW; ++q) {
                         uint32_t v[32];
-                        SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + 32u * q, v);
+                        SSBH_TMEM_LD32(tmem + ((sp * 32u) << 16) + 32u * (qb + q), v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         uint32_t w = 0;
 #pragma unroll
@@ -664,12 +670,13 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[0]);
             }
-            const uint32_t jj = d.mt * kM + warp * 32 + lane;
+            const uint32_t jj = d.mt * kM + sp * 32 + lane;
             if (d.nst && jj < a.nown) {
-                uint32_t* dst = a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32);
+                uint32_t* dst =
+                    a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32) + qb;
 #pragma unroll
-                for (int q = 0; q < kN / 32; ++q)
-                    if (d.nt * (kN / 32) + q < a.kw) {
+                for (int q = 0; q < kQW; ++q)
+                    if (d.nt * (kN / 32) + qb + q < a.kw) {
                         if (a.ksplit == 1)
                             dst[q] = acc_w[q];
                         else
@@ -677,7 +684,7 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
                     }
             }
         }
-    } else if (warp == kMmaWarp) {
+    } else if (warp == kMmaW) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
         const uint32_t base_y = smem_u32(slots), base_g = base_y + kF4YBytes;
@@ -720,10 +727,10 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
                 }
             }
         }
-    } else if (((warp - kProdWarp0) & 7) < 4) {
+    } else if (((warp - kProd0) & 7) < 4) {
         // ---------------------------------------------------------------- A producers
-        const uint32_t set = (warp - kProdWarp0) >> 3;
-        const uint32_t jl = 32u * ((warp - kProdWarp0) & 3) + lane;
+        const uint32_t set = (warp - kProd0) >> 3;
+        const uint32_t jl = 32u * ((warp - kProd0) & 3) + lane;
         const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
         // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0
         auto expand = [&](const uint4 (&x)[4], uint32_t slot) {
@@ -784,8 +791,8 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_f4(MmaHashAr
         }
     } else {
         // ---------------------------------------------------------------- B producers
-        const uint32_t set = (warp - kProdWarp0) >> 3;
-        const uint32_t gw = ((warp - kProdWarp0) & 7) - 4;
+        const uint32_t set = (warp - kProd0) >> 3;
+        const uint32_t gw = ((warp - kProd0) & 7) - 4;
         const uint32_t gt = gw * 32 + lane;
         uint32_t* raw = raw_s + set * (kF4RawS / 4) + gw * kF4Pre * 32;
         StageIt cur, pre;
@@ -1280,14 +1287,21 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
             const char* e = std::getenv("SSBH_MMA_F4_REGY");
             return e && *e == '1';
         }();
-        auto go = [&](auto kern, int s) {
+        // epilogue warps (dev A/B knob SSBH_MMA_F4_EPI=8: two per TMEM sub-partition)
+        static const int epi = [] {
+            const char* e = std::getenv("SSBH_MMA_F4_EPI");
+            return e && *e == '8' ? 8 : 4;
+        }();
+        auto go = [&](auto kern, int s, int e) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f4_smem(s));
-            kern<<<grid, threads_for(s), f4_smem(s), st>>>(a);
+            kern<<<grid, f4_threads(s, e), f4_smem(s), st>>>(a);
         };
-        if (sets == 2)
-            regy ? go(k_toeplitz_f4<2, true>, 2) : go(k_toeplitz_f4<2, false>, 2);
+        if (sets == 2 && epi == 8 && !regy)
+            go(k_toeplitz_f4<2, false, 8>, 2, 8);
+        else if (sets == 2)
+            regy ? go(k_toeplitz_f4<2, true, 4>, 2, 4) : go(k_toeplitz_f4<2, false, 4>, 2, 4);
         else
-            regy ? go(k_toeplitz_f4<3, true>, 3) : go(k_toeplitz_f4<3, false>, 3);
+            regy ? go(k_toeplitz_f4<3, true, 4>, 3, 4) : go(k_toeplitz_f4<3, false, 4>, 3, 4);
         return;
     }
     // dev A/B knobs: SSBH_MMA_ATMEM=0 stages A in shared memory (one producer set);
