@@ -1287,10 +1287,12 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
             const char* e = std::getenv("SSBH_MMA_F4_REGY");
             return e && *e == '1';
         }();
-        // epilogue warps (dev A/B knob SSBH_MMA_F4_EPI=8: two per TMEM sub-partition)
+        // epilogue warps: two per TMEM sub-partition (8) measured 1.4 % faster on the split's
+        // leaf GEMM (config 3 hash 44.63 -> 43.99 ms, config 2 0.199 -> 0.195 ms); dev A/B knob
+        // SSBH_MMA_F4_EPI=4
         static const int epi = [] {
             const char* e = std::getenv("SSBH_MMA_F4_EPI");
-            return e && *e == '8' ? 8 : 4;
+            return e && *e == '4' ? 4 : 8;
         }();
         auto go = [&](auto kern, int s, int e) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f4_smem(s));
