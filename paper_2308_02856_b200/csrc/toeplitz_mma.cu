@@ -519,7 +519,8 @@ __global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_mma(MmaHashA
 //     LBO 16 B, SBO 128 B.
 // Block-scaled kinds take A from shared memory only, so both operands are staged in shared
 // memory (4 stages x 42 KB); TMEM = one 128 x 256 f32 accumulator + the constant scale
-// factors. Warp roles as in k_toeplitz_mma (two producer sets alternating stages).
+// factors. Warp roles: kE epilogue warps (default 8, two per TMEM sub-partition), one MMA warp,
+// then two producer sets alternating stages as in k_toeplitz_mma.
 constexpr int kF4StageK = 512;                    // input positions per stage (8 MMAs, K = 64)
 constexpr int kF4GUnits = kN + 3 + 384 + 1;       // 643 Hankel units per stage
 constexpr int kF4YBytes = kM * kF4StageK / 2;     // 32768
