@@ -655,6 +655,28 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
                 mbar_wait_sleep(&tfull[0], t & 1);
                 tc_fence_after();
                 if (d.nst) {
+#ifdef SSBH_F4_EPI_DB
+                    // double-buffered: column group q + 1 is loaded while q's parities are formed
+                    uint32_t v0[32], v1[32];
+                    const uint32_t ta = tmem + ((sp * 32u) << 16) + 32u * qb;
+                    SSBH_TMEM_LD32(ta, v0);
+#pragma unroll
+                    for (int q = 0; q < kQW; ++q) {
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        uint32_t* cur = (q & 1) ? v1 : v0;
+                        if (q + 1 < kQW) {
+                            if (q & 1)
+                                SSBH_TMEM_LD32(ta + 32u * (q + 1), v0);
+                            else
+                                SSBH_TMEM_LD32(ta + 32u * (q + 1), v1);
+                        }
+                        uint32_t w = 0;
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            w |= (__float_as_uint(__uint_as_float(cur[e]) + 8388608.0f) & 1u) << e;
+                        acc_w[q] ^= w;
+                    }
+#else
 #pragma unroll 1
                     for (int q = 0; q < kQW; ++q) {
                         uint32_t v[32];
@@ -666,6 +688,7 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
                             w |= (__float_as_uint(__uint_as_float(v[e]) + 8388608.0f) & 1u) << e;
                         acc_w[q] ^= w;
                     }
+#endif
                 }
                 tc_fence_before();
                 __syncwarp();
