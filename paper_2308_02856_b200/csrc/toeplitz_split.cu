@@ -281,7 +281,10 @@ uint32_t split_levels(uint64_t k, bool gemm) {
         if (nc < 64) break;
         if (gemm) {
             // config 2 (k = 2^15, L = 1) measured no gain: short keys keep the direct GEMM
-            if (k < (1ull << 18) || (k >> L) < (1ull << 14)) break;
+            // leaves >= 2^13 positions (16 FP4 stages per work item): with 8 epilogue warps the
+            // per-item drain is short enough that config 3 gains from L = 6 (hash 44.0 -> 39.6-42.5
+            // ms; L = 5 before); config 5 stays at kMaxL = 7
+            if (k < (1ull << 18) || (k >> L) < (1ull << 13)) break;
             best = L;
             continue;
         }
