@@ -39,7 +39,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "input Gbit/s hashed (sample+Toeplitz)"
 UNIT = "Gbit/s"
-HBM_PEAK_GBS = 6531.6  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth on this pool's B200s)
+
+
+def _hbm_peak():
+    """MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth on this pool's B200s), else
+    the profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6531.6, "fallback (no MEASURED_PEAKS.json)"
+
+
+HBM_PEAK_GBS, HBM_PEAK_SRC = _hbm_peak()
+GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.json")
 
 
 def cfg_desc(cid, c):
@@ -54,7 +67,7 @@ def log2s(v):
     return f"2^{v.bit_length() - 1}" if v & (v - 1) == 0 else str(v)
 
 
-def config_dict(cid, c, world):
+def config_dict(cid, c, n_gpus):
     return {
         "workload": f"config{cid}: n={log2s(c['n'])} rounds, s={c['s']} sub-blocks, "
                     f"k={c['k']} out bits/sub-block, p={c['p']} ({cfg_desc(cid, c)})"
@@ -63,7 +76,7 @@ def config_dict(cid, c, world):
         "n_bits": c["n"], "n_subblocks": c["s"], "out_bits_per_block": c["k"], "p": c["p"],
         "seed_mode": "per-block (hash-seed sub=j)" if c["per_block"] else "shared (hash-seed sub=0)",
         "seeds": {"input": c["seed_in"], "sampling": c["seed_samp"], "hash": c["seed_hash"]},
-        "parallelism": f"sub-blocks sharded over {world} GPU(s)",
+        "parallelism": f"sub-blocks sharded over {n_gpus} GPU(s)",
         "l2": "L2 (126 MB) flushed between steps by a 256 MiB write outside the step events"
               + ("; input and payload exceed L2" if c["n"] >= (1 << 30) else ""),
     }
@@ -185,7 +198,7 @@ def run_reference(args, cid, c):
         "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64 (GF(2) bit-packed)",
         "data": "synthetic (KeyedStream input, seeds per BASELINE)",
-        "config": config_dict(cid, c, 1), "impl": "reference",
+        "config": config_dict(cid, c, args.gpus), "impl": "reference",
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(nb, threads), "kind": kind,
                          "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -230,7 +243,50 @@ def sampler_line(n, world, stats, sharded):
     return {"ms": ms, "rounds": rounds, "rounds_per_s": rounds / (ms * 1e-3) if ms else None,
             "hbm_bytes_algorithmic": int(bytes_), "achieved_gbs": gbs,
             "hbm_frac": gbs / HBM_PEAK_GBS if gbs else None, "peak_gbs": HBM_PEAK_GBS,
+            "peak_source": HBM_PEAK_SRC,
             "bound": "int-alu (Threefry4x64-20 per round), not HBM"}
+
+
+def spawn_ranks(n):
+    """Re-launch this command as n ranks (torch.distributed.run on 127.0.0.1); rank 0 prints
+    the JSON line. Returns the launcher's exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def reference_digest(cid, c, key_u64, nj, fnv):
+    """The whole key (configs 1-3) or the reference-pinned blocks (configs 4-5) against the
+    digests tests/golden/gen_golden.py made by running the compiled reference
+    (golden.json["extract"][cid]); n_j digest too when the lengths are at hand."""
+    if c.get("rounds_override"):
+        return {"match": None, "why": "n/k overridden: no reference digest for this shape"}
+    try:
+        with open(GOLDEN) as f:
+            g = json.load(f)["extract"][str(cid)]
+    except (OSError, KeyError):
+        return {"match": None, "why": "no golden entry"}
+    out = {"source": "tests/golden/golden.json (compiled reference, gen_golden.py)"}
+    if "key_fnv" in g:
+        got = f"{fnv(key_u64):016x}"
+        out.update(scope="whole key", want=g["key_fnv"], got=got, match=got == g["key_fnv"])
+    else:
+        kw = c["k"] // 64
+        got = [f"{fnv(key_u64[j * kw:(j + 1) * kw]):016x}" for j in g["which"]]
+        out.update(scope=f"blocks {g['which']} (reference-pinned; every block is spot-checked "
+                         "in tests/test_gpu_parity.py)", want=g["block_fnv"], got=got,
+                   match=got == g["block_fnv"])
+    if nj is not None:
+        got = f"{fnv(nj):016x}"
+        out["nj_match"] = got == g["nj_fnv"]
+        out["match"] = out["match"] and out["nj_match"]
+    return out
 
 
 def main():
@@ -256,14 +312,19 @@ def main():
                     help="testing aid: override k (the line's config then names the override)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: one rank per GPU via torchrun
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
-    import paper_2308_02856_b200 as P
+    from workloads import CONFIGS  # plain data: the reference arm loads no product code
 
     cid = args.config
-    c = dict(P.CONFIGS[cid])
+    c = dict(CONFIGS[cid])
     if args.rounds:
         c["n"] = args.rounds
         c["rounds_override"] = True
@@ -275,6 +336,8 @@ def main():
             run_reference(args, cid, c)
         return
 
+    import paper_2308_02856_b200 as P
+
     if args.engine == "lop3":  # read by every plan this process creates (shard owners too)
         os.environ["SSBH_HASH_ENGINE"] = "lop3"
     import torch
@@ -285,6 +348,7 @@ def main():
     P.lib.ssbh_set_device(dev_index)
     backend = os.environ.get("SSBH_DIST_BACKEND", "nccl")  # gloo: multi-rank test on 1 GPU
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator ranks in the log
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:
@@ -487,6 +551,10 @@ def main():
     else:
         full = d_key.view(torch.int64)[:key_words64].cpu().numpy().view("uint64")
     key_sha = hashlib.sha256(full.tobytes()).hexdigest()[:16]
+    digest = None
+    if rank == 0:
+        nj_host = d_len[:count].cpu().numpy().view("uint64") if world == 1 else None
+        digest = reference_digest(cid, c, full, nj_host, P.fnv1a64)
 
     vals = torch.tensor([total_ms, e2e_s, max(hash_ms)], dtype=torch.float64, device=coll_dev)
     if world > 1:
@@ -547,10 +615,11 @@ def main():
                                 "hash kernel's operand layouts"),
                 "int_alu_equivalent": {"achieved": achieved / 1e12, "peak": peak / 1e12,
                                        "unit": "T LOP3 word-ops/s",
-                                       "frac": achieved / peak,
-                                       "note": "the same work counted as the north_star LOP3 "
-                                               "roofline; > 1 because the tensor cores do "
-                                               "the GF(2) product faster than the ALUs"},
+                                       "times_lop3_peak": achieved / peak,
+                                       "note": "not a roofline fraction: the direct-form work "
+                                               "counted in north_star's LOP3 unit, divided by "
+                                               "the live LOP3 peak (how many LOP3-peak GPUs "
+                                               "this hash equals)"},
                 "hbm_term_ms": hbm_ms,
             }
         else:
@@ -579,12 +648,13 @@ def main():
                       "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)"),
             "hash_engine": "tensor" if tensor else "lop3",
             "data": "synthetic (KeyedStream input on device, seeds per BASELINE/SURVEY §8a)",
-            "config": dict(config_dict(cid, c, world), multi_gpu=(
+            "config": config_dict(cid, c, world),
+            "multi_gpu": (
                 "sharded sampling: each rank samples n/N rounds, payloads stored into the "
                 "owning rank by NVLink peer stores (IPC), owners hash their blocks"
                 if sharded else ("streaming plan, 8 input chunks" if streaming else
                                  "single plan" if world == 1 else
-                                 "replicated sampling, owned blocks hashed per rank"))),
+                                 "replicated sampling, owned blocks hashed per rank")),
             "roofline": roof,
             "phases_ms_last_step": {"sample_count_scan_layout": stats.ms_sample,
                                     "scatter": stats.ms_scatter, "seeds": stats.ms_seed,
@@ -593,6 +663,8 @@ def main():
             "sampler": sampler_line(n, world, stats, sharded),
             "gpu_launches": int(stats.launches) * args.steps,
             "key_sha256_16": key_sha,
+            "key_matches_reference_digest": digest["match"],
+            "reference_digest": digest,
             "clocks": clk,
         }
         if lop3_cmp is not None:

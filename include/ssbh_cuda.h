@@ -100,6 +100,11 @@ ssbh_status ssbh_binomial_tail_bound(uint64_t n_rounds, uint64_t limit, double p
 ssbh_status ssbh_relative_entropy(double x, double p, double* out);
 int ssbh_abort_check(const uint64_t* lengths, uint64_t count, uint64_t limit);
 
+/* Key digest used by reports and golden fixtures (not a reference entry point): FNV-1a-64
+ * over the little-endian bytes of `count` u64 words (offset 0xcbf29ce484222325, prime
+ * 0x100000001b3). Host memory, host computation. */
+uint64_t ssbh_fnv1a64(const uint64_t* words, uint64_t count);
+
 /* ----------------------------------------------------------------- toeplitz */
 /* Reference: toeplitz_hash — proj/include/ssbh/toeplitz.hpp:27, proj/src/toeplitz.cpp:34-52
  * (and ToeplitzSeed validation toeplitz.cpp:9-15): K = T x over GF(2) with

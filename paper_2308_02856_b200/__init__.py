@@ -51,7 +51,7 @@ ABI_SYMBOLS = (
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
     "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2", "ssbh_measure_mma_f4_peak",
     "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel", "ssbh_shard_hash_kernel",
-    "ssbh_plan_split_geometry", "ssbh_shard_split_geometry",
+    "ssbh_plan_split_geometry", "ssbh_shard_split_geometry", "ssbh_fnv1a64",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
@@ -141,6 +141,8 @@ def _load():
     L.ssbh_device_count.restype = C.c_int
     L.ssbh_set_device.restype = st
     L.ssbh_set_device.argtypes = [C.c_int]
+    L.ssbh_fnv1a64.restype = C.c_uint64
+    L.ssbh_fnv1a64.argtypes = [U64P, C.c_uint64]
     L.ssbh_prf_block.restype = st
     L.ssbh_prf_block.argtypes = [U64P, U64P, U64P]
     L.ssbh_plan_set_engine.restype = st
@@ -729,6 +731,12 @@ def measure_mma_i8_peak(iters: int = 4000, layout: int = 0, pairs: bool = False)
     return r.value, ms.value
 
 
+def fnv1a64(words) -> int:
+    """FNV-1a-64 key digest (ssbh_fnv1a64; host computation over u64 words)."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    return int(lib.ssbh_fnv1a64(w.ctypes.data_as(U64P), w.size))
+
+
 def measure_mma_f4_peak(iters: int = 200000):
     """Measured tcgen05 kind::mxf4 MAC/s with the FP4 hash kernel's operand layouts."""
     r, ms = C.c_double(0), C.c_double(0)
@@ -736,15 +744,16 @@ def measure_mma_f4_peak(iters: int = 200000):
     return r.value, ms.value
 
 
-# BASELINE.json configs (seeds per SURVEY §8a / Appendix A4)
-CONFIGS = {
-    1: dict(n=1 << 20, s=64, k=8192, p=0.5, seed_in=1, seed_samp=2, seed_hash=3, per_block=False),
-    2: dict(n=1 << 24, s=256, k=32768, p=0.3, seed_in=11, seed_samp=2, seed_hash=3,
-            per_block=False),
-    3: dict(n=1 << 30, s=1024, k=1 << 19, p=0.5, seed_in=1, seed_samp=2, seed_hash=3,
-            per_block=False),
-    4: dict(n=1 << 34, s=16384, k=3 << 18, p=0.4, seed_in=1, seed_samp=2, seed_hash=3,
-            per_block=True),
-    5: dict(n=1 << 37, s=32768, k=1 << 21, p=0.5, seed_in=1, seed_samp=2, seed_hash=3,
-            per_block=False),
-}
+# BASELINE.json configs: one table in workloads.py at the repo root (plain data, so that
+# bench.py's reference arm reads it without loading this package's CUDA library)
+def _load_configs():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "_ssbh_workloads", os.path.join(os.path.dirname(HERE), "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.CONFIGS
+
+
+CONFIGS = _load_configs()

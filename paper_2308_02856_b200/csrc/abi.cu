@@ -275,6 +275,15 @@ extern "C" int ssbh_abort_check(const uint64_t* lengths, uint64_t count, uint64_
     return 1;
 }
 
+extern "C" uint64_t ssbh_fnv1a64(const uint64_t* words, uint64_t count) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (uint64_t i = 0; i < count; ++i) {
+        uint64_t w = words[i];
+        for (int b = 0; b < 8; ++b, w >>= 8) h = (h ^ (w & 0xff)) * 0x100000001b3ull;
+    }
+    return h;
+}
+
 extern "C" ssbh_status ssbh_cycle_estimate(uint64_t input_len, uint64_t output_len,
                                            uint64_t m_prime, uint64_t* out) {
     if (m_prime == 0)
@@ -491,18 +500,36 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         // SSBH_MMA_SPLIT=L forces (0 disables). Shared-seed leaves run on the all-blocks GEMM
         // (default) or the tiled kernel (SSBH_MMA_SPLIT_LEAF=pb, dev A/B knob).
         const char* sl = std::getenv("SSBH_MMA_SPLIT_LEAF");
-        const bool gemm = !params->per_block_seed && !(sl && std::strcmp(sl, "pb") == 0);
+        bool gemm = !params->per_block_seed && !(sl && std::strcmp(sl, "pb") == 0);
         const char* se = std::getenv("SSBH_MMA_SPLIT");
-        const uint32_t L =
-            se && *se ? (uint32_t)std::strtoul(se, nullptr, 10) : split_levels(k, gemm);
+        const bool forced = se && *se;
+        uint32_t L = forced ? (uint32_t)std::strtoul(se, nullptr, 10) : split_levels(k, gemm);
         pl->split = (gemm || pl->shared_pb || params->per_block_seed) &&
                     pl->engine == kEngineMma && mma_uses_fp4() && split_applicable(k, mean_nj, L);
         if (pl->split) {
             const char* sb = std::getenv("SSBH_MMA_SPLIT_MB");  // leaf buffer budget, default 8 GB
             const uint64_t budget =
                 (sb && *sb ? (uint64_t)std::strtoull(sb, nullptr, 10) : 8192ull) << 20;
+            const bool pb_ok = pl->shared_pb || params->per_block_seed;
             pl->sg = make_split_geom(nown, k, mean_nj, L, params->per_block_seed != 0, gemm,
                                      budget);
+            // a batch the budget cannot hold (few, very long blocks: GEMM groups are padded to
+            // 128 blocks; 3^L leaves of one square grow as 1.5^L): tiled leaves, then fewer
+            // levels, then the direct kernel
+            if (pl->sg.bytes > budget && gemm && pb_ok) {
+                gemm = false;
+                pl->sg = make_split_geom(nown, k, mean_nj, L, params->per_block_seed != 0, false,
+                                         budget);
+            }
+            while (pl->sg.bytes > budget && L > 1 && !forced) {
+                --L;
+                pl->sg = make_split_geom(nown, k, mean_nj, L, params->per_block_seed != 0, gemm,
+                                         budget);
+            }
+            if (pl->sg.bytes > budget && !forced)
+                pl->split = false;
+        }
+        if (pl->split) {
             const uint32_t lw = (uint32_t)(pl->sg.sL / 32);
             if (pl->sg.gemm) {
                 pl->mmv = make_mma_geom((uint32_t)pl->sg.nvirt, lw, pl->sg.sL, pl->device);

@@ -252,6 +252,7 @@ struct SplitGeom {
     uint32_t gpad;           // virtual blocks per (t, path) group: batch, 128-aligned for gemm;
                              // virtual block v = (t * leaves + path) * gpad + jl
     uint64_t vlw;            // u32 words per leaf input (sL / 32, 16-aligned for gemm)
+    uint64_t bytes;          // leaf inputs + outputs + seeds one batch allocates
 };
 uint32_t split_levels(uint64_t k, bool gemm);  // 0 = not worth it
 SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L,

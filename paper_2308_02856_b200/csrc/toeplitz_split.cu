@@ -314,13 +314,19 @@ SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t 
     // matrix-vector product (tiled kernel).
     g.gemm = !per_block && gemm_leaves;
     g.vlw = g.gemm ? (g.sL / 32 + 15) / 16 * 16 : g.sL / 32;
-    // blocks per batch: leaf inputs + leaf outputs (+ leaf seeds) within the budget
+    // blocks per batch within the budget, counted on what the plan allocates: leaf inputs and
+    // outputs for gpad (not batch) blocks per (t, path) group, plus the leaf seeds (per leaf
+    // for per-block seeds, per (t, path) for a shared seed)
     const uint64_t per_blk = (uint64_t)g.T * g.leaves *
                              (g.vlw * 4 + g.sL / 8 + (per_block ? g.seed_words * 4 : 0));
-    g.batch = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nown, budget_bytes / per_blk));
-    if (g.gemm && g.batch < nown && g.batch >= 128) g.batch = g.batch / 128 * 128;
+    const uint64_t fixed = per_block ? 0 : (uint64_t)g.T * g.leaves * g.seed_words * 4;
+    const uint64_t avail = budget_bytes > fixed ? budget_bytes - fixed : 0;
+    uint64_t b = std::max<uint64_t>(1, std::min<uint64_t>(nown, avail / per_blk));
+    if (g.gemm && b < nown) b = std::max<uint64_t>(128, b / 128 * 128);
+    g.batch = (uint32_t)std::min<uint64_t>(b, nown);
     g.gpad = g.gemm ? (g.batch + 127) / 128 * 128 : g.batch;
     g.nvirt = (uint64_t)g.gpad * g.T * g.leaves;
+    g.bytes = g.gpad * per_blk + fixed;
     return g;
 }
 

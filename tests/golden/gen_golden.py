@@ -87,6 +87,8 @@ def main():
     ap.add_argument("--config5", action="store_true")
     ap.add_argument("--pipeline", action="store_true",
                     help="run_extraction / simulate_rounds cases (pipeline.cpp)")
+    ap.add_argument("--split", action="store_true",
+                    help="shapes that take the 3-for-4 split path (k >= 2^18, T >= 1 squares)")
     ap.add_argument("--only-large", action="store_true", help="skip the small vectors")
     args = ap.parse_args()
     ref, o = Reference(), Oracle()
@@ -147,8 +149,16 @@ def main():
     cfgs["small_perblock"] = (100000, 16, 1000, 0.5, 7, 8, 9, 1)
     cfgs["small_k_odd"] = (50000, 8, 77, 0.5, 7, 8, 9, 0)
     cfgs["small_k_32"] = (70000, 32, 96, 0.3, 7, 8, 9, 0)
+    # 3-for-4 split shapes (csrc/toeplitz_split.cu runs them; the reference hashes them directly)
+    split = {"split_smoke": (1 << 20, 2, 1 << 18, 0.5, 31, 32, 33, 0),
+             "split_t2": ((1 << 24) + 777, 16, 1 << 19, 0.5, 22, 7, 8, 0),
+             "split_deep": ((1 << 24) + 4097, 16, 1 << 19, 0.5, 25, 13, 14, 0),
+             "split_perblock": ((1 << 24) + 777, 16, 3 << 17, 0.5, 24, 11, 12, 1)}
+    todo = {} if args.only_large else dict(cfgs)
+    if args.split:
+        todo = dict(split) if args.only_large else {**todo, **split}
     ext = g.get("extract", {})
-    for name, (n, s, k, p, si, ss, sh, pb) in ([] if args.only_large else cfgs.items()):
+    for name, (n, s, k, p, si, ss, sh, pb) in todo.items():
         x = o.make_input(si, p, n)
         t = time.time()
         key, nj = ref.extract(x, n, s, ss, sh, pb, k)

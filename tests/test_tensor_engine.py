@@ -231,6 +231,48 @@ def test_split_per_block_seeds(dev, oracle, levels, budget_mb, monkeypatch):
     assert (keys[0] == keys[1]).all()
 
 
+@pytest.mark.parametrize("name,levels", [("split_smoke", None), ("split_t2", None),
+                                         ("split_deep", 7), ("split_deep", 3),
+                                         ("split_perblock", None), ("split_perblock", 2)])
+def test_split_reference_digests(dev, oracle, golden, name, levels, monkeypatch):
+    """The headline path — the 3-for-4 split (csrc/toeplitz_split.cu: leaf GEMMs / tiled
+    leaves, remainder, level combine) — against digests made by running the compiled
+    reference (toeplitz.cpp:34-52 hashing every block directly; gen_golden.py --split)."""
+    if levels is None:
+        monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)
+    else:
+        monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
+    c = golden["extract"][name]
+    n, s, k = c["n"], c["s"], c["k"]
+    x = oracle.make_input(c["seed_in"], c["p"], n)
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=bool(c["per_block"]))
+    if _split_possible() and os.environ.get("SSBH_HASH_ENGINE") != "lop3":
+        assert plan.hash_kernel.endswith("+split"), plan.hash_kernel
+        if levels is not None:
+            assert plan.split_geometry[0] == levels
+    key, nj, _ = plan.run_host(x)
+    plan.close()
+    assert f"{oracle.fnv(nj):016x}" == c["nj_fnv"]
+    assert int(np.unpackbits(key.view(np.uint8)).sum()) == c["key_popcount"]
+    assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
+
+
+def test_split_budget_few_long_blocks(dev, monkeypatch):
+    """Few very long shared-seed blocks: GEMM leaf groups are padded to 128 blocks, so the
+    leaf budget (SSBH_MMA_SPLIT_MB, default 8 GB) is charged for the padded batch and the plan
+    falls back to tiled leaves / fewer levels instead of allocating ~390 GB (s = 4,
+    n = 2^32, k = 2^19: T = 2048 squares per block)."""
+    monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)
+    monkeypatch.delenv("SSBH_MMA_SPLIT_MB", raising=False)
+    n = 1 << 32
+    plan = dev.Plan(n, 4, 1 << 19, 2, 3)
+    kernel, geom, nbytes = plan.hash_kernel, plan.split_geometry, plan.device_bytes
+    plan.close()
+    # payload (2 B/round) + reversed blocks + seed + key + the leaf budget
+    assert nbytes < 2 * n + n // 8 * 2 + (8 << 30) + (1 << 30), (kernel, geom, nbytes)
+    assert kernel.endswith("+split"), kernel
+
+
 def test_split_disabled_by_env(dev, monkeypatch):
     """SSBH_MMA_SPLIT=0 keeps long shared blocks on the direct tiled kernel."""
     monkeypatch.setenv("SSBH_MMA_SPLIT", "0")
