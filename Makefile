@@ -17,7 +17,7 @@ HOST_SRCS:= $(CSRC)/host/ssbh_api.cpp $(CSRC)/host/ssbh_pipeline.cpp
 HDRS_API := $(wildcard include/ssbh/*.hpp)
 CUDA_LIB := /usr/local/cuda/lib64
 
-all: $(PKG)/libssbh_cuda.so $(PKG)/libssbh.so $(PKG)/ssbh-b200 oracle cpptests
+all: $(PKG)/libssbh_cuda.so $(PKG)/libssbh.so $(PKG)/ssbh-b200 oracle cpptests tools/call_overhead
 
 # CLI (file-mode extract + bench analogue of proj/tools/ssbh_main.cpp)
 $(PKG)/ssbh-b200: $(CSRC)/host/ssbh_cli.cpp $(HDRS_API) $(PKG)/libssbh.so
@@ -33,6 +33,10 @@ $(PKG)/libssbh_cuda.so: $(CU_OBJS)
 $(PKG)/libssbh.so: $(HOST_SRCS) $(HDRS_API) include/ssbh_cuda.h $(PKG)/libssbh_cuda.so
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(HOST_SRCS) \
 	    -L$(PKG) -lssbh_cuda -Wl,-rpath,'$$ORIGIN'
+
+tools/call_overhead: tools/call_overhead.cpp $(HDRS_API) $(PKG)/libssbh.so
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(PKG) -lssbh -lssbh_cuda \
+	    -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 CPP_TESTS := $(patsubst tests/cpp/%.cpp,tests/cpp/bin/%,$(wildcard tests/cpp/test_*.cpp))
 cpptests: $(CPP_TESTS)

@@ -131,6 +131,19 @@ ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, const uint64_t*
                                      const uint64_t* seeds, const uint64_t* seed_off,
                                      uint64_t* out);
 
+/* The same batch with one host pointer per block (no host-side concatenation: each block's
+ * input and seed are copied straight from the caller's BitStrings); what the C++ drop-in's
+ * toeplitz_hash_batch (include/ssbh/extract.hpp) binds. */
+ssbh_status ssbh_toeplitz_hash_batch_ptrs(uint64_t count, uint64_t m, const uint64_t* n,
+                                          const uint64_t* const* inputs,
+                                          const uint64_t* const* seeds, uint64_t* out);
+
+/* The reference-facing calls above (toeplitz_hash, KeyedStream::bits, assign_subblocks,
+ * sift_partition, ...) keep a per-thread, per-device stream and device arena between calls,
+ * so that steady-state calls allocate nothing. This frees the calling thread's arenas (they
+ * are also freed when the thread exits). */
+ssbh_status ssbh_release_thread_cache(void);
+
 /* -------------------------------------------------------- fused extraction */
 /* The whole file-mode hot path (ssbh_main.cpp:306-345 with distinct seeds):
  * assign_subblocks(n, s, samp) -> sift (all kept, or keep mask) -> per block j gather ->

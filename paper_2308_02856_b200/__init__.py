@@ -52,6 +52,7 @@ ABI_SYMBOLS = (
     "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2", "ssbh_measure_mma_f4_peak",
     "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel", "ssbh_shard_hash_kernel",
     "ssbh_plan_split_geometry", "ssbh_shard_split_geometry", "ssbh_fnv1a64",
+    "ssbh_toeplitz_hash_batch_ptrs", "ssbh_release_thread_cache",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2

@@ -111,7 +111,118 @@ struct DBuf {
 uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 uint64_t words64(uint64_t bits) { return (bits + 63) / 64; }
 
+// ---- per-thread call context of the reference-facing entry points ----------------------
+// toeplitz_hash, KeyedStream::bits, assign_subblocks, sift_partition ... are called once per
+// block by the reference's own callers (pipeline.cpp:129-136), so their fixed cost matters.
+// Each thread keeps, per device, a non-blocking stream and a device arena that survives the
+// call: buffers of one call are carved from it (256-B aligned), nothing is cudaMalloc'ed or
+// freed in steady state, and every copy/launch of the call is ordered on the thread's stream
+// (no legacy-stream device-wide syncs, so threads calling concurrently overlap). An arena
+// that runs out mid-call chains one more block; at the end of the call the blocks are merged
+// into one of the combined size for the next call.
+struct CallArena {
+    struct Blk {
+        char* p;
+        size_t cap, used;
+    };
+    int device = -1;
+    cudaStream_t st = nullptr;
+    std::vector<Blk> blks;
+    size_t want = 0;  // capacity of the merged block to allocate at the next call
+    int depth = 0;
+
+    cudaError_t take(size_t bytes, void** out) {
+        bytes = round_up(bytes ? bytes : 16, 256);
+        if (blks.empty() || blks.back().used + bytes > blks.back().cap) {
+            size_t cap = std::max(bytes, want);
+            want = 0;
+            if (!blks.empty()) cap = std::max(bytes, blks.back().cap);
+            Blk b{nullptr, cap, 0};
+            if (cudaError_t e = cudaMalloc(&b.p, cap)) return e;
+            blks.push_back(b);
+        }
+        *out = blks.back().p + blks.back().used;
+        blks.back().used += bytes;
+        return cudaSuccess;
+    }
+    void end_call() {  // the call's work is complete (every entry point synchronises)
+        for (auto& b : blks) b.used = 0;
+        if (blks.size() > 1) {
+            size_t tot = 0;
+            for (auto& b : blks) {
+                tot += b.cap;
+                cudaFree(b.p);
+            }
+            blks.clear();
+            want = tot;
+        }
+    }
+    void release() {
+        for (auto& b : blks) cudaFree(b.p);
+        blks.clear();
+        want = 0;
+        if (st) cudaStreamDestroy(st);
+        st = nullptr;
+    }
+    ~CallArena() { release(); }  // thread exit (errors during process teardown are ignored)
+};
+
+struct CallCtx {
+    std::vector<std::unique_ptr<CallArena>> per_dev;
+    CallArena* cur = nullptr;
+};
+thread_local CallCtx g_call;
+
+// Opens the calling thread's context on the current device for one entry-point call.
+struct CallScope {
+    CallArena* a = nullptr;
+    cudaError_t err = cudaSuccess;
+    CallScope() {
+        int dev = 0;
+        if ((err = cudaGetDevice(&dev))) return;
+        if ((size_t)dev >= g_call.per_dev.size()) g_call.per_dev.resize(dev + 1);
+        auto& slot = g_call.per_dev[dev];
+        if (!slot) {
+            slot.reset(new CallArena());
+            slot->device = dev;
+            if ((err = cudaStreamCreateWithFlags(&slot->st, cudaStreamNonBlocking))) return;
+        }
+        a = slot.get();
+        ++a->depth;
+    }
+    ~CallScope() {
+        if (a && --a->depth == 0) {
+            cudaStreamSynchronize(a->st);
+            a->end_call();
+        }
+    }
+    cudaStream_t stream() const { return a->st; }
+};
+
+// Arena-backed buffer with DBuf's interface (valid until the enclosing CallScope ends).
+struct SBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t alloc(size_t b) {
+        bytes = b ? b : 16;
+        int dev = 0;
+        if (cudaError_t e = cudaGetDevice(&dev)) return e;
+        CallArena* a = (size_t)dev < g_call.per_dev.size() ? g_call.per_dev[dev].get() : nullptr;
+        if (!a || !a->depth) return cudaErrorInvalidValue;  // only inside a CallScope
+        return a->take(bytes, &p);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 }  // namespace
+
+#define CALL_SCOPE(name)                                                                   \
+    CallScope name;                                                                        \
+    if (name.err)                                                                          \
+        return fail(SSBH_CUDA, "call context: %s", cudaGetErrorString(name.err));
 
 // ======================================================================== runtime
 extern "C" int ssbh_abi_version(void) { return SSBH_ABI_VERSION; }
@@ -143,13 +254,16 @@ extern "C" ssbh_status ssbh_stream_bits(const uint64_t key[4], uint64_t tag, uin
                                         uint64_t nbits, uint64_t* out_words) {
     if (nbits == 0) return ok();
     NEED_DEVICE();
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
     const uint64_t w64 = words64(nbits);
-    DBuf d;
+    SBuf d;
     CU(d.alloc(w64 * 8));
-    CU(cudaMemset(d.p, 0, w64 * 8));
-    launch_stream_bits(key, tag, sub, nbits, d.as<uint32_t>(), 0);
+    CU(cudaMemsetAsync(d.p, 0, w64 * 8, st));
+    launch_stream_bits(key, tag, sub, nbits, d.as<uint32_t>(), st);
     if (auto s = check_launch("stream_bits")) return s;
-    CU(cudaMemcpy(out_words, d.p, w64 * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(out_words, d.p, w64 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return ok();
 }
 
@@ -157,11 +271,14 @@ extern "C" ssbh_status ssbh_stream_words(const uint64_t key[4], uint64_t tag, ui
                                          uint64_t first, uint64_t count, uint64_t* out) {
     if (count == 0) return ok();
     NEED_DEVICE();
-    DBuf d;
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
+    SBuf d;
     CU(d.alloc(count * 8));
-    launch_stream_words(key, tag, sub, first, count, d.as<uint64_t>(), 0);
+    launch_stream_words(key, tag, sub, first, count, d.as<uint64_t>(), st);
     if (auto s = check_launch("stream_words")) return s;
-    CU(cudaMemcpy(out, d.p, count * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(out, d.p, count * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return ok();
 }
 
@@ -171,11 +288,14 @@ extern "C" ssbh_status ssbh_stream_uniform_below(const uint64_t key[4], uint64_t
     if (bound == 0) return fail(SSBH_INVALID_ARGUMENT, "uniform_below: bound must be positive");
     if (count == 0) return ok();
     NEED_DEVICE();
-    DBuf d;
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
+    SBuf d;
     CU(d.alloc(count * 8));
-    launch_stream_uniform(key, tag, sub, bound, first, count, d.as<uint64_t>(), 0);
+    launch_stream_uniform(key, tag, sub, bound, first, count, d.as<uint64_t>(), st);
     if (auto s = check_launch("stream_uniform")) return s;
-    CU(cudaMemcpy(out, d.p, count * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(out, d.p, count * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return ok();
 }
 
@@ -185,13 +305,16 @@ extern "C" ssbh_status ssbh_stream_bernoulli(const uint64_t key[4], uint64_t tag
     if (p < 0.0 || p > 1.0) return fail(SSBH_INVALID_ARGUMENT, "bernoulli: p outside [0,1]");
     if (count == 0) return ok();
     NEED_DEVICE();
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
     const uint64_t w64 = words64(count);
-    DBuf d;
+    SBuf d;
     CU(d.alloc(w64 * 8));
-    CU(cudaMemset(d.p, 0, w64 * 8));
-    launch_stream_bernoulli(key, tag, sub, p, first, count, d.as<uint32_t>(), 0);
+    CU(cudaMemsetAsync(d.p, 0, w64 * 8, st));
+    launch_stream_bernoulli(key, tag, sub, p, first, count, d.as<uint32_t>(), st);
     if (auto s = check_launch("stream_bernoulli")) return s;
-    CU(cudaMemcpy(out_words, d.p, w64 * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(out_words, d.p, w64 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return ok();
 }
 
@@ -300,8 +423,9 @@ extern "C" ssbh_status ssbh_cycle_estimate(uint64_t input_len, uint64_t output_l
 // ======================================================================== device layout
 namespace {
 
-struct LayoutBufs {
-    DBuf nj, yoff, ypad, ktl, items, soff, stats;
+template <class Buf>
+struct LayoutBufsT {
+    Buf nj, yoff, ypad, ktl, items, soff, stats;
     cudaError_t alloc(uint32_t nown) {
         cudaError_t e;
         if ((e = nj.alloc((size_t)nown * 8 + 8))) return e;
@@ -315,16 +439,18 @@ struct LayoutBufs {
     }
     Layout view() const {
         Layout l;
-        l.nj = nj.as<unsigned long long>();
-        l.yoff = yoff.as<unsigned long long>();
-        l.ypad = ypad.as<uint32_t>();
-        l.ktl = ktl.as<uint32_t>();
-        l.items = items.as<unsigned long long>();
-        l.soff = soff.as<unsigned long long>();
-        l.stats = stats.as<DevStats>();
+        l.nj = nj.template as<unsigned long long>();
+        l.yoff = yoff.template as<unsigned long long>();
+        l.ypad = ypad.template as<uint32_t>();
+        l.ktl = ktl.template as<uint32_t>();
+        l.items = items.template as<unsigned long long>();
+        l.soff = soff.template as<unsigned long long>();
+        l.stats = stats.template as<DevStats>();
         return l;
     }
 };
+using LayoutBufs = LayoutBufsT<DBuf>;   // plans: owned for the plan's lifetime
+using LayoutScratch = LayoutBufsT<SBuf>;  // one call (CallScope arena)
 
 // Choose the k-tile so that the persistent grid gets enough items (>= ~16 per CTA)
 // while keeping tiles long enough to amortise per-item overhead.
@@ -487,7 +613,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     pl->key_words32 = ((uint64_t)nown * k + 31) / 32;
     pl->engine = default_engine(params->per_block_seed);
     pl->mma = make_mma_geom(nown, pl->kw, mean_nj, pl->device);
-    pl->pb = make_pb_geom(nown, pl->kw, pl->device);
+    pl->pb = make_pb_geom(nown, pl->kw, pl->device, mean_nj);
     // Long shared-seed blocks: the tiled matrix-vector kernel keeps each block's y chunks in
     // shared memory for 256 D steps instead of re-expanding them for every 256-row tile (config
     // 3: hash 155 -> 145 ms); its window ramp (255 D steps per item) costs < 5 % once the mean
@@ -537,7 +663,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
                 pl->mmr = make_mma_geom(nown, pl->kw, mean_nj > tk ? mean_nj - tk : 1, pl->device);
             }
             else
-                pl->pbv = make_pb_geom((uint32_t)pl->sg.nvirt, lw, pl->device);
+                pl->pbv = make_pb_geom((uint32_t)pl->sg.nvirt, lw, pl->device, pl->sg.sL);
         }
     }
 
@@ -1242,20 +1368,23 @@ extern "C" ssbh_status ssbh_assign_subblocks(uint64_t n, uint32_t s, const uint6
         return ok();
     }
     NEED_DEVICE();
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
     const SamplerGeom g = make_sampler_geom(n, s, 0, s, false);
-    DBuf assign, counts, gsum, nj;
+    SBuf assign, counts, gsum, nj;
     CU(assign.alloc((size_t)n * 4));
     CU(counts.alloc((size_t)g.nchunks * s * 4));
     CU(gsum.alloc((size_t)g.ngroups * s * 8));
     CU(nj.alloc((size_t)s * 8));
-    CU(cudaMemset(counts.p, 0, counts.bytes));
+    CU(cudaMemsetAsync(counts.p, 0, counts.bytes, st));
     launch_sample_count(g, key, nullptr, nullptr, nullptr, counts.as<uint32_t>(),
-                        assign.as<uint32_t>(), 0);
+                        assign.as<uint32_t>(), st);
     launch_scan(g, counts.as<uint32_t>(), gsum.as<unsigned long long>(),
-                nj.as<unsigned long long>(), 0);
-    if (auto st = check_launch("assign_subblocks")) return st;
-    CU(cudaMemcpy(assignment, assign.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(raw_counts, nj.p, (size_t)s * 8, cudaMemcpyDeviceToHost));
+                nj.as<unsigned long long>(), st);
+    if (auto e_ = check_launch("assign_subblocks")) return e_;
+    CU(cudaMemcpyAsync(assignment, assign.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(raw_counts, nj.p, (size_t)s * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return ok();
 }
 
@@ -1279,13 +1408,15 @@ extern "C" ssbh_status ssbh_sift_partition(const uint8_t* keep, uint64_t n,
         return ok();
     }
     NEED_DEVICE();
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
     const SamplerGeom g = make_sampler_geom(n, s, 0, s, true);
-    DBuf dassign, dkeep, payload, counts, gsum, nj, off, idx, bad;
+    SBuf dassign, dkeep, payload, counts, gsum, nj, off, idx, bad;
     CU(dassign.alloc((size_t)n * 4));
-    CU(cudaMemcpy(dassign.p, assignment, (size_t)n * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(dassign.p, assignment, (size_t)n * 4, cudaMemcpyHostToDevice, st));
     if (keep) {
         CU(dkeep.alloc((size_t)n));
-        CU(cudaMemcpy(dkeep.p, keep, (size_t)n, cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(dkeep.p, keep, (size_t)n, cudaMemcpyHostToDevice, st));
     }
     CU(payload.alloc((size_t)n * 4));
     CU(counts.alloc((size_t)g.nchunks * s * 4));
@@ -1294,30 +1425,33 @@ extern "C" ssbh_status ssbh_sift_partition(const uint8_t* keep, uint64_t n,
     CU(off.alloc(((size_t)s + 1) * 8));
     CU(idx.alloc((size_t)n * 8));
     CU(bad.alloc(4));
-    CU(cudaMemset(counts.p, 0, counts.bytes));
-    CU(cudaMemset(bad.p, 0, 4));
+    CU(cudaMemsetAsync(counts.p, 0, counts.bytes, st));
+    CU(cudaMemsetAsync(bad.p, 0, 4, st));
     launch_payload_from_assignment(g, dassign.as<uint32_t>(), keep ? dkeep.as<uint8_t>() : nullptr,
                                    payload.as<uint32_t>(), counts.as<uint32_t>(),
-                                   bad.as<uint32_t>(), 0);
+                                   bad.as<uint32_t>(), st);
     uint32_t hbad = 0;
-    CU(cudaMemcpy(&hbad, bad.p, 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     if (hbad)
         return fail(SSBH_INVALID_ARGUMENT,
                     "sift_partition: assignment value outside [1, n_subblocks]");
     launch_scan(g, counts.as<uint32_t>(), gsum.as<unsigned long long>(),
-                nj.as<unsigned long long>(), 0);
-    launch_csr_offsets(nj.as<unsigned long long>(), s, off.as<unsigned long long>(), 0);
+                nj.as<unsigned long long>(), st);
+    launch_csr_offsets(nj.as<unsigned long long>(), s, off.as<unsigned long long>(), st);
     launch_scatter(g, payload.p, counts.as<uint32_t>(), nj.as<unsigned long long>(), nullptr,
-                   nullptr, idx.as<unsigned long long>(), off.as<unsigned long long>(), 0);
-    if (auto st = check_launch("sift_partition")) return st;
-    CU(cudaMemcpy(offsets, off.p, ((size_t)s + 1) * 8, cudaMemcpyDeviceToHost));
+                   nullptr, idx.as<unsigned long long>(), off.as<unsigned long long>(), st);
+    if (auto e_ = check_launch("sift_partition")) return e_;
+    CU(cudaMemcpyAsync(offsets, off.p, ((size_t)s + 1) * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     const uint64_t kept = offsets[s];
-    if (kept) CU(cudaMemcpy(indices, idx.p, kept * 8, cudaMemcpyDeviceToHost));
+    if (kept) CU(cudaMemcpyAsync(indices, idx.p, kept * 8, cudaMemcpyDeviceToHost, st));
     if (max_len) {
         uint64_t m = 0;
         for (uint32_t j = 0; j < s; ++j) m = std::max<uint64_t>(m, offsets[j + 1] - offsets[j]);
         *max_len = m;
     }
+    CU(cudaStreamSynchronize(st));
     return ok();
 }
 
@@ -1326,63 +1460,84 @@ namespace ssbh_impl {
 void launch_pack_blocks(const uint64_t* d_seeds, const unsigned long long* d_seed_off,
                         const uint64_t* d_inputs, const unsigned long long* d_in_off,
                         const Layout& lay, uint32_t count, uint64_t m, uint32_t* d_sbuf,
-                        uint32_t* d_ybuf, cudaStream_t st);
+                        uint32_t* d_ybuf, cudaStream_t st, uint64_t max_words);
 }
 
-extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, const uint64_t* n,
-                                                const uint64_t* inputs, const uint64_t* in_off,
-                                                const uint64_t* seeds, const uint64_t* seed_off,
-                                                uint64_t* out) {
+// One batched hash through the calling thread's CallScope: block b's input words come from
+// in_ptr[b] (or inputs + in_off[b]), its seed words from seed_ptr[b] (or seeds + seed_off[b]).
+static ssbh_status hash_batch_impl(uint64_t count, uint64_t m, const uint64_t* n,
+                                   const uint64_t* inputs, const uint64_t* in_off,
+                                   const uint64_t* const* in_ptr, const uint64_t* seeds,
+                                   const uint64_t* seed_off, const uint64_t* const* seed_ptr,
+                                   uint64_t* out) {
     if (m == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
     for (uint64_t b = 0; b < count; ++b)
         if (n[b] == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
     if (count == 0) return ok();
     if (count > (1u << 30)) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: batch too large");
     NEED_DEVICE();
+    CALL_SCOPE(scope);
+    const cudaStream_t st = scope.stream();
     int dev = 0;
     CU(cudaGetDevice(&dev));
     const uint32_t nown = (uint32_t)count;
     const uint32_t kw = (uint32_t)((m + 31) / 32);
     const uint32_t rowtiles = (kw + kHashRowWords - 1) / kHashRowWords;
-    uint64_t in_words = 0, seed_words = 0, sum_n = 0, ybound = 8, sbound = 8;
+    // device-side offsets: the contiguous form keeps the caller's, the pointer form packs
+    std::vector<uint64_t> meta(3 * count);  // n | in_off | seed_off
+    uint64_t in_words = 0, seed_words = 0, sum_n = 0, ybound = 8, sbound = 8, maxw = 0;
     for (uint64_t b = 0; b < count; ++b) {
-        in_words = std::max<uint64_t>(in_words, in_off[b] + words64(n[b]));
-        seed_words = std::max<uint64_t>(seed_words, seed_off[b] + words64(m + n[b] - 1));
+        const uint64_t iw = words64(n[b]), sw = words64(m + n[b] - 1);
+        meta[b] = n[b];
+        meta[count + b] = in_ptr ? in_words : in_off[b];
+        meta[2 * count + b] = seed_ptr ? seed_words : seed_off[b];
+        in_words = in_ptr ? in_words + iw : std::max<uint64_t>(in_words, in_off[b] + iw);
+        seed_words = seed_ptr ? seed_words + sw : std::max<uint64_t>(seed_words, seed_off[b] + sw);
         sum_n += n[b];
         const uint64_t yp = round_up((n[b] + 31) / 32, kHashR);
         ybound += yp;
         sbound += round_up((uint64_t)rowtiles * kHashRowWords + 8 + yp, 8);
+        maxw = std::max<uint64_t>(maxw, 2 * sw);
     }
-    LayoutBufs lb;
-    DBuf din, dseeds, dinoff, dseedoff, ybuf, sbuf, scratch, key;
+    LayoutScratch lb;
+    SBuf din, dseeds, dmeta, ybuf, sbuf, scratch, key;
     CU(lb.alloc(nown));
     CU(din.alloc(in_words * 8));
     CU(dseeds.alloc(seed_words * 8));
-    CU(dinoff.alloc(count * 8));
-    CU(dseedoff.alloc(count * 8));
+    CU(dmeta.alloc(count * 24));
     CU(ybuf.alloc(ybound * 4));
     CU(sbuf.alloc((sbound + 64) * 4));  // + the tensor kernels' read-ahead of unused units
     CU(scratch.alloc((size_t)nown * kw * 4));
     const uint64_t key_w64 = words64(count * m);
     CU(key.alloc(key_w64 * 8));
-    CU(cudaMemcpy(din.p, inputs, in_words * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(dseeds.p, seeds, seed_words * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(dinoff.p, in_off, count * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(dseedoff.p, seed_off, count * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(lb.nj.p, n, count * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemset(ybuf.p, 0, ybuf.bytes));
-    CU(cudaMemset(sbuf.p, 0, sbuf.bytes));
-    CU(cudaMemset(scratch.p, 0, scratch.bytes));
-    CU(cudaMemset(key.p, 0, key.bytes));
+    if (in_ptr) {
+        for (uint64_t b = 0; b < count; ++b)
+            CU(cudaMemcpyAsync(din.as<uint64_t>() + meta[count + b], in_ptr[b],
+                               words64(n[b]) * 8, cudaMemcpyHostToDevice, st));
+    } else {
+        CU(cudaMemcpyAsync(din.p, inputs, in_words * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (seed_ptr) {
+        for (uint64_t b = 0; b < count; ++b)
+            CU(cudaMemcpyAsync(dseeds.as<uint64_t>() + meta[2 * count + b], seed_ptr[b],
+                               words64(m + n[b] - 1) * 8, cudaMemcpyHostToDevice, st));
+    } else {
+        CU(cudaMemcpyAsync(dseeds.p, seeds, seed_words * 8, cudaMemcpyHostToDevice, st));
+    }
+    CU(cudaMemcpyAsync(dmeta.p, meta.data(), count * 24, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(lb.nj.p, meta.data(), count * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(ybuf.p, 0, ybuf.bytes, st));
+    CU(cudaMemsetAsync(sbuf.p, 0, sbuf.bytes, st));
+    CU(cudaMemsetAsync(key.p, 0, key.bytes, st));
     const Layout lay = lb.view();
     const int grid = hash_grid_size(dev);
     const uint32_t kt = choose_kt(sum_n / count, nown, rowtiles, grid);
-    launch_layout(lay, nown, m, rowtiles, kt, 1, 0, 0);
-    launch_pack_blocks(dseeds.as<uint64_t>(), dseedoff.as<unsigned long long>(),
-                       din.as<uint64_t>(), dinoff.as<unsigned long long>(), lay, nown, m,
-                       sbuf.as<uint32_t>(), ybuf.as<uint32_t>(), 0);
+    launch_layout(lay, nown, m, rowtiles, kt, 1, 0, st);
+    launch_pack_blocks(dseeds.as<uint64_t>(), dmeta.as<unsigned long long>() + 2 * count,
+                       din.as<uint64_t>(), dmeta.as<unsigned long long>() + count, lay, nown, m,
+                       sbuf.as<uint32_t>(), ybuf.as<uint32_t>(), st, maxw);
     if (default_engine(1) == kEngineMma) {  // every block its own matrix: tiled matvec MMAs
-        const PbGeom pg = make_pb_geom(nown, kw, dev);
+        const PbGeom pg = make_pb_geom(nown, kw, dev, sum_n / count);
         PbHashArgs a{};
         a.ybuf = ybuf.as<uint32_t>();
         a.sbuf = sbuf.as<uint32_t>();
@@ -1393,9 +1548,9 @@ extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, cons
         a.kw = kw;
         a.ntiles = pg.ntiles;
         a.nwin = pg.nwin;
-        a.items = pg.items;
-        launch_hash_mma_pb(a, pg, 0);
+        launch_hash_mma_pb(a, pg, st);
     } else {
+        CU(cudaMemsetAsync(scratch.p, 0, scratch.bytes, st));
         HashArgs a{};
         a.ybuf = ybuf.as<uint32_t>();
         a.sbuf = sbuf.as<uint32_t>();
@@ -1406,11 +1561,33 @@ extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, cons
         a.kw = kw;
         a.rowtiles = rowtiles;
         a.per_block_seed = 1;
-        launch_hash(a, grid, 0);
+        launch_hash(a, grid, st);
     }
-    launch_concat(scratch.as<uint32_t>(), kw, nown, m, key.as<uint32_t>(), 0);
-    if (auto st = check_launch("toeplitz_hash")) return st;
-    CU(cudaMemcpy(out, key.p, key_w64 * 8, cudaMemcpyDeviceToHost));
+    launch_concat(scratch.as<uint32_t>(), kw, nown, m, key.as<uint32_t>(), st);
+    if (auto e = check_launch("toeplitz_hash")) return e;
+    CU(cudaMemcpyAsync(out, key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_toeplitz_hash_batch(uint64_t count, uint64_t m, const uint64_t* n,
+                                                const uint64_t* inputs, const uint64_t* in_off,
+                                                const uint64_t* seeds, const uint64_t* seed_off,
+                                                uint64_t* out) {
+    return hash_batch_impl(count, m, n, inputs, in_off, nullptr, seeds, seed_off, nullptr, out);
+}
+
+extern "C" ssbh_status ssbh_toeplitz_hash_batch_ptrs(uint64_t count, uint64_t m,
+                                                     const uint64_t* n,
+                                                     const uint64_t* const* inputs,
+                                                     const uint64_t* const* seeds,
+                                                     uint64_t* out) {
+    return hash_batch_impl(count, m, n, nullptr, nullptr, inputs, nullptr, nullptr, seeds, out);
+}
+
+extern "C" ssbh_status ssbh_release_thread_cache(void) {
+    for (auto& a : g_call.per_dev)
+        if (a && !a->depth) a.reset();
     return ok();
 }
 

@@ -319,22 +319,20 @@ BitString toeplitz_hash_batch(const std::vector<ToeplitzSeed>& seeds,
         throw std::invalid_argument("toeplitz_hash_batch: seeds/inputs count mismatch");
     if (seeds.empty()) return BitString();
     const std::uint64_t m = seeds[0].m;
-    std::vector<std::uint64_t> n, in_off, seed_off, in_words, seed_words;
+    std::vector<std::uint64_t> n(seeds.size());
+    std::vector<const std::uint64_t*> in_ptr(seeds.size()), seed_ptr(seeds.size());
     for (std::size_t b = 0; b < seeds.size(); ++b) {
         if (seeds[b].m != m)
             throw std::invalid_argument("toeplitz_hash_batch: output lengths differ");
         if (inputs[b].size() != seeds[b].n)
             throw std::invalid_argument("toeplitz: input length does not match seed.n");
-        n.push_back(seeds[b].n);
-        in_off.push_back(in_words.size());
-        seed_off.push_back(seed_words.size());
-        in_words.insert(in_words.end(), inputs[b].words().begin(), inputs[b].words().end());
-        seed_words.insert(seed_words.end(), seeds[b].seed.words().begin(),
-                          seeds[b].seed.words().end());
+        n[b] = seeds[b].n;
+        in_ptr[b] = inputs[b].words().data();
+        seed_ptr[b] = seeds[b].seed.words().data();
     }
     BitString out(m * seeds.size());
-    check(ssbh_toeplitz_hash_batch(seeds.size(), m, n.data(), in_words.data(), in_off.data(),
-                                   seed_words.data(), seed_off.data(), out.words().data()));
+    check(ssbh_toeplitz_hash_batch_ptrs(seeds.size(), m, n.data(), in_ptr.data(),
+                                        seed_ptr.data(), out.words().data()));
     return out;
 }
 

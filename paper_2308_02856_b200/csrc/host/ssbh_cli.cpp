@@ -23,6 +23,7 @@
 //
 // Exit codes follow ssbh_main.cpp:26-33: 0 ok, 2 parse/invalid, 3 infeasible,
 // 4 oversize abort, 5 statistics abort, 6 io; device failures exit 7.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -59,6 +60,7 @@ struct Args {
     std::uint64_t in_bits = 0, out_bits = 0;
     std::uint32_t ns = 1, gpus = 1;
     double eps_abort = 1e-8, out_ratio = 0.06303;
+    int repeats = 5;  // bench: median of this many timed calls per size
     std::vector<std::uint64_t> sizes;
     // simulate mode (Bbm92Params defaults, bbm92.hpp:14-26) and limit
     bool simulate = false;
@@ -95,6 +97,7 @@ Args parse(int argc, char** argv) {
         else if (f == "--gpus") a.gpus = static_cast<std::uint32_t>(parse_u64(val()));
         else if (f == "--eps-abort") a.eps_abort = std::stod(val());
         else if (f == "--out-ratio") a.out_ratio = std::stod(val());
+        else if (f == "--repeats") a.repeats = std::max(1, std::stoi(val()));
         else if (f == "--simulate") a.simulate = true;
         else if (f == "--n-rounds") a.params.n_rounds = parse_u64(val());
         else if (f == "--p-x") a.params.p_x = std::stod(val());
@@ -250,11 +253,19 @@ int cmd_bench(const Args& a) {
         const BitString input = KeyedStream(seed, "bench-input").bits(size);
         const ToeplitzSeed fseed(KeyedStream(seed, "bench-seed-full").bits(m_full + size - 1),
                                  m_full, size);
-        (void)toeplitz_hash(fseed, input);  // warm-up (module load, allocator)
-        auto t0 = std::chrono::steady_clock::now();
-        const BitString full = toeplitz_hash(fseed, input);
-        const double full_s =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        // median of a.repeats timed calls each (the reference times one call, :381-385)
+        auto median_s = [&](auto&& fn) {
+            fn();  // warm-up (module load, the per-thread device arena)
+            std::vector<double> t(a.repeats);
+            for (double& v : t) {
+                const auto t0 = std::chrono::steady_clock::now();
+                fn();
+                v = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            }
+            std::sort(t.begin(), t.end());
+            return t[t.size() / 2];
+        };
+        const double full_s = median_s([&] { (void)toeplitz_hash(fseed, input); });
         // split: partition + gather + per-block seeds untimed (ssbh_main.cpp:388-404), then
         // the hashing of every block timed — one batched launch on the GPU (:405-410)
         const std::uint64_t m_block = std::max<std::uint64_t>(1, m_full / a.ns);
@@ -270,12 +281,7 @@ int cmd_bench(const Args& a) {
             seeds.emplace_back(KeyedStream(seed, "hash-seed", j).bits(m_block + inputs[j].size() - 1),
                                m_block, inputs[j].size());
         }
-        (void)toeplitz_hash_batch(seeds, inputs);  // warm-up
-        t0 = std::chrono::steady_clock::now();
-        const BitString split = toeplitz_hash_batch(seeds, inputs);
-        const double split_s =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        (void)split;
+        const double split_s = median_s([&] { (void)toeplitz_hash_batch(seeds, inputs); });
         const double modeled = static_cast<double>(model_cycles(size, m_full, 1, a.eps_abort)) /
                                static_cast<double>(model_cycles(size, m_block * a.ns, a.ns,
                                                                 a.eps_abort));
@@ -284,7 +290,6 @@ int cmd_bench(const Args& a) {
                       static_cast<unsigned long long>(size), full_s, split_s, full_s / split_s,
                       modeled);
         out += line;
-        (void)full;
     }
     emit(a.out, out);
     return kOk;

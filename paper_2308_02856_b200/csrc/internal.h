@@ -225,19 +225,24 @@ struct PbGeom {
     uint32_t ntiles;   // ceil(kw / 4): 128-row tiles per block
     uint32_t nwin;     // ceil(ntiles / 256)
     uint32_t grid;
-    uint64_t items;    // nown * nwin
+    uint32_t nparts;   // D-step parts per (block, window): split-K when windows are few
+    uint32_t part_steps;  // D steps per part (multiple of 256; the last part takes the rest)
+    uint64_t items;    // nown * nwin * nparts
 };
 struct PbHashArgs {
     const uint32_t* ybuf;
     const uint32_t* sbuf;    // per-block seed regions at lay.soff[jj], pre-shifted by one bit
-    uint32_t* out;           // out[jj * out_stride + word], every word written once
+    uint32_t* out;           // out[jj * out_stride + word]: stored (1 part) or XORed (parts)
     unsigned long long out_stride;
     Layout lay;
     uint32_t nown, kw;
     uint32_t ntiles, nwin;
     uint64_t items;
+    uint32_t nparts, part_steps;  // set from PbGeom by launch_hash_mma_pb
 };
-PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device);
+// mean_bits: expected input bits per block; with few (block, window) items the D steps are
+// split into parts (XOR-accumulated into the pre-zeroed output) to fill the grid.
+PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device, uint64_t mean_bits = 0);
 void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st);
 // 3-for-4 split of long shared-seed squares (toeplitz_split.cu): T squares of k x k per block,
 // each split L times into 3^L Hankel leaves of size k / 2^L run by the tiled kernel.

@@ -259,19 +259,22 @@ __global__ void k_reverse(const uint32_t* __restrict__ x, uint64_t n, uint32_t* 
         y[u] = reversed_word(x, n, u);
 }
 
-// Batched API path: one CTA per block copies its seed (m+n-1 bits, tail masked) into the
-// per-block seed region and writes the reversed input into its y region.
+// Batched API path: CTA row blockIdx.y = block; the blockIdx.x slices of a row copy its seed
+// (m+n-1 bits, tail masked, pre-shifted one bit) into the per-block seed region and write the
+// reversed input into its y region, gridDim.x * blockDim.x words per sweep.
 __global__ void k_pack_blocks(const uint64_t* __restrict__ seeds,
                               const unsigned long long* __restrict__ seed_off,
                               const uint64_t* __restrict__ inputs,
                               const unsigned long long* __restrict__ in_off, Layout lay,
-                              uint64_t m, uint32_t* __restrict__ sbuf,
+                              uint64_t m, uint32_t count, uint32_t* __restrict__ sbuf,
                               uint32_t* __restrict__ ybuf) {
-    const uint32_t jj = blockIdx.x;
+  for (uint32_t jj = blockIdx.y; jj < count; jj += gridDim.y) {
     const uint64_t n = lay.nj[jj];
     const uint64_t sbits = m + n - 1;
     const uint32_t* s32 = reinterpret_cast<const uint32_t*>(seeds + seed_off[jj]);
     uint32_t* dst = sbuf + lay.soff[jj];
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     // pre-shifted by one bit (S'[b] = S[b-1]), see the seed kernels
     const uint64_t sw = (sbits + 31) / 32;
     auto seed_word = [&](uint64_t w) {
@@ -280,7 +283,7 @@ __global__ void k_pack_blocks(const uint64_t* __restrict__ seeds,
         if (lo + 32 > sbits) v &= (1u << (uint32_t)(sbits - lo)) - 1u;
         return v;
     };
-    for (uint64_t w = threadIdx.x; w <= sw; w += blockDim.x) {
+    for (uint64_t w = t0; w <= sw; w += step) {
         const uint32_t cur = w < sw ? seed_word(w) : 0u;
         const uint32_t prev = w ? seed_word(w - 1) : 0u;
         dst[w] = (cur << 1) | (prev >> 31);
@@ -288,7 +291,8 @@ __global__ void k_pack_blocks(const uint64_t* __restrict__ seeds,
     const uint32_t* x32 = reinterpret_cast<const uint32_t*>(inputs + in_off[jj]);
     uint32_t* y = ybuf + lay.yoff[jj];
     const uint64_t yp = lay.ypad[jj];
-    for (uint64_t u = threadIdx.x; u < yp; u += blockDim.x) y[u] = reversed_word(x32, n, u);
+    for (uint64_t u = t0; u < yp; u += step) y[u] = reversed_word(x32, n, u);
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -589,10 +593,13 @@ void launch_concat(const uint32_t* d_blocks, uint32_t kw, uint32_t nown, uint64_
 void launch_pack_blocks(const uint64_t* d_seeds, const unsigned long long* d_seed_off,
                         const uint64_t* d_inputs, const unsigned long long* d_in_off,
                         const Layout& lay, uint32_t count, uint64_t m, uint32_t* d_sbuf,
-                        uint32_t* d_ybuf, cudaStream_t st) {
+                        uint32_t* d_ybuf, cudaStream_t st, uint64_t max_words) {
     if (!count) return;
-    k_pack_blocks<<<count, 256, 0, st>>>(d_seeds, d_seed_off, d_inputs, d_in_off, lay, m,
-                                         d_sbuf, d_ybuf);
+    // ~8 words per thread per sweep; at least one CTA per block, <= 2 waves in total
+    uint64_t gx = (max_words + 2047) / 2048;
+    gx = std::max<uint64_t>(1, std::min<uint64_t>(gx, std::max<uint64_t>(1, 2048 / count)));
+    k_pack_blocks<<<dim3((unsigned)gx, std::min<uint32_t>(count, 65535)), 256, 0, st>>>(
+        d_seeds, d_seed_off, d_inputs, d_in_off, lay, m, count, d_sbuf, d_ybuf);
 }
 
 }  // namespace ssbh_impl

@@ -544,6 +544,22 @@ constexpr uint32_t kF4SfCol = kN;                            // scale factors: c
 constexpr uint32_t kF4Idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) | (1u << 23) |
                               ((uint32_t)(kM >> 4) << 24);
 
+// kind::mxf4 instruction descriptor with a runtime N (multiple of 16, 16..256; M = 128)
+__host__ __device__ constexpr uint32_t f4_idesc(uint32_t n) {
+    return (kF4Idesc & ~(0x3Fu << 17)) | ((n >> 3) << 17);
+}
+__device__ __forceinline__ void mma_f4n(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t sf, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(sf)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_f4(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t sf,
                                        uint32_t accum) {
     asm volatile(
@@ -913,18 +929,27 @@ constexpr int kPbThreads = 13 * 32;          // 4 epilogue, 1 MMA, 4 y, 4 Hankel
 
 struct PbItem {
     uint32_t jj, I0, ncols;   // block, first row tile, valid row tiles in the window
-    uint32_t nD;              // D steps: ncols + nC - 1
+    uint32_t nD;              // D steps of this item: [s0, s0 + nD) of the window's ncols + nC - 1
     uint32_t nC;              // y chunks of 128 positions
+    uint32_t s0;              // first D step (a multiple of kPbL)
+    uint32_t nmma;            // MMA N: ncols rounded up to 16 (FP4), 256 (u8)
 };
 
+// item = ((block * nwin) + window) * nparts + part
 __device__ __forceinline__ bool pb_decode(const PbHashArgs& a, uint32_t item, PbItem& d) {
     if (item >= a.items) return false;
-    d.jj = item / a.nwin;
-    const uint32_t w = item - d.jj * a.nwin;
+    const uint32_t part = item % a.nparts;
+    const uint32_t bw = item / a.nparts;
+    d.jj = bw / a.nwin;
+    const uint32_t w = bw - d.jj * a.nwin;
     d.I0 = w * kPbWin;
     d.ncols = min((uint32_t)kPbWin, a.ntiles - d.I0);
+    d.nmma = (d.ncols + 15) & ~15u;
     d.nC = a.lay.ypad[d.jj] / 4;
-    d.nD = d.nC ? d.ncols + d.nC - 1 : 0;
+    const uint32_t total = d.nC ? d.ncols + d.nC - 1 : 0;
+    d.s0 = part * a.part_steps;
+    const uint32_t end = part + 1 == a.nparts ? total : min(total, d.s0 + a.part_steps);
+    d.nD = end > d.s0 ? end - d.s0 : 0;
     return true;
 }
 
@@ -1021,6 +1046,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 if (d.nD) {
 #pragma unroll 1
                     for (int q = 0; q < kPbWin / 32; ++q) {
+                        if (32u * q >= d.ncols) break;  // columns past the window's tiles
                         uint32_t v[32];
                         SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kPbWin + 32u * q, v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -1045,7 +1071,10 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 for (int q = 0; q < kPbWin / 32; ++q) {
                     const uint32_t n = 32u * q + lane;
                     const uint32_t word = 4u * (d.I0 + n) + warp;  // rows 128 I + 32 warp ..
-                    if (n < d.ncols && word < a.kw) dst[word] = acc[q];
+                    if (n < d.ncols && word < a.kw) {
+                        if (a.nparts == 1) dst[word] = acc[q];
+                        else if (acc[q]) atomicXor(dst + word, acc[q]);  // D parts: XOR
+                    }
                 }
             }
         }
@@ -1064,6 +1093,8 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 continue;
             }
             uint32_t ab = 0, round_end = 0;
+            const uint32_t idesc = kF4 ? f4_idesc(d.nmma) : kIdesc;
+            // D0: D step relative to the item's first step d.s0
             for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
                 if (D0 % kRound == 0) {  // a new accumulation round (kRound is a multiple of kPbL)
                     ab = t % G::nacc;
@@ -1093,7 +1124,8 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                                 const uint64_t adesc = sdesc(ha + 2048u * j + 32u * m, 16, 128);
                                 const uint64_t bdesc = sdesc(ya + 2u * m * (kPbUnits * 16), kPbUnits * 16, 128);
                                 if constexpr (kF4)
-                                    mma_f4(tmem, adesc, bdesc, tmem + kF4SfCol, (first | (uint32_t)m) != 0);
+                                    mma_f4n(tmem, adesc, bdesc, idesc, tmem + kF4SfCol,
+                                            (first | (uint32_t)m) != 0);
                                 else
                                     mma_i8(tmem + ab * kPbWin, adesc, bdesc, (first | (uint32_t)m) != 0);
                             }
@@ -1115,14 +1147,15 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
             PbItem d;
             if (!pb_decode(a, item, d)) break;
             const uint32_t* y = a.ybuf + a.lay.yoff[d.jj];
-            for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
+            const uint32_t nunits = kPbL - 1 + d.nmma;  // units the buffer's MMAs read
+            for (uint32_t D0 = d.s0; D0 < d.s0 + d.nD; D0 += kPbL, ++yb) {
                 const uint32_t b = yb & 1;
                 if (yb >= 2) mbar_wait_sleep(&yempty[b], ((yb >> 1) - 1) & 1);
                 uint8_t* buf = ybufs + b * G::ybytes;
                 // unit P holds chunk C = D0 + kPbL - 1 - P (the buffer's D steps D0 .. +255
                 // read units kPbL - 1 - s + n, n < 256)
 #pragma unroll 1
-                for (uint32_t P = yt; P < kPbUnits - 1; P += 128) {
+                for (uint32_t P = yt; P < nunits; P += 128) {
                     const int64_t C = (int64_t)D0 + kPbL - 1 - P;
                     uint4 x = make_uint4(0, 0, 0, 0);
                     if (C >= 0 && C < (int64_t)d.nC) x = __ldg(reinterpret_cast<const uint4*>(y) + C);
@@ -1154,8 +1187,8 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 const uint32_t slot = hs % kPbHStages;
                 if (hs >= (uint32_t)kPbHStages)
                     mbar_wait_sleep(&hempty[slot], ((hs / kPbHStages) - 1) & 1);
-                // D = I0 + s (column n reads chunk C = D - I0 - n)
-                const uint64_t wbase = 4ull * (d.I0 + s);  // word of S' bit 128 D
+                // D = I0 + s0 + s (column n reads chunk C = D - I0 - n)
+                const uint64_t wbase = 4ull * (d.I0 + d.s0 + s);  // word of S' bit 128 D
                 uint8_t* hsm = hst + slot * G::hbytes;
 #pragma unroll
                 for (int r = 0; r < (G::hunits + 127) / 128; ++r) {
@@ -1250,19 +1283,40 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     return g;
 }
 
-PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device) {
+PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device, uint64_t mean_bits) {
     PbGeom g{};
     g.ntiles = (kw + 3) / 4;  // 128-row tiles
     g.nwin = (g.ntiles + kPbWin - 1) / kPbWin;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     g.grid = sms;
-    g.items = (uint64_t)nown * g.nwin;
+    g.nparts = 1;
+    g.part_steps = 0xFFFFFFFFu;
+    const uint64_t bw = (uint64_t)nown * g.nwin;
+    if (mean_bits && bw < (uint64_t)sms) {
+        // few (block, window) items: split each one's D steps into parts of >= 1024 steps
+        // (4 y buffers) so that ~one wave of items covers the grid
+        const uint64_t steps = std::min<uint64_t>(g.ntiles, kPbWin) + mean_bits / 128;
+        const uint64_t want = ((uint64_t)sms + bw - 1) / bw;
+        const uint64_t maxp = std::max<uint64_t>(1, steps / 1024);
+        g.nparts = (uint32_t)std::min<uint64_t>(want, maxp);
+        if (g.nparts > 1) {
+            const uint64_t ps = (steps + g.nparts - 1) / g.nparts;
+            g.part_steps = (uint32_t)((ps + kPbL - 1) / kPbL * kPbL);
+        }
+    }
+    g.items = bw * g.nparts;
     return g;
 }
 
-void launch_hash_mma_pb(const PbHashArgs& a, const PbGeom& g, cudaStream_t st) {
-    if (!a.nown || !g.items) return;
+void launch_hash_mma_pb(const PbHashArgs& a0, const PbGeom& g, cudaStream_t st) {
+    if (!a0.nown || !g.items) return;
+    PbHashArgs a = a0;
+    a.nparts = g.nparts;
+    a.part_steps = g.part_steps;
+    a.items = g.items;
+    if (g.nparts > 1)  // the parts XOR into the output rows
+        cudaMemset2DAsync(a.out, a.out_stride * 4, 0, (size_t)a.kw * 4, a.nown, st);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
     if (mma_uses_fp4()) {
         cudaFuncSetAttribute(k_toeplitz_mma_pb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
