@@ -81,9 +81,48 @@ std::uint64_t timing_model(std::uint64_t input_len, std::uint64_t output_len,
 }
 
 // -------------------------------------------------------------------- run_extraction
+namespace {
+// hash_bits: the solver's key length when feasible, else 0 (bits_per_block = hash_bits / ns);
+// model_bits: the solver's length as the reference feeds it to timing_model (pipeline.cpp:118)
+ExtractionReport run_extraction_impl(const std::vector<RoundRecord>& rounds,
+                                     const SamplingPlan& plan, const Bbm92Params& params,
+                                     std::uint64_t key_length, std::uint64_t model_bits,
+                                     const BlockingParams& blocking);
+}  // namespace
+
+// The reference's signature (pipeline.hpp:56-60). key_length is the reference's own solver
+// (proj/src/bbm92.cpp), bound weakly: linked by callers that keep the reference's security
+// library, absent otherwise.
+KeyLengthResult key_length(const Bbm92Params& params, const Scenario& scenario)
+    __attribute__((weak));
+
+ExtractionReport run_extraction(const std::vector<RoundRecord>& rounds, const SamplingPlan& plan,
+                                const Bbm92Params& params, const BlockingParams& blocking) {
+    if (!&key_length)
+        throw std::logic_error(
+            "run_extraction: the finite-key solver ssbh::key_length (the reference's "
+            "bbm92.cpp) is not linked; link it or pass the key length explicitly");
+    params.validate();
+    if (plan.n_subblocks == 0)
+        throw std::invalid_argument("run_extraction: plan.n_subblocks must be positive");
+    const std::uint32_t ns = plan.n_subblocks;
+    const KeyLengthResult kl =
+        key_length(params, ns == 1 ? Scenario::full() : Scenario::splitting(ns));
+    return run_extraction_impl(rounds, plan, params, kl.feasible ? kl.length : 0, kl.length,
+                               blocking);
+}
+
 ExtractionReport run_extraction(const std::vector<RoundRecord>& rounds, const SamplingPlan& plan,
                                 const Bbm92Params& params, std::uint64_t key_length,
                                 const BlockingParams& blocking) {
+    return run_extraction_impl(rounds, plan, params, key_length, key_length, blocking);
+}
+
+namespace {
+ExtractionReport run_extraction_impl(const std::vector<RoundRecord>& rounds,
+                                     const SamplingPlan& plan, const Bbm92Params& params,
+                                     std::uint64_t key_length, std::uint64_t model_bits,
+                                     const BlockingParams& blocking) {
     params.validate();
     if (plan.n_subblocks == 0)
         throw std::invalid_argument("run_extraction: plan.n_subblocks must be positive");
@@ -124,12 +163,13 @@ ExtractionReport run_extraction(const std::vector<RoundRecord>& rounds, const Sa
     for (const std::uint64_t b : report.block_lengths) sifted_total += b;
     report.bits_per_block = res.bits_per_block;
     report.cycle_count =
-        timing_model(sifted_total, key_length, ns == 1 ? Scenario::full() : Scenario::splitting(ns),
+        timing_model(sifted_total, model_bits, ns == 1 ? Scenario::full() : Scenario::splitting(ns),
                      blocking, plan.eps_abort, plan.block_limit);
     if (report.bits_per_block == 0) return report;  // nothing extractable; not an abort
     report.key = std::move(key);
     report.wall_seconds = res.hash_seconds;
     return report;
 }
+}  // namespace
 
 }  // namespace ssbh
