@@ -695,3 +695,231 @@ void or_rounds_split(const uint8_t* rounds, uint64_t n, uint64_t* bits, uint8_t*
         counts[3] += keep[i];
     }
 }
+
+/* ------------------------------------------- whole-partition checker (configs 4-5) */
+/* Eight consecutive sampling draws V_i = uniform_below(s, i) for a power-of-two s
+ * (prf.cpp:87-88: block({tag, 0, i, 0})[0] & (s-1)), written lane-parallel so that the
+ * compiler vectorises the 64-bit Threefry rounds (prf.cpp:47-76); target_clones picks the
+ * AVX-512 / AVX2 body on the host it runs on. Same arithmetic as or_threefry. */
+__attribute__((target_clones("avx512f", "avx2", "default")))
+static void sample8(const uint64_t ks[5], uint64_t tag, uint64_t i0, uint64_t mask,
+                    uint32_t v[8]) {
+    static const unsigned rot[8][2] = {{14, 16}, {52, 57}, {23, 40}, {5, 37},
+                                       {25, 33}, {46, 12}, {58, 22}, {32, 32}};
+    uint64_t x0[8], x1[8], x2[8], x3[8];
+    for (int l = 0; l < 8; ++l) {
+        x0[l] = tag + ks[0];
+        x1[l] = ks[1];
+        x2[l] = i0 + (uint64_t)l + ks[2];
+        x3[l] = ks[3];
+    }
+#pragma GCC unroll 20
+    for (unsigned d = 0; d < 20; ++d) {
+        const unsigned r0 = rot[d & 7][0], r1 = rot[d & 7][1];
+        for (int l = 0; l < 8; ++l) {
+            x0[l] += x1[l];
+            const uint64_t a = ((x1[l] << r0) | (x1[l] >> (64 - r0))) ^ x0[l];
+            x2[l] += x3[l];
+            const uint64_t b = ((x3[l] << r1) | (x3[l] >> (64 - r1))) ^ x2[l];
+            x1[l] = b; /* x1 <-> x3 swap */
+            x3[l] = a;
+        }
+        if ((d & 3) == 3) {
+            const uint64_t sidx = d / 4 + 1;
+            for (int l = 0; l < 8; ++l) {
+                x0[l] += ks[sidx % 5];
+                x1[l] += ks[(sidx + 1) % 5];
+                x2[l] += ks[(sidx + 2) % 5];
+                x3[l] += ks[(sidx + 3) % 5] + sidx;
+            }
+        }
+    }
+    for (int l = 0; l < 8; ++l) v[l] = (uint32_t)(x0[l] & mask);
+}
+
+typedef struct {
+    const uint64_t* input;
+    uint64_t n;
+    uint32_t s;
+    const uint64_t* key;
+    uint64_t ks[5];
+    uint64_t tag;
+    uint64_t* counts; /* nthreads x s: pass 1 counts, then each thread's starting ranks */
+    const uint64_t* nj;
+    const uint64_t* yoff;
+    uint64_t* y;
+    int pass;
+} part_ctx;
+
+static void part_range(void* vc, uint64_t lo, uint64_t hi, int tid) {
+    part_ctx* c = (part_ctx*)vc;
+    uint64_t* rank = c->counts + (uint64_t)tid * c->s;
+    const int pow2 = (c->s & (c->s - 1)) == 0;
+    uint32_t v[8];
+    for (uint64_t i = lo; i < hi; i += 8) {
+        const unsigned cnt = hi - i < 8 ? (unsigned)(hi - i) : 8u;
+        if (pow2 && cnt == 8)
+            sample8(c->ks, c->tag, i, c->s - 1, v);
+        else
+            for (unsigned l = 0; l < cnt; ++l)
+                v[l] = (uint32_t)or_uniform_below(c->key, c->tag, 0, c->s, i + l);
+        for (unsigned l = 0; l < cnt; ++l) {
+            const uint32_t j = v[l];
+            const uint64_t r = rank[j]++;
+            if (c->pass == 2 && ((c->input[(i + l) >> 6] >> ((i + l) & 63)) & 1)) {
+                const uint64_t pos = c->nj[j] - 1 - r; /* reversed: y[c] = x_j[n_j-1-c] */
+                __atomic_fetch_or(&c->y[c->yoff[j] + (pos >> 6)], 1ull << (pos & 63),
+                                  __ATOMIC_RELAXED);
+            }
+        }
+    }
+}
+
+/* assign_subblocks + sift (all kept) + gather of EVERY block without materialising the
+ * 12 B/round Partition (sampling.cpp:10-39, ssbh_main.cpp:329-331): two passes of the
+ * sampling draw over contiguous per-thread round ranges (counts, then the bits placed at
+ * their in-block rank). Block j's input is written REVERSED (bit c = x_j[n_j-1-c]) at u64
+ * word yoff[j]; y must hold n/64 + s + 1 zeroed words. */
+int or_partition_reversed(const uint64_t* input, uint64_t n, uint32_t s, const uint64_t key[4],
+                          int nthreads, uint64_t* nj, uint64_t* yoff, uint64_t* y) {
+    if (s == 0) return -1;
+    nthreads = resolve_threads(nthreads);
+    if (nthreads > 512) nthreads = 512;
+    part_ctx c;
+    memset(&c, 0, sizeof c);
+    c.input = input;
+    c.n = n;
+    c.s = s;
+    c.key = key;
+    for (int q = 0; q < 4; ++q) c.ks[q] = key[q];
+    c.ks[4] = 0x1BD11BDAA9FC1A22ull ^ key[0] ^ key[1] ^ key[2] ^ key[3];
+    c.tag = or_tag("sampling");
+    c.counts = (uint64_t*)calloc((size_t)nthreads * s, 8);
+    c.pass = 1;
+    parallel_ranges(n, 64, nthreads, part_range, &c);
+    yoff[0] = 0;
+    for (uint32_t j = 0; j < s; ++j) {
+        uint64_t t = 0;
+        for (int q = 0; q < nthreads; ++q) {
+            const uint64_t v = c.counts[(uint64_t)q * s + j];
+            c.counts[(uint64_t)q * s + j] = t; /* thread q's first rank in block j */
+            t += v;
+        }
+        nj[j] = t;
+        yoff[j + 1] = yoff[j] + (t + 63) / 64;
+    }
+    c.nj = nj;
+    c.yoff = yoff;
+    c.y = y;
+    c.pass = 2;
+    parallel_ranges(n, 64, nthreads, part_range, &c);
+    free(c.counts);
+    return 0;
+}
+
+typedef struct {
+    const uint64_t* y;
+    const uint64_t* yoff;
+    const uint64_t* nj;
+    const uint64_t* hash_key;
+    int per_block;
+    uint64_t k;
+    const uint64_t* key;
+    uint32_t rows;
+    uint64_t row_seed;
+    const uint64_t* shared_seed; /* shared mode: one seed for every block (prefix-stable) */
+    uint64_t seed_words;         /* padded words of a seed buffer */
+    uint64_t tag;
+    uint64_t* bad;     /* per thread: mismatches */
+    uint64_t* first;   /* per thread: first mismatching block (or ~0) */
+} spot_ctx;
+
+static inline uint64_t splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+static void spot_range(void* vc, uint64_t lo, uint64_t hi, int tid) {
+    spot_ctx* c = (spot_ctx*)vc;
+    uint64_t* buf = c->per_block ? (uint64_t*)malloc(c->seed_words * 8) : NULL;
+    for (uint64_t j = lo; j < hi; ++j) {
+        const uint64_t n = c->nj[j];
+        if (n == 0) continue;
+        const uint64_t* seed = c->shared_seed;
+        if (c->per_block) { /* KeyedStream(hash, "hash-seed", j).bits(k + n - 1), zero padded */
+            memset(buf, 0, c->seed_words * 8);
+            or_stream_bits(c->hash_key, c->tag, j, c->k + n - 1, buf);
+            seed = buf;
+        }
+        const uint64_t* yr = c->y + c->yoff[j];
+        const uint64_t yw = (n + 63) / 64;
+        for (uint32_t q = 0; q < c->rows; ++q) {
+            /* rows 0 and k-1, then seeded rows */
+            const uint64_t i = q == 0 ? 0 : q == 1 ? c->k - 1
+                                                   : splitmix64(c->row_seed ^ (j << 20) ^ q) % c->k;
+            uint64_t acc = 0; /* K[i] = parity(S[i .. i+n) & y), toeplitz.cpp:34-52 reversed */
+            for (uint64_t w = 0; w < yw; ++w) {
+                const uint64_t bit = i + 64 * w, qw = bit >> 6;
+                const unsigned r = (unsigned)(bit & 63);
+                uint64_t win = seed[qw] >> r;
+                if (r) win |= seed[qw + 1] << (64 - r);
+                acc ^= win & yr[w];
+            }
+            const uint64_t kb = j * c->k + i;
+            const unsigned got = (unsigned)((c->key[kb >> 6] >> (kb & 63)) & 1);
+            if ((unsigned)(__builtin_popcountll(acc) & 1) != got) {
+                if (c->bad[tid]++ == 0) c->first[tid] = j;
+            }
+        }
+    }
+    free(buf);
+}
+
+/* Every block's sampled output rows recomputed from the definition (toeplitz.cpp:34-52 with
+ * the seed of pipeline.cpp:132 / KeyedStream::bits prf.cpp:104-115) and compared with the
+ * concatenated key (bitstring.cpp:42-47; block j at bits [j k, (j+1) k)). Returns the number
+ * of mismatching rows; *first_bad = the first block with one (or ~0). */
+uint64_t or_spot_check(const uint64_t* y, const uint64_t* yoff, const uint64_t* nj, uint32_t s,
+                       const uint64_t hash_key[4], int per_block, uint64_t k,
+                       const uint64_t* key, uint32_t rows, uint64_t row_seed, int nthreads,
+                       uint64_t* first_bad) {
+    nthreads = resolve_threads(nthreads);
+    if (nthreads > 512) nthreads = 512;
+    uint64_t maxn = 0;
+    for (uint32_t j = 0; j < s; ++j) maxn = nj[j] > maxn ? nj[j] : maxn;
+    spot_ctx c;
+    memset(&c, 0, sizeof c);
+    c.y = y;
+    c.yoff = yoff;
+    c.nj = nj;
+    c.hash_key = hash_key;
+    c.per_block = per_block;
+    c.k = k;
+    c.key = key;
+    c.rows = rows;
+    c.row_seed = row_seed;
+    c.tag = or_tag("hash-seed");
+    c.seed_words = (k + maxn + 63) / 64 + 2;
+    uint64_t* shared = NULL;
+    if (!per_block) { /* prefix-stable: block j uses the first k + n_j - 1 bits */
+        shared = (uint64_t*)calloc(c.seed_words, 8);
+        or_stream_bits(hash_key, c.tag, 0, k + maxn - 1, shared);
+        c.shared_seed = shared;
+    }
+    c.bad = (uint64_t*)calloc(512, 8);
+    c.first = (uint64_t*)malloc(512 * 8);
+    for (int t = 0; t < 512; ++t) c.first[t] = ~0ull;
+    parallel_ranges(s, 1, nthreads, spot_range, &c);
+    uint64_t bad = 0, fb = ~0ull;
+    for (int t = 0; t < 512; ++t) {
+        bad += c.bad[t];
+        if (c.first[t] < fb) fb = c.first[t];
+    }
+    if (first_bad) *first_bad = fb;
+    free(shared);
+    free(c.bad);
+    free(c.first);
+    return bad;
+}

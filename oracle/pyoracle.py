@@ -240,6 +240,35 @@ class Oracle:
             raise ValueError("toeplitz: m and n must be positive (empty sub-block)")
         return keys[: len(which) * kw].reshape(len(which), kw), nj
 
+    def partition_reversed(self, x, n, s, samp, nthreads=0):
+        """Every block's input, reversed (bit c = x_j[n_j-1-c]), at u64 word yoff[j] of y —
+        the whole partition in 1/8 B per round (configs 4-5; no 12 B/round Partition)."""
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        nj = np.zeros(s, dtype=np.uint64)
+        yoff = np.zeros(s + 1, dtype=np.uint64)
+        y = np.zeros(n // 64 + s + 1, dtype=np.uint64)
+        f = self.L.or_partition_reversed
+        f.restype = C.c_int
+        f.argtypes = [U64P, C.c_uint64, C.c_uint32, U64P, C.c_int, U64P, U64P, U64P]
+        rc = f(_p64(x), n, s, _p64(key_of(samp)), nthreads, _p64(nj), _p64(yoff), _p64(y))
+        if rc:
+            raise ValueError("partition_reversed: n_subblocks must be positive")
+        return nj, yoff, y
+
+    def spot_check(self, y, yoff, nj, hsh, per_block, k, key, rows=64, row_seed=2308,
+                   nthreads=0):
+        """(mismatching rows, first bad block or None): `rows` output bits of every block
+        (rows 0, k-1 and seeded ones) recomputed from the definition against the key."""
+        f = self.L.or_spot_check
+        f.restype = C.c_uint64
+        f.argtypes = [U64P, U64P, U64P, C.c_uint32, U64P, C.c_int, C.c_uint64, U64P,
+                      C.c_uint32, C.c_uint64, C.c_int, U64P]
+        key = np.ascontiguousarray(key, dtype=np.uint64)
+        first = np.zeros(1, dtype=np.uint64)
+        bad = f(_p64(y), _p64(yoff), _p64(nj), len(nj), _p64(key_of(hsh)), int(per_block), k,
+                _p64(key), rows, row_seed, nthreads, _p64(first))
+        return int(bad), (None if int(first[0]) == 2**64 - 1 else int(first[0]))
+
     def fnv(self, words) -> int:
         w = np.ascontiguousarray(words, dtype=np.uint64)
         return int(self.L.or_fnv_words(_p64(w), len(w)))

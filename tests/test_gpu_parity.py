@@ -426,6 +426,24 @@ def test_config4_full_blocks_vs_reference(dev, oracle, golden):
         assert f"{oracle.fnv(blk):016x}" == want["block_fnv"][q], j
     assert int(st.hash_word_ops) == n * k // 32
     plan.close()
+    _every_block_spot_check(oracle, want, d_in, d_key, n, s, k, c)
+
+
+def _every_block_spot_check(oracle, want, d_in, d_key, n, s, k, c, rows=64):
+    """EVERY block checked, not only the reference-pinned ones. The oracle
+    rebuilds the whole partition from the seeds (assign_subblocks + sift + gather,
+    sampling.cpp:10-39, without the 12 B/round Partition) from the input — whose digest must be
+    the reference's — and recomputes `rows` output bits of each block (0, k-1 and seeded rows)
+    from the definition (toeplitz.cpp:34-52, seeds of pipeline.cpp:132)."""
+    x = d_in.cpu().numpy().view(np.uint64)[: (n + 63) // 64]
+    assert f"{oracle.fnv(x):016x}" == want["input_fnv"]
+    nj, yoff, y = oracle.partition_reversed(x, n, s, c["seed_samp"])
+    assert f"{oracle.fnv(nj):016x}" == want["nj_fnv"]
+    del x
+    key = d_key.cpu().numpy().view(np.uint64)
+    bad, first = oracle.spot_check(y, yoff, nj, c["seed_hash"], c["per_block"], k, key, rows)
+    assert bad == 0, f"{bad} mismatching rows, first in block {first}"
+    print(f"every-block spot check: {s} blocks x {rows} rows from the definition, 0 mismatches")
 
 
 # ------------------------------------- config 5 (2^37 rounds streamed in 8 chunks, k = 2^21)
@@ -465,6 +483,7 @@ def test_config5_streamed_vs_reference(dev, oracle, golden):
         assert f"{oracle.fnv(blk):016x}" == want["block_fnv"][q], j
     assert int(st.hash_word_ops) == n * k // 32
     plan.close()
+    _every_block_spot_check(oracle, want, d_in, d_key, n, s, k, c)
 
 
 # ------------------------------------------------------- sifted runs (keep flags)

@@ -248,3 +248,32 @@ def test_run_extraction_golden(oracle, golden):
         if abort != 2:
             assert [int(v) for v in lens] == c["block_lengths"], name
         assert f"{oracle.fnv(key):016x}" == c["key_fnv"], name
+
+
+def test_partition_reversed_and_spot_check(oracle):
+    """The configs-4/5 checker (or_partition_reversed + or_spot_check) against the oracle's
+    full extraction at small sizes; a single flipped key bit is found in its block."""
+    for (n, s, k, pb) in [(100000, 16, 1000, 1), (200000, 7, 640, 0), (1 << 20, 64, 8192, 0),
+                          (300000, 32, 96, 1), (70001, 1, 64, 0)]:
+        x = oracle.make_input(5, 0.5, n)
+        key, nj_want = oracle.extract(x, n, s, 2, 3, pb, k)
+        nj, yoff, y = oracle.partition_reversed(x, n, s, 2)
+        assert (nj == nj_want).all()
+        for j in (0, s - 1):
+            blk = y[int(yoff[j]):int(yoff[j + 1])]
+            assert (blk == oracle.reverse_bits(_gather(oracle, x, n, s, j), int(nj[j]))).all()
+        assert oracle.spot_check(y, yoff, nj, 3, pb, k, key, rows=64) == (0, None)
+        j = s // 2
+        bad_key = key.copy()
+        bad_key[(j * k) // 64] ^= np.uint64(1) << np.uint64((j * k) % 64)  # block j, row 0
+        assert oracle.spot_check(y, yoff, nj, 3, pb, k, bad_key, rows=2) == (1, j)
+
+
+def _gather(oracle, x, n, s, j):
+    a, _ = oracle.assign_subblocks(n, s, 2)
+    idx = np.nonzero(a == j + 1)[0]
+    bits = (x[idx // 64] >> (idx % 64).astype(np.uint64)) & np.uint64(1)
+    out = np.zeros((len(idx) + 63) // 64, dtype=np.uint64)
+    for q in range(len(idx)):
+        out[q // 64] |= bits[q] << np.uint64(q % 64)
+    return out
