@@ -79,6 +79,7 @@ def config_dict(cid, c, n_gpus):
         "parallelism": f"sub-blocks sharded over {n_gpus} GPU(s)",
         "l2": "L2 (126 MB) flushed between steps by a 256 MiB write outside the step events"
               + ("; input and payload exceed L2" if c["n"] >= (1 << 30) else ""),
+        **({"overrides": c["overrides"]} if c.get("overrides") else {}),
     }
 
 
@@ -302,10 +303,13 @@ def main():
                     help="N>1: sharded sampling + peer-memory owner exchange, or every rank "
                          "re-sampling all rounds")
     ap.add_argument("--engine", default="auto", choices=["auto", "lop3", "tensor"],
-                    help="hash engine (auto = tensor: tcgen05 u8 MMAs mod 2; lop3 = the "
+                    help="hash engine (auto = tensor: tcgen05 kind::mxf4 counts mod 2; lop3 = the "
                          "integer-ALU kernel)")
     ap.add_argument("--no-lop3-compare", action="store_true",
                     help="skip the extra LOP3-engine step reported beside a tensor-engine line")
+    ap.add_argument("--override", action="append", default=[], metavar="KEY=VALUE",
+                    help="dev A/B: plan-construction override (ssbh_set_plan_overrides), e.g. "
+                         "split_levels=0; the line then records it under config.overrides")
     ap.add_argument("--rounds", type=int, default=0,
                     help="testing aid: override n (the line's config then names the override)")
     ap.add_argument("--out-bits", type=int, default=0,
@@ -338,8 +342,12 @@ def main():
 
     import paper_2308_02856_b200 as P
 
-    if args.engine == "lop3":  # read by every plan this process creates (shard owners too)
-        os.environ["SSBH_HASH_ENGINE"] = "lop3"
+    ovr = {kv.split("=", 1)[0]: int(kv.split("=", 1)[1]) for kv in args.override}
+    if args.engine == "lop3":  # every plan this process creates (shard owners too)
+        ovr["engine"] = P.ENGINE_LOP3
+    if ovr:
+        P.set_overrides(**ovr)
+        c["overrides"] = ovr
     import torch
     import torch.distributed as dist
 
@@ -390,14 +398,13 @@ def main():
         check, close = plan.check, plan.close
     tensor = args.engine != "lop3"
     hash_kernel = ex.shard.hash_kernel if sharded else plan.hash_kernel
-    fp4 = hash_kernel.split("+")[0] in ("k_toeplitz_f4", "k_toeplitz_mma_pb<f4>")
 
     # roofline denominators, measured live on this GPU: LOP3 issue rate (int-ALU engine) and
     # the tcgen05 MAC rate (kind::mxf4 or kind::i8) with the hash kernel's operand layouts
     peak, _ = P.measure_lop3_peak(20000)
     tc_peak = None
     if tensor:  # ~120-140 ms probes: the sustained rate
-        tc_peak = P.measure_mma_f4_peak(200000)[0] if fp4 else P.measure_mma_i8_peak(200000, 0)[0]
+        tc_peak = P.measure_mma_f4_peak(200000)[0]
 
     def step():
         if sharded:
@@ -573,7 +580,7 @@ def main():
         hbm_ms = (n / 8 + count * k / 8) / (HBM_PEAK_GBS * 1e9) * 1e3
         split = (ex.shard if sharded else plan).split_geometry if tensor else (0, 0, 0)
         if tensor:
-            macs = hash_ops * 32  # sum_j n_j * k bit products = u8 tensor MACs doing useful work
+            macs = hash_ops * 32  # sum_j n_j * k bit products = tensor MACs doing useful work
             direct_macs = macs
             split_info = None
             if split[0]:
@@ -592,12 +599,11 @@ def main():
                             "direct_equivalent_rate the sum_j n_j*k products of the direct form "
                             "per second (can exceed the MMA peak)"}
             roof = {
-                "bound": "tensor (tcgen05 kind::mxf4)" if fp4 else "tensor (tcgen05 kind::i8)",
+                "bound": "tensor (tcgen05 kind::mxf4)",
                 "kernel": hash_kernel,
                 "achieved": macs / (avg_hash_ms * 1e-3) / 1e12, "peak": tc_peak / 1e12,
                 "unit": ("T MAC/s (E2M1 0/1.0 x 0/1.0 -> f32 exact integer counts; one MAC = "
-                         "one GF(2) bit product)" if fp4 else
-                         "T MAC/s (u8 x u8 -> s32; one MAC = one GF(2) bit product)"),
+                         "one GF(2) bit product)"),
                 "frac": macs / (avg_hash_ms * 1e-3) / tc_peak,
                 "traffic": traffic,
                 "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/)",
@@ -609,10 +615,7 @@ def main():
                 "split": split_info,
                 "peak_source": ("measured live in this run: k_f4_probe mode 2 (csrc/diag.cu), "
                                 "one CTA per SM issuing back-to-back 128x256x64 kind::mxf4 "
-                                "MMAs with the hash kernel's operand layouts" if fp4 else
-                                "measured live in this run: k_i8_peak (csrc/diag.cu), one CTA "
-                                "per SM issuing back-to-back 128x256x32 kind::i8 MMAs with the "
-                                "hash kernel's operand layouts"),
+                                "MMAs with the hash kernel's operand layouts"),
                 "int_alu_equivalent": {"achieved": achieved / 1e12, "peak": peak / 1e12,
                                        "unit": "T LOP3 word-ops/s",
                                        "times_lop3_peak": achieved / peak,
@@ -642,10 +645,7 @@ def main():
             "vs_baseline": None,
             "dtype": ("e2m1 (one GF(2) bit per element as 0 / 1.0) on tcgen05 kind::mxf4, "
                       "f32 accumulate of exact integer counts, parity = count mod 2; bit-exact"
-                      if fp4 else
-                      "u8 (one GF(2) bit per byte) on tcgen05 kind::i8, s32 accumulate, parity "
-                      "= sum mod 2; bit-exact" if tensor else
-                      "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)"),
+                      if tensor else "u32 (GF(2) bit-packed; LOP3/SHF/POPC, no FP)"),
             "hash_engine": "tensor" if tensor else "lop3",
             "data": "synthetic (KeyedStream input on device, seeds per BASELINE/SURVEY §8a)",
             "config": config_dict(cid, c, world),

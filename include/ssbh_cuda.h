@@ -203,23 +203,40 @@ ssbh_status ssbh_plan_check(ssbh_plan* plan, ssbh_extract_stats* stats);
 ssbh_status ssbh_plan_set_timing(ssbh_plan* plan, int enable);
 
 /* Hash engine of a plan (not a reference interface: the reference has one CPU loop).
- *   SSBH_ENGINE_LOP3   : GF(2) product on the integer ALUs (LOP3/SHF/POPC).
- *   SSBH_ENGINE_TENSOR : the product as u8 MMAs mod 2 on the tcgen05 tensor cores (kind::i8):
- *                        shared seeds = one GEMM of all blocks against the one Hankel matrix,
- *                        per-block seeds = each block's matrix-vector product tiled into
- *                        128 x 128 Hankel blocks.
- *   SSBH_ENGINE_AUTO   : the plan's default: TENSOR (environment SSBH_HASH_ENGINE=lop3 makes it
- *                        LOP3).
+ *   SSBH_ENGINE_LOP3   : GF(2) product on the integer ALUs (LOP3/SHF/POPC; north_star's kernel).
+ *   SSBH_ENGINE_TENSOR : the product as exact integer counts mod 2 on the tcgen05 tensor cores
+ *                        (kind::mxf4, E2M1 0 / 1.0 operands, f32 accumulators): shared seeds =
+ *                        one GEMM of all blocks against the one Hankel matrix, per-block seeds
+ *                        and long shared blocks = each block's matrix-vector product tiled into
+ *                        128 x 128 Hankel blocks; long keys through the 3-for-4 split.
+ *   SSBH_ENGINE_AUTO   : the plan's default: TENSOR (unless ssbh_set_plan_overrides says LOP3).
  * Both engines produce identical keys. ssbh_plan_engine returns the engine in use. */
 #define SSBH_ENGINE_AUTO 0
 #define SSBH_ENGINE_LOP3 1
 #define SSBH_ENGINE_TENSOR 2
 ssbh_status ssbh_plan_set_engine(ssbh_plan* plan, int engine);
 int ssbh_plan_engine(const ssbh_plan* plan);
-/* Name of the hash kernel a plan launches: "k_toeplitz_f4" (shared seeds, FP4 operands),
- * "k_toeplitz_mma" (shared seeds, u8; SSBH_MMA_FP4=0), "k_toeplitz_mma_pb<f4>" /
- * "k_toeplitz_mma_pb<i8>" (per-block seeds) or "k_toeplitz_hash" (LOP3). */
+/* Name of the hash kernel a plan launches: "k_toeplitz_f4" (shared seeds, all-blocks GEMM),
+ * "k_toeplitz_mma_pb" (per-block seeds / long shared blocks, tiled), either with "+split"
+ * when the 3-for-4 split runs (the leaves' kernel), or "k_toeplitz_hash" (LOP3). */
 const char* ssbh_plan_hash_kernel(const ssbh_plan* plan);
+
+/* Plan-construction overrides: explicit testing / A-B hooks that steer which code path a plan
+ * takes at sizes where the cost models would not (the parity suite forces every path at small
+ * sizes). Never read from the environment. Process-wide; plans copy them when created;
+ * NULL restores the defaults. */
+typedef struct ssbh_plan_overrides {
+    int32_t engine;             /* SSBH_ENGINE_AUTO (default) / _LOP3 / _TENSOR */
+    int32_t split_levels;       /* -1: cost model; 0: no 3-for-4 split; L: force L levels */
+    int32_t split_tiled_leaves; /* 0: shared-seed leaves on the all-blocks GEMM; 1: tiled kernel */
+    int32_t shared_tiled;       /* -1: heuristic (mean n_j >= 620 K bits); 0/1: force the tiled
+                                   kernel off/on for shared seeds */
+    int32_t buckets;            /* -1: heuristic (>= 4096 owned blocks); 0/1: force the
+                                   two-level sampler split off/on */
+    uint32_t split_budget_mb;   /* leaf buffer budget; 0: default 8192 MiB */
+} ssbh_plan_overrides;
+ssbh_status ssbh_set_plan_overrides(const ssbh_plan_overrides* overrides);
+ssbh_status ssbh_get_plan_overrides(ssbh_plan_overrides* overrides);
 /* 3-for-4 Toeplitz split of long shared-seed blocks (csrc/toeplitz_split.cu; a B200 addition,
    no reference counterpart): levels L (0 = direct product), squares T of k positions per block,
    owned blocks per leaf batch. The hash then runs T*3^L leaf products of k/2^L per block plus
@@ -383,10 +400,6 @@ ssbh_status ssbh_make_input_device(const uint64_t key[4], double p, uint64_t nbi
 /* Diagnostics (not a reference interface): measured LOP3 lane-ops/s of the current device
  * (the int-ALU roofline denominator of the hash kernel) over one timed launch. */
 ssbh_status ssbh_measure_lop3_peak(uint32_t iters, double* lop3_per_s, double* ms);
-/* Diagnostics: measured tcgen05.mma kind::i8 MAC/s of the current device (the roofline
- * denominator of the tensor hash engine): one CTA per SM issuing back-to-back 128x256x32
- * MMAs. layout 0 = the hash kernel's operand layouts, 1 = plain K-major tiles. */
-ssbh_status ssbh_measure_mma_i8_peak(uint32_t iters, int layout, double* macs_per_s, double* ms);
 /* FP4 roofline of the shared-seed tensor kernel: tcgen05.mma kind::mxf4 (E2M1, unit UE8M0
  * scales) 128x256x64 back to back with the hash kernel's operand layouts. */
 ssbh_status ssbh_measure_mma_f4_peak(uint32_t iters, double* macs_per_s, double* ms);
@@ -395,8 +408,6 @@ ssbh_status ssbh_measure_mma_f4_peak(uint32_t iters, double* macs_per_s, double*
  * accumulator's bits), 2 = rate with the hash kernel's layouts. */
 ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_per_s, double* ms,
                               uint32_t* mismatches, uint32_t* sample_bits);
-/* Same with CTA pairs (cta_group::2, M = 256 across two SMs). */
-ssbh_status ssbh_measure_mma_i8_peak2(uint32_t iters, int layout, double* macs_per_s, double* ms);
 
 #ifdef __cplusplus
 }

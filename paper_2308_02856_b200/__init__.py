@@ -49,10 +49,11 @@ ABI_SYMBOLS = (
     "ssbh_shard_open_peers", "ssbh_shard_sample", "ssbh_shard_exchange", "ssbh_shard_finish",
     "ssbh_shard_check", "ssbh_shard_set_timing", "ssbh_simulate_rounds_device",
     "ssbh_simulate_rounds", "ssbh_run_extraction", "ssbh_run_extraction_device",
-    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_i8_peak", "ssbh_measure_mma_i8_peak2", "ssbh_measure_mma_f4_peak",
+    "ssbh_extract_multi", "ssbh_plan_set_engine", "ssbh_plan_engine", "ssbh_measure_mma_f4_peak",
     "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel", "ssbh_shard_hash_kernel",
     "ssbh_plan_split_geometry", "ssbh_shard_split_geometry", "ssbh_fnv1a64",
-    "ssbh_toeplitz_hash_batch_ptrs", "ssbh_release_thread_cache",
+    "ssbh_toeplitz_hash_batch_ptrs", "ssbh_release_thread_cache", "ssbh_set_plan_overrides",
+    "ssbh_get_plan_overrides",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2
@@ -108,6 +109,18 @@ class ExtractStats(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class PlanOverrides(C.Structure):
+    """ssbh_plan_overrides (include/ssbh_cuda.h): explicit testing / A-B hooks for which code
+    path a plan takes; never read from the environment."""
+    _fields_ = [("engine", C.c_int32), ("split_levels", C.c_int32),
+                ("split_tiled_leaves", C.c_int32), ("shared_tiled", C.c_int32),
+                ("buckets", C.c_int32), ("split_budget_mb", C.c_uint32)]
+
+
+DEFAULT_OVERRIDES = dict(engine=0, split_levels=-1, split_tiled_leaves=0, shared_tiled=-1,
+                         buckets=-1, split_budget_mb=0)
+
+
 class RoundParams(C.Structure):
     _fields_ = [("n_rounds", C.c_uint64), ("p_x", C.c_double), ("e_ph", C.c_double),
                 ("e_bit", C.c_double), ("p_det", C.c_double)]
@@ -160,12 +173,6 @@ def _load():
     L.ssbh_shard_split_geometry.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint32)] * 3
     L.ssbh_shard_hash_kernel.restype = C.c_char_p
     L.ssbh_shard_hash_kernel.argtypes = [C.c_void_p]
-    L.ssbh_measure_mma_i8_peak2.restype = st
-    L.ssbh_measure_mma_i8_peak2.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double),
-                                            C.POINTER(C.c_double)]
-    L.ssbh_measure_mma_i8_peak.restype = st
-    L.ssbh_measure_mma_i8_peak.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double),
-                                           C.POINTER(C.c_double)]
     L.ssbh_prf_tag.restype = C.c_uint64
     L.ssbh_prf_tag.argtypes = [C.c_char_p, C.c_size_t]
     L.ssbh_stream_bits.restype = st
@@ -723,13 +730,41 @@ def measure_lop3_peak(iters: int = 20000):
     return r.value, ms.value
 
 
-def measure_mma_i8_peak(iters: int = 4000, layout: int = 0, pairs: bool = False):
-    """Measured tcgen05 kind::i8 MAC/s of the current device (tensor-engine roofline);
-    pairs=True: CTA pairs (cta_group::2, M = 256)."""
-    r, ms = C.c_double(0), C.c_double(0)
-    f = lib.ssbh_measure_mma_i8_peak2 if pairs else lib.ssbh_measure_mma_i8_peak
-    _check(f(iters, layout, C.byref(r), C.byref(ms)))
-    return r.value, ms.value
+def get_overrides() -> dict:
+    o = PlanOverrides()
+    _check(lib.ssbh_get_plan_overrides(C.byref(o)))
+    return {f: getattr(o, f) for f, _ in PlanOverrides._fields_}
+
+
+def set_overrides(**kw) -> dict:
+    """Set plan-construction overrides (process-wide, read when a plan is created); fields not
+    given keep their defaults (DEFAULT_OVERRIDES). Returns the previous values."""
+    prev = get_overrides()
+    vals = dict(DEFAULT_OVERRIDES)
+    for key, v in kw.items():
+        if key not in vals:
+            raise TypeError(f"unknown override {key}")
+        vals[key] = v
+    _check(lib.ssbh_set_plan_overrides(C.byref(PlanOverrides(**vals))))
+    return prev
+
+
+class overrides:
+    """Context manager: `with overrides(split_levels=3): plan = Plan(...)`; the previous
+    overrides are restored on exit. Fields not given are merged over the current ones."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        cur = get_overrides()
+        cur.update(self.kw)
+        self.prev = set_overrides(**cur)
+        return self
+
+    def __exit__(self, *exc):
+        set_overrides(**self.prev)
+        return False
 
 
 def fnv1a64(words) -> int:

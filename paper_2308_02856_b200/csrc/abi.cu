@@ -457,10 +457,7 @@ using LayoutScratch = LayoutBufsT<SBuf>;  // one call (CallScope arena)
 uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid) {
     const uint64_t yw = std::max<uint64_t>(1, (mean_nj + 31) / 32);
     uint64_t kt = kHashKTMax;
-    static const uint64_t per_cta = [] {  // dev A/B knob: SSBH_KT_ITEMS_PER_CTA
-        const char* e = std::getenv("SSBH_KT_ITEMS_PER_CTA");
-        return e ? std::strtoull(e, nullptr, 10) : 8ull;  // 8: config 2 hash 0.870 -> 0.888
-    }();
+    const uint64_t per_cta = 8;  // round 1: 8 items per CTA, config 2 hash 0.870 -> 0.888
     const uint64_t want_items = (uint64_t)grid * per_cta;
     while (kt > 64) {
         const uint64_t items = (uint64_t)rowtiles * nown * ((yw + kt - 1) / kt);
@@ -475,11 +472,20 @@ uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid)
 // Engine of a new plan: the tensor cores (toeplitz_mma.cu: shared seeds as one GEMM over all
 // blocks, per-block seeds as tiled matrix-vector products) unless SSBH_HASH_ENGINE=lop3 keeps
 // the plan on the integer ALUs (toeplitz.cu).
+// Plan-construction overrides (ssbh_set_plan_overrides): explicit testing / A-B hooks, never
+// read from the environment — a plan's kernels depend only on its parameters unless a caller
+// sets these. Process-wide; copied when a plan is created.
+static std::mutex g_over_mu;
+static ssbh_plan_overrides g_over{SSBH_ENGINE_AUTO, -1, 0, -1, -1, 0};
+
+static ssbh_plan_overrides overrides() {
+    std::lock_guard<std::mutex> lk(g_over_mu);
+    return g_over;
+}
+
 static int default_engine(uint32_t per_block_seed) {
     (void)per_block_seed;
-    const char* e = std::getenv("SSBH_HASH_ENGINE");
-    if (e && std::strcmp(e, "lop3") == 0) return kEngineLop3;
-    return kEngineMma;
+    return overrides().engine == SSBH_ENGINE_LOP3 ? kEngineLop3 : kEngineMma;
 }
 
 // ======================================================================== plan
@@ -617,25 +623,22 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     // Long shared-seed blocks: the tiled matrix-vector kernel keeps each block's y chunks in
     // shared memory for 256 D steps instead of re-expanding them for every 256-row tile (config
     // 3: hash 155 -> 145 ms); its window ramp (255 D steps per item) costs < 5 % once the mean
-    // block has > 620 K bits. SSBH_MMA_SHARED_PB=0/1 overrides (dev A/B knob).
+    // block has > 620 K bits.
+    const ssbh_plan_overrides ov = overrides();
     {
-        const char* e = std::getenv("SSBH_MMA_SHARED_PB");
         pl->shared_pb = !params->per_block_seed &&
-                        (e && *e ? *e == '1' : mean_nj >= (uint64_t)620000);
-        // 3-for-4 split (toeplitz_split.cu) of long blocks: levels by split_levels;
-        // SSBH_MMA_SPLIT=L forces (0 disables). Shared-seed leaves run on the all-blocks GEMM
-        // (default) or the tiled kernel (SSBH_MMA_SPLIT_LEAF=pb, dev A/B knob).
-        const char* sl = std::getenv("SSBH_MMA_SPLIT_LEAF");
-        bool gemm = !params->per_block_seed && !(sl && std::strcmp(sl, "pb") == 0);
-        const char* se = std::getenv("SSBH_MMA_SPLIT");
-        const bool forced = se && *se;
-        uint32_t L = forced ? (uint32_t)std::strtoul(se, nullptr, 10) : split_levels(k, gemm);
+                        (ov.shared_tiled >= 0 ? ov.shared_tiled == 1 : mean_nj >= (uint64_t)620000);
+        // 3-for-4 split (toeplitz_split.cu) of long blocks: levels by split_levels (or
+        // forced by the overrides). Shared-seed leaves run on the all-blocks GEMM, or on the
+        // tiled kernel (override split_tiled_leaves).
+        bool gemm = !params->per_block_seed && !ov.split_tiled_leaves;
+        const bool forced = ov.split_levels >= 0;
+        uint32_t L = forced ? (uint32_t)ov.split_levels : split_levels(k, gemm);
         pl->split = (gemm || pl->shared_pb || params->per_block_seed) &&
-                    pl->engine == kEngineMma && mma_uses_fp4() && split_applicable(k, mean_nj, L);
+                    pl->engine == kEngineMma && split_applicable(k, mean_nj, L);
         if (pl->split) {
-            const char* sb = std::getenv("SSBH_MMA_SPLIT_MB");  // leaf buffer budget, default 8 GB
-            const uint64_t budget =
-                (sb && *sb ? (uint64_t)std::strtoull(sb, nullptr, 10) : 8192ull) << 20;
+            // leaf buffer budget, default 8 GB
+            const uint64_t budget = (uint64_t)(ov.split_budget_mb ? ov.split_budget_mb : 8192u) << 20;
             const bool pb_ok = pl->shared_pb || params->per_block_seed;
             pl->sg = make_split_geom(nown, k, mean_nj, L, params->per_block_seed != 0, gemm,
                                      budget);
@@ -667,9 +670,8 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         }
     }
 
-    // two-level split for large key spaces (SSBH_BUCKETS=0 disables it, =1 forces it)
-    const char* be = std::getenv("SSBH_BUCKETS");
-    pl->bucketed = be && *be ? *be == '1' : nown >= kBucketMinBlocks;
+    // two-level split for large key spaces (override buckets = 0 / 1 disables / forces it)
+    pl->bucketed = ov.buckets >= 0 ? ov.buckets == 1 : nown >= kBucketMinBlocks;
     if (pl->bucketed) {
         const uint64_t n_src = pl->streaming ? chunk_bits : n;
         const double mean = (double)n / (double)(external_payload ? nown : params->n_subblocks);
@@ -730,6 +732,19 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         return fail(SSBH_CUDA, "plan_create: device allocation failed: %s", cudaGetErrorString(e));
     }
     *out = pl;
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_set_plan_overrides(const ssbh_plan_overrides* o) {
+    std::lock_guard<std::mutex> lk(g_over_mu);
+    g_over = o ? *o : ssbh_plan_overrides{SSBH_ENGINE_AUTO, -1, 0, -1, -1, 0};
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_get_plan_overrides(ssbh_plan_overrides* o) {
+    if (!o) return fail(SSBH_INVALID_ARGUMENT, "null overrides");
+    std::lock_guard<std::mutex> lk(g_over_mu);
+    *o = g_over;
     return ok();
 }
 
@@ -838,10 +853,10 @@ extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
     if (!pl) return "";
     if (pl->engine != kEngineMma) return "k_toeplitz_hash";
     if (pl->split)  // engine checked above
-        return pl->sg.gemm ? "k_toeplitz_f4+split" : "k_toeplitz_mma_pb<f4>+split";
+        return pl->sg.gemm ? "k_toeplitz_f4+split" : "k_toeplitz_mma_pb+split";
     if (pl->p.per_block_seed || pl->shared_pb)
-        return mma_uses_fp4() ? "k_toeplitz_mma_pb<f4>" : "k_toeplitz_mma_pb<i8>";
-    return mma_uses_fp4() ? "k_toeplitz_f4" : "k_toeplitz_mma";
+        return "k_toeplitz_mma_pb";
+    return "k_toeplitz_f4";
 }
 
 extern "C" ssbh_status ssbh_plan_split_geometry(const ssbh_plan* pl, uint32_t* levels,
@@ -1151,14 +1166,7 @@ static ssbh_status plan_enqueue(ssbh_plan* pl, const RunArgs& r, cudaStream_t st
     return check_launch("plan_run");
 }
 
-static bool graphs_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        const char* e = std::getenv("SSBH_NO_GRAPH");
-        on = (e && *e == '1') ? 0 : 1;
-    }
-    return on == 1;
-}
+static bool graphs_enabled() { return true; }
 
 static ssbh_status capture(ssbh_plan* pl, const RunArgs& r, int s0, int s1, cudaStream_t st,
                            cudaGraphExec_t* exec, uint32_t& launches) {

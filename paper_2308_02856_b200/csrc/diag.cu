@@ -28,144 +28,6 @@ __global__ void __launch_bounds__(256) k_lop3_peak(uint32_t iters, uint32_t* out
     if (x == 0x12345678u) out[blockIdx.x] = x;  // keep the chains live
 }
 
-// Tensor-core roofline of the tensor hash engine: one CTA per SM, one thread issues
-// back-to-back tcgen05.mma kind::i8 (M = 128, N = 256, K = 32, s32 accumulate) into two TMEM
-// accumulators, 8 MMAs per commit — the hash kernel's instruction mix without its producers.
-// layout 0: the hash kernel's operand layouts (A: LBO 128 / SBO 2048; B: overlapping Hankel
-// units, LBO 16 / SBO 128); layout 1: plain non-overlapping K-major tiles for both operands.
-__global__ void __launch_bounds__(128, 1) k_i8_peak(uint32_t iters, int layout) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
-    __shared__ uint32_t tslot;
-    const uint32_t warp = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i < 40960 / 4; i += blockDim.x)
-        reinterpret_cast<uint32_t*>(smem)[i] = i * 0x9E3779B9u;
-    const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tslot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tslot;
-    if (threadIdx.x == 0) {
-        const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
-        const uint32_t idesc = (2u << 4) | (32u << 17) | (8u << 24);
-        auto desc = [](uint32_t a, uint32_t lbo, uint32_t sbo) {
-            return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-                   ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-        };
-        for (uint32_t it = 0; it < iters; ++it) {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const uint64_t a = desc(base + 256u * m, 128, 2048);
-                const uint64_t b = layout == 0
-                    ? desc(base + 32768u + 16u * (2u * (m & 3) + 128u * (m >> 2)), 16, 128)
-                    : desc(base + 32768u + 0u, 128, 256);
-                const uint32_t d = tmem + (it & 1) * 256u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                    "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)m)
-                    : "memory");
-            }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         bar_a)
-                     : "memory");
-        asm volatile(
-            "{\n.reg .pred P1;\nW:\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-            "@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(bar_a)
-            : "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
-// Same with CTA pairs (cta_group::2, M = 256 across the pair, each CTA holding half of B):
-// the leader issues, both CTAs' operands at the same shared-memory offsets.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
-    k_i8_peak2(uint32_t iters, int layout) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
-    __shared__ uint32_t tslot;
-    const uint32_t warp = threadIdx.x >> 5;
-    uint32_t rank;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    for (uint32_t i = threadIdx.x; i < 40960 / 4; i += blockDim.x)
-        reinterpret_cast<uint32_t*>(smem)[i] = i * 0x9E3779B9u;
-    const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tslot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tslot;
-    if (rank == 0 && threadIdx.x == 0) {
-        const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
-        const uint32_t idesc = (2u << 4) | (32u << 17) | (16u << 24);  // M = 256, N = 256
-        auto desc = [](uint32_t a, uint32_t lbo, uint32_t sbo) {
-            return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-                   ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-        };
-        for (uint32_t it = 0; it < iters; ++it) {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const uint64_t a = desc(base + 256u * m, 128, 2048);
-                const uint64_t b = layout == 0
-                    ? desc(base + 32768u + 16u * (2u * (m & 3) + 128u * (m >> 2)), 16, 128)
-                    : desc(base + 32768u + 0u, 128, 256);
-                const uint32_t d = tmem + (it & 1) * 256u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                    "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)m)
-                    : "memory");
-            }
-        }
-        asm volatile(
-            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                bar_a), "h"((uint16_t)3)
-            : "memory");
-    }
-    if (threadIdx.x == 0) {
-        asm volatile(
-            "{\n.reg .pred P1;\nW:\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-            "@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(bar_a)
-            : "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
 // Block-scaled FP4 probe (kind::mxf4, E2M1 operands, every UE8M0 scale = 1.0): rate of
 // 128x256x64 MMAs and exactness of the f32 accumulation of integer sums. mode 0: A and B all
 // 1.0 (rate); mode 1: A all 1.0, B one 1.0 per row, so every MMA adds exactly 1 and the
@@ -320,59 +182,6 @@ extern "C" ssbh_status ssbh_probe_mma_f4(uint32_t iters, int mode, double* macs_
 extern "C" ssbh_status ssbh_measure_mma_f4_peak(uint32_t iters, double* macs_per_s,
                                                 double* ms_out) {
     return ssbh_probe_mma_f4(iters, 2, macs_per_s, ms_out, nullptr, nullptr);
-}
-
-extern "C" ssbh_status ssbh_measure_mma_i8_peak2(uint32_t iters, int layout, double* macs_per_s,
-                                                 double* ms_out) {
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return SSBH_NO_DEVICE;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int smem = 120 * 1024;
-    cudaFuncSetAttribute(k_i8_peak2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int grid = sms & ~1;
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    k_i8_peak2<<<grid, 128, smem>>>(iters / 8 + 1, layout);
-    cudaEventRecord(e0);
-    k_i8_peak2<<<grid, 128, smem>>>(iters, layout);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
-    const double macs = (double)(grid / 2) * iters * 8.0 * 256.0 * 256.0 * 32.0;
-    if (macs_per_s) *macs_per_s = macs / (ms * 1e-3);
-    if (ms_out) *ms_out = ms;
-    return SSBH_OK;
-}
-
-extern "C" ssbh_status ssbh_measure_mma_i8_peak(uint32_t iters, int layout, double* macs_per_s,
-                                                double* ms_out) {
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return SSBH_NO_DEVICE;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int smem = 120 * 1024;  // > half the SM's shared memory: one CTA per SM
-    cudaFuncSetAttribute(k_i8_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    k_i8_peak<<<sms, 128, smem>>>(iters / 8 + 1, layout);  // warm-up / clock ramp
-    cudaEventRecord(e0);
-    k_i8_peak<<<sms, 128, smem>>>(iters, layout);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
-    const double macs = (double)sms * iters * 8.0 * 128.0 * 256.0 * 32.0;
-    if (macs_per_s) *macs_per_s = macs / (ms * 1e-3);
-    if (ms_out) *ms_out = ms;
-    return SSBH_OK;
 }
 
 extern "C" ssbh_status ssbh_measure_lop3_peak(uint32_t iters, double* lop3_per_s, double* ms_out) {

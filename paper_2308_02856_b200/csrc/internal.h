@@ -196,7 +196,7 @@ void launch_reverse(const uint32_t* d_x32, uint64_t nbits, uint32_t* d_y, uint64
 int hash_grid_size(int device);
 void launch_hash(const HashArgs& a, int grid, cudaStream_t st);
 // Tensor-core engine for shared-seed plans (toeplitz_mma.cu): the hash of all owned blocks
-// as one u8 GEMM mod 2 (tcgen05.mma kind::i8). Same inputs/outputs as launch_hash.
+// as one FP4 GEMM mod 2 (tcgen05.mma kind::mxf4). Same inputs/outputs as launch_hash.
 enum HashEngine : int { kEngineAuto = 0, kEngineLop3 = 1, kEngineMma = 2 };
 struct MmaGeom {
     uint32_t mtiles;   // ceil(nown / 128)
@@ -216,7 +216,6 @@ struct MmaHashArgs {
     uint32_t ntiles, ksplit;
     uint64_t items;
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
-    uint32_t spin;           // dev knob: MMA warp spins instead of suspending on its waits
     uint32_t stage_bits;     // input positions per pipeline stage (set by launch_hash_mma)
 };
 // Per-block seeds on the tensor cores: work item = (owned block, window of 256 row tiles of
@@ -278,9 +277,7 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
                               uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
-bool mma_uses_fp4();
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
-size_t mma_hash_smem();
 void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st);
 
 // Concatenate nown blocks of k bits (block stride kw words) into key (bit offset jj*k).

@@ -360,7 +360,7 @@ struct ScatterArgs {
     const uint32_t* rank_base;  // staged kModeBits: per-block rank offset (streaming) or null
 };
 
-template <typename Src, bool kSmemRow, bool kMatch, int kMode>
+template <typename Src, bool kSmemRow, int kMode>
 __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
     using B = typename Src::Bits;
     using P = typename std::conditional<B::kDataShift == 15, uint16_t, uint32_t>::type;
@@ -441,10 +441,9 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                     jjv[q] = (p & B::kVMask) - j_lo;
                     inv[q] = kept && jjv[q] < nown;
                 }
-                if (kMatch)
-                    peers[q] = __match_any_sync(0xffffffffu, inv[q] ? jjv[q] : 0xffffffffu);
-                else
-                    peers[q] = peers_by_ballot(jjv[q], inv[q], a.kbits);
+                // one __ballot_sync per key bit (MATCH.ANY is throughput-bound on sm_100:
+                // round 1, config 3 scatter 8.6 -> 6.3 ms)
+                peers[q] = peers_by_ballot(jjv[q], inv[q], a.kbits);
             }
             // (2) in round order: all peers read the running rank (same address: broadcast),
             //     the highest peer writes it back. The warp owns `row` (no atomics); groups
@@ -666,15 +665,6 @@ void sample_count_any(const SamplerGeom& g, const uint64_t key[4], const uint32_
     }
 }
 
-bool scatter_match() {  // dev switch for A/B: SSBH_SCATTER_PEERS=ballot|match
-    static int m = -1;
-    if (m < 0) {
-        const char* e = std::getenv("SSBH_SCATTER_PEERS");
-        m = (e && e[0] == 'm') ? 1 : 0;  // ballot default: 6.3 ms vs 8.6 ms (config 3)
-    }
-    return m == 1;
-}
-
 template <int kMode, typename Src>
 void scatter_launch(const Src& src, ScatterArgs a, cudaStream_t st) {
     // per-warp bytes: running-rank row (+ write-combining sectors for the bucket split)
@@ -695,11 +685,10 @@ void scatter_launch(const Src& src, ScatterArgs a, cudaStream_t st) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
         kern<<<(unsigned)blocks, wpb * 32, shm, st>>>(src, a);
     };
-    const bool m = scatter_match();
     if (smem)
-        m ? go(k_scatter<Src, true, true, kMode>) : go(k_scatter<Src, true, false, kMode>);
+        go(k_scatter<Src, true, kMode>);
     else
-        m ? go(k_scatter<Src, false, true, kMode>) : go(k_scatter<Src, false, false, kMode>);
+        go(k_scatter<Src, false, kMode>);
 }
 
 ScatterArgs scatter_args(const SamplerGeom& g, uint32_t* d_offsets,
@@ -723,24 +712,9 @@ ScatterArgs scatter_args(const SamplerGeom& g, uint32_t* d_offsets,
     return a;
 }
 
-// Count-table geometry knobs (dev A/B switches; defaults are the measured choice).
-int table_budget_shift() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("SSBH_TABLE_BUDGET_SHIFT");
-        v = e ? std::atoi(e) : 7;
-    }
-    return v;
-}
-
-uint64_t max_table_chunks() {
-    static uint64_t v = 0;
-    if (!v) {
-        const char* e = std::getenv("SSBH_MAX_CHUNKS");
-        v = e ? std::strtoull(e, nullptr, 10) : 16384ull;
-    }
-    return v;
-}
+// Count-table geometry (round 1 A/B: a table budget of n >> 7 entries, <= 16384 chunks).
+constexpr int kTableBudgetShift = 7;
+constexpr uint64_t kMaxTableChunks = 16384;
 
 }  // namespace
 
@@ -761,8 +735,8 @@ SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t no
         return nc * (uint64_t)nown * 4ull;
     };
     // table budget: 256 MiB, or n / 2^budget_shift bytes for very large n (configs 4-5)
-    const uint64_t budget = std::max<uint64_t>(256ull << 20, n >> table_budget_shift());
-    const uint64_t max_chunks = max_table_chunks();
+    const uint64_t budget = std::max<uint64_t>(256ull << 20, n >> kTableBudgetShift);
+    const uint64_t max_chunks = kMaxTableChunks;
     while (cs < max_chunk_shift && (((n >> cs) > max_chunks) || table_bytes(cs) > budget)) ++cs;
     g.chunk_shift = cs;
     g.nchunks = (n + (1ull << cs) - 1) >> cs;

@@ -311,35 +311,19 @@ constexpr size_t kHashSmem =
     (size_t)kHashStages * kStageWords * 4 + kHashStages * (sizeof(ItemDesc) + 16) + 64;
 
 // Lane l's 32-bit seed window starting at bit 32t + l, from the pre-shifted seed S':
-// funnelshift(S'[t], S'[t+1], l+1) = umulhi(S'[t], m) + S'[t+1] * m with m = 2^(31-l)
-// (the two products occupy disjoint bit ranges). Two IMADs on the otherwise idle FMA pipe
-// replace one SHF on the ALU pipe, which is left to the algorithmic LOP3s alone.
-// kWin selects how the window is formed (both read the pre-shifted seed S'):
-//   0: SHF  — __funnelshift_rc(S'[t], S'[t+1], l+1)  (one ALU-pipe instruction)
-//   1: IMAD — umulhi(S'[t], m) + S'[t+1]*m, m = 2^(31-l) (two FMA-pipe instructions)
-template <int kWin>
+// funnelshift(S'[t], S'[t+1], l+1), one SHF on the ALU pipe. (Round 1 also tried the window
+// as two FMA-pipe IMADs, umulhi(S'[t], 2^(31-l)) + S'[t+1] * 2^(31-l), to leave the ALU pipe
+// to the LOP3s alone; it measured no faster and is not built.)
 __device__ __forceinline__ uint32_t window(uint32_t a, uint32_t b, uint32_t m) {
-    if constexpr (kWin == 0)
-        return __funnelshift_rc(a, b, m);
-    else
-        return __umulhi(a, m) + b * m;
+    return __funnelshift_rc(a, b, m);
 }
 
-// 2^(31-l) per lane, read from memory so ptxas cannot strength-reduce b * m back into an
-// ALU shift.
-__constant__ uint32_t c_lane_mult[32] = {
-    1u << 31, 1u << 30, 1u << 29, 1u << 28, 1u << 27, 1u << 26, 1u << 25, 1u << 24,
-    1u << 23, 1u << 22, 1u << 21, 1u << 20, 1u << 19, 1u << 18, 1u << 17, 1u << 16,
-    1u << 15, 1u << 14, 1u << 13, 1u << 12, 1u << 11, 1u << 10, 1u << 9,  1u << 8,
-    1u << 7,  1u << 6,  1u << 5,  1u << 4,  1u << 3,  1u << 2,  1u << 1,  1u << 0};
-
-template <int kWin>
 __device__ __forceinline__ void hash_tile(const uint32_t* __restrict__ Ys,
                                           const uint32_t* __restrict__ Sw, int L,
                                           uint32_t m, uint32_t (&acc)[R]) {
     uint32_t win[R];
 #pragma unroll
-    for (int t = 0; t < R; ++t) win[t] = window<kWin>(Sw[t], Sw[t + 1], m);
+    for (int t = 0; t < R; ++t) win[t] = window(Sw[t], Sw[t + 1], m);
 #pragma unroll 1
     for (int T = 0; T < L; T += R) {
         const uint32_t* sb = Sw + T + R;
@@ -356,7 +340,7 @@ __device__ __forceinline__ void hash_tile(const uint32_t* __restrict__ Ys,
                 const int q = 4 * g + e;
 #pragma unroll
                 for (int r = 0; r < R; ++r) acc[r] ^= win[(q + r) % R] & yv[e];
-                win[q] = window<kWin>(sv[e], sv[e + 1], m);
+                win[q] = window(sv[e], sv[e + 1], m);
             }
         }
     }
@@ -385,7 +369,6 @@ __device__ __forceinline__ bool decode_item(const HashArgs& a, unsigned long lon
     return true;
 }
 
-template <int kWin>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint32_t* stage_base = reinterpret_cast<uint32_t*>(smem_raw);
@@ -437,8 +420,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) 
     }
 
     // -------------------- compute warps --------------------------------------------------
-    // per-lane window parameter: shift l+1 (SHF) or multiplier 2^(31-l) (IMAD)
-    const uint32_t lane_mult = kWin == 0 ? lane + 1 : c_lane_mult[lane];
+    const uint32_t lane_mult = lane + 1;  // per-lane window shift l+1
     for (uint32_t it = 0;; ++it) {
         const int s = it % kHashStages;
         mbar_wait(&full[s], (it / kHashStages) & 1);
@@ -449,7 +431,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_toeplitz_hash(HashArgs a) 
         uint32_t acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0;
-        hash_tile<kWin>(Ys, Ss + warp * R, (int)d.L, lane_mult, acc);
+        hash_tile(Ys, Ss + warp * R, (int)d.L, lane_mult, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // stage may be refilled
         // lane r%32 collects output word r (R/32 words per lane, R a multiple of 32)
@@ -540,46 +522,25 @@ void launch_reverse(const uint32_t* d_x32, uint64_t nbits, uint32_t* d_y, uint64
     k_reverse<<<(unsigned)blocks, 256, 0, st>>>(d_x32, nbits, d_y, ywords);
 }
 
-int hash_window_mode() {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = std::getenv("SSBH_HASH_WIN");  // dev switch for A/B measurements
-        mode = (e && *e == '1') ? 1 : 0;
-    }
-    return mode;
-}
-
-template <int kWin>
-int hash_grid_size_t(int device) {
-    cudaFuncSetAttribute(k_toeplitz_hash<kWin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+int hash_grid_size(int device) {
+    static int cached[64] = {};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    cudaFuncSetAttribute(k_toeplitz_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kHashSmem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_toeplitz_hash<kWin>,
-                                                  (NW + 1) * 32, kHashSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_toeplitz_hash, (NW + 1) * 32,
+                                                  kHashSmem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return std::max(1, per_sm) * sms;
-}
-
-int hash_grid_size(int device) {
-    static int cached[2][64] = {};
-    const int w = hash_window_mode();
-    if (device >= 0 && device < 64 && cached[w][device]) return cached[w][device];
-    const int g = w ? hash_grid_size_t<1>(device) : hash_grid_size_t<0>(device);
-    if (device >= 0 && device < 64) cached[w][device] = g;
+    const int g = std::max(1, per_sm) * sms;
+    if (device >= 0 && device < 64) cached[device] = g;
     return g;
 }
 
 void launch_hash(const HashArgs& a, int grid, cudaStream_t st) {
-    if (hash_window_mode() == 1) {
-        cudaFuncSetAttribute(k_toeplitz_hash<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kHashSmem);
-        k_toeplitz_hash<1><<<grid, (NW + 1) * 32, kHashSmem, st>>>(a);
-    } else {
-        cudaFuncSetAttribute(k_toeplitz_hash<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kHashSmem);
-        k_toeplitz_hash<0><<<grid, (NW + 1) * 32, kHashSmem, st>>>(a);
-    }
+    cudaFuncSetAttribute(k_toeplitz_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kHashSmem);
+    k_toeplitz_hash<<<grid, (NW + 1) * 32, kHashSmem, st>>>(a);
 }
 
 void launch_concat(const uint32_t* d_blocks, uint32_t kw, uint32_t nown, uint64_t k,

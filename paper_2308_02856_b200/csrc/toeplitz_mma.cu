@@ -6,50 +6,24 @@
 // output is K_j[i] = XOR_c S[i+c] y_j[c] (toeplitz.cu). With ONE shared seed every block
 // multiplies the SAME Hankel matrix H[i][c] = S[i+c], so the whole hash is a GF(2) matrix
 // product D = Y * H^T (blocks x input positions times input positions x output rows), and a
-// GF(2) product is an integer product mod 2: D[j][i] = (sum_c y_j[c] * S[i+c]) mod 2. Per-block
-// seeds (and long shared blocks) tile each block's matrix-vector product into 128 x 128 Hankel
-// blocks instead (k_toeplitz_mma_pb, below). Kernels in this file:
-//   k_toeplitz_mma<AT, sets>  shared seeds, u8 operands (kind::i8, s32 sums wrap mod 2^32)
-//   k_toeplitz_f4<sets>       shared seeds, FP4 operands (kind::mxf4, exact f32 counts), default
-//                             for short blocks
-//   k_toeplitz_mma_pb<F4>     tiled matrix-vector products: per-block seeds, long shared blocks
-// The first is described here; the others where they are defined.
+// GF(2) product is an integer product mod 2: D[j][i] = (sum_c y_j[c] * S[i+c]) mod 2. The
+// tensor cores compute the integer sums exactly on block-scaled FP4 operands (kind::mxf4:
+// every element 0 or 1.0 as E2M1, every UE8M0 scale 1.0, f32 accumulator holding exact
+// integer counts below 2^24) and the epilogue keeps the parity. Per-block seeds (and long
+// shared blocks) tile each block's matrix-vector product into 128 x 128 Hankel blocks
+// instead. Kernels in this file:
+//   k_toeplitz_f4        shared seeds: all owned blocks x one Hankel matrix as a GEMM
+//   k_toeplitz_mma_pb    tiled matrix-vector products: per-block seeds, long shared blocks
 //
-// Operands carry one bit per byte, in the byte's LSB; the other 7 bits may hold anything,
-// because they only add even multiples to the sum (a = a0 + 2a', b = b0 + 2b' gives
-// ab = a0 b0 + 2(...)). That makes both operands cheap to form in shared memory:
-//
-// * K order inside a 256-bit pipeline stage: byte (chunk q = 8g + kc, word w, byte b) of a
-//   K-major row is input position 128g + kc + 8b + 32w (any permutation of K is allowed as
-//   long as both operands use it).
-// * A = Y (M = 128 blocks): chunk q word w of block j is y-word (4g + w) >> kc — one shift
-//   per 4 bytes. Default: written into TMEM by the producers (tcgen05.st, lane = block row,
-//   column 8m + c = chunk 2m + c/4, word c%4 of MMA m); fallback (SSBH_MMA_ATMEM=0): the
-//   canonical no-swizzle K-major smem layout (LBO 128 B along K, SBO 2048 B along M).
-// * B = Hankel (N = 256 output rows): with that K order, row r chunk (g, kc) holds S bits
-//   i0 + c0 + (r + kc + 128g) + 8b + 32w — a function of the UNIT index u = r + kc + 128g
-//   alone. So the operand is a table of 16-byte units, unit u word w = the 32-bit seed
-//   window starting at bit i0 + c0 + u + 32w (one funnel shift), and the descriptor walks
-//   it with LBO = 16 B (next K chunk = next unit) and SBO = 128 B (8 rows = 8 units):
-//   rows overlap in memory exactly as Hankel rows overlap in the seed. 392 units (6 KB)
-//   cover a 256-row x 256-position stage.
-// Operand bytes are masked to 0/1 anyway: the don't-care bits toggling in the multipliers
-// drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965).
-//
-// Kernel: persistent, one CTA per SM, TMEM = one 128 x 256 s32 accumulator + a 4-stage ring
-// of A operands (smem-A fallback: two accumulators). Work item = (M tile of 128 owned blocks,
-// K part, N tile of 256 output rows); every CTA walks items blockIdx.x, +grid, ... with N
-// tiles innermost, so concurrently running CTAs stream the same blocks' y words (L2 reuse).
-// Warp roles:
-//   warps 0-3  epilogue: tcgen05.ld 32x32b (lane = block, 32 columns = 32 rows) -> parity
-//              bits -> one key word per load (st.global, or red.xor when K is split)
-//   warp 4     MMA issuer: 8 x tcgen05.mma (128x256x32) per stage, commit -> stage barrier,
-//              last stage of an item -> accumulator barrier
-//   then two producer sets (set q fills the stages g with g % 2 == q), each of
-//     4 A warps: block row jl, cp.async of its 32 y bytes 4 own stages ahead, 64 columns
-//     4 B warps: cp.async of 128 B of seed per stage, 392 units per stage
-// mbarriers between the roles; one producer set alone left the tensor core ~10 % idle (its
-// per-stage chain is latency-bound), two reach the sustained kind::i8 probe rate.
+// The Hankel operand. With the K order used inside a pipeline stage (chunk q, word w, nibble
+// i = position 128g + kc + 4i + 32w), row r of chunk (g, kc) holds seed bits
+// base + (r + kc + 128g) + 4i + 32w — a function of the UNIT index u = r + kc + 128g alone. So
+// the operand is a table of 16-byte units, unit u word w = the seed window starting at bit
+// base + u + 32w (one funnel shift, masked to the E2M1 1.0 nibble bit), and the descriptor
+// walks it with LBO = 16 B (next K chunk = next unit) and SBO = 128 B (8 rows = 8 units):
+// rows overlap in memory exactly as Hankel rows overlap in the seed.
+// Operand nibbles are masked to clean 0 / 1.0: toggling don't-care bits in the multipliers
+// drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965; round 1).
 #include <algorithm>
 #include <cstdlib>
 
@@ -64,25 +38,7 @@ namespace {
 
 constexpr int kM = 128;                      // blocks per M tile (= TMEM lanes)
 constexpr int kN = 256;                      // output rows per N tile (= accumulator columns)
-constexpr int kMmaK = 32;                    // K bytes per tcgen05.mma kind::i8
-constexpr int kStageK = 256;                 // input positions per pipeline stage
-constexpr int kStageMmas = kStageK / kMmaK;  // 8
-constexpr int kGUnits = kN + 7 + 128 + 1;    // 392 Hankel units per stage
-constexpr int kStages = 5;                   // A in shared memory: 5 x 38 KB
-constexpr int kStagesAT = 4;                 // A in TMEM: 4 x 64 columns next to the accumulator
-constexpr int kPre = 4;                      // cp.async prefetch depth (stages)
-constexpr int kYBytes = kM * kStageK;        // 32768: A operand of one stage
-constexpr int kGBytes = kGUnits * 16;        // 6272: B operand of one stage
-constexpr int kSlotBytes = kYBytes + kGBytes;
-constexpr int kRawYBytes = kPre * kM * 32;   // y words staged by cp.async
-constexpr int kRawSBytes = 4 * kPre * 128;   // seed words staged by cp.async (per B warp)
-// warps 0-3 epilogue, 4 MMA, then kSets producer sets of 4 A warps + 4 B warps; set q fills
-// the stages g with g % kSets == q, so a set has kSets stage-times per stage (its per-stage
-// chain of cp.async wait -> expand -> tcgen05.st / STS -> wait::st -> arrive is latency-bound)
-constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5;
-constexpr int threads_for(int sets) { return (kProdWarp0 + 8 * sets) * 32; }
-constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps
-static_assert(kSlotBytes % 128 == 0, "slot alignment");
+constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps per stage
 
 // ------------------------------------------------------------------ tcgen05 / cp.async
 __device__ __forceinline__ void tc_fence_before() {
@@ -95,31 +51,6 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
-// kind::i8 instruction descriptor: s32 accumulate, u8 x u8, both K-major, M = 128, N = 256.
-constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
-
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(kIdesc), "r"(accum)
-        : "memory");
-}
-// A operand from TMEM (columns a_tmem .. +8: lane = row, 4 K bytes per 32-bit column).
-__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
-                                          uint32_t accum) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(kIdesc), "r"(accum)
-        : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -212,24 +143,6 @@ struct StageIt {
     }
 };
 
-// A producer (one block row jl): stage the row's 256 y bits by cp.async (zero-filled past
-// the block's padded length or past the owned blocks).
-__device__ __forceinline__ void y_prefetch(const MmaHashArgs& a, const StageIt& p, uint32_t jl,
-                                           uint32_t* raw) {
-    const uint32_t* src = a.ybuf;
-    uint32_t bytes = 0;
-    if (p.valid) {
-        const uint32_t jj = p.d.mt * kM + jl;
-        const uint64_t w0 = (uint64_t)(p.d.st0 + p.s) * (kStageK / 32);
-        if (jj < a.nown && w0 < a.lay.ypad[jj]) {
-            src = a.ybuf + a.lay.yoff[jj] + w0;
-            bytes = 16;
-        }
-    }
-    cp_async16(raw, src, bytes);
-    cp_async16(raw + kM * 4, src + 4, bytes);
-}
-
 // B producer warp: stage 32 seed words (pre-shifted seed S', S'[b] = S[b-1]) covering the
 // stage's windows; lanes 0-7 copy 16 B each.
 __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& p, uint32_t lane,
@@ -242,264 +155,6 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
         }
         cp_async16(raw + 4 * lane, a.sbuf + (p.valid ? p.d.soff : 0ull) + q0a + 4 * lane,
                    p.valid ? 16u : 0u);
-    }
-}
-
-// Operand bytes are masked to 0/1 (M8): the 7 don't-care bits would not change the sums mod 2,
-// but toggling them drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965).
-// kAT: the A operand (y bits) lives in TMEM (tcgen05.st from the producers' registers, one
-// 128 x 256 accumulator + a 4-stage A ring) instead of shared memory (two accumulators).
-template <bool kAT, int kSets>
-struct Geo {
-    static constexpr int stages = kAT ? kStagesAT : kStages;
-    static constexpr int slot = kAT ? kGBytes : kSlotBytes;  // shared-memory bytes per stage
-    static constexpr int goff = kAT ? 0 : kYBytes;           // B tile offset in a slot
-    static constexpr int nacc = kAT ? 1 : 2;                 // accumulators
-    static constexpr size_t bar = (size_t)stages * slot + kSets * (kRawYBytes + kRawSBytes);
-    static constexpr size_t smem = bar + (2 * stages + 4) * 8 + 16;
-};
-static_assert(Geo<false, 1>::smem <= 232448 && Geo<true, 2>::smem <= 232448, "smem budget");
-
-template <bool kAT, int kSets>
-__global__ void __launch_bounds__(threads_for(kSets), 1) k_toeplitz_mma(MmaHashArgs a) {
-    using G = Geo<kAT, kSets>;
-    constexpr int kS = G::stages;
-    constexpr uint32_t M8 = 0x01010101u;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* slots = smem;
-    uint32_t* raw_y = reinterpret_cast<uint32_t*>(smem + (size_t)kS * G::slot);
-    uint32_t* raw_s = raw_y + kSets * (kRawYBytes / 4);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::bar);
-    uint64_t* empty = full + kS;
-    uint64_t* tfull = empty + kS;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kS; ++s) {
-            mbar_init(&full[s], kFullArrivals);
-            mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kEpiWarps);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         smem_u32(tmem_slot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp < kEpiWarps) {
-        // ---------------------------------------------------------------- epilogue
-        uint32_t t = 0;
-        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
-            Item d;
-            if (!decode(a, item, d)) break;
-            const uint32_t ab = t % G::nacc;
-            mbar_wait_sleep(&tfull[ab], (t / G::nacc) & 1);
-            tc_fence_after();
-            if (d.nst) {
-                const uint32_t jj = d.mt * kM + warp * 32 + lane;
-                const bool row_ok = jj < a.nown;
-                uint32_t* dst = a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32);
-#pragma unroll 1
-                for (int q = 0; q < kN / 32; ++q) {
-                    uint32_t v[32];
-                    SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kN + 32u * q, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    uint32_t w = 0;
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) w |= (v[e] & 1u) << e;
-                    if (row_ok && d.nt * (kN / 32) + q < a.kw) {
-                        if (a.ksplit == 1)
-                            dst[q] = w;
-                        else
-                            atomicXor(dst + q, w);
-                    }
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ab]);
-        }
-    } else if (warp == kMmaWarp) {
-        // ---------------------------------------------------------------- MMA issuer
-        uint32_t g = 0, t = 0;
-        const uint32_t base_y = smem_u32(slots), base_g = base_y + G::goff;
-        for (uint32_t item = blockIdx.x;; item += gridDim.x, ++t) {
-            Item d;
-            if (!decode(a, item, d)) break;
-            const uint32_t ab = t % G::nacc;
-            if (t >= (uint32_t)G::nacc) mbar_wait_sleep(&tempty[ab], ((t / G::nacc) - 1) & 1);
-            tc_fence_after();
-            if (d.nst == 0) {
-                if (lane == 0) mbar_arrive(&tfull[ab]);
-                continue;
-            }
-            for (uint32_t s = 0; s < d.nst; ++s, ++g) {
-                const uint32_t slot = g % kS;
-                if (a.spin)
-                    mbar_wait(&full[slot], (g / kS) & 1);
-                else
-                    mbar_wait_sleep(&full[slot], (g / kS) & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t ya = base_y + slot * G::slot;
-                    const uint32_t ga = base_g + slot * G::slot;
-#pragma unroll
-                    for (int m = 0; m < kStageMmas; ++m) {
-                        const uint32_t unit = 2u * (m & 3) + 128u * (m >> 2);
-                        const uint64_t bdesc = sdesc(ga + 16u * unit, 16, 128);
-                        if constexpr (kAT)
-                            mma_i8_ts(tmem, tmem + kN + 64u * slot + 8u * m, bdesc,
-                                      (s | (uint32_t)m) != 0);
-                        else
-                            mma_i8(tmem + ab * kN, sdesc(ya + 256u * m, 128, 2048), bdesc,
-                                   (s | (uint32_t)m) != 0);
-                    }
-                    mma_commit(&empty[slot]);
-                    if (s + 1 == d.nst) mma_commit(&tfull[ab]);
-                }
-                __syncwarp();
-            }
-        }
-    } else if (((warp - kProdWarp0) & 7) < 4) {
-        // ---------------------------------------------------------------- A producers
-        // block row: TMEM lane quadrant 32*(warp%4) is the only one this warp may access
-        const uint32_t set = (warp - kProdWarp0) >> 3;
-        const uint32_t jl = kAT ? 32u * (warp & 3) + lane : 32u * ((warp - kProdWarp0) & 3) + lane;
-        // [slot][half][jl][4 words] per set: a warp's reads are contiguous
-        uint32_t* raw = raw_y + set * (kRawYBytes / 4) + jl * 4;
-        StageIt cur, pre;
-        cur.start(a);
-        cur.advance(a, set);
-        pre = cur;
-        for (int i = 0; i < kPre; ++i) {
-            y_prefetch(a, pre, jl, raw + i * kM * 8);
-            cp_async_commit();
-            pre.advance(a, kSets);
-        }
-        const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
-        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
-            const uint32_t rs = i % kPre;
-            cp_async_wait<kPre - 1>();
-            const uint4 x0 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8);
-            const uint4 x1 = *reinterpret_cast<const uint4*>(raw + rs * kM * 8 + kM * 4);
-            const uint32_t slot = g % kS;
-            if (g >= (uint32_t)kS) {
-                if (a.spin >= 2)
-                    mbar_wait(&empty[slot], ((g / kS) - 1) & 1);
-                else
-                    mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
-            }
-            if constexpr (kAT) {
-                // TMEM column 8m + c of the stage = chunk 2m + c/4, word c%4 (K bytes 4c..4c+3
-                // of MMA m, the order of the K-major smem chunks)
-                tc_fence_after();
-                const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                const uint32_t taddr = tmem + ((32u * (warp & 3)) << 16) + kN + 64u * slot;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t v[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int col = 32 * h + e, m = col >> 3, c = col & 7;
-                        const int q = 2 * m + (c >> 2), w = c & 3;
-                        v[e] = (xs[4 * (q >> 3) + w] >> (q & 7)) & M8;
-                    }
-                    SSBH_TMEM_ST32(taddr + 32u * h, v);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                tc_fence_before();
-            } else {
-                uint8_t* ys = slots + (size_t)slot * G::slot + row_off;
-#pragma unroll
-                for (int kc = 0; kc < 8; ++kc) {
-                    *reinterpret_cast<uint4*>(ys + kc * 128) =
-                        make_uint4((x0.x >> kc) & M8, (x0.y >> kc) & M8, (x0.z >> kc) & M8,
-                                   (x0.w >> kc) & M8);
-                    *reinterpret_cast<uint4*>(ys + (8 + kc) * 128) =
-                        make_uint4((x1.x >> kc) & M8, (x1.y >> kc) & M8, (x1.z >> kc) & M8,
-                                   (x1.w >> kc) & M8);
-                }
-                fence_proxy_async_smem();
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[slot]);
-            // refill the raw slot just consumed (its values are in registers and stored)
-            y_prefetch(a, pre, jl, raw + rs * kM * 8);
-            cp_async_commit();
-            pre.advance(a, kSets);
-        }
-        cp_async_wait<0>();
-    } else {
-        // ---------------------------------------------------------------- B producers
-        const uint32_t set = (warp - kProdWarp0) >> 3;
-        const uint32_t gw = ((warp - kProdWarp0) & 7) - 4;  // 0..3
-        const uint32_t gt = gw * 32 + lane;                 // 0..127
-        uint32_t* raw = raw_s + set * (kRawSBytes / 4) + gw * kPre * 32;
-        StageIt cur, pre;
-        cur.start(a);
-        cur.advance(a, set);
-        pre = cur;
-        for (int i = 0; i < kPre; ++i) {
-            s_prefetch(a, pre, lane, raw + i * 32);
-            cp_async_commit();
-            pre.advance(a, kSets);
-        }
-        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
-            const uint32_t rs = i % kPre;
-            cp_async_wait<kPre - 1>();
-            __syncwarp();  // the warp's copies are visible to every lane
-            const uint32_t* sw = raw + rs * 32;
-            const uint64_t b1 =
-                (uint64_t)cur.d.nt * kN + (uint64_t)(cur.d.st0 + cur.s) * kStageK + 1;
-            const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));  // < 128
-            const uint32_t slot = g % kS;
-            if (g >= (uint32_t)kS) {
-                if (a.spin >= 2)
-                    mbar_wait(&empty[slot], ((g / kS) - 1) & 1);
-                else
-                    mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
-            }
-            uint8_t* gs = slots + (size_t)slot * G::slot + G::goff;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const uint32_t u = gt + 128u * r;
-                if (u < (uint32_t)kGUnits) {
-                    const uint32_t rel = rel0 + u;
-                    const uint32_t q = rel >> 5, sh = rel & 31;
-                    const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3],
-                                   w4 = sw[q + 4];
-                    *reinterpret_cast<uint4*>(gs + 16 * u) =
-                        make_uint4(__funnelshift_r(w0, w1, sh) & M8, __funnelshift_r(w1, w2, sh) & M8,
-                                   __funnelshift_r(w2, w3, sh) & M8, __funnelshift_r(w3, w4, sh) & M8);
-                }
-            }
-            fence_proxy_async_smem();
-            __syncwarp();  // every lane is done with raw slot rs before it is refilled
-            if (lane == 0) mbar_arrive(&full[slot]);
-            s_prefetch(a, pre, lane, raw + rs * 32);
-            cp_async_commit();
-            pre.advance(a, kSets);
-        }
-        cp_async_wait<0>();
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
 }
 
@@ -527,15 +182,12 @@ constexpr int kF4YBytes = kM * kF4StageK / 2;     // 32768
 constexpr int kF4GBytes = ((kF4GUnits * 16 + 127) / 128) * 128;  // 10368
 constexpr int kF4Slot = kF4YBytes + kF4GBytes;
 constexpr int kF4Stages = 4;
-#ifndef SSBH_F4_PRE
-#define SSBH_F4_PRE 2
-#endif
-constexpr int kF4Pre = SSBH_F4_PRE;               // cp.async prefetch depth per set
+constexpr int kF4Pre = 2;                         // cp.async prefetch depth per set
 constexpr int kF4RawY = kF4Pre * kM * 64;         // per set
 constexpr int kF4RawS = 4 * kF4Pre * 128;         // per set
 __host__ __device__ constexpr size_t f4_bar(int sets) { return (size_t)kF4Stages * kF4Slot + sets * (kF4RawY + kF4RawS); }
 __host__ __device__ constexpr size_t f4_smem(int sets) { return f4_bar(sets) + (2 * kF4Stages + 4) * 8 + 16; }
-static_assert(f4_smem(SSBH_F4_PRE > 2 ? 2 : 3) <= 232448, "f4 smem budget");
+static_assert(f4_smem(2) <= 232448, "f4 smem budget");
 // exact f32 counts per round, < 2^23 so that the epilogue's parity read (count + 2^23: the
 // integer lands in the low mantissa bits, FADD instead of the slower F2I) stays exact
 constexpr uint32_t kF4MaxStages = (1u << 23) / kF4StageK;
@@ -588,29 +240,15 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
     for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
 }
 
-// kRegY variant of the A producers: the row's 512 y bits go global -> registers (one stage ahead)
-// instead of global -> shared (cp.async) -> registers, taking 16 KB per stage of shared-memory
-// traffic off the pipe the producers' operand stores and the MMA's operand reads share.
-__device__ __forceinline__ void y_load_f4(const MmaHashArgs& a, const StageIt& p, uint32_t jl,
-                                          uint4 (&x)[4]) {
-#pragma unroll
-    for (int h = 0; h < 4; ++h) x[h] = make_uint4(0u, 0u, 0u, 0u);
-    if (p.valid) {
-        const uint32_t jj = p.d.mt * kM + jl;
-        const uint64_t w0 = (uint64_t)(p.d.st0 + p.s) * (kF4StageK / 32);
-        if (jj < a.nown && w0 < a.lay.ypad[jj]) {
-            const uint4* src = reinterpret_cast<const uint4*>(a.ybuf + a.lay.yoff[jj] + w0);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) x[h] = __ldg(src + h);
-        }
-    }
-}
-
-// kE epilogue warps: 4 (one per TMEM sub-partition) or 8 (two per sub-partition, half of the
-// 256 accumulator columns each: a shorter drain of the single accumulator between work items)
-constexpr int f4_threads(int sets, int epi) { return (epi + 1 + 8 * sets) * 32; }
-template <int kSets, bool kRegY, int kE>
-__global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHashArgs a) {
+// Warp roles: 8 epilogue warps (two per TMEM sub-partition, half of the 256 accumulator
+// columns each: a shorter drain of the single accumulator between work items; 1.4 % faster
+// than 4 in round 1), 1 MMA warp, then two producer sets of 4 A + 4 B warps that fill
+// alternate stages (one set's per-stage chain — cp.async wait -> expand -> STS -> arrive — is
+// latency-bound). Round-1 A/B variants that lost (3 producer sets, register-staged y, 4
+// epilogue warps, double-buffered TMEM loads, a polling MMA warp) are not built.
+constexpr int kSets = 2, kE = 8;
+constexpr int kF4Threads = (kE + 1 + 8 * kSets) * 32;
+__global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     constexpr int kEpiW = kE, kMmaW = kE, kProd0 = kE + 1;
     constexpr int kQW = (kN / 32) / (kE / 4);  // accumulator column groups per epilogue warp
     constexpr int kS = kF4Stages;
@@ -671,28 +309,6 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
                 mbar_wait_sleep(&tfull[0], t & 1);
                 tc_fence_after();
                 if (d.nst) {
-#ifdef SSBH_F4_EPI_DB
-                    // double-buffered: column group q + 1 is loaded while q's parities are formed
-                    uint32_t v0[32], v1[32];
-                    const uint32_t ta = tmem + ((sp * 32u) << 16) + 32u * qb;
-                    SSBH_TMEM_LD32(ta, v0);
-#pragma unroll
-                    for (int q = 0; q < kQW; ++q) {
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        uint32_t* cur = (q & 1) ? v1 : v0;
-                        if (q + 1 < kQW) {
-                            if (q & 1)
-                                SSBH_TMEM_LD32(ta + 32u * (q + 1), v0);
-                            else
-                                SSBH_TMEM_LD32(ta + 32u * (q + 1), v1);
-                        }
-                        uint32_t w = 0;
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            w |= (__float_as_uint(__uint_as_float(cur[e]) + 8388608.0f) & 1u) << e;
-                        acc_w[q] ^= w;
-                    }
-#else
 #pragma unroll 1
                     for (int q = 0; q < kQW; ++q) {
                         uint32_t v[32];
@@ -704,7 +320,6 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
                             w |= (__float_as_uint(__uint_as_float(v[e]) + 8388608.0f) & 1u) << e;
                         acc_w[q] ^= w;
                     }
-#endif
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -743,12 +358,9 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
                 const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
                 for (uint32_t s = s0; s < s1; ++s, ++g) {
                     const uint32_t slot = g % kS;
-                    // default (SSBH_MMA_F4_SPIN unset): hardware-suspended wait, no try_wait polls
-                    // on the L1 data pipe the producers' stores and the MMA operand reads share
-                    if (a.spin)
-                        mbar_wait(&full[slot], (g / kS) & 1);
-                    else
-                        mbar_wait_sleep(&full[slot], (g / kS) & 1);
+                    // hardware-suspended wait: no try_wait polls on the L1 data pipe the
+                    // producers' stores and the MMA operand reads share (round 1: 1.1 % faster)
+                    mbar_wait_sleep(&full[slot], (g / kS) & 1);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t ya = base_y + slot * kF4Slot;
@@ -792,21 +404,6 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
         cur.start(a);
         cur.advance(a, set);
         pre = cur;
-        if constexpr (kRegY) {
-            uint4 x[4];
-            y_load_f4(a, pre, jl, x);
-            pre.advance(a, kSets);
-            for (uint32_t g = set; cur.valid; g += kSets, cur.advance(a, kSets)) {
-                uint4 nx[4];
-                y_load_f4(a, pre, jl, nx);  // next stage's bits in flight while this one is stored
-                pre.advance(a, kSets);
-                const uint32_t slot = g % kS;
-                if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
-                expand(x, slot);
-#pragma unroll
-                for (int h = 0; h < 4; ++h) x[h] = nx[h];
-            }
-        } else {
         uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
         for (int i = 0; i < kF4Pre; ++i) {
             y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
@@ -828,7 +425,6 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
             pre.advance(a, kSets);
         }
         cp_async_wait<0>();
-        }
     } else {
         // ---------------------------------------------------------------- B producers
         const uint32_t set = (warp - kProd0) >> 3;
@@ -917,14 +513,9 @@ __global__ void __launch_bounds__(f4_threads(kSets, kE), 1) k_toeplitz_f4(MmaHas
 constexpr int kPbWin = 256;                  // row tiles per work item (accumulator columns)
 constexpr int kPbL = 256;                    // D steps per y buffer
 constexpr int kPbUnits = 512;                // units per K-chunk plane of a y buffer
-#ifndef SSBH_PB_SD_F4
-#define SSBH_PB_SD_F4 8  // 8 D steps (16 MMAs) per stage: config 3 hash 144.6 -> 137.6 ms vs 4
-#endif
-#ifndef SSBH_PB_HST
-#define SSBH_PB_HST 8
-#endif
-constexpr int kPbHStages = SSBH_PB_HST;
+constexpr int kPbHStages = 8;                // Hankel stages in flight
 constexpr int kPbThreads = 13 * 32;          // 4 epilogue, 1 MMA, 4 y, 4 Hankel warps
+constexpr int kPbEpiWarps = 4, kPbMmaWarp = 4, kPbProdWarp0 = 5;
 // kind::i8, M = 128, N = 256 (same instruction descriptor as the shared kernel)
 
 struct PbItem {
@@ -953,33 +544,30 @@ __device__ __forceinline__ bool pb_decode(const PbHashArgs& a, uint32_t item, Pb
     return true;
 }
 
-// kF4: the same tiling on FP4 operands (kind::mxf4, E2M1 0 / 1.0, unit scales; 2x the MAC
-// rate). A D step is then 2 MMAs of K = 64; the y buffer has 4 K-chunk planes (position
-// kc + 4i + 32w of the 128-chunk, word w = ((y word >> kc) << 1) & 0x22222222) and the Hankel
-// unit u word w = (S' window at bit 128 D + u + 32 w) & 0x22222222. TMEM: one f32 accumulator
-// + the constant scale factors; the f32 counts are exact below 2^24, so longer rows of D
-// steps accumulate in rounds of 2^17 steps whose parities are XORed.
-// A pipeline stage is kSD consecutive D steps (8 MMAs): H_{D+1} is H_D shifted by 128 units, so
-// 128 kSD + 8 units cover all of them and the per-stage barrier work is amortised.
-template <bool kF4>
+// FP4 operands (kind::mxf4, E2M1 0 / 1.0, unit scales): a D step is 2 MMAs of K = 64; the y
+// buffer has 4 K-chunk planes (position kc + 4i + 32w of the 128-chunk, word w =
+// ((y word >> kc) << 1) & 0x22222222) and the Hankel unit u word w = (S' window at bit
+// 128 D + u + 32 w) & 0x22222222. TMEM: one f32 accumulator + the constant scale factors; the
+// f32 counts are exact below 2^24, so longer rows of D steps accumulate in rounds of 2^17 steps
+// whose parities are XORed. A pipeline stage is kSD consecutive D steps: H_{D+1} is H_D shifted
+// by 128 units, so 128 kSD + 8 units cover all of them and the per-stage barrier work is
+// amortised (round 1: 8 steps per stage 144.6 -> 137.6 ms at config 3 against 4).
 struct PbGeo {
-    static constexpr int planes = kF4 ? 4 : 8;      // K-chunk planes of a y buffer
-    static constexpr int mmas = kF4 ? 2 : 4;        // MMAs per D step (K = 128 positions)
-    static constexpr int sd = kF4 ? SSBH_PB_SD_F4 : 2;  // D steps per stage
+    static constexpr int planes = 4;               // K-chunk planes of a y buffer
+    static constexpr int mmas = 2;                 // MMAs per D step (K = 128 positions)
+    static constexpr int sd = 8;                   // D steps per stage
     static constexpr int hunits = 128 * sd + 8;
     static constexpr int hbytes = hunits * 16;
     static constexpr int ybytes = planes * kPbUnits * 16;
-    static constexpr int nacc = kF4 ? 1 : 2;
     static constexpr size_t bar = 2 * (size_t)ybytes + (size_t)kPbHStages * hbytes;
     static constexpr size_t smem = bar + (2 * kPbHStages + 8) * 8 + 16;
     static_assert(kPbL % sd == 0, "stages must not straddle y buffers");
 };
 constexpr uint32_t kPbF4MaxSteps = (1u << 24) / 128;  // D steps per f32-exact round
 
-template <bool kF4>
 __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a) {
-    using G = PbGeo<kF4>;
-    constexpr uint32_t kRound = kF4 ? kPbF4MaxSteps : 0xFFFFFFFFu;
+    using G = PbGeo;
+    constexpr uint32_t kRound = kPbF4MaxSteps;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* ybufs = smem;                                  // 2 y buffers
     uint8_t* hst = smem + 2 * (size_t)G::ybytes;            // kPbHStages x G::hbytes
@@ -990,7 +578,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
     uint64_t* tfull = yempty + 2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    constexpr uint32_t M8 = 0x01010101u, M2 = 0x22222222u;
+    constexpr uint32_t M2 = 0x22222222u;
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -1002,7 +590,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
             mbar_init(&yfull[b], 4);
             mbar_init(&yempty[b], 1);
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kEpiWarps);
+            mbar_init(&tempty[b], kPbEpiWarps);
         }
         fence_barrier_init();
     }
@@ -1016,20 +604,18 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if constexpr (kF4) {
-        if (warp < kEpiWarps) {  // constant scale factors 0x7f = 2^0
-            uint32_t v[32];
+    if (warp < kPbEpiWarps) {  // constant scale factors 0x7f = 2^0
+        uint32_t v[32];
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = 0x7F7F7F7Fu;
-            SSBH_TMEM_ST32(tmem + ((warp * 32u) << 16) + kF4SfCol, v);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
+        for (int e = 0; e < 32; ++e) v[e] = 0x7F7F7F7Fu;
+        SSBH_TMEM_ST32(tmem + ((warp * 32u) << 16) + kF4SfCol, v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
-    if (warp < kEpiWarps) {
+    if (warp < kPbEpiWarps) {
         // ------------------------------------------------------------------ epilogue
         uint32_t t = 0;  // accumulation rounds consumed
         for (uint32_t item = blockIdx.x;; item += gridDim.x) {
@@ -1040,21 +626,19 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
 #pragma unroll
             for (int q = 0; q < kPbWin / 32; ++q) acc[q] = 0;
             for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
-                const uint32_t ab = t % G::nacc;
-                mbar_wait_sleep(&tfull[ab], (t / G::nacc) & 1);
+                mbar_wait_sleep(&tfull[0], t & 1);
                 tc_fence_after();
                 if (d.nD) {
 #pragma unroll 1
                     for (int q = 0; q < kPbWin / 32; ++q) {
                         if (32u * q >= d.ncols) break;  // columns past the window's tiles
                         uint32_t v[32];
-                        SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + ab * kPbWin + 32u * q, v);
+                        SSBH_TMEM_LD32(tmem + ((warp * 32u) << 16) + 32u * q, v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         uint32_t mine = 0;
 #pragma unroll
                         for (int e = 0; e < 32; ++e) {
-                            const uint32_t bit = kF4 ? __float2uint_rz(__uint_as_float(v[e])) & 1u
-                                                     : v[e] & 1u;
+                            const uint32_t bit = __float2uint_rz(__uint_as_float(v[e])) & 1u;
                             const uint32_t wd = __ballot_sync(0xffffffffu, bit);
                             if (lane == (uint32_t)e) mine = wd;
                         }
@@ -1063,7 +647,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[ab]);
+                if (lane == 0) mbar_arrive(&tempty[0]);
             }
             if (d.nD) {
                 uint32_t* dst = a.out + (unsigned long long)d.jj * a.out_stride;
@@ -1078,7 +662,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 }
             }
         }
-    } else if (warp == kMmaWarp) {
+    } else if (warp == kPbMmaWarp) {
         // ------------------------------------------------------------------ MMA issuer
         uint32_t hs = 0, yb = 0, t = 0;
         const uint32_t ybase = smem_u32(ybufs), hbase = smem_u32(hst);
@@ -1086,21 +670,19 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
             PbItem d;
             if (!pb_decode(a, item, d)) break;
             if (d.nD == 0) {
-                const uint32_t ab = t % G::nacc;
-                if (t >= (uint32_t)G::nacc) mbar_wait_sleep(&tempty[ab], ((t / G::nacc) - 1) & 1);
-                if (lane == 0) mbar_arrive(&tfull[ab]);
+                if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
+                if (lane == 0) mbar_arrive(&tfull[0]);
                 ++t;
                 continue;
             }
-            uint32_t ab = 0, round_end = 0;
-            const uint32_t idesc = kF4 ? f4_idesc(d.nmma) : kIdesc;
+            uint32_t round_end = 0;
+            const uint32_t idesc = f4_idesc(d.nmma);
             // D0: D step relative to the item's first step d.s0
             for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
                 if (D0 % kRound == 0) {  // a new accumulation round (kRound is a multiple of kPbL)
-                    ab = t % G::nacc;
-                    if (t >= (uint32_t)G::nacc) mbar_wait_sleep(&tempty[ab], ((t / G::nacc) - 1) & 1);
+                    if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
                     tc_fence_after();
-                    round_end = kF4 ? min(d.nD, D0 + kRound) : d.nD;
+                    round_end = min(d.nD, D0 + kRound);
                 }
                 const uint32_t b = yb & 1;
                 mbar_wait(&yfull[b], (yb >> 1) & 1);
@@ -1123,25 +705,22 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                             for (int m = 0; m < G::mmas; ++m) {
                                 const uint64_t adesc = sdesc(ha + 2048u * j + 32u * m, 16, 128);
                                 const uint64_t bdesc = sdesc(ya + 2u * m * (kPbUnits * 16), kPbUnits * 16, 128);
-                                if constexpr (kF4)
-                                    mma_f4n(tmem, adesc, bdesc, idesc, tmem + kF4SfCol,
-                                            (first | (uint32_t)m) != 0);
-                                else
-                                    mma_i8(tmem + ab * kPbWin, adesc, bdesc, (first | (uint32_t)m) != 0);
+                                mma_f4n(tmem, adesc, bdesc, idesc, tmem + kF4SfCol,
+                                        (first | (uint32_t)m) != 0);
                             }
                         }
                         mma_commit(&hempty[slot]);
                         if (sb + nst == steps) mma_commit(&yempty[b]);
-                        if (D0 + sb + nst == round_end) mma_commit(&tfull[ab]);
+                        if (D0 + sb + nst == round_end) mma_commit(&tfull[0]);
                     }
                     __syncwarp();
                 }
                 if (D0 + steps == round_end) ++t;
             }
         }
-    } else if (warp < kProdWarp0 + 4) {
+    } else if (warp < kPbProdWarp0 + 4) {
         // ------------------------------------------------------------------ y buffers
-        const uint32_t yt = threadIdx.x - kProdWarp0 * 32;  // 0..127
+        const uint32_t yt = threadIdx.x - kPbProdWarp0 * 32;  // 0..127
         uint32_t yb = 0;
         for (uint32_t item = blockIdx.x;; item += gridDim.x) {
             PbItem d;
@@ -1161,10 +740,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                     if (C >= 0 && C < (int64_t)d.nC) x = __ldg(reinterpret_cast<const uint4*>(y) + C);
 #pragma unroll
                     for (int kc = 0; kc < G::planes; ++kc) {
-                        auto f = [&](uint32_t v) {
-                            if constexpr (kF4) return (kc ? v >> (kc - 1) : v << 1) & M2;
-                            else return (v >> kc) & M8;
-                        };
+                        auto f = [&](uint32_t v) { return (kc ? v >> (kc - 1) : v << 1) & M2; };
                         *reinterpret_cast<uint4*>(buf + (kc * kPbUnits + P) * 16) =
                             make_uint4(f(x.x), f(x.y), f(x.z), f(x.w));
                     }
@@ -1176,7 +752,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
         }
     } else {
         // ------------------------------------------------------------------ Hankel units
-        const uint32_t ht = threadIdx.x - (kProdWarp0 + 4) * 32;  // 0..127
+        const uint32_t ht = threadIdx.x - (kPbProdWarp0 + 4) * 32;  // 0..127
         uint32_t hs = 0;
         for (uint32_t item = blockIdx.x;; item += gridDim.x) {
             PbItem d;
@@ -1194,10 +770,9 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 for (int r = 0; r < (G::hunits + 127) / 128; ++r) {
                     const uint32_t u = ht + 128u * r;
                     if (u < (uint32_t)G::hunits) {
-                        // i8: S bit 128D + u + 32w + 8b at bit 8b (S' window one bit up);
-                        // f4: S bit 128D + u + 32w + 4i at bit 4i + 1 (S' window at the bit)
-                        const uint32_t rel = kF4 ? u : u + 1, q = rel >> 5, sh = rel & 31;
-                        const uint32_t mk = kF4 ? M2 : M8;
+                        // S bit 128D + u + 32w + 4i at bit 4i + 1 (the S' window at the bit)
+                        const uint32_t rel = u, q = rel >> 5, sh = rel & 31;
+                        const uint32_t mk = M2;
                         const uint32_t* p = sw + wbase + q;
                         const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2),
                                        w3 = __ldg(p + 3), w4 = __ldg(p + 4);
@@ -1242,16 +817,6 @@ __global__ void k_mma_tiles(const uint32_t* __restrict__ ypad, uint32_t nown,
 
 uint32_t mma_mtiles(uint32_t nown) { return (nown + kM - 1) / kM; }
 
-// FP4 (kind::mxf4) operands for shared seeds: 2x the kind::i8 MAC rate (default);
-// SSBH_MMA_FP4=0 keeps the i8 variant (dev A/B knob).
-bool mma_uses_fp4() {
-    static const int fp4 = [] {
-        const char* e = std::getenv("SSBH_MMA_FP4");
-        return e && *e == '0' ? 0 : 1;
-    }();
-    return fp4 != 0;
-}
-
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) {
     MmaGeom g{};
     g.mtiles = mma_mtiles(nown);
@@ -1261,23 +826,15 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     g.grid = sms;
     // K split: the smallest split whose item count leaves the last wave >= 90 % full (or gives
     // >= 8 waves), keeping >= 8 stages per part (FP4 stages are 512 positions)
-    const uint64_t stage_bits = mma_uses_fp4() ? 512 : kStageK;
+    const uint64_t stage_bits = kF4StageK;
     const uint64_t mean_stages = std::max<uint64_t>(1, (mean_nj + stage_bits - 1) / stage_bits);
     const uint64_t base = (uint64_t)g.mtiles * g.ntiles;
     g.ksplit = 1;
-    static const uint32_t forced = [] {  // dev knob SSBH_MMA_KSPLIT
-        const char* e = std::getenv("SSBH_MMA_KSPLIT");
-        return e ? (uint32_t)std::strtoul(e, nullptr, 10) : 0u;
-    }();
-    if (forced) {
-        g.ksplit = forced;
-    } else {
-        for (uint32_t ks = 1; ks <= 16; ++ks) {
-            if (ks > 1 && mean_stages / ks < 8) break;
-            g.ksplit = ks;
-            const uint64_t items = base * ks, waves = (items + sms - 1) / sms;
-            if (waves >= 8 || (double)items / (double)(waves * sms) >= 0.9) break;
-        }
+    for (uint32_t ks = 1; ks <= 16; ++ks) {
+        if (ks > 1 && mean_stages / ks < 8) break;
+        g.ksplit = ks;
+        const uint64_t items = base * ks, waves = (items + sms - 1) / sms;
+        if (waves >= 8 || (double)items / (double)(waves * sms) >= 0.9) break;
     }
     g.items = base * g.ksplit;
     return g;
@@ -1318,98 +875,20 @@ void launch_hash_mma_pb(const PbHashArgs& a0, const PbGeom& g, cudaStream_t st) 
     if (g.nparts > 1)  // the parts XOR into the output rows
         cudaMemset2DAsync(a.out, a.out_stride * 4, 0, (size_t)a.kw * 4, a.nown, st);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
-    if (mma_uses_fp4()) {
-        cudaFuncSetAttribute(k_toeplitz_mma_pb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)PbGeo<true>::smem);
-        k_toeplitz_mma_pb<true><<<grid, kPbThreads, PbGeo<true>::smem, st>>>(a);
-    } else {
-        cudaFuncSetAttribute(k_toeplitz_mma_pb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)PbGeo<false>::smem);
-        k_toeplitz_mma_pb<false><<<grid, kPbThreads, PbGeo<false>::smem, st>>>(a);
-    }
+    cudaFuncSetAttribute(k_toeplitz_mma_pb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)PbGeo::smem);
+    k_toeplitz_mma_pb<<<grid, kPbThreads, PbGeo::smem, st>>>(a);
 }
-
-size_t mma_hash_smem() { return Geo<true, 2>::smem; }
 
 void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     if (!a0.nown || !g.items) return;
     k_mma_tiles<<<g.mtiles, kM, 0, st>>>(a0.lay.ypad, a0.nown, a0.mt_words);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
-    // MMA warp: spinning on its stage barriers measured 2 % faster than suspending (config 3
-    // hash 285.4 -> 279.2 ms). Dev A/B knob SSBH_MMA_SPIN: 0 = suspend, 1 = MMA warp spins
-    // (default), 2 = producers spin on their slot barriers too.
-    static const int spin = [] {
-        const char* e = std::getenv("SSBH_MMA_SPIN");
-        return e && *e ? *e - '0' : 1;
-    }();
     MmaHashArgs a = a0;
-    a.spin = spin;
-    a.stage_bits = kStageK;
-    if (mma_uses_fp4()) {
-        a.stage_bits = kF4StageK;
-        // producer sets (dev A/B knob SSBH_MMA_F4_SETS=2|3; default 2); A producers' y path
-        // (dev A/B knob SSBH_MMA_F4_REGY=1: global -> registers, 0: cp.async staging)
-        static const int sets = [] {
-            const char* e = std::getenv("SSBH_MMA_F4_SETS");
-            return e && *e == '3' ? 3 : 2;  // 3 sets measured no faster (157-158 ms)
-        }();
-        // MMA-warp stage wait (dev A/B knob SSBH_MMA_F4_SPIN=1: poll): the hardware-suspended
-        // wait measured 1.1 % faster on the split's leaf GEMM (config 3 hash 45.13 -> 44.65 ms,
-        // profiles/r01_ab_leaf_gemm.md) — polls compete for the L1 data pipe with the producers
-        static const int f4spin = [] {
-            const char* e = std::getenv("SSBH_MMA_F4_SPIN");
-            return e && *e == '1' ? 1 : 0;
-        }();
-        a.spin = f4spin;
-        static const bool regy = [] {
-            const char* e = std::getenv("SSBH_MMA_F4_REGY");
-            return e && *e == '1';
-        }();
-        // epilogue warps: two per TMEM sub-partition (8) measured 1.4 % faster on the split's
-        // leaf GEMM (config 3 hash 44.63 -> 43.99 ms, config 2 0.199 -> 0.195 ms); dev A/B knob
-        // SSBH_MMA_F4_EPI=4
-        static const int epi = [] {
-            const char* e = std::getenv("SSBH_MMA_F4_EPI");
-            return e && *e == '4' ? 4 : 8;
-        }();
-        auto go = [&](auto kern, int s, int e) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f4_smem(s));
-            kern<<<grid, f4_threads(s, e), f4_smem(s), st>>>(a);
-        };
-        if (sets == 2 && epi == 8 && !regy)
-            go(k_toeplitz_f4<2, false, 8>, 2, 8);
-        else if (sets == 2)
-            regy ? go(k_toeplitz_f4<2, true, 4>, 2, 4) : go(k_toeplitz_f4<2, false, 4>, 2, 4);
-        else
-            regy ? go(k_toeplitz_f4<3, true, 4>, 3, 4) : go(k_toeplitz_f4<3, false, 4>, 3, 4);
-        return;
-    }
-    // dev A/B knobs: SSBH_MMA_ATMEM=0 stages A in shared memory (one producer set);
-    // SSBH_MMA_SETS=1|2 producer sets with A in TMEM (default 2)
-    static const int atmem = [] {
-        const char* e = std::getenv("SSBH_MMA_ATMEM");
-        return e && *e == '0' ? 0 : 1;
-    }();
-    static const int sets = [] {
-        const char* e = std::getenv("SSBH_MMA_SETS");
-        return e && *e == '1' ? 1 : 2;
-    }();
-    if (!atmem) {
-        using G = Geo<false, 1>;
-        cudaFuncSetAttribute(k_toeplitz_mma<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)G::smem);
-        k_toeplitz_mma<false, 1><<<grid, threads_for(1), G::smem, st>>>(a);
-    } else if (sets == 1) {
-        using G = Geo<true, 1>;
-        cudaFuncSetAttribute(k_toeplitz_mma<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)G::smem);
-        k_toeplitz_mma<true, 1><<<grid, threads_for(1), G::smem, st>>>(a);
-    } else {
-        using G = Geo<true, 2>;
-        cudaFuncSetAttribute(k_toeplitz_mma<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)G::smem);
-        k_toeplitz_mma<true, 2><<<grid, threads_for(2), G::smem, st>>>(a);
-    }
+    a.stage_bits = kF4StageK;
+    cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)f4_smem(kSets));
+    k_toeplitz_f4<<<grid, kF4Threads, f4_smem(kSets), st>>>(a);
 }
 
 }  // namespace ssbh_impl

@@ -176,42 +176,6 @@ __global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vl
     }
 }
 
-// key word w of block jj = remainder ^ XOR over segments of the leaves that reach word w.
-__global__ void k_split_combine(const uint32_t* __restrict__ vout, const uint32_t* __restrict__ rem,
-                                uint32_t jj0, uint32_t count, uint32_t kw, SplitGeom g,
-                                uint32_t* __restrict__ out, unsigned long long out_stride) {
-    const uint64_t lw = g.sL / 32;
-    const uint64_t total = (uint64_t)count * kw;
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t jl = (uint32_t)(e / kw), w = (uint32_t)(e % kw);  // block jj0 + jl
-        uint32_t acc = rem[(uint64_t)(jj0 + jl) * kw + w];
-        // the word's half at each level selects Q (low) or R (high) next to P
-        uint32_t hsel = 0;  // bit l set: high half at level l
-        uint64_t i = (uint64_t)w * 32, m = g.k;
-        for (uint32_t l = 0; l < g.L; ++l) {
-            m >>= 1;
-            if (i >= m) {
-                hsel |= 1u << l;
-                i -= m;
-            }
-        }
-        const uint64_t wl = i / 32;  // word inside a leaf
-        for (uint32_t t = 0; t < g.T; ++t) {
-            for (uint32_t sub = 0; sub < (1u << g.L); ++sub) {  // bit l: P (0) or Q/R (1)
-                uint32_t path = 0;
-                for (uint32_t l = 0; l < g.L; ++l) {
-                    const uint32_t d = (sub >> l & 1u) ? ((hsel >> l & 1u) ? 2u : 1u) : 0u;
-                    path = path * 3 + d;
-                }
-                const uint64_t v = ((uint64_t)t * g.leaves + path) * g.gpad + jl;
-                acc ^= vout[v * lw + wl];
-            }
-        }
-        out[(unsigned long long)(jj0 + jl) * out_stride + w] = acc;
-    }
-}
-
 // Hierarchical combine, one level per launch: the nodes of level l - 1 from their children at
 // level l (child size m = k >> l bits, cw = m / 32 words): node = [P ^ Q | P ^ R]. Node
 // (t, p, jl) of level l sits at ((t * 3^l + p) * gpad + jl) * (k >> l) / 32. Reads 2 words per
@@ -371,18 +335,10 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
     const uint64_t total = (uint64_t)count * kw;
     if (!total) return 0;
     const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
-    // flat (one pass, 2^L reads per key word) or level by level (default; dev A/B knob
-    // SSBH_MMA_SPLIT_COMBINE=flat)
-    static const bool flat = [] {
-        const char* e = std::getenv("SSBH_MMA_SPLIT_COMBINE");
-        return e && std::strcmp(e, "flat") == 0;
-    }();
-    if (flat || g.L == 1) {
-        if (g.L == 1)
-            k_split_root<<<grid, 256, 0, st>>>(d_vout, d_rem, jj0, count, kw, g, d_out, out_stride);
-        else
-            k_split_combine<<<grid, 256, 0, st>>>(d_vout, d_rem, jj0, count, kw, g, d_out,
-                                                  out_stride);
+    // level by level (a flat one-pass combine reads 2^L words per key word: round 1 config 3
+    // 2.99 -> 1.93 ms)
+    if (g.L == 1) {
+        k_split_root<<<grid, 256, 0, st>>>(d_vout, d_rem, jj0, count, kw, g, d_out, out_stride);
         return 1;
     }
     uint32_t* src = d_vout;

@@ -12,7 +12,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, cases, q):
+def _worker(rank, world, port, cases, q, overrides):
     import torch
     import torch.distributed as dist
 
@@ -23,6 +23,7 @@ def _worker(rank, world, port, cases, q):
     from oracle.pyoracle import Oracle
     from paper_2308_02856_b200.multigpu import ShardedExtractor, gather_key
 
+    P.set_overrides(**overrides)
     torch.cuda.set_device(0)
     o = Oracle()
     res = []
@@ -49,7 +50,7 @@ def _worker(rank, world, port, cases, q):
     q.put((rank, res))
 
 
-def _run(world, cases):
+def _run(world, cases, overrides=None):
     import multiprocessing as mp
 
     with socket.socket() as sk:
@@ -57,7 +58,8 @@ def _run(world, cases):
         port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, overrides or {}))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in procs]
@@ -81,11 +83,10 @@ def test_sharded_world3_uneven():
 
 
 @pytest.mark.gpu
-def test_sharded_world2_two_level(monkeypatch):
-    # owners forced onto the two-level split (SSBH_BUCKETS=1 reaches the spawned ranks):
+def test_sharded_world2_two_level():
+    # owners forced onto the two-level split (plan override buckets=1 in every rank):
     # several buckets per owner, a partial last bucket, per-block seeds
-    monkeypatch.setenv("SSBH_BUCKETS", "1")
-    _run(2, [(600000, 600, 320, True), (400000, 300, 96, False)])
+    _run(2, [(600000, 600, 320, True), (400000, 300, 96, False)], dict(buckets=1))
 
 
 @pytest.mark.gpu

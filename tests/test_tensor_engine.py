@@ -30,6 +30,14 @@ def _run_plan(dev, x, n, s, k, samp, hsh, engine, **kw):
 ENGINES = pytest.mark.parametrize("engine", [1, 2], ids=["lop3", "tensor"])
 
 
+@pytest.fixture(autouse=True)
+def _tensor_engine_suite(request):
+    """This file pins engines per plan; a session that forces the LOP3 engine for every plan
+    (--ssbh-override engine=1) runs the engine-agnostic suites instead."""
+    if any(kv.replace(" ", "") == "engine=1" for kv in request.config.getoption("--ssbh-override")):
+        pytest.skip("the session forces the LOP3 engine")
+
+
 def test_default_engine_is_tensor(dev):
     plan = dev.Plan(100000, 8, 64, 2, 3)
     assert plan.engine == dev.ENGINE_TENSOR
@@ -81,7 +89,7 @@ def test_shared_seed_long_blocks_use_the_tiled_kernel(dev, oracle):
     got, _, _ = plan.run_host(x)
     plan.close()
     assert (got == want).all()
-    if not os.environ.get("SSBH_MMA_SHARED_PB"):  # the heuristic, unless forced
+    if dev.get_overrides()["shared_tiled"] < 0:  # the heuristic, unless forced
         plan = dev.Plan(1 << 20, 64, 8192, 2, 3)  # config 1: short blocks keep the GEMM kernel
         assert plan.hash_kernel in ("k_toeplitz_f4", "k_toeplitz_mma")
         plan.close()
@@ -111,34 +119,31 @@ def test_host_run_overlaps_input_copy(dev, oracle, s, k):
 
 
 def _split_possible():
-    """The split runs on FP4 operands in the tiled kernel (dev knobs can turn either off)."""
-    return (os.environ.get("SSBH_MMA_FP4", "1") != "0"
-            and os.environ.get("SSBH_MMA_SHARED_PB", "") != "0")
+    """The split runs on the tensor engine unless the session forces the LOP3 engine or the
+    GEMM kernel for shared seeds (--ssbh-override)."""
+    import paper_2308_02856_b200 as P
+
+    o = P.get_overrides()
+    return o["engine"] != P.ENGINE_LOP3 and o["shared_tiled"] != 0
 
 
 @pytest.mark.parametrize("levels,budget_mb", [(1, None), (1, 1), (2, 1), (3, None), (4, 1),
                                               (None, None)],
                          ids=["L1", "L1-batched", "L2-batched", "L3", "L4-batched", "auto"])
-def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, budget_mb, monkeypatch):
+def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, budget_mb, ovr):
     """3-for-4 split (toeplitz_split.cu): many small squares vs the oracle (leaf buffers in
     batches of blocks when the budget is small, the last batch partial), and BASELINE-sized
     squares with a remainder vs the LOP3 engine on the same input."""
     import torch
 
-    if levels is None:
-        monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)  # levels by the cost model
-    else:
-        monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
-    if budget_mb is None:
-        monkeypatch.delenv("SSBH_MMA_SPLIT_MB", raising=False)
-    else:
-        monkeypatch.setenv("SSBH_MMA_SPLIT_MB", str(budget_mb))
+    # levels None: the cost model; budget None: the default leaf budget
+    ovr(split_levels=-1 if levels is None else levels, split_budget_mb=budget_mb or 0)
     n, s, k = (1 << 22) + 4321, 5, 4096  # T = 204 squares of 4096 per block + remainder
     x = oracle.make_input(21, 0.5, n)
     want, wnj = oracle.extract(x, n, s, 5, 6, 0, k)
     plan = dev.Plan(n, s, k, 5, 6)
     # the cost model splits only squares of >= ~2^18 (window ramp vs saved MACs)
-    if _split_possible() and os.environ.get("SSBH_HASH_ENGINE") != "lop3":
+    if _split_possible() and _split_possible():
         assert plan.hash_kernel.endswith("+split") == (levels is not None)
     got, nj, _ = plan.run_host(x)
     plan.close()
@@ -161,14 +166,13 @@ def test_split_hash_vs_oracle_and_lop3(dev, oracle, levels, budget_mb, monkeypat
 
 
 @pytest.mark.parametrize("levels,leaf", [(5, "gemm"), (6, "gemm"), (2, "pb")])
-def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, monkeypatch):
+def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, ovr):
     """Shared-seed leaves run as one GEMM per leaf matrix (k_toeplitz_f4, 128-block groups,
-    512-bit padded leaf inputs) by default, or on the tiled kernel (SSBH_MMA_SPLIT_LEAF=pb):
+    512-bit padded leaf inputs) by default, or on the tiled kernel (split_tiled_leaves=1):
     deep splits and both leaf kernels vs the LOP3 engine on T = 2 squares of 2^19 + remainder."""
     import torch
 
-    monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
-    monkeypatch.setenv("SSBH_MMA_SPLIT_LEAF", leaf)
+    ovr(split_levels=levels, split_tiled_leaves=int(leaf == "pb"))
     n, s, k = (1 << 24) + 4097, 16, 1 << 19
     x = oracle.make_input(25, 0.5, n)
     d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
@@ -176,7 +180,7 @@ def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, monkeypat
     for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
         plan = dev.Plan(n, s, k, 13, 14, engine=engine)
         if engine == dev.ENGINE_TENSOR and _split_possible():
-            want = "k_toeplitz_f4+split" if leaf == "gemm" else "k_toeplitz_mma_pb<f4>+split"
+            want = "k_toeplitz_f4+split" if leaf == "gemm" else "k_toeplitz_mma_pb+split"
             assert plan.hash_kernel == want
             assert plan.split_geometry[:2] == (levels, 2)
         d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
@@ -189,26 +193,19 @@ def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, monkeypat
 
 @pytest.mark.parametrize("levels,budget_mb", [(1, None), (3, 2), (4, None), (None, None)],
                          ids=["L1", "L3-batched", "L4", "auto"])
-def test_split_per_block_seeds(dev, oracle, levels, budget_mb, monkeypatch):
+def test_split_per_block_seeds(dev, oracle, levels, budget_mb, ovr):
     """The split with per-block seeds (config-4 style): leaf seeds are XORs of windows of each
     block's own seed region, made per leaf batch. Small squares vs the oracle; a config-4-like
     shape (k = 3 * 2^17, T = 2 squares + a remainder) vs the LOP3 engine."""
     import torch
 
-    if levels is None:
-        monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)
-    else:
-        monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
-    if budget_mb is None:
-        monkeypatch.delenv("SSBH_MMA_SPLIT_MB", raising=False)
-    else:
-        monkeypatch.setenv("SSBH_MMA_SPLIT_MB", str(budget_mb))
+    ovr(split_levels=-1 if levels is None else levels, split_budget_mb=budget_mb or 0)
     if levels is not None:
         n, s, k = (1 << 21) + 999, 7, 4096
         x = oracle.make_input(23, 0.5, n)
         want, wnj = oracle.extract(x, n, s, 9, 10, 1, k)
         plan = dev.Plan(n, s, k, 9, 10, per_block=True)
-        if _split_possible() and os.environ.get("SSBH_HASH_ENGINE") != "lop3":
+        if _split_possible() and _split_possible():
             assert plan.hash_kernel.endswith("+split")
             assert plan.split_geometry[0] == levels
         got, nj, _ = plan.run_host(x)
@@ -221,7 +218,7 @@ def test_split_per_block_seeds(dev, oracle, levels, budget_mb, monkeypatch):
     keys = []
     for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
         plan = dev.Plan(n, s, k, 11, 12, per_block=True, engine=engine)
-        if engine == dev.ENGINE_TENSOR and os.environ.get("SSBH_MMA_FP4", "1") != "0":
+        if engine == dev.ENGINE_TENSOR:
             assert plan.hash_kernel.endswith("+split")
         d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
         plan.run_device(d_in.data_ptr(), d_key.data_ptr())
@@ -234,19 +231,16 @@ def test_split_per_block_seeds(dev, oracle, levels, budget_mb, monkeypatch):
 @pytest.mark.parametrize("name,levels", [("split_smoke", None), ("split_t2", None),
                                          ("split_deep", 7), ("split_deep", 3),
                                          ("split_perblock", None), ("split_perblock", 2)])
-def test_split_reference_digests(dev, oracle, golden, name, levels, monkeypatch):
+def test_split_reference_digests(dev, oracle, golden, name, levels, ovr):
     """The headline path — the 3-for-4 split (csrc/toeplitz_split.cu: leaf GEMMs / tiled
     leaves, remainder, level combine) — against digests made by running the compiled
     reference (toeplitz.cpp:34-52 hashing every block directly; gen_golden.py --split)."""
-    if levels is None:
-        monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)
-    else:
-        monkeypatch.setenv("SSBH_MMA_SPLIT", str(levels))
+    ovr(split_levels=-1 if levels is None else levels)
     c = golden["extract"][name]
     n, s, k = c["n"], c["s"], c["k"]
     x = oracle.make_input(c["seed_in"], c["p"], n)
     plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=bool(c["per_block"]))
-    if _split_possible() and os.environ.get("SSBH_HASH_ENGINE") != "lop3":
+    if _split_possible() and _split_possible():
         assert plan.hash_kernel.endswith("+split"), plan.hash_kernel
         if levels is not None:
             assert plan.split_geometry[0] == levels
@@ -257,13 +251,12 @@ def test_split_reference_digests(dev, oracle, golden, name, levels, monkeypatch)
     assert f"{oracle.fnv(key):016x}" == c["key_fnv"]
 
 
-def test_split_budget_few_long_blocks(dev, monkeypatch):
+def test_split_budget_few_long_blocks(dev, ovr):
     """Few very long shared-seed blocks: GEMM leaf groups are padded to 128 blocks, so the
-    leaf budget (SSBH_MMA_SPLIT_MB, default 8 GB) is charged for the padded batch and the plan
+    leaf budget (split_budget_mb, default 8 GB) is charged for the padded batch and the plan
     falls back to tiled leaves / fewer levels instead of allocating ~390 GB (s = 4,
     n = 2^32, k = 2^19: T = 2048 squares per block)."""
-    monkeypatch.delenv("SSBH_MMA_SPLIT", raising=False)
-    monkeypatch.delenv("SSBH_MMA_SPLIT_MB", raising=False)
+    ovr(split_levels=-1, split_budget_mb=0)
     n = 1 << 32
     plan = dev.Plan(n, 4, 1 << 19, 2, 3)
     kernel, geom, nbytes = plan.hash_kernel, plan.split_geometry, plan.device_bytes
@@ -273,9 +266,9 @@ def test_split_budget_few_long_blocks(dev, monkeypatch):
     assert kernel.endswith("+split"), kernel
 
 
-def test_split_disabled_by_env(dev, monkeypatch):
-    """SSBH_MMA_SPLIT=0 keeps long shared blocks on the direct tiled kernel."""
-    monkeypatch.setenv("SSBH_MMA_SPLIT", "0")
+def test_split_disabled_by_override(dev, ovr):
+    """split_levels = 0 keeps long shared blocks on the direct tiled kernel."""
+    ovr(split_levels=0)
     plan = dev.Plan((1 << 22) + 4321, 5, 4096, 5, 6)
     assert not plan.hash_kernel.endswith("+split")
     plan.close()

@@ -20,5 +20,3 @@ for mode, iters in ((0, 20000), (0, 200000), (2, 200000), (3, 200000), (1, 1000)
     print(json.dumps({"mode": mode, "iters": iters, "status": st, "ms": round(ms.value, 2),
                       "T_mac_s": round(r.value / 1e12, 1), "mismatches": bad.value,
                       "acc_sample": val}), flush=True)
-i8, _ = P.measure_mma_i8_peak(200000, 0)
-print(json.dumps({"i8_T_mac_s": round(i8 / 1e12, 1)}))
