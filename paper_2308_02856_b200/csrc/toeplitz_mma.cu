@@ -178,10 +178,14 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
 // then two producer sets alternating stages as in k_toeplitz_mma.
 constexpr int kF4StageK = 512;                    // input positions per stage (8 MMAs, K = 64)
 constexpr int kF4GUnits = kN + 3 + 384 + 1;       // 643 Hankel units per stage
-constexpr int kF4YBytes = kM * kF4StageK / 2;     // 32768
+// A operand (the blocks' y bits as E2M1 nibbles) in TMEM: 64 columns per stage (128 lanes = block
+// rows, column 4q + w = chunk q word w; nibble i of a column = K element 8c + i, probed by
+// k_f4_tmem_a_probe), a ring of kF4Stages next to the accumulator (columns 0..255) and the scale
+// factors (256..287). B (Hankel units) stays in shared memory.
+constexpr uint32_t kF4ACol0 = 320;                // A ring: columns 320..511
 constexpr int kF4GBytes = ((kF4GUnits * 16 + 127) / 128) * 128;  // 10368
-constexpr int kF4Slot = kF4YBytes + kF4GBytes;
-constexpr int kF4Stages = 4;
+constexpr int kF4Slot = kF4GBytes;                // shared memory per stage: B only
+constexpr int kF4Stages = 3;                      // = TMEM A stages (3 x 64 columns)
 constexpr int kF4Pre = 2;                         // cp.async prefetch depth per set
 constexpr int kF4RawY = kF4Pre * kM * 64;         // per set
 constexpr int kF4RawS = 4 * kF4Pre * 128;         // per set
@@ -209,6 +213,19 @@ __device__ __forceinline__ void mma_f4n(uint32_t d_tmem, uint64_t a, uint64_t b,
         "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n"
         "}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(sf)
+        : "memory");
+}
+
+// A operand from TMEM (a_tmem: lane = row, 8 columns per K = 64).
+__device__ __forceinline__ void mma_f4_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                          uint32_t sf, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%5], p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(kF4Idesc), "r"(accum), "r"(sf)
         : "memory");
 }
 
@@ -342,7 +359,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     } else if (warp == kMmaW) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
-        const uint32_t base_y = smem_u32(slots), base_g = base_y + kF4YBytes;
+        const uint32_t base_g = smem_u32(slots);
         for (uint32_t item = blockIdx.x;; item += gridDim.x) {
             Item d;
             if (!decode(a, item, d)) break;
@@ -363,14 +380,13 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     mbar_wait_sleep(&full[slot], (g / kS) & 1);
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t ya = base_y + slot * kF4Slot;
                         const uint32_t ga = base_g + slot * kF4Slot;
+                        const uint32_t at = tmem + kF4ACol0 + 64u * slot;
 #pragma unroll
-                        for (int m = 0; m < 8; ++m) {
+                        for (int m = 0; m < 8; ++m) {  // MMA m: chunks 2m, 2m+1 = columns 8m..
                             const uint32_t unit = 2u * (m & 1) + 128u * (m >> 1);
-                            mma_f4(tmem, sdesc(ya + 256u * m, 128, 2048),
-                                   sdesc(ga + 16u * unit, 16, 128), tmem + kF4SfCol,
-                                   ((s - s0) | (uint32_t)m) != 0);
+                            mma_f4_ts(tmem, at + 8u * m, sdesc(ga + 16u * unit, 16, 128),
+                                      tmem + kF4SfCol, ((s - s0) | (uint32_t)m) != 0);
                         }
                         mma_commit(&empty[slot]);
                         if (s + 1 == s1) mma_commit(&tfull[0]);
@@ -382,21 +398,32 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     } else if (((warp - kProd0) & 7) < 4) {
         // ---------------------------------------------------------------- A producers
         const uint32_t set = (warp - kProd0) >> 3;
-        const uint32_t jl = 32u * ((warp - kProd0) & 3) + lane;
-        const uint32_t row_off = (jl & 7) * 16 + (jl >> 3) * 2048;
-        // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0
+        // TMEM lane = block row: a warp reaches the 32 lanes of its sub-partition (warp % 4)
+        const uint32_t jl = 32u * (warp & 3) + lane;
+        const uint32_t lane_addr = (32u * (warp & 3)) << 16;
+        // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0; chunk
+        // q = 4 gg + kc, word w -> column 4 q + w of the stage
         auto expand = [&](const uint4 (&x)[4], uint32_t slot) {
-            uint8_t* ys = slots + (size_t)slot * kF4Slot + row_off;
+            const uint32_t ta = tmem + lane_addr + kF4ACol0 + 64u * slot;
 #pragma unroll
-            for (int gg = 0; gg < 4; ++gg) {
+            for (int h = 0; h < 2; ++h) {  // columns 32h .. 32h + 31: chunks 8h .. 8h + 7
+                uint32_t v[32];
 #pragma unroll
-                for (int kc = 0; kc < 4; ++kc) {
-                    auto f = [&](uint32_t v) { return (kc ? v >> (kc - 1) : v << 1) & M2; };
-                    *reinterpret_cast<uint4*>(ys + (4 * gg + kc) * 128) =
-                        make_uint4(f(x[gg].x), f(x[gg].y), f(x[gg].z), f(x[gg].w));
+                for (int g2 = 0; g2 < 2; ++g2) {
+                    const uint4 xg = x[2 * h + g2];
+#pragma unroll
+                    for (int kc = 0; kc < 4; ++kc) {
+                        auto f = [&](uint32_t u) { return (kc ? u >> (kc - 1) : u << 1) & M2; };
+                        v[16 * g2 + 4 * kc + 0] = f(xg.x);
+                        v[16 * g2 + 4 * kc + 1] = f(xg.y);
+                        v[16 * g2 + 4 * kc + 2] = f(xg.z);
+                        v[16 * g2 + 4 * kc + 3] = f(xg.w);
+                    }
                 }
+                SSBH_TMEM_ST32(ta + 32u * h, v);
             }
-            fence_proxy_async_smem();
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
         };
@@ -450,7 +477,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
-            uint8_t* gs = slots + (size_t)slot * kF4Slot + kF4YBytes;
+            uint8_t* gs = slots + (size_t)slot * kF4Slot;
             // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
             // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position. Unit u + 128 starts 4
             // words later with the same shift, so its first word is this unit's last: 4 shared

@@ -1,5 +1,5 @@
 """Quick per-phase timing of the fused path on one GPU (development aid, not the bench).
-Prints one compact JSON line per (config, rep); SSBH_HASH_WIN selects the hash window mode."""
+Prints one compact JSON line per (config, rep)."""
 import argparse
 import json
 import os
@@ -19,11 +19,12 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "lop3", "tensor"])
     ap.add_argument("--per-block", action="store_true", help="force per-block seeds")
     args = ap.parse_args()
-    tag = os.environ.get("SSBH_HASH_WIN", "default") + ("/nograph" if os.environ.get("SSBH_NO_GRAPH") == "1" else "/graph")
+    tag = os.environ.get("SSBH_CUDA_LIB", "in-tree")
     peak, _ = P.measure_lop3_peak(20000)
     print(json.dumps({"win": tag, "lop3_peak_T": round(peak / 1e12, 3)}), flush=True)
     for cid in [int(c) for c in args.configs.split(",")]:
         c = dict(P.CONFIGS[cid])
+
         if args.per_block:
             c["per_block"] = True
         n, s, k = c["n"], c["s"], c["k"]
