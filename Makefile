@@ -11,7 +11,7 @@ CSRC     := $(PKG)/csrc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclude
 CU_SRCS  := $(CSRC)/prf.cu $(CSRC)/sampler.cu $(CSRC)/toeplitz.cu $(CSRC)/toeplitz_mma.cu $(CSRC)/toeplitz_split.cu $(CSRC)/abi.cu $(CSRC)/diag.cu $(CSRC)/rounds.cu
-CU_HDRS  := $(CSRC)/common.cuh $(CSRC)/ptx.cuh $(CSRC)/internal.h include/ssbh_cuda.h
+CU_HDRS  := $(CSRC)/common.cuh $(CSRC)/ptx.cuh $(CSRC)/internal.h $(CSRC)/split_tree.cuh include/ssbh_cuda.h
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HOST_SRCS:= $(CSRC)/host/ssbh_api.cpp $(CSRC)/host/ssbh_pipeline.cpp
 HDRS_API := $(wildcard include/ssbh/*.hpp)

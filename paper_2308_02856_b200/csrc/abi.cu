@@ -661,7 +661,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         if (pl->split) {
             const uint32_t lw = (uint32_t)(pl->sg.sL / 32);
             if (pl->sg.gemm) {
-                pl->mmv = make_mma_geom((uint32_t)pl->sg.nvirt, lw, pl->sg.sL, pl->device);
+                pl->mmv = make_leaf_geom((uint32_t)pl->sg.nvirt, lw, pl->device);
                 const uint64_t tk = (uint64_t)pl->sg.T * k;  // remainder: one GEMM as well
                 pl->mmr = make_mma_geom(nown, pl->kw, mean_nj > tk ? mean_nj - tk : 1, pl->device);
             }
@@ -1015,13 +1015,28 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
         }
         for (uint32_t jj0 = 0; jj0 < pl->nown; jj0 += g.batch) {  // leaf batches
             const uint32_t cnt = std::min<uint32_t>(g.batch, pl->nown - jj0);
-            launch_split_batch(pl->ybuf.as<uint32_t>(), pl->sbuf.as<uint32_t>(), pl->sbuf_words,
-                               lay, pl->nown, g, jj0, pl->vy.as<uint32_t>(),
-                               pl->vs.as<uint32_t>(), st);
-            launches += g.per_block ? 1 : 0;
+            if (!g.gemm) {  // tiled leaves: materialised leaf inputs (+ per-block leaf seeds)
+                launch_split_batch(pl->ybuf.as<uint32_t>(), pl->sbuf.as<uint32_t>(),
+                                   pl->sbuf_words, lay, pl->nown, g, jj0, pl->vy.as<uint32_t>(),
+                                   pl->vs.as<uint32_t>(), st);
+                launches += g.per_block ? 2 : 1;
+            }
             if (g.gemm) {
+                // leaf mode: the GEMM builds each M tile's leaf inputs in shared memory from the
+                // original reversed blocks (no k_split_inputs, no leaf-input buffer)
                 MmaHashArgs v{};
                 v.ybuf = pl->vy.as<uint32_t>();
+                v.leaf = 1;
+                v.src.ybuf = pl->ybuf.as<uint32_t>();
+                v.src.lay = lay;
+                v.src.k = g.k;
+                v.src.L = g.L;
+                v.src.leaves = g.leaves;
+                v.src.gpad = g.gpad;
+                v.src.batch = g.batch;
+                v.src.jj0 = jj0;
+                v.src.nown = pl->nown;
+                v.src.kpw = (uint32_t)(g.sL / 32 / pl->mmv.ksplit);
                 v.sbuf = pl->vs.as<uint32_t>();
                 v.out = pl->vout.as<uint32_t>();
                 v.out_stride = g.sL / 32;

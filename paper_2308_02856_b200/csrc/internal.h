@@ -205,6 +205,18 @@ struct MmaGeom {
     uint32_t grid;     // persistent CTAs (one per SM)
     uint64_t items;    // mtiles * ntiles * ksplit
 };
+// Leaf mode of k_toeplitz_f4 (the 3-for-4 split's shared-seed leaves): a CTA keeps one M tile's
+// leaf inputs (128 virtual blocks x kpw words) in shared memory for all N tiles, building them
+// from the original reversed blocks as XORs of the leaf's input pieces (no materialised leaf
+// inputs). Virtual block v = group * gpad + jl (group = segment t * 3^L + path).
+struct LeafSrc {
+    const uint32_t* ybuf;    // original reversed blocks
+    Layout lay;              // their layout (yoff, ypad)
+    unsigned long long k;    // square size (bits)
+    uint32_t L, leaves, gpad, batch, jj0, nown;
+    uint32_t kpw;            // leaf input words per K part (held in shared memory)
+};
+
 struct MmaHashArgs {
     const uint32_t* ybuf;
     const uint32_t* sbuf;    // shared seed, pre-shifted by one bit (see launch_seeds)
@@ -217,6 +229,9 @@ struct MmaHashArgs {
     uint64_t items;
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
     uint32_t stage_bits;     // input positions per pipeline stage (set by launch_hash_mma)
+    uint32_t leaf;           // 1: leaf mode (src below; items walked N tile innermost per
+                             // (M tile, K part); ksplit = K parts)
+    LeafSrc src;
 };
 // Per-block seeds on the tensor cores: work item = (owned block, window of 256 row tiles of
 // 128 rows); see toeplitz_mma.cu.
@@ -277,6 +292,8 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
                               uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
+// Leaf mode (the split's shared-seed leaf GEMM): K parts of <= 8192 positions, N tiles innermost.
+MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device);
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
 void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st);
 

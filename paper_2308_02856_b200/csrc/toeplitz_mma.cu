@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ptx.cuh"
+#include "split_tree.cuh"
 
 namespace ssbh_impl {
 using namespace ssbh_dev;
@@ -113,6 +114,18 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
     return true;
 }
 
+// A CTA's item sequence: items blockIdx.x, +grid, ...; in leaf mode super-items (M tile, K part)
+// blockIdx.x, +grid, ... with their N tiles in order (the M tile's leaf inputs stay in shared
+// memory across them).
+__device__ __forceinline__ uint32_t first_item(const MmaHashArgs& a) {
+    return a.leaf ? blockIdx.x * a.ntiles : blockIdx.x;
+}
+__device__ __forceinline__ uint32_t next_item(const MmaHashArgs& a, uint32_t item) {
+    if (!a.leaf) return item + gridDim.x;
+    const uint32_t nt = item % a.ntiles;
+    return nt + 1 < a.ntiles ? item + 1 : item - nt + gridDim.x * a.ntiles;
+}
+
 // Walks (item, stage) pairs of this CTA in order; used by the producers twice (consume and
 // prefetch kPre stages ahead).
 struct StageIt {
@@ -121,14 +134,14 @@ struct StageIt {
     Item d;
     bool valid;
     __device__ void start(const MmaHashArgs& a) {
-        item = blockIdx.x;
+        item = first_item(a);
         s = 0;
         valid = decode(a, item, d);
         skip_empty(a);
     }
     __device__ void skip_empty(const MmaHashArgs& a) {
         while (valid && s >= d.nst) {
-            item += gridDim.x;
+            item = next_item(a, item);
             s = 0;
             valid = decode(a, item, d);
         }
@@ -257,6 +270,83 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
     for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
 }
 
+// Leaf mode (the split's shared-seed leaves): kLeafKpw words of each of the 128 virtual blocks'
+// leaf input per K part live in shared memory for all N tiles of the M tile.
+constexpr uint32_t kLeafKpw = 256;                     // 8192 positions per K part
+constexpr uint32_t kLeafStride = kLeafKpw + 4;
+constexpr size_t kLeafSmem = (size_t)kM * kLeafStride * 4 + (1u << kMaxL) * 8 + 16;
+
+// Builds the M tile's leaf inputs for K part d (words [d.st0 * 16, + kpw) of each leaf) into
+// lraw: row jl = XOR over the leaf's input pieces of the original block's reversed input
+// (the k_split_inputs arithmetic, toeplitz_split.cu), zero past the block's padded length and
+// for padding rows. Called by the 8 A producer warps together (named barrier 1, 256 threads).
+__device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, uint32_t aw,
+                                           uint32_t lane, uint32_t* lraw,
+                                           unsigned long long* loff, int* lnoff) {
+    const LeafSrc& q = a.src;
+    const uint64_t v0 = (uint64_t)d.mt * kM;  // first virtual block (one group per M tile)
+    const uint32_t grp = (uint32_t)(v0 / q.gpad), jl0 = (uint32_t)(v0 % q.gpad);
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // every expansion of the last tile done
+    if (aw == 0 && lane == 0) {
+        uint64_t off[1 << kMaxL];
+        const uint32_t t = grp / q.leaves, path = grp % q.leaves;
+        const int n = leaf_offsets(path, q.L, q.k, (uint64_t)t * q.k, false, off);
+        for (int e = 0; e < n; ++e) loff[e] = off[e] / 32;
+        *lnoff = n;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int n = *lnoff;
+    const uint64_t w0 = (uint64_t)d.st0 * 16;  // K part start (words, a multiple of 16)
+    // 16-B loads with many L2 reads outstanding (the build is latency-bound otherwise): per
+    // lane 2 rows x 2 vectors per piece, pieces unrolled by 2; 8 warps x 16 rows
+    const uint32_t nvec = q.kpw / 4;  // uint4 per row (>= 4: kpw is a multiple of 16 words)
+    constexpr int RB = 2;
+    for (uint32_t r0 = aw * 16; r0 < aw * 16 + 16; r0 += RB) {
+        const uint4* y[RB];
+        uint64_t yp4[RB];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            const uint32_t jlg = jl0 + r0 + rr, jj = q.jj0 + jlg;
+            const bool live = jlg < q.batch && jj < q.nown;
+            y[rr] = reinterpret_cast<const uint4*>(live ? q.ybuf + q.lay.yoff[jj] : q.ybuf);
+            yp4[rr] = live ? q.lay.ypad[jj] / 4 : 0;  // ypad is a multiple of 32 words
+        }
+        uint4 acc[RB][2];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[rr][h] = make_uint4(0, 0, 0, 0);
+#pragma unroll 2
+        for (int e = 0; e < n; ++e) {
+            const uint64_t base4 = (loff[e] + w0) / 4;
+#pragma unroll
+            for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t vl = lane + 32u * h;
+                    const uint64_t qv = base4 + vl;
+                    if (vl < nvec && qv < yp4[rr]) {
+                        const uint4 v = __ldg(y[rr] + qv);
+                        acc[rr][h].x ^= v.x;
+                        acc[rr][h].y ^= v.y;
+                        acc[rr][h].z ^= v.z;
+                        acc[rr][h].w ^= v.w;
+                    }
+                }
+        }
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t vl = lane + 32u * h;
+                if (vl < nvec)
+                    *reinterpret_cast<uint4*>(lraw + (size_t)(r0 + rr) * kLeafStride + 4u * vl) =
+                        acc[rr][h];
+            }
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
 // Warp roles: 8 epilogue warps (two per TMEM sub-partition, half of the 256 accumulator
 // columns each: a shorter drain of the single accumulator between work items; 1.4 % faster
 // than 4 in round 1), 1 MMA warp, then two producer sets of 4 A + 4 B warps that fill
@@ -279,6 +369,12 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     uint64_t* tfull = empty + kS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // leaf mode: the M tile's leaf inputs, row stride kLeafStride words (+4: conflict-free
+    // 16-B reads of 8 consecutive rows), and the leaf's input piece offsets (words)
+    uint32_t* lraw = reinterpret_cast<uint32_t*>(smem + f4_smem(kSets));
+    unsigned long long* loff =
+        reinterpret_cast<unsigned long long*>(lraw + (size_t)kM * kLeafStride);
+    int* lnoff = reinterpret_cast<int*>(loff + (1 << kMaxL));
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -315,7 +411,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- epilogue
         const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;  // TMEM sub-partition, columns
         uint32_t t = 0;  // accumulation rounds consumed
-        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
+        for (uint32_t item = first_item(a);; item = next_item(a, item)) {
             Item d;
             if (!decode(a, item, d)) break;
             const uint32_t rounds = d.nst ? (d.nst + kF4MaxStages - 1) / kF4MaxStages : 1;
@@ -325,7 +421,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
                 mbar_wait_sleep(&tfull[0], t & 1);
                 tc_fence_after();
+#ifndef SSBH_EXP_NODRAIN
                 if (d.nst) {
+#else
+                if (false) {
+#endif
 #pragma unroll 1
                     for (int q = 0; q < kQW; ++q) {
                         uint32_t v[32];
@@ -360,7 +460,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
         const uint32_t base_g = smem_u32(slots);
-        for (uint32_t item = blockIdx.x;; item += gridDim.x) {
+        for (uint32_t item = first_item(a);; item = next_item(a, item)) {
             Item d;
             if (!decode(a, item, d)) break;
             if (d.nst == 0) {
@@ -430,8 +530,32 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         StageIt cur, pre;
         cur.start(a);
         cur.advance(a, set);
+        if (a.leaf) {
+            // both A sets build the super-item's leaf inputs together (named barrier 1 over
+            // the 8 A warps), then expand stages from shared memory
+            const uint32_t aw = set * 4 + ((warp - kProd0) & 3);  // 0..7
+            uint32_t built = 0xFFFFFFFFu;
+            const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
+            for (uint32_t g = set; cur.valid; g += kSets, cur.advance(a, kSets)) {
+                const uint32_t sup = cur.item / a.ntiles;
+                if (sup != built) {
+                    leaf_build(a, cur.d, aw, lane, lraw, loff, lnoff);
+                    built = sup;
+                }
+                uint4 x[4];
+                const uint32_t* src = lrow + 16u * cur.s;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) x[h] = *reinterpret_cast<const uint4*>(src + 4 * h);
+                const uint32_t slot = g % kS;
+                if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+                expand(x, slot);
+            }
+        } else {
         pre = cur;
         uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
+#ifdef SSBH_EXP_NOYLOAD
+        pre.valid = false;
+#endif
         for (int i = 0; i < kF4Pre; ++i) {
             y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
             cp_async_commit();
@@ -452,6 +576,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             pre.advance(a, kSets);
         }
         cp_async_wait<0>();
+        }
     } else {
         // ---------------------------------------------------------------- B producers
         const uint32_t set = (warp - kProd0) >> 3;
@@ -867,6 +992,18 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     return g;
 }
 
+MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device) {
+    MmaGeom g{};
+    g.mtiles = mma_mtiles(nvirt);
+    g.ntiles = (lw + kN / 32 - 1) / (kN / 32);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    g.grid = sms;
+    g.ksplit = (lw + kLeafKpw - 1) / kLeafKpw;  // K parts held in shared memory one at a time
+    g.items = (uint64_t)g.mtiles * g.ksplit * g.ntiles;
+    return g;
+}
+
 PbGeom make_pb_geom(uint32_t nown, uint32_t kw, int device, uint64_t mean_bits) {
     PbGeom g{};
     g.ntiles = (kw + 3) / 4;  // 128-row tiles
@@ -913,9 +1050,14 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
     MmaHashArgs a = a0;
     a.stage_bits = kF4StageK;
-    cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)f4_smem(kSets));
-    k_toeplitz_f4<<<grid, kF4Threads, f4_smem(kSets), st>>>(a);
+    const size_t smem = f4_smem(kSets) + (a.leaf ? kLeafSmem : 0);
+    cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a.leaf) {  // super-items (M tile, K part) of N tiles; grid = one wave of CTAs at most
+        const uint64_t supers = g.items / a.ntiles;
+        k_toeplitz_f4<<<(unsigned)std::min<uint64_t>(g.grid, supers), kF4Threads, smem, st>>>(a);
+        return;
+    }
+    k_toeplitz_f4<<<grid, kF4Threads, smem, st>>>(a);
 }
 
 }  // namespace ssbh_impl

@@ -26,47 +26,11 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "split_tree.cuh"
 
 namespace ssbh_impl {
 
 namespace {
-
-constexpr int kMaxL = 7;
-
-// Offsets (bits) whose windows / pieces a leaf XORs. seed: S windows; input: y pieces.
-__device__ __forceinline__ int leaf_offsets(uint32_t path, uint32_t L, uint64_t k, uint64_t base,
-                                            bool seed, uint64_t* off) {
-    int n = 1;
-    off[0] = base;
-    uint64_t m = k;
-    for (uint32_t l = 0; l < L; ++l) {
-        m >>= 1;
-        // digit l of the path (most significant = level 0)
-        uint32_t p = path;
-        for (uint32_t q = l + 1; q < L; ++q) p /= 3;
-        const uint32_t d = p % 3;  // 0 = P, 1 = Q, 2 = R
-        const int n0 = n;
-        if (seed) {
-            if (d == 0) {
-                for (int e = 0; e < n0; ++e) off[e] += m;                       // B1
-            } else if (d == 1) {
-                for (int e = 0; e < n0; ++e) off[n0 + e] = off[e] + m;          // B0 ^ B1
-                n = 2 * n0;
-            } else {
-                for (int e = 0; e < n0; ++e) { off[n0 + e] = off[e] + m; off[e] += 2 * m; }  // B2 ^ B1
-                n = 2 * n0;
-            }
-        } else {
-            if (d == 0) {
-                for (int e = 0; e < n0; ++e) off[n0 + e] = off[e] + m;          // x0 ^ x1
-                n = 2 * n0;
-            } else if (d == 2) {
-                for (int e = 0; e < n0; ++e) off[e] += m;                       // x1
-            }                                                                   // Q: x0
-        }
-    }
-    return n;
-}
 
 // Leaf seed regions (pre-shifted seed S': an XOR of word-aligned windows stays pre-shifted).
 // Shared seed: one region per (segment, path), r = blockIdx.y, source sbuf[0, sbuf_words).
