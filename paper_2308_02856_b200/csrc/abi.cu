@@ -717,7 +717,8 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         const SplitGeom& g = pl->sg;
         e = alloc(pl->vs,
                   ((g.per_block ? g.nvirt : (size_t)g.T * g.leaves) * g.seed_words + 256) * 4);
-        if (!e) e = alloc(pl->vy, (size_t)g.nvirt * g.vlw * 4 + 16);
+        // leaf inputs: materialised only for tiled leaves (the leaf GEMM builds its own)
+        if (!e && !g.gemm) e = alloc(pl->vy, (size_t)g.nvirt * g.vlw * 4 + 16);
         if (!e) e = alloc(pl->vout, (size_t)g.nvirt * (g.sL / 8) + 16);
         if (!e) e = alloc(pl->vrem, (size_t)nown * pl->kw * 4 + 16);
         if (!e) e = pl->vlay.alloc((uint32_t)g.nvirt);

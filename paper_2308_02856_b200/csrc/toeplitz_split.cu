@@ -140,52 +140,92 @@ __global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vl
     }
 }
 
-// Hierarchical combine, one level per launch: the nodes of level l - 1 from their children at
-// level l (child size m = k >> l bits, cw = m / 32 words): node = [P ^ Q | P ^ R]. Node
-// (t, p, jl) of level l sits at ((t * 3^l + p) * gpad + jl) * (k >> l) / 32. Reads 2 words per
-// word written, (3/2)^l k bits per square at level l — instead of the flat combine's 2^L reads
-// per key word.
-__global__ void k_split_level(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                              uint32_t l, uint32_t count, SplitGeom g) {
-    const uint64_t cw = (g.k >> l) / 32, pw = 2 * cw;
-    uint32_t n_par = 1;  // 3^(l - 1)
-    for (uint32_t q = 1; q < l; ++q) n_par *= 3;
-    const uint64_t per_t = (uint64_t)n_par * count * pw;
-    const uint64_t total = (uint64_t)g.T * per_t;
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t w = e % pw;
-        const uint64_t r = e / pw;  // (t * n_par + p) * count + jl
-        const uint32_t jl = (uint32_t)(r % count);
-        const uint64_t tp = r / count;  // t * n_par + p
-        const bool hi = w >= cw;
-        const uint64_t wl = hi ? w - cw : w;
-        const uint64_t child0 = tp * 3;  // t * 3^l + 3 p
-        const uint32_t p0 = src[((child0 + 0) * g.gpad + jl) * cw + wl];
-        const uint32_t px = src[((child0 + (hi ? 2 : 1)) * g.gpad + jl) * cw + wl];
-        dst[(tp * g.gpad + jl) * pw + w] = p0 ^ px;
-    }
-}
-
-// Root: key word w of block jj0 + jl = remainder ^ XOR over squares t of [P ^ Q | P ^ R] from the
-// level-1 nodes (t, 0..2).
-__global__ void k_split_root(const uint32_t* __restrict__ src, const uint32_t* __restrict__ rem,
-                             uint32_t jj0, uint32_t count, uint32_t kw, SplitGeom g,
-                             uint32_t* __restrict__ out, unsigned long long out_stride) {
-    const uint64_t cw = (g.k >> 1) / 32;
-    const uint64_t total = (uint64_t)count * kw;
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t jl = (uint32_t)(e / kw), w = (uint32_t)(e % kw);
-        uint32_t acc = rem[(uint64_t)(jj0 + jl) * kw + w];
-        const bool hi = w >= cw;
-        const uint64_t wl = hi ? w - cw : w;
-        for (uint32_t t = 0; t < g.T; ++t) {
-            const uint64_t c0 = (uint64_t)t * 3;
-            acc ^= src[((c0 + 0) * g.gpad + jl) * cw + wl] ^
-                   src[((c0 + (hi ? 2 : 1)) * g.gpad + jl) * cw + wl];
+// Single-pass combine: leaves -> key. CTA (block jl, chunk c of W words of every leaf) handles,
+// per square t, the chunk of all 3^L leaves: each thread reduces depth-D subtrees (3^D leaves at
+// one word position, loaded straight into registers: 3^D independent loads in flight) to their
+// 2^D-word root, the subtree roots go to shared memory and the remaining L - D levels are
+// reduced there (node = [P ^ Q | P ^ R], ping-pong buffers). The squares' level-0 chunks and the
+// remainder are XORed and the 2^L key segments the chunk maps to are written (key word
+// s * cw + c W + j for segment s, j < W). Every leaf word is read once; no intermediate level
+// goes through HBM.
+template <int D>
+__global__ void __launch_bounds__(256) k_split_tree(const uint32_t* __restrict__ vout,
+                                                    const uint32_t* __restrict__ rem,
+                                                    uint32_t jj0, uint32_t count, uint32_t kw,
+                                                    SplitGeom g, uint32_t W,
+                                                    uint32_t* __restrict__ out,
+                                                    unsigned long long out_stride) {
+    constexpr int kSub = D == 1 ? 3 : D == 2 ? 9 : 27;  // 3^D leaves per subtree
+    constexpr int kOut = 1 << D;                         // its root's words per position
+    extern __shared__ __align__(16) uint32_t tsm[];
+    const uint64_t cw = g.sL / 32;  // leaf words
+    const uint32_t nchunks = (uint32_t)(cw / W);
+    const uint32_t jl = blockIdx.x / nchunks, c = blockIdx.x % nchunks;
+    if (jl >= count) return;
+    const uint32_t nsub = g.leaves / kSub;       // subtree roots (level L - D nodes)
+    uint32_t* buf0 = tsm;                        // nsub nodes x kOut W words
+    uint32_t* buf1 = tsm + (size_t)nsub * kOut * W;  // next level: (nsub / 3) x 2 kOut W
+    uint32_t* acc = buf1 + (size_t)(nsub / 3) * 2 * kOut * W;  // 2^L W words
+    const uint32_t outw = (1u << g.L) * W;
+    for (uint32_t i = threadIdx.x; i < outw; i += blockDim.x) acc[i] = 0;
+    const uint64_t lstride = (uint64_t)g.gpad * cw;  // next path, same block
+    for (uint32_t t = 0; t < g.T; ++t) {
+        const uint32_t* base = vout + ((uint64_t)t * g.leaves * g.gpad + jl) * cw + (uint64_t)c * W;
+        for (uint32_t it = threadIdx.x; it < nsub * W; it += blockDim.x) {
+            const uint32_t q = it / W, j = it % W;
+            uint32_t v[kSub];
+            const uint32_t* src = base + (uint64_t)q * kSub * lstride + j;
+#pragma unroll
+            for (int e = 0; e < kSub; ++e) v[e] = __ldg(src + e * lstride);
+            // levels L .. L - D + 1 in registers: n nodes of width w -> n / 3 of width 2 w
+#pragma unroll
+            for (int n = kSub, w = 1; n > 1; n /= 3, w *= 2) {
+#pragma unroll
+                for (int p = 0; p < n / 3; ++p) {
+                    uint32_t o[64];
+#pragma unroll
+                    for (int e = 0; e < w; ++e) {
+                        o[e] = v[3 * p * w + e] ^ v[(3 * p + 1) * w + e];
+                        o[w + e] = v[3 * p * w + e] ^ v[(3 * p + 2) * w + e];
+                    }
+#pragma unroll
+                    for (int e = 0; e < 2 * w; ++e) v[2 * p * w + e] = o[e];
+                }
+            }
+            uint32_t* dst = buf0 + (size_t)q * kOut * W + j;
+#pragma unroll
+            for (int e = 0; e < kOut; ++e) dst[e * W] = v[e];
         }
-        out[(unsigned long long)(jj0 + jl) * out_stride + w] = acc;
+        __syncthreads();
+        uint32_t* src = buf0;
+        uint32_t* dst = buf1;
+        uint32_t n = nsub, w = kOut * W;  // nodes and chunk width at the current level
+        while (n > 1) {
+            const uint32_t np = n / 3, pw = 2 * w;
+            for (uint32_t i = threadIdx.x; i < np * pw; i += blockDim.x) {
+                const uint32_t pnode = i / pw, e = i % pw;
+                const bool hi = e >= w;
+                const uint32_t el = hi ? e - w : e;
+                const uint32_t* ch = src + (size_t)pnode * 3 * w;
+                dst[i] = ch[el] ^ ch[(hi ? 2 : 1) * w + el];
+            }
+            __syncthreads();
+            n = np;
+            w = pw;
+            uint32_t* tmp = src;
+            src = dst;
+            dst = tmp;
+        }
+        // src: the square's level-0 chunk (2^L W words)
+        for (uint32_t i = threadIdx.x; i < outw; i += blockDim.x) acc[i] ^= src[i];
+        __syncthreads();
+    }
+    // key segments: acc[s W + j] -> key word s cw + c W + j, XOR the remainder's word
+    const uint64_t jj = (uint64_t)jj0 + jl;
+    for (uint32_t i = threadIdx.x; i < outw; i += blockDim.x) {
+        const uint32_t sgm = i / W, j = i % W;
+        const uint64_t wk = (uint64_t)sgm * cw + (uint64_t)c * W + j;
+        if (wk < kw) out[jj * out_stride + wk] = acc[i] ^ rem[jj * kw + wk];
     }
 }
 
@@ -242,11 +282,13 @@ SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t 
     // matrix-vector product (tiled kernel).
     g.gemm = !per_block && gemm_leaves;
     g.vlw = g.gemm ? (g.sL / 32 + 15) / 16 * 16 : g.sL / 32;
-    // blocks per batch within the budget, counted on what the plan allocates: leaf inputs and
-    // outputs for gpad (not batch) blocks per (t, path) group, plus the leaf seeds (per leaf
-    // for per-block seeds, per (t, path) for a shared seed)
+    // blocks per batch within the budget, counted on what the plan allocates: leaf outputs (and
+    // tiled leaves' inputs) for gpad (not batch) blocks per (t, path) group, plus the leaf seeds
+    // (per leaf for per-block seeds, per (t, path) for a shared seed)
+    // (GEMM leaves build their inputs in shared memory: no leaf-input buffer)
     const uint64_t per_blk = (uint64_t)g.T * g.leaves *
-                             (g.vlw * 4 + g.sL / 8 + (per_block ? g.seed_words * 4 : 0));
+                             ((g.gemm ? 0 : g.vlw * 4) + g.sL / 8 +
+                              (per_block ? g.seed_words * 4 : 0));
     const uint64_t fixed = per_block ? 0 : (uint64_t)g.T * g.leaves * g.seed_words * 4;
     const uint64_t avail = budget_bytes > fixed ? budget_bytes - fixed : 0;
     uint64_t b = std::max<uint64_t>(1, std::min<uint64_t>(nown, avail / per_blk));
@@ -296,23 +338,34 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
                               uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st) {
-    const uint64_t total = (uint64_t)count * kw;
-    if (!total) return 0;
-    const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
-    // level by level (a flat one-pass combine reads 2^L words per key word: round 1 config 3
-    // 2.99 -> 1.93 ms)
-    if (g.L == 1) {
-        k_split_root<<<grid, 256, 0, st>>>(d_vout, d_rem, jj0, count, kw, g, d_out, out_stride);
-        return 1;
-    }
-    uint32_t* src = d_vout;
-    uint32_t* dst = d_tmp;
-    for (uint32_t l = g.L; l >= 2; --l) {  // level l children -> level l - 1 nodes
-        k_split_level<<<grid, 256, 0, st>>>(src, dst, l, count, g);
-        std::swap(src, dst);
-    }
-    k_split_root<<<grid, 256, 0, st>>>(src, d_rem, jj0, count, kw, g, d_out, out_stride);
-    return g.L;
+    (void)d_tmp;
+    if (!count || !kw) return 0;
+    // one pass from the leaves (round 1: level by level, L launches through HBM, config 3
+    // 3.0 ms): depth-D register subtrees, chunk width W words (the largest power of two <= 32
+    // and <= the leaf whose buffers fit 48 KB of shared memory: several CTAs per SM)
+    const uint32_t D = g.L >= 3 ? 3 : g.L;
+    const uint32_t sub = D == 1 ? 3 : D == 2 ? 9 : 27, outd = 1u << D;
+    const uint64_t cw = g.sL / 32;
+    const uint32_t nsub = g.leaves / sub;
+    auto smem_of = [&](uint32_t w) {
+        return ((size_t)nsub * outd * w + (size_t)(nsub / 3) * 2 * outd * w + ((size_t)w << g.L)) * 4;
+    };
+    uint32_t W = 32;
+    while (W > 1 && (W > cw || smem_of(W) > 48 * 1024)) W /= 2;
+    const size_t smem = smem_of(W);
+    const uint64_t grid = (uint64_t)count * (cw / W);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)grid, 256, smem, st>>>(d_vout, d_rem, jj0, count, kw, g, W, d_out,
+                                                out_stride);
+    };
+    if (D == 3)
+        go(k_split_tree<3>);
+    else if (D == 2)
+        go(k_split_tree<2>);
+    else
+        go(k_split_tree<1>);
+    return 1;
 }
 
 }  // namespace ssbh_impl
