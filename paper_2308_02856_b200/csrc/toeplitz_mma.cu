@@ -470,7 +470,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 continue;
             }
             for (uint32_t s0 = 0; s0 < d.nst; s0 += kF4MaxStages, ++t) {
+#ifndef SSBH_EXP_NOTEMPTY
                 if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
+#endif
                 tc_fence_after();
                 const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
                 for (uint32_t s = s0; s < s1; ++s, ++g) {
@@ -539,7 +541,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             for (uint32_t g = set; cur.valid; g += kSets, cur.advance(a, kSets)) {
                 const uint32_t sup = cur.item / a.ntiles;
                 if (sup != built) {
+#ifndef SSBH_EXP_NOBUILD
                     leaf_build(a, cur.d, aw, lane, lraw, loff, lnoff);
+#endif
                     built = sup;
                 }
                 uint4 x[4];
@@ -607,6 +611,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position. Unit u + 128 starts 4
             // words later with the same shift, so its first word is this unit's last: 4 shared
             // loads per unit instead of 5 (the L1 data pipe is the leaf GEMM's contended resource)
+#ifndef SSBH_EXP_NOBPROD
             const uint32_t rel = rel0 + gt - 1;
             const uint32_t q0 = rel >> 5, sh = rel & 31;
             uint32_t w0 = sw[q0];
@@ -622,6 +627,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     w0 = w4;
                 }
             }
+#endif
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
