@@ -1027,6 +1027,8 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 // original reversed blocks (no k_split_inputs, no leaf-input buffer)
                 MmaHashArgs v{};
                 v.ybuf = pl->vy.as<uint32_t>();
+                // one CTA per M tile (round 2 A/B: a CTA-pair variant, cta_group::2 with M = 256
+                // and half the Hankel table per SM, measured 32.3 vs 29.3 ms at config 3)
                 v.leaf = 1;
                 v.src.ybuf = pl->ybuf.as<uint32_t>();
                 v.src.lay = lay;

@@ -272,6 +272,132 @@ __global__ void __launch_bounds__(128, 1) k_f4_tmem_a_probe(uint32_t iters, int 
     }
 }
 
+
+// CTA-pair (cta_group::2) kind::mxf4 with A from TMEM: M = 256 across the pair (each CTA's TMEM
+// lanes = its 128 rows of A and of D), N = 256 with each CTA holding 128 rows of B at the same
+// shared-memory offset, the leader issuing. mode 1: layout — A row r (global) one-hot at element
+// r % 64, B row n (global) one-hot at element n % 64; D copied to dout (256 x 256).
+// mode 2: rate — back-to-back MMAs, B in the Hankel-unit layout of the leaf GEMM's half table.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    k_f4_pair_probe(uint32_t iters, int mode, uint32_t* bad, float* dout) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+    for (uint32_t i = threadIdx.x; i < 45056 / 4; i += blockDim.x) w[i] = mode == 2 ? 0x22222222u : 0u;
+    __syncthreads();
+    if (mode == 1) {  // B: this CTA's 128 rows, row n local at bytes (n%8)*16 + (n/8)*256 + ...
+        const uint32_t nl = threadIdx.x, n = 128u * rank + nl, e = n % 64u;
+        const uint32_t byte = (nl % 8) * 16 + (nl / 8) * 256 + (e / 32) * 128 + (e % 32) / 2;
+        smem[byte] = (uint8_t)((e & 1) ? 0x20 : 0x02);
+    }
+    const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tslot;
+    {
+        const uint32_t v = 0x7F7F7F7Fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+            "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                tmem + ((32u * warp) << 16) + 256u),
+            "r"(v)
+            : "memory");
+        const uint32_t r = 128u * rank + 32u * warp + lane, e = r % 64u;
+        uint32_t a[8];
+        for (int c = 0; c < 8; ++c)
+            a[c] = mode == 1 ? ((uint32_t)c == e / 8 ? (2u << (4 * (e % 8))) : 0u) : 0x22222222u;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         tmem + ((32u * warp) << 16) + 320u),
+                     "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]),
+                     "r"(a[7])
+                     : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+        // M = 256 (pair), N = 256
+        const uint32_t idesc = (1u << 7) | (1u << 10) | (32u << 17) | (1u << 23) | (16u << 24);
+        auto desc = [](uint32_t a, uint32_t lbo, uint32_t sbo) {
+            return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+                   ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+        };
+        const uint32_t n_it = mode == 1 ? 1u : iters;
+        for (uint32_t it = 0; it < n_it; ++it) {
+            const uint32_t m = it & 7;
+            const uint64_t b = mode == 2
+                ? desc(base + 16u * (2u * (m & 1) + 128u * (m >> 1)), 16, 128)
+                : desc(base, 128, 256);
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n}\n"
+                ::"r"(tmem), "r"(tmem + 320u), "l"(b), "r"(idesc), "r"(it), "r"(tmem + 256u),
+                "r"(tmem + 264u)
+                : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                bar_a), "h"((uint16_t)3)
+            : "memory");
+    }
+    asm volatile(
+        "{\n.reg .pred P1;\nW:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(bar_a)
+        : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (mode == 1) {
+        uint32_t nbad = 0;
+        for (int q = 0; q < 8; ++q) {
+            uint32_t v[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+                "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                  "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                  "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                  "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                  "=r"(v[30]), "=r"(v[31])
+                : "r"(tmem + ((32u * warp) << 16) + 32u * q));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const uint32_t r = 128u * rank + 32u * warp + lane;
+            for (int e = 0; e < 32; ++e) {
+                const uint32_t n = 32u * q + e;
+                const float want = (r % 64u == n % 64u) ? 1.0f : 0.0f;
+                nbad += __uint_as_float(v[e]) != want;
+                if (blockIdx.x < 2) dout[r * 256u + n] = __uint_as_float(v[e]);
+            }
+        }
+        if (nbad) atomicAdd(bad, nbad);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 }  // namespace
 
 // FP4 probe: rate (MAC/s) and exactness (modes above; mode 2 = rate with the hash kernel's
@@ -342,6 +468,45 @@ extern "C" ssbh_status ssbh_probe_mma_f4_tmem_a(uint32_t iters, int mode, double
     cudaEventDestroy(e1);
     if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
     if (macs_per_s) *macs_per_s = (double)sms * iters * 128.0 * 256.0 * 64.0 / (ms * 1e-3);
+    if (ms_out) *ms_out = ms;
+    if (mismatches) *mismatches = hb[0];
+    return SSBH_OK;
+}
+
+extern "C" ssbh_status ssbh_probe_mma_f4_pair(uint32_t iters, int mode, double* macs_per_s,
+                                              double* ms_out, uint32_t* mismatches,
+                                              float* d_out_host) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SSBH_NO_DEVICE;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int smem = 120 * 1024;
+    cudaFuncSetAttribute(k_f4_pair_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    uint32_t* bad = nullptr;
+    float* dout = nullptr;
+    if (cudaMalloc(&bad, 8) != cudaSuccess) return SSBH_CUDA;
+    if (cudaMalloc(&dout, 256 * 256 * 4) != cudaSuccess) return SSBH_CUDA;
+    cudaMemset(bad, 0, 8);
+    cudaMemset(dout, 0, 256 * 256 * 4);
+    const int grid = sms & ~1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k_f4_pair_probe<<<grid, 128, smem>>>(iters, mode, bad, dout);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    uint32_t hb[2] = {0, 0};
+    cudaMemcpy(hb, bad, 8, cudaMemcpyDeviceToHost);
+    if (d_out_host) cudaMemcpy(d_out_host, dout, 256 * 256 * 4, cudaMemcpyDeviceToHost);
+    cudaFree(bad);
+    cudaFree(dout);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
+    // per pair and MMA: 256 x 256 x 64 MACs
+    if (macs_per_s) *macs_per_s = (double)(grid / 2) * iters * 256.0 * 256.0 * 64.0 / (ms * 1e-3);
     if (ms_out) *ms_out = ms;
     if (mismatches) *mismatches = hb[0];
     return SSBH_OK;

@@ -83,3 +83,4 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 }
 
 }  // namespace ssbh_dev
+

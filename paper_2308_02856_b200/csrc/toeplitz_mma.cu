@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // q = 4 gg + kc, word w -> column 4 q + w of the stage
         auto expand = [&](const uint4 (&x)[4], uint32_t slot) {
             const uint32_t ta = tmem + lane_addr + kF4ACol0 + 64u * slot;
+#ifndef SSBH_EXP_NOAPROD
 #pragma unroll
             for (int h = 0; h < 2; ++h) {  // columns 32h .. 32h + 31: chunks 8h .. 8h + 7
                 uint32_t v[32];
@@ -525,6 +526,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 SSBH_TMEM_ST32(ta + 32u * h, v);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#else
+            (void)x;
+            (void)ta;
+#endif
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
