@@ -577,6 +577,10 @@ static ssbh_status validate_params(const ssbh_extract_params* p, uint32_t* nown)
 
 // external_payload: the plan consumes a payload it does not own (shard owners), whose element
 // size is external_payload_bytes.
+// Parent mode of the leaf GEMM: leaves of <= 4096 positions (the parent's input, 2 leaves, fits
+// the 8192-position leaf buffer) and L >= 2.
+static bool leaf_parent_mode(const SplitGeom& g) { return g.gemm && g.L >= 2 && g.sL <= 4096; }
+
 static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t chunk_bits,
                                     ssbh_plan** out, bool external_payload = false,
                                     int external_payload_bytes = 0) {
@@ -661,7 +665,8 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         if (pl->split) {
             const uint32_t lw = (uint32_t)(pl->sg.sL / 32);
             if (pl->sg.gemm) {
-                pl->mmv = make_leaf_geom((uint32_t)pl->sg.nvirt, lw, pl->device);
+                pl->mmv = make_leaf_geom((uint32_t)pl->sg.nvirt, lw, pl->device,
+                                         leaf_parent_mode(pl->sg));
                 const uint64_t tk = (uint64_t)pl->sg.T * k;  // remainder: one GEMM as well
                 pl->mmr = make_mma_geom(nown, pl->kw, mean_nj > tk ? mean_nj - tk : 1, pl->device);
             }
@@ -1029,7 +1034,7 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 v.ybuf = pl->vy.as<uint32_t>();
                 // one CTA per M tile (round 2 A/B: a CTA-pair variant, cta_group::2 with M = 256
                 // and half the Hankel table per SM, measured 32.3 vs 29.3 ms at config 3)
-                v.leaf = 1;
+                v.leaf = leaf_parent_mode(g) ? 2 : 1;
                 v.src.ybuf = pl->ybuf.as<uint32_t>();
                 v.src.lay = lay;
                 v.src.k = g.k;
@@ -1039,7 +1044,8 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 v.src.batch = g.batch;
                 v.src.jj0 = jj0;
                 v.src.nown = pl->nown;
-                v.src.kpw = (uint32_t)(g.sL / 32 / pl->mmv.ksplit);
+                v.src.kpw = leaf_parent_mode(g) ? (uint32_t)(2 * g.sL / 32)
+                                                : (uint32_t)(g.sL / 32 / pl->mmv.ksplit);
                 v.sbuf = pl->vs.as<uint32_t>();
                 v.out = pl->vout.as<uint32_t>();
                 v.out_stride = g.sL / 32;

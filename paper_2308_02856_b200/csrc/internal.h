@@ -214,7 +214,8 @@ struct LeafSrc {
     Layout lay;              // their layout (yoff, ypad)
     unsigned long long k;    // square size (bits)
     uint32_t L, leaves, gpad, batch, jj0, nown;
-    uint32_t kpw;            // leaf input words per K part (held in shared memory)
+    uint32_t kpw;            // leaf input words per K part (held in shared memory); parent
+                             // mode: the parent's input words (2 leaves)
 };
 
 struct MmaHashArgs {
@@ -230,7 +231,9 @@ struct MmaHashArgs {
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
     uint32_t stage_bits;     // input positions per pipeline stage (set by launch_hash_mma)
     uint32_t leaf;           // 1: leaf mode (src below; items walked N tile innermost per
-                             // (M tile, K part); ksplit = K parts)
+                             // (M tile, K part); ksplit = K parts); 2: parent mode — a CTA
+                             // keeps one M tile of a level L-1 node's input and runs its three
+                             // children (P = lo ^ hi, Q = lo, R = hi) N tile by N tile
     LeafSrc src;
 };
 // Per-block seeds on the tensor cores: work item = (owned block, window of 256 row tiles of
@@ -293,7 +296,8 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
 // Leaf mode (the split's shared-seed leaf GEMM): K parts of <= 8192 positions, N tiles innermost.
-MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device);
+// parent: the parent-node variant (leaves of <= 4096 positions: 2 leaves fit the buffer)
+MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device, bool parent);
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
 void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st);
 

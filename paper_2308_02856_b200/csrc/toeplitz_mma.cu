@@ -95,6 +95,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // ------------------------------------------------------------------ work items
 struct Item {
     uint32_t mt, nt;     // M tile (128 owned blocks), N tile (256 output rows)
+    uint32_t child;      // parent mode: 0 = P (lo ^ hi), 1 = Q (lo), 2 = R (hi)
     uint32_t st0, nst;   // stage range [st0, st0 + nst) of this K part
     uint64_t soff;       // seed offset (u32 words) of the M tile's first block: 0 for a plan's
                          // shared seed; the split's leaf groups (128-aligned) each have their own
@@ -103,6 +104,23 @@ struct Item {
 __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item& d) {
     if (item >= a.items) return false;
     d.nt = item % a.ntiles;
+    d.child = 0;
+    if (a.leaf == 2) {
+        // item = ((parent group * mpg + M tile in group) * 3 + child) * ntiles + nt
+        const uint32_t c3 = item / a.ntiles;
+        d.child = c3 % 3;
+        const uint32_t sup = c3 / 3;
+        const uint32_t mpg = a.src.gpad / kM;
+        const uint32_t pg = sup / mpg, mtl = sup % mpg;
+        const uint32_t pleaves = a.src.leaves / 3;
+        const uint32_t t = pg / pleaves, pp = pg % pleaves;
+        const uint32_t grp = t * a.src.leaves + 3 * pp + d.child;  // the child's group
+        d.mt = grp * mpg + mtl;
+        d.soff = a.lay.soff[(uint64_t)d.mt * kM];
+        d.st0 = 0;
+        d.nst = a.mt_words[d.mt] / (a.stage_bits / 32);
+        return true;
+    }
     const uint32_t r = item / a.ntiles;
     const uint32_t kp = r % a.ksplit;
     d.mt = r / a.ksplit;
@@ -117,13 +135,16 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
 // A CTA's item sequence: items blockIdx.x, +grid, ...; in leaf mode super-items (M tile, K part)
 // blockIdx.x, +grid, ... with their N tiles in order (the M tile's leaf inputs stay in shared
 // memory across them).
+__device__ __forceinline__ uint32_t super_items(const MmaHashArgs& a) {
+    return a.leaf == 2 ? 3 * a.ntiles : a.ntiles;
+}
 __device__ __forceinline__ uint32_t first_item(const MmaHashArgs& a) {
-    return a.leaf ? blockIdx.x * a.ntiles : blockIdx.x;
+    return a.leaf ? blockIdx.x * super_items(a) : blockIdx.x;
 }
 __device__ __forceinline__ uint32_t next_item(const MmaHashArgs& a, uint32_t item) {
     if (!a.leaf) return item + gridDim.x;
-    const uint32_t nt = item % a.ntiles;
-    return nt + 1 < a.ntiles ? item + 1 : item - nt + gridDim.x * a.ntiles;
+    const uint32_t per = super_items(a), i = item % per;
+    return i + 1 < per ? item + 1 : item - i + gridDim.x * per;
 }
 
 // Walks (item, stage) pairs of this CTA in order; used by the producers twice (consume and
@@ -290,7 +311,10 @@ __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, 
     if (aw == 0 && lane == 0) {
         uint64_t off[1 << kMaxL];
         const uint32_t t = grp / q.leaves, path = grp % q.leaves;
-        const int n = leaf_offsets(path, q.L, q.k, (uint64_t)t * q.k, false, off);
+        // parent mode: the input of the children's parent (level L - 1, path / 3)
+        const int n = a.leaf == 2
+                          ? leaf_offsets(path / 3, q.L - 1, q.k, (uint64_t)t * q.k, false, off)
+                          : leaf_offsets(path, q.L, q.k, (uint64_t)t * q.k, false, off);
         for (int e = 0; e < n; ++e) loff[e] = off[e] / 32;
         *lnoff = n;
     }
@@ -543,8 +567,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             const uint32_t aw = set * 4 + ((warp - kProd0) & 3);  // 0..7
             uint32_t built = 0xFFFFFFFFu;
             const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
+            const uint32_t per = super_items(a);
+            const uint32_t half = a.src.kpw / 2;  // parent mode: words of the lo half
             for (uint32_t g = set; cur.valid; g += kSets, cur.advance(a, kSets)) {
-                const uint32_t sup = cur.item / a.ntiles;
+                const uint32_t sup = cur.item / per;
                 if (sup != built) {
 #ifndef SSBH_EXP_NOBUILD
                     leaf_build(a, cur.d, aw, lane, lraw, loff, lnoff);
@@ -553,8 +579,25 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 }
                 uint4 x[4];
                 const uint32_t* src = lrow + 16u * cur.s;
+                if (a.leaf == 2 && cur.d.child != 1) {
+                    // P = lo ^ hi, R = hi (Q = lo reads the lo half as a leaf would)
+                    const uint32_t* hi = src + half;
 #pragma unroll
-                for (int h = 0; h < 4; ++h) x[h] = *reinterpret_cast<const uint4*>(src + 4 * h);
+                    for (int h = 0; h < 4; ++h) {
+                        uint4 u = *reinterpret_cast<const uint4*>(hi + 4 * h);
+                        if (cur.d.child == 0) {
+                            const uint4 l = *reinterpret_cast<const uint4*>(src + 4 * h);
+                            u.x ^= l.x;
+                            u.y ^= l.y;
+                            u.z ^= l.z;
+                            u.w ^= l.w;
+                        }
+                        x[h] = u;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) x[h] = *reinterpret_cast<const uint4*>(src + 4 * h);
+                }
                 const uint32_t slot = g % kS;
                 if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
                 expand(x, slot);
@@ -1003,8 +1046,18 @@ MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device) 
     return g;
 }
 
-MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device) {
+MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device, bool parent) {
     MmaGeom g{};
+    if (parent) {  // one K part; the parent's 2 lw words per row fit the leaf buffer
+        g.mtiles = mma_mtiles(nvirt);
+        g.ntiles = (lw + kN / 32 - 1) / (kN / 32);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        g.grid = sms;
+        g.ksplit = 1;
+        g.items = (uint64_t)g.mtiles * g.ntiles;  // = supers * 3 * ntiles
+        return g;
+    }
     g.mtiles = mma_mtiles(nvirt);
     g.ntiles = (lw + kN / 32 - 1) / (kN / 32);
     int sms = 148;
@@ -1063,8 +1116,8 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     a.stage_bits = kF4StageK;
     const size_t smem = f4_smem(kSets) + (a.leaf ? kLeafSmem : 0);
     cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (a.leaf) {  // super-items (M tile, K part) of N tiles; grid = one wave of CTAs at most
-        const uint64_t supers = g.items / a.ntiles;
+    if (a.leaf) {  // super-items of N tiles (x3 children in parent mode); one wave of CTAs
+        const uint64_t supers = g.items / (a.leaf == 2 ? 3ull * a.ntiles : a.ntiles);
         k_toeplitz_f4<<<(unsigned)std::min<uint64_t>(g.grid, supers), kF4Threads, smem, st>>>(a);
         return;
     }
