@@ -1044,6 +1044,7 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 v.src.batch = g.batch;
                 v.src.jj0 = jj0;
                 v.src.nown = pl->nown;
+                v.src.seed_words = g.seed_words;
                 v.src.kpw = leaf_parent_mode(g) ? (uint32_t)(2 * g.sL / 32)
                                                 : (uint32_t)(g.sL / 32 / pl->mmv.ksplit);
                 v.sbuf = pl->vs.as<uint32_t>();

@@ -4,6 +4,7 @@
 // hash kernel is judged against is measured live: every SM runs independent
 // acc ^= a & b chains (each one LOP3.LUT 0x78, the hash kernel's inner instruction) at
 // full occupancy, timed with CUDA events.
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,6 +38,11 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SSBH_EXP_CLOCK
+    const long long exp_c0 = clock64();
+    unsigned long long exp_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(exp_t0));
+#endif
     uint32_t* w = reinterpret_cast<uint32_t*>(smem);
     if (mode >= 2)  // hash-kernel layouts / K96 tiles: fill the first 44 KB
         for (uint32_t i = threadIdx.x; i < 45056 / 4; i += blockDim.x) w[i] = 0x22222222u;
@@ -139,6 +145,15 @@ __global__ void __launch_bounds__(128, 1) k_f4_probe(uint32_t iters, int mode, u
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
+#ifdef SSBH_EXP_CLOCK
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        const long long c1 = clock64();
+        printf("EXPCLOCK k_f4_probe mode=%d ns=%llu MHz=%.1f\n", mode, t1 - exp_t0,
+               (double)(c1 - exp_c0) * 1e3 / (double)(t1 - exp_t0));
+    }
+#endif
 }
 
 

@@ -216,6 +216,7 @@ struct LeafSrc {
     uint32_t L, leaves, gpad, batch, jj0, nown;
     uint32_t kpw;            // leaf input words per K part (held in shared memory); parent
                              // mode: the parent's input words (2 leaves)
+    unsigned long long seed_words;  // u32 words per leaf seed region (SplitGeom::seed_words)
 };
 
 struct MmaHashArgs {

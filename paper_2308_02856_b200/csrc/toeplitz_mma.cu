@@ -25,6 +25,7 @@
 // Operand nibbles are masked to clean 0 / 1.0: toggling don't-care bits in the multipliers
 // drew the 1000 W power cap (SM clock 1.61 GHz instead of 1.965; round 1).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -40,6 +41,7 @@ namespace {
 constexpr int kM = 128;                      // blocks per M tile (= TMEM lanes)
 constexpr int kN = 256;                      // output rows per N tile (= accumulator columns)
 constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps per stage
+constexpr uint32_t kF4StageWords = 16;       // y words per 512-position pipeline stage
 
 // ------------------------------------------------------------------ tcgen05 / cp.async
 __device__ __forceinline__ void tc_fence_before() {
@@ -92,6 +94,18 @@ __device__ __forceinline__ void cp_async_wait() {
         "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                               \
         : "memory")
 
+// Dev A/B hooks (tools/build_exp.sh): which waits poll instead of suspending.
+#if defined(SSBH_EXP_SPIN_ALL)
+#define F4_WAIT_T mbar_wait
+#define F4_WAIT_S mbar_wait
+#elif defined(SSBH_EXP_SPIN_T)
+#define F4_WAIT_T mbar_wait
+#define F4_WAIT_S mbar_wait_sleep
+#else
+#define F4_WAIT_T mbar_wait_sleep
+#define F4_WAIT_S mbar_wait_sleep
+#endif
+
 // ------------------------------------------------------------------ work items
 struct Item {
     uint32_t mt, nt;     // M tile (128 owned blocks), N tile (256 output rows)
@@ -132,48 +146,90 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
     return true;
 }
 
-// A CTA's item sequence: items blockIdx.x, +grid, ...; in leaf mode super-items (M tile, K part)
-// blockIdx.x, +grid, ... with their N tiles in order (the M tile's leaf inputs stay in shared
-// memory across them).
+// A CTA's item sequence. Direct mode: items blockIdx.x, +grid, ..., each decoded on its own.
+// Leaf modes: super-items (leaf: M tile x K part; parent mode: the parent's M tile with its
+// three children) blockIdx.x, +grid, ..., whose N tiles follow each other while the M tile's
+// leaf inputs stay in shared memory. Everything but the N tile (and the child) is decoded once
+// per super-item: the per-item decode (five divisions and two layout loads, in every warp) was
+// ~1100 clocks of tensor-pipe bubble per item (skeleton A/B, profiles/r02_ab_leaf_gemm.md).
 __device__ __forceinline__ uint32_t super_items(const MmaHashArgs& a) {
     return a.leaf == 2 ? 3 * a.ntiles : a.ntiles;
 }
-__device__ __forceinline__ uint32_t first_item(const MmaHashArgs& a) {
-    return a.leaf ? blockIdx.x * super_items(a) : blockIdx.x;
-}
-__device__ __forceinline__ uint32_t next_item(const MmaHashArgs& a, uint32_t item) {
-    if (!a.leaf) return item + gridDim.x;
-    const uint32_t per = super_items(a), i = item % per;
-    return i + 1 < per ? item + 1 : item - i + gridDim.x * per;
-}
+struct ItemWalk {
+    Item d;
+    bool valid;
+    uint32_t sup;  // leaf modes: super-item index; direct mode: item index
+    __device__ __forceinline__ void load(const MmaHashArgs& a) {
+        if (!a.leaf) {
+            valid = decode(a, sup, d);
+            return;
+        }
+        valid = sup < (uint32_t)(a.items / super_items(a));
+        if (!valid) return;
+        d.nt = 0;
+        d.child = 0;
+        if (a.leaf == 2) {
+            // super-item = parent group * mpg + M tile in the group; child c is leaf group
+            // t * leaves + 3 * pp + c, whose M tiles lie mpg further and whose seed region
+            // follows the previous child's (k_split_layout: soff = group * seed words)
+            const uint32_t mpg = a.src.gpad / kM;
+            const uint32_t pg = sup / mpg, mtl = sup % mpg;
+            const uint32_t pleaves = a.src.leaves / 3;
+            const uint32_t t = pg / pleaves, pp = pg % pleaves;
+            d.mt = (t * a.src.leaves + 3 * pp) * mpg + mtl;
+            d.st0 = 0;
+            d.nst = a.mt_words[d.mt] / (kF4StageWords);  // the same rows in all three children
+        } else {
+            const uint32_t kp = sup % a.ksplit;
+            d.mt = sup / a.ksplit;
+            const uint32_t ns = a.mt_words[d.mt] / (kF4StageWords);
+            d.st0 = (uint32_t)((uint64_t)ns * kp / a.ksplit);
+            d.nst = (uint32_t)((uint64_t)ns * (kp + 1) / a.ksplit) - d.st0;
+        }
+        d.soff = a.lay.soff[(uint64_t)d.mt * kM];
+    }
+    __device__ __forceinline__ void start(const MmaHashArgs& a) {
+        sup = blockIdx.x;
+        load(a);
+    }
+    __device__ __forceinline__ void next(const MmaHashArgs& a) {
+        if (a.leaf) {
+            if (++d.nt < a.ntiles) return;
+            d.nt = 0;
+            if (a.leaf == 2 && ++d.child < 3) {
+                d.mt += a.src.gpad / kM;
+                d.soff += a.src.seed_words;
+                return;
+            }
+        }
+        sup += gridDim.x;
+        load(a);
+    }
+};
 
 // Walks (item, stage) pairs of this CTA in order; used by the producers twice (consume and
 // prefetch kPre stages ahead).
 struct StageIt {
-    uint32_t item;
+    ItemWalk w;
     uint32_t s;      // stage within the item
-    Item d;
-    bool valid;
-    __device__ void start(const MmaHashArgs& a) {
-        item = first_item(a);
+    __device__ __forceinline__ void start(const MmaHashArgs& a) {
+        w.start(a);
         s = 0;
-        valid = decode(a, item, d);
         skip_empty(a);
     }
-    __device__ void skip_empty(const MmaHashArgs& a) {
-        while (valid && s >= d.nst) {
-            item = next_item(a, item);
+    __device__ __forceinline__ void skip_empty(const MmaHashArgs& a) {
+        while (w.valid && s >= w.d.nst) {
+            w.next(a);
             s = 0;
-            valid = decode(a, item, d);
         }
     }
-    __device__ void next(const MmaHashArgs& a) {
+    __device__ __forceinline__ void next(const MmaHashArgs& a) {
         ++s;
         skip_empty(a);
     }
     // skip over the stages other producer sets fill
-    __device__ void advance(const MmaHashArgs& a, int count) {
-        for (int i = 0; i < count && valid; ++i) next(a);
+    __device__ __forceinline__ void advance(const MmaHashArgs& a, int count) {
+        for (int i = 0; i < count && w.valid; ++i) next(a);
     }
 };
 
@@ -183,12 +239,13 @@ __device__ __forceinline__ void s_prefetch(const MmaHashArgs& a, const StageIt& 
                                            uint32_t* raw) {
     if (lane < 8) {
         uint64_t q0a = 0;
-        if (p.valid) {
-            const uint64_t b1 = (uint64_t)p.d.nt * kN + (uint64_t)(p.d.st0 + p.s) * a.stage_bits + 1;
+        if (p.w.valid) {
+            const uint64_t b1 =
+                (uint64_t)p.w.d.nt * kN + (uint64_t)(p.w.d.st0 + p.s) * a.stage_bits + 1;
             q0a = (b1 >> 5) & ~3ull;
         }
-        cp_async16(raw + 4 * lane, a.sbuf + (p.valid ? p.d.soff : 0ull) + q0a + 4 * lane,
-                   p.valid ? 16u : 0u);
+        cp_async16(raw + 4 * lane, a.sbuf + (p.w.valid ? p.w.d.soff : 0ull) + q0a + 4 * lane,
+                   p.w.valid ? 16u : 0u);
     }
 }
 
@@ -279,9 +336,9 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
                                               uint32_t jl, uint32_t* raw) {
     const uint32_t* src = a.ybuf;
     uint32_t bytes = 0;
-    if (p.valid) {
-        const uint32_t jj = p.d.mt * kM + jl;
-        const uint64_t w0 = (uint64_t)(p.d.st0 + p.s) * (kF4StageK / 32);
+    if (p.w.valid) {
+        const uint32_t jj = p.w.d.mt * kM + jl;
+        const uint64_t w0 = (uint64_t)(p.w.d.st0 + p.s) * (kF4StageK / 32);
         if (jj < a.nown && w0 < a.lay.ypad[jj]) {
             src = a.ybuf + a.lay.yoff[jj] + w0;
             bytes = 16;
@@ -401,6 +458,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     int* lnoff = reinterpret_cast<int*>(loff + (1 << kMaxL));
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SSBH_EXP_CLOCK  // dev builds: the SM clock the kernel actually ran at (power cap)
+    const long long exp_c0 = clock64();
+    unsigned long long exp_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(exp_t0));
+#endif
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], kFullArrivals);
@@ -435,15 +497,15 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- epilogue
         const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;  // TMEM sub-partition, columns
         uint32_t t = 0;  // accumulation rounds consumed
-        for (uint32_t item = first_item(a);; item = next_item(a, item)) {
-            Item d;
-            if (!decode(a, item, d)) break;
+        ItemWalk wk;
+        for (wk.start(a); wk.valid; wk.next(a)) {
+            const Item d = wk.d;
             const uint32_t rounds = d.nst ? (d.nst + kF4MaxStages - 1) / kF4MaxStages : 1;
             uint32_t acc_w[kQW];
 #pragma unroll
             for (int q = 0; q < kQW; ++q) acc_w[q] = 0;
             for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
-                mbar_wait_sleep(&tfull[0], t & 1);
+                F4_WAIT_T(&tfull[0], t & 1);
                 tc_fence_after();
 #ifndef SSBH_EXP_NODRAIN
                 if (d.nst) {
@@ -484,18 +546,18 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
         const uint32_t base_g = smem_u32(slots);
-        for (uint32_t item = first_item(a);; item = next_item(a, item)) {
-            Item d;
-            if (!decode(a, item, d)) break;
+        ItemWalk wk;
+        for (wk.start(a); wk.valid; wk.next(a)) {
+            const Item d = wk.d;
             if (d.nst == 0) {
-                if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
+                if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
                 if (lane == 0) mbar_arrive(&tfull[0]);
                 ++t;
                 continue;
             }
             for (uint32_t s0 = 0; s0 < d.nst; s0 += kF4MaxStages, ++t) {
 #ifndef SSBH_EXP_NOTEMPTY
-                if (t >= 1) mbar_wait_sleep(&tempty[0], (t - 1) & 1);
+                if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
 #endif
                 tc_fence_after();
                 const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
@@ -503,7 +565,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     const uint32_t slot = g % kS;
                     // hardware-suspended wait: no try_wait polls on the L1 data pipe the
                     // producers' stores and the MMA operand reads share (round 1: 1.1 % faster)
-                    mbar_wait_sleep(&full[slot], (g / kS) & 1);
+                    F4_WAIT_S(&full[slot], (g / kS) & 1);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t ga = base_g + slot * kF4Slot;
@@ -567,25 +629,24 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             const uint32_t aw = set * 4 + ((warp - kProd0) & 3);  // 0..7
             uint32_t built = 0xFFFFFFFFu;
             const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
-            const uint32_t per = super_items(a);
             const uint32_t half = a.src.kpw / 2;  // parent mode: words of the lo half
-            for (uint32_t g = set; cur.valid; g += kSets, cur.advance(a, kSets)) {
-                const uint32_t sup = cur.item / per;
+            for (uint32_t g = set; cur.w.valid; g += kSets, cur.advance(a, kSets)) {
+                const uint32_t sup = cur.w.sup;
                 if (sup != built) {
 #ifndef SSBH_EXP_NOBUILD
-                    leaf_build(a, cur.d, aw, lane, lraw, loff, lnoff);
+                    leaf_build(a, cur.w.d, aw, lane, lraw, loff, lnoff);
 #endif
                     built = sup;
                 }
                 uint4 x[4];
                 const uint32_t* src = lrow + 16u * cur.s;
-                if (a.leaf == 2 && cur.d.child != 1) {
+                if (a.leaf == 2 && cur.w.d.child != 1) {
                     // P = lo ^ hi, R = hi (Q = lo reads the lo half as a leaf would)
                     const uint32_t* hi = src + half;
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
                         uint4 u = *reinterpret_cast<const uint4*>(hi + 4 * h);
-                        if (cur.d.child == 0) {
+                        if (cur.w.d.child == 0) {
                             const uint4 l = *reinterpret_cast<const uint4*>(src + 4 * h);
                             u.x ^= l.x;
                             u.y ^= l.y;
@@ -599,21 +660,21 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     for (int h = 0; h < 4; ++h) x[h] = *reinterpret_cast<const uint4*>(src + 4 * h);
                 }
                 const uint32_t slot = g % kS;
-                if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+                if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
                 expand(x, slot);
             }
         } else {
         pre = cur;
         uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
 #ifdef SSBH_EXP_NOYLOAD
-        pre.valid = false;
+        pre.w.valid = false;
 #endif
         for (int i = 0; i < kF4Pre; ++i) {
             y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
             cp_async_commit();
             pre.advance(a, kSets);
         }
-        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
+        for (uint32_t g = set, i = 0; cur.w.valid; g += kSets, ++i, cur.advance(a, kSets)) {
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
             uint4 x[4];
@@ -621,7 +682,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             for (int h = 0; h < 4; ++h)
                 x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + h * kM * 4);
             const uint32_t slot = g % kS;
-            if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+            if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
             expand(x, slot);
             y_prefetch_f4(a, pre, jl, raw + rs * kM * 16);
             cp_async_commit();
@@ -644,16 +705,16 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             cp_async_commit();
             pre.advance(a, kSets);
         }
-        for (uint32_t g = set, i = 0; cur.valid; g += kSets, ++i, cur.advance(a, kSets)) {
+        for (uint32_t g = set, i = 0; cur.w.valid; g += kSets, ++i, cur.advance(a, kSets)) {
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
             __syncwarp();
             const uint32_t* sw = raw + rs * 32;
             const uint64_t b1 =
-                (uint64_t)cur.d.nt * kN + (uint64_t)(cur.d.st0 + cur.s) * kF4StageK + 1;
+                (uint64_t)cur.w.d.nt * kN + (uint64_t)(cur.w.d.st0 + cur.s) * kF4StageK + 1;
             const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));
             const uint32_t slot = g % kS;
-            if (g >= (uint32_t)kS) mbar_wait_sleep(&empty[slot], ((g / kS) - 1) & 1);
+            if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
             uint8_t* gs = slots + (size_t)slot * kF4Slot;
             // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
             // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position. Unit u + 128 starts 4
@@ -692,6 +753,16 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
+#ifdef SSBH_EXP_CLOCK
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        const long long c1 = clock64();
+        printf("EXPCLOCK k_toeplitz_f4 leaf=%u items=%llu ns=%llu MHz=%.1f\n", a.leaf,
+               (unsigned long long)a.items, t1 - exp_t0,
+               (double)(c1 - exp_c0) * 1e3 / (double)(t1 - exp_t0));
+    }
+#endif
 }
 
 // =========================================================================================

@@ -246,13 +246,14 @@ uint32_t split_levels(uint64_t k, bool gemm) {
         f *= 0.75;
         if (k % (256ull << L) != 0) break;
         const double nc = (double)(k >> L) / 128.0;
-        if (nc < 64) break;
+        if (nc < (gemm ? 32 : 64)) break;
         if (gemm) {
-            // config 2 (k = 2^15, L = 1) measured no gain: short keys keep the direct GEMM
-            // leaves >= 2^13 positions (16 FP4 stages per work item): with 8 epilogue warps the
-            // per-item drain is short enough that config 3 gains from L = 6 (hash 44.0 -> 39.6-42.5
-            // ms; L = 5 before); config 5 stays at kMaxL = 7
-            if (k < (1ull << 18) || (k >> L) < (1ull << 13)) break;
+            // config 2 (k = 2^15, L = 1) measured no gain: short keys keep the direct GEMM.
+            // Leaves >= 2^12 positions: leaves of 2^13 run as leaf-mode items of 16 FP4 stages;
+            // leaves of 2^12 run in the leaf GEMM's parent mode (a CTA builds the parent's 2^13
+            // positions once for its three children), which is what makes the seventh level pay
+            // (config 3 hash L = 6 / 7 = 31.2 / 27.6 ms); config 5 stays at kMaxL = 7
+            if (k < (1ull << 18) || (k >> L) < (1ull << 12)) break;
             best = L;
             continue;
         }

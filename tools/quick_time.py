@@ -20,12 +20,17 @@ def main():
     ap.add_argument("--per-block", action="store_true", help="force per-block seeds")
     ap.add_argument("--override", action="append", default=[], metavar="KEY=VALUE",
                     help="plan-construction override (ssbh_set_plan_overrides)")
+    ap.add_argument("--f4-peak", action="store_true", help="also run the kind::mxf4 probe")
     args = ap.parse_args()
     tag = os.environ.get("SSBH_CUDA_LIB", "in-tree") + "".join(" " + o for o in args.override)
     if args.override:
         P.set_overrides(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.override})
     peak, _ = P.measure_lop3_peak(20000)
     print(json.dumps({"win": tag, "lop3_peak_T": round(peak / 1e12, 3)}), flush=True)
+    if args.f4_peak:
+        r, ms = P.measure_mma_f4_peak()
+        print(json.dumps({"win": tag, "f4_peak_P": round(r / 1e15, 4), "ms": round(ms, 2)}),
+              flush=True)
     for cid in [int(c) for c in args.configs.split(",")]:
         c = dict(P.CONFIGS[cid])
 
