@@ -724,7 +724,10 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
                   ((g.per_block ? g.nvirt : (size_t)g.T * g.leaves) * g.seed_words + 256) * 4);
         // leaf inputs: materialised only for tiled leaves (the leaf GEMM builds its own)
         if (!e && !g.gemm) e = alloc(pl->vy, (size_t)g.nvirt * g.vlw * 4 + 16);
-        if (!e) e = alloc(pl->vout, (size_t)g.nvirt * (g.sL / 8) + 16);
+        // leaf outputs (parent mode: level L - 1 nodes, 2/3 of the leaves' bytes)
+        if (!e)
+            e = alloc(pl->vout, (size_t)g.nvirt * (g.sL / 8) / (leaf_parent_mode(g) ? 3 : 1) *
+                                        (leaf_parent_mode(g) ? 2 : 1) + 16);
         if (!e) e = alloc(pl->vrem, (size_t)nown * pl->kw * 4 + 16);
         if (!e) e = pl->vlay.alloc((uint32_t)g.nvirt);
         if (!e && g.gemm) e = alloc(pl->vmt, (size_t)pl->mmv.mtiles * 4);
@@ -1049,7 +1052,8 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                                                 : (uint32_t)(g.sL / 32 / pl->mmv.ksplit);
                 v.sbuf = pl->vs.as<uint32_t>();
                 v.out = pl->vout.as<uint32_t>();
-                v.out_stride = g.sL / 32;
+                // parent mode writes level L - 1 nodes (2 leaves wide, a third as many rows)
+                v.out_stride = (leaf_parent_mode(g) ? 2 : 1) * (g.sL / 32);
                 v.lay = vlay;  // soff per 128-block M tile = the group's leaf seed
                 v.nown = (uint32_t)g.nvirt;
                 v.kw = (uint32_t)(g.sL / 32);
@@ -1074,8 +1078,15 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 v.items = pl->pbv.items;
                 launch_hash_mma_pb(v, pl->pbv, st);
             }
+            // the parent-mode leaf GEMM has done the deepest level: combine from level L - 1
+            SplitGeom gc = g;
+            if (leaf_parent_mode(g)) {
+                gc.L = g.L - 1;
+                gc.leaves = g.leaves / 3;
+                gc.sL = 2 * g.sL;
+            }
             launches += 2 + launch_split_combine(pl->vout.as<uint32_t>(), pl->vy.as<uint32_t>(),
-                                                 pl->vrem.as<uint32_t>(), jj0, cnt, pl->kw, g, out,
+                                                 pl->vrem.as<uint32_t>(), jj0, cnt, pl->kw, gc, out,
                                                  pl->direct_out ? pl->p.out_bits / 32 : pl->kw,
                                                  st);
         }

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(128, 1) k_f4_tmem_a_probe(uint32_t iters, int 
     uint32_t* w = reinterpret_cast<uint32_t*>(smem);
     for (uint32_t i = threadIdx.x; i < 45056 / 4; i += blockDim.x) w[i] = 0u;
     __syncthreads();
-    if (mode == 2) {
+    if (mode >= 2) {
         for (uint32_t i = threadIdx.x; i < 45056 / 4; i += blockDim.x) w[i] = 0x22222222u;
     } else if (threadIdx.x < 128) {
         // B rows n = threadIdx.x and n + 128: row n, element e at byte (n%8)*16 + (n/8)*256 +
@@ -232,16 +232,20 @@ __global__ void __launch_bounds__(128, 1) k_f4_tmem_a_probe(uint32_t iters, int 
                    ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
         };
         const uint32_t n_it = mode == 1 ? 1u : iters;
+        // mode 3: rate of N = 128 MMAs alternating between the two halves of the accumulator
+        // (columns 0..127 / 128..255, Hankel rows 128 units further)
+        const uint32_t idesc128 = (idesc & ~(0x3Fu << 17)) | (16u << 17);
         for (uint32_t it = 0; it < n_it; ++it) {
             const uint32_t m = it & 7;
-            const uint64_t b = mode == 2
-                ? desc(base + 16u * (2u * (m & 1) + 128u * (m >> 1)), 16, 128)
+            const uint32_t h = mode == 3 ? (it >> 3) & 1u : 0u;
+            const uint64_t b = mode >= 2
+                ? desc(base + 16u * (2u * (m & 1) + 128u * (m >> 1) + 128u * h), 16, 128)
                 : desc(base, 128, 256);
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n}\n"
-                ::"r"(tmem), "r"(tmem + 320u), "l"(b), "r"(idesc), "r"(it), "r"(tmem + 256u),
-                "r"(tmem + 264u)
+                ::"r"(tmem + 128u * h), "r"(tmem + 320u), "l"(b), "r"(mode == 3 ? idesc128 : idesc),
+                "r"(it), "r"(tmem + 256u), "r"(tmem + 264u)
                 : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -482,7 +486,8 @@ extern "C" ssbh_status ssbh_probe_mma_f4_tmem_a(uint32_t iters, int mode, double
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (cudaGetLastError() != cudaSuccess) return SSBH_CUDA;
-    if (macs_per_s) *macs_per_s = (double)sms * iters * 128.0 * 256.0 * 64.0 / (ms * 1e-3);
+    if (macs_per_s)
+        *macs_per_s = (double)sms * iters * 128.0 * (mode == 3 ? 128.0 : 256.0) * 64.0 / (ms * 1e-3);
     if (ms_out) *ms_out = ms;
     if (mismatches) *mismatches = hb[0];
     return SSBH_OK;

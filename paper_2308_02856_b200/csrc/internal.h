@@ -234,7 +234,9 @@ struct MmaHashArgs {
     uint32_t leaf;           // 1: leaf mode (src below; items walked N tile innermost per
                              // (M tile, K part); ksplit = K parts); 2: parent mode — a CTA
                              // keeps one M tile of a level L-1 node's input and runs its three
-                             // children (P = lo ^ hi, Q = lo, R = hi) N tile by N tile
+                             // children (P = lo ^ hi, Q = lo, R = hi) N tile by N tile, writing
+                             // the parent node's rows [P ^ Q | P ^ R] (out: one row of 2 kw
+                             // words per parent virtual block = super-item * 128 + row)
     LeafSrc src;
 };
 // Per-block seeds on the tensor cores: work item = (owned block, window of 256 row tiles of

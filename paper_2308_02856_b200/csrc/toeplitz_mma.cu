@@ -94,6 +94,19 @@ __device__ __forceinline__ void cp_async_wait() {
         "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                               \
         : "memory")
 
+// 16 accumulator columns v[o .. o + 15] (exact f32 counts < 2^23) -> their parities, column e
+// in bit e: bit 0 of count + 2^23 is shifted in from the top (one SHF per column), in two
+// independent chains.
+__device__ __forceinline__ uint32_t parity16(const uint32_t (&v)[32], int o) {
+    uint32_t c0 = 0, c1 = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        c0 = __funnelshift_r(c0, __float_as_uint(__uint_as_float(v[o + e]) + 8388608.0f), 1);
+        c1 = __funnelshift_r(c1, __float_as_uint(__uint_as_float(v[o + 8 + e]) + 8388608.0f), 1);
+    }
+    return __byte_perm(c0, c1, 0x4473);  // c0 bits 24..31 -> 0..7, c1 bits 24..31 -> 8..15
+}
+
 // Dev A/B hooks (tools/build_exp.sh): which waits poll instead of suspending.
 #if defined(SSBH_EXP_SPIN_ALL)
 #define F4_WAIT_T mbar_wait
@@ -148,8 +161,8 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
 
 // A CTA's item sequence. Direct mode: items blockIdx.x, +grid, ..., each decoded on its own.
 // Leaf modes: super-items (leaf: M tile x K part; parent mode: the parent's M tile with its
-// three children) blockIdx.x, +grid, ..., whose N tiles follow each other while the M tile's
-// leaf inputs stay in shared memory. Everything but the N tile (and the child) is decoded once
+// three children, child fastest) blockIdx.x, +grid, ..., whose N tiles follow each other while
+// the M tile's leaf inputs stay in shared memory. Everything but the N tile (and the child) is decoded once
 // per super-item: the per-item decode (five divisions and two layout loads, in every warp) was
 // ~1100 clocks of tensor-pipe bubble per item (skeleton A/B, profiles/r02_ab_leaf_gemm.md).
 __device__ __forceinline__ uint32_t super_items(const MmaHashArgs& a) {
@@ -193,14 +206,21 @@ struct ItemWalk {
         load(a);
     }
     __device__ __forceinline__ void next(const MmaHashArgs& a) {
-        if (a.leaf) {
-            if (++d.nt < a.ntiles) return;
-            d.nt = 0;
-            if (a.leaf == 2 && ++d.child < 3) {
-                d.mt += a.src.gpad / kM;
+        if (a.leaf == 2) {
+            // N tile by N tile, the three children P, Q, R of each in turn: the epilogue keeps
+            // P's parities in registers and writes the parent's rows P ^ Q and P ^ R
+            const uint32_t mpg = a.src.gpad / kM;
+            if (++d.child < 3) {
+                d.mt += mpg;
                 d.soff += a.src.seed_words;
                 return;
             }
+            d.child = 0;
+            d.mt -= 2 * mpg;
+            d.soff -= 2 * a.src.seed_words;
+            if (++d.nt < a.ntiles) return;
+        } else if (a.leaf) {
+            if (++d.nt < a.ntiles) return;
         }
         sup += gridDim.x;
         load(a);
@@ -497,6 +517,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- epilogue
         const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;  // TMEM sub-partition, columns
         uint32_t t = 0;  // accumulation rounds consumed
+        uint32_t par_w[kQW];  // parent mode: child P's parities of the current N tile
+#pragma unroll
+        for (int q = 0; q < kQW; ++q) par_w[q] = 0;
         ItemWalk wk;
         for (wk.start(a); wk.valid; wk.next(a)) {
             const Item d = wk.d;
@@ -512,24 +535,47 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
 #else
                 if (false) {
 #endif
+                    // The hand-off of the single accumulator is serial with the MMAs (about
+                    // 770 clocks per item at the start of round 2's session 4), so the warp
+                    // releases the accumulator as soon as its last TMEM load has landed and
+                    // only then reduces that load (parity16: independent funnel-shift chains
+                    // instead of one 32-long dependent LOP3 chain).
+                    // (16-column loads double-buffered against the reduction measured slower:
+                    // hash 25.53 -> 26.05 ms.)
 #pragma unroll 1
                     for (int q = 0; q < kQW; ++q) {
                         uint32_t v[32];
                         SSBH_TMEM_LD32(tmem + ((sp * 32u) << 16) + 32u * (qb + q), v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        uint32_t w = 0;
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            w |= (__float_as_uint(__uint_as_float(v[e]) + 8388608.0f) & 1u) << e;
-                        acc_w[q] ^= w;
+                        if (q == kQW - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&tempty[0]);
+                        }
+                        acc_w[q] ^= parity16(v, 0) | (parity16(v, 16) << 16);
                     }
+                } else {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[0]);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[0]);
             }
             const uint32_t jj = d.mt * kM + sp * 32 + lane;
-            if (d.nst && jj < a.nown) {
+            if (a.leaf == 2) {
+                // parent mode: the first combine level here — P stays in registers, the parent
+                // node's rows are [P ^ Q | P ^ R] (row = parent M tile row, a.kw words per half)
+                if (d.child == 0) {
+#pragma unroll
+                    for (int q = 0; q < kQW; ++q) par_w[q] = acc_w[q];
+                } else if (d.nst && jj < a.nown) {
+                    uint32_t* dst = a.out +
+                                    (unsigned long long)(wk.sup * kM + sp * 32 + lane) * a.out_stride +
+                                    (d.child - 1) * a.kw + d.nt * (kN / 32) + qb;
+#pragma unroll
+                    for (int q = 0; q < kQW; ++q)
+                        if (d.nt * (kN / 32) + qb + q < a.kw) dst[q] = acc_w[q] ^ par_w[q];
+                }
+            } else if (d.nst && jj < a.nown) {
                 uint32_t* dst =
                     a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32) + qb;
 #pragma unroll

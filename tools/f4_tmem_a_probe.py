@@ -15,7 +15,7 @@ f = P.lib.ssbh_probe_mma_f4_tmem_a
 f.restype = C.c_int
 f.argtypes = [C.c_uint32, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
               C.POINTER(C.c_uint32), C.c_void_p]
-for mode, iters in ((0, 1000), (0, (1 << 20) + 3), (1, 1), (2, 200000)):
+for mode, iters in ((0, 1000), (0, (1 << 20) + 3), (1, 1), (2, 200000), (3, 400000)):
     r, ms, bad = C.c_double(), C.c_double(), C.c_uint32()
     d = np.zeros((128, 256), dtype=np.float32)
     st = f(iters, mode, C.byref(r), C.byref(ms), C.byref(bad), d.ctypes.data)
