@@ -76,6 +76,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// One thread of the (converged) warp. Unlike `lane == 0`, ptxas knows that an elect.sync region
+// has a single active thread and feeds tcgen05.mma / commit their uniform-register operands
+// directly; under `if (lane == 0)` it wrapped every MMA in an ELECT / R2UR.BROADCAST / BRA.U.ANY
+// loop (17 SASS per MMA, ~115 clocks of issue per 128-clock MMA: the tensor pipe starved).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(p));
+    return p != 0;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -41,6 +41,7 @@ namespace {
 constexpr int kM = 128;                      // blocks per M tile (= TMEM lanes)
 constexpr int kN = 256;                      // output rows per N tile (= accumulator columns)
 constexpr int kFullArrivals = 8;             // 4 A warps + 4 B warps per stage
+constexpr int kSetsC = 2;                     // producer sets (kSets below)
 constexpr uint32_t kF4StageWords = 16;       // y words per 512-position pipeline stage
 
 // ------------------------------------------------------------------ tcgen05 / cp.async
@@ -372,37 +373,66 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
 // leaf input per K part live in shared memory for all N tiles of the M tile.
 constexpr uint32_t kLeafKpw = 256;                     // 8192 positions per K part
 constexpr uint32_t kLeafStride = kLeafKpw + 4;
-constexpr size_t kLeafSmem = (size_t)kM * kLeafStride * 4 + (1u << kMaxL) * 8 + 16;
+constexpr uint32_t kLeafPieces = 1u << kMaxL;           // input pieces of a leaf, at most
+constexpr size_t kLeafSmem = (size_t)kM * kLeafStride * 4 + 2 * kLeafPieces * 8 + 16;
+constexpr uint32_t kBuildWarps = 8 * kSetsC;            // A and B producer warps of both sets
+
+// Offset (bits) of input piece e of the node `path` at level L (digits base 3, most significant
+// = level 0; 0 = P: x0 ^ x1 doubles the pieces, 1 = Q: x0, 2 = R: x1) — leaf_offsets
+// (split_tree.cuh) in closed form, so that every piece is computed by its own thread. Returns
+// the number of pieces through *n.
+__device__ __forceinline__ uint64_t piece_offset(uint32_t path, uint32_t L, uint64_t k,
+                                                 uint64_t base, uint32_t e, uint32_t* n) {
+    uint32_t pw = 1;
+    for (uint32_t l = 1; l < L; ++l) pw *= 3;
+    uint64_t off = base, m = k;
+    uint32_t np = 0;
+    for (uint32_t l = 0; l < L; ++l, pw /= 3) {
+        m >>= 1;
+        const uint32_t dg = path / pw % 3;
+        if (dg == 2) off += m;
+        if (dg == 0) {
+            if ((e >> np) & 1u) off += m;
+            ++np;
+        }
+    }
+    *n = 1u << np;
+    return off;
+}
 
 // Builds the M tile's leaf inputs for K part d (words [d.st0 * 16, + kpw) of each leaf) into
 // lraw: row jl = XOR over the leaf's input pieces of the original block's reversed input
 // (the k_split_inputs arithmetic, toeplitz_split.cu), zero past the block's padded length and
-// for padding rows. Called by the 8 A producer warps together (named barrier 1, 256 threads).
-__device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, uint32_t aw,
+// for padding rows. Called by all 16 producer warps together (bw = 0..15, named barrier 1,
+// 512 threads): the build is bound by the L2 reads in flight, so the Hankel producers, idle
+// while the tensor pipe waits for the new inputs, carry half of them. nb = builds done so far
+// (the piece offsets are double-buffered, so one barrier covers "last tile's expansions done"
+// and "offsets visible").
+__device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, uint32_t bw,
                                            uint32_t lane, uint32_t* lraw,
-                                           unsigned long long* loff, int* lnoff) {
+                                           unsigned long long* loff2, uint32_t nb) {
     const LeafSrc& q = a.src;
     const uint64_t v0 = (uint64_t)d.mt * kM;  // first virtual block (one group per M tile)
     const uint32_t grp = (uint32_t)(v0 / q.gpad), jl0 = (uint32_t)(v0 % q.gpad);
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // every expansion of the last tile done
-    if (aw == 0 && lane == 0) {
-        uint64_t off[1 << kMaxL];
-        const uint32_t t = grp / q.leaves, path = grp % q.leaves;
-        // parent mode: the input of the children's parent (level L - 1, path / 3)
-        const int n = a.leaf == 2
-                          ? leaf_offsets(path / 3, q.L - 1, q.k, (uint64_t)t * q.k, false, off)
-                          : leaf_offsets(path, q.L, q.k, (uint64_t)t * q.k, false, off);
-        for (int e = 0; e < n; ++e) loff[e] = off[e] / 32;
-        *lnoff = n;
+    const uint32_t t = grp / q.leaves, path = grp % q.leaves;
+    unsigned long long* loff = loff2 + (nb & 1u) * kLeafPieces;
+    // parent mode: the input of the children's parent (level L - 1, path / 3)
+    const uint32_t pL = a.leaf == 2 ? q.L - 1 : q.L, ppath = a.leaf == 2 ? path / 3 : path;
+    uint32_t un = 1;
+    {
+        const uint32_t e = bw * 32 + lane;
+        const uint64_t off = piece_offset(ppath, pL, q.k, (uint64_t)t * q.k, e, &un);
+        if (e < un) loff[e] = off / 32;
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const int n = *lnoff;
+    const int n = (int)un;
+    asm volatile("bar.sync 1, 512;" ::: "memory");  // the last tile's expansions done too
     const uint64_t w0 = (uint64_t)d.st0 * 16;  // K part start (words, a multiple of 16)
     // 16-B loads with many L2 reads outstanding (the build is latency-bound otherwise): per
-    // lane 2 rows x 2 vectors per piece, pieces unrolled by 2; 8 warps x 16 rows
+    // lane 2 rows x 2 vectors per piece, pieces unrolled by 2; 16 warps x 8 rows
     const uint32_t nvec = q.kpw / 4;  // uint4 per row (>= 4: kpw is a multiple of 16 words)
     constexpr int RB = 2;
-    for (uint32_t r0 = aw * 16; r0 < aw * 16 + 16; r0 += RB) {
+    constexpr uint32_t kRows = kM / kBuildWarps;
+    for (uint32_t r0 = bw * kRows; r0 < bw * kRows + kRows; r0 += RB) {
         const uint4* y[RB];
         uint64_t yp4[RB];
 #pragma unroll
@@ -445,8 +475,20 @@ __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, 
                         acc[rr][h];
             }
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    asm volatile("bar.sync 1, 512;" ::: "memory");
 }
+
+#ifdef SSBH_EXP_TRACE  // dev builds: clock64 timestamps of CTA 0's pipeline events for stages
+                       // [kTrG0, kTrG0 + kTrN), printed at kernel end (leaf modes only)
+constexpr uint32_t kTrG0 = 4000, kTrN = 256, kTrRoles = 10;
+#define F4_TRACE(role, g)                                                               \
+    do {                                                                                \
+        if (blockIdx.x == 0 && a.leaf && (g) >= kTrG0 && (g) < kTrG0 + kTrN)             \
+            trace[(role) * kTrN + ((g) - kTrG0)] = clock64();                           \
+    } while (0)
+#else
+#define F4_TRACE(role, g) do { } while (0)
+#endif
 
 // Warp roles: 8 epilogue warps (two per TMEM sub-partition, half of the 256 accumulator
 // columns each: a shorter drain of the single accumulator between work items; 1.4 % faster
@@ -454,7 +496,7 @@ __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, 
 // alternate stages (one set's per-stage chain — cp.async wait -> expand -> STS -> arrive — is
 // latency-bound). Round-1 A/B variants that lost (3 producer sets, register-staged y, 4
 // epilogue warps, double-buffered TMEM loads, a polling MMA warp) are not built.
-constexpr int kSets = 2, kE = 8;
+constexpr int kSets = kSetsC, kE = 8;
 constexpr int kF4Threads = (kE + 1 + 8 * kSets) * 32;
 __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     constexpr int kEpiW = kE, kMmaW = kE, kProd0 = kE + 1;
@@ -474,8 +516,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     // 16-B reads of 8 consecutive rows), and the leaf's input piece offsets (words)
     uint32_t* lraw = reinterpret_cast<uint32_t*>(smem + f4_smem(kSets));
     unsigned long long* loff =
-        reinterpret_cast<unsigned long long*>(lraw + (size_t)kM * kLeafStride);
-    int* lnoff = reinterpret_cast<int*>(loff + (1 << kMaxL));
+        reinterpret_cast<unsigned long long*>(lraw + (size_t)kM * kLeafStride);  // [2][pieces]
+#ifdef SSBH_EXP_TRACE
+    long long* trace = reinterpret_cast<long long*>(loff + 2 * kLeafPieces + 2);
+    for (uint32_t i = threadIdx.x; a.leaf && i < kTrRoles * kTrN; i += blockDim.x) trace[i] = 0;
+#endif
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SSBH_EXP_CLOCK  // dev builds: the SM clock the kernel actually ran at (power cap)
@@ -517,6 +562,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- epilogue
         const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;  // TMEM sub-partition, columns
         uint32_t t = 0;  // accumulation rounds consumed
+#ifdef SSBH_EXP_TRACE
+        uint32_t eg = 0;  // stages before the current item
+#endif
         uint32_t par_w[kQW];  // parent mode: child P's parities of the current N tile
 #pragma unroll
         for (int q = 0; q < kQW; ++q) par_w[q] = 0;
@@ -530,6 +578,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
                 F4_WAIT_T(&tfull[0], t & 1);
                 tc_fence_after();
+#ifdef SSBH_EXP_TRACE
+                if (warp == 0 && lane == 0) F4_TRACE(7, eg);
+#endif
 #ifndef SSBH_EXP_NODRAIN
                 if (d.nst) {
 #else
@@ -547,10 +598,16 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                         uint32_t v[32];
                         SSBH_TMEM_LD32(tmem + ((sp * 32u) << 16) + 32u * (qb + q), v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifdef SSBH_EXP_TRACE
+                        if (warp == 0 && lane == 0 && q == 0) F4_TRACE(8, eg);
+#endif
                         if (q == kQW - 1) {
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&tempty[0]);
+#ifdef SSBH_EXP_TRACE
+                            if (warp == 0 && lane == 0) F4_TRACE(9, eg);
+#endif
                         }
                         acc_w[q] ^= parity16(v, 0) | (parity16(v, 16) << 16);
                     }
@@ -560,6 +617,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     if (lane == 0) mbar_arrive(&tempty[0]);
                 }
             }
+#ifdef SSBH_EXP_TRACE
+            eg += d.nst;
+#endif
             const uint32_t jj = d.mt * kM + sp * 32 + lane;
             if (a.leaf == 2) {
                 // parent mode: the first combine level here — P stays in registers, the parent
@@ -592,6 +652,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
         const uint32_t base_g = smem_u32(slots);
+#ifdef SSBH_EXP_STALL
+        long long exp_wait[3] = {0, 0, 0}, exp_swait[3] = {0, 0, 0}, exp_tw = 0;
+        uint32_t exp_n[3] = {0, 0, 0}, exp_starved[3] = {0, 0, 0};
+#endif
         ItemWalk wk;
         for (wk.start(a); wk.valid; wk.next(a)) {
             const Item d = wk.d;
@@ -602,18 +666,64 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 continue;
             }
             for (uint32_t s0 = 0; s0 < d.nst; s0 += kF4MaxStages, ++t) {
+#ifdef SSBH_EXP_STALL
+                const long long tw0 = clock64();
+#endif
 #ifndef SSBH_EXP_NOTEMPTY
                 if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
 #endif
+#ifdef SSBH_EXP_STALL
+                exp_tw += clock64() - tw0;
+#endif
                 tc_fence_after();
+                if (lane == 0) F4_TRACE(6, g);
                 const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
                 for (uint32_t s = s0; s < s1; ++s, ++g) {
                     const uint32_t slot = g % kS;
+#ifdef SSBH_EXP_STALL  // dev builds: was the tensor pipe already drained when this stage's
+                       // operands arrived, and how long did the issuer wait for them
+                    const int cat = s != s0 ? 0 : (wk.d.nt == 0 && wk.d.child == 0) ? 2 : 1;
+                    bool drained = false;
+                    if (g >= 1) {
+                        uint32_t ok;
+                        asm volatile(
+                            "{\n.reg .pred P1;\n"
+                            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+                            "selp.u32 %0, 1, 0, P1;\n}\n"
+                            : "=r"(ok)
+                            : "r"(smem_u32(&empty[(g - 1) % kS])), "r"(((g - 1) / kS) & 1)
+                            : "memory");
+                        drained = ok != 0;
+                    }
+                    const long long w0c = clock64();
+#endif
                     // hardware-suspended wait: no try_wait polls on the L1 data pipe the
                     // producers' stores and the MMA operand reads share (round 1: 1.1 % faster)
                     F4_WAIT_S(&full[slot], (g / kS) & 1);
+#ifdef SSBH_EXP_STALL
+                    {
+                        const long long dt = clock64() - w0c;
+                        uint32_t ok;
+                        asm volatile(
+                            "{\n.reg .pred P1;\n"
+                            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+                            "selp.u32 %0, 1, 0, P1;\n}\n"
+                            : "=r"(ok)
+                            : "r"(smem_u32(&empty[(g + kS - 1) % kS])),
+                              "r"(g >= 1 ? ((g - 1) / kS) & 1 : 1u)
+                            : "memory");
+                        exp_n[cat] += 1;
+                        exp_wait[cat] += dt;
+                        if (g >= 1 && ok) {  // stage g - 1 complete before g is issued: idle
+                            exp_starved[cat] += 1;
+                            exp_swait[cat] += dt;
+                        }
+                        (void)drained;
+                    }
+#endif
                     tc_fence_after();
-                    if (lane == 0) {
+                    if (lane == 0) F4_TRACE(4, g);
+                    if (elect_one()) {
                         const uint32_t ga = base_g + slot * kF4Slot;
                         const uint32_t at = tmem + kF4ACol0 + 64u * slot;
 #pragma unroll
@@ -624,11 +734,20 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                         }
                         mma_commit(&empty[slot]);
                         if (s + 1 == s1) mma_commit(&tfull[0]);
+                        F4_TRACE(5, g);
                     }
                     __syncwarp();
                 }
             }
         }
+#ifdef SSBH_EXP_STALL
+        if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77) && a.leaf)
+            printf("EXPSTALL cta %u leaf %u: stages mid/item/super %u %u %u; wait clk %lld %lld "
+                   "%lld; starved %u %u %u (wait %lld %lld %lld); tempty wait %lld\n",
+                   blockIdx.x, a.leaf, exp_n[0], exp_n[1], exp_n[2], exp_wait[0], exp_wait[1],
+                   exp_wait[2], exp_starved[0], exp_starved[1], exp_starved[2], exp_swait[0],
+                   exp_swait[1], exp_swait[2], exp_tw);
+#endif
     } else if (((warp - kProd0) & 7) < 4) {
         // ---------------------------------------------------------------- A producers
         const uint32_t set = (warp - kProd0) >> 3;
@@ -670,19 +789,20 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         cur.start(a);
         cur.advance(a, set);
         if (a.leaf) {
-            // both A sets build the super-item's leaf inputs together (named barrier 1 over
-            // the 8 A warps), then expand stages from shared memory
+            // all producer warps build the super-item's leaf inputs together (named barrier
+            // 1), then the A warps expand stages from shared memory
             const uint32_t aw = set * 4 + ((warp - kProd0) & 3);  // 0..7
-            uint32_t built = 0xFFFFFFFFu;
+            uint32_t built = 0xFFFFFFFFu, nbuilt = 0;
             const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
             const uint32_t half = a.src.kpw / 2;  // parent mode: words of the lo half
             for (uint32_t g = set; cur.w.valid; g += kSets, cur.advance(a, kSets)) {
                 const uint32_t sup = cur.w.sup;
                 if (sup != built) {
 #ifndef SSBH_EXP_NOBUILD
-                    leaf_build(a, cur.w.d, aw, lane, lraw, loff, lnoff);
+                    leaf_build(a, cur.w.d, aw, lane, lraw, loff, nbuilt);
 #endif
                     built = sup;
+                    ++nbuilt;
                 }
                 uint4 x[4];
                 const uint32_t* src = lrow + 16u * cur.s;
@@ -707,7 +827,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 }
                 const uint32_t slot = g % kS;
                 if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
+                if (lane == 0 && (warp & 3) == 0) F4_TRACE(0, g);
                 expand(x, slot);
+                if (lane == 0 && (warp & 3) == 0) F4_TRACE(1, g);
             }
         } else {
         pre = cur;
@@ -751,7 +873,15 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             cp_async_commit();
             pre.advance(a, kSets);
         }
+        uint32_t built = 0xFFFFFFFFu, nbuilt = 0;
         for (uint32_t g = set, i = 0; cur.w.valid; g += kSets, ++i, cur.advance(a, kSets)) {
+#ifndef SSBH_EXP_NOBUILD
+            if (a.leaf && cur.w.sup != built) {  // carry half of the leaf-input build
+                leaf_build(a, cur.w.d, 8 + set * 4 + gw, lane, lraw, loff, nbuilt);
+                built = cur.w.sup;
+                ++nbuilt;
+            }
+#endif
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
             __syncwarp();
@@ -761,6 +891,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
+            if (lane == 0 && gw == 0) F4_TRACE(2, g);
             uint8_t* gs = slots + (size_t)slot * kF4Slot;
             // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
             // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position. Unit u + 128 starts 4
@@ -786,6 +917,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
+            if (lane == 0 && gw == 0) F4_TRACE(3, g);
             s_prefetch(a, pre, lane, raw + rs * 32);
             cp_async_commit();
             pre.advance(a, kSets);
@@ -799,6 +931,19 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
+#ifdef SSBH_EXP_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0 && a.leaf) {
+        const long long t00 = trace[4 * kTrN];
+        for (uint32_t i = 0; i < kTrN; ++i)
+            printf("EXPTRACE %u %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", kTrG0 + i,
+                   trace[0 * kTrN + i] - t00, trace[1 * kTrN + i] - t00, trace[2 * kTrN + i] - t00,
+                   trace[3 * kTrN + i] - t00, trace[4 * kTrN + i] - t00, trace[5 * kTrN + i] - t00,
+                   trace[6 * kTrN + i] ? trace[6 * kTrN + i] - t00 : 0,
+                   trace[7 * kTrN + i] ? trace[7 * kTrN + i] - t00 : 0,
+                   trace[8 * kTrN + i] ? trace[8 * kTrN + i] - t00 : 0,
+                   trace[9 * kTrN + i] ? trace[9 * kTrN + i] - t00 : 0);
+    }
+#endif
 #ifdef SSBH_EXP_CLOCK
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         unsigned long long t1;
@@ -1016,7 +1161,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                     mbar_wait(&hfull[slot], (hs / kPbHStages) & 1);
                     tc_fence_after();
                     const uint32_t nst = min((uint32_t)G::sd, steps - sb);
-                    if (lane == 0) {
+                    if (elect_one()) {
                         const uint32_t ha = hbase + slot * G::hbytes;
                         for (uint32_t j = 0; j < nst; ++j) {
                             const uint32_t s = sb + j;
@@ -1231,7 +1376,11 @@ void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
     MmaHashArgs a = a0;
     a.stage_bits = kF4StageK;
+#ifdef SSBH_EXP_TRACE
+    const size_t smem = f4_smem(kSets) + (a.leaf ? kLeafSmem + 8 * kTrRoles * kTrN + 64 : 0);
+#else
     const size_t smem = f4_smem(kSets) + (a.leaf ? kLeafSmem : 0);
+#endif
     cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (a.leaf) {  // super-items of N tiles (x3 children in parent mode); one wave of CTAs
         const uint64_t supers = g.items / (a.leaf == 2 ? 3ull * a.ntiles : a.ntiles);
