@@ -534,6 +534,7 @@ struct ssbh_plan {
     SplitGeom sg{};
     PbGeom pbv{};
     DBuf vs, vy, vout, vrem;
+    DBuf vu;         // GEMM leaves: Hankel unit tables of the leaf seeds
     LayoutBufs vlay, rlay;
     DBuf mt_words;
     DBuf vmt;        // split leaves on the GEMM kernel: max ypad per virtual M tile
@@ -722,6 +723,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         const SplitGeom& g = pl->sg;
         e = alloc(pl->vs,
                   ((g.per_block ? g.nvirt : (size_t)g.T * g.leaves) * g.seed_words + 256) * 4);
+        if (!e && g.gemm) e = alloc(pl->vu, (size_t)g.T * g.leaves * g.unit_stride * 16 + 16);
         // leaf inputs: materialised only for tiled leaves (the leaf GEMM builds its own)
         if (!e && !g.gemm) e = alloc(pl->vy, (size_t)g.nvirt * g.vlw * 4 + 16);
         // leaf outputs (parent mode: level L - 1 nodes, 2/3 of the leaves' bytes)
@@ -991,6 +993,11 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
         const Layout vlay = pl->vlay.view(), rlay = pl->rlay.view();
         launch_split_setup(pl->sbuf.as<uint32_t>(), pl->sbuf_words, g, pl->vs.as<uint32_t>(), lay,
                            pl->nown, vlay, rlay, st);
+        if (g.gemm) {  // the leaf GEMM's B operand: unit tables of the leaf seeds
+            launch_hankel_units(pl->vs.as<uint32_t>(), g.seed_words, (uint64_t)g.T * g.leaves,
+                                g.unit_stride, pl->vu.as<uint32_t>(), st);
+            launches += 1;
+        }
         CU(cudaMemsetAsync(pl->vrem.p, 0, pl->vrem.bytes, st));
         if (g.gemm) {  // shared seed: the remainders are one short GEMM (seed offset T k)
             MmaHashArgs r{};
@@ -1048,6 +1055,8 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 v.src.jj0 = jj0;
                 v.src.nown = pl->nown;
                 v.src.seed_words = g.seed_words;
+                v.units = pl->vu.as<uint32_t>();
+                v.unit_stride = g.unit_stride;
                 v.src.kpw = leaf_parent_mode(g) ? (uint32_t)(2 * g.sL / 32)
                                                 : (uint32_t)(g.sL / 32 / pl->mmv.ksplit);
                 v.sbuf = pl->vs.as<uint32_t>();

@@ -231,6 +231,9 @@ struct MmaHashArgs {
     uint64_t items;
     uint32_t* mt_words;      // [mtiles] device scratch: max ypad per M tile
     uint32_t stage_bits;     // input positions per pipeline stage (set by launch_hash_mma)
+    const uint32_t* units;   // leaf modes: Hankel unit tables (launch_hankel_units), 4 words
+                             // per unit, unit_stride units per leaf seed
+    unsigned long long unit_stride;
     uint32_t leaf;           // 1: leaf mode (src below; items walked N tile innermost per
                              // (M tile, K part); ksplit = K parts); 2: parent mode — a CTA
                              // keeps one M tile of a level L-1 node's input and runs its three
@@ -278,6 +281,7 @@ struct SplitGeom {
                              // virtual block v = (t * leaves + path) * gpad + jl
     uint64_t vlw;            // u32 words per leaf input (sL / 32, 16-aligned for gemm)
     uint64_t bytes;          // leaf inputs + outputs + seeds one batch allocates
+    uint64_t unit_stride;    // GEMM leaves: Hankel units per leaf seed (leaf_unit_stride)
 };
 uint32_t split_levels(uint64_t k, bool gemm);  // 0 = not worth it
 SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t L,
@@ -303,6 +307,14 @@ uint32_t mma_mtiles(uint32_t nown);
 MmaGeom make_leaf_geom(uint32_t nvirt, uint32_t lw, int device, bool parent);
 MmaGeom make_mma_geom(uint32_t nown, uint32_t kw, uint64_t mean_nj, int device);
 void launch_hash_mma(const MmaHashArgs& a, const MmaGeom& g, cudaStream_t st);
+// Hankel unit tables of `regions` leaf seeds (seed_words pre-shifted words each at d_vs): unit G
+// word j = (S' >> (G + 32 j)) & 0x22222222, unit_stride units (16 B) per region.
+void launch_hankel_units(const uint32_t* d_vs, uint64_t seed_words, uint64_t regions,
+                         uint64_t unit_stride, uint32_t* d_units, cudaStream_t st);
+// units per leaf seed region the leaf GEMM reads (N tiles of 256 rows x stages of 512 positions)
+inline uint64_t leaf_unit_stride(uint64_t sL, uint64_t vlw) {
+    return ((sL + 255) / 256 * 256 + vlw * 32 + 131 + 7) / 8 * 8;
+}
 
 // Concatenate nown blocks of k bits (block stride kw words) into key (bit offset jj*k).
 void launch_concat(const uint32_t* d_blocks, uint32_t kw, uint32_t nown, uint64_t k,

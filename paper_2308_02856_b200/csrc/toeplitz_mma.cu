@@ -127,12 +127,15 @@ struct Item {
     uint32_t st0, nst;   // stage range [st0, st0 + nst) of this K part
     uint64_t soff;       // seed offset (u32 words) of the M tile's first block: 0 for a plan's
                          // shared seed; the split's leaf groups (128-aligned) each have their own
+    uint64_t uoff;       // leaf modes: first unit of the M tile's leaf group in the Hankel unit
+                         // tables (k_hankel_units)
 };
 
 __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item& d) {
     if (item >= a.items) return false;
     d.nt = item % a.ntiles;
     d.child = 0;
+    d.uoff = 0;
     if (a.leaf == 2) {
         // item = ((parent group * mpg + M tile in group) * 3 + child) * ntiles + nt
         const uint32_t c3 = item / a.ntiles;
@@ -201,6 +204,7 @@ struct ItemWalk {
             d.nst = (uint32_t)((uint64_t)ns * (kp + 1) / a.ksplit) - d.st0;
         }
         d.soff = a.lay.soff[(uint64_t)d.mt * kM];
+        d.uoff = (uint64_t)(d.mt / (a.src.gpad / kM)) * a.unit_stride;
     }
     __device__ __forceinline__ void start(const MmaHashArgs& a) {
         sup = blockIdx.x;
@@ -214,11 +218,13 @@ struct ItemWalk {
             if (++d.child < 3) {
                 d.mt += mpg;
                 d.soff += a.src.seed_words;
+                d.uoff += a.unit_stride;
                 return;
             }
             d.child = 0;
             d.mt -= 2 * mpg;
             d.soff -= 2 * a.src.seed_words;
+            d.uoff -= 2 * a.unit_stride;
             if (++d.nt < a.ntiles) return;
         } else if (a.leaf) {
             if (++d.nt < a.ntiles) return;
@@ -408,6 +414,7 @@ __device__ __forceinline__ uint64_t piece_offset(uint32_t path, uint32_t L, uint
 // while the tensor pipe waits for the new inputs, carry half of them. nb = builds done so far
 // (the piece offsets are double-buffered, so one barrier covers "last tile's expansions done"
 // and "offsets visible").
+template <int kBW>
 __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, uint32_t bw,
                                            uint32_t lane, uint32_t* lraw,
                                            unsigned long long* loff2, uint32_t nb) {
@@ -425,13 +432,13 @@ __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, 
         if (e < un) loff[e] = off / 32;
     }
     const int n = (int)un;
-    asm volatile("bar.sync 1, 512;" ::: "memory");  // the last tile's expansions done too
+    asm volatile("bar.sync 1, %0;" ::"n"(kBW * 32) : "memory");  // last tile's expansions done
     const uint64_t w0 = (uint64_t)d.st0 * 16;  // K part start (words, a multiple of 16)
     // 16-B loads with many L2 reads outstanding (the build is latency-bound otherwise): per
     // lane 2 rows x 2 vectors per piece, pieces unrolled by 2; 16 warps x 8 rows
     const uint32_t nvec = q.kpw / 4;  // uint4 per row (>= 4: kpw is a multiple of 16 words)
     constexpr int RB = 2;
-    constexpr uint32_t kRows = kM / kBuildWarps;
+    constexpr uint32_t kRows = kM / kBW;
     for (uint32_t r0 = bw * kRows; r0 < bw * kRows + kRows; r0 += RB) {
         const uint4* y[RB];
         uint64_t yp4[RB];
@@ -475,12 +482,12 @@ __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, 
                         acc[rr][h];
             }
     }
-    asm volatile("bar.sync 1, 512;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kBW * 32) : "memory");
 }
 
 #ifdef SSBH_EXP_TRACE  // dev builds: clock64 timestamps of CTA 0's pipeline events for stages
                        // [kTrG0, kTrG0 + kTrN), printed at kernel end (leaf modes only)
-constexpr uint32_t kTrG0 = 4000, kTrN = 256, kTrRoles = 10;
+constexpr uint32_t kTrG0 = 4000, kTrN = 128, kTrRoles = 10;
 #define F4_TRACE(role, g)                                                               \
     do {                                                                                \
         if (blockIdx.x == 0 && a.leaf && (g) >= kTrG0 && (g) < kTrG0 + kTrN)             \
@@ -799,7 +806,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 const uint32_t sup = cur.w.sup;
                 if (sup != built) {
 #ifndef SSBH_EXP_NOBUILD
-                    leaf_build(a, cur.w.d, aw, lane, lraw, loff, nbuilt);
+                    leaf_build<kBuildWarps>(a, cur.w.d, aw, lane, lraw, loff, nbuilt);
 #endif
                     built = sup;
                     ++nbuilt;
@@ -877,7 +884,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         for (uint32_t g = set, i = 0; cur.w.valid; g += kSets, ++i, cur.advance(a, kSets)) {
 #ifndef SSBH_EXP_NOBUILD
             if (a.leaf && cur.w.sup != built) {  // carry half of the leaf-input build
-                leaf_build(a, cur.w.d, 8 + set * 4 + gw, lane, lraw, loff, nbuilt);
+                leaf_build<kBuildWarps>(a, cur.w.d, 8 + set * 4 + gw, lane, lraw, loff, nbuilt);
                 built = cur.w.sup;
                 ++nbuilt;
             }
@@ -954,6 +961,351 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                (double)(c1 - exp_c0) * 1e3 / (double)(t1 - exp_t0));
     }
 #endif
+}
+
+// =========================================================================================
+// The split's shared-seed leaves (leaf / parent mode) as their own kernel, k_leaf_gemm. Same
+// product, operand layouts and item order as k_toeplitz_f4's leaf mode, re-plumbed after the
+// pipeline trace of round 2 (profiles/r02_ab_leaf_gemm.md):
+//  * the Hankel operand comes from a precomputed table of units (k_hankel_units: for every leaf
+//    seed, unit G word j = the seed window at bit G + 32 j masked to the E2M1 1.0 bit). A stage's
+//    643 units are consecutive there, so the B tile is ONE 10 KB bulk copy (cp.async.bulk
+//    completing on the stage's mbarrier) issued by one thread — no funnel shifts, no shared
+//    loads / stores by eight producer warps, which were the last to arrive at every stage;
+//  * B has its own ring (kLfBS slots of shared memory, deep enough for the copy latency), the A
+//    operand keeps its 3-stage ring in TMEM;
+//  * 16 epilogue warps (four per TMEM sub-partition, 64 accumulator columns each): the hand-off
+//    of the single accumulator between items is two TMEM loads per warp instead of four.
+constexpr int kLfBS = 8;                    // B ring (Hankel unit tiles, shared memory)
+constexpr int kLfAS = 3;                    // A ring (TMEM, 64 columns per stage)
+constexpr int kLfEW = 16;                   // epilogue warps
+constexpr int kLfAW = 8;                    // A producer warps: 2 sets of 4 (one per sub-partition)
+constexpr int kLfMmaW = kLfEW, kLfLoadW = kLfEW + 1, kLfProd0 = kLfEW + 2;
+constexpr int kLfThreads = (kLfEW + 2 + kLfAW) * 32;
+constexpr size_t kLfBar =
+    (size_t)kLfBS * kF4Slot + (size_t)kM * kLeafStride * 4 + 2 * kLeafPieces * 8;
+constexpr size_t kLfSmem = kLfBar + (2 * kLfAS + 2 * kLfBS + 4) * 8 + 16;
+static_assert(kLfSmem <= 232448, "leaf GEMM smem budget");
+constexpr uint32_t kLfTileBytes = kF4GUnits * 16;  // one stage's Hankel units
+
+// Hankel unit tables: region r (a leaf seed of seed_words pre-shifted words at vs), unit G,
+// word j = (S' >> (G + 32 j)) & 0x22222222 — what the B producers of k_toeplitz_f4 form per
+// stage (unit u of the stage at N tile nt, stage st is G = 256 nt + 512 st + u).
+__global__ void __launch_bounds__(256) k_hankel_units(const uint32_t* __restrict__ vs,
+                                                      uint64_t seed_words, uint64_t unit_stride,
+                                                      uint4* __restrict__ units) {
+    const uint64_t r = blockIdx.y;
+    const uint32_t* sw = vs + r * seed_words;
+    for (uint64_t G = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; G < unit_stride;
+         G += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = G >> 5;
+        const uint32_t sh = (uint32_t)G & 31u;
+        uint32_t w[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) w[j] = q + j < seed_words ? __ldg(sw + q + j) : 0u;
+        constexpr uint32_t M2 = 0x22222222u;
+        units[r * unit_stride + G] =
+            make_uint4(__funnelshift_r(w[0], w[1], sh) & M2, __funnelshift_r(w[1], w[2], sh) & M2,
+                       __funnelshift_r(w[2], w[3], sh) & M2, __funnelshift_r(w[3], w[4], sh) & M2);
+    }
+}
+
+__global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
+    constexpr uint32_t M2 = 0x22222222u;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* bslots = smem;
+    uint32_t* lraw = reinterpret_cast<uint32_t*>(smem + (size_t)kLfBS * kF4Slot);
+    unsigned long long* loff =
+        reinterpret_cast<unsigned long long*>(lraw + (size_t)kM * kLeafStride);  // [2][pieces]
+    uint64_t* afull = reinterpret_cast<uint64_t*>(smem + kLfBar);
+    uint64_t* aempty = afull + kLfAS;
+    uint64_t* bfull = aempty + kLfAS;
+    uint64_t* bempty = bfull + kLfBS;
+    uint64_t* tfull = bempty + kLfBS;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+#ifdef SSBH_EXP_TRACE
+    long long* trace = reinterpret_cast<long long*>(smem + kLfSmem);
+    for (uint32_t i = threadIdx.x; i < kTrRoles * kTrN; i += blockDim.x) trace[i] = 0;
+#endif
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kLfAS; ++s) {
+            mbar_init(&afull[s], 4);
+            mbar_init(&aempty[s], 1);
+        }
+        for (int s = 0; s < kLfBS; ++s) {
+            mbar_init(&bfull[s], 1);
+            mbar_init(&bempty[s], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tempty[0], kLfEW);
+        fence_barrier_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) {  // constant scale factors: 0x7f = 2^0 in every byte
+        uint32_t v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0x7F7F7F7Fu;
+        SSBH_TMEM_ST32(tmem + ((warp * 32u) << 16) + kF4SfCol, v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp < kLfEW) {
+        // ---------------------------------------------------------------- epilogue
+        constexpr int kQW = (kN / 32) / (kLfEW / 4);  // 32-column groups per warp (2)
+        const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;
+        uint32_t t = 0;
+#ifdef SSBH_EXP_TRACE
+        uint32_t eg = 0;
+#endif
+        uint32_t par_w[kQW];  // parent mode: child P's parities of the current N tile
+#pragma unroll
+        for (int q = 0; q < kQW; ++q) par_w[q] = 0;
+        ItemWalk wk;
+        for (wk.start(a); wk.valid; wk.next(a)) {
+            const Item d = wk.d;
+            uint32_t acc_w[kQW];
+#pragma unroll
+            for (int q = 0; q < kQW; ++q) acc_w[q] = 0;
+            F4_WAIT_T(&tfull[0], t & 1);
+            ++t;
+            tc_fence_after();
+            if (warp == 0 && lane == 0) F4_TRACE(7, eg);
+            if (d.nst) {
+                // the accumulator is released as soon as this warp's last TMEM load has landed
+#pragma unroll
+                for (int q = 0; q < kQW; ++q) {
+                    uint32_t v[32];
+                    SSBH_TMEM_LD32(tmem + ((sp * 32u) << 16) + 32u * (qb + q), v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (warp == 0 && lane == 0 && q == 0) F4_TRACE(8, eg);
+                    if (q == kQW - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[0]);
+                        if (warp == 0 && lane == 0) F4_TRACE(9, eg);
+                    }
+                    acc_w[q] = parity16(v, 0) | (parity16(v, 16) << 16);
+                }
+            } else {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[0]);
+            }
+#ifdef SSBH_EXP_TRACE
+            eg += d.nst;
+#endif
+            const uint32_t jj = d.mt * kM + sp * 32 + lane;
+            if (a.leaf == 2) {
+                // parent mode: the first combine level here — P stays in registers, the parent
+                // node's rows are [P ^ Q | P ^ R] (row = parent M tile row, a.kw words per half)
+                if (d.child == 0) {
+#pragma unroll
+                    for (int q = 0; q < kQW; ++q) par_w[q] = acc_w[q];
+                } else if (d.nst && jj < a.nown) {
+                    uint32_t* dst = a.out +
+                                    (unsigned long long)(wk.sup * kM + sp * 32 + lane) * a.out_stride +
+                                    (d.child - 1) * a.kw + d.nt * (kN / 32) + qb;
+#pragma unroll
+                    for (int q = 0; q < kQW; ++q)
+                        if (d.nt * (kN / 32) + qb + q < a.kw) dst[q] = acc_w[q] ^ par_w[q];
+                }
+            } else if (d.nst && jj < a.nown) {
+                uint32_t* dst =
+                    a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32) + qb;
+#pragma unroll
+                for (int q = 0; q < kQW; ++q)
+                    if (d.nt * (kN / 32) + qb + q < a.kw) {
+                        if (a.ksplit == 1)
+                            dst[q] = acc_w[q];
+                        else
+                            atomicXor(dst + q, acc_w[q]);
+                    }
+            }
+        }
+    } else if (warp == kLfMmaW) {
+        // ---------------------------------------------------------------- MMA issuer
+        uint32_t t = 0;
+#ifdef SSBH_EXP_TRACE
+        uint32_t g = 0;
+#endif
+        uint32_t sa = 0, pa = 0, sb = 0, pb = 0;  // ring slots and their phases
+        const uint32_t base_b = smem_u32(bslots);
+        ItemWalk wk;
+        for (wk.start(a); wk.valid; wk.next(a)) {
+            const uint32_t nst = wk.d.nst;
+            if (nst == 0) {
+                if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
+                ++t;
+                if (lane == 0) mbar_arrive(&tfull[0]);
+                continue;
+            }
+            // the first stage's operands are ready long before the accumulator is handed back:
+            // their barrier round trips stay off the hand-off path
+            F4_WAIT_S(&afull[sa], pa);
+            F4_WAIT_S(&bfull[sb], pb);
+            if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
+            ++t;
+            tc_fence_after();
+            if (lane == 0) F4_TRACE(6, g);
+            for (uint32_t s = 0; s < nst; ++s) {
+                if (s) {
+                    F4_WAIT_S(&afull[sa], pa);
+                    F4_WAIT_S(&bfull[sb], pb);
+                    tc_fence_after();
+                }
+                if (lane == 0) F4_TRACE(4, g);
+                if (elect_one()) {
+                    const uint32_t gb = base_b + sb * kF4Slot;
+                    const uint32_t at = tmem + kF4ACol0 + 64u * sa;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {  // MMA m: chunks 2m, 2m+1 = columns 8m..
+                        const uint32_t unit = 2u * (m & 1) + 128u * (m >> 1);
+                        mma_f4_ts(tmem, at + 8u * m, sdesc(gb + 16u * unit, 16, 128),
+                                  tmem + kF4SfCol, (s | (uint32_t)m) != 0);
+                    }
+                    mma_commit(&aempty[sa]);
+                    mma_commit(&bempty[sb]);
+                    if (s + 1 == nst) mma_commit(&tfull[0]);
+                }
+                __syncwarp();
+                if (lane == 0) F4_TRACE(5, g);
+#ifdef SSBH_EXP_TRACE
+                ++g;
+#endif
+                if (++sa == kLfAS) {
+                    sa = 0;
+                    pa ^= 1;
+                }
+                if (++sb == kLfBS) {
+                    sb = 0;
+                    pb ^= 1;
+                }
+            }
+        }
+    } else if (warp == kLfLoadW) {
+        // ---------------------------------------------------------------- B loader
+        uint32_t sb = 0, pb = 1;  // waits for the slot's previous use: phase of (use - 1)
+        uint32_t g = 0;
+        StageIt cur;
+        for (cur.start(a); cur.w.valid; cur.next(a), ++g) {
+            if (g >= (uint32_t)kLfBS) F4_WAIT_S(&bempty[sb], pb);
+            if (lane == 0) F4_TRACE(2, g);
+            if (elect_one()) {
+                const uint64_t G0 = (uint64_t)cur.w.d.nt * kN +
+                                    (uint64_t)(cur.w.d.st0 + cur.s) * kF4StageK;
+                mbar_arrive_expect_tx(&bfull[sb], kLfTileBytes);
+                bulk_g2s(bslots + (size_t)sb * kF4Slot, a.units + (cur.w.d.uoff + G0) * 4,
+                         kLfTileBytes, &bfull[sb]);
+            }
+            __syncwarp();
+            if (lane == 0) F4_TRACE(3, g);
+            if (++sb == kLfBS) {
+                sb = 0;
+                pb ^= 1;
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- A producers
+        const uint32_t aw = warp - kLfProd0, set = aw >> 2;
+        // TMEM lane = block row: a warp reaches the 32 lanes of its sub-partition (warp % 4)
+        const uint32_t jl = 32u * (warp & 3) + lane;
+        const uint32_t lane_addr = (32u * (warp & 3)) << 16;
+        StageIt cur;
+        cur.start(a);
+        cur.advance(a, set);
+        uint32_t built = 0xFFFFFFFFu, nbuilt = 0;
+        const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
+        const uint32_t half = a.src.kpw / 2;  // parent mode: words of the lo half
+        for (uint32_t g = set; cur.w.valid; g += 2, cur.advance(a, 2)) {
+            if (cur.w.sup != built) {
+                leaf_build<kLfAW>(a, cur.w.d, aw, lane, lraw, loff, nbuilt);
+                built = cur.w.sup;
+                ++nbuilt;
+            }
+            uint4 x[4];
+            const uint32_t* src = lrow + 16u * cur.s;
+            if (a.leaf == 2 && cur.w.d.child != 1) {
+                // P = lo ^ hi, R = hi (Q = lo reads the lo half as a leaf would)
+                const uint32_t* hi = src + half;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    uint4 u = *reinterpret_cast<const uint4*>(hi + 4 * h);
+                    if (cur.w.d.child == 0) {
+                        const uint4 l = *reinterpret_cast<const uint4*>(src + 4 * h);
+                        u.x ^= l.x;
+                        u.y ^= l.y;
+                        u.z ^= l.z;
+                        u.w ^= l.w;
+                    }
+                    x[h] = u;
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) x[h] = *reinterpret_cast<const uint4*>(src + 4 * h);
+            }
+            const uint32_t slot = g % kLfAS;
+            if (g >= (uint32_t)kLfAS) F4_WAIT_S(&aempty[slot], ((g / kLfAS) - 1) & 1);
+            if (lane == 0 && (aw & 3) == 0) F4_TRACE(0, g);
+            // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0; chunk
+            // q = 4 gg + kc, word w -> column 4 q + w of the stage
+            const uint32_t ta = tmem + lane_addr + kF4ACol0 + 64u * slot;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // columns 32h .. 32h + 31: chunks 8h .. 8h + 7
+                uint32_t v[32];
+#pragma unroll
+                for (int g2 = 0; g2 < 2; ++g2) {
+                    const uint4 xg = x[2 * h + g2];
+#pragma unroll
+                    for (int kc = 0; kc < 4; ++kc) {
+                        auto f = [&](uint32_t u) { return (kc ? u >> (kc - 1) : u << 1) & M2; };
+                        v[16 * g2 + 4 * kc + 0] = f(xg.x);
+                        v[16 * g2 + 4 * kc + 1] = f(xg.y);
+                        v[16 * g2 + 4 * kc + 2] = f(xg.z);
+                        v[16 * g2 + 4 * kc + 3] = f(xg.w);
+                    }
+                }
+                SSBH_TMEM_ST32(ta + 32u * h, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afull[slot]);
+            if (lane == 0 && (aw & 3) == 0) F4_TRACE(1, g);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+#ifdef SSBH_EXP_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const long long t00 = trace[4 * kTrN];
+        for (uint32_t i = 0; i < kTrN; ++i) {
+            printf("EXPTRACE %u", kTrG0 + i);
+            for (uint32_t r = 0; r < kTrRoles; ++r)
+                printf(" %lld", trace[r * kTrN + i] ? trace[r * kTrN + i] - t00 : 0);
+            printf("\n");
+        }
+    }
+#endif
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
 }
 
 // =========================================================================================
@@ -1370,23 +1722,39 @@ void launch_hash_mma_pb(const PbHashArgs& a0, const PbGeom& g, cudaStream_t st) 
     k_toeplitz_mma_pb<<<grid, kPbThreads, PbGeo::smem, st>>>(a);
 }
 
+void launch_hankel_units(const uint32_t* d_vs, uint64_t seed_words, uint64_t regions,
+                         uint64_t unit_stride, uint32_t* d_units, cudaStream_t st) {
+    if (!regions) return;
+    const unsigned gx = (unsigned)std::min<uint64_t>((unit_stride + 255) / 256, 64);
+    for (uint64_t r0 = 0; r0 < regions; r0 += 65535) {
+        const unsigned gy = (unsigned)std::min<uint64_t>(regions - r0, 65535);
+        k_hankel_units<<<dim3(gx, gy), 256, 0, st>>>(
+            d_vs + r0 * seed_words, seed_words, unit_stride,
+            reinterpret_cast<uint4*>(d_units) + r0 * unit_stride);
+    }
+}
+
 void launch_hash_mma(const MmaHashArgs& a0, const MmaGeom& g, cudaStream_t st) {
     if (!a0.nown || !g.items) return;
     k_mma_tiles<<<g.mtiles, kM, 0, st>>>(a0.lay.ypad, a0.nown, a0.mt_words);
     const unsigned grid = (unsigned)std::min<uint64_t>(g.grid, g.items);
     MmaHashArgs a = a0;
     a.stage_bits = kF4StageK;
-#ifdef SSBH_EXP_TRACE
-    const size_t smem = f4_smem(kSets) + (a.leaf ? kLeafSmem + 8 * kTrRoles * kTrN + 64 : 0);
-#else
-    const size_t smem = f4_smem(kSets) + (a.leaf ? kLeafSmem : 0);
-#endif
-    cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (a.leaf) {  // super-items of N tiles (x3 children in parent mode); one wave of CTAs
         const uint64_t supers = g.items / (a.leaf == 2 ? 3ull * a.ntiles : a.ntiles);
-        k_toeplitz_f4<<<(unsigned)std::min<uint64_t>(g.grid, supers), kF4Threads, smem, st>>>(a);
+        cudaFuncSetAttribute(k_leaf_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kLfSmem);
+#ifdef SSBH_EXP_TRACE
+        const size_t lsm = kLfSmem + 8 * kTrRoles * kTrN;
+        cudaFuncSetAttribute(k_leaf_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+        k_leaf_gemm<<<(unsigned)std::min<uint64_t>(g.grid, supers), kLfThreads, lsm, st>>>(a);
+#else
+        k_leaf_gemm<<<(unsigned)std::min<uint64_t>(g.grid, supers), kLfThreads, kLfSmem, st>>>(a);
+#endif
         return;
     }
+    const size_t smem = f4_smem(kSets);
+    cudaFuncSetAttribute(k_toeplitz_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_toeplitz_f4<<<grid, kF4Threads, smem, st>>>(a);
 }
 

@@ -290,7 +290,10 @@ SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t 
     const uint64_t per_blk = (uint64_t)g.T * g.leaves *
                              ((g.gemm ? 0 : g.vlw * 4) + g.sL / 8 +
                               (per_block ? g.seed_words * 4 : 0));
-    const uint64_t fixed = per_block ? 0 : (uint64_t)g.T * g.leaves * g.seed_words * 4;
+    // + for GEMM leaves the Hankel unit tables (16 B per unit, leaf_unit_stride units per seed)
+    g.unit_stride = g.gemm ? leaf_unit_stride(g.sL, g.vlw) : 0;
+    const uint64_t fixed =
+        per_block ? 0 : (uint64_t)g.T * g.leaves * (g.seed_words * 4 + g.unit_stride * 16);
     const uint64_t avail = budget_bytes > fixed ? budget_bytes - fixed : 0;
     uint64_t b = std::max<uint64_t>(1, std::min<uint64_t>(nown, avail / per_blk));
     if (g.gemm && b < nown) b = std::max<uint64_t>(128, b / 128 * 128);
