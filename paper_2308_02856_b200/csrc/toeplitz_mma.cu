@@ -84,6 +84,16 @@ __device__ __forceinline__ void cp_async_wait() {
           "=r"(v[31])                                                                            \
         : "r"(taddr))
 
+// Compiler-level fence on 32 registers: later uses of v cannot be scheduled above this point.
+#define SSBH_REG_FENCE32(v)                                                                      \
+    asm volatile(""                                                                              \
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),       \
+                   "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),     \
+                   "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), \
+                   "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]), \
+                   "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), \
+                   "+r"(v[30]), "+r"(v[31])::"memory")
+
 #define SSBH_TMEM_ST32(taddr, v)                                                                 \
     asm volatile(                                                                                \
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"   \
@@ -124,6 +134,7 @@ __device__ __forceinline__ uint32_t parity16(const uint32_t (&v)[32], int o) {
 struct Item {
     uint32_t mt, nt;     // M tile (128 owned blocks), N tile (256 output rows)
     uint32_t child;      // parent mode: 0 = P (lo ^ hi), 1 = Q (lo), 2 = R (hi)
+    uint32_t ph;         // parent mode: phase of the super-item, 0 = Q, 1 = P, 2 = R
     uint32_t st0, nst;   // stage range [st0, st0 + nst) of this K part
     uint64_t soff;       // seed offset (u32 words) of the M tile's first block: 0 for a plan's
                          // shared seed; the split's leaf groups (128-aligned) each have their own
@@ -135,6 +146,7 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
     if (item >= a.items) return false;
     d.nt = item % a.ntiles;
     d.child = 0;
+    d.ph = 0;
     d.uoff = 0;
     if (a.leaf == 2) {
         // item = ((parent group * mpg + M tile in group) * 3 + child) * ntiles + nt
@@ -165,8 +177,8 @@ __device__ __forceinline__ bool decode(const MmaHashArgs& a, uint32_t item, Item
 
 // A CTA's item sequence. Direct mode: items blockIdx.x, +grid, ..., each decoded on its own.
 // Leaf modes: super-items (leaf: M tile x K part; parent mode: the parent's M tile with its
-// three children, child fastest) blockIdx.x, +grid, ..., whose N tiles follow each other while
-// the M tile's leaf inputs stay in shared memory. Everything but the N tile (and the child) is decoded once
+// three children, one child after the other) blockIdx.x, +grid, ..., whose N tiles follow each
+// other while the M tile's leaf inputs stay in shared memory. Everything but the N tile (and the child) is decoded once
 // per super-item: the per-item decode (five divisions and two layout loads, in every warp) was
 // ~1100 clocks of tensor-pipe bubble per item (skeleton A/B, profiles/r02_ab_leaf_gemm.md).
 __device__ __forceinline__ uint32_t super_items(const MmaHashArgs& a) {
@@ -185,15 +197,17 @@ struct ItemWalk {
         if (!valid) return;
         d.nt = 0;
         d.child = 0;
+        d.ph = 0;
         if (a.leaf == 2) {
             // super-item = parent group * mpg + M tile in the group; child c is leaf group
-            // t * leaves + 3 * pp + c, whose M tiles lie mpg further and whose seed region
-            // follows the previous child's (k_split_layout: soff = group * seed words)
+            // t * leaves + 3 * pp + c, whose M tiles lie c * mpg further and whose seed region /
+            // unit table follow the previous child's. The phases run Q, P, R (see next()).
             const uint32_t mpg = a.src.gpad / kM;
             const uint32_t pg = sup / mpg, mtl = sup % mpg;
             const uint32_t pleaves = a.src.leaves / 3;
             const uint32_t t = pg / pleaves, pp = pg % pleaves;
-            d.mt = (t * a.src.leaves + 3 * pp) * mpg + mtl;
+            d.child = 1;
+            d.mt = (t * a.src.leaves + 3 * pp + 1) * mpg + mtl;
             d.st0 = 0;
             d.nst = a.mt_words[d.mt] / (kF4StageWords);  // the same rows in all three children
         } else {
@@ -212,20 +226,29 @@ struct ItemWalk {
     }
     __device__ __forceinline__ void next(const MmaHashArgs& a) {
         if (a.leaf == 2) {
-            // N tile by N tile, the three children P, Q, R of each in turn: the epilogue keeps
-            // P's parities in registers and writes the parent's rows P ^ Q and P ^ R
+            // child by child in the order Q (reads the lo half of the parent's input), P (lo ^
+            // hi), R (hi): while R runs the lo half is free for the next parent's input, and
+            // while the next Q runs so is the hi half — the epilogue warps build them in the
+            // background (k_leaf_gemm)
+            if (++d.nt < a.ntiles) return;
+            d.nt = 0;
             const uint32_t mpg = a.src.gpad / kM;
-            if (++d.child < 3) {
-                d.mt += mpg;
-                d.soff += a.src.seed_words;
-                d.uoff += a.unit_stride;
+            if (d.ph == 0) {  // Q -> P
+                d.ph = 1;
+                d.child = 0;
+                d.mt -= mpg;
+                d.soff -= a.src.seed_words;
+                d.uoff -= a.unit_stride;
                 return;
             }
-            d.child = 0;
-            d.mt -= 2 * mpg;
-            d.soff -= 2 * a.src.seed_words;
-            d.uoff -= 2 * a.unit_stride;
-            if (++d.nt < a.ntiles) return;
+            if (d.ph == 1) {  // P -> R
+                d.ph = 2;
+                d.child = 2;
+                d.mt += 2 * mpg;
+                d.soff += 2 * a.src.seed_words;
+                d.uoff += 2 * a.unit_stride;
+                return;
+            }
         } else if (a.leaf) {
             if (++d.nt < a.ntiles) return;
         }
@@ -375,13 +398,41 @@ __device__ __forceinline__ void y_prefetch_f4(const MmaHashArgs& a, const StageI
     for (int h = 0; h < 4; ++h) cp_async16(raw + h * kM * 4, src + 4 * h, bytes);
 }
 
+__device__ __forceinline__ void red_xor(uint32_t* p, uint32_t v) {
+    asm volatile("red.global.xor.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// A operand of one stage: the row's 512 y bits (x: 16 words) as E2M1 nibbles into the 64 TMEM
+// columns at ta. ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0;
+// chunk q = 4 gg + kc, word w -> column 4 q + w of the stage.
+__device__ __forceinline__ void expand_a(const uint4 (&x)[4], uint32_t ta) {
+    constexpr uint32_t M2 = 0x22222222u;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // columns 32h .. 32h + 31: chunks 8h .. 8h + 7
+        uint32_t v[32];
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2) {
+            const uint4 xg = x[2 * h + g2];
+#pragma unroll
+            for (int kc = 0; kc < 4; ++kc) {
+                auto f = [&](uint32_t u) { return (kc ? u >> (kc - 1) : u << 1) & M2; };
+                v[16 * g2 + 4 * kc + 0] = f(xg.x);
+                v[16 * g2 + 4 * kc + 1] = f(xg.y);
+                v[16 * g2 + 4 * kc + 2] = f(xg.z);
+                v[16 * g2 + 4 * kc + 3] = f(xg.w);
+            }
+        }
+        SSBH_TMEM_ST32(ta + 32u * h, v);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // Leaf mode (the split's shared-seed leaves): kLeafKpw words of each of the 128 virtual blocks'
 // leaf input per K part live in shared memory for all N tiles of the M tile.
 constexpr uint32_t kLeafKpw = 256;                     // 8192 positions per K part
 constexpr uint32_t kLeafStride = kLeafKpw + 4;
 constexpr uint32_t kLeafPieces = 1u << kMaxL;           // input pieces of a leaf, at most
 constexpr size_t kLeafSmem = (size_t)kM * kLeafStride * 4 + 2 * kLeafPieces * 8 + 16;
-constexpr uint32_t kBuildWarps = 8 * kSetsC;            // A and B producer warps of both sets
 
 // Offset (bits) of input piece e of the node `path` at level L (digits base 3, most significant
 // = level 0; 0 = P: x0 ^ x1 doubles the pieces, 1 = Q: x0, 2 = R: x1) — leaf_offsets
@@ -498,10 +549,11 @@ constexpr uint32_t kTrG0 = 4000, kTrN = 128, kTrRoles = 10;
 #endif
 
 // Warp roles: 8 epilogue warps (two per TMEM sub-partition, half of the 256 accumulator
-// columns each: a shorter drain of the single accumulator between work items; 1.4 % faster
-// than 4 in round 1), 1 MMA warp, then two producer sets of 4 A + 4 B warps that fill
-// alternate stages (one set's per-stage chain — cp.async wait -> expand -> STS -> arrive — is
-// latency-bound). Round-1 A/B variants that lost (3 producer sets, register-staged y, 4
+// columns each), 1 MMA warp (one elected thread issues), then two producer sets of 4 A + 4 B
+// warps that fill alternate stages (one set's per-stage chain — cp.async wait -> expand ->
+// tcgen05.st / STS -> arrive — is latency-bound). Direct mode only: whole blocks against a
+// plan's shared seed (configs 1-2) and the split's remainder; the split's leaves run on
+// k_leaf_gemm below. Round-1 A/B variants that lost (3 producer sets, register-staged y, 4
 // epilogue warps, double-buffered TMEM loads, a polling MMA warp) are not built.
 constexpr int kSets = kSetsC, kE = 8;
 constexpr int kF4Threads = (kE + 1 + 8 * kSets) * 32;
@@ -519,22 +571,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
     uint64_t* tfull = empty + kS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    // leaf mode: the M tile's leaf inputs, row stride kLeafStride words (+4: conflict-free
-    // 16-B reads of 8 consecutive rows), and the leaf's input piece offsets (words)
-    uint32_t* lraw = reinterpret_cast<uint32_t*>(smem + f4_smem(kSets));
-    unsigned long long* loff =
-        reinterpret_cast<unsigned long long*>(lraw + (size_t)kM * kLeafStride);  // [2][pieces]
-#ifdef SSBH_EXP_TRACE
-    long long* trace = reinterpret_cast<long long*>(loff + 2 * kLeafPieces + 2);
-    for (uint32_t i = threadIdx.x; a.leaf && i < kTrRoles * kTrN; i += blockDim.x) trace[i] = 0;
-#endif
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef SSBH_EXP_CLOCK  // dev builds: the SM clock the kernel actually ran at (power cap)
-    const long long exp_c0 = clock64();
-    unsigned long long exp_t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(exp_t0));
-#endif
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], kFullArrivals);
@@ -569,12 +607,6 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- epilogue
         const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;  // TMEM sub-partition, columns
         uint32_t t = 0;  // accumulation rounds consumed
-#ifdef SSBH_EXP_TRACE
-        uint32_t eg = 0;  // stages before the current item
-#endif
-        uint32_t par_w[kQW];  // parent mode: child P's parities of the current N tile
-#pragma unroll
-        for (int q = 0; q < kQW; ++q) par_w[q] = 0;
         ItemWalk wk;
         for (wk.start(a); wk.valid; wk.next(a)) {
             const Item d = wk.d;
@@ -585,36 +617,19 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             for (uint32_t rd = 0; rd < rounds; ++rd, ++t) {
                 F4_WAIT_T(&tfull[0], t & 1);
                 tc_fence_after();
-#ifdef SSBH_EXP_TRACE
-                if (warp == 0 && lane == 0) F4_TRACE(7, eg);
-#endif
-#ifndef SSBH_EXP_NODRAIN
                 if (d.nst) {
-#else
-                if (false) {
-#endif
-                    // The hand-off of the single accumulator is serial with the MMAs (about
-                    // 770 clocks per item at the start of round 2's session 4), so the warp
-                    // releases the accumulator as soon as its last TMEM load has landed and
-                    // only then reduces that load (parity16: independent funnel-shift chains
-                    // instead of one 32-long dependent LOP3 chain).
-                    // (16-column loads double-buffered against the reduction measured slower:
-                    // hash 25.53 -> 26.05 ms.)
+                    // The hand-off of the single accumulator is serial with the MMAs, so the
+                    // warp releases it as soon as its last TMEM load has landed and only then
+                    // reduces that load (parity16: independent funnel-shift chains).
 #pragma unroll 1
                     for (int q = 0; q < kQW; ++q) {
                         uint32_t v[32];
                         SSBH_TMEM_LD32(tmem + ((sp * 32u) << 16) + 32u * (qb + q), v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#ifdef SSBH_EXP_TRACE
-                        if (warp == 0 && lane == 0 && q == 0) F4_TRACE(8, eg);
-#endif
                         if (q == kQW - 1) {
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&tempty[0]);
-#ifdef SSBH_EXP_TRACE
-                            if (warp == 0 && lane == 0) F4_TRACE(9, eg);
-#endif
                         }
                         acc_w[q] ^= parity16(v, 0) | (parity16(v, 16) << 16);
                     }
@@ -624,25 +639,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     if (lane == 0) mbar_arrive(&tempty[0]);
                 }
             }
-#ifdef SSBH_EXP_TRACE
-            eg += d.nst;
-#endif
             const uint32_t jj = d.mt * kM + sp * 32 + lane;
-            if (a.leaf == 2) {
-                // parent mode: the first combine level here — P stays in registers, the parent
-                // node's rows are [P ^ Q | P ^ R] (row = parent M tile row, a.kw words per half)
-                if (d.child == 0) {
-#pragma unroll
-                    for (int q = 0; q < kQW; ++q) par_w[q] = acc_w[q];
-                } else if (d.nst && jj < a.nown) {
-                    uint32_t* dst = a.out +
-                                    (unsigned long long)(wk.sup * kM + sp * 32 + lane) * a.out_stride +
-                                    (d.child - 1) * a.kw + d.nt * (kN / 32) + qb;
-#pragma unroll
-                    for (int q = 0; q < kQW; ++q)
-                        if (d.nt * (kN / 32) + qb + q < a.kw) dst[q] = acc_w[q] ^ par_w[q];
-                }
-            } else if (d.nst && jj < a.nown) {
+            if (d.nst && jj < a.nown) {
                 uint32_t* dst =
                     a.out + (unsigned long long)jj * a.out_stride + d.nt * (kN / 32) + qb;
 #pragma unroll
@@ -659,10 +657,6 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         // ---------------------------------------------------------------- MMA issuer
         uint32_t g = 0, t = 0;
         const uint32_t base_g = smem_u32(slots);
-#ifdef SSBH_EXP_STALL
-        long long exp_wait[3] = {0, 0, 0}, exp_swait[3] = {0, 0, 0}, exp_tw = 0;
-        uint32_t exp_n[3] = {0, 0, 0}, exp_starved[3] = {0, 0, 0};
-#endif
         ItemWalk wk;
         for (wk.start(a); wk.valid; wk.next(a)) {
             const Item d = wk.d;
@@ -673,63 +667,15 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 continue;
             }
             for (uint32_t s0 = 0; s0 < d.nst; s0 += kF4MaxStages, ++t) {
-#ifdef SSBH_EXP_STALL
-                const long long tw0 = clock64();
-#endif
-#ifndef SSBH_EXP_NOTEMPTY
                 if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
-#endif
-#ifdef SSBH_EXP_STALL
-                exp_tw += clock64() - tw0;
-#endif
                 tc_fence_after();
-                if (lane == 0) F4_TRACE(6, g);
                 const uint32_t s1 = min(d.nst, s0 + kF4MaxStages);
                 for (uint32_t s = s0; s < s1; ++s, ++g) {
                     const uint32_t slot = g % kS;
-#ifdef SSBH_EXP_STALL  // dev builds: was the tensor pipe already drained when this stage's
-                       // operands arrived, and how long did the issuer wait for them
-                    const int cat = s != s0 ? 0 : (wk.d.nt == 0 && wk.d.child == 0) ? 2 : 1;
-                    bool drained = false;
-                    if (g >= 1) {
-                        uint32_t ok;
-                        asm volatile(
-                            "{\n.reg .pred P1;\n"
-                            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-                            "selp.u32 %0, 1, 0, P1;\n}\n"
-                            : "=r"(ok)
-                            : "r"(smem_u32(&empty[(g - 1) % kS])), "r"(((g - 1) / kS) & 1)
-                            : "memory");
-                        drained = ok != 0;
-                    }
-                    const long long w0c = clock64();
-#endif
                     // hardware-suspended wait: no try_wait polls on the L1 data pipe the
                     // producers' stores and the MMA operand reads share (round 1: 1.1 % faster)
                     F4_WAIT_S(&full[slot], (g / kS) & 1);
-#ifdef SSBH_EXP_STALL
-                    {
-                        const long long dt = clock64() - w0c;
-                        uint32_t ok;
-                        asm volatile(
-                            "{\n.reg .pred P1;\n"
-                            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-                            "selp.u32 %0, 1, 0, P1;\n}\n"
-                            : "=r"(ok)
-                            : "r"(smem_u32(&empty[(g + kS - 1) % kS])),
-                              "r"(g >= 1 ? ((g - 1) / kS) & 1 : 1u)
-                            : "memory");
-                        exp_n[cat] += 1;
-                        exp_wait[cat] += dt;
-                        if (g >= 1 && ok) {  // stage g - 1 complete before g is issued: idle
-                            exp_starved[cat] += 1;
-                            exp_swait[cat] += dt;
-                        }
-                        (void)drained;
-                    }
-#endif
                     tc_fence_after();
-                    if (lane == 0) F4_TRACE(4, g);
                     if (elect_one()) {
                         const uint32_t ga = base_g + slot * kF4Slot;
                         const uint32_t at = tmem + kF4ACol0 + 64u * slot;
@@ -741,109 +687,22 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                         }
                         mma_commit(&empty[slot]);
                         if (s + 1 == s1) mma_commit(&tfull[0]);
-                        F4_TRACE(5, g);
                     }
                     __syncwarp();
                 }
             }
         }
-#ifdef SSBH_EXP_STALL
-        if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77) && a.leaf)
-            printf("EXPSTALL cta %u leaf %u: stages mid/item/super %u %u %u; wait clk %lld %lld "
-                   "%lld; starved %u %u %u (wait %lld %lld %lld); tempty wait %lld\n",
-                   blockIdx.x, a.leaf, exp_n[0], exp_n[1], exp_n[2], exp_wait[0], exp_wait[1],
-                   exp_wait[2], exp_starved[0], exp_starved[1], exp_starved[2], exp_swait[0],
-                   exp_swait[1], exp_swait[2], exp_tw);
-#endif
     } else if (((warp - kProd0) & 7) < 4) {
         // ---------------------------------------------------------------- A producers
         const uint32_t set = (warp - kProd0) >> 3;
         // TMEM lane = block row: a warp reaches the 32 lanes of its sub-partition (warp % 4)
         const uint32_t jl = 32u * (warp & 3) + lane;
         const uint32_t lane_addr = (32u * (warp & 3)) << 16;
-        // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0; chunk
-        // q = 4 gg + kc, word w -> column 4 q + w of the stage
-        auto expand = [&](const uint4 (&x)[4], uint32_t slot) {
-            const uint32_t ta = tmem + lane_addr + kF4ACol0 + 64u * slot;
-#ifndef SSBH_EXP_NOAPROD
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {  // columns 32h .. 32h + 31: chunks 8h .. 8h + 7
-                uint32_t v[32];
-#pragma unroll
-                for (int g2 = 0; g2 < 2; ++g2) {
-                    const uint4 xg = x[2 * h + g2];
-#pragma unroll
-                    for (int kc = 0; kc < 4; ++kc) {
-                        auto f = [&](uint32_t u) { return (kc ? u >> (kc - 1) : u << 1) & M2; };
-                        v[16 * g2 + 4 * kc + 0] = f(xg.x);
-                        v[16 * g2 + 4 * kc + 1] = f(xg.y);
-                        v[16 * g2 + 4 * kc + 2] = f(xg.z);
-                        v[16 * g2 + 4 * kc + 3] = f(xg.w);
-                    }
-                }
-                SSBH_TMEM_ST32(ta + 32u * h, v);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-#else
-            (void)x;
-            (void)ta;
-#endif
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[slot]);
-        };
         StageIt cur, pre;
         cur.start(a);
         cur.advance(a, set);
-        if (a.leaf) {
-            // all producer warps build the super-item's leaf inputs together (named barrier
-            // 1), then the A warps expand stages from shared memory
-            const uint32_t aw = set * 4 + ((warp - kProd0) & 3);  // 0..7
-            uint32_t built = 0xFFFFFFFFu, nbuilt = 0;
-            const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
-            const uint32_t half = a.src.kpw / 2;  // parent mode: words of the lo half
-            for (uint32_t g = set; cur.w.valid; g += kSets, cur.advance(a, kSets)) {
-                const uint32_t sup = cur.w.sup;
-                if (sup != built) {
-#ifndef SSBH_EXP_NOBUILD
-                    leaf_build<kBuildWarps>(a, cur.w.d, aw, lane, lraw, loff, nbuilt);
-#endif
-                    built = sup;
-                    ++nbuilt;
-                }
-                uint4 x[4];
-                const uint32_t* src = lrow + 16u * cur.s;
-                if (a.leaf == 2 && cur.w.d.child != 1) {
-                    // P = lo ^ hi, R = hi (Q = lo reads the lo half as a leaf would)
-                    const uint32_t* hi = src + half;
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        uint4 u = *reinterpret_cast<const uint4*>(hi + 4 * h);
-                        if (cur.w.d.child == 0) {
-                            const uint4 l = *reinterpret_cast<const uint4*>(src + 4 * h);
-                            u.x ^= l.x;
-                            u.y ^= l.y;
-                            u.z ^= l.z;
-                            u.w ^= l.w;
-                        }
-                        x[h] = u;
-                    }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) x[h] = *reinterpret_cast<const uint4*>(src + 4 * h);
-                }
-                const uint32_t slot = g % kS;
-                if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
-                if (lane == 0 && (warp & 3) == 0) F4_TRACE(0, g);
-                expand(x, slot);
-                if (lane == 0 && (warp & 3) == 0) F4_TRACE(1, g);
-            }
-        } else {
         pre = cur;
         uint32_t* raw = raw_y + set * (kF4RawY / 4) + jl * 4;  // [slot][quarter][jl][4 words]
-#ifdef SSBH_EXP_NOYLOAD
-        pre.w.valid = false;
-#endif
         for (int i = 0; i < kF4Pre; ++i) {
             y_prefetch_f4(a, pre, jl, raw + i * kM * 16);
             cp_async_commit();
@@ -858,13 +717,15 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                 x[h] = *reinterpret_cast<const uint4*>(raw + rs * kM * 16 + h * kM * 4);
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
-            expand(x, slot);
+            expand_a(x, tmem + lane_addr + kF4ACol0 + 64u * slot);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[slot]);
             y_prefetch_f4(a, pre, jl, raw + rs * kM * 16);
             cp_async_commit();
             pre.advance(a, kSets);
         }
         cp_async_wait<0>();
-        }
     } else {
         // ---------------------------------------------------------------- B producers
         const uint32_t set = (warp - kProd0) >> 3;
@@ -880,15 +741,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             cp_async_commit();
             pre.advance(a, kSets);
         }
-        uint32_t built = 0xFFFFFFFFu, nbuilt = 0;
         for (uint32_t g = set, i = 0; cur.w.valid; g += kSets, ++i, cur.advance(a, kSets)) {
-#ifndef SSBH_EXP_NOBUILD
-            if (a.leaf && cur.w.sup != built) {  // carry half of the leaf-input build
-                leaf_build<kBuildWarps>(a, cur.w.d, 8 + set * 4 + gw, lane, lraw, loff, nbuilt);
-                built = cur.w.sup;
-                ++nbuilt;
-            }
-#endif
             const uint32_t rs = i % kF4Pre;
             cp_async_wait<kF4Pre - 1>();
             __syncwarp();
@@ -898,13 +751,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
             const uint32_t rel0 = (uint32_t)(b1 - (((b1 >> 5) & ~3ull) << 5));
             const uint32_t slot = g % kS;
             if (g >= (uint32_t)kS) F4_WAIT_S(&empty[slot], ((g / kS) - 1) & 1);
-            if (lane == 0 && gw == 0) F4_TRACE(2, g);
             uint8_t* gs = slots + (size_t)slot * kF4Slot;
             // the window one bit lower (rel0 >= 1: base is a multiple of 256) has S bit
             // base + u + 32w + 4i at bit 4i + 1 — the E2M1 1.0 position. Unit u + 128 starts 4
             // words later with the same shift, so its first word is this unit's last: 4 shared
-            // loads per unit instead of 5 (the L1 data pipe is the leaf GEMM's contended resource)
-#ifndef SSBH_EXP_NOBPROD
+            // loads per unit instead of 5
             const uint32_t rel = rel0 + gt - 1;
             const uint32_t q0 = rel >> 5, sh = rel & 31;
             uint32_t w0 = sw[q0];
@@ -920,11 +771,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
                     w0 = w4;
                 }
             }
-#endif
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
-            if (lane == 0 && gw == 0) F4_TRACE(3, g);
             s_prefetch(a, pre, lane, raw + rs * 32);
             cp_async_commit();
             pre.advance(a, kSets);
@@ -938,53 +787,41 @@ __global__ void __launch_bounds__(kF4Threads, 1) k_toeplitz_f4(MmaHashArgs a) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
-#ifdef SSBH_EXP_TRACE
-    if (threadIdx.x == 0 && blockIdx.x == 0 && a.leaf) {
-        const long long t00 = trace[4 * kTrN];
-        for (uint32_t i = 0; i < kTrN; ++i)
-            printf("EXPTRACE %u %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", kTrG0 + i,
-                   trace[0 * kTrN + i] - t00, trace[1 * kTrN + i] - t00, trace[2 * kTrN + i] - t00,
-                   trace[3 * kTrN + i] - t00, trace[4 * kTrN + i] - t00, trace[5 * kTrN + i] - t00,
-                   trace[6 * kTrN + i] ? trace[6 * kTrN + i] - t00 : 0,
-                   trace[7 * kTrN + i] ? trace[7 * kTrN + i] - t00 : 0,
-                   trace[8 * kTrN + i] ? trace[8 * kTrN + i] - t00 : 0,
-                   trace[9 * kTrN + i] ? trace[9 * kTrN + i] - t00 : 0);
-    }
-#endif
-#ifdef SSBH_EXP_CLOCK
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        const long long c1 = clock64();
-        printf("EXPCLOCK k_toeplitz_f4 leaf=%u items=%llu ns=%llu MHz=%.1f\n", a.leaf,
-               (unsigned long long)a.items, t1 - exp_t0,
-               (double)(c1 - exp_c0) * 1e3 / (double)(t1 - exp_t0));
-    }
-#endif
 }
 
 // =========================================================================================
 // The split's shared-seed leaves (leaf / parent mode) as their own kernel, k_leaf_gemm. Same
-// product, operand layouts and item order as k_toeplitz_f4's leaf mode, re-plumbed after the
-// pipeline trace of round 2 (profiles/r02_ab_leaf_gemm.md):
+// product and operand layouts as k_toeplitz_f4, re-plumbed after the pipeline trace of round 2
+// (profiles/r02_ab_leaf_gemm.md):
 //  * the Hankel operand comes from a precomputed table of units (k_hankel_units: for every leaf
 //    seed, unit G word j = the seed window at bit G + 32 j masked to the E2M1 1.0 bit). A stage's
 //    643 units are consecutive there, so the B tile is ONE 10 KB bulk copy (cp.async.bulk
 //    completing on the stage's mbarrier) issued by one thread — no funnel shifts, no shared
 //    loads / stores by eight producer warps, which were the last to arrive at every stage;
 //  * B has its own ring (kLfBS slots of shared memory, deep enough for the copy latency), the A
-//    operand keeps its 3-stage ring in TMEM;
-//  * 16 epilogue warps (four per TMEM sub-partition, 64 accumulator columns each): the hand-off
-//    of the single accumulator between items is two TMEM loads per warp instead of four.
+//    operand keeps its 3-stage ring in TMEM, filled by 4 warps (one per TMEM sub-partition);
+//  * 16 epilogue warps (four per TMEM sub-partition, 64 accumulator columns each): a shorter
+//    hand-off of the single accumulator between items;
+//  * parent mode runs a parent's children in the order Q, P, R (ItemWalk) and kLfBW build warps
+//    prepare the NEXT inputs in the background: the next parent's lo half while R runs (which
+//    reads hi only), its hi half while its Q runs (which reads lo only). (Building from the
+//    epilogue warps between hand-offs made them late for the next hand-off: 22.5 -> 36 ms.)
+//    The first combine level stays fused: the parent's rows are written as lo = Q, then
+//    lo ^= P and hi = P, then hi ^= R by the same thread.
 constexpr int kLfBS = 8;                    // B ring (Hankel unit tiles, shared memory)
 constexpr int kLfAS = 3;                    // A ring (TMEM, 64 columns per stage)
 constexpr int kLfEW = 16;                   // epilogue warps
-constexpr int kLfAW = 8;                    // A producer warps: 2 sets of 4 (one per sub-partition)
+constexpr int kLfAW = 4;                    // A producer warps: sets of 4 (one per sub-partition)
+constexpr int kLfSets = kLfAW / 4;          // a set fills every kLfSets-th stage
+constexpr int kLfBW = 4;                    // background-build warps (parent mode); 8 build in
+                                            // time for every parent but cap the CTA at 64
+                                            // registers per thread (25.1 ms against 22.4)
 constexpr int kLfMmaW = kLfEW, kLfLoadW = kLfEW + 1, kLfProd0 = kLfEW + 2;
-constexpr int kLfThreads = (kLfEW + 2 + kLfAW) * 32;
+constexpr int kLfBuild0 = kLfProd0 + kLfAW;
+constexpr int kLfThreads = (kLfEW + 2 + kLfAW + kLfBW) * 32;
 constexpr size_t kLfBar =
     (size_t)kLfBS * kF4Slot + (size_t)kM * kLeafStride * 4 + 2 * kLeafPieces * 8;
-constexpr size_t kLfSmem = kLfBar + (2 * kLfAS + 2 * kLfBS + 4) * 8 + 16;
+constexpr size_t kLfSmem = kLfBar + (2 * kLfAS + 2 * kLfBS + 8) * 8 + 16;
 static_assert(kLfSmem <= 232448, "leaf GEMM smem budget");
 constexpr uint32_t kLfTileBytes = kF4GUnits * 16;  // one stage's Hankel units
 
@@ -1010,8 +847,76 @@ __global__ void __launch_bounds__(256) k_hankel_units(const uint32_t* __restrict
     }
 }
 
+// Parent mode, background build: rows [r0, r1) of super-item `sup`'s M tile, half h (0 = lo,
+// 1 = hi) of the parent's input -> lraw. Row = XOR over the parent's input pieces of the
+// original block's reversed input (piece e: base + the P levels' sizes selected by e's bits),
+// zero past the block's padded length and for padding rows; one uint4 per lane per piece,
+// kBuildInFlight pieces in flight. Variants measured (profiles/r02_ab_leaf_gemm.md): the
+// epilogue warps building between hand-offs (late for the next hand-off), one warp through the
+// bulk-copy engine (~300 clocks per 512-byte copy) and warps staging pieces with cp.async (slower
+// per piece than register loads) all lose to dedicated warps with plain loads.
+constexpr int kBuildInFlight = 8;
+constexpr uint32_t kLfBRows = kM / kLfBW;          // rows of the M tile per build warp
+__device__ __forceinline__ void build_half_rows(const MmaHashArgs& a, uint32_t sup, uint32_t h,
+                                                uint32_t r0, uint32_t r1, uint32_t lane,
+                                                uint32_t* lraw) {
+    const LeafSrc& q = a.src;
+    const uint32_t mpg = q.gpad / kM, pleaves = q.leaves / 3;
+    const uint32_t pg = sup / mpg, jl0 = (sup % mpg) * kM;
+    const uint32_t t = pg / pleaves, pp = pg % pleaves;
+    const uint32_t hw = q.kpw / 2;  // words per half (= the leaf size)
+    uint32_t mP[kMaxL];             // sizes (words) of the levels whose digit is P
+    uint32_t np = 0;
+    uint64_t base = (uint64_t)t * (q.k / 32) + (uint64_t)h * hw;
+    {
+        uint32_t pw = 1;
+        for (uint32_t l = 2; l < q.L; ++l) pw *= 3;
+        uint64_t m = q.k / 32;
+#pragma unroll
+        for (int l = 0; l < kMaxL - 1; ++l) {
+            if ((uint32_t)l + 1 < q.L) {
+                m >>= 1;
+                const uint32_t dg = pp / pw % 3;
+                pw /= 3;
+                if (dg == 2) base += m;
+                if (dg == 0) mP[np++] = (uint32_t)m;
+            }
+        }
+    }
+    const uint32_t n = 1u << np;
+    const bool lane_on = lane < hw / 4;
+    for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t jlg = jl0 + r, jj = q.jj0 + jlg;
+        const bool live = lane_on && jlg < q.batch && jj < q.nown;
+        const uint4* y = reinterpret_cast<const uint4*>(live ? q.ybuf + q.lay.yoff[jj] : q.ybuf);
+        const uint64_t yp4 = live ? q.lay.ypad[jj] / 4 : 0;  // ypad is a multiple of 32 words
+        uint4 acc = make_uint4(0, 0, 0, 0);
+        for (uint32_t e0 = 0; e0 < n; e0 += kBuildInFlight) {
+            uint4 v[kBuildInFlight];
+#pragma unroll
+            for (int i = 0; i < kBuildInFlight; ++i) {
+                const uint32_t e = e0 + i;
+                uint64_t off = base;
+#pragma unroll
+                for (int b = 0; b < kMaxL - 1; ++b)
+                    if ((uint32_t)b < np && ((e >> b) & 1u)) off += mP[b];
+                const uint64_t qv = off / 4 + lane;
+                v[i] = e < n && qv < yp4 ? __ldg(y + qv) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int i = 0; i < kBuildInFlight; ++i) {
+                acc.x ^= v[i].x;
+                acc.y ^= v[i].y;
+                acc.z ^= v[i].z;
+                acc.w ^= v[i].w;
+            }
+        }
+        if (lane_on)
+            *reinterpret_cast<uint4*>(lraw + (size_t)r * kLeafStride + h * hw + 4u * lane) = acc;
+    }
+}
+
 __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
-    constexpr uint32_t M2 = 0x22222222u;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* bslots = smem;
     uint32_t* lraw = reinterpret_cast<uint32_t*>(smem + (size_t)kLfBS * kF4Slot);
@@ -1023,13 +928,20 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
     uint64_t* bempty = bfull + kLfBS;
     uint64_t* tfull = bempty + kLfBS;
     uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // parent mode: the halves of the parent's input — free (the A warps have read the last
+    // stage that uses it) and ready (the 16 build warps have written the next one)
+    uint64_t* lo_free = tempty + 1;
+    uint64_t* hi_free = lo_free + 1;
+    uint64_t* lo_ready = hi_free + 1;
+    uint64_t* hi_ready = lo_ready + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hi_ready + 2);
 #ifdef SSBH_EXP_TRACE
     long long* trace = reinterpret_cast<long long*>(smem + kLfSmem);
     for (uint32_t i = threadIdx.x; i < kTrRoles * kTrN; i += blockDim.x) trace[i] = 0;
 #endif
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nsupers = (uint32_t)(a.items / super_items(a));
     if (threadIdx.x == 0) {
         for (int s = 0; s < kLfAS; ++s) {
             mbar_init(&afull[s], 4);
@@ -1041,6 +953,10 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
         }
         mbar_init(&tfull[0], 1);
         mbar_init(&tempty[0], kLfEW);
+        mbar_init(lo_free, kLfAW);
+        mbar_init(hi_free, kLfAW);
+        mbar_init(lo_ready, kLfBW);
+        mbar_init(hi_ready, kLfBW);
         fence_barrier_init();
     }
     if (warp == 0) {
@@ -1065,42 +981,61 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
     tc_fence_after();
 
     if (warp < kLfEW) {
-        // ---------------------------------------------------------------- epilogue
+        // ---------------------------------------------------------------- epilogue + builds
         constexpr int kQW = (kN / 32) / (kLfEW / 4);  // 32-column groups per warp (2)
         const uint32_t sp = warp & 3, qb = (warp >> 2) * kQW;
         uint32_t t = 0;
 #ifdef SSBH_EXP_TRACE
         uint32_t eg = 0;
 #endif
-        uint32_t par_w[kQW];  // parent mode: child P's parities of the current N tile
-#pragma unroll
-        for (int q = 0; q < kQW; ++q) par_w[q] = 0;
         ItemWalk wk;
-        for (wk.start(a); wk.valid; wk.next(a)) {
+        wk.start(a);
+        for (; wk.valid; wk.next(a)) {
             const Item d = wk.d;
-            uint32_t acc_w[kQW];
-#pragma unroll
-            for (int q = 0; q < kQW; ++q) acc_w[q] = 0;
             F4_WAIT_T(&tfull[0], t & 1);
             ++t;
             tc_fence_after();
             if (warp == 0 && lane == 0) F4_TRACE(7, eg);
+            uint32_t acc_w[kQW];
+#pragma unroll
+            for (int q = 0; q < kQW; ++q) acc_w[q] = 0;
+#ifndef SSBH_EXP_NODRAIN
             if (d.nst) {
-                // the accumulator is released as soon as this warp's last TMEM load has landed
+#else
+            if (false) {
+#endif
+#ifndef SSBH_EXP_DRAIN2  // one load at a time (32 registers)
+                const uint32_t tcol = tmem + ((sp * 32u) << 16) + 32u * qb;
 #pragma unroll
                 for (int q = 0; q < kQW; ++q) {
                     uint32_t v[32];
-                    SSBH_TMEM_LD32(tmem + ((sp * 32u) << 16) + 32u * (qb + q), v);
+                    SSBH_TMEM_LD32(tcol + 32u * q, v);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (warp == 0 && lane == 0 && q == 0) F4_TRACE(8, eg);
                     if (q == kQW - 1) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[0]);
-                        if (warp == 0 && lane == 0) F4_TRACE(9, eg);
                     }
                     acc_w[q] = parity16(v, 0) | (parity16(v, 16) << 16);
                 }
+#else
+                // dev A/B: both loads in flight (64 registers: no gain measured, 20.94 vs 21.00 ms)
+                uint32_t v0[32], v1[32];
+                const uint32_t tcol = tmem + ((sp * 32u) << 16) + 32u * qb;
+                SSBH_TMEM_LD32(tcol, v0);
+                SSBH_TMEM_LD32(tcol + 32u, v1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (warp == 0 && lane == 0) F4_TRACE(8, eg);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[0]);
+                if (warp == 0 && lane == 0) F4_TRACE(9, eg);
+                // the reduction must not be scheduled ahead of the release
+                SSBH_REG_FENCE32(v0);
+                SSBH_REG_FENCE32(v1);
+                acc_w[0] = parity16(v0, 0) | (parity16(v0, 16) << 16);
+                acc_w[1] = parity16(v1, 0) | (parity16(v1, 16) << 16);
+#endif
             } else {
                 tc_fence_before();
                 __syncwarp();
@@ -1111,18 +1046,29 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
 #endif
             const uint32_t jj = d.mt * kM + sp * 32 + lane;
             if (a.leaf == 2) {
-                // parent mode: the first combine level here — P stays in registers, the parent
-                // node's rows are [P ^ Q | P ^ R] (row = parent M tile row, a.kw words per half)
-                if (d.child == 0) {
-#pragma unroll
-                    for (int q = 0; q < kQW; ++q) par_w[q] = acc_w[q];
-                } else if (d.nst && jj < a.nown) {
-                    uint32_t* dst = a.out +
-                                    (unsigned long long)(wk.sup * kM + sp * 32 + lane) * a.out_stride +
-                                    (d.child - 1) * a.kw + d.nt * (kN / 32) + qb;
+                // the first combine level: the parent node's rows [P ^ Q | P ^ R] (row = parent
+                // M tile row, a.kw words per half) in three steps by the same thread
+                if (d.nst && jj < a.nown) {
+                    uint32_t* lo = a.out +
+                                   (unsigned long long)(wk.sup * kM + sp * 32 + lane) * a.out_stride +
+                                   d.nt * (kN / 32) + qb;
+                    uint32_t* hi = lo + a.kw;
 #pragma unroll
                     for (int q = 0; q < kQW; ++q)
-                        if (d.nt * (kN / 32) + qb + q < a.kw) dst[q] = acc_w[q] ^ par_w[q];
+                        if (d.nt * (kN / 32) + qb + q < a.kw) {
+                            // XOR by red.global (fire and forget, ordered after this thread's
+                            // earlier store to the word): a load-modify-store here put 1024
+                            // scattered L2 reads per item into the L1 miss queue, behind which
+                            // the A and MMA warps' shared-memory operations stalled
+                            if (d.ph == 0) {
+                                lo[q] = acc_w[q];
+                            } else if (d.ph == 1) {
+                                red_xor(lo + q, acc_w[q]);
+                                hi[q] = acc_w[q];
+                            } else {
+                                red_xor(hi + q, acc_w[q]);
+                            }
+                        }
                 }
             } else if (d.nst && jj < a.nown) {
                 uint32_t* dst =
@@ -1158,7 +1104,9 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
             // their barrier round trips stay off the hand-off path
             F4_WAIT_S(&afull[sa], pa);
             F4_WAIT_S(&bfull[sb], pb);
+#ifndef SSBH_EXP_NOTEMPTY
             if (t >= 1) F4_WAIT_T(&tempty[0], (t - 1) & 1);
+#endif
             ++t;
             tc_fence_after();
             if (lane == 0) F4_TRACE(6, g);
@@ -1219,6 +1167,53 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
                 pb ^= 1;
             }
         }
+    } else if (warp >= kLfBuild0) {
+        // ---------------------------------------------------------------- background builds
+        // Parent mode: the next parent's lo half while R runs (free once the A warps are
+        // through P), its hi half while its Q runs (free once they are through the previous R).
+        // Driven by the half barriers alone.
+#ifndef SSBH_EXP_NOBUILD
+        if (a.leaf == 2) {
+            const uint32_t row0 = (warp - kLfBuild0) * kLfBRows;
+            uint32_t seq = 0;
+#ifdef SSBH_EXP_BSTAT
+            long long tb = 0, tw = 0;
+#endif
+            for (uint32_t sup = blockIdx.x; sup < nsupers; sup += gridDim.x, ++seq) {
+#ifdef SSBH_EXP_BSTAT
+                long long c0 = clock64();
+#endif
+                if (seq) F4_WAIT_T(lo_free, (seq - 1) & 1);
+#ifdef SSBH_EXP_BSTAT
+                long long c1 = clock64();
+                tw += c1 - c0;
+#endif
+                build_half_rows(a, sup, 0, row0, row0 + kLfBRows, lane, lraw);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(lo_ready);
+#ifdef SSBH_EXP_BSTAT
+                c0 = clock64();
+                tb += c0 - c1;
+#endif
+                if (seq) F4_WAIT_T(hi_free, (seq - 1) & 1);
+#ifdef SSBH_EXP_BSTAT
+                c1 = clock64();
+                tw += c1 - c0;
+#endif
+                build_half_rows(a, sup, 1, row0, row0 + kLfBRows, lane, lraw);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(hi_ready);
+#ifdef SSBH_EXP_BSTAT
+                tb += clock64() - c1;
+#endif
+            }
+#ifdef SSBH_EXP_BSTAT
+            if (lane == 0 && blockIdx.x < 2)
+                printf("EXPBSTAT cta %u: supers %u build clk %lld wait-free clk %lld\n",
+                       blockIdx.x, seq, tb, tw);
+#endif
+        }
+#endif
     } else {
         // ---------------------------------------------------------------- A producers
         const uint32_t aw = warp - kLfProd0, set = aw >> 2;
@@ -1228,15 +1223,42 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
         StageIt cur;
         cur.start(a);
         cur.advance(a, set);
-        uint32_t built = 0xFFFFFFFFu, nbuilt = 0;
+        uint32_t built = 0xFFFFFFFFu, nbuilt = 0;           // leaf mode: foreground builds
+        uint32_t seq = 0, cur_sup = 0xFFFFFFFFu, cur_ph = 0;  // parent mode: phase hand-shakes
+#ifdef SSBH_EXP_BSTAT
+        long long exp_wr = 0;
+#endif
         const uint32_t* lrow = lraw + (size_t)jl * kLeafStride;
         const uint32_t half = a.src.kpw / 2;  // parent mode: words of the lo half
-        for (uint32_t g = set; cur.w.valid; g += 2, cur.advance(a, 2)) {
-            if (cur.w.sup != built) {
+        for (uint32_t g = set; cur.w.valid; g += kLfSets, cur.advance(a, kLfSets)) {
+#ifndef SSBH_EXP_NOBUILD
+            if (a.leaf == 2) {
+                if (cur.w.sup != cur_sup || cur.w.d.ph != cur_ph) {
+                    __syncwarp();
+                    if (cur_sup != 0xFFFFFFFFu && lane == 0) {
+                        if (cur_ph == 1) mbar_arrive(lo_free);  // through P: lo is not read again
+                        if (cur_ph == 2) mbar_arrive(hi_free);  // through R
+                    }
+                    if (cur.w.sup != cur_sup) {
+                        if (cur_sup != 0xFFFFFFFFu) ++seq;
+                        cur_sup = cur.w.sup;
+                    }
+                    cur_ph = cur.w.d.ph;
+#ifdef SSBH_EXP_BSTAT
+                    const long long c0 = clock64();
+#endif
+                    if (cur_ph == 0) F4_WAIT_T(lo_ready, seq & 1);
+                    if (cur_ph == 1) F4_WAIT_T(hi_ready, seq & 1);
+#ifdef SSBH_EXP_BSTAT
+                    exp_wr += clock64() - c0;
+#endif
+                }
+            } else if (cur.w.sup != built) {
                 leaf_build<kLfAW>(a, cur.w.d, aw, lane, lraw, loff, nbuilt);
                 built = cur.w.sup;
                 ++nbuilt;
             }
+#endif
             uint4 x[4];
             const uint32_t* src = lrow + 16u * cur.s;
             if (a.leaf == 2 && cur.w.d.child != 1) {
@@ -1260,33 +1282,21 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
             }
             const uint32_t slot = g % kLfAS;
             if (g >= (uint32_t)kLfAS) F4_WAIT_S(&aempty[slot], ((g / kLfAS) - 1) & 1);
-            if (lane == 0 && (aw & 3) == 0) F4_TRACE(0, g);
-            // ((x >> kc) << 1) & M2 == shift by kc - 1 (one SHF), left by one for kc = 0; chunk
-            // q = 4 gg + kc, word w -> column 4 q + w of the stage
-            const uint32_t ta = tmem + lane_addr + kF4ACol0 + 64u * slot;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {  // columns 32h .. 32h + 31: chunks 8h .. 8h + 7
-                uint32_t v[32];
-#pragma unroll
-                for (int g2 = 0; g2 < 2; ++g2) {
-                    const uint4 xg = x[2 * h + g2];
-#pragma unroll
-                    for (int kc = 0; kc < 4; ++kc) {
-                        auto f = [&](uint32_t u) { return (kc ? u >> (kc - 1) : u << 1) & M2; };
-                        v[16 * g2 + 4 * kc + 0] = f(xg.x);
-                        v[16 * g2 + 4 * kc + 1] = f(xg.y);
-                        v[16 * g2 + 4 * kc + 2] = f(xg.z);
-                        v[16 * g2 + 4 * kc + 3] = f(xg.w);
-                    }
-                }
-                SSBH_TMEM_ST32(ta + 32u * h, v);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (lane == 0 && aw == 0) F4_TRACE(0, g);
+#ifndef SSBH_EXP_NOAPROD
+            expand_a(x, tmem + lane_addr + kF4ACol0 + 64u * slot);
+#else
+            (void)x;
+#endif
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[slot]);
-            if (lane == 0 && (aw & 3) == 0) F4_TRACE(1, g);
+            if (lane == 0 && aw == 0) F4_TRACE(1, g);
         }
+#ifdef SSBH_EXP_BSTAT
+        if (lane == 0 && aw == 0 && blockIdx.x < 2)
+            printf("EXPBSTAT cta %u: A wait-ready clk %lld\n", blockIdx.x, exp_wr);
+#endif
     }
 
     tc_fence_before();

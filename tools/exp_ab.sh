@@ -8,7 +8,7 @@ out=gpurun_out/exp_ab.log; : > $out
 for name in intree "$@"; do
   lib=""
   [ "$name" != intree ] && lib="SSBH_CUDA_LIB=build_exp/$name/libssbh_cuda.so"
-  for ov in "--override split_levels=6" ""; do
+  for ov in ""; do
     env $lib timeout 300 python tools/quick_time.py --configs 3 --reps 3 $ov 2>&1 | grep -v lop3_peak >> $out
   done
 done
