@@ -99,7 +99,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -110,6 +110,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self):
+        """Start of the timed region: the sampler is started before the warm-up (nvidia-smi
+        takes ~0.1 s to come up, longer than a short timed region) and only the samples from
+        here on are reported."""
+        self.first = len(self.lines)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -119,7 +125,8 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        if not self.lines:  # timed region shorter than the 200 ms poll: one direct query
+        self.lines = self.lines[getattr(self, "first", 0):]
+        if not self.lines:  # timed region shorter than the poll period: one direct query
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
@@ -418,15 +425,16 @@ def main():
                 plan.stream_chunk(ci, d_in.data_ptr() + ci * (chunk_bits // 8), stream.cuda_stream)
             plan.stream_finish(d_key.data_ptr(), d_len.data_ptr(), stream.cuda_stream)
 
+    clocks = ClockSampler(dev_index)
+    clocks.start()
     for _ in range(max(3, args.warmup)):
         step()
         check()
 
-    clocks = ClockSampler(dev_index)
-    clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    clocks.mark()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     hash_ms, hash_ops, stats = [], 0, None

@@ -864,7 +864,7 @@ extern "C" const char* ssbh_plan_hash_kernel(const ssbh_plan* pl) {
     if (!pl) return "";
     if (pl->engine != kEngineMma) return "k_toeplitz_hash";
     if (pl->split)  // engine checked above
-        return pl->sg.gemm ? "k_toeplitz_f4+split" : "k_toeplitz_mma_pb+split";
+        return pl->sg.gemm ? "k_leaf_gemm+split" : "k_toeplitz_mma_pb+split";
     if (pl->p.per_block_seed || pl->shared_pb)
         return "k_toeplitz_mma_pb";
     return "k_toeplitz_f4";

@@ -180,7 +180,7 @@ def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, ovr):
     for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
         plan = dev.Plan(n, s, k, 13, 14, engine=engine)
         if engine == dev.ENGINE_TENSOR and _split_possible():
-            want = "k_toeplitz_f4+split" if leaf == "gemm" else "k_toeplitz_mma_pb+split"
+            want = "k_leaf_gemm+split" if leaf == "gemm" else "k_toeplitz_mma_pb+split"
             assert plan.hash_kernel == want
             assert plan.split_geometry[:2] == (levels, 2)
         d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
