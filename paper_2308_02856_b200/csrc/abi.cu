@@ -603,6 +603,9 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     const uint64_t n = params->n_rounds, k = params->out_bits;
     pl->geom = make_sampler_geom(n, params->n_subblocks, params->block_first, nown, false, max_cs);
     if (external_payload && external_payload_bytes) pl->geom.payload_bytes = external_payload_bytes;
+    // in-memory single-level plans: ranks found in pass 1, order-free pass 3 (make_ranked)
+    if (!external_payload && !chunk_bits && nown < kBucketMinBlocks && overrides().buckets != 1)
+        pl->geom = make_ranked(pl->geom);
     pl->kw = (uint32_t)((k + 31) / 32);
     pl->rowtiles = (pl->kw + kHashRowWords - 1) / kHashRowWords;
     pl->direct_out = (k % 32) == 0;

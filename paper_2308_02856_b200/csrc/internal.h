@@ -86,7 +86,14 @@ struct SamplerGeom {
     uint64_t group_chunks; // chunks per scan group
     uint64_t ngroups;
     int payload_bytes;     // 2 (u16: V | bit<<15) or 4 (u32: V | keep<<30 | bit<<31)
+    bool ranked;           // 4-byte payload V | bit<<15 | rank<<16 (rank = the round's rank in its
+                           // block within the warp-chunk, found in pass 1; 0x7fff: sifted out):
+                           // pass 3 then needs no ordering at all (make_ranked)
 };
+// Ranked variant of a single-level u16 geometry (in-memory plans): pass 1 is ALU-bound on
+// Threefry, so the stable ranking (ballot peer masks + the warp's running-rank row) costs it
+// < 1 %, and pass 3 drops from 157 to ~30 SASS per 32 rounds.
+SamplerGeom make_ranked(const SamplerGeom& g);
 // max_chunk_shift bounds the warp-chunk (streaming: input chunks must be a whole number of
 // warp-chunks).
 SamplerGeom make_sampler_geom(uint64_t n, uint64_t s, uint32_t j_lo, uint32_t nown,

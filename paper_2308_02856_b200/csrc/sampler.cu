@@ -165,6 +165,137 @@ __global__ void __launch_bounds__(256) k_count_rows(Src src, uint64_t n, uint32_
     }
 }
 
+// Mask of the lanes whose `in` is set and whose key equals this lane's key (kbits low
+// bits compared): one ballot per key bit.
+__device__ __forceinline__ uint32_t peers_by_ballot(uint32_t key, bool in, int kbits) {
+    uint32_t m = __ballot_sync(0xffffffffu, in);
+    for (int b = 0; b < kbits; ++b) {
+        const uint32_t kb = (key >> b) & 1u;
+        const uint32_t bb = __ballot_sync(0xffffffffu, kb);
+        m &= bb ^ (kb - 1u);  // kb ? bb : ~bb
+    }
+    return m;
+}
+
+// Ranked pass 1 (SamplerGeom::ranked): one warp per chunk, in round order. V by Threefry (two
+// independent chains per lane), then the stable rank of every round among its block's rounds of
+// this chunk (running rank in the warp's shared-memory row), stored with the payload: V | bit << 15 | rank << 16 (0x7fff:
+// sifted out). The row is the chunk's count row at the end (plain stores, no atomics).
+template <bool kPow2>
+__global__ void __launch_bounds__(256) k_count_ranked(Key key, uint64_t n, uint64_t s,
+                                                      uint32_t j_lo, uint32_t nown,
+                                                      const uint32_t* __restrict__ in32,
+                                                      const uint32_t* __restrict__ keep32,
+                                                      uint32_t* __restrict__ payload, int cs,
+                                                      uint64_t nchunks, int kbits,
+                                                      uint32_t* __restrict__ counts) {
+    extern __shared__ uint32_t hist_all[];
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t* hist = hist_all + (size_t)(threadIdx.x >> 5) * 2 * nown;
+    uint32_t* own = hist + nown;  // per block: the lane that ranks next (0xffffffff: none)
+    for (uint32_t t = lane; t < nown; t += 32) own[t] = 0xffffffffu;
+    const uint64_t gpc = (1ull << cs) / 32;  // groups per chunk
+    const uint64_t ngroups = (n + 31) / 32;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    auto draw = [&](uint64_t g) -> uint32_t {
+        const uint64_t i = g * 32 + lane;
+        if (i >= n) return 0;
+        return kPow2 ? (uint32_t)(threefry_w0(key.ks, kTagSampling, 0, i, 0) & (s - 1))
+                     : (uint32_t)uniform_below(key.ks, kTagSampling, 0, s, i);
+    };
+    auto rank_store = [&](uint64_t g, uint32_t v) {
+        const uint64_t i = g * 32 + lane;
+        const bool valid = i < n;
+        const uint32_t bit = in32 ? (__ldg(in32 + g) >> lane) & 1u : 0u;
+        const bool kept = valid && (keep32 ? ((__ldg(keep32 + g) >> lane) & 1u) != 0 : true);
+        const uint32_t jj = v - j_lo;
+        const bool in = kept && jj < nown;
+        // Stable rank without a peer mask (one ballot per key bit made pass 1 VOTE-bound: +3.4
+        // ms at config 3): the lanes of a block race for its owner word with atomicMin, the
+        // lowest lane wins, takes the running rank and frees the word; the others go again.
+        // Most groups (62 % at 1024 blocks) have no two rounds of one block: one pass.
+        uint32_t rank = 0;
+        bool pend = in;
+        while (__any_sync(0xffffffffu, pend)) {
+            if (pend) atomicMin(&own[jj], lane);
+            __syncwarp();
+            if (pend && own[jj] == lane) {
+                rank = hist[jj];
+                hist[jj] = rank + 1;
+                own[jj] = 0xffffffffu;
+                pend = false;
+            }
+            __syncwarp();
+        }
+        if (valid) payload[i] = kept ? (v | (bit << 15) | (rank << 16)) : 0x7fffu;
+    };
+    for (uint64_t c = warp; c < nchunks; c += nwarps) {
+        for (uint32_t t = lane; t < nown; t += 32) hist[t] = 0;
+        __syncwarp();
+        const uint64_t g0 = c * gpc, g1 = min(ngroups, g0 + gpc);
+        uint64_t g = g0;
+        for (; g + 1 < g1; g += 2) {
+            const uint32_t va = draw(g), vb = draw(g + 1);
+            rank_store(g, va);
+            rank_store(g + 1, vb);
+        }
+        if (g < g1) rank_store(g, draw(g));
+        __syncwarp();
+        for (uint32_t t = lane; t < nown; t += 32) counts[c * nown + t] = hist[t];
+        __syncwarp();
+    }
+}
+
+// Ranked pass 3: position = the chunk's scanned offset of the block + the rank stored with the
+// round; no order between rounds is needed. One warp per chunk (its offset row in shared
+// memory), 8 groups of 32 rounds in flight.
+template <bool kLate>
+__global__ void __launch_bounds__(256) k_scatter_ranked(const uint32_t* __restrict__ payload,
+                                                        const uint32_t* __restrict__ in32_late,
+                                                        uint64_t n, int cs, uint64_t nchunks,
+                                                        uint32_t j_lo, uint32_t nown,
+                                                        const uint32_t* __restrict__ offs,
+                                                        const unsigned long long* __restrict__ nj,
+                                                        const unsigned long long* __restrict__ yoff,
+                                                        uint32_t* __restrict__ ybuf) {
+    constexpr int U = 8;
+    extern __shared__ __align__(16) uint8_t rk_smem[];
+    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(rk_smem);
+    uint32_t* row = reinterpret_cast<uint32_t*>(rk_smem + (size_t)nown * 8) +
+                    (size_t)(threadIdx.x >> 5) * nown;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
+        s_key[t] = yoff[t] * 32ull + nj[t] - 1ull;  // the block's last bit: rank r lands on it - r
+    __syncthreads();
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t c = warp; c < nchunks; c += nwarps) {
+        for (uint32_t t = lane; t < nown; t += 32) row[t] = offs[c * nown + t];
+        __syncwarp();
+        const uint64_t i0 = c << cs, i1 = min(n, (c + 1) << cs);
+        for (uint64_t ib = i0; ib < i1; ib += 32 * U) {
+            uint32_t p[U], lw[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint64_t i = ib + 32 * q + lane;
+                p[q] = i < i1 ? payload[i] : 0x7fffu;
+                if (kLate) lw[q] = i < i1 ? __ldg(in32_late + (i >> 5)) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint32_t v = p[q] & 0x7fffu, jj = v - j_lo;
+                const uint32_t bit = kLate ? (lw[q] >> lane) & 1u : (p[q] >> 15) & 1u;
+                if (v != 0x7fffu && jj < nown && bit) {
+                    const unsigned long long qb = s_key[jj] - (row[jj] + (p[q] >> 16));
+                    atomicOr(ybuf + (qb >> 5), 1u << (qb & 31));
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // Pass 1, large key spaces: counts go straight to the global (chunk, key) table.
 template <typename Src>
 __global__ void __launch_bounds__(256) k_count_global(Src src, uint64_t n, uint32_t nkeys, int cs,
@@ -276,18 +407,6 @@ __global__ void k_scan_apply(uint32_t* __restrict__ counts, uint64_t nchunks, ui
             base += v[e];
         }
     }
-}
-
-// Mask of the lanes whose `in` is set and whose key equals this lane's key (kbits low
-// bits compared): one ballot per key bit.
-__device__ __forceinline__ uint32_t peers_by_ballot(uint32_t key, bool in, int kbits) {
-    uint32_t m = __ballot_sync(0xffffffffu, in);
-    for (int b = 0; b < kbits; ++b) {
-        const uint32_t kb = (key >> b) & 1u;
-        const uint32_t bb = __ballot_sync(0xffffffffu, kb);
-        m &= bb ^ (kb - 1u);  // kb ? bb : ~bb
-    }
-    return m;
 }
 
 // ---- pass-3 sources -------------------------------------------------------------------
@@ -756,9 +875,49 @@ SamplerGeom geom_with_n(const SamplerGeom& g0, uint64_t n) {
     return g;
 }
 
+SamplerGeom make_ranked(const SamplerGeom& g0) {
+    SamplerGeom g = g0;
+    // u16-eligible, both rows of a warp in shared memory, payload doubled to <= 8 GiB
+    if (g.payload_bytes != 2 || (size_t)g.nown * 8 * 8 > 96 * 1024 || g.n > (1ull << 31)) return g;
+    g.ranked = true;
+    g.payload_bytes = 4;
+    // one warp per chunk in pass 1: twice the chunks of the two-part count kernel when the
+    // input is large enough to want them (table <= 256 MiB)
+    while (g.chunk_shift > 8 && g.nchunks < 2 * kMaxTableChunks &&
+           (g.nchunks * 2) * (uint64_t)g.nown * 4 <= (256ull << 20) && (g.n >> g.chunk_shift) >= kMaxTableChunks) {
+        --g.chunk_shift;
+        g.nchunks = (g.n + (1ull << g.chunk_shift) - 1) >> g.chunk_shift;
+    }
+    g.group_chunks = std::min<uint64_t>(
+        64, std::max<uint64_t>(8, g.nchunks * (uint64_t)std::max<uint32_t>(g.nown, 1) / (148ull * 2048)));
+    g.ngroups = (g.nchunks + g.group_chunks - 1) / g.group_chunks;
+    return g;
+}
+
 void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint32_t* d_in32,
                          const uint32_t* d_keep, void* d_payload, uint32_t* d_counts,
                          uint32_t* d_assign_out, cudaStream_t st) {
+    if (g.ranked && d_payload && !d_assign_out) {
+        if (g.n == 0) return;
+        Key k;
+        threefry_ks(key, k.ks);
+        int kbits = 1;
+        while ((1ull << kbits) < g.nown) ++kbits;
+        const size_t shm = (size_t)g.nown * 8 * 8;  // rank row + owner row per warp
+        const uint64_t blocks = std::min<uint64_t>((g.nchunks + 7) / 8, (uint64_t)sm_count() * 8);
+        auto go = [&](auto kern) {
+            if (shm > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
+                k, g.n, g.s, g.j_lo, g.nown, d_in32, d_keep, static_cast<uint32_t*>(d_payload),
+                g.chunk_shift, g.nchunks, kbits, d_counts);
+        };
+        if ((g.s & (g.s - 1)) == 0)
+            go(k_count_ranked<true>);
+        else
+            go(k_count_ranked<false>);
+        return;
+    }
     sample_count_any(g, key, d_in32, d_keep, d_payload, d_counts, d_assign_out, 0, 0, 0, st);
 }
 
@@ -890,6 +1049,22 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
                     const unsigned long long* d_csr_off, cudaStream_t st,
                     const uint32_t* d_in32_late) {
     if (g.n == 0 || g.nown == 0) return;
+    if (g.ranked && !d_idx_out) {
+        const size_t shm = (size_t)g.nown * 8 + (size_t)g.nown * 4 * 8 + 16;
+        const uint64_t blocks = std::min<uint64_t>((g.nchunks + 7) / 8, (uint64_t)sm_count() * 16);
+        auto go = [&](auto kern) {
+            if (shm > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
+                static_cast<const uint32_t*>(d_payload), d_in32_late, g.n, g.chunk_shift, g.nchunks,
+                g.j_lo, g.nown, d_offsets, d_nj, d_yoff, d_ybuf);
+        };
+        if (d_in32_late)
+            go(k_scatter_ranked<true>);
+        else
+            go(k_scatter_ranked<false>);
+        return;
+    }
     const ScatterArgs a = scatter_args(g, d_offsets, d_nj, d_yoff, d_ybuf, d_idx_out, d_csr_off);
     if (d_in32_late) {  // host runs: data bits from the input (no index mode there)
         if (g.payload_bytes == 2)

@@ -813,9 +813,12 @@ constexpr int kLfAS = 3;                    // A ring (TMEM, 64 columns per stag
 constexpr int kLfEW = 16;                   // epilogue warps
 constexpr int kLfAW = 4;                    // A producer warps: sets of 4 (one per sub-partition)
 constexpr int kLfSets = kLfAW / 4;          // a set fills every kLfSets-th stage
-constexpr int kLfBW = 4;                    // background-build warps (parent mode); 8 build in
-                                            // time for every parent but cap the CTA at 64
-                                            // registers per thread (25.1 ms against 22.4)
+#ifndef SSBH_EXP_BW
+#define SSBH_EXP_BW 6
+#endif
+constexpr int kLfBW = SSBH_EXP_BW;          // background-build warps (parent mode): 28 warps in
+                                            // all keep 72 registers per thread; 8 build warps
+                                            // (30 warps, 64 registers) measured 25.1 ms
 constexpr int kLfMmaW = kLfEW, kLfLoadW = kLfEW + 1, kLfProd0 = kLfEW + 2;
 constexpr int kLfBuild0 = kLfProd0 + kLfAW;
 constexpr int kLfThreads = (kLfEW + 2 + kLfAW + kLfBW) * 32;
@@ -856,7 +859,7 @@ __global__ void __launch_bounds__(256) k_hankel_units(const uint32_t* __restrict
 // bulk-copy engine (~300 clocks per 512-byte copy) and warps staging pieces with cp.async (slower
 // per piece than register loads) all lose to dedicated warps with plain loads.
 constexpr int kBuildInFlight = 8;
-constexpr uint32_t kLfBRows = kM / kLfBW;          // rows of the M tile per build warp
+constexpr uint32_t kLfBRows = (kM + kLfBW - 1) / kLfBW;  // rows of the M tile per build warp
 __device__ __forceinline__ void build_half_rows(const MmaHashArgs& a, uint32_t sup, uint32_t h,
                                                 uint32_t r0, uint32_t r1, uint32_t lane,
                                                 uint32_t* lraw) {
@@ -1175,6 +1178,7 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
 #ifndef SSBH_EXP_NOBUILD
         if (a.leaf == 2) {
             const uint32_t row0 = (warp - kLfBuild0) * kLfBRows;
+            const uint32_t row1 = row0 + kLfBRows < (uint32_t)kM ? row0 + kLfBRows : (uint32_t)kM;
             uint32_t seq = 0;
 #ifdef SSBH_EXP_BSTAT
             long long tb = 0, tw = 0;
@@ -1188,7 +1192,7 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
                 long long c1 = clock64();
                 tw += c1 - c0;
 #endif
-                build_half_rows(a, sup, 0, row0, row0 + kLfBRows, lane, lraw);
+                build_half_rows(a, sup, 0, row0, row1, lane, lraw);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(lo_ready);
 #ifdef SSBH_EXP_BSTAT
@@ -1200,7 +1204,7 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
                 c1 = clock64();
                 tw += c1 - c0;
 #endif
-                build_half_rows(a, sup, 1, row0, row0 + kLfBRows, lane, lraw);
+                build_half_rows(a, sup, 1, row0, row1, lane, lraw);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(hi_ready);
 #ifdef SSBH_EXP_BSTAT
