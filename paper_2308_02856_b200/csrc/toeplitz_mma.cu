@@ -1510,7 +1510,6 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                 continue;
             }
             uint32_t round_end = 0;
-            const uint32_t idesc = f4_idesc(d.nmma);
             // D0: D step relative to the item's first step d.s0
             for (uint32_t D0 = 0; D0 < d.nD; D0 += kPbL, ++yb) {
                 if (D0 % kRound == 0) {  // a new accumulation round (kRound is a multiple of kPbL)
@@ -1533,13 +1532,27 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_toeplitz_mma_pb(PbHashArgs a)
                             const uint32_t s = sb + j;
                             // column n of step D0+s is unit (kPbL - 1 - s) + n of the buffer;
                             // H of step j of the stage starts at unit 128 j
-                            const uint32_t ya = ybase + b * G::ybytes + 16u * (kPbL - 1 - s);
                             const uint32_t first = (D0 % kRound) | s;
+                            // Only the columns whose y chunk D - n lies inside the block carry
+                            // products: n in [D - nC + 1, D]. The window's ramps (255 of its
+                            // ncols + nC - 1 steps each way) run as narrower MMAs on that column
+                            // range (16-column granularity; an MMA's time falls with N: 87 clocks
+                            // at N = 128 against 128 at N = 256). The round's first step stays
+                            // full width: it initialises every accumulator column.
+                            uint32_t c_lo = 0, c_hi = d.nmma;
+                            if (first != 0) {
+                                const uint32_t dabs = d.s0 + D0 + s;
+                                c_lo = (dabs + 1 > d.nC ? dabs + 1 - d.nC : 0u) & ~15u;
+                                c_hi = (min(d.ncols, dabs + 1) + 15u) & ~15u;
+                            }
+                            const uint32_t idesc_n = f4_idesc(c_hi - c_lo);
+                            const uint32_t ya =
+                                ybase + b * G::ybytes + 16u * (kPbL - 1 - s) + 16u * c_lo;
 #pragma unroll
                             for (int m = 0; m < G::mmas; ++m) {
                                 const uint64_t adesc = sdesc(ha + 2048u * j + 32u * m, 16, 128);
                                 const uint64_t bdesc = sdesc(ya + 2u * m * (kPbUnits * 16), kPbUnits * 16, 128);
-                                mma_f4n(tmem, adesc, bdesc, idesc, tmem + kF4SfCol,
+                                mma_f4n(tmem + c_lo, adesc, bdesc, idesc_n, tmem + kF4SfCol,
                                         (first | (uint32_t)m) != 0);
                             }
                         }
