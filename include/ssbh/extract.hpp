@@ -51,4 +51,21 @@ ExtractResult extract(const BitString& input, std::uint32_t n_subblocks,
 BitString toeplitz_hash_batch(const std::vector<ToeplitzSeed>& seeds,
                               const std::vector<BitString>& inputs);
 
+/// The same batch with the seeds and inputs uploaded once and kept on the device: run() hashes
+/// every block and returns the concatenation. What the reference's cmd_bench times
+/// (ssbh_main.cpp:405-410: the toeplitz_hash calls alone, gather and seed generation untimed)
+/// corresponds to run().
+class PreparedHashBatch {
+public:
+    PreparedHashBatch(const std::vector<ToeplitzSeed>& seeds, const std::vector<BitString>& inputs);
+    ~PreparedHashBatch();
+    PreparedHashBatch(const PreparedHashBatch&) = delete;
+    PreparedHashBatch& operator=(const PreparedHashBatch&) = delete;
+    BitString run() const;
+
+private:
+    void* handle_ = nullptr;
+    std::uint64_t out_bits_ = 0;
+};
+
 }  // namespace ssbh

@@ -138,6 +138,18 @@ ssbh_status ssbh_toeplitz_hash_batch_ptrs(uint64_t count, uint64_t m, const uint
                                           const uint64_t* const* inputs,
                                           const uint64_t* const* seeds, uint64_t* out);
 
+/* Prepared batch: the same hashes with the inputs and seeds resident on the device. create
+ * uploads and packs them once (what the reference's cmd_bench does untimed before its timed
+ * toeplitz_hash loop, ssbh_main.cpp:388-404); run hashes every block and copies the
+ * concatenated result (ceil(count*m/64) words) to out — the call that corresponds to the
+ * reference's timed region (ssbh_main.cpp:405-410). A B200 addition (no reference symbol). */
+typedef struct ssbh_hash_batch ssbh_hash_batch;
+ssbh_status ssbh_hash_batch_create(uint64_t count, uint64_t m, const uint64_t* n,
+                                   const uint64_t* const* inputs, const uint64_t* const* seeds,
+                                   ssbh_hash_batch** out);
+ssbh_status ssbh_hash_batch_run(ssbh_hash_batch* batch, uint64_t* out);
+ssbh_status ssbh_hash_batch_destroy(ssbh_hash_batch* batch);
+
 /* The reference-facing calls above (toeplitz_hash, KeyedStream::bits, assign_subblocks,
  * sift_partition, ...) keep a per-thread, per-device stream and device arena between calls,
  * so that steady-state calls allocate nothing. This frees the calling thread's arenas (they

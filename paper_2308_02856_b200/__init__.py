@@ -53,7 +53,8 @@ ABI_SYMBOLS = (
     "ssbh_probe_mma_f4", "ssbh_plan_hash_kernel", "ssbh_shard_hash_kernel",
     "ssbh_plan_split_geometry", "ssbh_shard_split_geometry", "ssbh_fnv1a64",
     "ssbh_toeplitz_hash_batch_ptrs", "ssbh_release_thread_cache", "ssbh_set_plan_overrides",
-    "ssbh_get_plan_overrides",
+    "ssbh_get_plan_overrides", "ssbh_hash_batch_create", "ssbh_hash_batch_run",
+    "ssbh_hash_batch_destroy",
 )
 
 ENGINE_AUTO, ENGINE_LOP3, ENGINE_TENSOR = 0, 1, 2

@@ -1641,6 +1641,132 @@ extern "C" ssbh_status ssbh_toeplitz_hash_batch_ptrs(uint64_t count, uint64_t m,
     return hash_batch_impl(count, m, n, nullptr, nullptr, inputs, nullptr, nullptr, seeds, out);
 }
 
+// Prepared batch (device-resident inputs and seeds; see include/ssbh_cuda.h).
+struct ssbh_hash_batch {
+    uint32_t nown = 0, kw = 0, rowtiles = 0, kt = 0;
+    uint64_t m = 0, mean_n = 0, key_w64 = 0;
+    int device = 0, grid = 0;
+    LayoutBufs lb;
+    DBuf ybuf, sbuf, scratch, key;
+    cudaStream_t st = nullptr;
+};
+
+extern "C" ssbh_status ssbh_hash_batch_create(uint64_t count, uint64_t m, const uint64_t* n,
+                                              const uint64_t* const* inputs,
+                                              const uint64_t* const* seeds,
+                                              ssbh_hash_batch** out) {
+    if (!out || !n || !inputs || !seeds)
+        return fail(SSBH_INVALID_ARGUMENT, "hash_batch_create: null argument");
+    if (m == 0 || count == 0)
+        return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    for (uint64_t b = 0; b < count; ++b)
+        if (n[b] == 0) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: m and n must be positive");
+    if (count > (1u << 30)) return fail(SSBH_INVALID_ARGUMENT, "toeplitz: batch too large");
+    NEED_DEVICE();
+    std::unique_ptr<ssbh_hash_batch> hb(new ssbh_hash_batch());
+    CU(cudaGetDevice(&hb->device));
+    hb->nown = (uint32_t)count;
+    hb->m = m;
+    hb->kw = (uint32_t)((m + 31) / 32);
+    hb->rowtiles = (hb->kw + kHashRowWords - 1) / kHashRowWords;
+    std::vector<uint64_t> meta(3 * count);  // n | in_off | seed_off (u64 words)
+    uint64_t in_words = 0, seed_words = 0, sum_n = 0, ybound = 8, sbound = 8, maxw = 0;
+    for (uint64_t b = 0; b < count; ++b) {
+        const uint64_t iw = words64(n[b]), sw = words64(m + n[b] - 1);
+        meta[b] = n[b];
+        meta[count + b] = in_words;
+        meta[2 * count + b] = seed_words;
+        in_words += iw;
+        seed_words += sw;
+        sum_n += n[b];
+        const uint64_t yp = round_up((n[b] + 31) / 32, kHashR);
+        ybound += yp;
+        sbound += round_up((uint64_t)hb->rowtiles * kHashRowWords + 8 + yp, 8);
+        maxw = std::max<uint64_t>(maxw, 2 * sw);
+    }
+    hb->mean_n = sum_n / count;
+    hb->key_w64 = words64(count * m);
+    DBuf din, dseeds, dmeta;  // only needed until the blocks are packed
+    CU(hb->lb.alloc(hb->nown));
+    CU(din.alloc(in_words * 8));
+    CU(dseeds.alloc(seed_words * 8));
+    CU(dmeta.alloc(count * 24));
+    CU(hb->ybuf.alloc(ybound * 4));
+    CU(hb->sbuf.alloc((sbound + 64) * 4));
+    CU(hb->scratch.alloc((size_t)hb->nown * hb->kw * 4));
+    CU(hb->key.alloc(hb->key_w64 * 8));
+    CU(cudaStreamCreateWithFlags(&hb->st, cudaStreamNonBlocking));
+    const cudaStream_t st = hb->st;
+    for (uint64_t b = 0; b < count; ++b) {
+        CU(cudaMemcpyAsync(din.as<uint64_t>() + meta[count + b], inputs[b], words64(n[b]) * 8,
+                           cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(dseeds.as<uint64_t>() + meta[2 * count + b], seeds[b],
+                           words64(m + n[b] - 1) * 8, cudaMemcpyHostToDevice, st));
+    }
+    CU(cudaMemcpyAsync(dmeta.p, meta.data(), count * 24, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(hb->lb.nj.p, meta.data(), count * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(hb->ybuf.p, 0, hb->ybuf.bytes, st));
+    CU(cudaMemsetAsync(hb->sbuf.p, 0, hb->sbuf.bytes, st));
+    const Layout lay = hb->lb.view();
+    hb->grid = hash_grid_size(hb->device);
+    hb->kt = choose_kt(hb->mean_n, hb->nown, hb->rowtiles, hb->grid);
+    launch_layout(lay, hb->nown, m, hb->rowtiles, hb->kt, 1, 0, st);
+    launch_pack_blocks(dseeds.as<uint64_t>(), dmeta.as<unsigned long long>() + 2 * count,
+                       din.as<uint64_t>(), dmeta.as<unsigned long long>() + count, lay, hb->nown,
+                       m, hb->sbuf.as<uint32_t>(), hb->ybuf.as<uint32_t>(), st, maxw);
+    if (auto e = check_launch("hash_batch_create")) return e;
+    CU(cudaStreamSynchronize(st));
+    *out = hb.release();
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_hash_batch_run(ssbh_hash_batch* hb, uint64_t* out) {
+    if (!hb || !out) return fail(SSBH_INVALID_ARGUMENT, "hash_batch_run: null argument");
+    CU(cudaSetDevice(hb->device));
+    const cudaStream_t st = hb->st;
+    const Layout lay = hb->lb.view();
+    CU(cudaMemsetAsync(hb->key.p, 0, hb->key.bytes, st));
+    if (default_engine(1) == kEngineMma) {  // every block its own matrix: tiled matvec MMAs
+        const PbGeom pg = make_pb_geom(hb->nown, hb->kw, hb->device, hb->mean_n);
+        PbHashArgs a{};
+        a.ybuf = hb->ybuf.as<uint32_t>();
+        a.sbuf = hb->sbuf.as<uint32_t>();
+        a.out = hb->scratch.as<uint32_t>();
+        a.out_stride = hb->kw;
+        a.lay = lay;
+        a.nown = hb->nown;
+        a.kw = hb->kw;
+        a.ntiles = pg.ntiles;
+        a.nwin = pg.nwin;
+        launch_hash_mma_pb(a, pg, st);
+    } else {
+        CU(cudaMemsetAsync(hb->scratch.p, 0, hb->scratch.bytes, st));
+        HashArgs a{};
+        a.ybuf = hb->ybuf.as<uint32_t>();
+        a.sbuf = hb->sbuf.as<uint32_t>();
+        a.out = hb->scratch.as<uint32_t>();
+        a.out_stride = hb->kw;
+        a.lay = lay;
+        a.nown = hb->nown;
+        a.kw = hb->kw;
+        a.rowtiles = hb->rowtiles;
+        a.per_block_seed = 1;
+        launch_hash(a, hb->grid, st);
+    }
+    launch_concat(hb->scratch.as<uint32_t>(), hb->kw, hb->nown, hb->m, hb->key.as<uint32_t>(), st);
+    if (auto e = check_launch("hash_batch_run")) return e;
+    CU(cudaMemcpyAsync(out, hb->key.p, hb->key_w64 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return ok();
+}
+
+extern "C" ssbh_status ssbh_hash_batch_destroy(ssbh_hash_batch* hb) {
+    if (!hb) return ok();
+    if (hb->st) cudaStreamDestroy(hb->st);
+    delete hb;
+    return ok();
+}
+
 extern "C" ssbh_status ssbh_release_thread_cache(void) {
     for (auto& a : g_call.per_dev)
         if (a && !a->depth) a.reset();

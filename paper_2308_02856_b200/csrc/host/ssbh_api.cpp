@@ -336,4 +336,37 @@ BitString toeplitz_hash_batch(const std::vector<ToeplitzSeed>& seeds,
     return out;
 }
 
+PreparedHashBatch::PreparedHashBatch(const std::vector<ToeplitzSeed>& seeds,
+                                     const std::vector<BitString>& inputs) {
+    if (seeds.size() != inputs.size())
+        throw std::invalid_argument("toeplitz_hash_batch: seeds/inputs count mismatch");
+    if (seeds.empty()) throw std::invalid_argument("toeplitz: m and n must be positive");
+    const std::uint64_t m = seeds[0].m;
+    std::vector<std::uint64_t> n(seeds.size());
+    std::vector<const std::uint64_t*> in_ptr(seeds.size()), seed_ptr(seeds.size());
+    for (std::size_t b = 0; b < seeds.size(); ++b) {
+        if (seeds[b].m != m)
+            throw std::invalid_argument("toeplitz_hash_batch: output lengths differ");
+        if (inputs[b].size() != seeds[b].n)
+            throw std::invalid_argument("toeplitz: input length does not match seed.n");
+        n[b] = seeds[b].n;
+        in_ptr[b] = inputs[b].words().data();
+        seed_ptr[b] = seeds[b].seed.words().data();
+    }
+    ssbh_hash_batch* h = nullptr;
+    check(ssbh_hash_batch_create(seeds.size(), m, n.data(), in_ptr.data(), seed_ptr.data(), &h));
+    handle_ = h;
+    out_bits_ = m * seeds.size();
+}
+
+PreparedHashBatch::~PreparedHashBatch() {
+    ssbh_hash_batch_destroy(static_cast<ssbh_hash_batch*>(handle_));
+}
+
+BitString PreparedHashBatch::run() const {
+    BitString out(out_bits_);
+    check(ssbh_hash_batch_run(static_cast<ssbh_hash_batch*>(handle_), out.words().data()));
+    return out;
+}
+
 }  // namespace ssbh

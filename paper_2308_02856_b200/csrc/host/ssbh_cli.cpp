@@ -245,7 +245,13 @@ std::uint64_t model_cycles(std::uint64_t in, std::uint64_t out, std::uint32_t ns
 int cmd_bench(const Args& a) {
     if (a.sizes.empty()) throw std::invalid_argument("bench: --sizes required");
     const MasterSeed seed = MasterSeed::from_hex(a.seed_hex);
-    std::string out = "size_bits,full_seconds,split_seconds,measured_ratio,modeled_ratio\n";
+    // The reference's columns (ssbh_main.cpp:371) + the same two timings with the operands
+    // resident on the device (PreparedHashBatch::run): the reference times toeplitz_hash on
+    // operands that sit where it computes; through host containers both GPU calls are bound by
+    // the host-to-device copy of input and seed (2 x size/8 bytes either way).
+    std::string out =
+        "size_bits,full_seconds,split_seconds,measured_ratio,modeled_ratio,"
+        "full_device_seconds,split_device_seconds,device_ratio\n";
     for (const std::uint64_t size : a.sizes) {
         if (size == 0) throw std::invalid_argument("bench: sizes must be positive");
         const std::uint64_t m_full =
@@ -282,13 +288,20 @@ int cmd_bench(const Args& a) {
                                m_block, inputs[j].size());
         }
         const double split_s = median_s([&] { (void)toeplitz_hash_batch(seeds, inputs); });
+        double full_dev_s = 0, split_dev_s = 0;
+        {
+            const PreparedHashBatch full_dev({fseed}, {input});
+            full_dev_s = median_s([&] { (void)full_dev.run(); });
+            const PreparedHashBatch split_dev(seeds, inputs);
+            split_dev_s = median_s([&] { (void)split_dev.run(); });
+        }
         const double modeled = static_cast<double>(model_cycles(size, m_full, 1, a.eps_abort)) /
                                static_cast<double>(model_cycles(size, m_block * a.ns, a.ns,
                                                                 a.eps_abort));
-        char line[256];
-        std::snprintf(line, sizeof line, "%llu,%.6g,%.6g,%.6g,%.6g\n",
+        char line[320];
+        std::snprintf(line, sizeof line, "%llu,%.6g,%.6g,%.6g,%.6g,%.6g,%.6g,%.6g\n",
                       static_cast<unsigned long long>(size), full_s, split_s, full_s / split_s,
-                      modeled);
+                      modeled, full_dev_s, split_dev_s, full_dev_s / split_dev_s);
         out += line;
     }
     emit(a.out, out);

@@ -146,8 +146,10 @@ def test_cli_bench_runs(tmp_path, oracle):
             cwd=tmp_path)
     assert r.returncode == 0, r.stderr
     lines = r.stdout.strip().splitlines()
-    assert lines[0] == "size_bits,full_seconds,split_seconds,measured_ratio,modeled_ratio"
+    assert lines[0] == ("size_bits,full_seconds,split_seconds,measured_ratio,modeled_ratio,"
+                        "full_device_seconds,split_device_seconds,device_ratio")
     for ln in lines[1:]:
-        size, full_s, split_s, meas, model = ln.split(",")
+        size, full_s, split_s, meas, model, full_d, split_d, ratio_d = ln.split(",")
         assert float(full_s) > 0 and float(split_s) > 0 and float(model) > 1.0
+        assert float(full_d) > 0 and float(split_d) > 0
         print("cmd_bench", ln)
