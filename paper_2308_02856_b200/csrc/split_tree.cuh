@@ -6,7 +6,7 @@
 
 namespace ssbh_impl {
 
-constexpr int kMaxL = 7;
+constexpr int kMaxL = 9;  // k = 2^21 (config 5) reaches leaves of 2^12 positions at L = 9
 
 // Offsets (bits) whose windows / pieces a leaf XORs. seed: S windows; input: y pieces.
 __device__ __forceinline__ int leaf_offsets(uint32_t path, uint32_t L, uint64_t k, uint64_t base,

@@ -477,8 +477,7 @@ __device__ __forceinline__ void leaf_build(const MmaHashArgs& a, const Item& d, 
     // parent mode: the input of the children's parent (level L - 1, path / 3)
     const uint32_t pL = a.leaf == 2 ? q.L - 1 : q.L, ppath = a.leaf == 2 ? path / 3 : path;
     uint32_t un = 1;
-    {
-        const uint32_t e = bw * 32 + lane;
+    for (uint32_t e = bw * 32 + lane; e < kLeafPieces; e += kBW * 32) {
         const uint64_t off = piece_offset(ppath, pL, q.k, (uint64_t)t * q.k, e, &un);
         if (e < un) loff[e] = off / 32;
     }
@@ -862,48 +861,34 @@ constexpr int kBuildInFlight = 8;
 constexpr uint32_t kLfBRows = (kM + kLfBW - 1) / kLfBW;  // rows of the M tile per build warp
 __device__ __forceinline__ void build_half_rows(const MmaHashArgs& a, uint32_t sup, uint32_t h,
                                                 uint32_t r0, uint32_t r1, uint32_t lane,
-                                                uint32_t* lraw) {
+                                                uint32_t* lraw, uint32_t* woff) {
     const LeafSrc& q = a.src;
     const uint32_t mpg = q.gpad / kM, pleaves = q.leaves / 3;
     const uint32_t pg = sup / mpg, jl0 = (sup % mpg) * kM;
     const uint32_t t = pg / pleaves, pp = pg % pleaves;
     const uint32_t hw = q.kpw / 2;  // words per half (= the leaf size)
-    uint32_t mP[kMaxL];             // sizes (words) of the levels whose digit is P
-    uint32_t np = 0;
-    uint64_t base = (uint64_t)t * (q.k / 32) + (uint64_t)h * hw;
-    {
-        uint32_t pw = 1;
-        for (uint32_t l = 2; l < q.L; ++l) pw *= 3;
-        uint64_t m = q.k / 32;
-#pragma unroll
-        for (int l = 0; l < kMaxL - 1; ++l) {
-            if ((uint32_t)l + 1 < q.L) {
-                m >>= 1;
-                const uint32_t dg = pp / pw % 3;
-                pw /= 3;
-                if (dg == 2) base += m;
-                if (dg == 0) mP[np++] = (uint32_t)m;
-            }
-        }
+    // the pieces' word offsets into a block's reversed input, once per call into the warp's
+    // table woff (lane e, e + 32, ...): piece_offset in words, + the half
+    uint32_t un = 1;
+    for (uint32_t e = lane; e < kLeafPieces / 2; e += 32) {
+        const uint64_t off = piece_offset(pp, q.L - 1, q.k, (uint64_t)t * q.k, e, &un);
+        if (e < un) woff[e] = (uint32_t)(off / 32) + h * hw;
     }
-    const uint32_t n = 1u << np;
+    __syncwarp();
+    const uint32_t n = un;
     const bool lane_on = lane < hw / 4;
     for (uint32_t r = r0; r < r1; ++r) {
         const uint32_t jlg = jl0 + r, jj = q.jj0 + jlg;
         const bool live = lane_on && jlg < q.batch && jj < q.nown;
         const uint4* y = reinterpret_cast<const uint4*>(live ? q.ybuf + q.lay.yoff[jj] : q.ybuf);
-        const uint64_t yp4 = live ? q.lay.ypad[jj] / 4 : 0;  // ypad is a multiple of 32 words
+        const uint32_t yp4 = live ? q.lay.ypad[jj] / 4 : 0;  // ypad is a multiple of 32 words
         uint4 acc = make_uint4(0, 0, 0, 0);
         for (uint32_t e0 = 0; e0 < n; e0 += kBuildInFlight) {
             uint4 v[kBuildInFlight];
 #pragma unroll
             for (int i = 0; i < kBuildInFlight; ++i) {
                 const uint32_t e = e0 + i;
-                uint64_t off = base;
-#pragma unroll
-                for (int b = 0; b < kMaxL - 1; ++b)
-                    if ((uint32_t)b < np && ((e >> b) & 1u)) off += mP[b];
-                const uint64_t qv = off / 4 + lane;
+                const uint32_t qv = (e < n ? woff[e] : 0u) / 4 + lane;
                 v[i] = e < n && qv < yp4 ? __ldg(y + qv) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
@@ -917,6 +902,7 @@ __device__ __forceinline__ void build_half_rows(const MmaHashArgs& a, uint32_t s
         if (lane_on)
             *reinterpret_cast<uint4*>(lraw + (size_t)r * kLeafStride + h * hw + 4u * lane) = acc;
     }
+    __syncwarp();
 }
 
 __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
@@ -1179,6 +1165,11 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
         if (a.leaf == 2) {
             const uint32_t row0 = (warp - kLfBuild0) * kLfBRows;
             const uint32_t row1 = row0 + kLfBRows < (uint32_t)kM ? row0 + kLfBRows : (uint32_t)kM;
+            // parent mode never runs the foreground build: its offset buffer holds the build
+            // warps' piece tables (kLeafPieces / 2 words each)
+            uint32_t* woff =
+                reinterpret_cast<uint32_t*>(loff) + (warp - kLfBuild0) * (kLeafPieces / 2);
+            static_assert(kLfBW * (kLeafPieces / 2) * 4 <= 2 * kLeafPieces * 8, "piece tables");
             uint32_t seq = 0;
 #ifdef SSBH_EXP_BSTAT
             long long tb = 0, tw = 0;
@@ -1192,7 +1183,7 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
                 long long c1 = clock64();
                 tw += c1 - c0;
 #endif
-                build_half_rows(a, sup, 0, row0, row1, lane, lraw);
+                build_half_rows(a, sup, 0, row0, row1, lane, lraw, woff);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(lo_ready);
 #ifdef SSBH_EXP_BSTAT
@@ -1204,7 +1195,7 @@ __global__ void __launch_bounds__(kLfThreads, 1) k_leaf_gemm(MmaHashArgs a) {
                 c1 = clock64();
                 tw += c1 - c0;
 #endif
-                build_half_rows(a, sup, 1, row0, row1, lane, lraw);
+                build_half_rows(a, sup, 1, row0, row1, lane, lraw, woff);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(hi_ready);
 #ifdef SSBH_EXP_BSTAT

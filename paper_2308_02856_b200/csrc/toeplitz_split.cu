@@ -252,7 +252,8 @@ uint32_t split_levels(uint64_t k, bool gemm) {
             // Leaves >= 2^12 positions: leaves of 2^13 run as leaf-mode items of 16 FP4 stages;
             // leaves of 2^12 run in the leaf GEMM's parent mode (a CTA builds the parent's 2^13
             // positions once for its three children), which is what makes the seventh level pay
-            // (config 3 hash L = 6 / 7 = 31.2 / 27.6 ms); config 5 stays at kMaxL = 7
+            // (config 3 hash L = 6 / 7 = 31.2 / 27.6 ms); config 5 (k = 2^21) takes L = 9: hash of
+            // 1024 of its blocks L = 7 / 8 / 9 = 404 / 308 / 240 ms
             if (k < (1ull << 18) || (k >> L) < (1ull << 12)) break;
             best = L;
             continue;
@@ -339,6 +340,11 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
     if (g.per_block) split_seeds(d_sbuf, sbuf_words, lay, nown, g, jj0, d_vs, st);
 }
 
+#ifndef SSBH_EXP_TREE_KB
+#define SSBH_EXP_TREE_KB 112
+#endif
+constexpr size_t kTreeSmemCap = SSBH_EXP_TREE_KB * 1024;
+
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
                               uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st) {
@@ -346,7 +352,7 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
     if (!count || !kw) return 0;
     // one pass from the leaves (round 1: level by level, L launches through HBM, config 3
     // 3.0 ms): depth-D register subtrees, chunk width W words (the largest power of two <= 32
-    // and <= the leaf whose buffers fit 48 KB of shared memory: several CTAs per SM)
+    // and <= the leaf whose buffers fit kTreeSmemCap of shared memory: two CTAs per SM)
     const uint32_t D = g.L >= 3 ? 3 : g.L;
     const uint32_t sub = D == 1 ? 3 : D == 2 ? 9 : 27, outd = 1u << D;
     const uint64_t cw = g.sL / 32;
@@ -354,8 +360,14 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
     auto smem_of = [&](uint32_t w) {
         return ((size_t)nsub * outd * w + (size_t)(nsub / 3) * 2 * outd * w + ((size_t)w << g.L)) * 4;
     };
+    // (deep trees — config 5 combines 8 levels of 3^8 nodes — need the wider chunks: at 48 KB W
+    // was 2 words, 8-byte reads of 32-byte sectors, 3.2 ms per 1.7 GB batch)
     uint32_t W = 32;
     while (W > 1 && (W > cw || smem_of(W) > 48 * 1024)) W /= 2;
+    if (W < 8) {  // deep tree: two CTAs per SM instead
+        W = 8;
+        while (W > 1 && (W > cw || smem_of(W) > kTreeSmemCap)) W /= 2;
+    }
     const size_t smem = smem_of(W);
     const uint64_t grid = (uint64_t)count * (cw / W);
     auto go = [&](auto kern) {
