@@ -12,7 +12,9 @@
 // integer counts below 2^24) and the epilogue keeps the parity. Per-block seeds (and long
 // shared blocks) tile each block's matrix-vector product into 128 x 128 Hankel blocks
 // instead. Kernels in this file:
-//   k_toeplitz_f4        shared seeds: all owned blocks x one Hankel matrix as a GEMM
+//   k_toeplitz_f4        shared seeds, direct mode: all owned blocks x one Hankel matrix as a GEMM
+//   k_leaf_gemm          the 3-for-4 split's shared-seed leaves (toeplitz_split.cu) as GEMMs
+//                        (+ k_hankel_units: its Hankel operand tables)
 //   k_toeplitz_mma_pb    tiled matrix-vector products: per-block seeds, long shared blocks
 //
 // The Hankel operand. With the K order used inside a pipeline stage (chunk q, word w, nibble
@@ -432,7 +434,6 @@ __device__ __forceinline__ void expand_a(const uint4 (&x)[4], uint32_t ta) {
 constexpr uint32_t kLeafKpw = 256;                     // 8192 positions per K part
 constexpr uint32_t kLeafStride = kLeafKpw + 4;
 constexpr uint32_t kLeafPieces = 1u << kMaxL;           // input pieces of a leaf, at most
-constexpr size_t kLeafSmem = (size_t)kM * kLeafStride * 4 + 2 * kLeafPieces * 8 + 16;
 
 // Offset (bits) of input piece e of the node `path` at level L (digits base 3, most significant
 // = level 0; 0 = P: x0 ^ x1 doubles the pieces, 1 = Q: x0, 2 = R: x1) — leaf_offsets
@@ -812,10 +813,7 @@ constexpr int kLfAS = 3;                    // A ring (TMEM, 64 columns per stag
 constexpr int kLfEW = 16;                   // epilogue warps
 constexpr int kLfAW = 4;                    // A producer warps: sets of 4 (one per sub-partition)
 constexpr int kLfSets = kLfAW / 4;          // a set fills every kLfSets-th stage
-#ifndef SSBH_EXP_BW
-#define SSBH_EXP_BW 6
-#endif
-constexpr int kLfBW = SSBH_EXP_BW;          // background-build warps (parent mode): 28 warps in
+constexpr int kLfBW = 6;                    // background-build warps (parent mode): 28 warps in
                                             // all keep 72 registers per thread; 8 build warps
                                             // (30 warps, 64 registers) measured 25.1 ms
 constexpr int kLfMmaW = kLfEW, kLfLoadW = kLfEW + 1, kLfProd0 = kLfEW + 2;

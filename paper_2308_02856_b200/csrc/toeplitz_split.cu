@@ -340,10 +340,7 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
     if (g.per_block) split_seeds(d_sbuf, sbuf_words, lay, nown, g, jj0, d_vs, st);
 }
 
-#ifndef SSBH_EXP_TREE_KB
-#define SSBH_EXP_TREE_KB 112
-#endif
-constexpr size_t kTreeSmemCap = SSBH_EXP_TREE_KB * 1024;
+constexpr size_t kTreeSmemCap = 112 * 1024;
 
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
                               uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
