@@ -191,6 +191,32 @@ def test_split_deep_levels_and_leaf_kernels(dev, oracle, levels, leaf, ovr):
     assert (keys[0] == keys[1]).all()
 
 
+@pytest.mark.parametrize("levels", [8, 9, None], ids=["L8-leaf-256-pieces", "L9-parent", "auto"])
+def test_split_config5_block_shape(dev, oracle, levels, ovr):
+    """Config 5's block shape (k = 2^21, m = 2^22) on two blocks: L = 8 runs the leaf GEMM's leaf
+    mode with up to 256 input pieces per leaf (more than the 4 A warps x 32 lanes that compute
+    the piece offsets in one pass), L = 9 its parent mode with 8-level combines; the cost model
+    picks 9. Keys against the LOP3 engine."""
+    import torch
+
+    ovr(split_levels=-1 if levels is None else levels)
+    n, s, k = (1 << 23) + 12345, 2, 1 << 21
+    x = oracle.make_input(31, 0.5, n)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    keys = []
+    for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
+        plan = dev.Plan(n, s, k, 15, 16, engine=engine)
+        if engine == dev.ENGINE_TENSOR and _split_possible():
+            assert plan.hash_kernel == "k_leaf_gemm+split"
+            assert plan.split_geometry[:2] == (9 if levels is None else levels, 2)
+        d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr())
+        plan.check()
+        keys.append(d_key.cpu().numpy())
+        plan.close()
+    assert (keys[0] == keys[1]).all()
+
+
 @pytest.mark.parametrize("levels,budget_mb", [(1, None), (3, 2), (4, None), (None, None)],
                          ids=["L1", "L3-batched", "L4", "auto"])
 def test_split_per_block_seeds(dev, oracle, levels, budget_mb, ovr):
