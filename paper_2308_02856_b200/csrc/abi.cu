@@ -524,6 +524,12 @@ struct ssbh_plan {
     uint64_t chunk_bits = 0;
     uint64_t stream_samp[4]{}, stream_hash[4]{};
     uint32_t stream_launches = 0;
+    // forward streaming (two-level streaming plans): no count pass over the whole input; block
+    // j's rounds fill [j * fwd_cap, ...) of yfwd in round order, run_rank = its length so far
+    bool fwd_stream = false;
+    uint64_t fwd_cap = 0;  // bits per block region (a multiple of 256)
+    uint64_t next_chunk = 0;  // forward streaming takes the input chunks in order
+    DBuf yfwd, run_rank;
     // hash engine (shared-seed plans may run on the tensor cores, toeplitz_mma.cu)
     int engine = kEngineLop3;
     MmaGeom mma{};
@@ -714,10 +720,19 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
         if (!e) e = alloc(pl->gsum_b, (size_t)bg.b.ngroups * bg.b.nown * 8);
         if (!e) e = alloc(pl->nj_b, (size_t)bg.nbuckets * bg.b.nown * 8);
     }
-    // single-level count table (bucketed streaming plans keep it: its scanned rows give every
-    // block's rank at the start of each input chunk)
-    if (!e && (!pl->bucketed || pl->streaming)) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
-    if (!e && (!pl->bucketed || pl->streaming)) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
+    // single-level count table (two-level streaming plans do without: forward streaming)
+    pl->fwd_stream = pl->bucketed && pl->streaming;
+    if (!e && !pl->bucketed) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
+    if (!e && !pl->bucketed) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
+    if (!e && pl->fwd_stream) {
+        // region per block: mean + 16 sigma of Binomial(n, 1/s) (a longer block raises the
+        // overflow flag -> SSBH_CUDA, never silently)
+        const double mean = (double)n / (double)params->n_subblocks;
+        const uint64_t cap = (uint64_t)(mean + 16.0 * std::sqrt(mean) + 64.0);
+        pl->fwd_cap = round_up(cap, 256);
+        e = alloc(pl->yfwd, (size_t)nown * (pl->fwd_cap / 8) + 64);
+        if (!e) e = alloc(pl->run_rank, (size_t)nown * 4 + 16);
+    }
     if (!e) e = alloc(pl->ybuf, pl->ybuf_words * 4);
     if (!e) e = alloc(pl->sbuf, pl->sbuf_words * 4);
     if (!e && !pl->direct_out) e = alloc(pl->scratch, (size_t)nown * pl->kw * 4);
@@ -780,6 +795,7 @@ extern "C" ssbh_status ssbh_plan_stream_begin(ssbh_plan* pl, const uint64_t* sam
     std::memcpy(pl->stream_samp, samp_key ? samp_key : pl->p.samp_key, 32);
     std::memcpy(pl->stream_hash, hash_key ? hash_key : pl->p.hash_key, 32);
     pl->stream_launches = 0;
+    pl->next_chunk = 0;
     if (auto s = phase_sample(pl, nullptr, nullptr, pl->stream_samp, st, pl->stream_launches))
         return s;
     return check_launch("stream_begin");
@@ -797,17 +813,25 @@ extern "C" ssbh_status ssbh_plan_stream_chunk(ssbh_plan* pl, uint64_t chunk_inde
     pl->last_stream = st;
     const Layout lay = pl->lay.view();
     if (pl->bucketed) {
-        // two-level split of this chunk; ranks continue from the block's rounds in earlier
-        // chunks = the scanned single-level table's row at the chunk start
+        // two-level split of this chunk. The blocks' ranks continue from chunk to chunk in a
+        // running array (no count pass over the whole input), so the chunks come in order.
+        if (chunk_index != pl->next_chunk)
+            return fail(SSBH_INVALID_ARGUMENT,
+                        "stream_chunk: a two-level streaming plan takes its chunks in order "
+                        "(expected chunk %llu)", (unsigned long long)pl->next_chunk);
+        ++pl->next_chunk;
         const SamplerGeom ga = geom_with_n(pl->bg.a, count);
         if (auto s = bucket_passes(pl, ga, pl->stream_samp, first, d_chunk, nullptr, nullptr, st,
                                    pl->stream_launches))
             return s;
-        const uint32_t* rank_base =
-            pl->counts.as<uint32_t>() + (first >> pl->geom.chunk_shift) * (uint64_t)pl->nown;
+        // forward streaming: ranks continue from the blocks' lengths so far; the bits go to the
+        // blocks' fixed regions in round order
         launch_bucket_scatter(pl->bg, pl->staging.as<uint16_t>(), pl->counts_b.as<uint32_t>(),
-                              lay.nj, lay.yoff, pl->ybuf.as<uint32_t>(), rank_base, st);
-        pl->stream_launches += 1;
+                              lay.nj, lay.yoff, pl->yfwd.as<uint32_t>(),
+                              pl->run_rank.as<uint32_t>(), st, pl->fwd_cap);
+        launch_add_ranks(pl->run_rank.as<uint32_t>(), pl->nj_b.as<unsigned long long>(), pl->nown,
+                         pl->fwd_cap, &lay.stats->pad, st);
+        pl->stream_launches += 2;
         return check_launch("stream_chunk");
     }
     launch_scatter_stream(pl->geom, pl->stream_samp, d_chunk, first, count,
@@ -937,6 +961,11 @@ static ssbh_status seg_sample(ssbh_plan* pl, const uint32_t* d_input, const uint
     if (pl->bucketed || pl->streaming)
         CU(cudaMemsetAsync(&lay.stats->pad, 0, 4, st));  // kFlagBucketOverflow of this run
     if (pl->late_input) d_input = nullptr;  // the data bits join in the split / scatter
+    if (pl->fwd_stream) {  // stream_begin: nothing is counted ahead of the chunks
+        CU(cudaMemsetAsync(pl->run_rank.p, 0, pl->run_rank.bytes, st));
+        CU(cudaMemsetAsync(pl->yfwd.p, 0, pl->yfwd.bytes, st));
+        return SSBH_OK;
+    }
     if (pl->bucketed && !pl->streaming) {
         if (auto s = bucket_passes(pl, pl->bg.a, sk, 0, d_input, d_keep, nullptr, st, launches))
             return s;
@@ -1167,6 +1196,19 @@ static ssbh_status phase_sample(ssbh_plan* pl, const uint32_t* d_input, const ui
 // Phase C (direct launches): S2 + S3 with their events.
 static ssbh_status phase_finish(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                                 const uint64_t* hk, cudaStream_t st, uint32_t& launches) {
+    if (pl->fwd_stream) {
+        // block lengths = the running ranks; layout; the forward regions reversed into the
+        // compact padded blocks the hash kernels read
+        const Layout lay = pl->lay.view();
+        launch_ranks_to_nj(pl->run_rank.as<uint32_t>(), pl->nown, lay.nj, st);
+        launch_layout(lay, pl->nown, pl->p.out_bits, pl->rowtiles, pl->kt, pl->p.per_block_seed,
+                      pl->p.block_limit, st);
+        CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
+        launch_reverse_blocks(pl->yfwd.as<uint32_t>(), pl->fwd_cap / 32, lay, pl->nown,
+                              pl->p.n_rounds / pl->p.n_subblocks / 32 + 1,
+                              pl->ybuf.as<uint32_t>(), st);
+        launches += 3;
+    }
     rec(pl, 2, st);
     if (auto s = seg_seeds(pl, hk, st, launches)) return s;
     rec(pl, 3, st);

@@ -183,9 +183,20 @@ void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32
                          cudaStream_t st);
 // Pass B scatter into the reversed blocks; d_rank_base (per owned block, may be null) is
 // added to every rank (streaming: the block's rounds in earlier input chunks).
+// fwd_cap > 0 (forward streaming): bit r of block jf goes to jf * fwd_cap + r of d_ybuf.
 void launch_bucket_scatter(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_offsets_b,
                            const unsigned long long* d_nj, const unsigned long long* d_yoff,
-                           uint32_t* d_ybuf, const uint32_t* d_rank_base, cudaStream_t st);
+                           uint32_t* d_ybuf, const uint32_t* d_rank_base, cudaStream_t st,
+                           uint64_t fwd_cap = 0);
+// Forward streaming (two-level streaming plans): no count pass over the whole input — every
+// block gets a fixed-capacity region filled in round order chunk by chunk; run_rank holds the
+// blocks' lengths so far, and at the end the regions are reversed into the compact layout.
+void launch_add_ranks(uint32_t* d_run_rank, const unsigned long long* d_nj_chunk, uint32_t nown,
+                      uint64_t cap, uint32_t* d_flags, cudaStream_t st);
+void launch_ranks_to_nj(const uint32_t* d_run_rank, uint32_t nown, unsigned long long* d_nj,
+                        cudaStream_t st);
+void launch_reverse_blocks(const uint32_t* d_fwd, uint64_t cap_words, const Layout& lay,
+                           uint32_t nown, uint64_t mean_words, uint32_t* d_ybuf, cudaStream_t st);
 
 // ---- layout / seeds / hash -----------------------------------------------------------
 // Computes ypad/ktl/yoff/items/soff/stats from lay.nj for nown blocks.

@@ -477,6 +477,8 @@ struct ScatterArgs {
     const unsigned long long* tot;  // kModeBucket: rounds per bucket (end of the last chunk)
     uint64_t cpb;               // staged kModeBits: chunks per bucket region (0: not staged)
     const uint32_t* rank_base;  // staged kModeBits: per-block rank offset (streaming) or null
+    uint64_t fwd_cap;           // staged kModeBits, forward streaming: block jf's bit r goes to
+                                // jf * fwd_cap + r of ybuf (n_j unknown yet); 0: reversed blocks
 };
 
 template <typename Src, bool kSmemRow, int kMode>
@@ -596,9 +598,14 @@ __global__ void __launch_bounds__(256) k_scatter(Src src, ScatterArgs a) {
                         if (a.cpb) {  // staged rounds: chunk c lies in bucket c / cpb
                             const uint32_t jf = (uint32_t)((c / a.cpb) << a.bshift) + jj;
                             const uint64_t r = pos + (a.rank_base ? __ldg(a.rank_base + jf) : 0u);
-                            const uint64_t qb =
-                                __ldg(a.yoff + jf) * 32ull + __ldg(a.nj + jf) - 1ull - r;
-                            atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
+                            if (a.fwd_cap) {
+                                const uint64_t qb = (uint64_t)jf * a.fwd_cap + r;
+                                if (r < a.fwd_cap) atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
+                            } else {
+                                const uint64_t qb =
+                                    __ldg(a.yoff + jf) * 32ull + __ldg(a.nj + jf) - 1ull - r;
+                                atomicOr(a.ybuf + (qb >> 5), 1u << (qb & 31));
+                            }
                         } else {
                             const unsigned long long e =
                                 kSmemRow ? s_key[jj]
@@ -1035,12 +1042,40 @@ void launch_bucket_count(const BucketGeom& bg, const uint16_t* d_staging, uint32
 
 void launch_bucket_scatter(const BucketGeom& bg, const uint16_t* d_staging, uint32_t* d_offsets_b,
                            const unsigned long long* d_nj, const unsigned long long* d_yoff,
-                           uint32_t* d_ybuf, const uint32_t* d_rank_base, cudaStream_t st) {
+                           uint32_t* d_ybuf, const uint32_t* d_rank_base, cudaStream_t st,
+                           uint64_t fwd_cap) {
     ScatterArgs a = scatter_args(bg.b, d_offsets_b, d_nj, d_yoff, d_ybuf, nullptr, nullptr);
     a.bshift = bg.shift;
     a.cpb = bg.cpb;
     a.rank_base = d_rank_base;
+    a.fwd_cap = fwd_cap;
     scatter_launch<kModeBits>(PayloadSrc<uint16_t>{d_staging}, a, st);
+}
+
+// Forward streaming: the blocks' running ranks after an input chunk (+= the chunk's per-block
+// totals of pass B; a rank past the block's capacity raises the overflow flag), and the block
+// lengths at the end.
+__global__ void k_add_ranks(uint32_t* __restrict__ run_rank,
+                            const unsigned long long* __restrict__ nj_chunk, uint32_t nown,
+                            uint64_t cap, uint32_t* __restrict__ flags) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nown) return;
+    const unsigned long long r = run_rank[j] + nj_chunk[j];
+    if (r > cap) atomicOr(flags, kFlagBucketOverflow);
+    run_rank[j] = (uint32_t)(r > cap ? cap : r);
+}
+__global__ void k_ranks_to_nj(const uint32_t* __restrict__ run_rank, uint32_t nown,
+                              unsigned long long* __restrict__ nj) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nown) nj[j] = run_rank[j];
+}
+void launch_add_ranks(uint32_t* d_run_rank, const unsigned long long* d_nj_chunk, uint32_t nown,
+                      uint64_t cap, uint32_t* d_flags, cudaStream_t st) {
+    if (nown) k_add_ranks<<<(nown + 255) / 256, 256, 0, st>>>(d_run_rank, d_nj_chunk, nown, cap, d_flags);
+}
+void launch_ranks_to_nj(const uint32_t* d_run_rank, uint32_t nown, unsigned long long* d_nj,
+                        cudaStream_t st) {
+    if (nown) k_ranks_to_nj<<<(nown + 255) / 256, 256, 0, st>>>(d_run_rank, nown, d_nj);
 }
 
 void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_offsets,

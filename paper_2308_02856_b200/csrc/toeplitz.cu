@@ -259,6 +259,21 @@ __global__ void k_reverse(const uint32_t* __restrict__ x, uint64_t n, uint32_t* 
         y[u] = reversed_word(x, n, u);
 }
 
+// Forward streaming: block jj's bits sit in order at fwd + jj * cap_words (capacity cap_words
+// words); its reversed, padded form goes to ybuf + yoff[jj] (ypad[jj] words).
+__global__ void k_reverse_blocks(const uint32_t* __restrict__ fwd, uint64_t cap_words, Layout lay,
+                                 uint32_t nown, uint32_t* __restrict__ ybuf) {
+    for (uint32_t jj = blockIdx.y; jj < nown; jj += gridDim.y) {
+        const uint32_t* x = fwd + (uint64_t)jj * cap_words;
+        const uint64_t n = lay.nj[jj];
+        uint32_t* y = ybuf + lay.yoff[jj];
+        const uint64_t yp = lay.ypad[jj];
+        for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < yp;
+             u += (uint64_t)gridDim.x * blockDim.x)
+            y[u] = reversed_word(x, n, u);
+    }
+}
+
 // Batched API path: CTA row blockIdx.y = block; the blockIdx.x slices of a row copy its seed
 // (m+n-1 bits, tail masked, pre-shifted one bit) into the per-block seed region and write the
 // reversed input into its y region, gridDim.x * blockDim.x words per sweep.
@@ -520,6 +535,14 @@ void launch_reverse(const uint32_t* d_x32, uint64_t nbits, uint32_t* d_y, uint64
     if (!ywords) return;
     const uint64_t blocks = std::min<uint64_t>((ywords + 255) / 256, 148ull * 16);
     k_reverse<<<(unsigned)blocks, 256, 0, st>>>(d_x32, nbits, d_y, ywords);
+}
+
+void launch_reverse_blocks(const uint32_t* d_fwd, uint64_t cap_words, const Layout& lay,
+                           uint32_t nown, uint64_t mean_words, uint32_t* d_ybuf, cudaStream_t st) {
+    if (!nown) return;
+    const unsigned gx = (unsigned)std::min<uint64_t>(std::max<uint64_t>(1, (mean_words + 255) / 256), 64);
+    const unsigned gy = std::min<unsigned>(nown, 65535u);
+    k_reverse_blocks<<<dim3(gx, gy), 256, 0, st>>>(d_fwd, cap_words, lay, nown, d_ybuf);
 }
 
 int hash_grid_size(int device) {

@@ -676,10 +676,14 @@ def test_two_level_streaming(dev, oracle, two_level):
     for (n, s, k, cb, pb) in ((600000, 1000, 64, 1 << 16, False), (300001, 257, 96, 1 << 15, True)):
         x = oracle.make_input(int(rng.integers(1000)), 0.5, n)
         want, wnj = oracle.extract(x, n, s, 31, 32, pb, k)
-        order = list(rng.permutation((n + cb - 1) // cb))
-        got, nj, _ = _stream_run(dev, x, n, s, k, 31, 32, cb, per_block=pb, order=order)
+        # two-level streaming plans keep the blocks' running ranks from chunk to chunk (no count
+        # pass over the whole input): chunks in order; any other order is refused
+        got, nj, _ = _stream_run(dev, x, n, s, k, 31, 32, cb, per_block=pb)
         assert (nj == wnj).all()
         assert (got[: len(want)] == want).all(), (n, s, k, cb, pb)
+        order = list(range((n + cb - 1) // cb))[::-1]
+        with pytest.raises(ValueError):
+            _stream_run(dev, x, n, s, k, 31, 32, cb, per_block=pb, order=order)
     n, s, k = 400000, 600, 64
     x = oracle.make_input(9, 0.5, n)
     want, _ = oracle.extract(x, n, s, 31, 32, 0, k)
