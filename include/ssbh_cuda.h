@@ -283,10 +283,15 @@ ssbh_status ssbh_extract_sifted(const ssbh_extract_params* params, const uint64_
 /* Streaming plans — inputs fed in pieces (BASELINE config 5: 2^37 rounds "streamed in 8
  * chunks"; also any input larger than device memory). No per-round payload buffer: V_i is
  * recomputed by Threefry in the scatter pass. Every chunk except the last holds exactly
- * chunk_bits rounds (a multiple of 1024); chunks may be fed in any order, each once.
+ * chunk_bits rounds (a multiple of 1024), each chunk once. Plans with fewer than 4096 owned
+ * blocks take their chunks in any order; larger plans (two-level partition, config 5) keep the
+ * blocks' running lengths from chunk to chunk instead of counting the whole input first and
+ * take them in order 0, 1, 2, ... (another index -> SSBH_INVALID_ARGUMENT).
  *   ssbh_plan_stream_begin  : count pass over all n rounds (needs no input), scan, layout
+ *                             (two-level plans: only zeroes the blocks' regions)
  *   ssbh_plan_stream_chunk  : chunk c's rounds [c*chunk_bits, ...) as uint32 words on device
- *   ssbh_plan_stream_finish : seeds, hash, concatenation into d_key (+ lengths)
+ *   ssbh_plan_stream_finish : (two-level plans: lengths, layout, block reversal,) seeds, hash,
+ *                             concatenation into d_key (+ lengths)
  * then ssbh_plan_check as for in-memory plans. */
 ssbh_status ssbh_plan_create_streaming(const ssbh_extract_params* params, uint64_t chunk_bits,
                                        ssbh_plan** plan);
