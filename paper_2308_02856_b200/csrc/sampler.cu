@@ -910,12 +910,13 @@ void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint
         threefry_ks(key, k.ks);
         int kbits = 1;
         while ((1ull << kbits) < g.nown) ++kbits;
-        const size_t shm = (size_t)g.nown * 8 * 8;  // rank row + owner row per warp
+        const int cwarps = 8;
+        const size_t shm = (size_t)g.nown * 8 * cwarps;  // rank row + owner row per warp
         const uint64_t blocks = std::min<uint64_t>((g.nchunks + 7) / 8, (uint64_t)sm_count() * 8);
         auto go = [&](auto kern) {
             if (shm > 48 * 1024)
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
+            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), cwarps * 32, shm, st>>>(
                 k, g.n, g.s, g.j_lo, g.nown, d_in32, d_keep, static_cast<uint32_t*>(d_payload),
                 g.chunk_shift, g.nchunks, kbits, d_counts);
         };
