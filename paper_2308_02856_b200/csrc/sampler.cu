@@ -296,6 +296,72 @@ __global__ void __launch_bounds__(256) k_scatter_ranked(const uint32_t* __restri
     }
 }
 
+// Ranked pass 3, windowed: a CTA takes one chunk at a time. The rounds of one (chunk, block)
+// cell land on a run of consecutive bits that ends at top = the block's last bit - the chunk's
+// scanned offset, so their bits are first ORed into a window of W words per block in shared
+// memory (plane-major; word w of the window is global word (top >> 5) - w) and each non-zero
+// window word goes out as ONE global red.or — a cell of ~32 rounds costs ~2 L2 atomics instead
+// of one per set bit (the per-bit form is bound by the L2's atomic throughput). Ranks past the
+// window fall back to the per-bit global atomic.
+template <bool kLate>
+__global__ void __launch_bounds__(256) k_scatter_windowed(const uint32_t* __restrict__ payload,
+                                                          const uint32_t* __restrict__ in32_late,
+                                                          uint64_t n, int cs, uint64_t nchunks,
+                                                          uint32_t j_lo, uint32_t nown, uint32_t W,
+                                                          const uint32_t* __restrict__ offs,
+                                                          const unsigned long long* __restrict__ nj,
+                                                          const unsigned long long* __restrict__ yoff,
+                                                          uint32_t* __restrict__ ybuf) {
+    constexpr int U = 8;
+    extern __shared__ __align__(16) uint8_t rk_smem[];
+    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(rk_smem);
+    unsigned long long* top = s_key + nown;
+    uint32_t* win = reinterpret_cast<uint32_t*>(top + nown);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
+        s_key[t] = yoff[t] * 32ull + nj[t] - 1ull;
+    for (uint32_t t = threadIdx.x; t < nown * W; t += blockDim.x) win[t] = 0u;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        __syncthreads();  // s_key / the zeroed window; the previous chunk's flush
+        for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
+            top[t] = s_key[t] - offs[c * nown + t];
+        __syncthreads();
+        const uint64_t i0 = c << cs, i1 = min(n, (c + 1) << cs);
+        for (uint64_t ib = i0 + (threadIdx.x & ~31u) * U; ib < i1; ib += (uint64_t)blockDim.x * U) {
+            uint32_t p[U], lw[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint64_t i = ib + 32 * q + lane;
+                p[q] = i < i1 ? payload[i] : 0x7fffu;
+                if (kLate) lw[q] = i < i1 ? __ldg(in32_late + (i >> 5)) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const uint32_t v = p[q] & 0x7fffu, jj = v - j_lo;
+                const uint32_t bit = kLate ? (lw[q] >> lane) & 1u : (p[q] >> 15) & 1u;
+                if (v != 0x7fffu && jj < nown && bit) {
+                    const unsigned long long tp = top[jj];
+                    const uint32_t o = (uint32_t)tp & 31u, r = p[q] >> 16;
+                    const uint32_t w = (r + 31u - o) >> 5, b = 1u << ((o - r) & 31u);
+                    if (w < W)
+                        atomicOr(win + (size_t)w * nown + jj, b);
+                    else
+                        atomicOr(ybuf + ((tp - r) >> 5), b);
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < nown * W; t += blockDim.x) {
+            const uint32_t val = win[t];
+            if (val) {
+                const uint32_t w = t / nown, jj = t - w * nown;
+                atomicOr(ybuf + ((top[jj] >> 5) - w), val);
+                win[t] = 0u;
+            }
+        }
+    }
+}
+
 // Pass 1, large key spaces: counts go straight to the global (chunk, key) table.
 template <typename Src>
 __global__ void __launch_bounds__(256) k_count_global(Src src, uint64_t n, uint32_t nkeys, int cs,
@@ -1085,6 +1151,27 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
                     const unsigned long long* d_csr_off, cudaStream_t st,
                     const uint32_t* d_in32_late) {
     if (g.n == 0 || g.nown == 0) return;
+    if (g.ranked && !d_idx_out && (1ull << g.chunk_shift) >= 8ull * g.s) {
+        // cells of >= 8 rounds: combine a cell's bits in shared memory first. Window = mean
+        // cell + 6 sigma + the word alignment, within 48 KB.
+        const double mean = (double)(1ull << g.chunk_shift) / (double)g.s;
+        uint32_t W = (uint32_t)((mean + 6.0 * std::sqrt(mean) + 31.0) / 32.0) + 1;
+        W = std::max<uint32_t>(2, std::min<uint32_t>(W, (48u * 1024u) / (4u * g.nown)));
+        const size_t shm = (size_t)g.nown * (16 + 4 * (size_t)W);
+        const uint64_t blocks = std::min<uint64_t>(g.nchunks, (uint64_t)sm_count() * 8);
+        auto go = [&](auto kern) {
+            if (shm > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
+                static_cast<const uint32_t*>(d_payload), d_in32_late, g.n, g.chunk_shift, g.nchunks,
+                g.j_lo, g.nown, W, d_offsets, d_nj, d_yoff, d_ybuf);
+        };
+        if (d_in32_late)
+            go(k_scatter_windowed<true>);
+        else
+            go(k_scatter_windowed<false>);
+        return;
+    }
     if (g.ranked && !d_idx_out) {
         const size_t shm = (size_t)g.nown * 8 + (size_t)g.nown * 4 * 8 + 16;
         const uint64_t blocks = std::min<uint64_t>((g.nchunks + 7) / 8, (uint64_t)sm_count() * 16);
