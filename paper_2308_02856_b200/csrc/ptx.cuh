@@ -80,6 +80,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // has a single active thread and feeds tcgen05.mma / commit their uniform-register operands
 // directly; under `if (lane == 0)` it wrapped every MMA in an ELECT / R2UR.BROADCAST / BRA.U.ANY
 // loop (17 SASS per MMA, ~115 clocks of issue per 128-clock MMA: the tensor pipe starved).
+// Predicated shared-memory OR without a branch around it (reduction form: no return value).
+__device__ __forceinline__ void red_or_shared_if(uint32_t addr, uint32_t v, bool p) {
+    asm volatile(
+        "{\n.reg .pred P;\nsetp.ne.u32 P, %2, 0;\n@P red.shared.or.b32 [%0], %1;\n}\n" ::"r"(addr),
+        "r"(v), "r"((uint32_t)p));
+}
+
 __device__ __forceinline__ bool elect_one() {
     uint32_t p;
     asm volatile(

@@ -303,62 +303,97 @@ __global__ void __launch_bounds__(256) k_scatter_ranked(const uint32_t* __restri
 // window word goes out as ONE global red.or — a cell of ~32 rounds costs ~2 L2 atomics instead
 // of one per set bit (the per-bit form is bound by the L2's atomic throughput). Ranks past the
 // window fall back to the per-bit global atomic.
+#ifndef SSBH_EXP_WIN_T
+#define SSBH_EXP_WIN_T 256
+#endif
+constexpr int kWinThreads = SSBH_EXP_WIN_T;
+constexpr uint32_t kWinMaxOwn = 1536;  // make_ranked: nown * 64 B <= 96 KB
+constexpr int kWinKeys = (kWinMaxOwn + kWinThreads - 1) / kWinThreads;
 template <bool kLate>
-__global__ void __launch_bounds__(256) k_scatter_windowed(const uint32_t* __restrict__ payload,
-                                                          const uint32_t* __restrict__ in32_late,
-                                                          uint64_t n, int cs, uint64_t nchunks,
-                                                          uint32_t j_lo, uint32_t nown, uint32_t W,
-                                                          const uint32_t* __restrict__ offs,
-                                                          const unsigned long long* __restrict__ nj,
-                                                          const unsigned long long* __restrict__ yoff,
-                                                          uint32_t* __restrict__ ybuf) {
+__global__ void __launch_bounds__(kWinThreads) k_scatter_windowed(
+    const uint32_t* __restrict__ payload, const uint32_t* __restrict__ in32_late, uint64_t n, int cs,
+    uint64_t nchunks, uint32_t j_lo, uint32_t nown, uint32_t W, const uint32_t* __restrict__ offs,
+    const unsigned long long* __restrict__ nj, const unsigned long long* __restrict__ yoff,
+    uint32_t* __restrict__ ybuf) {
     constexpr int U = 8;
     extern __shared__ __align__(16) uint8_t rk_smem[];
-    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(rk_smem);
-    unsigned long long* top = s_key + nown;
-    uint32_t* win = reinterpret_cast<uint32_t*>(top + nown);
+    unsigned long long* top = reinterpret_cast<unsigned long long*>(rk_smem);  // [nown]
+    uint32_t* win = reinterpret_cast<uint32_t*>(top + nown);                    // [W][nown]
+    const uint32_t* top_lo = reinterpret_cast<const uint32_t*>(top);
+    const uint32_t win_a = smem_u32(win);
     const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
-        s_key[t] = yoff[t] * 32ull + nj[t] - 1ull;
-    for (uint32_t t = threadIdx.x; t < nown * W; t += blockDim.x) win[t] = 0u;
+    // the last bit of this thread's blocks: rank r of a chunk lands on it - (offset + r)
+    unsigned long long key[kWinKeys];
+#pragma unroll
+    for (int k = 0; k < kWinKeys; ++k) {
+        const uint32_t t = threadIdx.x + k * kWinThreads;
+        key[k] = t < nown ? yoff[t] * 32ull + nj[t] - 1ull : 0ull;
+    }
+    for (uint32_t t = threadIdx.x; t < nown * W; t += kWinThreads) win[t] = 0u;
     for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        __syncthreads();  // s_key / the zeroed window; the previous chunk's flush
-        for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x)
-            top[t] = s_key[t] - offs[c * nown + t];
+        __syncthreads();  // the zeroed window; the previous chunk's flush
+#pragma unroll
+        for (int k = 0; k < kWinKeys; ++k) {
+            const uint32_t t = threadIdx.x + k * kWinThreads;
+            if (t < nown) top[t] = key[k] - offs[c * nown + t];
+        }
         __syncthreads();
-        const uint64_t i0 = c << cs, i1 = min(n, (c + 1) << cs);
-        for (uint64_t ib = i0 + (threadIdx.x & ~31u) * U; ib < i1; ib += (uint64_t)blockDim.x * U) {
+        const uint64_t i0 = c << cs;
+        const uint32_t len = (uint32_t)(min(n, (c + 1) << cs) - i0);
+        const uint32_t* pl = payload + i0 + lane;
+        const uint32_t* lt = kLate ? in32_late + (i0 >> 5) : nullptr;
+        for (uint32_t ib = (threadIdx.x & ~31u) * U; ib < len; ib += kWinThreads * U) {
             uint32_t p[U], lw[U];
+            if (ib + 32 * U <= len) {
 #pragma unroll
-            for (int q = 0; q < U; ++q) {
-                const uint64_t i = ib + 32 * q + lane;
-                p[q] = i < i1 ? payload[i] : 0x7fffu;
-                if (kLate) lw[q] = i < i1 ? __ldg(in32_late + (i >> 5)) : 0u;
+                for (int q = 0; q < U; ++q) {
+                    p[q] = pl[ib + 32 * q];
+                    if (kLate) lw[q] = __ldg(lt + (ib >> 5) + q);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const bool in = ib + 32 * q + lane < len;
+                    p[q] = in ? pl[ib + 32 * q] : 0x7fffu;
+                    if (kLate) lw[q] = in ? __ldg(lt + (ib >> 5) + q) : 0u;
+                }
             }
+            // straight-line per round: sifted-out rounds carry block 0x7fff (>= j_lo + nown)
+            bool past = false;
 #pragma unroll
             for (int q = 0; q < U; ++q) {
-                const uint32_t v = p[q] & 0x7fffu, jj = v - j_lo;
-                const uint32_t bit = kLate ? (lw[q] >> lane) & 1u : (p[q] >> 15) & 1u;
-                if (v != 0x7fffu && jj < nown && bit) {
-                    const unsigned long long tp = top[jj];
-                    const uint32_t o = (uint32_t)tp & 31u, r = p[q] >> 16;
-                    const uint32_t w = (r + 31u - o) >> 5, b = 1u << ((o - r) & 31u);
-                    if (w < W)
-                        atomicOr(win + (size_t)w * nown + jj, b);
-                    else
-                        atomicOr(ybuf + ((tp - r) >> 5), b);
+                const uint32_t jj = (p[q] & 0x7fffu) - j_lo;
+                const uint32_t bit = kLate ? (lw[q] >> lane) & 1u : p[q] & 0x8000u;
+                const bool ok = jj < nown && bit;
+                const uint32_t jc = ok ? jj : 0u;
+                const uint32_t o = top_lo[2 * jc] & 31u, r = p[q] >> 16;
+                const uint32_t w = (r + 31u - o) >> 5;
+                red_or_shared_if(win_a + (w * nown + jc) * 4u, 1u << ((o - r) & 31u), ok && w < W);
+                past |= ok && w >= W;
+            }
+            if (past) {  // a cell longer than the window: per-bit global atomics for its tail
+#pragma unroll 1
+                for (int q = 0; q < U; ++q) {
+                    const uint32_t jj = (p[q] & 0x7fffu) - j_lo;
+                    const uint32_t bit = kLate ? (lw[q] >> lane) & 1u : p[q] & 0x8000u;
+                    if (jj < nown && bit) {
+                        const unsigned long long tp = top[jj];
+                        const uint32_t o = (uint32_t)tp & 31u, r = p[q] >> 16;
+                        if (((r + 31u - o) >> 5) >= W)
+                            atomicOr(ybuf + ((tp - r) >> 5), 1u << ((o - r) & 31u));
+                    }
                 }
             }
         }
         __syncthreads();
-        for (uint32_t t = threadIdx.x; t < nown * W; t += blockDim.x) {
-            const uint32_t val = win[t];
-            if (val) {
-                const uint32_t w = t / nown, jj = t - w * nown;
-                atomicOr(ybuf + ((top[jj] >> 5) - w), val);
-                win[t] = 0u;
+        for (uint32_t w = 0; w < W; ++w)
+            for (uint32_t jj = threadIdx.x; jj < nown; jj += kWinThreads) {
+                const uint32_t val = win[w * nown + jj];
+                if (val) {
+                    atomicOr(ybuf + ((top[jj] >> 5) - w), val);
+                    win[w * nown + jj] = 0u;
+                }
             }
-        }
     }
 }
 
@@ -1157,12 +1192,15 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
         const double mean = (double)(1ull << g.chunk_shift) / (double)g.s;
         uint32_t W = (uint32_t)((mean + 6.0 * std::sqrt(mean) + 31.0) / 32.0) + 1;
         W = std::max<uint32_t>(2, std::min<uint32_t>(W, (48u * 1024u) / (4u * g.nown)));
-        const size_t shm = (size_t)g.nown * (16 + 4 * (size_t)W);
-        const uint64_t blocks = std::min<uint64_t>(g.nchunks, (uint64_t)sm_count() * 8);
+        const size_t shm = (size_t)g.nown * (8 + 4 * (size_t)W);
         auto go = [&](auto kern) {
             if (shm > 48 * 1024)
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, shm, st>>>(
+            int per_sm = 1;  // one wave of resident CTAs: the chunks are equal work
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWinThreads, shm);
+            const uint64_t blocks =
+                std::min<uint64_t>(g.nchunks, (uint64_t)sm_count() * std::max(per_sm, 1));
+            kern<<<(unsigned)std::max<uint64_t>(blocks, 1), kWinThreads, shm, st>>>(
                 static_cast<const uint32_t*>(d_payload), d_in32_late, g.n, g.chunk_shift, g.nchunks,
                 g.j_lo, g.nown, W, d_offsets, d_nj, d_yoff, d_ybuf);
         };

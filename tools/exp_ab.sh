@@ -17,6 +17,6 @@ import sys,json
 for l in sys.stdin:
     try: d=json.loads(l)
     except Exception: print(l.strip()); continue
-    if 'ms_hash' in d: print(d['win'][-40:], 'hash', d['ms_hash'], 'total', d['ms_total'])
+    if 'ms_hash' in d: print(d['win'][-40:], 'scatter', d['ms_scatter'], 'hash', d['ms_hash'], 'total', d['ms_total'])
     elif 'key_sha' in d: print(d['win'][-40:], 'sha', d['key_sha'])
 "
