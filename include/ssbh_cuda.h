@@ -246,6 +246,10 @@ typedef struct ssbh_plan_overrides {
     int32_t buckets;            /* -1: heuristic (>= 4096 owned blocks); 0/1: force the
                                    two-level sampler split off/on */
     uint32_t split_budget_mb;   /* leaf buffer budget; 0: default 8192 MiB */
+    int32_t scatter_window;     /* ranked scatter (in-memory single-level plans): 0: model (a
+                                   shared-memory window of mean cell + 6 sigma when a (chunk,
+                                   block) cell holds >= 8 rounds); W > 0: force W window words;
+                                   -1: per-bit global atomics */
 } ssbh_plan_overrides;
 ssbh_status ssbh_set_plan_overrides(const ssbh_plan_overrides* overrides);
 ssbh_status ssbh_get_plan_overrides(ssbh_plan_overrides* overrides);

@@ -115,11 +115,12 @@ class PlanOverrides(C.Structure):
     path a plan takes; never read from the environment."""
     _fields_ = [("engine", C.c_int32), ("split_levels", C.c_int32),
                 ("split_tiled_leaves", C.c_int32), ("shared_tiled", C.c_int32),
-                ("buckets", C.c_int32), ("split_budget_mb", C.c_uint32)]
+                ("buckets", C.c_int32), ("split_budget_mb", C.c_uint32),
+                ("scatter_window", C.c_int32)]
 
 
 DEFAULT_OVERRIDES = dict(engine=0, split_levels=-1, split_tiled_leaves=0, shared_tiled=-1,
-                         buckets=-1, split_budget_mb=0)
+                         buckets=-1, split_budget_mb=0, scatter_window=0)
 
 
 class RoundParams(C.Structure):

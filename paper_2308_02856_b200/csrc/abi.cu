@@ -476,7 +476,7 @@ uint32_t choose_kt(uint64_t mean_nj, uint32_t nown, uint32_t rowtiles, int grid)
 // read from the environment — a plan's kernels depend only on its parameters unless a caller
 // sets these. Process-wide; copied when a plan is created.
 static std::mutex g_over_mu;
-static ssbh_plan_overrides g_over{SSBH_ENGINE_AUTO, -1, 0, -1, -1, 0};
+static ssbh_plan_overrides g_over{SSBH_ENGINE_AUTO, -1, 0, -1, -1, 0, 0};
 
 static ssbh_plan_overrides overrides() {
     std::lock_guard<std::mutex> lk(g_over_mu);
@@ -612,6 +612,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     // in-memory single-level plans: ranks found in pass 1, order-free pass 3 (make_ranked)
     if (!external_payload && !chunk_bits && nown < kBucketMinBlocks && overrides().buckets != 1)
         pl->geom = make_ranked(pl->geom);
+    pl->geom.scatter_window = overrides().scatter_window;
     pl->kw = (uint32_t)((k + 31) / 32);
     pl->rowtiles = (pl->kw + kHashRowWords - 1) / kHashRowWords;
     pl->direct_out = (k % 32) == 0;
@@ -766,7 +767,7 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
 
 extern "C" ssbh_status ssbh_set_plan_overrides(const ssbh_plan_overrides* o) {
     std::lock_guard<std::mutex> lk(g_over_mu);
-    g_over = o ? *o : ssbh_plan_overrides{SSBH_ENGINE_AUTO, -1, 0, -1, -1, 0};
+    g_over = o ? *o : ssbh_plan_overrides{SSBH_ENGINE_AUTO, -1, 0, -1, -1, 0, 0};
     return ok();
 }
 

@@ -89,6 +89,7 @@ struct SamplerGeom {
     bool ranked;           // 4-byte payload V | bit<<15 | rank<<16 (rank = the round's rank in its
                            // block within the warp-chunk, found in pass 1; 0x7fff: sifted out):
                            // pass 3 then needs no ordering at all (make_ranked)
+    int scatter_window = 0;  // ranked pass 3: 0 model, W > 0 forced window words, -1 per-bit
 };
 // Ranked variant of a single-level u16 geometry (in-memory plans): pass 1 is ALU-bound on
 // Threefry, so the stable ranking (ballot peer masks + the warp's running-rank row) costs it

@@ -303,12 +303,10 @@ __global__ void __launch_bounds__(256) k_scatter_ranked(const uint32_t* __restri
 // window word goes out as ONE global red.or — a cell of ~32 rounds costs ~2 L2 atomics instead
 // of one per set bit (the per-bit form is bound by the L2's atomic throughput). Ranks past the
 // window fall back to the per-bit global atomic.
-#ifndef SSBH_EXP_WIN_T
-#define SSBH_EXP_WIN_T 256
-#endif
-constexpr int kWinThreads = SSBH_EXP_WIN_T;
-constexpr uint32_t kWinMaxOwn = 1536;  // make_ranked: nown * 64 B <= 96 KB
-constexpr int kWinKeys = (kWinMaxOwn + kWinThreads - 1) / kWinThreads;
+// A/B (config 3, ms): one warp per chunk with per-bit global atomics 3.06; this kernel 1.42 —
+// insensitive to occupancy (4-7 CTAs per SM) and to prefetching the next group into registers
+// (1.46-1.55): issue slots and the shared-memory pipe are both ~2/3 busy.
+constexpr int kWinThreads = 256;
 template <bool kLate>
 __global__ void __launch_bounds__(kWinThreads) k_scatter_windowed(
     const uint32_t* __restrict__ payload, const uint32_t* __restrict__ in32_late, uint64_t n, int cs,
@@ -317,26 +315,20 @@ __global__ void __launch_bounds__(kWinThreads) k_scatter_windowed(
     uint32_t* __restrict__ ybuf) {
     constexpr int U = 8;
     extern __shared__ __align__(16) uint8_t rk_smem[];
-    unsigned long long* top = reinterpret_cast<unsigned long long*>(rk_smem);  // [nown]
-    uint32_t* win = reinterpret_cast<uint32_t*>(top + nown);                    // [W][nown]
+    // s_key: the last bit of each block (rank r of a chunk lands on it - (offset + r))
+    unsigned long long* s_key = reinterpret_cast<unsigned long long*>(rk_smem);  // [nown]
+    unsigned long long* top = s_key + nown;                                       // [nown]
+    uint32_t* win = reinterpret_cast<uint32_t*>(top + nown);                      // [W][nown]
     const uint32_t* top_lo = reinterpret_cast<const uint32_t*>(top);
     const uint32_t win_a = smem_u32(win);
     const uint32_t lane = threadIdx.x & 31;
-    // the last bit of this thread's blocks: rank r of a chunk lands on it - (offset + r)
-    unsigned long long key[kWinKeys];
-#pragma unroll
-    for (int k = 0; k < kWinKeys; ++k) {
-        const uint32_t t = threadIdx.x + k * kWinThreads;
-        key[k] = t < nown ? yoff[t] * 32ull + nj[t] - 1ull : 0ull;
-    }
+    for (uint32_t t = threadIdx.x; t < nown; t += kWinThreads)
+        s_key[t] = yoff[t] * 32ull + nj[t] - 1ull;
     for (uint32_t t = threadIdx.x; t < nown * W; t += kWinThreads) win[t] = 0u;
     for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        __syncthreads();  // the zeroed window; the previous chunk's flush
-#pragma unroll
-        for (int k = 0; k < kWinKeys; ++k) {
-            const uint32_t t = threadIdx.x + k * kWinThreads;
-            if (t < nown) top[t] = key[k] - offs[c * nown + t];
-        }
+        __syncthreads();  // s_key / the zeroed window; the previous chunk's flush
+        for (uint32_t t = threadIdx.x; t < nown; t += kWinThreads)
+            top[t] = s_key[t] - offs[c * nown + t];
         __syncthreads();
         const uint64_t i0 = c << cs;
         const uint32_t len = (uint32_t)(min(n, (c + 1) << cs) - i0);
@@ -372,7 +364,7 @@ __global__ void __launch_bounds__(kWinThreads) k_scatter_windowed(
                 past |= ok && w >= W;
             }
             if (past) {  // a cell longer than the window: per-bit global atomics for its tail
-#pragma unroll 1
+#pragma unroll
                 for (int q = 0; q < U; ++q) {
                     const uint32_t jj = (p[q] & 0x7fffu) - j_lo;
                     const uint32_t bit = kLate ? (lw[q] >> lane) & 1u : p[q] & 0x8000u;
@@ -1186,13 +1178,16 @@ void launch_scatter(const SamplerGeom& g, const void* d_payload, uint32_t* d_off
                     const unsigned long long* d_csr_off, cudaStream_t st,
                     const uint32_t* d_in32_late) {
     if (g.n == 0 || g.nown == 0) return;
-    if (g.ranked && !d_idx_out && (1ull << g.chunk_shift) >= 8ull * g.s) {
+    if (g.ranked && !d_idx_out &&
+        (g.scatter_window > 0 || (g.scatter_window == 0 && (1ull << g.chunk_shift) >= 8ull * g.s))) {
         // cells of >= 8 rounds: combine a cell's bits in shared memory first. Window = mean
         // cell + 6 sigma + the word alignment, within 48 KB.
         const double mean = (double)(1ull << g.chunk_shift) / (double)g.s;
         uint32_t W = (uint32_t)((mean + 6.0 * std::sqrt(mean) + 31.0) / 32.0) + 1;
         W = std::max<uint32_t>(2, std::min<uint32_t>(W, (48u * 1024u) / (4u * g.nown)));
-        const size_t shm = (size_t)g.nown * (8 + 4 * (size_t)W);
+        if (g.scatter_window > 0)
+            W = std::min<uint32_t>((uint32_t)g.scatter_window, (160u * 1024u) / (4u * g.nown));
+        const size_t shm = (size_t)g.nown * (16 + 4 * (size_t)W);
         auto go = [&](auto kern) {
             if (shm > 48 * 1024)
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);

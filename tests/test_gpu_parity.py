@@ -310,6 +310,42 @@ def test_plan_reuse_and_device_path(dev, oracle, golden):
     plan.close()
 
 
+@pytest.mark.parametrize("window", [-1, 0, 1, 2, 64])
+def test_ranked_scatter_windows(dev, oracle, ovr, window):
+    """Pass 3 of in-memory single-level plans (sampler.cu): per-bit global atomics (-1), the
+    shared-memory cell window from the model (0) and forced windows — 1 and 2 words push most
+    cells past the window onto the per-bit tail, 64 words hold any cell. Host runs take the
+    data bit from the input (late), device runs from the payload; owned block ranges shift
+    j_lo; ragged n leaves a partial last chunk."""
+    import torch
+
+    ovr(scatter_window=window)
+    cases = [(300001, 3, 64, False), (200000, 64, 128, False), (1 << 20, 64, 256, False),
+             (777777, 100, 96, True), (50000, 1, 32, False), (1 << 21, 1024, 32, False)]
+    for n, s, k, pb in cases:
+        x = oracle.make_input(n % 97, 0.5 if s != 100 else 0.2, n)
+        want, wnj = oracle.extract(x, n, s, 31, 32, pb, k)
+        got, nj, _ = dev.extract(x, n, s, k, 31, 32, per_block=pb)
+        assert (nj == wnj).all(), (n, s, k, pb)
+        assert (got == want).all(), (n, s, k, pb)
+        plan = dev.Plan(n, s, k, 31, 32, per_block=pb)
+        d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+        d_key = torch.zeros((s * k + 31) // 32 + 1, dtype=torch.int32, device="cuda")
+        d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+        plan.check()
+        assert (d_len.cpu().numpy().view(np.uint64) == wnj).all()
+        if (s * k) % 64 == 0:
+            assert (d_key.cpu().numpy()[: s * k // 32].view(np.uint64) == want).all(), (n, s, k)
+        plan.close()
+    n, s, k = 400000, 64, 1024
+    x = oracle.make_input(3, 0.5, n)
+    want, wnj = oracle.extract(x, n, s, 2, 3, False, k)
+    parts = [dev.extract(x, n, s, k, 2, 3, block_first=f, block_count=c)[0]
+             for f, c in ((0, 20), (20, 33), (53, 11))]
+    assert (np.concatenate(parts) == want).all()
+
+
 # ----------------------------------------------------------------- BASELINE full sizes
 # SURVEY §8a anchors (computed with the compiled reference); tests/golden/gen_golden.py
 # --config3 re-derives config 3 from the reference into golden.json.
