@@ -1128,7 +1128,8 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 gc.sL = 2 * g.sL;
             }
             launches += 2 + launch_split_combine(pl->vout.as<uint32_t>(), pl->vy.as<uint32_t>(),
-                                                 pl->vrem.as<uint32_t>(), jj0, cnt, pl->kw, gc, out,
+                                                 pl->vrem.as<uint32_t>(), rlay.ktl, jj0, cnt,
+                                                 pl->kw, gc, out,
                                                  pl->direct_out ? pl->p.out_bits / 32 : pl->kw,
                                                  st);
         }

@@ -307,7 +307,8 @@ SplitGeom make_split_geom(uint32_t nown, uint64_t k, uint64_t mean_nj, uint32_t 
                           bool per_block, bool gemm_leaves, uint64_t budget_bytes);
 bool split_applicable(uint64_t k, uint64_t mean_nj, uint32_t L);
 // the batch-relative leaf layout (vlay: yoff/ypad/soff), the remainder layout (rlay: the
-// original input from position T k, seed offset T k) and, for a shared seed, the leaf seeds
+// original input from position T k, seed offset T k; shared seed: rows sorted by remainder
+// length, rlay.ktl[block] = its row) and, for a shared seed, the leaf seeds
 void launch_split_setup(const uint32_t* d_sbuf, uint64_t sbuf_words, const SplitGeom& g,
                         uint32_t* d_vs, const Layout& lay, uint32_t nown, const Layout& vlay,
                         const Layout& rlay, cudaStream_t st);
@@ -318,7 +319,7 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
 // out[jj * out_stride + w] = rem[jj * kw + w] ^ the leaves reaching word w, blocks jj0 + [0, count)
 // returns the launches made; d_tmp (>= the leaf outputs) holds intermediate levels
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
-                              uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
+                              const uint32_t* d_rrow, uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st);
 uint32_t mma_mtiles(uint32_t nown);
 // Leaf mode (the split's shared-seed leaf GEMM): K parts of <= 8192 positions, N tiles innermost.

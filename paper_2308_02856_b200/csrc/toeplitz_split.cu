@@ -134,9 +134,24 @@ __global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vl
     for (uint64_t jj = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jj < nown;
          jj += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t yp = lay.ypad[jj];
-        rlay.yoff[jj] = lay.yoff[jj] + tw;
-        rlay.ypad[jj] = yp > tw ? (uint32_t)(yp - tw) : 0u;
-        rlay.soff[jj] = (g.per_block ? lay.soff[jj] : 0ull) + tw;
+        const uint32_t rp = yp > tw ? (uint32_t)(yp - tw) : 0u;
+        // Shared seed: the remainder GEMM's rows in order of remainder length (rank by
+        // counting), so that an M tile's K extent — its longest row — follows the tile's own
+        // blocks: the tiles of blocks no longer than T k are empty, the others stop at their
+        // quantile instead of the longest remainder of all blocks. rlay.ktl[jj] = the row.
+        uint32_t row = (uint32_t)jj;
+        if (g.gemm) {
+            row = 0;
+            for (uint32_t i = 0; i < nown; ++i) {
+                const uint64_t q = lay.ypad[i];
+                const uint32_t rq = q > tw ? (uint32_t)(q - tw) : 0u;
+                row += (rq < rp || (rq == rp && i < jj)) ? 1u : 0u;
+            }
+        }
+        rlay.yoff[row] = lay.yoff[jj] + tw;
+        rlay.ypad[row] = rp;
+        rlay.soff[row] = (g.per_block ? lay.soff[jj] : 0ull) + tw;
+        rlay.ktl[jj] = row;
     }
 }
 
@@ -151,6 +166,7 @@ __global__ void k_split_layout(Layout lay, uint32_t nown, SplitGeom g, Layout vl
 template <int D>
 __global__ void __launch_bounds__(256) k_split_tree(const uint32_t* __restrict__ vout,
                                                     const uint32_t* __restrict__ rem,
+                                                    const uint32_t* __restrict__ rrow,
                                                     uint32_t jj0, uint32_t count, uint32_t kw,
                                                     SplitGeom g, uint32_t W,
                                                     uint32_t* __restrict__ out,
@@ -222,10 +238,11 @@ __global__ void __launch_bounds__(256) k_split_tree(const uint32_t* __restrict__
     }
     // key segments: acc[s W + j] -> key word s cw + c W + j, XOR the remainder's word
     const uint64_t jj = (uint64_t)jj0 + jl;
+    const uint64_t rr = rrow[jj];  // the block's row of the remainder product (k_split_layout)
     for (uint32_t i = threadIdx.x; i < outw; i += blockDim.x) {
         const uint32_t sgm = i / W, j = i % W;
         const uint64_t wk = (uint64_t)sgm * cw + (uint64_t)c * W + j;
-        if (wk < kw) out[jj * out_stride + wk] = acc[i] ^ rem[jj * kw + wk];
+        if (wk < kw) out[jj * out_stride + wk] = acc[i] ^ rem[rr * kw + wk];
     }
 }
 
@@ -343,7 +360,7 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
 constexpr size_t kTreeSmemCap = 112 * 1024;
 
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
-                              uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
+                              const uint32_t* d_rrow, uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
                               uint32_t* d_out, uint64_t out_stride, cudaStream_t st) {
     (void)d_tmp;
     if (!count || !kw) return 0;
@@ -369,8 +386,8 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
     const uint64_t grid = (uint64_t)count * (cw / W);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<(unsigned)grid, 256, smem, st>>>(d_vout, d_rem, jj0, count, kw, g, W, d_out,
-                                                out_stride);
+        kern<<<(unsigned)grid, 256, smem, st>>>(d_vout, d_rem, d_rrow, jj0, count, kw, g, W,
+                                                d_out, out_stride);
     };
     if (D == 3)
         go(k_split_tree<3>);
