@@ -553,6 +553,12 @@ struct ssbh_plan {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t late_ev = nullptr, prev_ev = nullptr;
     const uint32_t* late_input = nullptr;
+    // host runs of single-batch GEMM-split plans: the combine runs in block slices and each
+    // slice of the key leaves for the host (copy_stream) while the next one is combined
+    uint64_t* host_key = nullptr;
+    bool host_key_sent = false;
+    static constexpr int kKeySlices = 8;
+    cudaEvent_t slice_ev[kKeySlices] = {};
     cudaStream_t own_stream = nullptr;
     uint64_t bytes = 0;
 };
@@ -862,6 +868,8 @@ extern "C" ssbh_status ssbh_plan_destroy(ssbh_plan* pl) {
     if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
     if (pl->late_ev) cudaEventDestroy(pl->late_ev);
     if (pl->prev_ev) cudaEventDestroy(pl->prev_ev);
+    for (auto& e : pl->slice_ev)
+        if (e) cudaEventDestroy(e);
     for (auto x : pl->exec)
         if (x) cudaGraphExecDestroy(x);
     delete pl;
@@ -1127,11 +1135,34 @@ static ssbh_status seg_hash(ssbh_plan* pl, uint32_t* d_key, uint64_t* d_lengths,
                 gc.leaves = g.leaves / 3;
                 gc.sL = 2 * g.sL;
             }
-            launches += 2 + launch_split_combine(pl->vout.as<uint32_t>(), pl->vy.as<uint32_t>(),
-                                                 pl->vrem.as<uint32_t>(), rlay.ktl, jj0, cnt,
-                                                 pl->kw, gc, out,
-                                                 pl->direct_out ? pl->p.out_bits / 32 : pl->kw,
-                                                 st);
+            const uint64_t ostride = pl->direct_out ? pl->p.out_bits / 32 : pl->kw;
+            if (pl->host_key && pl->copy_stream && pl->direct_out && out == d_key &&
+                cnt == pl->nown && pl->p.out_bits % 64 == 0 &&
+                cnt >= 4u * ssbh_plan::kKeySlices) {
+                for (int sl = 0; sl < ssbh_plan::kKeySlices; ++sl) {
+                    const uint32_t a = (uint32_t)((uint64_t)cnt * sl / ssbh_plan::kKeySlices);
+                    const uint32_t b = (uint32_t)((uint64_t)cnt * (sl + 1) / ssbh_plan::kKeySlices);
+                    launches += launch_split_combine(pl->vout.as<uint32_t>(),
+                                                     pl->vy.as<uint32_t>(), pl->vrem.as<uint32_t>(),
+                                                     rlay.ktl, jj0, cnt, pl->kw, gc, out, ostride,
+                                                     st, a, b);
+                    if (!pl->slice_ev[sl])
+                        CU(cudaEventCreateWithFlags(&pl->slice_ev[sl], cudaEventDisableTiming));
+                    CU(cudaEventRecord(pl->slice_ev[sl], st));
+                    CU(cudaStreamWaitEvent(pl->copy_stream, pl->slice_ev[sl], 0));
+                    CU(cudaMemcpyAsync(pl->host_key + (uint64_t)a * (pl->p.out_bits / 64),
+                                       d_key + (uint64_t)a * ostride,
+                                       (uint64_t)(b - a) * (pl->p.out_bits / 8),
+                                       cudaMemcpyDeviceToHost, pl->copy_stream));
+                }
+                launches += 2;
+                pl->host_key_sent = true;
+            } else {
+                launches += 2 + launch_split_combine(pl->vout.as<uint32_t>(),
+                                                     pl->vy.as<uint32_t>(), pl->vrem.as<uint32_t>(),
+                                                     rlay.ktl, jj0, cnt, pl->kw, gc, out, ostride,
+                                                     st);
+            }
         }
     } else if (pl->engine == kEngineMma && (pl->p.per_block_seed || pl->shared_pb)) {
         PbHashArgs m{};
@@ -1418,20 +1449,35 @@ extern "C" ssbh_status ssbh_plan_run_host_sifted(ssbh_plan* pl, const uint64_t* 
     if ((pl->key_words32 & 1) != 0) CU(cudaMemsetAsync(pl->d_key.p, 0, key_w64 * 8, st));
     if (late) {  // direct launches: the cross-stream wait is not part of a captured graph
         pl->late_input = pl->d_input.as<uint32_t>();
+        pl->host_key = out_key;
+        pl->host_key_sent = false;
         pl->last_stream = st;
         const RunArgs r{pl->d_input.as<uint32_t>(), nullptr, pl->d_key.as<uint32_t>(),
                         pl->d_len.as<uint64_t>(), pl->p.samp_key, pl->p.hash_key};
         const ssbh_status s = plan_enqueue(pl, r, st);
         pl->late_input = nullptr;
-        if (s) return s;
+        pl->host_key = nullptr;
+        if (s) {
+            if (pl->host_key_sent) cudaStreamSynchronize(pl->copy_stream);
+            pl->host_key_sent = false;
+            return s;
+        }
     } else if (auto s = ssbh_plan_run_device_sifted(pl, pl->d_input.as<uint32_t>(),
                                                     keep ? pl->d_keep.as<uint32_t>() : nullptr,
                                                     pl->d_key.as<uint32_t>(),
                                                     pl->d_len.as<uint64_t>(), nullptr, nullptr,
                                                     st))
         return s;
-    if (auto s = ssbh_plan_check(pl, stats)) return s;
-    CU(cudaMemcpyAsync(out_key, pl->d_key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));
+    const bool key_sent = pl->host_key_sent;  // the key left in slices behind the combine
+    pl->host_key_sent = false;
+    if (auto s = ssbh_plan_check(pl, stats)) {
+        if (key_sent) cudaStreamSynchronize(pl->copy_stream);
+        return s;
+    }
+    if (key_sent)
+        CU(cudaStreamSynchronize(pl->copy_stream));
+    else
+        CU(cudaMemcpyAsync(out_key, pl->d_key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));
     if (out_lengths)
         CU(cudaMemcpyAsync(out_lengths, pl->d_len.p, (size_t)pl->nown * 8, cudaMemcpyDeviceToHost,
                            st));

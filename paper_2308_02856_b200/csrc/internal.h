@@ -319,8 +319,9 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
 // out[jj * out_stride + w] = rem[jj * kw + w] ^ the leaves reaching word w, blocks jj0 + [0, count)
 // returns the launches made; d_tmp (>= the leaf outputs) holds intermediate levels
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
-                              const uint32_t* d_rrow, uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
-                              uint32_t* d_out, uint64_t out_stride, cudaStream_t st);
+                              const uint32_t* d_rrow, uint32_t jj0, uint32_t count, uint32_t kw,
+                              const SplitGeom& g, uint32_t* d_out, uint64_t out_stride,
+                              cudaStream_t st, uint32_t jl0 = 0, uint32_t jl1 = 0xffffffffu);
 uint32_t mma_mtiles(uint32_t nown);
 // Leaf mode (the split's shared-seed leaf GEMM): K parts of <= 8192 positions, N tiles innermost.
 // parent: the parent-node variant (leaves of <= 4096 positions: 2 leaves fit the buffer)

@@ -167,7 +167,8 @@ template <int D>
 __global__ void __launch_bounds__(256) k_split_tree(const uint32_t* __restrict__ vout,
                                                     const uint32_t* __restrict__ rem,
                                                     const uint32_t* __restrict__ rrow,
-                                                    uint32_t jj0, uint32_t count, uint32_t kw,
+                                                    uint32_t jj0, uint32_t jl0, uint32_t count,
+                                                    uint32_t kw,
                                                     SplitGeom g, uint32_t W,
                                                     uint32_t* __restrict__ out,
                                                     unsigned long long out_stride) {
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(256) k_split_tree(const uint32_t* __restrict__
     extern __shared__ __align__(16) uint32_t tsm[];
     const uint64_t cw = g.sL / 32;  // leaf words
     const uint32_t nchunks = (uint32_t)(cw / W);
-    const uint32_t jl = blockIdx.x / nchunks, c = blockIdx.x % nchunks;
+    const uint32_t jl = jl0 + blockIdx.x / nchunks, c = blockIdx.x % nchunks;  // batch-local block
     if (jl >= count) return;
     const uint32_t nsub = g.leaves / kSub;       // subtree roots (level L - D nodes)
     uint32_t* buf0 = tsm;                        // nsub nodes x kOut W words
@@ -360,10 +361,12 @@ void launch_split_batch(const uint32_t* d_ybuf, const uint32_t* d_sbuf, uint64_t
 constexpr size_t kTreeSmemCap = 112 * 1024;
 
 uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t* d_rem,
-                              const uint32_t* d_rrow, uint32_t jj0, uint32_t count, uint32_t kw, const SplitGeom& g,
-                              uint32_t* d_out, uint64_t out_stride, cudaStream_t st) {
+                              const uint32_t* d_rrow, uint32_t jj0, uint32_t count, uint32_t kw,
+                              const SplitGeom& g, uint32_t* d_out, uint64_t out_stride,
+                              cudaStream_t st, uint32_t jl0, uint32_t jl1) {
     (void)d_tmp;
-    if (!count || !kw) return 0;
+    jl1 = std::min(jl1, count);  // batch-local blocks [jl0, jl1): one launch per slice
+    if (jl0 >= jl1 || !kw) return 0;
     // one pass from the leaves (round 1: level by level, L launches through HBM, config 3
     // 3.0 ms): depth-D register subtrees, chunk width W words (the largest power of two <= 32
     // and <= the leaf whose buffers fit kTreeSmemCap of shared memory: two CTAs per SM)
@@ -383,10 +386,10 @@ uint32_t launch_split_combine(uint32_t* d_vout, uint32_t* d_tmp, const uint32_t*
         while (W > 1 && (W > cw || smem_of(W) > kTreeSmemCap)) W /= 2;
     }
     const size_t smem = smem_of(W);
-    const uint64_t grid = (uint64_t)count * (cw / W);
+    const uint64_t grid = (uint64_t)(jl1 - jl0) * (cw / W);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<(unsigned)grid, 256, smem, st>>>(d_vout, d_rem, d_rrow, jj0, count, kw, g, W,
+        kern<<<(unsigned)grid, 256, smem, st>>>(d_vout, d_rem, d_rrow, jj0, jl0, jl1, kw, g, W,
                                                 d_out, out_stride);
     };
     if (D == 3)

@@ -292,6 +292,38 @@ def test_split_budget_few_long_blocks(dev, ovr):
     assert kernel.endswith("+split"), kernel
 
 
+def test_split_host_run_key_slices(dev, oracle):
+    """Host runs of >= 2^26 rounds (late input copy) on a single-batch GEMM-split plan combine
+    the key in block slices and send each slice to the host behind its combine
+    (abi.cu seg_hash): the host key = the device-run key = the LOP3 engine's key, on repeated
+    runs through the same plan (block ranges too)."""
+    import torch
+
+    n, s, k = 1 << 26, 64, 1 << 19
+    x = oracle.make_input(5, 0.5, n)
+    d_in = torch.from_numpy(x.view(np.int32).copy()).cuda()
+    keys = {}
+    for engine in (dev.ENGINE_TENSOR, dev.ENGINE_LOP3):
+        plan = dev.Plan(n, s, k, 7, 8, engine=engine)
+        d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+        d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+        plan.run_device(d_in.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+        plan.check()
+        keys[engine] = d_key.cpu().numpy().view(np.uint64)
+        if engine == dev.ENGINE_TENSOR:
+            assert plan.hash_kernel == "k_leaf_gemm+split"
+            for _ in range(2):
+                hk, hl, _ = plan.run_host(x)
+                assert (hk == keys[engine]).all()
+                assert (hl == d_len.cpu().numpy().view(np.uint64)).all()
+        plan.close()
+    assert (keys[dev.ENGINE_TENSOR] == keys[dev.ENGINE_LOP3]).all()
+    plan = dev.Plan(n, s, k, 7, 8, block_first=16, block_count=40)
+    hk, _, _ = plan.run_host(x)
+    plan.close()
+    assert (hk == keys[dev.ENGINE_TENSOR][16 * k // 64: 56 * k // 64]).all()
+
+
 def test_split_disabled_by_override(dev, ovr):
     """split_levels = 0 keeps long shared blocks on the direct tiled kernel."""
     ovr(split_levels=0)
