@@ -19,6 +19,12 @@
 //        Owner — the payload itself into the owning rank's receive buffer at a global rank,
 //                by direct stores through NVLink peer memory (multi-GPU sharded sampling:
 //                the dispatch half of an all-to-all fused into the partition pass).
+//
+//  In-memory single-level plans (configs 1-3) take the ranked variant of passes 1 and 3
+//  (make_ranked): pass 1 (k_count_ranked) also finds each round's stable rank inside its
+//  (chunk, block) cell — it is ALU-bound on Threefry, so the ranking is free there — and
+//  stores it with the payload; pass 3 (k_scatter_windowed) then needs no order at all: a CTA
+//  takes a chunk, ORs each cell's bits into a shared-memory window and writes whole words.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
