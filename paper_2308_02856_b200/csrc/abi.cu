@@ -729,7 +729,8 @@ static ssbh_status plan_create_impl(const ssbh_extract_params* params, uint64_t 
     }
     // single-level count table (two-level streaming plans do without: forward streaming)
     pl->fwd_stream = pl->bucketed && pl->streaming;
-    if (!e && !pl->bucketed) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4);
+    // + the ranked count pass's chunk counter (zeroed with the table)
+    if (!e && !pl->bucketed) e = alloc(pl->counts, (size_t)pl->geom.nchunks * nown * 4 + 4);
     if (!e && !pl->bucketed) e = alloc(pl->gsum, (size_t)pl->geom.ngroups * nown * 8);
     if (!e && pl->fwd_stream) {
         // region per block: mean + 16 sigma of Binomial(n, 1/s) (a longer block raises the
@@ -987,7 +988,12 @@ static ssbh_status seg_sample(ssbh_plan* pl, const uint32_t* d_input, const uint
         CU(cudaMemsetAsync(pl->ybuf.p, 0, pl->ybuf.bytes, st));
         return SSBH_OK;
     }
-    CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
+    // the ranked count pass writes every row of the table with plain stores: only its chunk
+    // counter (the word after the table) starts at zero
+    if (pl->geom.ranked && !pl->streaming)
+        CU(cudaMemsetAsync(pl->counts.as<uint8_t>() + pl->counts.bytes - 4, 0, 4, st));
+    else
+        CU(cudaMemsetAsync(pl->counts.p, 0, pl->counts.bytes, st));
     // streaming: count only (a bucketed streaming plan's payload buffer holds one chunk)
     launch_sample_count(pl->geom, sk, d_input, d_keep, pl->streaming ? nullptr : pl->payload.p,
                         pl->counts.as<uint32_t>(), nullptr, st);

@@ -202,8 +202,6 @@ __global__ void __launch_bounds__(256) k_count_ranked(Key key, uint64_t n, uint6
     for (uint32_t t = lane; t < nown; t += 32) own[t] = 0xffffffffu;
     const uint64_t gpc = (1ull << cs) / 32;  // groups per chunk
     const uint64_t ngroups = (n + 31) / 32;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     auto draw = [&](uint64_t g) -> uint32_t {
         const uint64_t i = g * 32 + lane;
         if (i >= n) return 0;
@@ -236,7 +234,15 @@ __global__ void __launch_bounds__(256) k_count_ranked(Key key, uint64_t n, uint6
         }
         if (valid) payload[i] = kept ? (v | (bit << 15) | (rank << 16)) : 0x7fffu;
     };
-    for (uint64_t c = warp; c < nchunks; c += nwarps) {
+    // chunks are handed out dynamically (the counter is the word after the count table, zeroed
+    // with it): equal work per chunk, but a static split leaves the last CTAs of a 2.7-wave
+    // grid running alone
+    uint32_t* next_chunk = counts + nchunks * nown;
+    for (;;) {
+        uint32_t cn = 0;
+        if (lane == 0) cn = atomicAdd(next_chunk, 1u);
+        const uint64_t c = __shfl_sync(0xffffffffu, cn, 0);
+        if (c >= nchunks) break;
         for (uint32_t t = lane; t < nown; t += 32) hist[t] = 0;
         __syncwarp();
         const uint64_t g0 = c * gpc, g1 = min(ngroups, g0 + gpc);
@@ -1011,10 +1017,13 @@ void launch_sample_count(const SamplerGeom& g, const uint64_t key[4], const uint
         while ((1ull << kbits) < g.nown) ++kbits;
         const int cwarps = 8;
         const size_t shm = (size_t)g.nown * 8 * cwarps;  // rank row + owner row per warp
-        const uint64_t blocks = std::min<uint64_t>((g.nchunks + 7) / 8, (uint64_t)sm_count() * 8);
         auto go = [&](auto kern) {
             if (shm > 48 * 1024)
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+            int per_sm = 1;  // resident CTAs only: the warps fetch chunks from a counter
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cwarps * 32, shm);
+            const uint64_t blocks = std::min<uint64_t>(
+                (g.nchunks + 7) / 8, (uint64_t)sm_count() * std::max(per_sm, 1));
             kern<<<(unsigned)std::max<uint64_t>(blocks, 1), cwarps * 32, shm, st>>>(
                 k, g.n, g.s, g.j_lo, g.nown, d_in32, d_keep, static_cast<uint32_t*>(d_payload),
                 g.chunk_shift, g.nchunks, kbits, d_counts);
