@@ -346,6 +346,20 @@ def test_ranked_scatter_windows(dev, oracle, ovr, window):
     assert (np.concatenate(parts) == want).all()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("s", [1, 2])
+def test_ranked_long_cells(dev, oracle, s):
+    """Ranked passes at their largest cells: 2^29 rounds give chunks of 2^15 rounds, and with
+    one or two sub-blocks a (chunk, block) cell holds up to all of them — ranks up to 2^15 in
+    the payload's 16 rank bits, windows of hundreds of words in the scatter."""
+    n, k = (1 << 29) + 12345, 64
+    x = oracle.make_input(9, 0.5, n)
+    want, wnj = oracle.extract(x, n, s, 41, 42, False, k)
+    got, nj, _ = dev.extract(x, n, s, k, 41, 42)
+    assert (nj == wnj).all()
+    assert (got == want).all()
+
+
 # ----------------------------------------------------------------- BASELINE full sizes
 # SURVEY §8a anchors (computed with the compiled reference); tests/golden/gen_golden.py
 # --config3 re-derives config 3 from the reference into golden.json.
