@@ -1476,19 +1476,20 @@ extern "C" ssbh_status ssbh_plan_run_host_sifted(ssbh_plan* pl, const uint64_t* 
         return s;
     const bool key_sent = pl->host_key_sent;  // the key left in slices behind the combine
     pl->host_key_sent = false;
-    if (auto s = ssbh_plan_check(pl, stats)) {
-        if (key_sent) cudaStreamSynchronize(pl->copy_stream);
-        return s;
-    }
-    if (key_sent)
-        CU(cudaStreamSynchronize(pl->copy_stream));
-    else
+    // the read-backs are queued behind the run, so the one synchronisation of plan_check also
+    // covers them (a failed run leaves unspecified bytes in the caller's buffers)
+    if (!key_sent)
         CU(cudaMemcpyAsync(out_key, pl->d_key.p, key_w64 * 8, cudaMemcpyDeviceToHost, st));
     if (out_lengths)
         CU(cudaMemcpyAsync(out_lengths, pl->d_len.p, (size_t)pl->nown * 8, cudaMemcpyDeviceToHost,
                            st));
-    CU(cudaStreamSynchronize(st));
-    return ok();
+    const ssbh_status s = ssbh_plan_check(pl, stats);  // synchronises st
+    if (key_sent) {
+        const std::string msg = g_err;
+        cudaStreamSynchronize(pl->copy_stream);
+        g_err = msg;
+    }
+    return s;
 }
 
 extern "C" ssbh_status ssbh_extract(const ssbh_extract_params* params, const uint64_t* input,
