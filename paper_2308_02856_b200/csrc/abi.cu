@@ -1435,7 +1435,7 @@ extern "C" ssbh_status ssbh_plan_run_host_sifted(ssbh_plan* pl, const uint64_t* 
     cudaStream_t st = pl->own_stream;
     // large inputs without a keep mask: copy the input on a second stream while the count pass
     // runs (it needs only the round indices); the split / scatter wait for the copy
-    const bool late = !keep && pl->p.n_rounds >= (1ull << 26);
+    const bool late = !keep && pl->p.n_rounds >= (1ull << 24);
     if (late) {
         if (!pl->copy_stream) {
             CU(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));

@@ -97,7 +97,7 @@ def test_shared_seed_long_blocks_use_the_tiled_kernel(dev, oracle):
 
 @pytest.mark.parametrize("s,k", [(64, 1024), (4096, 256)], ids=["single-level", "two-level"])
 def test_host_run_overlaps_input_copy(dev, oracle, s, k):
-    """Host runs of >= 2^26 rounds copy the input on a second stream while the count pass runs
+    """Host runs of >= 2^24 rounds copy the input on a second stream while the count pass runs
     (it needs only the round indices); the scatter / bucket split take the data bits from the
     input. Same key and lengths as the oracle, and as the device-resident run."""
     import torch
@@ -293,7 +293,7 @@ def test_split_budget_few_long_blocks(dev, ovr):
 
 
 def test_split_host_run_key_slices(dev, oracle):
-    """Host runs of >= 2^26 rounds (late input copy) on a single-batch GEMM-split plan combine
+    """Host runs of >= 2^24 rounds (late input copy) on a single-batch GEMM-split plan combine
     the key in block slices and send each slice to the host behind its combine
     (abi.cu seg_hash): the host key = the device-run key = the LOP3 engine's key, on repeated
     runs through the same plan (block ranges too)."""
