@@ -391,6 +391,36 @@ def test_config3_full_key_digest(dev, oracle, golden):
     plan.close()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_linearity(dev, cfg):
+    """Size-independent property at BASELINE's full sizes (configs[2] and configs[3]): with the
+    sampling and hash seeds fixed the extractor is GF(2)-linear in the raw string — the sampler
+    moves bit i of every input to the same place and the Toeplitz product is linear — so
+    key(x ^ y) = key(x) ^ key(y) and the block lengths do not depend on the data."""
+    import torch
+
+    c = dev.CONFIGS[cfg]
+    n, s, k = c["n"], c["s"], c["k"]
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], per_block=c["per_block"])
+    words = (n + 63) // 64 * 2
+    xs = [torch.zeros(words, dtype=torch.int32, device="cuda") for _ in range(2)]
+    dev.make_input_device(c["seed_in"], c["p"], n, xs[0].data_ptr())
+    dev.make_input_device(c["seed_in"] + 1000, 0.5, n, xs[1].data_ptr())
+    keys, lens = [], []
+    for x in (xs[0], xs[1], xs[0] ^ xs[1]):
+        d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+        d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+        plan.run_device(x.data_ptr(), d_key.data_ptr(), d_len.data_ptr())
+        plan.check()
+        keys.append(d_key)
+        lens.append(d_len)
+    assert bool((keys[2] == (keys[0] ^ keys[1])).all())
+    assert bool((lens[0] == lens[1]).all()) and bool((lens[0] == lens[2]).all())
+    assert int(keys[0].ne(0).sum()) > 0 and not bool((keys[0] == keys[1]).all())
+    plan.close()
+
+
 # ------------------------------------------------------------------- streaming plans
 def _stream_run(dev, x_words, n, s, k, samp, hsh, chunk_bits, per_block=False, order=None,
                 block_first=0, block_count=0):
