@@ -392,6 +392,33 @@ def test_config3_full_key_digest(dev, oracle, golden):
 
 
 @pytest.mark.slow
+def test_config3_block_ranges_concatenate(dev, oracle, golden):
+    """Multi-GPU sharding at BASELINE configs[2]: the sub-block ranges the ranks of an N = 4 run
+    own (uneven on purpose), each extracted by its own plan from the whole input, concatenate to
+    the reference's whole-key digest."""
+    import torch
+
+    c = dev.CONFIGS[3]
+    want = golden["extract"].get("3", SURVEY_C3)
+    n, s, k = c["n"], c["s"], c["k"]
+    d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    d_key = torch.zeros(s * k // 32, dtype=torch.int32, device="cuda")
+    d_len = torch.zeros(s, dtype=torch.int64, device="cuda")
+    for first, cnt in ((0, 256), (256, 300), (556, 212), (768, 256)):
+        plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"], block_first=first,
+                        block_count=cnt)
+        plan.run_device(d_in.data_ptr(), d_key[first * (k // 32):].data_ptr(),
+                        d_len[first:].data_ptr())
+        plan.check()
+        plan.close()
+    key = d_key.cpu().numpy().view(np.uint64)
+    nj = d_len.cpu().numpy().view(np.uint64)
+    assert int(nj.sum()) == n and int(nj.min()) == want["nj_min"]
+    assert f"{oracle.fnv(key):016x}" == want["key_fnv"]
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("cfg", [3, 4])
 def test_full_size_linearity(dev, cfg):
     """Size-independent property at BASELINE's full sizes (configs[2] and configs[3]): with the
