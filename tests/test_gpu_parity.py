@@ -392,6 +392,28 @@ def test_config3_full_key_digest(dev, oracle, golden):
 
 
 @pytest.mark.slow
+def test_config3_host_run_digest(dev, oracle, golden):
+    """BASELINE configs[2] through the host entry point (ssbh_plan_run_host: input copy behind
+    the count pass, key read back in slices behind the combine), twice through one plan: the
+    reference's whole-key digest and block lengths."""
+    import torch
+
+    c = dev.CONFIGS[3]
+    want = golden["extract"].get("3", SURVEY_C3)
+    n, s, k = c["n"], c["s"], c["k"]
+    d_in = torch.zeros((n + 63) // 64 * 2, dtype=torch.int32, device="cuda")
+    dev.make_input_device(c["seed_in"], c["p"], n, d_in.data_ptr())
+    x = d_in.cpu().numpy().view(np.uint64)
+    del d_in
+    plan = dev.Plan(n, s, k, c["seed_samp"], c["seed_hash"])
+    for _ in range(2):
+        key, nj, _ = plan.run_host(x)
+        assert int(nj.sum()) == n and int(nj.max()) == want["nj_max"]
+        assert f"{oracle.fnv(key):016x}" == want["key_fnv"]
+    plan.close()
+
+
+@pytest.mark.slow
 def test_config3_block_ranges_concatenate(dev, oracle, golden):
     """Multi-GPU sharding at BASELINE configs[2]: the sub-block ranges the ranks of an N = 4 run
     own (uneven on purpose), each extracted by its own plan from the whole input, concatenate to
